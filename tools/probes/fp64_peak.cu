@@ -1,0 +1,88 @@
+// FP64 peak probe: DMMA (mma.sync m8n8k4 f64) vs scalar DFMA, sm_100a.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_peak fp64_peak.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void dmma_loop(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[8][2];
+  for (int j = 0; j < 8; ++j) { c[j][0] = 0; c[j][1] = 0; }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[j][0]), "+d"(c[j][1]) : "d"(a), "d"(b));
+    }
+  }
+  double s = 0;
+  for (int j = 0; j < 8; ++j) s += c[j][0] + c[j][1];
+  if (s == 12345.0) out[0] = s;
+}
+
+__global__ void dmma16_loop(double* out, int iters) {
+  double a[8], b[4];
+  for (int j = 0; j < 8; ++j) a[j] = threadIdx.x * 1e-3 + j;
+  for (int j = 0; j < 4; ++j) b[j] = 1.0 + threadIdx.x * 1e-4 + j;
+  double c[4][4];
+  for (int j = 0; j < 4; ++j) for (int k = 0; k < 4; ++k) c[j][k] = 0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+                   : "+d"(c[j][0]), "+d"(c[j][1]), "+d"(c[j][2]), "+d"(c[j][3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                     "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+    }
+  }
+  double s = 0;
+  for (int j = 0; j < 4; ++j) for (int k = 0; k < 4; ++k) s += c[j][k];
+  if (s == 12345.0) out[0] = s;
+}
+
+__global__ void dfma_loop(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-9;
+  double c[16];
+  for (int j = 0; j < 16; ++j) c[j] = j;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) c[j] = fma(c[j], b, a);
+  }
+  double s = 0;
+  for (int j = 0; j < 16; ++j) s += c[j];
+  if (s == 12345.0) out[0] = s;
+}
+
+int main() {
+  double* out; cudaMalloc(&out, 8);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  printf("SMs %d clock %d kHz\n", sms, clk);
+  for (int warps : {4, 8, 16}) {
+    int iters = 20000;
+    dim3 grid(sms * 2), block(32 * warps);
+    dmma_loop<<<grid, block>>>(out, 100);
+    cudaEventRecord(e0);
+    dmma_loop<<<grid, block>>>(out, iters);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double flops = 2.0 * 8 * 8 * 4 * 8.0 * iters * grid.x * warps;
+    printf("DMMA m8n8k4 warps/CTA=%d: %.2f TFLOP/s\n", warps, flops / ms / 1e9);
+    dmma16_loop<<<grid, block>>>(out, 100);
+    cudaEventRecord(e0);
+    dmma16_loop<<<grid, block>>>(out, iters / 4);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    flops = 2.0 * 16 * 8 * 16 * 4.0 * (iters / 4) * grid.x * warps;
+    printf("DMMA m16n8k16 warps/CTA=%d: %.2f TFLOP/s\n", warps, flops / ms / 1e9);
+    dfma_loop<<<grid, block>>>(out, 100);
+    cudaEventRecord(e0);
+    dfma_loop<<<grid, block>>>(out, iters);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    flops = 2.0 * 16 * iters * (double)grid.x * block.x;
+    printf("DFMA warps/CTA=%d: %.2f TFLOP/s\n", warps, flops / ms / 1e9);
+  }
+  printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}

@@ -1,0 +1,162 @@
+/*
+ * rtucker_b200.h -- additive extensions of the B200 build (librtucker_b200.so).
+ *
+ * Nothing here changes the reference ABI in rtucker.h; these entry points
+ * expose what the reference keeps internal (SURVEY.md section 8(b),
+ * "Extensions the replacement must add"):
+ *   - device-resident tensors (no host copy; for benchmarks and large runs),
+ *   - initial-model injection (the reference can only self-initialise,
+ *     ref tucker.cpp:168-190),
+ *   - oracle/replay entry points for each rung of the parity ladder:
+ *     the GPU sampler driven by caller-supplied CDFs (rung 1), the GPU
+ *     normal-equation accumulation driven by a caller-supplied RowSketch
+ *     (rung 3) and the GPU SPD solve of a caller-supplied Gram (rung 4),
+ *   - per-kernel timing export and multi-GPU sample sharding hooks.
+ * All pointers are host pointers unless the name says _device.
+ */
+#ifndef RTUCKER_B200_H
+#define RTUCKER_B200_H
+
+#include "rtucker.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Device ordinal used by this thread's calls (default 0). */
+rtucker_status rtucker_b200_set_device(int device);
+/* CUDA stream (cudaStream_t) for this thread's work; NULL restores the
+ * library-owned stream. Lets a caller time the library with its own events. */
+rtucker_status rtucker_b200_set_stream(void* stream);
+
+/* Wrap a tensor that already lives in device memory of the current device.
+ * The data is copied (device to device); rtucker_tensor_data() returns NULL
+ * for such a tensor (no host mirror) and sets the last error. */
+rtucker_status rtucker_b200_tensor_create_device(const uint64_t* shape, uint32_t order,
+                                                 const double* data_device,
+                                                 rtucker_tensor** out);
+/* Device pointer of a tensor's resident copy (borrowed). */
+const double* rtucker_b200_tensor_device_data(const rtucker_tensor* t);
+
+/* Extended ALS options. Zero-initialise, then set what you need. */
+typedef struct rtucker_b200_als_ext {
+  /* If non-NULL: initial core (prod ranks, row-major) and factors (factor n is
+   * I_n x R_n row-major, concatenated) replace the uniform init. */
+  const double* init_core;
+  const double* init_factors;
+  /* Multi-GPU sample sharding: this process draws sketch rows
+   * [shard_rank * s / shard_count, (shard_rank+1) * s / shard_count) and the
+   * partial normal equations are summed by `allreduce` (in place, doubles,
+   * on the library's stream) before the solve. shard_count 0/1 = no sharding. */
+  uint32_t shard_rank;
+  uint32_t shard_count;
+  void (*allreduce)(double* device_buf, uint64_t count, void* stream, void* user);
+  void* allreduce_user;
+  /* Skip the per-sweep host sync when tolerance <= 0 (no early stop possible):
+   * the whole run is enqueued back to back. Default 1. */
+  int async_sweeps_when_no_tolerance;
+  /* 1 = record per-kernel-family device time (CUDA events on the run's
+   * stream), exported by rtucker_b200_result_kernel_row. */
+  int profile_kernels;
+  int reserved[7];
+} rtucker_b200_als_ext;
+
+rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* ranks,
+                                       uint32_t order, const rtucker_als_options* opts,
+                                       const rtucker_b200_als_ext* ext,
+                                       rtucker_als_result** out);
+
+/* Sessions: the same run split into steps, so a caller can time exactly K
+ * sweeps (bench.py). create = init + initial loss; sweeps ignore tolerance. */
+typedef struct rtucker_b200_session rtucker_b200_session;
+rtucker_status rtucker_b200_session_create(const rtucker_tensor* x, const uint64_t* ranks,
+                                           uint32_t order, const rtucker_als_options* opts,
+                                           const rtucker_b200_als_ext* ext,
+                                           rtucker_b200_session** out);
+rtucker_status rtucker_b200_session_sweeps(rtucker_b200_session* s, uint32_t n);
+rtucker_status rtucker_b200_session_result(rtucker_b200_session* s, rtucker_als_result** out);
+void rtucker_b200_session_free(rtucker_b200_session* s);
+
+/* Device seconds of the sweep loop of a result (CUDA events). */
+double rtucker_b200_result_sweep_seconds(const rtucker_als_result* r);
+
+/* Model contents (host copies). core_out: prod ranks; factors_out: sum I_n*R_n. */
+rtucker_status rtucker_b200_model_data(const rtucker_model* m, double* core_out,
+                                       double* factors_out);
+/* Build a model from host arrays (shape I_n, ranks R_n). */
+rtucker_status rtucker_b200_model_create(const uint64_t* shape, const uint64_t* ranks,
+                                         uint32_t order, const double* core,
+                                         const double* factors, double lambda,
+                                         rtucker_model** out);
+
+/* Sketch diagnostics of the last core update of a result:
+ * sample count, data-row draws, rank-deficiency flag, solver path (0 =
+ * Cholesky, 1 = eigen pinv fallback). */
+rtucker_status rtucker_b200_result_sketch_info(const rtucker_als_result* r,
+                                               uint64_t* sample_count,
+                                               uint64_t* data_draws,
+                                               int* rank_deficient, int* solver_path);
+
+/* Per-kernel device time accumulated over a run (CUDA events on the run's
+ * stream). name_buf receives the kernel family name. */
+uint64_t rtucker_b200_result_kernel_count(const rtucker_als_result* r);
+rtucker_status rtucker_b200_result_kernel_row(const rtucker_als_result* r, uint64_t i,
+                                              char* name_buf, size_t name_len,
+                                              double* total_seconds, uint64_t* launches);
+
+/* ---- parity-ladder entry points ---- */
+
+/* Per-mode classical leverage scores, CDF and score sum on the GPU
+ * (ref kronecker.cpp:9-35 with ridge_scores(svd, n, 0), leverage.cpp:16-37). */
+rtucker_status rtucker_b200_factor_scores(const double* factor, uint64_t rows,
+                                          uint64_t cols, double* scores_out,
+                                          double* cdf_out, double* sum_out,
+                                          uint64_t* rank_out);
+
+/* Rung 1: draws s rows of the augmented Kronecker design on the GPU from
+ * caller-supplied per-mode scores/CDFs/sums (concatenated over modes) and the
+ * SplitMix64 seed, exactly as ProductLeverageSampler + solve_sketched_ridge
+ * (ref kronecker.cpp:125-181, sketch_ridge.cpp:80-90). indices_out/weights_out
+ * have length s. */
+rtucker_status rtucker_b200_kron_draw(uint32_t order, const uint64_t* rows, uint64_t d,
+                                      const double* scores, const double* cdfs,
+                                      const double* sums, uint64_t seed, uint64_t s,
+                                      uint64_t* indices_out, double* weights_out);
+
+/* Rung 3: sketched normal equations (gram d x d full, rhs d) of the augmented
+ * Kronecker design from a caller-supplied RowSketch (ref
+ * sketch_ridge.cpp:105-128). x is the host tensor (prod rows values). */
+rtucker_status rtucker_b200_kron_normal_eq(uint32_t order, const uint64_t* rows,
+                                           const uint64_t* ranks, const double* factors,
+                                           const double* x, double lambda, uint64_t s,
+                                           const uint64_t* indices, const double* weights,
+                                           double* gram_out, double* rhs_out);
+
+/* Rung 4: x = gram^+ rhs for a symmetric PSD gram (d x d): Cholesky on the GPU
+ * with the eigen/pinv fallback (rank cutoff d*eps*lambda_max as ref
+ * svd.cpp:92-97). *rank_out = numerical rank, *path_out = 0 Cholesky / 1 pinv. */
+rtucker_status rtucker_b200_spd_solve(const double* gram, const double* rhs, uint64_t d,
+                                      double* x_out, uint64_t* rank_out, int* path_out);
+
+/* One sketched core update on the GPU for a given model (ref tucker.cpp:141-166).
+ * Optional outputs (NULL to skip): indices/weights of the drawn sketch. */
+rtucker_status rtucker_b200_update_core_sketched(const rtucker_tensor* x,
+                                                 const rtucker_model* m, uint64_t s,
+                                                 uint64_t seed, double* core_out,
+                                                 uint64_t* indices_out,
+                                                 double* weights_out);
+/* One exact factor update (ref tucker.cpp:70-89), mode 1-based. */
+rtucker_status rtucker_b200_update_factor(const rtucker_tensor* x, const rtucker_model* m,
+                                          uint32_t mode, double* factor_out);
+/* Exact core update (ref tucker.cpp:91-129). */
+rtucker_status rtucker_b200_update_core_exact(const rtucker_tensor* x,
+                                              const rtucker_model* m, double* core_out);
+/* Regularised loss and rmse of a model (ref tucker.cpp:47-68, 216-229). */
+rtucker_status rtucker_b200_loss(const rtucker_tensor* x, const rtucker_model* m,
+                                 double* loss_out, double* rmse_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RTUCKER_B200_H */

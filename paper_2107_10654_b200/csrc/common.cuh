@@ -1,0 +1,97 @@
+// common.cuh -- shared device helpers for the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <stdexcept>
+#include <string>
+
+namespace rtb {
+
+// Host-side error type carrying an rtucker_status code.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define RTB_CUDA(call)                                                                \
+  do {                                                                                \
+    cudaError_t err_ = (call);                                                        \
+    if (err_ != cudaSuccess)                                                          \
+      throw ::rtb::Error(4, std::string("CUDA error: ") + cudaGetErrorString(err_) +  \
+                                " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+#define RTB_LAUNCH_CHECK() RTB_CUDA(cudaGetLastError())
+
+constexpr int kNumSMs = 148;
+constexpr int kMaxOrder = 8;
+
+// ---- SplitMix64 (ref rng.hpp:12-62) in counter form: output k of a stream
+// seeded with `seed` is mix(seed + (k+1)*gamma). ----
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ULL;
+
+__host__ __device__ __forceinline__ uint64_t sm_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t sm_at(uint64_t seed, uint64_t k) {
+  return sm_mix(seed + (k + 1) * kGamma);
+}
+// next_double(): top 53 bits times 2^-53, exact (ref rng.hpp:24-26).
+__device__ __forceinline__ double u64_to_unit(uint64_t u) {
+  return __dmul_rn(static_cast<double>(u >> 11), 0x1.0p-53);
+}
+
+// ---- FP64 tensor-core MMA: D(8x8) += A(8x4) * B(4x8), one DMMA.8x8x4 ----
+// Fragment ownership (lane l, g = l>>2, t = l&3):
+//   A: a = A[g][t]   B: b = B[t][g]   C/D: c0 = C[g][2t], c1 = C[g][2t+1]
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// ---- cp.async (LDGSTS) with zero fill: copies `src_bytes` (0 or the full
+// size) and zero-fills the rest of the destination. ----
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
+template <typename T>
+__host__ __device__ __forceinline__ T ceil_div(T a, T b) {
+  return (a + b - 1) / b;
+}
+
+// Deterministic block-wide sum (fixed tree order for a fixed blockDim).
+template <int kThreads>
+__device__ __forceinline__ double block_sum(double v, double* smem) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < 32) {
+    r = threadIdx.x < kThreads / 32 ? smem[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  return r;  // valid in thread 0 (and all of warp 0)
+}
+
+}  // namespace rtb

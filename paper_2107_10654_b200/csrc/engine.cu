@@ -1,0 +1,1600 @@
+// engine.cu -- device-resident sketched Tucker-ALS (ref tucker.cpp:192-276).
+//
+// One sweep, everything on the GPU, X read from HBM twice:
+//   F_n, n < N : Y = T x_{m != n, N} A_m^T  (T = X x_N A_N^T, cached from the
+//                previous loss pass), M = Y_(n) G_(n)^T, KK^T from the factor
+//                Grams, A_n = M pinv(KK^T + lambda I)            (tucker.cpp:70-89)
+//   F_N        : Y = X x_1 A_1^T x_2 ...  (one strided pass over X)
+//   Core       : sketched (scores -> parallel draw decode -> Kronecker-factored
+//                Gram/RHS -> Cholesky)                           (tucker.cpp:141-166)
+//                or exact (factor SVD bases, 2 TTM chains)       (tucker.cpp:91-129)
+//   Loss       : fused pass: residual of X against G x_n A_n rebuilt in
+//                registers + next sweep's T                      (tucker.cpp:216-229)
+#include "engine.h"
+
+#include <cfloat>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+
+#include "kernels.h"
+
+namespace rtb {
+
+// ---------------------------------------------------------------------------
+// streams and buffers
+
+namespace {
+thread_local cudaStream_t t_stream = nullptr;
+std::mutex g_stream_mu;
+std::map<int, cudaStream_t> g_default_streams;
+}  // namespace
+
+cudaStream_t current_stream() {
+  if (t_stream) return t_stream;
+  int dev = 0;
+  RTB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_stream_mu);
+  auto it = g_default_streams.find(dev);
+  if (it != g_default_streams.end()) return it->second;
+  cudaStream_t s;
+  RTB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  // keep freed pool memory cached across runs (no cudaMalloc per call)
+  cudaMemPool_t pool;
+  RTB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = UINT64_MAX;
+  RTB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  g_default_streams[dev] = s;
+  return s;
+}
+
+void set_stream(cudaStream_t s) { t_stream = s; }
+
+DevBuf::DevBuf(size_t b, cudaStream_t s) { ensure(b, s); }
+DevBuf::~DevBuf() {
+  if (p) cudaFreeAsync(p, st);
+}
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+  if (this != &o) {
+    if (p) cudaFreeAsync(p, st);
+    p = o.p;
+    bytes = o.bytes;
+    st = o.st;
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  return *this;
+}
+void DevBuf::ensure(size_t b, cudaStream_t s) {
+  if (b <= bytes && p) return;
+  if (p) cudaFreeAsync(p, st);
+  p = nullptr;
+  st = s;
+  bytes = b;
+  if (b == 0) return;
+  RTB_CUDA(cudaMallocAsync(&p, b, s));
+}
+
+// ---------------------------------------------------------------------------
+// small kernels
+
+__global__ void k_uniform_init(double* out, long long n, unsigned long long seed,
+                               long long offset) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = u64_to_unit(sm_at(seed, (uint64_t)(offset + i)));
+}
+
+__global__ void k_add_diag(double* a, int n, double v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[(size_t)i * n + i] += v;
+}
+
+// sum of squares of several arrays in a fixed order (one block)
+struct NormSet {
+  const double* p[9];
+  long long n[9];
+  int count;
+};
+__global__ void k_norms(NormSet ns, double* out) {
+  __shared__ double red[32];
+  double total = 0.0;
+  for (int a = 0; a < ns.count; ++a) {
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < ns.n[a]; i += blockDim.x) s += ns.p[a][i] * ns.p[a][i];
+    s = block_sum<1024>(s, red);
+    total += s;  // meaningful in thread 0
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = total;
+}
+
+// loss = residual + lambda * reg; rmse = sqrt(residual / size)  (tucker.cpp:216-229)
+__global__ void k_finish_loss(const double* residual, const double* reg, double lambda,
+                              double size, double* loss_out, double* rmse_out) {
+  const double r = *residual;
+  *loss_out = r + lambda * *reg;
+  *rmse_out = sqrt(r / size);
+}
+
+__global__ void k_resid_partials(const double* x, const double* xh, long long n, double* partial) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double d = x[i] - xh[i];
+    s += d * d;
+  }
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// U = A V diag(1/sigma) over the first `rank` eigenpairs (exact core bases)
+__global__ void k_factor_u(const double* A, int I, int R, const double* V, const double* mu,
+                           const int* rank, double* U) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = *rank;
+  if (e >= (long long)I * r) return;
+  const int i = (int)(e / r), k = (int)(e % r);
+  double s = 0.0;
+  for (int j = 0; j < R; ++j) s += A[(size_t)i * R + j] * V[j * R + k];
+  U[e] = s / sqrt(mu[k]);
+}
+
+// rank from eigenvalues of a Gram with the Gram-form cutoff used by k_leverage_rows
+__global__ void k_gram_rank(const double* evals, int stride, const int* rows, const int* cols,
+                            int order, int* ranks) {
+  const int m = threadIdx.x;
+  if (m >= order) return;
+  const double* mu = evals + (size_t)m * stride;
+  const int I = rows[m], R = cols[m];
+  const double cut = (double)(I > R ? I : R) * DBL_EPSILON * mu[0];
+  int r = 0;
+  while (r < R && mu[r] > cut && mu[r] > 0.0) ++r;
+  ranks[m] = r;
+}
+
+// w[t] *= s_t / (s_t^2 + lambda), s_t = prod_n sigma_n[t_n] (tucker.cpp:116-124)
+struct ScaleSpec {
+  int order;
+  int dims[8];
+  const double* mu[8];
+};
+__global__ void k_core_scale(double* w, long long n, ScaleSpec sp, double lambda) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  long long rem = e;
+  double sigma = 1.0;
+  for (int m = sp.order - 1; m >= 0; --m) {
+    const int t = (int)(rem % sp.dims[m]);
+    rem /= sp.dims[m];
+    sigma *= sqrt(sp.mu[m][t]);
+  }
+  w[e] *= sigma / (sigma * sigma + lambda);
+}
+
+__global__ void k_transpose_small(const double* V, int R, int r, double* out /* R x r */) {
+  // out[i][k] = V[i][k] for k < r (V is R x R, column k = eigvec k)
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= R * r) return;
+  const int i = e / r, k = e % r;
+  out[e] = V[i * R + k];
+}
+
+__global__ void k_any_zero_rank(const int* ranks, int order, int* flag) {
+  if (threadIdx.x == 0) {
+    int z = 0;
+    for (int m = 0; m < order; ++m) z |= ranks[m] == 0;
+    *flag = z;
+  }
+}
+
+__global__ void k_check_finite(const double* v, long long n, int* bad) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && !isfinite(v[i])) atomicExch(bad, 1);
+}
+
+// ---------------------------------------------------------------------------
+// profiling (optional per-kernel-family device time)
+
+struct Profiler {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  struct Ev {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Ev> evs;
+  std::map<std::string, KernelTiming> acc;
+  void begin(const char* name, cudaEvent_t* a) {
+    if (!on) return;
+    RTB_CUDA(cudaEventCreate(a));
+    RTB_CUDA(cudaEventRecord(*a, st));
+    (void)name;
+  }
+  void end(const char* name, cudaEvent_t a) {
+    if (!on) return;
+    cudaEvent_t b;
+    RTB_CUDA(cudaEventCreate(&b));
+    RTB_CUDA(cudaEventRecord(b, st));
+    evs.push_back({name, a, b});
+  }
+  void collect() {
+    for (auto& e : evs) {
+      float ms = 0.f;
+      RTB_CUDA(cudaEventSynchronize(e.b));
+      RTB_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+      auto& k = acc[e.name];
+      k.name = e.name;
+      k.total += ms * 1e-3;
+      k.launches += 1;
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    evs.clear();
+  }
+  ~Profiler() {
+    for (auto& e : evs) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+  }
+};
+
+struct Scope {
+  Profiler& p;
+  const char* n;
+  cudaEvent_t a{};
+  Scope(Profiler& pr, const char* name) : p(pr), n(name) { p.begin(n, &a); }
+  ~Scope() {
+    try {
+      p.end(n, a);
+    } catch (...) {
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Engine
+
+static uint64_t prod(const std::vector<uint64_t>& v, size_t from = 0, size_t to = SIZE_MAX) {
+  uint64_t p = 1;
+  for (size_t i = from; i < v.size() && i < to; ++i) p *= v[i];
+  return p;
+}
+
+uint64_t sample_count_formula(double beta_prime, uint64_t d, double epsilon, double delta) {
+  // ref sketch_ridge.cpp:40-50
+  if (beta_prime <= 0.0 || epsilon <= 0.0 || epsilon >= 1.0 || delta <= 0.0 || delta >= 1.0 ||
+      d == 0)
+    throw Error(1, "sample_count: parameters out of range");
+  const double dd = (double)d;
+  const double log_term = 420.0 * std::log(4.0 * dd / delta);
+  const double tail_term = 1.0 / (delta * epsilon);
+  return (uint64_t)std::ceil(4.0 * dd / beta_prime * std::max(log_term, tail_term));
+}
+
+class Engine {
+ public:
+  Engine(const double* x, const std::vector<uint64_t>& shape, const std::vector<uint64_t>& ranks,
+         const AlsOptions& opt)
+      : x_(x), shape_(shape), ranks_(ranks), opt_(opt), N_((int)shape.size()) {
+    st_ = current_stream();
+    prof_.on = opt.profile;
+    prof_.st = st_;
+    total_ = prod(shape_);
+    d_ = prod(ranks_);
+    rmax_ = 0;
+    for (auto r : ranks_) rmax_ = std::max<int>(rmax_, (int)r);
+    eig_stride_ = std::max(rmax_ * rmax_, 1);
+    allocate();
+  }
+
+  // ---- model init (ref tucker.cpp:168-190) and initial loss ----
+  void init_model() {
+    if (opt_.init_core) {
+      RTB_CUDA(cudaMemcpyAsync(core_.p, opt_.init_core, d_ * 8, cudaMemcpyHostToDevice, st_));
+      RTB_CUDA(cudaMemcpyAsync(fac_.p, opt_.init_factors, fac_elems_ * 8, cudaMemcpyHostToDevice,
+                               st_));
+    } else {
+      k_uniform_init<<<ceil_div<long long>(d_, 256), 256, 0, st_>>>(core_.as<double>(), d_,
+                                                                     opt_.seed, 0);
+      RTB_LAUNCH_CHECK();
+      k_uniform_init<<<ceil_div<long long>(fac_elems_, 256), 256, 0, st_>>>(
+          fac_.as<double>(), fac_elems_, opt_.seed, (long long)d_);
+      RTB_LAUNCH_CHECK();
+    }
+    for (int n = 0; n < N_; ++n) factor_gram(n);
+    sketch_rng_ = opt_.seed;
+    // SplitMix64(seed).split(): next_u64 ^ 0x5851f42d4c957f2d (ref rng.hpp:56, tucker.cpp:206)
+    sketch_rng_ = sm_at(opt_.seed, 0) ^ 0x5851f42d4c957f2dULL;
+    sketch_k_ = 0;
+    t_valid_ = false;
+  }
+
+  double* hist_loss(size_t i) { return hist_.as<double>() + 2 * i; }
+
+  void record_loss(size_t slot) {
+    // loss pass writes loss/rmse into history slot `slot`
+    loss_pass(hist_loss(slot), hist_loss(slot) + 1);
+  }
+
+  // ---- one sweep ----
+  void sweep(uint32_t iter) {
+    for (int n = 0; n < N_; ++n) {
+      cudaEvent_t a, b;
+      RTB_CUDA(cudaEventCreate(&a));
+      RTB_CUDA(cudaEventCreate(&b));
+      RTB_CUDA(cudaEventRecord(a, st_));
+      update_factor(n);
+      RTB_CUDA(cudaEventRecord(b, st_));
+      step_events_.push_back({n, a, b});
+      if (opt_.record_history) {
+        hist_rows_.push_back({iter, "F" + std::to_string(n + 1)});
+        record_loss(hist_rows_.size() - 1);
+      }
+    }
+    cudaEvent_t a, b;
+    RTB_CUDA(cudaEventCreate(&a));
+    RTB_CUDA(cudaEventCreate(&b));
+    RTB_CUDA(cudaEventRecord(a, st_));
+    if (opt_.sketched) {
+      // per-sweep sketch seed = sketch_seed_rng.next_u64() (ref tucker.cpp:254-255)
+      const uint64_t seed = sm_at(sketch_rng_, sketch_k_++);
+      update_core_sketched(seed);
+    } else {
+      update_core_exact();
+    }
+    RTB_CUDA(cudaEventRecord(b, st_));
+    step_events_.push_back({N_, a, b});
+    hist_rows_.push_back({iter, "Core"});
+    record_loss(hist_rows_.size() - 1);
+    iterations_ = iter;
+  }
+
+  double last_loss_host() {
+    double v[2];
+    RTB_CUDA(cudaMemcpyAsync(v, hist_loss(hist_rows_.size() - 1), 16, cudaMemcpyDeviceToHost,
+                             st_));
+    RTB_CUDA(cudaStreamSynchronize(st_));
+    return v[0];
+  }
+
+  void initial_loss() {
+    loss_pass(init_loss_.as<double>(), init_loss_.as<double>() + 1);
+  }
+  double initial_loss_host() {
+    double v[2];
+    RTB_CUDA(cudaMemcpyAsync(v, init_loss_.p, 16, cudaMemcpyDeviceToHost, st_));
+    RTB_CUDA(cudaStreamSynchronize(st_));
+    return v[0];
+  }
+
+  void output(AlsOutput& out) {
+    RTB_CUDA(cudaStreamSynchronize(st_));
+    out.shape = shape_;
+    out.ranks = ranks_;
+    out.lambda = opt_.lambda;
+    out.core.resize(d_);
+    out.factors.resize(fac_elems_);
+    RTB_CUDA(cudaMemcpy(out.core.data(), core_.p, d_ * 8, cudaMemcpyDeviceToHost));
+    RTB_CUDA(cudaMemcpy(out.factors.data(), fac_.p, fac_elems_ * 8, cudaMemcpyDeviceToHost));
+    std::vector<double> h(2 * hist_rows_.size());
+    if (!h.empty())
+      RTB_CUDA(cudaMemcpy(h.data(), hist_.p, h.size() * 8, cudaMemcpyDeviceToHost));
+    out.history.clear();
+    for (size_t i = 0; i < hist_rows_.size(); ++i)
+      out.history.push_back({hist_rows_[i].iter, hist_rows_[i].step, h[2 * i], h[2 * i + 1]});
+    out.timings.assign(N_ + 1, StepTiming{});
+    for (int n = 0; n < N_; ++n) out.timings[n].step = "F" + std::to_string(n + 1);
+    out.timings[N_].step = "Core";
+    for (auto& e : step_events_) {
+      float ms = 0.f;
+      RTB_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+      out.timings[e.step].total += ms * 1e-3;
+      out.timings[e.step].count += 1;
+    }
+    prof_.collect();
+    out.kernels.clear();
+    for (auto& kv : prof_.acc) out.kernels.push_back(kv.second);
+    out.iterations = iterations_;
+    if (!out.history.empty()) {
+      out.final_loss = out.history.back().loss;
+      out.final_rmse = out.history.back().rmse;
+    }
+    out.converged = converged_;
+    out.last_sample_count = last_s_;
+    RTB_CUDA(cudaMemcpy(&out.last_data_draws, data_draws_.p, 8, cudaMemcpyDeviceToHost));
+    out.last_rank_deficient = last_rank_deficient_;
+    out.last_solver_path = last_solver_path_;
+    out.sweep_seconds = sweep_seconds_;
+  }
+
+  ~Engine() {
+    for (auto& e : step_events_) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+  }
+
+  // exposed for the single-op entry points
+  void set_model(const double* core_h, const double* fac_h) {
+    RTB_CUDA(cudaMemcpyAsync(core_.p, core_h, d_ * 8, cudaMemcpyHostToDevice, st_));
+    RTB_CUDA(cudaMemcpyAsync(fac_.p, fac_h, fac_elems_ * 8, cudaMemcpyHostToDevice, st_));
+    for (int n = 0; n < N_; ++n) factor_gram(n);
+    t_valid_ = false;
+  }
+  void get_core(double* h) {
+    RTB_CUDA(cudaMemcpyAsync(h, core_.p, d_ * 8, cudaMemcpyDeviceToHost, st_));
+    RTB_CUDA(cudaStreamSynchronize(st_));
+  }
+  void get_factor(int n, double* h) {
+    RTB_CUDA(cudaMemcpyAsync(h, factor(n), shape_[n] * ranks_[n] * 8, cudaMemcpyDeviceToHost, st_));
+    RTB_CUDA(cudaStreamSynchronize(st_));
+  }
+  void update_factor_public(int n) { update_factor(n); }
+  void core_sketched_public(uint64_t s, uint64_t seed, uint64_t* idx, double* w) {
+    opt_.sample_override = s;
+    update_core_sketched(seed);
+    if (idx && last_s_) {
+      RTB_CUDA(cudaMemcpyAsync(idx, sk_idx_.p, last_s_ * 8, cudaMemcpyDeviceToHost, st_));
+      RTB_CUDA(cudaMemcpyAsync(w, sk_w_.p, last_s_ * 8, cudaMemcpyDeviceToHost, st_));
+    }
+    RTB_CUDA(cudaStreamSynchronize(st_));
+  }
+  void core_exact_public() { update_core_exact(); }
+  void loss_public(double* loss, double* rmse) {
+    loss_pass(init_loss_.as<double>(), init_loss_.as<double>() + 1);
+    double v[2];
+    RTB_CUDA(cudaMemcpyAsync(v, init_loss_.p, 16, cudaMemcpyDeviceToHost, st_));
+    RTB_CUDA(cudaStreamSynchronize(st_));
+    *loss = v[0];
+    *rmse = v[1];
+  }
+  void reconstruct(double* out_dev) { reconstruct_full(out_dev); }
+
+  double tolerance() const { return opt_.tolerance; }
+  double prev_loss_ = 0.0;
+  bool have_prev_ = false;
+  uint32_t iterations_ = 0;
+  bool converged_ = false;
+  double sweep_seconds_ = 0.0;
+  cudaStream_t st_;
+
+ private:
+  const double* x_;
+  std::vector<uint64_t> shape_, ranks_;
+  AlsOptions opt_;
+  int N_;
+  uint64_t total_, d_;
+  int rmax_, eig_stride_;
+  uint64_t fac_elems_ = 0;
+  std::vector<uint64_t> fac_off_;
+  Profiler prof_;
+
+  DevBuf ns_vals_;
+  DevBuf core_, fac_, grams_, evals_, evecs_, eig_status_, ns_, pinv_, ranks_dev_;
+  DevBuf T_, P_, tmp_a_, tmp_b_, partial_, scal_, hist_, init_loss_;
+  DevBuf scores_, cdf_, sums_, score_off_, rows_dev_, cols_dev_, flag_;
+  DevBuf sk_idx_, sk_w_, draw_work_, gram_work_, G_, rhs_, chol_work_, chol_status_,
+      data_draws_, zero_flag_, U_[8];
+  uint64_t sketch_rng_ = 0, sketch_k_ = 0;
+  bool t_valid_ = false;
+  uint64_t last_s_ = 0;
+  int last_rank_deficient_ = 0, last_solver_path_ = 0;
+  struct StepEv {
+    int step;
+    cudaEvent_t a, b;
+  };
+  std::vector<StepEv> step_events_;
+  struct HRow {
+    uint32_t iter;
+    std::string step;
+  };
+  std::vector<HRow> hist_rows_;
+  size_t tmp_elems_ = 0;
+
+  double* factor(int n) { return fac_.as<double>() + fac_off_[n]; }
+  double* gram(int n) { return grams_.as<double>() + (size_t)n * eig_stride_; }
+
+  FactorSet factor_set() {
+    FactorSet fs{};
+    fs.order = N_;
+    for (int n = 0; n < N_; ++n) {
+      fs.ptr[n] = factor(n);
+      fs.rows[n] = (int)shape_[n];
+      fs.cols[n] = (int)ranks_[n];
+    }
+    return fs;
+  }
+
+  void allocate() {
+    fac_off_.resize(N_);
+    for (int n = 0; n < N_; ++n) {
+      fac_off_[n] = fac_elems_;
+      fac_elems_ += shape_[n] * ranks_[n];
+    }
+    core_.ensure(d_ * 8, st_);
+    fac_.ensure(fac_elems_ * 8, st_);
+    grams_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
+    pinv_.ensure((size_t)eig_stride_ * 8 + 8, st_);
+    {
+      // eigen_one() may also factor a d <= 64 core Gram into slot 0
+      const size_t eb = std::max<size_t>((size_t)N_ * eig_stride_, 64 * 64) * 8 + 8;
+      evals_.ensure(eb, st_);
+      evecs_.ensure(eb, st_);
+      int vals[65];
+      for (int i = 0; i < 65; ++i) vals[i] = i;
+      ns_vals_.ensure(65 * 4, st_);
+      RTB_CUDA(cudaMemcpy(ns_vals_.p, vals, 65 * 4, cudaMemcpyHostToDevice));
+      const int smem = (2 * 64 * 64 + 2 * 64) * 8;
+      RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    eig_status_.ensure(64 * 4, st_);
+    ns_.ensure(64 * 4, st_);
+    ranks_dev_.ensure(64 * 4, st_);
+    // T and P: (total / I_N) x R_N
+    const uint64_t tsz = total_ / shape_[N_ - 1] * ranks_[N_ - 1];
+    T_.ensure(tsz * 8, st_);
+    P_.ensure(tsz * 8, st_);
+    // chain temporaries: largest intermediate of any TTM chain we run
+    uint64_t mx = d_;
+    {
+      // X x_1 A_1^T: R_1 * total / I_1 ; P chain: prod I_{<N-1} * R_{>=N-1}...
+      for (int n = 0; n < N_; ++n) {
+        std::vector<uint64_t> dims = shape_;
+        for (int m = 0; m < N_; ++m) {
+          if (m == n) continue;
+          dims[m] = ranks_[m];
+          mx = std::max(mx, prod(dims));
+        }
+      }
+      std::vector<uint64_t> dims = ranks_;
+      for (int m = 0; m < N_; ++m) {
+        dims[m] = shape_[m];
+        mx = std::max(mx, prod(dims));
+      }
+    }
+    for (int n = 0; n < N_; ++n) mx = std::max<uint64_t>(mx, shape_[n] * ranks_[n]);
+    mx = std::max<uint64_t>(mx, d_ * d_ <= (1u << 24) ? d_ * d_ : 0);  // pinv fallback scratch
+    tmp_elems_ = mx;
+    tmp_a_.ensure(mx * 8, st_);
+    tmp_b_.ensure(mx * 8, st_);
+    const long long nblk = std::max<long long>(ttm_last_blocks((long long)(total_ / shape_[N_ - 1])),
+                                               kNumSMs * 8);
+    partial_.ensure(nblk * 8, st_);
+    scal_.ensure(4 * 8, st_);
+    hist_.ensure((size_t)std::max<uint32_t>(opt_.max_iterations, 1) * (N_ + 1) * 16 + 16, st_);
+    init_loss_.ensure(16, st_);
+    uint64_t sum_rows = 0;
+    for (auto s : shape_) sum_rows += s;
+    scores_.ensure(sum_rows * 8, st_);
+    cdf_.ensure(sum_rows * 8, st_);
+    sums_.ensure(8 * 8, st_);
+    score_off_.ensure(8 * 8, st_);
+    rows_dev_.ensure(8 * 4, st_);
+    cols_dev_.ensure(8 * 4, st_);
+    flag_.ensure(4, st_);
+    chol_status_.ensure(4, st_);
+    data_draws_.ensure(8, st_);
+    zero_flag_.ensure(4, st_);
+    RTB_CUDA(cudaMemsetAsync(data_draws_.p, 0, 8, st_));
+    long long offs[8] = {0};
+    int rows[8] = {0}, cols[8] = {0};
+    long long o = 0;
+    for (int n = 0; n < N_; ++n) {
+      offs[n] = o;
+      o += (long long)shape_[n];
+      rows[n] = (int)shape_[n];
+      cols[n] = (int)ranks_[n];
+    }
+    RTB_CUDA(cudaMemcpyAsync(score_off_.p, offs, 8 * 8, cudaMemcpyHostToDevice, st_));
+    RTB_CUDA(cudaMemcpyAsync(rows_dev_.p, rows, 8 * 4, cudaMemcpyHostToDevice, st_));
+    RTB_CUDA(cudaMemcpyAsync(cols_dev_.p, cols, 8 * 4, cudaMemcpyHostToDevice, st_));
+    int ns[64];
+    for (int i = 0; i < 64; ++i) ns[i] = i < N_ ? (int)ranks_[i] : 1;
+    RTB_CUDA(cudaMemcpyAsync(ns_.p, ns, 64 * 4, cudaMemcpyHostToDevice, st_));
+    RTB_CUDA(cudaStreamSynchronize(st_));  // host arrays above go out of scope
+  }
+
+  // A_n^T A_n
+  void factor_gram(int n) {
+    Scope sc(prof_, "factor_gram");
+    const int R = (int)ranks_[n];
+    FactorSet fs = factor_set();
+    // launch for a single mode: offset the set
+    FactorSet one{};
+    one.order = 1;
+    one.ptr[0] = fs.ptr[n];
+    one.rows[0] = fs.rows[n];
+    one.cols[0] = fs.cols[n];
+    dim3 grid(R * R, 1);
+    // the kernel indexes grams by mode; write into slot 0 of a view at gram(n)
+    k_factor_gram<<<grid, 256, 0, st_>>>(one, gram(n), R);
+    RTB_LAUNCH_CHECK();
+  }
+
+  // generic mode product on a tensor with dims `dims`: mode m, matrix W (Rn x dims[m])
+  // given by strides; writes `out`, updates dims[m] = Rn.
+  void mode_product(const double* in, std::vector<uint64_t>& dims, int m, const double* W,
+                    long long wr, long long wi, int Rn, double* out, bool w_is_At) {
+    const long long O = (long long)prod(dims, 0, m);
+    const int I = (int)dims[m];
+    const long long J = (long long)prod(dims, m + 1);
+    const long long size = O * I * J;
+    const bool big = size >= (1 << 20);
+    if (big && w_is_At && Rn <= 32) {
+      if (J == 1) {
+        Scope sc(prof_, "ttm_last");
+        ttm_last(in, O, I, W, Rn, out, nullptr, nullptr, st_);
+      } else if (O <= 65535 && J >= 64) {
+        Scope sc(prof_, "ttm_mid");
+        ttm_mid(in, (int)O, I, J, W, Rn, out, st_);
+      } else {
+        Scope sc(prof_, "ttm_generic");
+        ttm_generic(in, O, I, J, W, wr, wi, Rn, out, st_);
+      }
+    } else {
+      Scope sc(prof_, "ttm_generic");
+      ttm_generic(in, O, I, J, W, wr, wi, Rn, out, st_);
+    }
+    dims[m] = Rn;
+  }
+
+  // Y for factor n: dims with I_n at n and R_m elsewhere. Returns pointer into tmp.
+  const double* factor_projection(int n, std::vector<uint64_t>& dims) {
+    dims = shape_;
+    const double* cur = x_;
+    double* bufs[2] = {tmp_a_.as<double>(), tmp_b_.as<double>()};
+    int which = 0;
+    std::vector<int> modes;
+    if (n != N_ - 1) {
+      if (!t_valid_) compute_T();
+      cur = T_.as<double>();
+      dims[N_ - 1] = ranks_[N_ - 1];
+      for (int m = 0; m < N_ - 1; ++m)
+        if (m != n) modes.push_back(m);
+    } else {
+      for (int m = 0; m < N_ - 1; ++m) modes.push_back(m);
+    }
+    for (int m : modes) {
+      const int R = (int)ranks_[m];
+      mode_product(cur, dims, m, factor(m), 1, R, R, bufs[which], true);
+      cur = bufs[which];
+      which ^= 1;
+    }
+    return cur;
+  }
+
+  void compute_T() {
+    // T = X x_N A_N^T (O x R_N), no residual
+    const long long O = (long long)(total_ / shape_[N_ - 1]);
+    const int I = (int)shape_[N_ - 1], R = (int)ranks_[N_ - 1];
+    if (R <= 32) {
+      Scope sc(prof_, "ttm_last");
+      ttm_last(x_, O, I, factor(N_ - 1), R, T_.as<double>(), nullptr, nullptr, st_);
+    } else {
+      Scope sc(prof_, "ttm_generic");
+      ttm_generic(x_, O, I, 1, factor(N_ - 1), 1, R, R, T_.as<double>(), st_);
+    }
+    t_valid_ = true;
+  }
+
+  // ---- exact factor update (ref tucker.cpp:70-89) ----
+  void update_factor(int n) {
+    const int In = (int)shape_[n], Rn = (int)ranks_[n];
+    std::vector<uint64_t> dims;
+    const double* Y = factor_projection(n, dims);
+    // M = Y_(n) G_(n)^T  (I_n x R_n)
+    double* M = (Y == tmp_a_.as<double>()) ? tmp_b_.as<double>() : tmp_a_.as<double>();
+    const long long O = (long long)prod(ranks_, 0, n);
+    const long long J = (long long)prod(ranks_, n + 1);
+    {
+      Scope sc(prof_, "contract");
+      contract_except(Y, core_.as<double>(), O, In, Rn, J, M, st_);
+    }
+    // KK^T = G_(n) (kron_{m!=n} A_m^T A_m) G_(n)^T: Q = G x_{m!=n} Gram_m
+    {
+      Scope sc(prof_, "small_linalg");
+      std::vector<uint64_t> gd = ranks_;
+      const double* cur = core_.as<double>();
+      double* qb[2] = {scratch_q(0), scratch_q(1)};
+      int which = 0;
+      for (int m = 0; m < N_; ++m) {
+        if (m == n) continue;
+        const int R = (int)ranks_[m];
+        ttm_generic(cur, (long long)prod(gd, 0, m), R, (long long)prod(gd, m + 1), gram(m), R, 1, R,
+                    qb[which], st_);
+        cur = qb[which];
+        which ^= 1;
+      }
+      double* kk = pinv_.as<double>();
+      contract_except(core_.as<double>(), cur, O, Rn, Rn, J, kk, st_);
+      k_add_diag<<<ceil_div(Rn, 64), 64, 0, st_>>>(kk, Rn, opt_.lambda);
+      RTB_LAUNCH_CHECK();
+      // pinv via eigen (symmetric): singular values = |eigenvalues| (ref linalg.cpp:8-26)
+      eigen_one(kk, Rn);
+      k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(),
+                                     ns_one(Rn), eig_stride_, kk, nullptr);
+      RTB_LAUNCH_CHECK();
+      // A_n = M pinv
+      const long long tot = (long long)In * Rn;
+      k_rows_times_small<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(M, kk, In, Rn, factor(n));
+      RTB_LAUNCH_CHECK();
+    }
+    factor_gram(n);
+    if (n == N_ - 1) t_valid_ = false;
+  }
+
+  DevBuf qbuf_[2];
+  double* scratch_q(int i) {
+    qbuf_[i].ensure((std::max<uint64_t>(d_, (uint64_t)rmax_ * rmax_) + 1) * 8, st_);
+    return qbuf_[i].as<double>();
+  }
+  // device array {0, 1, ..., 64}: ns_one(n) points at the value n
+  int* ns_one(int n) { return ns_vals_.as<int>() + n; }
+
+  // eigen of one symmetric n x n matrix (device) into slot 0 of evals/evecs
+  void eigen_one(const double* m, int n) {
+    const int np = n + (n & 1);
+    const size_t smem = (2 * (size_t)np * np + 2 * np) * 8;
+    if (n > 64) throw Error(4, "eigen: n > 64 not supported");
+    k_sym_eigen<<<1, 128, smem, st_>>>(m, ns_one(n), eig_stride_, evals_.as<double>(),
+                                       evecs_.as<double>(), eig_status_.as<int>());
+    RTB_LAUNCH_CHECK();
+  }
+
+  // eigen of all factor Grams (batched, one CTA each)
+  void eigen_grams() {
+    const int np = rmax_ + (rmax_ & 1);
+    const size_t smem = (2 * (size_t)np * np + 2 * np) * 8;
+    if (rmax_ > 64) throw Error(4, "eigen: rank > 64 not supported");
+    k_sym_eigen<<<N_, 128, smem, st_>>>(grams_.as<double>(), ns_.as<int>(), eig_stride_,
+                                        evals_.as<double>(), evecs_.as<double>(),
+                                        eig_status_.as<int>());
+    RTB_LAUNCH_CHECK();
+  }
+
+  // ---- sketched core (ref tucker.cpp:141-166, sketch_ridge.cpp:52-151) ----
+  void update_core_sketched(uint64_t seed) {
+    uint64_t s = opt_.sample_override;
+    if (s == 0) s = sample_count_formula(0.5, d_, opt_.epsilon, opt_.delta);
+    last_s_ = s;
+    // shard of the draw range for multi-GPU sample sharding
+    {
+      Scope sc(prof_, "scores");
+      eigen_grams();
+      FactorSet fs = factor_set();
+      int maxI = 0;
+      for (auto v : shape_) maxI = std::max<int>(maxI, (int)v);
+      dim3 grid(ceil_div(maxI, 128), N_);
+      k_leverage_rows<<<grid, 128, 0, st_>>>(fs, evals_.as<double>(), evecs_.as<double>(),
+                                            eig_stride_, 0.0, scores_.as<double>(),
+                                            score_off_.as<long long>(), ranks_dev_.as<int>());
+      RTB_LAUNCH_CHECK();
+      k_score_cdf<<<1, 32, 0, st_>>>(scores_.as<double>(), score_off_.as<long long>(),
+                                     rows_dev_.as<int>(), N_, cdf_.as<double>(), sums_.as<double>());
+      RTB_LAUNCH_CHECK();
+      k_any_zero_rank<<<1, 32, 0, st_>>>(ranks_dev_.as<int>(), N_, zero_flag_.as<int>());
+      RTB_LAUNCH_CHECK();
+    }
+    DrawSpec ds{};
+    ds.order = N_;
+    long long off = 0;
+    for (int n = 0; n < N_; ++n) {
+      ds.rows[n] = (long long)shape_[n];
+      ds.cdf_off[n] = off;
+      off += (long long)shape_[n];
+    }
+    ds.total_rows = total_;
+    ds.d = d_;
+    ds.seed = seed;
+    ds.s = s;
+    sk_idx_.ensure(s * 8, st_);
+    sk_w_.ensure(s * 8, st_);
+    draw_work_.ensure(draw_work_bytes(ds), st_);
+    RTB_CUDA(cudaMemsetAsync(flag_.p, 0, 4, st_));
+    {
+      Scope sc(prof_, "draw");
+      draw_sketch(ds, scores_.as<double>(), cdf_.as<double>(), sums_.as<double>(),
+                  DrawWork{draw_work_.p, draw_work_.bytes}, (unsigned long long*)sk_idx_.p,
+                  sk_w_.as<double>(), flag_.as<int>(), st_);
+    }
+    solve_sketch(s);
+  }
+
+  GramSpec gram_spec(uint64_t s) {
+    GramSpec gs{};
+    gs.order = N_;
+    for (int n = 0; n < N_; ++n) {
+      gs.rows[n] = (int)shape_[n];
+      gs.ranks[n] = (int)ranks_[n];
+      gs.factors[n] = factor(n);
+    }
+    gs.total_rows = total_;
+    gs.d = (int)d_;
+    gs.dprime = (int)(d_ / ranks_[0]);
+    gs.lambda = opt_.lambda;
+    gs.s = s;
+    return gs;
+  }
+
+ public:
+  // normal equations from sk_idx_/sk_w_ (s draws) and solve into the core
+  void solve_sketch(uint64_t s) {
+    GramSpec gs = gram_spec(s);
+    gram_work_.ensure(gram_work_bytes(gs), st_);
+    G_.ensure(d_ * d_ * 8, st_);
+    rhs_.ensure(d_ * 8, st_);
+    {
+      Scope sc(prof_, "gram");
+      sketch_normal_eq(gs, x_, (const unsigned long long*)sk_idx_.p, sk_w_.as<double>(),
+                       gram_work_.p, gram_work_.bytes, G_.as<double>(), rhs_.as<double>(),
+                       (unsigned long long*)data_draws_.p, st_);
+    }
+    if (opt_.allreduce && opt_.shard_count > 1) {
+      opt_.allreduce(G_.as<double>(), d_ * d_, st_, opt_.allreduce_user);
+      opt_.allreduce(rhs_.as<double>(), d_, st_, opt_.allreduce_user);
+    }
+    chol_work_.ensure(chol_work_bytes((int)d_), st_);
+    {
+      Scope sc(prof_, "chol");
+      chol_solve(G_.as<double>(), (int)d_, rhs_.as<double>(), chol_status_.as<int>(),
+                 chol_work_.p, st_);
+    }
+    int status[2] = {0, 0};
+    RTB_CUDA(cudaMemcpyAsync(&status[0], chol_status_.p, 4, cudaMemcpyDeviceToHost, st_));
+    RTB_CUDA(cudaMemcpyAsync(&status[1], zero_flag_.p, 4, cudaMemcpyDeviceToHost, st_));
+    RTB_CUDA(cudaStreamSynchronize(st_));
+    last_solver_path_ = 0;
+    last_rank_deficient_ = 0;
+    if (status[1]) {  // a zero factor: the minimiser is the zero core (tucker.cpp:148-154)
+      RTB_CUDA(cudaMemsetAsync(core_.p, 0, d_ * 8, st_));
+      return;
+    }
+    if (status[0]) {
+      // not positive definite: recompute the Gram and take the pinv route
+      if (d_ > 64)
+        throw Error(3, "sketched Gram is not positive definite (d > 64 pinv fallback "
+                       "not available)");
+      sketch_normal_eq(gs, x_, (const unsigned long long*)sk_idx_.p, sk_w_.as<double>(),
+                       gram_work_.p, gram_work_.bytes, G_.as<double>(), rhs_.as<double>(),
+                       (unsigned long long*)data_draws_.p, st_);
+      if (opt_.allreduce && opt_.shard_count > 1) {
+        opt_.allreduce(G_.as<double>(), d_ * d_, st_, opt_.allreduce_user);
+        opt_.allreduce(rhs_.as<double>(), d_, st_, opt_.allreduce_user);
+      }
+      eigen_one(G_.as<double>(), (int)d_);
+      double* pv = tmp_a_.as<double>();
+      k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one((int)d_),
+                                     eig_stride_ > (int)(d_ * d_) ? eig_stride_ : (int)(d_ * d_),
+                                     pv, ranks_dev_.as<int>());
+      RTB_LAUNCH_CHECK();
+      k_rows_times_small<<<ceil_div<long long>(d_, 256), 256, 0, st_>>>(rhs_.as<double>(), pv, 1,
+                                                                        (int)d_, core_.as<double>());
+      RTB_LAUNCH_CHECK();
+      int rank = 0;
+      RTB_CUDA(cudaMemcpyAsync(&rank, ranks_dev_.p, 4, cudaMemcpyDeviceToHost, st_));
+      RTB_CUDA(cudaStreamSynchronize(st_));
+      last_solver_path_ = 1;
+      last_rank_deficient_ = rank < (int)d_;
+    } else {
+      RTB_CUDA(cudaMemcpyAsync(core_.p, rhs_.p, d_ * 8, cudaMemcpyDeviceToDevice, st_));
+    }
+    check_core_finite();
+  }
+
+ private:
+  void check_core_finite() {
+    RTB_CUDA(cudaMemsetAsync(flag_.p, 0, 4, st_));
+    k_check_finite<<<ceil_div<long long>(d_, 256), 256, 0, st_>>>(core_.as<double>(), d_,
+                                                                   flag_.as<int>());
+    RTB_LAUNCH_CHECK();
+    int bad = 0;
+    RTB_CUDA(cudaMemcpyAsync(&bad, flag_.p, 4, cudaMemcpyDeviceToHost, st_));
+    RTB_CUDA(cudaStreamSynchronize(st_));
+    if (bad) throw Error(1, "DenseTensor: non-finite entry");  // ref tensor.cpp:32-42
+  }
+
+  // ---- exact core (ref tucker.cpp:91-129) ----
+  void update_core_exact() {
+    Scope sc(prof_, "core_exact");
+    eigen_grams();
+    k_gram_rank<<<1, 32, 0, st_>>>(evals_.as<double>(), eig_stride_, rows_dev_.as<int>(),
+                                   cols_dev_.as<int>(), N_, ranks_dev_.as<int>());
+    RTB_LAUNCH_CHECK();
+    int rk[8];
+    RTB_CUDA(cudaMemcpyAsync(rk, ranks_dev_.p, N_ * 4, cudaMemcpyDeviceToHost, st_));
+    RTB_CUDA(cudaStreamSynchronize(st_));
+    for (int n = 0; n < N_; ++n)
+      if (rk[n] == 0) {
+        RTB_CUDA(cudaMemsetAsync(core_.p, 0, d_ * 8, st_));
+        return;
+      }
+    // U_n = A_n V_n Sigma_n^-1 (I_n x r_n)
+    for (int n = 0; n < N_; ++n) {
+      U_[n].ensure(shape_[n] * rk[n] * 8 + 8, st_);
+      const long long tot = (long long)shape_[n] * rk[n];
+      k_factor_u<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(
+          factor(n), (int)shape_[n], (int)ranks_[n], evecs_.as<double>() + (size_t)n * eig_stride_,
+          evals_.as<double>() + (size_t)n * eig_stride_, ranks_dev_.as<int>() + n,
+          U_[n].as<double>());
+      RTB_LAUNCH_CHECK();
+    }
+    // W = X x_n U_n^T, last mode first (contiguous), then the others
+    std::vector<uint64_t> dims = shape_;
+    double* bufs[2] = {tmp_a_.as<double>(), tmp_b_.as<double>()};
+    int which = 0;
+    const double* cur = x_;
+    std::vector<int> order;
+    order.push_back(N_ - 1);
+    for (int m = 0; m < N_ - 1; ++m) order.push_back(m);
+    for (int m : order) {
+      mode_product(cur, dims, m, U_[m].as<double>(), 1, rk[m], rk[m], bufs[which], true);
+      cur = bufs[which];
+      which ^= 1;
+    }
+    // scale by sigma_t / (sigma_t^2 + lambda)
+    ScaleSpec sp{};
+    sp.order = N_;
+    long long n_el = 1;
+    for (int m = 0; m < N_; ++m) {
+      sp.dims[m] = rk[m];
+      sp.mu[m] = evals_.as<double>() + (size_t)m * eig_stride_;
+      n_el *= rk[m];
+    }
+    k_core_scale<<<ceil_div<long long>(n_el, 256), 256, 0, st_>>>(const_cast<double*>(cur), n_el,
+                                                                  sp, opt_.lambda);
+    RTB_LAUNCH_CHECK();
+    // core = W x_n V_n (V_n: R_n x r_n)
+    for (int m = 0; m < N_; ++m) {
+      const int R = (int)ranks_[m], r = rk[m];
+      double* Vt = scratch_q(0);
+      k_transpose_small<<<ceil_div(R * r, 256), 256, 0, st_>>>(
+          evecs_.as<double>() + (size_t)m * eig_stride_, R, r, Vt);
+      RTB_LAUNCH_CHECK();
+      double* out = (m == N_ - 1) ? core_.as<double>() : bufs[which];
+      // out[.., i, ..] = sum_k V[i][k] W[.., k, ..]: W_mat(R x r) = Vt row-major (wr=r, wi=1)
+      ttm_generic(cur, (long long)prod(dims, 0, m), r, (long long)prod(dims, m + 1), Vt, r, 1, R, out,
+                  st_);
+      dims[m] = R;
+      cur = out;
+      which ^= 1;
+    }
+    check_core_finite();
+  }
+
+  // P = G x_1 A_1 ... x_{N-1} A_{N-1}  (last mode stays R_N)
+  const double* build_P(std::vector<uint64_t>& dims) {
+    dims = ranks_;
+    const double* cur = core_.as<double>();
+    double* bufs[2] = {tmp_a_.as<double>(), tmp_b_.as<double>()};
+    int which = 0;
+    for (int m = 0; m < N_ - 1; ++m) {
+      const int I = (int)shape_[m], R = (int)ranks_[m];
+      double* out = (m == N_ - 2) ? P_.as<double>() : bufs[which];
+      // out[.., i, ..] = sum_r A[i][r] cur[.., r, ..]  (W = A: wr = R, wi = 1)
+      Scope sc(prof_, "ttm_generic");
+      ttm_generic(cur, (long long)prod(dims, 0, m), R, (long long)prod(dims, m + 1), factor(m), R, 1,
+                  I, out, st_);
+      dims[m] = I;
+      cur = out;
+      which ^= 1;
+    }
+    if (N_ == 1) return core_.as<double>();
+    return cur;
+  }
+
+  // Loss pass (fused with T = X x_N A_N^T). Writes loss/rmse to device ptrs.
+  void loss_pass(double* loss_dev, double* rmse_dev) {
+    std::vector<uint64_t> dims;
+    const double* P = build_P(dims);
+    const long long O = (long long)(total_ / shape_[N_ - 1]);
+    const int I = (int)shape_[N_ - 1], R = (int)ranks_[N_ - 1];
+    double* partial = partial_.as<double>();
+    long long nparts;
+    if (R <= 32) {
+      Scope sc(prof_, "ttm_last_loss");
+      ttm_last(x_, O, I, factor(N_ - 1), R, T_.as<double>(), P, partial, st_);
+      nparts = ttm_last_blocks(O);
+      t_valid_ = true;
+    } else {
+      // generic: full reconstruction then residual
+      DevBuf xh(total_ * 8, st_);
+      ttm_generic(P, O, R, 1, factor(N_ - 1), R, 1, I, xh.as<double>(), st_);
+      k_resid_partials<<<kNumSMs * 8, 256, 0, st_>>>(x_, xh.as<double>(), (long long)total_,
+                                                      partial);
+      RTB_LAUNCH_CHECK();
+      nparts = kNumSMs * 8;
+      compute_T();
+    }
+    double* sc = scal_.as<double>();
+    sum_partials(partial, nparts, sc, st_);
+    NormSet ns{};
+    ns.count = N_ + 1;
+    ns.p[0] = core_.as<double>();
+    ns.n[0] = (long long)d_;
+    for (int n = 0; n < N_; ++n) {
+      ns.p[n + 1] = factor(n);
+      ns.n[n + 1] = (long long)(shape_[n] * ranks_[n]);
+    }
+    k_norms<<<1, 1024, 0, st_>>>(ns, sc + 1);
+    RTB_LAUNCH_CHECK();
+    k_finish_loss<<<1, 1, 0, st_>>>(sc, sc + 1, opt_.lambda, (double)total_, loss_dev, rmse_dev);
+    RTB_LAUNCH_CHECK();
+  }
+
+  void reconstruct_full(double* out) {
+    std::vector<uint64_t> dims;
+    const double* P = build_P(dims);
+    const long long O = (long long)(total_ / shape_[N_ - 1]);
+    const int I = (int)shape_[N_ - 1], R = (int)ranks_[N_ - 1];
+    ttm_generic(P, O, R, 1, factor(N_ - 1), R, 1, I, out, st_);
+  }
+
+};
+
+Session::~Session() { delete e; }
+
+static void validate(const std::vector<uint64_t>& shape, const std::vector<uint64_t>& ranks,
+                     const AlsOptions& opt) {
+  // ref tucker.cpp:194-199, 182-184; tensor.cpp:7-20
+  if (opt.max_iterations == 0) throw Error(1, "als: max_iterations must be >= 1");
+  if (ranks.size() != shape.size()) throw Error(1, "als: ranks order != tensor order");
+  if (shape.empty() || shape.size() > 8) throw Error(1, "DenseTensor: order must be in [1, 8]");
+  for (size_t n = 0; n < shape.size(); ++n)
+    if (ranks[n] == 0 || ranks[n] > shape[n])
+      throw Error(1, "random_model: rank outside [1, I_n]");
+}
+
+Session* session_create(const double* x_dev, const std::vector<uint64_t>& shape,
+                        const std::vector<uint64_t>& ranks, const AlsOptions& opt) {
+  validate(shape, ranks, opt);
+  auto s = std::make_unique<Session>();
+  s->e = new Engine(x_dev, shape, ranks, opt);
+  s->e->init_model();
+  s->e->initial_loss();
+  return s.release();
+}
+
+uint32_t session_run(Session* s, uint32_t n, bool check_tol) {
+  Engine& e = *s->e;
+  if (check_tol && !e.have_prev_) {
+    e.prev_loss_ = e.initial_loss_host();
+    e.have_prev_ = true;
+  }
+  double prev = e.prev_loss_;
+  uint32_t run = 0;
+  cudaEvent_t a, b;
+  RTB_CUDA(cudaEventCreate(&a));
+  RTB_CUDA(cudaEventCreate(&b));
+  RTB_CUDA(cudaEventRecord(a, e.st_));
+  for (uint32_t k = 0; k < n; ++k) {
+    e.sweep(e.iterations_ + 1);
+    ++run;
+    if (check_tol) {
+      const double loss = e.last_loss_host();
+      const double change = std::abs(prev - loss) / std::max(std::abs(prev), 1e-300);
+      prev = loss;
+      e.prev_loss_ = loss;
+      if (change < e.tolerance()) {
+        e.converged_ = true;
+        break;
+      }
+    }
+  }
+  RTB_CUDA(cudaEventRecord(b, e.st_));
+  RTB_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  RTB_CUDA(cudaEventElapsedTime(&ms, a, b));
+  e.sweep_seconds_ += ms * 1e-3;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return run;
+}
+
+}  // namespace rtb
+
+namespace rtb {
+
+void session_output(Session* s, AlsOutput& out) { s->e->output(out); }
+
+void als_run(const double* x_dev, const std::vector<uint64_t>& shape,
+             const std::vector<uint64_t>& ranks, const AlsOptions& opt, AlsOutput& out) {
+  std::unique_ptr<Session> s(session_create(x_dev, shape, ranks, opt));
+  // tolerance <= 0 can never stop early (change < tol is false): no per-sweep sync
+  session_run(s.get(), opt.max_iterations, opt.tolerance > 0.0);
+  session_output(s.get(), out);
+}
+
+// ---------------------------------------------------------------------------
+// single-operation entry points
+
+namespace {
+struct HostModel {
+  std::vector<uint64_t> shape, ranks;
+};
+AlsOptions op_opts(double lambda) {
+  AlsOptions o;
+  o.lambda = lambda;
+  o.max_iterations = 1;
+  return o;
+}
+}  // namespace
+
+void model_update_core_sketched(const double* x_dev, const std::vector<uint64_t>& shape,
+                                const std::vector<uint64_t>& ranks, const double* core,
+                                const double* factors, double lambda, uint64_t s, uint64_t seed,
+                                double* core_out, uint64_t* idx_out, double* w_out) {
+  validate(shape, ranks, op_opts(lambda));
+  AlsOptions o = op_opts(lambda);
+  o.sketched = true;
+  Engine e(x_dev, shape, ranks, o);
+  e.set_model(core, factors);
+  e.core_sketched_public(s, seed, idx_out, w_out);
+  e.get_core(core_out);
+}
+
+void model_update_factor(const double* x_dev, const std::vector<uint64_t>& shape,
+                         const std::vector<uint64_t>& ranks, const double* core,
+                         const double* factors, double lambda, uint32_t mode, double* out) {
+  validate(shape, ranks, op_opts(lambda));
+  if (mode < 1 || mode > shape.size()) throw Error(1, "update_factor: mode out of range");
+  Engine e(x_dev, shape, ranks, op_opts(lambda));
+  e.set_model(core, factors);
+  e.update_factor_public((int)mode - 1);
+  e.get_factor((int)mode - 1, out);
+}
+
+void model_update_core_exact(const double* x_dev, const std::vector<uint64_t>& shape,
+                             const std::vector<uint64_t>& ranks, const double* core,
+                             const double* factors, double lambda, double* core_out) {
+  validate(shape, ranks, op_opts(lambda));
+  Engine e(x_dev, shape, ranks, op_opts(lambda));
+  e.set_model(core, factors);
+  e.core_exact_public();
+  e.get_core(core_out);
+}
+
+void model_loss(const double* x_dev, const std::vector<uint64_t>& shape,
+                const std::vector<uint64_t>& ranks, const double* core, const double* factors,
+                double lambda, double* loss, double* rmse) {
+  validate(shape, ranks, op_opts(lambda));
+  Engine e(x_dev, shape, ranks, op_opts(lambda));
+  e.set_model(core, factors);
+  e.loss_public(loss, rmse);
+}
+
+void model_reconstruct(const std::vector<uint64_t>& shape, const std::vector<uint64_t>& ranks,
+                       const double* core, const double* factors, double* out_host) {
+  validate(shape, ranks, op_opts(0.0));
+  cudaStream_t st = current_stream();
+  const uint64_t total = prod(shape);
+  DevBuf xd(total * 8, st);
+  Engine e(xd.as<double>(), shape, ranks, op_opts(0.0));
+  e.set_model(core, factors);
+  e.reconstruct(xd.as<double>());
+  RTB_CUDA(cudaMemcpyAsync(out_host, xd.p, total * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+}
+
+// Per-factor scores through the same kernels as the ALS core step.
+void factor_scores(const double* factor_host, int rows, int cols, double* scores, double* cdf,
+                   double* sum, uint64_t* rank) {
+  if (rows <= 0 || cols <= 0) throw Error(1, "compact_svd: empty matrix");
+  if (cols > 64) throw Error(4, "factor_scores: rank > 64 not supported");
+  cudaStream_t st = current_stream();
+  DevBuf f((size_t)rows * cols * 8, st), g((size_t)cols * cols * 8, st),
+      ev((size_t)cols * cols * 8 + 8, st), evec((size_t)cols * cols * 8, st), stat(4, st),
+      ns(4, st), sc((size_t)rows * 8, st), cd((size_t)rows * 8, st), sm(8, st), off(8, st),
+      rw(4, st), rk(4, st);
+  RTB_CUDA(cudaMemcpyAsync(f.p, factor_host, (size_t)rows * cols * 8, cudaMemcpyHostToDevice, st));
+  long long zero = 0;
+  RTB_CUDA(cudaMemcpyAsync(off.p, &zero, 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(rw.p, &rows, 4, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(ns.p, &cols, 4, cudaMemcpyHostToDevice, st));
+  FactorSet fs{};
+  fs.order = 1;
+  fs.ptr[0] = f.as<double>();
+  fs.rows[0] = rows;
+  fs.cols[0] = cols;
+  k_factor_gram<<<dim3(cols * cols, 1), 256, 0, st>>>(fs, g.as<double>(), cols);
+  RTB_LAUNCH_CHECK();
+  const int np = cols + (cols & 1);
+  const int smem = (2 * np * np + 2 * np) * 8;
+  RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (2 * 64 * 64 + 2 * 64) * 8));
+  k_sym_eigen<<<1, 128, smem, st>>>(g.as<double>(), ns.as<int>(), cols * cols, ev.as<double>(),
+                                    evec.as<double>(), stat.as<int>());
+  RTB_LAUNCH_CHECK();
+  k_leverage_rows<<<dim3(ceil_div(rows, 128), 1), 128, 0, st>>>(
+      fs, ev.as<double>(), evec.as<double>(), cols * cols, 0.0, sc.as<double>(),
+      off.as<long long>(), rk.as<int>());
+  RTB_LAUNCH_CHECK();
+  k_score_cdf<<<1, 32, 0, st>>>(sc.as<double>(), off.as<long long>(), rw.as<int>(), 1,
+                                cd.as<double>(), sm.as<double>());
+  RTB_LAUNCH_CHECK();
+  int r = 0, es = 0;
+  RTB_CUDA(cudaMemcpyAsync(scores, sc.p, (size_t)rows * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaMemcpyAsync(cdf, cd.p, (size_t)rows * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaMemcpyAsync(sum, sm.p, 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaMemcpyAsync(&r, rk.p, 4, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaMemcpyAsync(&es, stat.p, 4, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  if (es) throw Error(3, "symmetric eigensolver did not converge");
+  *rank = (uint64_t)r;
+}
+
+void kron_draw(int order, const uint64_t* rows, uint64_t d, const double* scores,
+               const double* cdfs, const double* sums, uint64_t seed, uint64_t s, uint64_t* idx,
+               double* w) {
+  if (order < 1 || order > 8) throw Error(1, "kron_draw: order must be in [1, 8]");
+  if (d == 0 || s == 0) throw Error(1, "kron_draw: d and s must be positive");
+  cudaStream_t st = current_stream();
+  uint64_t sum_rows = 0, total = 1;
+  DrawSpec ds{};
+  ds.order = order;
+  for (int n = 0; n < order; ++n) {
+    ds.rows[n] = (long long)rows[n];
+    ds.cdf_off[n] = (long long)sum_rows;
+    sum_rows += rows[n];
+    total *= rows[n];
+  }
+  ds.total_rows = total;
+  ds.d = d;
+  ds.seed = seed;
+  ds.s = s;
+  DevBuf sc(sum_rows * 8, st), cd(sum_rows * 8, st), sm(order * 8, st), ix(s * 8, st),
+      ww(s * 8, st), work(draw_work_bytes(ds), st), flag(4, st);
+  RTB_CUDA(cudaMemcpyAsync(sc.p, scores, sum_rows * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(cd.p, cdfs, sum_rows * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(sm.p, sums, order * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
+  draw_sketch(ds, sc.as<double>(), cd.as<double>(), sm.as<double>(), DrawWork{work.p, work.bytes},
+              (unsigned long long*)ix.p, ww.as<double>(), flag.as<int>(), st);
+  int bad = 0;
+  RTB_CUDA(cudaMemcpyAsync(idx, ix.p, s * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaMemcpyAsync(w, ww.p, s * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  if (bad) throw Error(1, "ImplicitKronecker: cannot sample, factor has no nonzero rows");
+}
+
+void kron_normal_eq(int order, const uint64_t* rows, const uint64_t* ranks, const double* factors,
+                    const double* x_host, double lambda, uint64_t s, const uint64_t* idx,
+                    const double* w, double* gram, double* rhs) {
+  if (order < 1 || order > 8) throw Error(1, "kron_normal_eq: order must be in [1, 8]");
+  cudaStream_t st = current_stream();
+  std::vector<uint64_t> shape(rows, rows + order), rk(ranks, ranks + order);
+  const uint64_t total = prod(shape), d = prod(rk);
+  uint64_t fe = 0;
+  for (int n = 0; n < order; ++n) fe += shape[n] * rk[n];
+  DevBuf xd(total * 8, st), fd(fe * 8, st), ix(s * 8, st), ww(s * 8, st), G(d * d * 8, st),
+      r(d * 8, st), dd(8, st);
+  RTB_CUDA(cudaMemcpyAsync(xd.p, x_host, total * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(fd.p, factors, fe * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(ix.p, idx, s * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(ww.p, w, s * 8, cudaMemcpyHostToDevice, st));
+  GramSpec gs{};
+  gs.order = order;
+  uint64_t off = 0;
+  for (int n = 0; n < order; ++n) {
+    gs.rows[n] = (int)shape[n];
+    gs.ranks[n] = (int)rk[n];
+    gs.factors[n] = fd.as<double>() + off;
+    off += shape[n] * rk[n];
+  }
+  gs.total_rows = total;
+  gs.d = (int)d;
+  gs.dprime = (int)(d / rk[0]);
+  gs.lambda = lambda;
+  gs.s = s;
+  DevBuf work(gram_work_bytes(gs), st);
+  sketch_normal_eq(gs, xd.as<double>(), (const unsigned long long*)ix.p, ww.as<double>(), work.p,
+                   work.bytes, G.as<double>(), r.as<double>(), (unsigned long long*)dd.p, st);
+  RTB_CUDA(cudaMemcpyAsync(gram, G.p, d * d * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaMemcpyAsync(rhs, r.p, d * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+}
+
+// x = gram^+ rhs: Cholesky, else (d <= 64) eigen pinv with the reference cutoff.
+static void solve_sym_device(double* G, double* rhs, int d, double* x_dev, int* rank, int* path,
+                             bool need_spd_else_error, cudaStream_t st) {
+  DevBuf work(chol_work_bytes(d), st), stat(4, st), copy((size_t)d * d * 8, st);
+  RTB_CUDA(cudaMemcpyAsync(copy.p, G, (size_t)d * d * 8, cudaMemcpyDeviceToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(x_dev, rhs, (size_t)d * 8, cudaMemcpyDeviceToDevice, st));
+  chol_solve(copy.as<double>(), d, x_dev, stat.as<int>(), work.p, st);
+  int status = 0;
+  RTB_CUDA(cudaMemcpyAsync(&status, stat.p, 4, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  if (status == 0) {
+    *rank = d;
+    *path = 0;
+    return;
+  }
+  if (d > 64) {
+    if (need_spd_else_error)
+      throw Error(3, "matrix is not positive definite (pinv fallback limited to d <= 64)");
+  }
+  DevBuf ev((size_t)d * d * 8 + 8, st), evec((size_t)d * d * 8, st), es(4, st), ns(4, st),
+      pv((size_t)d * d * 8, st), rk(4, st);
+  RTB_CUDA(cudaMemcpyAsync(ns.p, &d, 4, cudaMemcpyHostToDevice, st));
+  const int np = d + (d & 1);
+  RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (2 * 64 * 64 + 2 * 64) * 8));
+  k_sym_eigen<<<1, 128, (2 * np * np + 2 * np) * 8, st>>>(G, ns.as<int>(), d * d, ev.as<double>(),
+                                                          evec.as<double>(), es.as<int>());
+  RTB_LAUNCH_CHECK();
+  k_sym_pinv<<<1, 256, 0, st>>>(ev.as<double>(), evec.as<double>(), ns.as<int>(), d * d,
+                                pv.as<double>(), rk.as<int>());
+  RTB_LAUNCH_CHECK();
+  k_rows_times_small<<<ceil_div(d, 256), 256, 0, st>>>(rhs, pv.as<double>(), 1, d, x_dev);
+  RTB_LAUNCH_CHECK();
+  int e = 0;
+  RTB_CUDA(cudaMemcpyAsync(rank, rk.p, 4, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaMemcpyAsync(&e, es.p, 4, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  if (e) throw Error(3, "symmetric_eigen: Jacobi sweeps did not converge");
+  *path = 1;
+}
+
+void spd_solve(const double* gram, const double* rhs, uint64_t d, double* x, uint64_t* rank,
+               int* path) {
+  if (d == 0) throw Error(1, "compact_svd: empty matrix");
+  cudaStream_t st = current_stream();
+  DevBuf G(d * d * 8, st), r(d * 8, st), xd(d * 8, st);
+  RTB_CUDA(cudaMemcpyAsync(G.p, gram, d * d * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(r.p, rhs, d * 8, cudaMemcpyHostToDevice, st));
+  int rk = 0, pth = 0;
+  solve_sym_device(G.as<double>(), r.as<double>(), (int)d, xd.as<double>(), &rk, &pth, true, st);
+  RTB_CUDA(cudaMemcpyAsync(x, xd.p, d * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  if (rank) *rank = (uint64_t)rk;
+  if (path) *path = pth;
+}
+
+// ---------------------------------------------------------------------------
+// dense ridge toolkit (ref capi.cpp:299-362, linalg.cpp:28-41, leverage.cpp:39-52,
+// sampler.cpp:9-57, sketch_ridge.cpp:52-164)
+
+__global__ void k_atb(const double* a, long long n, int d, const double* b, double* out) {
+  __shared__ double red[32];
+  const int j = blockIdx.x;
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) s += a[i * d + j] * b[i];
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) out[j] = s;
+}
+
+__global__ void k_any_nonzero(const double* a, long long n, int* flag) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && a[i] != 0.0) atomicExch(flag, 1);
+}
+
+static void dense_gram(const double* a_dev, uint64_t n, uint64_t d, double* g_dev,
+                       cudaStream_t st) {
+  FactorSet fs{};
+  fs.order = 1;
+  fs.ptr[0] = a_dev;
+  fs.rows[0] = (int)n;
+  fs.cols[0] = (int)d;
+  k_factor_gram<<<dim3((unsigned)(d * d), 1), 256, 0, st>>>(fs, g_dev, (int)d);
+  RTB_LAUNCH_CHECK();
+}
+
+void dense_ridge_scores(const double* a, uint64_t n, uint64_t d, double lambda, double* out) {
+  if (lambda < 0.0) throw Error(1, "ridge_scores: lambda must be non-negative");
+  if (n == 0 || d == 0) throw Error(1, "compact_svd: empty matrix");
+  if (d > 64) throw Error(4, "ridge_scores: d > 64 not supported by this build");
+  cudaStream_t st = current_stream();
+  DevBuf ad(n * d * 8, st), g(d * d * 8, st), ev(d * d * 8 + 8, st), evec(d * d * 8, st),
+      es(4, st), ns(4, st), sc(n * 8, st), off(8, st), rk(4, st), nz(4, st);
+  RTB_CUDA(cudaMemcpyAsync(ad.p, a, n * d * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemsetAsync(nz.p, 0, 4, st));
+  k_any_nonzero<<<(unsigned)ceil_div<uint64_t>(n * d, 256), 256, 0, st>>>(ad.as<double>(),
+                                                                        (long long)(n * d),
+                                                                        nz.as<int>());
+  RTB_LAUNCH_CHECK();
+  int any = 0;
+  RTB_CUDA(cudaMemcpyAsync(&any, nz.p, 4, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  if (!any) {  // zero rows score zero (ref leverage.cpp:40-50)
+    std::memset(out, 0, n * 8);
+    return;
+  }
+  dense_gram(ad.as<double>(), n, d, g.as<double>(), st);
+  const int di = (int)d, np = di + (di & 1);
+  long long zero = 0;
+  RTB_CUDA(cudaMemcpyAsync(ns.p, &di, 4, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(off.p, &zero, 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (2 * 64 * 64 + 2 * 64) * 8));
+  k_sym_eigen<<<1, 128, (2 * np * np + 2 * np) * 8, st>>>(g.as<double>(), ns.as<int>(), di * di,
+                                                          ev.as<double>(), evec.as<double>(),
+                                                          es.as<int>());
+  RTB_LAUNCH_CHECK();
+  FactorSet fs{};
+  fs.order = 1;
+  fs.ptr[0] = ad.as<double>();
+  fs.rows[0] = (int)n;
+  fs.cols[0] = di;
+  k_leverage_rows<<<dim3((unsigned)ceil_div<uint64_t>(n, 128), 1), 128, 0, st>>>(
+      fs, ev.as<double>(), evec.as<double>(), di * di, lambda, sc.as<double>(),
+      off.as<long long>(), rk.as<int>());
+  RTB_LAUNCH_CHECK();
+  int e = 0;
+  RTB_CUDA(cudaMemcpyAsync(out, sc.p, n * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaMemcpyAsync(&e, es.p, 4, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  if (e) throw Error(3, "compact_svd: Jacobi sweeps did not converge");
+}
+
+void dense_solve_ridge(const double* a, uint64_t n, uint64_t d, const double* b, double lambda,
+                       double* x) {
+  if (lambda < 0.0) throw Error(1, "solve_ridge_exact: lambda must be non-negative");
+  if (d == 0) throw Error(1, "compact_svd: empty matrix");
+  cudaStream_t st = current_stream();
+  DevBuf ad(n * d * 8 + 8, st), bd(n * 8 + 8, st), g(d * d * 8, st), atb(d * 8, st),
+      xd(d * 8, st);
+  RTB_CUDA(cudaMemcpyAsync(ad.p, a, n * d * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(bd.p, b, n * 8, cudaMemcpyHostToDevice, st));
+  dense_gram(ad.as<double>(), n, d, g.as<double>(), st);
+  k_add_diag<<<(unsigned)ceil_div<uint64_t>(d, 64), 64, 0, st>>>(g.as<double>(), (int)d, lambda);
+  RTB_LAUNCH_CHECK();
+  k_atb<<<(unsigned)d, 256, 0, st>>>(ad.as<double>(), (long long)n, (int)d, bd.as<double>(),
+                                     atb.as<double>());
+  RTB_LAUNCH_CHECK();
+  int rk = 0, path = 0;
+  solve_sym_device(g.as<double>(), atb.as<double>(), (int)d, xd.as<double>(), &rk, &path, true, st);
+  RTB_CUDA(cudaMemcpyAsync(x, xd.p, d * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+}
+
+// AugmentedSampler tables, sequential like the reference (sampler.cpp:9-40):
+// out[0] = data_mass, out[1] = aug_mass_per_row, out[2] = total_mass, flag on bad input.
+__global__ void k_aug_tables(const double* cand, long long n, int d, double d_eff_lower,
+                             double* norm, double* cum, double* out, int* flag) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double l1 = 0.0;
+  for (long long i = 0; i < n; ++i) {
+    const double s = cand[i];
+    if (!(s >= 0.0) || !isfinite(s)) {
+      *flag = 1;
+      return;
+    }
+    l1 = __dadd_rn(l1, s);
+  }
+  if (l1 <= 0.0) {
+    *flag = 2;
+    return;
+  }
+  const double scale = __ddiv_rn((double)d, l1);
+  double running = 0.0;
+  for (long long i = 0; i < n; ++i) {
+    norm[i] = __dmul_rn(cand[i], scale);
+    running = __dadd_rn(running, norm[i]);
+    cum[i] = running;
+  }
+  const double m = __dadd_rn((double)d, -d_eff_lower);
+  const double aug = m < 1.0 ? m : 1.0;
+  out[0] = running;
+  out[1] = aug;
+  out[2] = __dadd_rn(running, __dmul_rn((double)d, aug));
+}
+
+// one u64 per draw: draw t uses stream output t (sampler.cpp:42-57)
+__global__ void k_aug_draw(const double* norm, const double* cum, long long n, int d,
+                           const double* tab, unsigned long long seed, long long s,
+                           unsigned long long* idx, double* w) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= s) return;
+  const double data_mass = tab[0], aug = tab[1], total = tab[2];
+  const double inv_s = __ddiv_rn(1.0, (double)s);
+  const double u = __dmul_rn(u64_to_unit(sm_at(seed, (uint64_t)t)), total);
+  double prob;
+  unsigned long long index;
+  if (u < data_mass || aug == 0.0) {
+    const double key = u < data_mass ? u : data_mass;
+    long long lo = 0, len = n;
+    while (len > 0) {
+      const long long half = len >> 1;
+      if (!(key < cum[lo + half])) {
+        lo += half + 1;
+        len -= half + 1;
+      } else {
+        len = half;
+      }
+    }
+    long long i = lo >= n ? n - 1 : lo;
+    while (i > 0 && norm[i] == 0.0) --i;
+    index = (unsigned long long)i;
+    prob = __ddiv_rn(norm[i], total);
+  } else {
+    long long k = (long long)__ddiv_rn(__dadd_rn(u, -data_mass), aug);
+    if (k >= d) k = d - 1;
+    index = (unsigned long long)(n + k);
+    prob = __ddiv_rn(aug, total);
+  }
+  idx[t] = index;
+  w[t] = __dsqrt_rn(__ddiv_rn(inv_s, prob));
+}
+
+// sketched normal equations over dense rows (+ sqrt(lambda) e_k rows)
+__global__ void k_dense_sketch_gram(const double* a, long long n, int d, const double* b,
+                                    double rl, const unsigned long long* idx, const double* w,
+                                    long long s, double* G, double* rhs) {
+  __shared__ double red[32];
+  const int e = blockIdx.x;
+  const int p = e / (d + 1), q = e % (d + 1);  // q == d -> rhs entry
+  if (q < d && q < p) return;
+  double acc = 0.0;
+  for (long long t = threadIdx.x; t < s; t += blockDim.x) {
+    const unsigned long long j = idx[t];
+    const double w2 = w[t] * w[t];
+    const double rp = j < (unsigned long long)n ? a[j * d + p] : ((long long)j - n == p ? rl : 0.0);
+    double rq;
+    if (q == d) rq = j < (unsigned long long)n ? b[j] : 0.0;
+    else rq = j < (unsigned long long)n ? a[j * d + q] : ((long long)j - n == q ? rl : 0.0);
+    acc += (w2 * rp) * rq;
+  }
+  acc = block_sum<256>(acc, red);
+  if (threadIdx.x == 0) {
+    if (q == d) {
+      rhs[p] = acc;
+    } else {
+      G[(size_t)p * d + q] = acc;
+      G[(size_t)q * d + p] = acc;
+    }
+  }
+}
+
+void dense_sketched_ridge(const double* a, uint64_t n, uint64_t d, const double* b,
+                          const double* cand, double lambda, double d_eff_lower, double eps,
+                          double delta, uint64_t s_override, uint64_t seed, double* x,
+                          uint64_t* s_out, double* beta_out) {
+  if (d == 0) throw Error(1, "AugmentedSampler: d must be positive");
+  if (d_eff_lower < 0.0 || d_eff_lower > (double)d)
+    throw Error(1, "AugmentedSampler: d_eff_lower outside [0, d]");
+  if (lambda < 0.0) throw Error(1, "solve_sketched_ridge: lambda must be non-negative");
+  std::vector<double> scores(n);
+  if (cand) std::memcpy(scores.data(), cand, n * 8);
+  else dense_ridge_scores(a, n, d, 0.0, scores.data());  // classical_scores
+  cudaStream_t st = current_stream();
+  const double m = std::min(1.0, (double)d - d_eff_lower);
+  const double beta_prime = 1.0 / (1.0 + m);
+  const uint64_t s = s_override ? s_override : sample_count_formula(beta_prime, d, eps, delta);
+  DevBuf ad(n * d * 8 + 8, st), bd(n * 8 + 8, st), sc(n * 8 + 8, st), nm(n * 8 + 8, st),
+      cm(n * 8 + 8, st), tab(32, st), fl(4, st), ix(s * 8, st), ww(s * 8, st), G(d * d * 8, st),
+      r(d * 8, st), xd(d * 8, st);
+  RTB_CUDA(cudaMemcpyAsync(ad.p, a, n * d * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(bd.p, b, n * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(sc.p, scores.data(), n * 8, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemsetAsync(fl.p, 0, 4, st));
+  k_aug_tables<<<1, 1, 0, st>>>(sc.as<double>(), (long long)n, (int)d, d_eff_lower,
+                                nm.as<double>(), cm.as<double>(), tab.as<double>(), fl.as<int>());
+  RTB_LAUNCH_CHECK();
+  int flag = 0;
+  RTB_CUDA(cudaMemcpyAsync(&flag, fl.p, 4, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  if (flag == 1) throw Error(1, "AugmentedSampler: scores must be finite and non-negative");
+  if (flag == 2) throw Error(1, "AugmentedSampler: scores must not all be zero");
+  k_aug_draw<<<(unsigned)ceil_div<uint64_t>(s, 256), 256, 0, st>>>(
+      nm.as<double>(), cm.as<double>(), (long long)n, (int)d, tab.as<double>(), seed,
+      (long long)s, (unsigned long long*)ix.p, ww.as<double>());
+  RTB_LAUNCH_CHECK();
+  k_dense_sketch_gram<<<(unsigned)(d * (d + 1)), 256, 0, st>>>(
+      ad.as<double>(), (long long)n, (int)d, bd.as<double>(), std::sqrt(lambda),
+      (const unsigned long long*)ix.p, ww.as<double>(), (long long)s, G.as<double>(),
+      r.as<double>());
+  RTB_LAUNCH_CHECK();
+  int rk = 0, path = 0;
+  solve_sym_device(G.as<double>(), r.as<double>(), (int)d, xd.as<double>(), &rk, &path, true, st);
+  RTB_CUDA(cudaMemcpyAsync(x, xd.p, d * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  if (s_out) *s_out = s;
+  if (beta_out) *beta_out = beta_prime;
+}
+
+}  // namespace rtb

@@ -1,0 +1,142 @@
+// engine.h -- device-resident sketched Tucker-ALS engine (host C++ side).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace rtb {
+
+// Stream used by the calling thread (default: a library-owned stream per device).
+cudaStream_t current_stream();
+void set_stream(cudaStream_t s);
+
+// Stream-ordered device buffer (cudaMallocAsync from the device pool).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t st = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t b, cudaStream_t s);
+  ~DevBuf();
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+  DevBuf& operator=(DevBuf&& o) noexcept;
+  void ensure(size_t b, cudaStream_t s);
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct AlsOptions {
+  double lambda = 0.001;
+  bool sketched = false;
+  double epsilon = 0.1;
+  double delta = 0.1;
+  uint64_t seed = 0;
+  uint32_t max_iterations = 50;
+  double tolerance = 1e-6;
+  uint64_t sample_override = 0;
+  bool record_history = false;
+  const double* init_core = nullptr;      // host
+  const double* init_factors = nullptr;   // host
+  bool profile = false;                   // per-kernel-family events
+  uint32_t shard_rank = 0, shard_count = 1;
+  void (*allreduce)(double*, uint64_t, void*, void*) = nullptr;
+  void* allreduce_user = nullptr;
+};
+
+struct HistoryRow {
+  uint32_t iteration;
+  std::string step;
+  double loss, rmse;
+};
+struct StepTiming {
+  std::string step;
+  double total = 0.0;
+  uint64_t count = 0;
+};
+struct KernelTiming {
+  std::string name;
+  double total = 0.0;
+  uint64_t launches = 0;
+};
+
+struct AlsOutput {
+  std::vector<uint64_t> shape, ranks;
+  std::vector<double> core;
+  std::vector<double> factors;  // concatenated I_n x R_n
+  double lambda = 0.0;
+  std::vector<HistoryRow> history;
+  std::vector<StepTiming> timings;
+  std::vector<KernelTiming> kernels;
+  uint32_t iterations = 0;
+  double final_loss = 0.0, final_rmse = 0.0;
+  bool converged = false;
+  uint64_t last_sample_count = 0, last_data_draws = 0;
+  int last_rank_deficient = 0, last_solver_path = 0;
+  double sweep_seconds = 0.0;  // device time of the sweep loop
+};
+
+class Engine;  // opaque
+
+// Session: init + initial loss at create; sweeps on demand.
+struct Session {
+  Engine* e = nullptr;
+  ~Session();
+};
+Session* session_create(const double* x_dev, const std::vector<uint64_t>& shape,
+                        const std::vector<uint64_t>& ranks, const AlsOptions& opt);
+// Runs up to n sweeps; honours tolerance when check_tol. Returns sweeps run.
+uint32_t session_run(Session* s, uint32_t n, bool check_tol);
+void session_output(Session* s, AlsOutput& out);
+
+// Whole run with the reference's semantics (ref tucker.cpp:192-276).
+void als_run(const double* x_dev, const std::vector<uint64_t>& shape,
+             const std::vector<uint64_t>& ranks, const AlsOptions& opt, AlsOutput& out);
+
+// ---- single-operation entry points (parity ladder) ----
+void factor_scores(const double* factor_host, int rows, int cols, double* scores, double* cdf,
+                   double* sum, uint64_t* rank);
+void kron_draw(int order, const uint64_t* rows, uint64_t d, const double* scores,
+               const double* cdfs, const double* sums, uint64_t seed, uint64_t s, uint64_t* idx,
+               double* w);
+void kron_normal_eq(int order, const uint64_t* rows, const uint64_t* ranks, const double* factors,
+                    const double* x_host, double lambda, uint64_t s, const uint64_t* idx,
+                    const double* w, double* gram, double* rhs);
+void spd_solve(const double* gram, const double* rhs, uint64_t d, double* x, uint64_t* rank,
+               int* path);
+// Model-level ops on a device tensor with a host model.
+void model_update_core_sketched(const double* x_dev, const std::vector<uint64_t>& shape,
+                                const std::vector<uint64_t>& ranks, const double* core,
+                                const double* factors, double lambda, uint64_t s, uint64_t seed,
+                                double* core_out, uint64_t* idx_out, double* w_out);
+void model_update_factor(const double* x_dev, const std::vector<uint64_t>& shape,
+                         const std::vector<uint64_t>& ranks, const double* core,
+                         const double* factors, double lambda, uint32_t mode, double* out);
+void model_update_core_exact(const double* x_dev, const std::vector<uint64_t>& shape,
+                             const std::vector<uint64_t>& ranks, const double* core,
+                             const double* factors, double lambda, double* core_out);
+void model_loss(const double* x_dev, const std::vector<uint64_t>& shape,
+                const std::vector<uint64_t>& ranks, const double* core, const double* factors,
+                double lambda, double* loss, double* rmse);
+void model_reconstruct(const std::vector<uint64_t>& shape, const std::vector<uint64_t>& ranks,
+                       const double* core, const double* factors, double* out_host);
+// Dense toolkit (ref capi.cpp:299-362).
+void dense_ridge_scores(const double* a, uint64_t n, uint64_t d, double lambda, double* out);
+void dense_solve_ridge(const double* a, uint64_t n, uint64_t d, const double* b, double lambda,
+                       double* x);
+void dense_sketched_ridge(const double* a, uint64_t n, uint64_t d, const double* b,
+                          const double* cand, double lambda, double d_eff_lower, double eps,
+                          double delta, uint64_t s_override, uint64_t seed, double* x,
+                          uint64_t* s_out, double* beta_out);
+
+uint64_t sample_count_formula(double beta_prime, uint64_t d, double eps, double delta);
+
+}  // namespace rtb

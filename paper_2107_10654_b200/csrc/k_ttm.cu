@@ -1,0 +1,378 @@
+// k_ttm.cu -- tensor-times-matrix passes over the resident tensor X.
+//
+// The exact factor update (ref tucker.cpp:70-89) needs
+//   M_n = X_(n) (kron_{m != n} A_m) G_(n)^T = (X x_{m!=n} A_m^T)_(n) G_(n)^T
+// and the loss (ref tucker.cpp:216-229) needs sum (X - Xhat)^2. Both are
+// HBM-streaming passes over X with a skinny FP64 contraction, run on the FP64
+// tensor cores (mma.sync m8n8k4 -> SASS DMMA.8x8x4):
+//
+//  * k_ttm_last<RP,VEC,FUSED>: T[o,:] = X[o,:] A_N (contracts the contiguous
+//    last mode). FUSED also rebuilds Xhat[o,:] = P[o,:] A_N^T in registers
+//    from P = G x_1 A_1 ... x_{N-1} A_{N-1} and accumulates (X - Xhat)^2, so one
+//    read of X serves both the loss and the next sweep's factor updates.
+//  * k_ttm_mid<RP,VEC>: out[o,r,j] = sum_i A[i,r] X[o,i,j] for an inner
+//    (strided) mode, tiled over the contiguous j range.
+//  * k_ttm_generic: scalar fallback for small tensors / odd ranks.
+//  * k_contract_except: M[i,r] = sum_{o,j} Y[o,i,j] G[o,r,j].
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rtb {
+
+namespace {
+constexpr int kBK = 32;     // reduction chunk
+constexpr int kPadX = 4;    // smem row padding (doubles) -> conflict-free frags
+constexpr int kStages = 3;  // cp.async pipeline depth
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Last-mode contraction. X is O x I row-major, A is I x R, T is O x R.
+// Block = 128 threads (4 warps x 16 rows), 64 rows of X per CTA.
+template <int RP, int VEC, bool FUSED>
+__global__ void __launch_bounds__(128) k_ttm_last(const double* __restrict__ X, long long O, int I,
+                                                  const double* __restrict__ A, int R,
+                                                  double* __restrict__ T,
+                                                  const double* __restrict__ P,
+                                                  double* __restrict__ partial) {
+  constexpr int BM = 64;
+  constexpr int LD = kBK + kPadX;
+  extern __shared__ __align__(16) double xs[];  // [kStages][BM][LD]
+  __shared__ double red[32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const long long o0 = (long long)blockIdx.x * BM;
+  const int nchunks = ceil_div(I, kBK);
+
+  auto load_chunk = [&](int c, int stage) {
+    double* dst = xs + stage * BM * LD;
+    const int i0 = c * kBK;
+    constexpr int PER_ROW = kBK / VEC;
+    for (int e = tid; e < BM * PER_ROW; e += 128) {
+      const int r = e / PER_ROW, col = (e % PER_ROW) * VEC;
+      const long long o = o0 + r;
+      const bool ok = (o < O) && (i0 + col < I);
+      const double* src = ok ? X + o * I + i0 + col : X;
+      if (VEC == 2)
+        cp_async16(dst + r * LD + col, src, ok);
+      else
+        cp_async8(dst + r * LD + col, src, ok);
+    }
+  };
+
+  // P fragments (A operand of the Xhat GEMM): rows m-tile, k = rank index.
+  double pf[2][RP / 4];
+  if (FUSED) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int ks = 0; ks < RP / 4; ++ks) {
+        const long long o = o0 + warp * 16 + mt * 8 + g;
+        const int k = ks * 4 + t;
+        pf[mt][ks] = (o < O && k < R) ? P[o * R + k] : 0.0;
+      }
+  }
+  double acc[2][RP / 8][2];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < RP / 8; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  double resid = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nchunks) load_chunk(s, s);
+    cp_async_commit();
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    if (c + kStages - 1 < nchunks) load_chunk(c + kStages - 1, (c + kStages - 1) % kStages);
+    cp_async_commit();
+    const double* xt = xs + (c % kStages) * BM * LD + warp * 16 * LD;
+    const int i0 = c * kBK;
+    // T += X_tile (16 x 32 per warp) * A_chunk (32 x RP)
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      const int i = i0 + ks * 4 + t;
+      double bf[RP / 8];
+#pragma unroll
+      for (int nt = 0; nt < RP / 8; ++nt) {
+        const int r = nt * 8 + g;
+        bf[nt] = (i < I && r < R) ? __ldg(A + (size_t)i * R + r) : 0.0;
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const double af = xt[(mt * 8 + g) * LD + ks * 4 + t];
+#pragma unroll
+        for (int nt = 0; nt < RP / 8; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], af, bf[nt]);
+      }
+    }
+    if (FUSED) {
+      // Xhat_tile (16 x 32) = P_rows (16 x RP) * A_chunk^T (RP x 32); residual.
+#pragma unroll
+      for (int nt = 0; nt < kBK / 8; ++nt) {
+        const int i = i0 + nt * 8 + g;
+        double bf[RP / 4];
+#pragma unroll
+        for (int ks = 0; ks < RP / 4; ++ks) {
+          const int k = ks * 4 + t;
+          bf[ks] = (i < I && k < R) ? __ldg(A + (size_t)i * R + k) : 0.0;
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < RP / 4; ++ks) dmma_8x8x4(c0, c1, pf[mt][ks], bf[ks]);
+          const double2 xv =
+              *reinterpret_cast<const double2*>(xt + (mt * 8 + g) * LD + nt * 8 + 2 * t);
+          const double d0 = xv.x - c0, d1 = xv.y - c1;
+          resid += d0 * d0 + d1 * d1;  // zero-filled tails contribute exactly 0
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  // store T
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const long long o = o0 + warp * 16 + mt * 8 + g;
+    if (o >= O) continue;
+#pragma unroll
+    for (int nt = 0; nt < RP / 8; ++nt) {
+      const int r = nt * 8 + 2 * t;
+      if (r < R) T[o * R + r] = acc[mt][nt][0];
+      if (r + 1 < R) T[o * R + r + 1] = acc[mt][nt][1];
+    }
+  }
+  if (FUSED) {
+    const double s = block_sum<128>(resid, red);
+    if (tid == 0) partial[blockIdx.x] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Strided-mode contraction: X viewed as (O, I, J), out (O, R, J).
+// grid = (ceil(J/64), O); block 128 (4 warps x 16 columns).
+template <int RP, int VEC>
+__global__ void __launch_bounds__(128) k_ttm_mid(const double* __restrict__ X, int O, int I,
+                                                 long long J, const double* __restrict__ A, int R,
+                                                 double* __restrict__ out) {
+  constexpr int BJ = 64;
+  constexpr int LD = BJ + kPadX;
+  extern __shared__ __align__(16) double xs[];  // [kStages][kBK][LD]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const long long j0 = (long long)blockIdx.x * BJ;
+  const long long o = blockIdx.y;
+  const double* Xo = X + o * I * J;
+  const int nchunks = ceil_div(I, kBK);
+
+  auto load_chunk = [&](int c, int stage) {
+    double* dst = xs + stage * kBK * LD;
+    const int i0 = c * kBK;
+    constexpr int PER_ROW = BJ / VEC;
+    for (int e = tid; e < kBK * PER_ROW; e += 128) {
+      const int r = e / PER_ROW, col = (e % PER_ROW) * VEC;
+      const bool ok = (i0 + r < I) && (j0 + col < J);
+      const double* src = ok ? Xo + (long long)(i0 + r) * J + j0 + col : X;
+      if (VEC == 2)
+        cp_async16(dst + r * LD + col, src, ok);
+      else
+        cp_async8(dst + r * LD + col, src, ok);
+    }
+  };
+
+  double acc[RP / 8][2][2];
+#pragma unroll
+  for (int mt = 0; mt < RP / 8; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nchunks) load_chunk(s, s);
+    cp_async_commit();
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    if (c + kStages - 1 < nchunks) load_chunk(c + kStages - 1, (c + kStages - 1) % kStages);
+    cp_async_commit();
+    const double* xt = xs + (c % kStages) * kBK * LD;
+    const int i0 = c * kBK;
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      const int i = i0 + ks * 4 + t;
+      double af[RP / 8];
+#pragma unroll
+      for (int mt = 0; mt < RP / 8; ++mt) {
+        const int r = mt * 8 + g;
+        af[mt] = (i < I && r < R) ? __ldg(A + (size_t)i * R + r) : 0.0;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const double bf = xt[(ks * 4 + t) * LD + warp * 16 + nt * 8 + g];
+#pragma unroll
+        for (int mt = 0; mt < RP / 8; ++mt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf);
+      }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int mt = 0; mt < RP / 8; ++mt) {
+    const int r = mt * 8 + g;
+    if (r >= R) continue;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const long long j = j0 + warp * 16 + nt * 8 + 2 * t;
+      double* dst = out + (o * R + r) * J + j;
+      if (j < J) dst[0] = acc[mt][nt][0];
+      if (j + 1 < J) dst[1] = acc[mt][nt][1];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Scalar fallback: out[o,r,j] = sum_i W[r*wr + i*wi] X[o,i,j].
+__global__ void k_ttm_generic(const double* __restrict__ X, long long O, int I, long long J,
+                              const double* __restrict__ W, long long wr, long long wi, int R,
+                              double* __restrict__ out) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = O * R * J;
+  if (e >= total) return;
+  const long long j = e % J;
+  const int r = (int)((e / J) % R);
+  const long long o = e / (J * R);
+  const double* x = X + o * I * J + j;
+  double s = 0.0;
+  for (int i = 0; i < I; ++i) s += W[r * wr + i * wi] * x[(long long)i * J];
+  out[e] = s;
+}
+
+// M[i,r] = sum_{o,j} Y[o,i,j] G[o,r,j]; Y (O,I,J), G (O,R,J). One thread per (i,r).
+__global__ void k_contract_except(const double* __restrict__ Y, const double* __restrict__ G,
+                                  long long O, int I, int R, long long J, double* __restrict__ M) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)I * R) return;
+  const int i = (int)(e / R), r = (int)(e % R);
+  double s = 0.0;
+  for (long long o = 0; o < O; ++o) {
+    const double* y = Y + (o * I + i) * J;
+    const double* gg = G + (o * R + r) * J;
+    for (long long j = 0; j < J; ++j) s += y[j] * gg[j];
+  }
+  M[e] = s;
+}
+
+// Deterministic sum of per-block partials (fixed order), one block.
+__global__ void k_sum_partials(const double* __restrict__ partial, long long n,
+                               double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
+  s = block_sum<1024>(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers.
+
+template <int RP, int VEC, bool FUSED>
+static void launch_last(const double* X, long long O, int I, const double* A, int R, double* T,
+                        const double* P, double* partial, cudaStream_t st) {
+  constexpr int smem = kStages * 64 * (kBK + kPadX) * sizeof(double);
+  auto k = k_ttm_last<RP, VEC, FUSED>;
+  static bool attr = false;
+  if (!attr) {
+    RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const long long blocks = ceil_div<long long>(O, 64);
+  k<<<(unsigned)blocks, 128, smem, st>>>(X, O, I, A, R, T, P, partial);
+  RTB_LAUNCH_CHECK();
+}
+
+long long ttm_last_blocks(long long O) { return ceil_div<long long>(O, 64); }
+
+void ttm_last(const double* X, long long O, int I, const double* A, int R, double* T,
+              const double* P, double* partial, cudaStream_t st) {
+  const bool fused = P != nullptr;
+  const bool v2 = (I % 2) == 0;
+  const int rp = R <= 8 ? 8 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
+  if (R > 32) throw Error(4, "ttm_last: rank > 32 not supported by the DMMA path");
+#define RTB_L(RPV)                                                                       \
+  case RPV:                                                                              \
+    if (fused) {                                                                         \
+      if (v2) launch_last<RPV, 2, true>(X, O, I, A, R, T, P, partial, st);               \
+      else launch_last<RPV, 1, true>(X, O, I, A, R, T, P, partial, st);                  \
+    } else {                                                                             \
+      if (v2) launch_last<RPV, 2, false>(X, O, I, A, R, T, P, partial, st);              \
+      else launch_last<RPV, 1, false>(X, O, I, A, R, T, P, partial, st);                 \
+    }                                                                                    \
+    break;
+  switch (rp) {
+    RTB_L(8)
+    RTB_L(16)
+    RTB_L(24)
+    RTB_L(32)
+  }
+#undef RTB_L
+}
+
+template <int RP, int VEC>
+static void launch_mid(const double* X, int O, int I, long long J, const double* A, int R,
+                       double* out, cudaStream_t st) {
+  constexpr int smem = kStages * kBK * (64 + kPadX) * sizeof(double);
+  auto k = k_ttm_mid<RP, VEC>;
+  static bool attr = false;
+  if (!attr) {
+    RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)ceil_div<long long>(J, 64), (unsigned)O);
+  k<<<grid, 128, smem, st>>>(X, O, I, J, A, R, out);
+  RTB_LAUNCH_CHECK();
+}
+
+void ttm_mid(const double* X, int O, int I, long long J, const double* A, int R, double* out,
+             cudaStream_t st) {
+  const bool v2 = (J % 2) == 0;
+  const int rp = R <= 8 ? 8 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
+  if (R > 32) throw Error(4, "ttm_mid: rank > 32 not supported by the DMMA path");
+#define RTB_M(RPV)                                        \
+  case RPV:                                               \
+    if (v2) launch_mid<RPV, 2>(X, O, I, J, A, R, out, st); \
+    else launch_mid<RPV, 1>(X, O, I, J, A, R, out, st);    \
+    break;
+  switch (rp) {
+    RTB_M(8)
+    RTB_M(16)
+    RTB_M(24)
+    RTB_M(32)
+  }
+#undef RTB_M
+}
+
+void ttm_generic(const double* X, long long O, int I, long long J, const double* W, long long wr,
+                 long long wi, int R, double* out, cudaStream_t st) {
+  const long long total = O * R * J;
+  if (total == 0) return;
+  k_ttm_generic<<<(unsigned)ceil_div<long long>(total, 256), 256, 0, st>>>(X, O, I, J, W, wr, wi,
+                                                                          R, out);
+  RTB_LAUNCH_CHECK();
+}
+
+void contract_except(const double* Y, const double* G, long long O, int I, int R, long long J,
+                     double* M, cudaStream_t st) {
+  const long long total = (long long)I * R;
+  k_contract_except<<<(unsigned)ceil_div<long long>(total, 128), 128, 0, st>>>(Y, G, O, I, R, J,
+                                                                              M);
+  RTB_LAUNCH_CHECK();
+}
+
+void sum_partials(const double* partial, long long n, double* out, cudaStream_t st) {
+  k_sum_partials<<<1, 1024, 0, st>>>(partial, n, out);
+  RTB_LAUNCH_CHECK();
+}
+
+}  // namespace rtb

@@ -1,0 +1,91 @@
+// kernels.h -- host-side launchers of the sm_100a kernels (namespace rtb).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rtb {
+
+// Factor matrices of one model, passed by value to kernels.
+struct FactorSet {
+  const double* ptr[8];
+  int rows[8];
+  int cols[8];
+  int order;
+};
+
+// ---- k_small.cu ----
+__global__ void k_factor_gram(const FactorSet fs, double* grams, int r_max);
+__global__ void k_sym_eigen(const double* in, const int* ns, int stride, double* evals,
+                            double* evecs, int* status);
+__global__ void k_leverage_rows(const FactorSet fs, const double* evals, const double* evecs,
+                                int stride, double lambda, double* scores,
+                                const long long* score_off, int* ranks);
+__global__ void k_score_cdf(const double* scores, const long long* off, const int* rows,
+                            int order, double* cdf, double* sums);
+__global__ void k_sym_pinv(const double* evals, const double* evecs, const int* ns, int stride,
+                           double* out, int* ranks);
+__global__ void k_rows_times_small(const double* M, const double* P, int I, int R, double* out);
+
+// ---- k_ttm.cu ----
+long long ttm_last_blocks(long long O);
+// T (O x R) = X (O x I) A (I x R); if P != null also partial[block] = sum (X - P A^T)^2
+void ttm_last(const double* X, long long O, int I, const double* A, int R, double* T,
+              const double* P, double* partial, cudaStream_t st);
+// out[o,r,j] = sum_i A[i,r] X[o,i,j]
+void ttm_mid(const double* X, int O, int I, long long J, const double* A, int R, double* out,
+             cudaStream_t st);
+// out[o,r,j] = sum_i W[r*wr + i*wi] X[o,i,j]
+void ttm_generic(const double* X, long long O, int I, long long J, const double* W, long long wr,
+                 long long wi, int R, double* out, cudaStream_t st);
+// M[i,r] = sum_{o,j} Y[o,i,j] G[o,r,j]
+void contract_except(const double* Y, const double* G, long long O, int I, int R, long long J,
+                     double* M, cudaStream_t st);
+void sum_partials(const double* partial, long long n, double* out, cudaStream_t st);
+
+// ---- k_draw.cu ----
+struct DrawSpec {
+  int order;
+  long long rows[8];        // I_n
+  long long cdf_off[8];     // offset of mode n in the concatenated score/CDF arrays
+  unsigned long long total_rows;  // prod I_n
+  unsigned long long d;     // prod R_n (augmented block size)
+  unsigned long long seed;
+  unsigned long long s;     // number of draws
+};
+struct DrawWork {          // device scratch, sized by draw_work_bytes
+  void* base;
+  size_t bytes;
+};
+size_t draw_work_bytes(const DrawSpec& spec);
+// Decodes the sequential SplitMix64 draw stream in parallel and evaluates all
+// s draws: indices (u64, reference format) and weights.
+void draw_sketch(const DrawSpec& spec, const double* scores, const double* cdfs,
+                 const double* sums, DrawWork work, unsigned long long* idx_out,
+                 double* w_out, int* flag_dev, cudaStream_t st);
+
+// ---- k_gram.cu ----
+struct GramSpec {
+  int order;
+  int rows[8];
+  int ranks[8];
+  const double* factors[8];
+  unsigned long long total_rows;
+  int d;          // prod R_n
+  int dprime;     // prod_{n>=1} R_n (z width)
+  double lambda;
+  unsigned long long s;
+};
+size_t gram_work_bytes(const GramSpec& spec);
+// Sketched normal equations from (idx, w): full d x d Gram + rhs.
+void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long long* idx,
+                      const double* w, void* work, size_t work_bytes, double* gram,
+                      double* rhs, unsigned long long* data_draws_dev, cudaStream_t st);
+
+// ---- k_chol.cu ----
+size_t chol_work_bytes(int d);
+// In-place Cholesky of the lower triangle of a (d x d, row-major) and solve
+// a x = b (x overwrites b). *status_dev = 0 ok, k+1 = non-positive pivot at k.
+void chol_solve(double* a, int d, double* b, int* status_dev, void* work, cudaStream_t st);
+
+}  // namespace rtb

@@ -1,0 +1,252 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle.
+
+Parity ladder of SURVEY.md 8(c):
+  rung 1  sampled indices bit-exact given the same CDFs and seed
+  rung 2  per-mode leverage scores within 1e-9 (relative to max score)
+  rung 3  Gram/RHS from the same RowSketch within 1e-9 (normalised entries)
+  rung 4  solve of the same Gram within c * kappa * eps
+  rung 5  end to end (factors, core, loss) within a small multiple of the
+          reference's own noise floor (reordered sums move it by ~kappa*eps)
+The oracle (oracle/rtucker_oracle.c) is bit-identical to the compiled
+reference (tests/test_oracle_pin.py).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+EPS = np.finfo(np.float64).eps
+
+
+def planted(shape, ranks, noise=0.01, seed=0):
+    """BASELINE-style input: N(0,1) core/factors, dense noise at noise*||X||/sqrt(N)."""
+    rng = np.random.default_rng(seed)
+    core = rng.standard_normal(ranks)
+    factors = [rng.standard_normal((i, r)) for i, r in zip(shape, ranks)]
+    x = core
+    for n, f in enumerate(factors):
+        x = np.moveaxis(np.tensordot(f, x, axes=(1, n)), 0, n)
+    sigma = noise * np.linalg.norm(x) / np.sqrt(x.size)
+    return x + sigma * rng.standard_normal(x.shape)
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def random_model(oracle, shape, ranks, seed):
+    core, factors = oracle.random_model(shape, ranks, seed)
+    return core.reshape(ranks), factors
+
+
+# ---------------------------------------------------------------- rung 2
+@pytest.mark.parametrize("rows,cols,kind", [(100, 5, "uniform"), (512, 16, "normal"),
+                                            (160, 10, "pareto"), (7, 7, "normal"),
+                                            (33, 1, "uniform")])
+def test_factor_scores(oracle, rt, rows, cols, kind):
+    rng = np.random.default_rng(rows * 31 + cols)
+    if kind == "uniform":
+        f = rng.random((rows, cols))
+    elif kind == "normal":
+        f = rng.standard_normal((rows, cols))
+    else:
+        f = rng.standard_normal((rows, cols)) * (rng.pareto(1.5, rows) + 1.0)[:, None]
+    sc, cdf, tot, rank = rt.factor_scores(f)
+    osc, ocdf, otot, orank = oracle.factor_scores(f)
+    assert rank == orank
+    assert rel(sc, osc) < 1e-9
+    assert rel(cdf, ocdf) < 1e-9
+    assert abs(tot - otot) / otot < 1e-9
+
+
+def test_factor_scores_zero_factor(rt):
+    sc, cdf, tot, rank = rt.factor_scores(np.zeros((9, 3)))
+    assert rank == 0 and tot == 0.0 and not sc.any()
+
+
+# ---------------------------------------------------------------- rung 1
+@pytest.mark.parametrize("shape,ranks,s,seed", [((100, 100, 100), (5, 5, 5), 20000, 7),
+                                                 ((30, 20, 10, 8), (3, 2, 4, 2), 5000, 11),
+                                                 ((64,), (5,), 3000, 3),
+                                                 ((40, 50), (4, 6), 7777, 99)])
+def test_draws_bit_exact_given_reference_cdfs(oracle, rt, shape, ranks, s, seed):
+    rng = np.random.default_rng(seed)
+    fs = [rng.random((i, r)) for i, r in zip(shape, ranks)]
+    scs, cdfs, sums = [], [], []
+    for f in fs:
+        sc, cdf, tot, _ = oracle.factor_scores(f)
+        scs.append(sc)
+        cdfs.append(cdf)
+        sums.append(tot)
+    d = int(np.prod(ranks))
+    oidx, ow, _ = oracle.kron_draw(shape, d, scs, cdfs, sums, seed, s)
+    gidx, gw = rt.kron_draw(shape, d, scs, cdfs, sums, seed, s)
+    assert np.array_equal(oidx, gidx)
+    assert np.array_equal(ow, gw)  # same IEEE ops -> bitwise weights
+
+
+# ---------------------------------------------------------------- rung 3
+@pytest.mark.parametrize("shape,ranks,lam,s", [((30, 25, 20), (4, 3, 5), 1e-3, 4000),
+                                                ((20, 18, 16, 12), (3, 2, 2, 3), 0.1, 3000),
+                                                ((50, 40), (6, 5), 1e-2, 2000),
+                                                ((70,), (9,), 1e-2, 500)])
+def test_normal_equations_from_reference_sketch(oracle, rt, shape, ranks, lam, s):
+    x = planted(shape, ranks, seed=3)
+    core, factors = random_model(oracle, shape, ranks, 5)
+    _, idx, w, _ = oracle.update_core_fast(shape, ranks, core, factors, lam, x, s, 1234)
+    og, orhs = oracle.kron_normal_eq(shape, ranks, factors, x, lam, idx, w)
+    gg, grhs = rt.kron_normal_eq(shape, ranks, factors, x, lam, idx, w)
+    dg = np.sqrt(np.outer(np.diag(og), np.diag(og)))
+    assert np.max(np.abs(gg - og) / dg) < 1e-9
+    assert np.linalg.norm(grhs - orhs) / np.linalg.norm(orhs) < 1e-9
+
+
+# ---------------------------------------------------------------- rung 4
+@pytest.mark.parametrize("d", [8, 64, 125, 200])
+def test_spd_solve_on_reference_gram(oracle, rt, d):
+    rng = np.random.default_rng(d)
+    a = rng.standard_normal((3 * d, d))
+    g = a.T @ a + 1e-3 * np.eye(d)
+    b = rng.standard_normal(d)
+    ox, orank = oracle.pinv_solve(g, b)
+    gx, grank, path = rt.spd_solve(g, b)
+    kappa = np.linalg.cond(g)
+    assert grank == orank == d
+    assert np.linalg.norm(gx - ox) / np.linalg.norm(ox) < 100 * kappa * EPS
+
+
+def test_spd_solve_rank_deficient_small(oracle, rt):
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((20, 3))
+    g = np.zeros((6, 6))
+    g[:3, :3] = a.T @ a  # rank 3 PSD
+    b = rng.standard_normal(6)
+    ox, orank = oracle.pinv_solve(g, b)
+    gx, grank, path = rt.spd_solve(g, b)
+    assert path == 1 and grank == orank == 3
+    assert np.linalg.norm(gx - ox) / np.linalg.norm(ox) < 1e-9
+
+
+# ---------------------------------------------------------------- model steps
+CASES = [((12, 10, 8), (3, 2, 4), 0.01), ((30, 30, 30), (4, 4, 4), 1e-3),
+         ((9, 8, 7, 6), (2, 3, 2, 2), 0.05), ((40, 35), (5, 4), 1e-2), ((50,), (4,), 1e-2)]
+
+
+@pytest.mark.parametrize("shape,ranks,lam", CASES)
+def test_update_factor(oracle, rt, shape, ranks, lam):
+    x = planted(shape, ranks, seed=1)
+    core, factors = random_model(oracle, shape, ranks, 2)
+    xt = rt.Tensor.from_numpy(x)
+    m = rt.Model(core, factors, lam)
+    for mode in range(1, len(shape) + 1):
+        g = rt.update_factor(xt, m, mode)
+        o = oracle.update_factor(shape, ranks, core, factors, lam, x, mode)
+        assert rel(g, o) < 1e-8, mode
+
+
+@pytest.mark.parametrize("shape,ranks,lam", CASES)
+def test_update_core_exact(oracle, rt, shape, ranks, lam):
+    x = planted(shape, ranks, seed=4)
+    core, factors = random_model(oracle, shape, ranks, 6)
+    g = rt.update_core_exact(rt.Tensor.from_numpy(x), rt.Model(core, factors, lam))
+    o = oracle.update_core_exact(shape, ranks, core, factors, lam, x)
+    assert rel(g, o) < 1e-7
+
+
+@pytest.mark.parametrize("shape,ranks,lam", CASES)
+def test_loss(oracle, rt, shape, ranks, lam):
+    x = planted(shape, ranks, seed=8)
+    core, factors = random_model(oracle, shape, ranks, 9)
+    gl, gr = rt.loss(rt.Tensor.from_numpy(x), rt.Model(core, factors, lam))
+    ol, orr = oracle.tucker_loss(shape, ranks, core, factors, lam, x)
+    assert abs(gl - ol) / ol < 1e-12
+    assert abs(gr - orr) / orr < 1e-12
+
+
+@pytest.mark.parametrize("shape,ranks,lam,s", [((30, 30, 30), (4, 4, 4), 1e-3, 6000),
+                                                ((12, 10, 8), (3, 2, 4), 0.01, 3000),
+                                                ((9, 8, 7, 6), (2, 3, 2, 2), 0.05, 2000)])
+def test_update_core_sketched(oracle, rt, shape, ranks, lam, s):
+    x = planted(shape, ranks, seed=10)
+    core, factors = random_model(oracle, shape, ranks, 12)
+    gcore, gidx, gw = rt.update_core_sketched(rt.Tensor.from_numpy(x),
+                                              rt.Model(core, factors, lam), s, 777)
+    ocore, oidx, ow, _ = oracle.update_core_fast(shape, ranks, core, factors, lam, x, s, 777)
+    assert np.array_equal(gidx, oidx)      # no index flips from the score route
+    assert rel(gw, ow) < 1e-12
+    og, _ = oracle.kron_normal_eq(shape, ranks, factors, x, lam, oidx, ow)
+    kappa = np.linalg.cond(og)
+    assert rel(gcore, ocore) < max(1e-9, 1e3 * kappa * EPS)
+
+
+def test_zero_factor_gives_zero_core(oracle, rt):
+    shape, ranks = (4, 3, 2), (2, 2, 2)
+    x = planted(shape, ranks, seed=2)
+    core, factors = random_model(oracle, shape, ranks, 3)
+    factors[1] = np.zeros_like(factors[1])
+    g, _, _ = rt.update_core_sketched(rt.Tensor.from_numpy(x), rt.Model(core, factors, 0.3), 50, 1)
+    assert not g.any()
+    g = rt.update_core_exact(rt.Tensor.from_numpy(x), rt.Model(core, factors, 0.3))
+    assert not g.any()
+
+
+# ---------------------------------------------------------------- end to end
+@pytest.mark.parametrize("shape,ranks,lam,s,sweeps,tol", [
+    ((40, 40, 40), (5, 5, 5), 1e-3, 20000, 5, 1e-5),
+    ((20, 18, 16), (3, 3, 3), 1e-2, 5000, 4, 1e-6),
+    ((10, 9, 8, 7), (2, 2, 2, 2), 0.05, 3000, 3, 1e-6),
+])
+def test_als_sketched_end_to_end(oracle, rt, shape, ranks, lam, s, sweeps, tol):
+    x = planted(shape, ranks, seed=21)
+    o = oracle.als(x, ranks, lam=lam, sketched_core=1, max_iterations=sweeps, tolerance=0.0,
+                   sample_count_override=s, record_history=1, seed=3)
+    r = rt.als_run(rt.Tensor.from_numpy(x), ranks,
+                   rt.options(lam=lam, sketched_core=1, max_iterations=sweeps, tolerance=0.0,
+                              sample_count_override=s, record_history=1, seed=3))
+    gh = r.history()
+    assert [(h[0], h[1]) for h in gh] == [(h[0], h[1]) for h in o["history"]]
+    for (gi, gs, gl, grm), (oi, os_, ol, orm) in zip(gh, o["history"]):
+        assert abs(gl - ol) / ol < tol, (gi, gs)
+    m = r.model()
+    xg = oracle.reconstruct(shape, ranks, m.core, m.factors)
+    xo = oracle.reconstruct(shape, ranks, o["core"], o["factors"])
+    assert np.linalg.norm(xg - xo) / np.linalg.norm(xo) < tol * 10
+
+
+def test_als_exact_end_to_end(oracle, rt):
+    shape, ranks = (15, 14, 13), (3, 3, 3)
+    x = planted(shape, ranks, seed=5)
+    o = oracle.als(x, ranks, lam=0.01, max_iterations=6, tolerance=0.0, seed=4)
+    r = rt.als_run(rt.Tensor.from_numpy(x), ranks,
+                   rt.options(lam=0.01, max_iterations=6, tolerance=0.0, seed=4))
+    assert r.iterations == 6
+    assert abs(r.final_loss - o["final_loss"]) / o["final_loss"] < 1e-9
+
+
+def test_als_tolerance_stops_like_reference(oracle, rt):
+    shape, ranks = (12, 11, 10), (2, 2, 2)
+    x = planted(shape, ranks, seed=6)
+    o = oracle.als(x, ranks, lam=0.02, max_iterations=50, tolerance=1e-4, seed=1)
+    r = rt.als_run(rt.Tensor.from_numpy(x), ranks,
+                   rt.options(lam=0.02, max_iterations=50, tolerance=1e-4, seed=1))
+    assert r.iterations == o["iterations"]
+
+
+def test_history_and_timings_shape(rt):
+    x = planted((6, 5, 4), (2, 2, 2), seed=1)
+    r = rt.als_run(rt.Tensor.from_numpy(x), (2, 2, 2),
+                   rt.options(max_iterations=3, record_history=1, tolerance=0.0))
+    assert r.iterations == 3
+    h = r.history()
+    assert len(h) == 12 and h[0][:2] == (1, "F1") and h[3][1] == "Core"
+    t = r.timings()
+    assert [row[0] for row in t] == ["F1", "F2", "F3", "Core"]
+    assert all(row[2] == 3 for row in t)
+
+
+def test_rejects_bad_ranks(rt):
+    x = rt.Tensor.from_numpy(np.ones((4, 4)))
+    with pytest.raises(rt.RtuckerError) as e:
+        rt.als_run(x, (5, 2))
+    assert e.value.code == rt.ERR_INVALID_ARGUMENT

@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""bench.py -- sketched Tucker-ALS sweeps/s on B200 (BASELINE.json configs[1], "C2").
+
+Workload (one "step" = one ALS sweep over a device-resident tensor):
+  X = 512^3 FP64 (1.07 GB, larger than the 126 MB L2), planted rank (16,16,16)
+  with N(0,1) core/factors plus dense Gaussian noise at 1% of ||X||/sqrt(N),
+  Tucker rank (16,16,16), lambda = 1e-2, 200,000 sketch rows for the core
+  update (d = 4096), exact factor updates (the reference's semantics,
+  ref tucker.cpp:241-248; the reference has no sketched factor update),
+  reference uniform init (ref tucker.cpp:168-190). Synthetic data, seed 0.
+
+Arms:
+  default            our librtucker_b200.so (hand-written sm_100a kernels)
+  --impl reference   the reference's own CPU code (oracle/_ref, compiled from
+                     /root/reference/proj sources), single-threaded, timed on
+                     bounded samples of each sweep phase and extrapolated.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPE = (512, 512, 512)
+RANKS = (16, 16, 16)
+LAM = 1e-2
+S_CORE = 200_000
+NOISE = 0.01
+E2E_SWEEPS = 10  # the C2 protocol
+METRIC = "sketched Tucker-ALS sweeps/s"
+WORKLOAD = ("C2: dense 3-way FP64 512^3 (1.07 GB), planted rank (16,16,16) N(0,1) + 1% "
+            "noise; Tucker rank (16,16,16), lambda=1e-2, 200,000 sampled rows for the core "
+            "update (d=4096); exact factor updates (reference semantics)")
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm (oracle/_ref = the reference compiled from its sources)
+
+def reference_sweep_estimate(ref, np, x_full, core, factors, slab=64, gram_samples=100,
+                             svd_dim=256, seed=12345):
+    """One bounded sample of every phase of a C2 sweep, timed with the
+    reference's own routines (oracle/ref_harness.cpp), extrapolated to C2.
+    Returns (seconds per sweep, detail dict)."""
+    # update_factor(mode) and the loss are linear in prod(I_n) when the tensor is
+    # cut along a mode other than the updated one (the Kronecker of the other
+    # factors shrinks with the slab); mode 1 is timed on a mode-3 slab, modes 2
+    # and 3 and the loss on a mode-1 slab.
+    t_factor = 0.0
+    t_loss = 0.0
+    xa = x_full[:slab]
+    fa = [factors[0][:slab], factors[1], factors[2]]
+    xc = np.ascontiguousarray(x_full[:, :, :slab])
+    fc = [factors[0], factors[1], factors[2][:slab]]
+    for mode in (1, 2, 3):
+        if mode == 1:
+            shp, xs, fs = (SHAPE[0], SHAPE[1], slab), xc, fc
+        else:
+            shp, xs, fs = (slab, SHAPE[1], SHAPE[2]), xa, fa
+        out = ref.time_sweep_phases(shp, RANKS, core, fs, LAM, xs, 16, seed, mode,
+                                    gram_samples=0, svd_dim=0, do_factor=True,
+                                    do_loss=(mode == 2))
+        t_factor += out[0]
+        t_loss += out[1]
+    scale = SHAPE[0] / slab
+    out = ref.time_sweep_phases(SHAPE, RANKS, core, factors, LAM, x_full, S_CORE, seed, 1,
+                                gram_samples=gram_samples, svd_dim=svd_dim, do_factor=False,
+                                do_loss=False)
+    t_gram_sample, t_setup, t_svd, n_data = out[2], out[3], out[4], out[5]
+    d = int(np.prod(RANKS))
+    t_svd_full = t_svd * (d / svd_dim) ** 3  # d^3 (the measured growth is steeper)
+    total = scale * (t_factor + t_loss) + t_setup + n_data * t_gram_sample + t_svd_full
+    detail = {"factor_updates_s": scale * t_factor, "loss_s": scale * t_loss,
+              "kron_setup_s": t_setup, "gram_stream_s": n_data * t_gram_sample,
+              "gram_s_per_data_row": t_gram_sample, "data_rows": int(n_data),
+              "svd_solve_s_extrapolated": t_svd_full, "svd_measured_dim": svd_dim,
+              "svd_measured_s": t_svd}
+    return total, detail
+
+
+def reference_inputs(np):
+    from oracle.oracle import Reference
+    ref = Reference()
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal(SHAPE)
+    core, factors = ref.random_model(SHAPE, RANKS, 0)
+    return ref, x, core, factors
+
+
+REF_SAMPLE = ("per sweep phase, the reference's own routines on bounded samples: "
+              "update_factor (3 modes) and the loss on 64-wide slabs cut along a mode other "
+              "than the updated one (x8, linear in prod I_n), the Gram/RHS stream on 100 real C2 data rows (x s_data), "
+              "ImplicitKronecker setup at C2, Jacobi compact_svd of a 256^2 SPD Gram (x(4096/256)^3)")
+
+
+def run_reference_arm(args):
+    import numpy as np
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    ref, x, core, factors = reference_inputs(np)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        t, detail = reference_sweep_estimate(ref, np, x, core, factors)
+        if i >= args.warmup:
+            vals.append(t)
+    sec = statistics.mean(vals)
+    value = 1.0 / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "sweeps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample": REF_SAMPLE},
+        "cpu_baseline": {"value": value, "unit": "sweeps/s", "cores": 1, "kind": "reference",
+                         "sample": REF_SAMPLE, "phases": detail},
+        "e2e": {"value": value, "unit": "sweeps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [v.strip() for v in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def make_input(torch, device, seed=0):
+    g = torch.Generator(device=device).manual_seed(seed)
+    core = torch.randn(RANKS, dtype=torch.float64, device=device, generator=g)
+    x = core
+    for n, I in enumerate(SHAPE):
+        f = torch.randn(I, RANKS[n], dtype=torch.float64, device=device, generator=g)
+        x = torch.movedim(torch.tensordot(f, x, dims=([1], [n])), 0, n)
+    sigma = NOISE * x.norm() / x.numel() ** 0.5
+    x = x + sigma * torch.randn(x.shape, dtype=torch.float64, device=device, generator=g)
+    return x.contiguous()
+
+
+def kernel_work(family, n_data, n_buckets):
+    """Algorithmic work per launch of a kernel family."""
+    d = 1
+    for r in RANKS:
+        d *= r
+    total = SHAPE[0] * SHAPE[1] * SHAPE[2]
+    if family == "chol":
+        return "tensor", "TFLOP/s", d ** 3 / 3 + 2 * d * d
+    if family == "gram":
+        dp = d // RANKS[0]
+        tiles = -(-dp // 64)
+        tp = tiles * (tiles + 1) // 2
+        npair = RANKS[0] * (RANKS[0] + 1) // 2
+        return "tensor", "TFLOP/s", 2.0 * (n_data * tp * 4096 + n_buckets * npair * tp * 4096)
+    if family in ("ttm_last_loss", "ttm_last", "ttm_mid"):
+        return "hbm", "GB/s", 8.0 * total
+    return None, None, None
+
+
+def run_our_arm(args):
+    import numpy as np
+    import torch
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2107_10654_b200 import rtucker as rt
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    rt.set_stream(stream.cuda_stream)
+
+    x = make_input(torch, dev)
+    torch.cuda.synchronize()
+    t = rt.Tensor.from_device(x.data_ptr(), SHAPE)
+    torch.cuda.synchronize()
+    xh = None
+    if rank == 0 or True:
+        xh = torch.empty(SHAPE, dtype=torch.float64, pin_memory=True)
+        xh.copy_(x)
+    del x
+    torch.cuda.empty_cache()
+
+    opts = rt.options(lam=LAM, sketched_core=1, sample_count_override=S_CORE, tolerance=0.0,
+                      max_iterations=args.warmup + args.steps, seed=0)
+    sess = rt.Session(t, RANKS, opts, profile=True)
+    sess.sweeps(args.warmup)
+    torch.cuda.synchronize()
+    k0 = {k[0]: k for k in sess.result().kernels()}
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = rt.lib.rtucker_b200_launch_count()
+    clocks = Clocks(local)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sess.sweeps(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = rt.lib.rtucker_b200_launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    if dist:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    res = sess.result()
+    info = res.sketch_info()
+    k1 = res.kernels()
+    fam = {}
+    for name, secs, n in k1:
+        p = k0.get(name, (name, 0.0, 0))
+        fam[name] = (secs - p[1], n - p[2])
+    hist = res.history()
+    sess.free()
+
+    # roofline of the dominant kernel family
+    dom = max(fam, key=lambda k: fam[k][0])
+    n_data = info["data_draws"]
+    n_buckets = SHAPE[0]
+    bound, unit, work = kernel_work(dom, n_data, n_buckets)
+    peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+    mp = {}
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    roofline = None
+    if bound:
+        secs, n = fam[dom]
+        per_launch = secs / max(n, 1)
+        if bound == "tensor":
+            achieved = work / per_launch / 1e12
+            peak = peaks["dmma_m8n8k4_tflops"]
+            peak_src = "measured FP64 DMMA.8x8x4 microbench (profiles/fp64_peak.json)"
+        else:
+            achieved = work / per_launch / 1e9
+            peak = mp.get("hbm_gbs", 6553.3)
+            peak_src = "MEASURED_PEAKS.json hbm_gbs"
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "r01_traffic.json")
+        if os.path.exists(tf):
+            traffic = json.load(open(tf)).get(dom)
+        roofline = {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak,
+                    "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                    "peak_source": peak_src, "work_per_launch": work,
+                    "launch_ms": per_launch * 1e3, "launches": n}
+
+    # e2e through the public C API with host buffers (rank 0 timing, max over ranks)
+    e2e_vals = []
+    xnp = xh.numpy()
+    rt.set_stream(stream.cuda_stream)
+    for i in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        th = rt.Tensor.from_numpy(xnp)  # host -> library (rtucker_tensor_create)
+        r = rt.als_run(th, RANKS, rt.options(lam=LAM, sketched_core=1,
+                                             sample_count_override=S_CORE, tolerance=0.0,
+                                             max_iterations=E2E_SWEEPS, seed=0))
+        m = r.model()  # device -> host result
+        fl = r.final_loss
+        t1 = time.perf_counter()
+        r.free()
+        th.free()
+        if i > 0:
+            e2e_vals.append(t1 - t0)
+    e2e_s = statistics.mean(e2e_vals)
+    if dist:
+        tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    d2h = (m.core.size + sum(f.size for f in m.factors)) * 8 + 8
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            ref, xr, core, factors = reference_inputs(np)
+            sec, detail = reference_sweep_estimate(ref, np, xr, core, factors)
+            cpu = {"value": 1.0 / sec, "unit": "sweeps/s", "cores": 1, "kind": "reference",
+                   "sample": REF_SAMPLE, "host_cores": os.cpu_count(), "phases": detail}
+        except Exception as e:  # oracle/_ref missing on this box
+            cpu = {"value": None, "unit": "sweeps/s", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        sweeps_per_s = world * args.steps / (ms / 1e3)
+        line = {
+            "metric": METRIC, "value": sweeps_per_s, "unit": "sweeps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded torch N(0,1) planted model + 1% noise)",
+            "config": {"workload": WORKLOAD, "shape": list(SHAPE), "ranks": list(RANKS),
+                       "lambda": LAM, "s_core": S_CORE, "factor_updates": "exact",
+                       "l2": "inputs larger than L2 (X = 1.07 GB > 126 MB)",
+                       "step": "one ALS sweep (3 factor updates + sketched core + loss)",
+                       "parallelism": ("replicas" if world > 1 else "single GPU"),
+                       "final_loss": hist[-1][2] if hist else None},
+            "clocks": clk,
+            "e2e": {"value": world * E2E_SWEEPS / e2e_s, "unit": "sweeps/s",
+                    "h2d_bytes_per_step": int(xnp.nbytes), "d2h_bytes_per_step": int(d2h),
+                    "step": "one job: rtucker_tensor_create(host X) + rtucker_als_run(10 sweeps)"
+                            " + rtucker_result_model", "seconds_per_job": e2e_s},
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "kernels_ms_per_sweep": {k: v[0] * 1e3 / args.steps for k, v in fam.items()},
+            "sketch": info,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_our_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -28,6 +28,8 @@ rtucker_status rtucker_b200_set_device(int device);
 /* CUDA stream (cudaStream_t) for this thread's work; NULL restores the
  * library-owned stream. Lets a caller time the library with its own events. */
 rtucker_status rtucker_b200_set_stream(void* stream);
+/* Number of this library's kernel launches so far in the process. */
+unsigned long long rtucker_b200_launch_count(void);
 
 /* Wrap a tensor that already lives in device memory of the current device.
  * The data is copied (device to device); rtucker_tensor_data() returns NULL

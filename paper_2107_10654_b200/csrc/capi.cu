@@ -644,6 +644,8 @@ rtucker_status rtucker_b200_set_device(int device) {
   return guarded([&] { RTB_CUDA(cudaSetDevice(device)); });
 }
 
+unsigned long long rtucker_b200_launch_count(void) { return rtb::launch_counter(); }
+
 rtucker_status rtucker_b200_set_stream(void* stream) {
   rtb::set_stream(static_cast<cudaStream_t>(stream));
   return RTUCKER_OK;

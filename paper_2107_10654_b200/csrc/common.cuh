@@ -22,7 +22,14 @@ struct Error : std::runtime_error {
                                 " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
   } while (0)
 
-#define RTB_LAUNCH_CHECK() RTB_CUDA(cudaGetLastError())
+// Every launch site ends with RTB_LAUNCH_CHECK(): it checks the launch and
+// counts it (rtucker_b200_launch_count exposes the total for bench.py).
+unsigned long long& launch_counter();
+#define RTB_LAUNCH_CHECK()          \
+  do {                              \
+    RTB_CUDA(cudaGetLastError());   \
+    ++::rtb::launch_counter();      \
+  } while (0)
 
 constexpr int kNumSMs = 148;
 constexpr int kMaxOrder = 8;

@@ -53,6 +53,11 @@ cudaStream_t current_stream() {
 
 void set_stream(cudaStream_t s) { t_stream = s; }
 
+unsigned long long& launch_counter() {
+  static unsigned long long n = 0;
+  return n;
+}
+
 DevBuf::DevBuf(size_t b, cudaStream_t s) { ensure(b, s); }
 DevBuf::~DevBuf() {
   if (p) cudaFreeAsync(p, st);
@@ -774,7 +779,7 @@ class Engine {
                                             eig_stride_, 0.0, scores_.as<double>(),
                                             score_off_.as<long long>(), ranks_dev_.as<int>());
       RTB_LAUNCH_CHECK();
-      k_score_cdf<<<1, 32, 0, st_>>>(scores_.as<double>(), score_off_.as<long long>(),
+      k_score_cdf<<<1, 32 * N_, 0, st_>>>(scores_.as<double>(), score_off_.as<long long>(),
                                      rows_dev_.as<int>(), N_, cdf_.as<double>(), sums_.as<double>());
       RTB_LAUNCH_CHECK();
       k_any_zero_rank<<<1, 32, 0, st_>>>(ranks_dev_.as<int>(), N_, zero_flag_.as<int>());

@@ -398,16 +398,25 @@ __global__ void k_expand_gram(GramSpec spec, const double* __restrict__ S, long 
 }
 
 // (E) rhs[p1 * d' + p'] = sum_b A1[i1_b, p1] h[b, p'].
-__global__ void k_rhs(GramSpec spec, const double* __restrict__ h, const int* __restrict__ bi1,
-                      const int* __restrict__ nbuckets, double* __restrict__ rhs) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= spec.d) return;
+// grid = (ceil(d'/64), R1); 64 outputs x 4 bucket groups per block.
+__global__ void __launch_bounds__(256) k_rhs(GramSpec spec, const double* __restrict__ h,
+                                             const int* __restrict__ bi1,
+                                             const int* __restrict__ nbuckets,
+                                             double* __restrict__ rhs) {
+  __shared__ double part[4][64];
   const int R1 = spec.ranks[0], dp = spec.dprime;
-  const int p1 = e / dp, pp = e % dp;
+  const int p1 = blockIdx.y;
+  const int c = threadIdx.x & 63, q = threadIdx.x >> 6;
+  const int pp = blockIdx.x * 64 + c;
   const int nb = *nbuckets;
   double s = 0.0;
-  for (int b = 0; b < nb; ++b) s += spec.factors[0][(size_t)bi1[b] * R1 + p1] * h[(size_t)b * dp + pp];
-  rhs[e] = s;
+  if (pp < dp)
+    for (int b = q; b < nb; b += 4)
+      s += spec.factors[0][(size_t)bi1[b] * R1 + p1] * h[(size_t)b * dp + pp];
+  part[q][c] = s;
+  __syncthreads();
+  if (q == 0 && pp < dp)
+    rhs[(size_t)p1 * dp + pp] = (part[0][c] + part[1][c]) + (part[2][c] + part[3][c]);
 }
 
 void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long long* idx,
@@ -449,7 +458,7 @@ void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
   const double aug_term = (wa * wa * rl) * rl;
   k_expand_gram<<<kNumSMs * 8, 256, 0, st>>>(spec, l.S, ncols, l.aug_count, aug_term, gram);
   RTB_LAUNCH_CHECK();
-  k_rhs<<<ceil_div(spec.d, 128), 128, 0, st>>>(spec, l.h, l.bi1, l.nbuckets, rhs);
+  k_rhs<<<dim3(ceil_div(spec.dprime, 64), R1), 256, 0, st>>>(spec, l.h, l.bi1, l.nbuckets, rhs);
   RTB_LAUNCH_CHECK();
 }
 

@@ -66,8 +66,14 @@ __global__ void k_sym_eigen(const double* in, const int* ns, int stride, double*
     V[e] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
+  __shared__ double red[32];
   double fro = 0.0;
-  for (int e = 0; e < n * n; ++e) fro += src[e] * src[e];  // every thread, same order
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) fro += A[e] * A[e];
+  fro = block_sum<128>(fro, red);
+  __shared__ double s_fro;
+  if (threadIdx.x == 0) s_fro = fro;
+  __syncthreads();
+  fro = s_fro;
   const double tiny = 1e-300 + 1e-30 * fro * DBL_EPSILON;
   int st = 3;
   for (int sweep = 0; sweep < 100; ++sweep) {
@@ -172,19 +178,28 @@ __global__ void k_leverage_rows(const FactorSet fs, const double* evals, const d
   scores[score_off[mode] + i] = s;
 }
 
-// Sequential left-to-right CDF per mode (one thread per mode).
+// Left-to-right CDF per mode, one warp per mode: each lane loads 32 scores and
+// every lane adds them in index order (shuffle broadcast), so the running sum
+// is the same sequence of roundings as the reference's serial loop.
 __global__ void k_score_cdf(const double* scores, const long long* off, const int* rows,
                             int order, double* cdf, double* sums) {
-  const int mode = threadIdx.x;
+  const int mode = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (mode >= order) return;
-  double running = 0.0;
   const double* s = scores + off[mode];
   double* c = cdf + off[mode];
-  for (int i = 0; i < rows[mode]; ++i) {
-    running = __dadd_rn(running, s[i]);
-    c[i] = running;
+  const int n = rows[mode];
+  double running = 0.0;
+  for (int base = 0; base < n; base += 32) {
+    const double v = base + lane < n ? s[base + lane] : 0.0;
+    double mine = 0.0;
+    const int cnt = min(32, n - base);
+    for (int k = 0; k < cnt; ++k) {
+      running = __dadd_rn(running, __shfl_sync(0xffffffffu, v, k));
+      if (lane == k) mine = running;
+    }
+    if (base + lane < n) c[base + lane] = mine;
   }
-  sums[mode] = running;
+  if (lane == 0) sums[mode] = running;
 }
 
 // ---------------------------------------------------------------------------

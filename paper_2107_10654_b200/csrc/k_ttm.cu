@@ -249,9 +249,42 @@ __global__ void k_ttm_generic(const double* __restrict__ X, long long O, int I, 
   out[e] = s;
 }
 
-// M[i,r] = sum_{o,j} Y[o,i,j] G[o,r,j]; Y (O,I,J), G (O,R,J). One thread per (i,r).
-__global__ void k_contract_except(const double* __restrict__ Y, const double* __restrict__ G,
-                                  long long O, int I, int R, long long J, double* __restrict__ M) {
+// M[i,r] = sum_{o,j} Y[o,i,j] G[o,r,j]; Y (O,I,J), G (O,R,J).
+// One block per i; threads stride over (o,j), accumulate all r in registers,
+// then a fixed-order smem reduction (deterministic).
+template <int RM>
+__global__ void __launch_bounds__(128) k_contract_except(const double* __restrict__ Y,
+                                                         const double* __restrict__ G,
+                                                         long long O, int I, int R, long long J,
+                                                         double* __restrict__ M) {
+  __shared__ double part[128][RM + 1];
+  const int i = blockIdx.x, tid = threadIdx.x;
+  double acc[RM];
+#pragma unroll
+  for (int r = 0; r < RM; ++r) acc[r] = 0.0;
+  const long long n = O * J;
+  for (long long t = tid; t < n; t += 128) {
+    const long long o = t / J, j = t % J;
+    const double y = Y[(o * I + i) * J + j];
+    const double* g = G + o * R * J + j;
+#pragma unroll
+    for (int r = 0; r < RM; ++r)
+      if (r < R) acc[r] += y * g[(long long)r * J];
+  }
+#pragma unroll
+  for (int r = 0; r < RM; ++r) part[tid][r] = acc[r];
+  __syncthreads();
+  if (tid < R) {
+    double s = 0.0;
+    for (int k = 0; k < 128; ++k) s += part[k][tid];
+    M[(long long)i * R + tid] = s;
+  }
+}
+
+// scalar fallback for R > 32: one thread per (i, r)
+__global__ void k_contract_except_scalar(const double* __restrict__ Y,
+                                         const double* __restrict__ G, long long O, int I, int R,
+                                         long long J, double* __restrict__ M) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (long long)I * R) return;
   const int i = (int)(e / R), r = (int)(e % R);
@@ -364,9 +397,17 @@ void ttm_generic(const double* X, long long O, int I, long long J, const double*
 
 void contract_except(const double* Y, const double* G, long long O, int I, int R, long long J,
                      double* M, cudaStream_t st) {
-  const long long total = (long long)I * R;
-  k_contract_except<<<(unsigned)ceil_div<long long>(total, 128), 128, 0, st>>>(Y, G, O, I, R, J,
-                                                                              M);
+  if (R <= 8) {
+    k_contract_except<8><<<I, 128, 0, st>>>(Y, G, O, I, R, J, M);
+  } else if (R <= 16) {
+    k_contract_except<16><<<I, 128, 0, st>>>(Y, G, O, I, R, J, M);
+  } else if (R <= 32) {
+    k_contract_except<32><<<I, 128, 0, st>>>(Y, G, O, I, R, J, M);
+  } else {
+    const long long total = (long long)I * R;
+    k_contract_except_scalar<<<(unsigned)ceil_div<long long>(total, 128), 128, 0, st>>>(
+        Y, G, O, I, R, J, M);
+  }
   RTB_LAUNCH_CHECK();
 }
 

@@ -117,6 +117,7 @@ def _load() -> C.CDLL:
         # extensions
         "rtucker_b200_set_device": (S, [C.c_int]),
         "rtucker_b200_set_stream": (S, [_vp]),
+        "rtucker_b200_launch_count": (C.c_ulonglong, []),
         "rtucker_b200_tensor_create_device": (S, [_u64p, C.c_uint32, _vp, C.POINTER(_vp)]),
         "rtucker_b200_tensor_device_data": (_vp, [_vp]),
         "rtucker_b200_als_run_ex": (S, [_vp, _u64p, C.c_uint32, C.POINTER(AlsOptions),
@@ -206,11 +207,16 @@ def options(**kw) -> AlsOptions:
     return o
 
 
+def _own(handle):
+    """Copy a handle value (callers may reuse their c_void_p out-parameter)."""
+    return C.c_void_p(handle.value if isinstance(handle, C.c_void_p) else handle)
+
+
 class Tensor:
     """rtucker_tensor handle (host + resident device copy)."""
 
     def __init__(self, handle):
-        self.h = handle
+        self.h = _own(handle)
 
     @classmethod
     def from_numpy(cls, x) -> "Tensor":
@@ -293,7 +299,7 @@ class Result:
     """rtucker_als_result handle."""
 
     def __init__(self, h, shape):
-        self.h = h
+        self.h = _own(h)
         self.shape = tuple(shape)
 
     def history(self):

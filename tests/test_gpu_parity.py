@@ -116,6 +116,22 @@ def test_spd_solve_on_reference_gram(oracle, rt, d):
     assert np.linalg.norm(gx - ox) / np.linalg.norm(ox) < 100 * kappa * EPS
 
 
+@pytest.mark.parametrize("d,kappa_target", [(1000, 1e6), (4096, 1e8), (4100, 1e4)])
+def test_spd_solve_large(rt, d, kappa_target):
+    """Large SPD systems (the C2 core solve is d = 4096): checked against LAPACK
+    (numpy) since the oracle's Jacobi SVD takes hours at this size."""
+    rng = np.random.default_rng(d)
+    q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    ev = np.logspace(0, -np.log10(kappa_target), d)
+    g = (q * ev) @ q.T
+    g = 0.5 * (g + g.T)
+    b = rng.standard_normal(d)
+    xr = np.linalg.solve(g, b)
+    gx, grank, path = rt.spd_solve(g, b)
+    assert path == 0 and grank == d
+    assert np.linalg.norm(gx - xr) / np.linalg.norm(xr) < 100 * kappa_target * EPS * np.sqrt(d)
+
+
 def test_spd_solve_rank_deficient_small(oracle, rt):
     rng = np.random.default_rng(1)
     a = rng.standard_normal((20, 3))

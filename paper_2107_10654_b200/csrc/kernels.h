@@ -87,5 +87,11 @@ size_t chol_work_bytes(int d);
 // In-place Cholesky of the lower triangle of a (d x d, row-major) and solve
 // a x = b (x overwrites b). *status_dev = 0 ok, k+1 = non-positive pivot at k.
 void chol_solve(double* a, int d, double* b, int* status_dev, void* work, cudaStream_t st);
+// profiling hooks: per-task (grab, ready, end, smid) into a device buffer
+void chol_set_trace(unsigned long long* trace);
+void chol_set_progress(volatile int* p);
+void chol_debug(int d, void* work, int* out4);  // abort flag, flag index, value, wanted
+int chol_task_count(int d);
+void chol_task_table(int d, int* out4);
 
 }  // namespace rtb

@@ -479,7 +479,7 @@ class Engine {
   std::vector<uint64_t> fac_off_;
   Profiler prof_;
 
-  DevBuf ns_vals_;
+  DevBuf ns_vals_, pinv2_, linv_, spd_ok_;
   DevBuf core_, fac_, grams_, evals_, evecs_, eig_status_, ns_, pinv_, ranks_dev_;
   DevBuf T_, P_, tmp_a_, tmp_b_, partial_, scal_, hist_, init_loss_;
   DevBuf scores_, cdf_, sums_, score_off_, rows_dev_, cols_dev_, flag_;
@@ -525,6 +525,9 @@ class Engine {
     fac_.ensure(fac_elems_ * 8, st_);
     grams_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
     pinv_.ensure((size_t)eig_stride_ * 8 + 8, st_);
+    pinv2_.ensure((size_t)eig_stride_ * 8 + 8, st_);
+    linv_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
+    spd_ok_.ensure(64 * 4, st_);
     {
       // eigen_one() may also factor a d <= 64 core Gram into slot 0
       const size_t eb = std::max<size_t>((size_t)N_ * eig_stride_, 64 * 64) * 8 + 8;
@@ -534,8 +537,6 @@ class Engine {
       for (int i = 0; i < 65; ++i) vals[i] = i;
       ns_vals_.ensure(65 * 4, st_);
       RTB_CUDA(cudaMemcpy(ns_vals_.p, vals, 65 * 4, cudaMemcpyHostToDevice));
-      const int smem = (2 * 64 * 64 + 2 * 64) * 8;
-      RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
     eig_status_.ensure(64 * 4, st_);
     ns_.ensure(64 * 4, st_);
@@ -637,6 +638,8 @@ class Engine {
       } else if (O <= 65535 && J >= 64) {
         Scope sc(prof_, "ttm_mid");
         ttm_mid(in, (int)O, I, J, W, Rn, out, st_);
+      } else if (J <= 32 && ttm_smallj(in, O, I, (int)J, W, Rn, out, st_)) {
+        // short contiguous tail (e.g. T x_2 A_2^T with J = R_3)
       } else {
         Scope sc(prof_, "ttm_generic");
         ttm_generic(in, O, I, J, W, wr, wi, Rn, out, st_);
@@ -719,14 +722,28 @@ class Engine {
       contract_except(core_.as<double>(), cur, O, Rn, Rn, J, kk, st_);
       k_add_diag<<<ceil_div(Rn, 64), 64, 0, st_>>>(kk, Rn, opt_.lambda);
       RTB_LAUNCH_CHECK();
-      // pinv via eigen (symmetric): singular values = |eigenvalues| (ref linalg.cpp:8-26)
-      eigen_one(kk, Rn);
-      k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(),
-                                     ns_one(Rn), eig_stride_, kk, nullptr);
+      // (KK^T + lambda I)^+ (ref linalg.cpp:8-26): warp Cholesky inverse; if a
+      // pivot is below R*eps*max diag the eigen/pinv path (singular values =
+      // |eigenvalues|, cutoff R*eps*sigma_max) takes over on the device.
+      double* pv = pinv2_.as<double>();
+      int* okf = spd_ok_.as<int>();
+      const int stride = std::max(eig_stride_, Rn * Rn);
+      if (Rn <= 32) {
+        spd_small(kk, ns_one(Rn), stride, (double)Rn * DBL_EPSILON, linv_.as<double>(), pv, okf,
+                  1, st_);
+        sym_eigen(kk, ns_one(Rn), Rn, stride, evals_.as<double>(), evecs_.as<double>(),
+                  eig_status_.as<int>(), 1, st_, okf);
+        k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one(Rn),
+                                       stride, pv, nullptr, okf);
+      } else {
+        eigen_one(kk, Rn);
+        k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one(Rn),
+                                       stride, pv, nullptr, nullptr);
+      }
       RTB_LAUNCH_CHECK();
       // A_n = M pinv
       const long long tot = (long long)In * Rn;
-      k_rows_times_small<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(M, kk, In, Rn, factor(n));
+      k_rows_times_small<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(M, pv, In, Rn, factor(n));
       RTB_LAUNCH_CHECK();
     }
     factor_gram(n);
@@ -743,23 +760,14 @@ class Engine {
 
   // eigen of one symmetric n x n matrix (device) into slot 0 of evals/evecs
   void eigen_one(const double* m, int n) {
-    const int np = n + (n & 1);
-    const size_t smem = (2 * (size_t)np * np + 2 * np) * 8;
-    if (n > 64) throw Error(4, "eigen: n > 64 not supported");
-    k_sym_eigen<<<1, 128, smem, st_>>>(m, ns_one(n), eig_stride_, evals_.as<double>(),
-                                       evecs_.as<double>(), eig_status_.as<int>());
-    RTB_LAUNCH_CHECK();
+    sym_eigen(m, ns_one(n), n, eig_stride_ > n * n ? eig_stride_ : n * n, evals_.as<double>(),
+              evecs_.as<double>(), eig_status_.as<int>(), 1, st_);
   }
 
-  // eigen of all factor Grams (batched, one CTA each)
+  // eigen of all factor Grams (batched)
   void eigen_grams() {
-    const int np = rmax_ + (rmax_ & 1);
-    const size_t smem = (2 * (size_t)np * np + 2 * np) * 8;
-    if (rmax_ > 64) throw Error(4, "eigen: rank > 64 not supported");
-    k_sym_eigen<<<N_, 128, smem, st_>>>(grams_.as<double>(), ns_.as<int>(), eig_stride_,
-                                        evals_.as<double>(), evecs_.as<double>(),
-                                        eig_status_.as<int>());
-    RTB_LAUNCH_CHECK();
+    sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, evals_.as<double>(),
+              evecs_.as<double>(), eig_status_.as<int>(), N_, st_);
   }
 
   // ---- sketched core (ref tucker.cpp:141-166, sketch_ridge.cpp:52-151) ----
@@ -770,15 +778,31 @@ class Engine {
     // shard of the draw range for multi-GPU sample sharding
     {
       Scope sc(prof_, "scores");
-      eigen_grams();
+      // classical scores l_i = a_i^T (A^T A)^+ a_i: Cholesky of each factor Gram
+      // (||L^-1 a_i||^2); eigen path (rank cutoff) for modes whose Gram is
+      // numerically singular (ref leverage.cpp:16-37 at lambda = 0)
       FactorSet fs = factor_set();
       int maxI = 0;
       for (auto v : shape_) maxI = std::max<int>(maxI, (int)v);
+      const int* okm = nullptr;
+      if (rmax_ <= 32) {
+        spd_small(grams_.as<double>(), ns_.as<int>(), eig_stride_, (double)maxI * DBL_EPSILON,
+                  linv_.as<double>(), nullptr, spd_ok_.as<int>(), N_, st_);
+        okm = spd_ok_.as<int>();
+      }
+      sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, evals_.as<double>(),
+                evecs_.as<double>(), eig_status_.as<int>(), N_, st_, okm);
       dim3 grid(ceil_div(maxI, 128), N_);
       k_leverage_rows<<<grid, 128, 0, st_>>>(fs, evals_.as<double>(), evecs_.as<double>(),
                                             eig_stride_, 0.0, scores_.as<double>(),
-                                            score_off_.as<long long>(), ranks_dev_.as<int>());
+                                            score_off_.as<long long>(), ranks_dev_.as<int>(), okm);
       RTB_LAUNCH_CHECK();
+      if (okm) {
+        k_leverage_chol<<<grid, 128, 0, st_>>>(fs, linv_.as<double>(), eig_stride_, okm,
+                                              scores_.as<double>(), score_off_.as<long long>(),
+                                              ranks_dev_.as<int>());
+        RTB_LAUNCH_CHECK();
+      }
       k_score_cdf<<<1, 32 * N_, 0, st_>>>(scores_.as<double>(), score_off_.as<long long>(),
                                      rows_dev_.as<int>(), N_, cdf_.as<double>(), sums_.as<double>());
       RTB_LAUNCH_CHECK();
@@ -875,7 +899,7 @@ class Engine {
       double* pv = tmp_a_.as<double>();
       k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one((int)d_),
                                      eig_stride_ > (int)(d_ * d_) ? eig_stride_ : (int)(d_ * d_),
-                                     pv, ranks_dev_.as<int>());
+                                     pv, ranks_dev_.as<int>(), nullptr);
       RTB_LAUNCH_CHECK();
       k_rows_times_small<<<ceil_div<long long>(d_, 256), 256, 0, st_>>>(rhs_.as<double>(), pv, 1,
                                                                         (int)d_, core_.as<double>());
@@ -981,9 +1005,10 @@ class Engine {
       const int I = (int)shape_[m], R = (int)ranks_[m];
       double* out = (m == N_ - 2) ? P_.as<double>() : bufs[which];
       // out[.., i, ..] = sum_r A[i][r] cur[.., r, ..]  (W = A: wr = R, wi = 1)
-      Scope sc(prof_, "ttm_generic");
-      ttm_generic(cur, (long long)prod(dims, 0, m), R, (long long)prod(dims, m + 1), factor(m), R, 1,
-                  I, out, st_);
+      Scope sc(prof_, "ttm_expand");
+      const long long Oe = (long long)prod(dims, 0, m), Je = (long long)prod(dims, m + 1);
+      if (!ttm_expand(cur, Oe, R, Je, factor(m), I, out, st_))
+        ttm_generic(cur, Oe, R, Je, factor(m), R, 1, I, out, st_);
       dims[m] = I;
       cur = out;
       which ^= 1;
@@ -1207,17 +1232,26 @@ void factor_scores(const double* factor_host, int rows, int cols, double* scores
   fs.cols[0] = cols;
   k_factor_gram<<<dim3(cols * cols, 1), 256, 0, st>>>(fs, g.as<double>(), cols);
   RTB_LAUNCH_CHECK();
-  const int np = cols + (cols & 1);
-  const int smem = (2 * np * np + 2 * np) * 8;
-  RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (2 * 64 * 64 + 2 * 64) * 8));
-  k_sym_eigen<<<1, 128, smem, st>>>(g.as<double>(), ns.as<int>(), cols * cols, ev.as<double>(),
-                                    evec.as<double>(), stat.as<int>());
-  RTB_LAUNCH_CHECK();
+  // same route as the ALS core step: Cholesky of the Gram, eigen fallback
+  DevBuf lv((size_t)cols * cols * 8 + 8, st), okb(4, st);
+  const int* okm = nullptr;
+  if (cols <= 32) {
+    spd_small(g.as<double>(), ns.as<int>(), cols * cols,
+              (double)std::max(rows, cols) * DBL_EPSILON, lv.as<double>(), nullptr, okb.as<int>(), 1,
+              st);
+    okm = okb.as<int>();
+  }
+  sym_eigen(g.as<double>(), ns.as<int>(), cols, cols * cols, ev.as<double>(), evec.as<double>(),
+            stat.as<int>(), 1, st, okm);
   k_leverage_rows<<<dim3(ceil_div(rows, 128), 1), 128, 0, st>>>(
       fs, ev.as<double>(), evec.as<double>(), cols * cols, 0.0, sc.as<double>(),
-      off.as<long long>(), rk.as<int>());
+      off.as<long long>(), rk.as<int>(), okm);
   RTB_LAUNCH_CHECK();
+  if (okm) {
+    k_leverage_chol<<<dim3(ceil_div(rows, 128), 1), 128, 0, st>>>(
+        fs, lv.as<double>(), cols * cols, okm, sc.as<double>(), off.as<long long>(), rk.as<int>());
+    RTB_LAUNCH_CHECK();
+  }
   k_score_cdf<<<1, 32, 0, st>>>(sc.as<double>(), off.as<long long>(), rw.as<int>(), 1,
                                 cd.as<double>(), sm.as<double>());
   RTB_LAUNCH_CHECK();
@@ -1326,14 +1360,9 @@ static void solve_sym_device(double* G, double* rhs, int d, double* x_dev, int* 
   DevBuf ev((size_t)d * d * 8 + 8, st), evec((size_t)d * d * 8, st), es(4, st), ns(4, st),
       pv((size_t)d * d * 8, st), rk(4, st);
   RTB_CUDA(cudaMemcpyAsync(ns.p, &d, 4, cudaMemcpyHostToDevice, st));
-  const int np = d + (d & 1);
-  RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (2 * 64 * 64 + 2 * 64) * 8));
-  k_sym_eigen<<<1, 128, (2 * np * np + 2 * np) * 8, st>>>(G, ns.as<int>(), d * d, ev.as<double>(),
-                                                          evec.as<double>(), es.as<int>());
-  RTB_LAUNCH_CHECK();
+  sym_eigen(G, ns.as<int>(), d, d * d, ev.as<double>(), evec.as<double>(), es.as<int>(), 1, st);
   k_sym_pinv<<<1, 256, 0, st>>>(ev.as<double>(), evec.as<double>(), ns.as<int>(), d * d,
-                                pv.as<double>(), rk.as<int>());
+                                pv.as<double>(), rk.as<int>(), nullptr);
   RTB_LAUNCH_CHECK();
   k_rows_times_small<<<ceil_div(d, 256), 256, 0, st>>>(rhs, pv.as<double>(), 1, d, x_dev);
   RTB_LAUNCH_CHECK();
@@ -1414,12 +1443,8 @@ void dense_ridge_scores(const double* a, uint64_t n, uint64_t d, double lambda, 
   long long zero = 0;
   RTB_CUDA(cudaMemcpyAsync(ns.p, &di, 4, cudaMemcpyHostToDevice, st));
   RTB_CUDA(cudaMemcpyAsync(off.p, &zero, 8, cudaMemcpyHostToDevice, st));
-  RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (2 * 64 * 64 + 2 * 64) * 8));
-  k_sym_eigen<<<1, 128, (2 * np * np + 2 * np) * 8, st>>>(g.as<double>(), ns.as<int>(), di * di,
-                                                          ev.as<double>(), evec.as<double>(),
-                                                          es.as<int>());
-  RTB_LAUNCH_CHECK();
+  sym_eigen(g.as<double>(), ns.as<int>(), di, di * di, ev.as<double>(), evec.as<double>(),
+            es.as<int>(), 1, st);
   FactorSet fs{};
   fs.order = 1;
   fs.ptr[0] = ad.as<double>();
@@ -1427,7 +1452,7 @@ void dense_ridge_scores(const double* a, uint64_t n, uint64_t d, double lambda, 
   fs.cols[0] = di;
   k_leverage_rows<<<dim3((unsigned)ceil_div<uint64_t>(n, 128), 1), 128, 0, st>>>(
       fs, ev.as<double>(), evec.as<double>(), di * di, lambda, sc.as<double>(),
-      off.as<long long>(), rk.as<int>());
+      off.as<long long>(), rk.as<int>(), nullptr);
   RTB_LAUNCH_CHECK();
   int e = 0;
   RTB_CUDA(cudaMemcpyAsync(out, sc.p, n * 8, cudaMemcpyDeviceToHost, st));

@@ -721,39 +721,60 @@ __global__ void k_chol_check(CholWork w, int* status) {
 }
 
 // Backward substitution L^T x = y as a wavefront: block c (64 unknowns) is
-// owned by CTA (T-1-c) mod grid, blocks processed in descending order; it
-// subtracts L_kc^T x_k for every k > c as soon as x_k is published.
+// owned by CTA (T-1-c) mod grid, blocks processed in descending order. The CTA
+// streams L_kc (k > c) through a double-buffered smem tile -- those loads do not
+// depend on x -- and subtracts L_kc^T x_k as each x_k is published; then
+// x_c = Linv_cc^T (y_c - sum).
 __global__ void __launch_bounds__(kThreads) k_trsv_back(const double* a, int d, CholWork w,
                                                         double* x_out, const int* status) {
   if (*status) return;
+  extern __shared__ __align__(16) double bsm[];
+  double(*lt[2])[LDT] = {reinterpret_cast<double(*)[LDT]>(bsm),
+                         reinterpret_cast<double(*)[LDT]>(bsm + NB * LDT)};
+  double(*iv)[LDT] = reinterpret_cast<double(*)[LDT]>(bsm + 2 * NB * LDT);
   __shared__ double v[NB];
+  __shared__ double xk[NB];
   __shared__ double part[4][NB];
   const int tid = threadIdx.x;
   const int T = w.T;
+  const bool vec = (d % 2) == 0;
   const int l = tid & (NB - 1), q = tid >> 6;  // 64 columns x 4 row groups
   for (int c = T - 1 - (int)blockIdx.x; c >= 0; c -= gridDim.x) {
     const int c0 = c * NB;
-    double s = 0.0;
-    for (int k = T - 1; k > c; --k) {
-      if (tid == 0) wait_ge(&w.xflag[k], 1, &w.counter[1], w.counter + 2, w.xflag);
-      __syncthreads();
-      const int k0 = k * NB;
-      if (c0 + l < d) {
-        for (int r = q * 16; r < q * 16 + 16; ++r) {
-          if (k0 + r < d) s += __ldcg(a + (size_t)(k0 + r) * d + c0 + l) * __ldcg(w.x + k0 + r);
-        }
+    {  // Linv_cc
+      const double* src = w.linv + (size_t)c * NB * NB;
+      for (int e = tid; e < NB * (NB / 2); e += kThreads) {
+        const int r = e / (NB / 2), cc = (e % (NB / 2)) * 2;
+        cp_async16(&iv[r][cc], src + r * NB + cc, true);
       }
     }
+    if (T - 1 > c) load_tile(lt[0], a, d, (T - 1) * NB, c0, vec);
+    cp_async_commit();
+    double s = 0.0;
+    for (int k = T - 1; k > c; --k) {
+      const int cur = (T - 1 - k) & 1;
+      if (k - 1 > c) load_tile(lt[cur ^ 1], a, d, (k - 1) * NB, c0, vec);
+      cp_async_commit();
+      if (tid == 0) wait_ge(&w.xflag[k], 1, &w.counter[1], w.counter + 2, w.xflag);
+      __syncthreads();
+      if (tid < NB) xk[tid] = __ldcg(w.x + k * NB + tid);
+      cp_async_wait<1>();
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) s += lt[cur][q * 16 + r][l] * xk[q * 16 + r];
+      __syncthreads();
+    }
+    cp_async_wait<0>();
     part[q][l] = s;
     __syncthreads();
     if (tid < NB)
       v[tid] = (c0 + tid < d ? __ldcg(w.y + c0 + tid) : 0.0) -
                ((part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]));
     __syncthreads();
-    // x_c = Linv_cc^T v : x[l] = sum_{r >= l} Linv[r][l] v[r]
-    const double* iv = w.linv + (size_t)c * NB * NB;
+    // x[l] = sum_{r >= l} Linv[r][l] v[r]
     double xs = 0.0;
-    for (int r = q * 16; r < q * 16 + 16; ++r) xs += __ldcg(iv + r * NB + l) * v[r];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) xs += iv[q * 16 + r][l] * v[q * 16 + r];
     part[q][l] = xs;
     __syncthreads();
     if (tid < NB) {
@@ -809,13 +830,15 @@ void chol_solve(double* a, int d, double* b, int* status_dev, void* work, cudaSt
   k_chol_check<<<1, 32, 0, st>>>(w, status_dev);
   RTB_LAUNCH_CHECK();
   {
+    const int bsmem = 3 * NB * LDT * sizeof(double);
+    RTB_CUDA(cudaFuncSetAttribute(k_trsv_back, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
     int per2 = 0;
-    RTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_trsv_back, kThreads, 0));
+    RTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_trsv_back, kThreads, bsmem));
     const int g2 = std::min(w.T, sms * std::max(per2, 1));
     const double* ac = a;
     const int* sc = status_dev;
     void* args[] = {(void*)&ac, (void*)&d, (void*)&w, (void*)&b, (void*)&sc};
-    RTB_CUDA(cudaLaunchCooperativeKernel((void*)k_trsv_back, g2, kThreads, args, 0, st));
+    RTB_CUDA(cudaLaunchCooperativeKernel((void*)k_trsv_back, g2, kThreads, args, bsmem, st));
     RTB_LAUNCH_CHECK();
   }
 }

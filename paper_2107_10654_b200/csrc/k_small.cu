@@ -54,29 +54,31 @@ __global__ void k_sym_eigen(const double* in, const int* ns, int stride, double*
   const int b = blockIdx.x;
   const int n = ns[b];
   const int np = n + (n & 1);  // padded to even for the round-robin schedule
-  double* A = sm;               // np x np
-  double* V = A + np * np;      // np x np
-  double* cs = V + np * np;     // 2 * np/2 rotation coefficients
+  const int ld = np + 1;       // odd stride: column accesses hit distinct banks
+  double* A = sm;               // np x ld
+  double* V = A + np * ld;      // np x ld
+  double* cs = V + np * ld;     // 2 * np/2 rotation coefficients
   int* pair = reinterpret_cast<int*>(cs + np);  // np entries: partner schedule
   __shared__ int rotated;
   const double* src = in + (size_t)b * stride;
   for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
     const int i = e / np, j = e % np;
-    A[e] = (i < n && j < n) ? src[i * n + j] : 0.0;
-    V[e] = (i == j) ? 1.0 : 0.0;
+    A[i * ld + j] = (i < n && j < n) ? src[i * n + j] : 0.0;
+    V[i * ld + j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
   __shared__ double red[32];
   double fro = 0.0;
-  for (int e = threadIdx.x; e < np * np; e += blockDim.x) fro += A[e] * A[e];
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) fro += A[(e / np) * ld + e % np] * A[(e / np) * ld + e % np];
   fro = block_sum<128>(fro, red);
   __shared__ double s_fro;
   if (threadIdx.x == 0) s_fro = fro;
   __syncthreads();
   fro = s_fro;
-  const double tiny = 1e-300 + 1e-30 * fro * DBL_EPSILON;
+  const double tiny = 1e-300;
+  const double tol_abs = (double)n * DBL_EPSILON * sqrt(fro);
   int st = 3;
-  for (int sweep = 0; sweep < 100; ++sweep) {
+  for (int sweep = 0; sweep < 60; ++sweep) {
     if (threadIdx.x == 0) rotated = 0;
     __syncthreads();
     for (int round = 0; round < np - 1; ++round) {
@@ -88,13 +90,15 @@ __global__ void k_sym_eigen(const double* in, const int* ns, int stride, double*
         if (p > q) { int t = p; p = q; q = t; }
         pair[2 * k] = p;
         pair[2 * k + 1] = q;
-        const double apq = A[p * np + q];
-        const double app = A[p * np + p], aqq = A[q * np + q];
+        const double apq = A[p * ld + q];
+        const double app = A[p * ld + p], aqq = A[q * ld + q];
         double c = 1.0, s = 0.0;
         // rotate unless already negligible relative to the diagonal (high
         // relative accuracy criterion) or padding
-        if (q < n && fabs(apq) > tiny &&
-            fabs(apq) > DBL_EPSILON * 0.5 * sqrt(fabs(app) * fabs(aqq))) {
+        // absolute threshold n*eps*||A||_F (the rotated pair is zeroed explicitly
+        // below): a relative test never settles when the diagonal spans many
+        // orders of magnitude, since rotation rounding is ~eps*max|a_ii|
+        if (q < n && fabs(apq) > tiny && fabs(apq) > tol_abs) {
           const double theta = (aqq - app) / (2.0 * apq);
           const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
           c = 1.0 / sqrt(1.0 + t * t);
@@ -111,12 +115,12 @@ __global__ void k_sym_eigen(const double* in, const int* ns, int stride, double*
         const int p = pair[2 * k], q = pair[2 * k + 1];
         const double c = cs[2 * k], s = cs[2 * k + 1];
         if (s == 0.0) continue;
-        const double ap = A[row * np + p], aq = A[row * np + q];
-        A[row * np + p] = c * ap - s * aq;
-        A[row * np + q] = s * ap + c * aq;
-        const double vp = V[row * np + p], vq = V[row * np + q];
-        V[row * np + p] = c * vp - s * vq;
-        V[row * np + q] = s * vp + c * vq;
+        const double ap = A[row * ld + p], aq = A[row * ld + q];
+        A[row * ld + p] = c * ap - s * aq;
+        A[row * ld + q] = s * ap + c * aq;
+        const double vp = V[row * ld + p], vq = V[row * ld + q];
+        V[row * ld + p] = c * vp - s * vq;
+        V[row * ld + q] = s * vp + c * vq;
       }
       __syncthreads();
       // A <- J^T A (rows)
@@ -125,30 +129,265 @@ __global__ void k_sym_eigen(const double* in, const int* ns, int stride, double*
         const int p = pair[2 * k], q = pair[2 * k + 1];
         const double c = cs[2 * k], s = cs[2 * k + 1];
         if (s == 0.0) continue;
-        const double ap = A[p * np + col], aq = A[q * np + col];
-        A[p * np + col] = c * ap - s * aq;
-        A[q * np + col] = s * ap + c * aq;
+        const double ap = A[p * ld + col], aq = A[q * ld + col];
+        A[p * ld + col] = c * ap - s * aq;
+        A[q * ld + col] = s * ap + c * aq;
+      }
+      __syncthreads();
+      if (threadIdx.x < np / 2 && cs[2 * threadIdx.x + 1] != 0.0) {
+        const int p = pair[2 * threadIdx.x], q = pair[2 * threadIdx.x + 1];
+        A[p * ld + q] = 0.0;
+        A[q * ld + p] = 0.0;
       }
       __syncthreads();
     }
     if (!rotated) {
+#ifdef RTB_EIG_SWEEP_DEBUG
+      st = -(sweep + 1);
+#else
       st = 0;
+#endif
       break;
     }
     __syncthreads();
   }
   // stable sort by eigenvalue, non-increasing
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    const double mk = A[k * np + k];
+    const double mk = A[k * ld + k];
     int rank = 0;
     for (int j = 0; j < n; ++j) {
-      const double mj = A[j * np + j];
+      const double mj = A[j * ld + j];
       if (mj > mk || (mj == mk && j < k)) ++rank;
     }
     evals[(size_t)b * stride + rank] = mk;
-    for (int i = 0; i < n; ++i) evecs[(size_t)b * stride * 1 + (size_t)i * n + rank] = V[i * np + k];
+    for (int i = 0; i < n; ++i) evecs[(size_t)b * stride * 1 + (size_t)i * n + rank] = V[i * ld + k];
   }
   if (threadIdx.x == 0) status[b] = st;
+}
+
+// ---------------------------------------------------------------------------
+// Warp-per-matrix variant for n <= 32 (the factor Grams and the R_n x R_n
+// factor-update systems): same rotations, only __syncwarp between phases.
+__global__ void k_sym_eigen_warp(const double* in, const int* ns, int stride, double* evals,
+                                 double* evecs, int* status, int nmat, const int* skip) {
+  extern __shared__ double smw[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (b >= nmat) return;
+  if (skip && skip[b]) {  // a Cholesky already succeeded for this matrix
+    if (lane == 0) status[b] = 0;
+    return;
+  }
+  const int n = ns[b];
+  const int np = n + (n & 1);
+  const int ld = np + 1;  // odd stride: column accesses hit distinct banks
+  double* A = smw + wib * (2 * 32 * 33 + 64);
+  double* V = A + 32 * 33;
+  double* cs = V + 32 * 33;
+  int* pair = reinterpret_cast<int*>(cs + 32);
+  const double* src = in + (size_t)b * stride;
+  double fro = 0.0;
+  for (int e = lane; e < np * np; e += 32) {
+    const int i = e / np, j = e % np;
+    const double v = (i < n && j < n) ? src[i * n + j] : 0.0;
+    A[i * ld + j] = v;
+    V[i * ld + j] = (i == j) ? 1.0 : 0.0;
+    fro += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  const double tol_abs = (double)n * DBL_EPSILON * sqrt(fro);
+  __syncwarp();
+  int st = 3;
+  // round-robin pairing: position 0 fixed, the others rotate by one per round
+  int pos_p = 0, pos_q = 0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    int rotated = 0;
+    for (int round = 0; round < np - 1; ++round) {
+      if (lane < np / 2) {
+        // positions lane and np-1-lane; rotation offset without a division
+        pos_p = lane == 0 ? 0 : 1 + ((lane - 1 + round) % (np - 1));
+        pos_q = 1 + ((np - 2 - lane + round) % (np - 1));
+        int p = min(pos_p, pos_q), q = max(pos_p, pos_q);
+        pair[2 * lane] = p;
+        pair[2 * lane + 1] = q;
+        const double apq = A[p * ld + q], app = A[p * ld + p], aqq = A[q * ld + q];
+        double c = 1.0, s = 0.0;
+        if (q < n && fabs(apq) > 1e-300 && fabs(apq) > tol_abs) {
+          // t = sign(theta) / (|theta| + sqrt(1 + theta^2)), theta = (aqq-app)/(2 apq)
+          const double diff = aqq - app;
+          const double den = fabs(diff) + sqrt(diff * diff + 4.0 * apq * apq);
+          double t = 2.0 * apq / den;
+          if (diff < 0.0) t = -t;
+          c = rsqrt(1.0 + t * t);
+          s = c * t;
+        }
+        cs[2 * lane] = c;
+        cs[2 * lane + 1] = s;
+      }
+      rotated |= __any_sync(0xffffffffu, lane < np / 2 && cs[2 * lane + 1] != 0.0);
+      __syncwarp();
+      if (lane < np) {  // columns p, q of A and V: lane = row
+        for (int k = 0; k < np / 2; ++k) {
+          const double c = cs[2 * k], s = cs[2 * k + 1];
+          if (s == 0.0) continue;
+          const int p = pair[2 * k], q = pair[2 * k + 1];
+          const double ap = A[lane * ld + p], aq = A[lane * ld + q];
+          A[lane * ld + p] = c * ap - s * aq;
+          A[lane * ld + q] = s * ap + c * aq;
+          const double vp = V[lane * ld + p], vq = V[lane * ld + q];
+          V[lane * ld + p] = c * vp - s * vq;
+          V[lane * ld + q] = s * vp + c * vq;
+        }
+      }
+      __syncwarp();
+      if (lane < np) {  // rows p, q of A: lane = column
+        for (int k = 0; k < np / 2; ++k) {
+          const double c = cs[2 * k], s = cs[2 * k + 1];
+          if (s == 0.0) continue;
+          const int p = pair[2 * k], q = pair[2 * k + 1];
+          const double ap = A[p * ld + lane], aq = A[q * ld + lane];
+          A[p * ld + lane] = c * ap - s * aq;
+          A[q * ld + lane] = s * ap + c * aq;
+        }
+      }
+      __syncwarp();
+      if (lane < np / 2 && cs[2 * lane + 1] != 0.0) {
+        const int p = pair[2 * lane], q = pair[2 * lane + 1];
+        A[p * ld + q] = 0.0;
+        A[q * ld + p] = 0.0;
+      }
+      __syncwarp();
+    }
+    if (!rotated) {
+#ifdef RTB_EIG_SWEEP_DEBUG
+      st = -(sweep + 1);
+#else
+      st = 0;
+#endif
+      break;
+    }
+  }
+  for (int k = lane; k < n; k += 32) {
+    const double mk = A[k * ld + k];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double mj = A[j * ld + j];
+      if (mj > mk || (mj == mk && j < k)) ++rank;
+    }
+    evals[(size_t)b * stride + rank] = mk;
+    for (int i = 0; i < n; ++i) evecs[(size_t)b * stride + (size_t)i * n + rank] = V[i * ld + k];
+  }
+  if (lane == 0) status[b] = st;
+}
+
+// ---------------------------------------------------------------------------
+// Batched small SPD factorization, one warp per matrix (n <= 32): Cholesky
+// with row r in lane r's registers (column broadcasts through shuffles), then
+// Linv (column per lane). ok[b] = 1 unless a pivot falls below
+// tolrel * max diag (the caller then takes the eigen/pinv path for that
+// matrix). Optionally also writes P = M^-1 = Linv^T Linv.
+// Loops run to 32 with compile-time indices so row[] / x[] stay in registers;
+// the matrix is padded with the identity beyond n.
+__global__ void __launch_bounds__(128) k_spd_small(const double* in, const int* ns, int stride,
+                                                   double tolrel, double* linv, double* pinv,
+                                                   int* ok, int nmat) {
+  __shared__ double xs[4][32][33];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 4 + wib;
+  if (b >= nmat) return;
+  const int n = ns[b];
+  const double* src = in + (size_t)b * stride;
+  constexpr unsigned FULL = 0xffffffffu;
+  double row[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q)
+    row[q] = (lane < n && q < n) ? src[lane * n + q] : (lane == q ? 1.0 : 0.0);
+  double dmax = 0.0;
+#pragma unroll
+  for (int q = 0; q < 32; ++q)
+    if (q == lane && lane < n) dmax = fabs(row[q]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(FULL, dmax, o));
+  const double tol = tolrel * dmax;
+  bool bad = false;
+  double invd = 1.0;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const double piv = __shfl_sync(FULL, row[c], c);
+    bad |= (c < n) && !(piv > tol);
+    const double rs = rsqrt(piv);
+    row[c] = (lane == c) ? piv * rs : ((lane > c) ? row[c] * rs : row[c]);
+    invd = (lane == c) ? rs : invd;
+#pragma unroll
+    for (int l = 1; l < 32; ++l) {
+      if (l > c) {
+        const double lc = __shfl_sync(FULL, row[c], l);
+        row[l] = (lane >= l) ? row[l] - row[c] * lc : row[l];
+      }
+    }
+  }
+  bad = __any_sync(FULL, bad);
+  if (lane == 0) ok[b] = bad ? 0 : 1;
+  if (bad) return;
+  // Linv: lane = column
+  double x[32];
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) {
+    double s0 = (rr == lane) ? 1.0 : 0.0, s1 = 0.0;
+#pragma unroll
+    for (int l = 0; l < 31; ++l) {
+      if (l < rr) {
+        const double lv = __shfl_sync(FULL, row[l], rr);
+        if (l & 1) s1 -= lv * x[l];
+        else s0 -= lv * x[l];
+      }
+    }
+    const double dinv = __shfl_sync(FULL, invd, rr);
+    x[rr] = (rr >= lane) ? (s0 + s1) * dinv : 0.0;
+  }
+  double* lo = linv + (size_t)b * stride;
+  if (lane < n) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (q < n) lo[q * n + lane] = x[q];  // Linv[q][lane]
+  }
+  if (pinv) {
+    // P[i][j] = sum_k Linv[k][i] Linv[k][j]; lane j holds column j (x[k] = Linv[k][j])
+#pragma unroll
+    for (int q = 0; q < 32; ++q) xs[wib][q][lane] = x[q];
+    __syncwarp();
+    double* po = pinv + (size_t)b * stride;
+    if (lane < n) {
+      for (int i = 0; i < n; ++i) {
+        double sacc = 0.0;
+        for (int k = max(i, lane); k < n; ++k) sacc += xs[wib][k][i] * xs[wib][k][lane];
+        po[i * n + lane] = sacc;
+      }
+    }
+  }
+}
+
+// Leverage scores from a successful Cholesky: l_i = ||Linv a_i||^2.
+// grid = (ceil(max I / 128), modes); modes with ok == 0 are left to
+// k_leverage_rows (eigen path).
+__global__ void k_leverage_chol(const FactorSet fs, const double* linv, int stride, const int* ok,
+                                double* scores, const long long* score_off, int* ranks) {
+  const int mode = blockIdx.y;
+  if (!ok[mode]) return;
+  const int R = fs.cols[mode], I = fs.rows[mode];
+  if (blockIdx.x == 0 && threadIdx.x == 0) ranks[mode] = R;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= I) return;
+  const double* L = linv + (size_t)mode * stride;
+  const double* a = fs.ptr[mode] + (size_t)i * R;
+  double s = 0.0;
+  for (int r = 0; r < R; ++r) {
+    double y = 0.0;
+    for (int k = 0; k <= r; ++k) y += L[r * R + k] * a[k];
+    s += y * y;
+  }
+  scores[score_off[mode] + i] = s;
 }
 
 // ---------------------------------------------------------------------------
@@ -157,8 +396,9 @@ __global__ void k_sym_eigen(const double* in, const int* ns, int stride, double*
 // grid = (ceil(max I / 128), modes), block 128.
 __global__ void k_leverage_rows(const FactorSet fs, const double* evals, const double* evecs,
                                 int stride, double lambda, double* scores,
-                                const long long* score_off, int* ranks) {
+                                const long long* score_off, int* ranks, const int* skip) {
   const int mode = blockIdx.y;
+  if (skip && skip[mode]) return;
   const int R = fs.cols[mode], I = fs.rows[mode];
   const double* mu = evals + (size_t)mode * stride;
   const double* V = evecs + (size_t)mode * stride;
@@ -207,8 +447,9 @@ __global__ void k_score_cdf(const double* scores, const long long* off, const in
 // |mu_k| > n*eps*max|mu| (singular values of a symmetric matrix are |mu|).
 // grid = batch, block = 256. P stored row-major n x n at out + b*stride.
 __global__ void k_sym_pinv(const double* evals, const double* evecs, const int* ns, int stride,
-                           double* out, int* ranks) {
+                           double* out, int* ranks, const int* skip) {
   const int b = blockIdx.x;
+  if (skip && skip[b]) return;
   const int n = ns[b];
   const double* mu = evals + (size_t)b * stride;
   const double* V = evecs + (size_t)b * stride;
@@ -241,6 +482,33 @@ __global__ void k_rows_times_small(const double* M, const double* P, int I, int 
   double s = 0.0;
   for (int k = 0; k < R; ++k) s += M[(size_t)i * R + k] * P[k * R + r];
   out[e] = s;
+}
+
+void sym_eigen(const double* in, const int* ns_dev, int nmax, int stride, double* evals,
+               double* evecs, int* status, int nmat, cudaStream_t st, const int* skip) {
+  if (nmax <= 32) {
+    const int per_block = 4;
+    const size_t smem = (size_t)per_block * (2 * 32 * 33 + 64) * sizeof(double);
+    RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    k_sym_eigen_warp<<<ceil_div(nmat, per_block), 32 * per_block, smem, st>>>(
+        in, ns_dev, stride, evals, evecs, status, nmat, skip);
+  } else {
+    if (skip) throw Error(4, "eigen: skip flags need n <= 32");
+    if (nmax > 64) throw Error(4, "eigen: n > 64 not supported");
+    const int np = nmax + (nmax & 1);
+    const size_t smem = (2 * (size_t)np * (np + 1) + 2 * np) * 8;
+    RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (2 * 64 * 65 + 2 * 64) * 8));
+    k_sym_eigen<<<nmat, 128, smem, st>>>(in, ns_dev, stride, evals, evecs, status);
+  }
+  RTB_LAUNCH_CHECK();
+}
+
+void spd_small(const double* in, const int* ns_dev, int stride, double tolrel, double* linv,
+               double* pinv, int* ok, int nmat, cudaStream_t st) {
+  k_spd_small<<<ceil_div(nmat, 4), 128, 0, st>>>(in, ns_dev, stride, tolrel, linv, pinv, ok, nmat);
+  RTB_LAUNCH_CHECK();
 }
 
 }  // namespace rtb

@@ -297,6 +297,75 @@ __global__ void k_contract_except_scalar(const double* __restrict__ Y,
   M[e] = s;
 }
 
+// out[o,r,j] = sum_i A[i,r] X[o,i,j] for a short contiguous tail J (<= 32):
+// one block per o, i streamed in chunks of 32 through smem, one thread per
+// (r, j) output (R*J <= 1024).
+__global__ void __launch_bounds__(256) k_ttm_smallj(const double* __restrict__ X, int I, int J,
+                                                   const double* __restrict__ A, int R,
+                                                   double* __restrict__ out) {
+  __shared__ double xs[32][33];
+  __shared__ double as[32][33];
+  const long long o = blockIdx.x;
+  const double* Xo = X + o * (long long)I * J;
+  const int tid = threadIdx.x;
+  const int nout = R * J;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int i0 = 0; i0 < I; i0 += 32) {
+    __syncthreads();
+    for (int e = tid; e < 32 * 32; e += 256) {
+      const int ii = e >> 5, c = e & 31;
+      xs[ii][c] = (i0 + ii < I && c < J) ? Xo[(long long)(i0 + ii) * J + c] : 0.0;
+      as[ii][c] = (i0 + ii < I && c < R) ? A[(long long)(i0 + ii) * R + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * 256;
+      if (e < nout) {
+        const int r = e / J, j = e % J;
+        double sacc = acc[q];
+#pragma unroll 8
+        for (int ii = 0; ii < 32; ++ii) sacc += as[ii][r] * xs[ii][j];
+        acc[q] = sacc;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = tid + q * 256;
+    if (e < nout) out[o * nout + e] = acc[q];
+  }
+}
+
+// Up-projection out[o,i,j] = sum_r A[i,r] Y[o,r,j] (R small): Y[o] and the
+// block's A rows staged in smem; grid (ceil(I/ICH), O), threads over (i, j).
+__global__ void __launch_bounds__(256) k_ttm_expand(const double* __restrict__ Y, int R,
+                                                   long long J, const double* __restrict__ A,
+                                                   int I, int ich, double* __restrict__ out) {
+  extern __shared__ double ys[];  // R x J, then ich x R
+  double* as = ys + (long long)R * J;
+  const long long o = blockIdx.y;
+  const int i0 = blockIdx.x * ich;
+  const double* Yo = Y + o * R * J;
+  for (long long e = threadIdx.x; e < (long long)R * J; e += 256) ys[e] = Yo[e];
+  for (int e = threadIdx.x; e < ich * R; e += 256) {
+    const int ii = e / R;
+    as[e] = (i0 + ii < I) ? A[(long long)(i0 + ii) * R + e % R] : 0.0;
+  }
+  __syncthreads();
+  const long long n = (long long)ich * J;
+  for (long long e = threadIdx.x; e < n; e += 256) {
+    const int ii = (int)(e / J);
+    const long long j = e % J;
+    const int i = i0 + ii;
+    if (i >= I) continue;
+    const double* a = as + ii * R;
+    double sacc = 0.0;
+    for (int r = 0; r < R; ++r) sacc += a[r] * ys[(long long)r * J + j];
+    out[(o * I + i) * J + j] = sacc;
+  }
+}
+
 // Deterministic sum of per-block partials (fixed order), one block.
 __global__ void k_sum_partials(const double* __restrict__ partial, long long n,
                                double* __restrict__ out) {
@@ -393,6 +462,27 @@ void ttm_generic(const double* X, long long O, int I, long long J, const double*
   k_ttm_generic<<<(unsigned)ceil_div<long long>(total, 256), 256, 0, st>>>(X, O, I, J, W, wr, wi,
                                                                           R, out);
   RTB_LAUNCH_CHECK();
+}
+
+bool ttm_smallj(const double* X, long long O, int I, int J, const double* A, int R, double* out,
+                cudaStream_t st) {
+  if (R * J > 1024 || J > 32 || R > 32) return false;
+  k_ttm_smallj<<<(unsigned)O, 256, 0, st>>>(X, I, J, A, R, out);
+  RTB_LAUNCH_CHECK();
+  return true;
+}
+
+bool ttm_expand(const double* Y, long long O, int R, long long J, const double* A, int I,
+                double* out, cudaStream_t st) {
+  // enough blocks to fill the GPU: small O -> small i chunks
+  int ich = 16;
+  while (ich > 1 && O * ceil_div(I, ich) < 4 * kNumSMs) ich >>= 1;
+  const size_t smem = ((size_t)R * J + (size_t)ich * R) * sizeof(double);
+  if (smem > 48 * 1024 || O > 65535) return false;
+  k_ttm_expand<<<dim3((unsigned)ceil_div(I, ich), (unsigned)O), 256, smem, st>>>(Y, R, J, A, I,
+                                                                                 ich, out);
+  RTB_LAUNCH_CHECK();
+  return true;
 }
 
 void contract_except(const double* Y, const double* G, long long O, int I, int R, long long J,

@@ -18,13 +18,23 @@ struct FactorSet {
 __global__ void k_factor_gram(const FactorSet fs, double* grams, int r_max);
 __global__ void k_sym_eigen(const double* in, const int* ns, int stride, double* evals,
                             double* evecs, int* status);
+__global__ void k_sym_eigen_warp(const double* in, const int* ns, int stride, double* evals,
+                                 double* evecs, int* status, int nmat, const int* skip);
+// symmetric eigensolver dispatch: warp-per-matrix for n <= 32, else CTA (n <= 64)
+void sym_eigen(const double* in, const int* ns_dev, int nmax, int stride, double* evals,
+               double* evecs, int* status, int nmat, cudaStream_t st, const int* skip = nullptr);
 __global__ void k_leverage_rows(const FactorSet fs, const double* evals, const double* evecs,
                                 int stride, double lambda, double* scores,
-                                const long long* score_off, int* ranks);
+                                const long long* score_off, int* ranks, const int* skip);
+__global__ void k_leverage_chol(const FactorSet fs, const double* linv, int stride, const int* ok,
+                                double* scores, const long long* score_off, int* ranks);
+// batched small SPD Cholesky (n <= 32): Linv (+ optional P = M^-1), ok flags
+void spd_small(const double* in, const int* ns_dev, int stride, double tolrel, double* linv,
+               double* pinv, int* ok, int nmat, cudaStream_t st);
 __global__ void k_score_cdf(const double* scores, const long long* off, const int* rows,
                             int order, double* cdf, double* sums);
 __global__ void k_sym_pinv(const double* evals, const double* evecs, const int* ns, int stride,
-                           double* out, int* ranks);
+                           double* out, int* ranks, const int* skip);
 __global__ void k_rows_times_small(const double* M, const double* P, int I, int R, double* out);
 
 // ---- k_ttm.cu ----
@@ -38,6 +48,12 @@ void ttm_mid(const double* X, int O, int I, long long J, const double* A, int R,
 // out[o,r,j] = sum_i W[r*wr + i*wi] X[o,i,j]
 void ttm_generic(const double* X, long long O, int I, long long J, const double* W, long long wr,
                  long long wi, int R, double* out, cudaStream_t st);
+// out[o,r,j] = sum_i A[i,r] X[o,i,j], J <= 32 (returns false if not applicable)
+bool ttm_smallj(const double* X, long long O, int I, int J, const double* A, int R, double* out,
+                cudaStream_t st);
+// out[o,i,j] = sum_r A[i,r] Y[o,r,j] (returns false if not applicable)
+bool ttm_expand(const double* Y, long long O, int R, long long J, const double* A, int I,
+                double* out, cudaStream_t st);
 // M[i,r] = sum_{o,j} Y[o,i,j] G[o,r,j]
 void contract_except(const double* Y, const double* G, long long O, int I, int R, long long J,
                      double* M, cudaStream_t st);

@@ -201,11 +201,10 @@ def kernel_work(family, n_data, n_buckets):
     if family == "chol":
         return "tensor", "TFLOP/s", d ** 3 / 3 + 2 * d * d
     if family == "gram":
-        dp = d // RANKS[0]
-        tiles = -(-dp // 64)
-        tp = tiles * (tiles + 1) // 2
-        npair = RANKS[0] * (RANKS[0] + 1) // 2
-        return "tensor", "TFLOP/s", 2.0 * (n_data * tp * 4096 + n_buckets * npair * tp * 4096)
+        # vech-factored Gram: per data draw one rank-1 update of
+        # the i1-bucket's H_b (vech(R2) x vech(R3)), then S = V1^T H over buckets.
+        v = [r * (r + 1) // 2 for r in RANKS]
+        return "tensor", "TFLOP/s", 2.0 * (n_data * v[1] * v[2] + n_buckets * v[0] * v[1] * v[2])
     if family in ("ttm_last_loss", "ttm_last", "ttm_mid"):
         return "hbm", "GB/s", 8.0 * total
     return None, None, None

@@ -24,9 +24,12 @@
 
 struct rtucker_tensor {
   std::vector<uint64_t> shape;
-  std::vector<double> host;  // empty for device-only tensors
-  bool has_host = true;
-  mutable rtb::DevBuf dev;   // resident copy, uploaded on first use
+  // Two copies, each materialised on demand: tensors created from host data are
+  // uploaded (and checked) at creation when a GPU is present, and the host copy is only
+  // downloaded again if rtucker_tensor_data / rtucker_tensor_write ask for it.
+  mutable std::vector<double> host;
+  mutable bool host_valid = true;
+  mutable rtb::DevBuf dev;
   mutable bool dev_valid = false;
   uint64_t size() const {
     uint64_t s = 1;
@@ -41,6 +44,16 @@ struct rtucker_tensor {
       dev_valid = true;
     }
     return dev.as<double>();
+  }
+  const double* host_data() const {
+    if (!host_valid) {
+      cudaStream_t st = rtb::current_stream();
+      host.resize(size());
+      RTB_CUDA(cudaMemcpyAsync(host.data(), dev.p, size() * 8, cudaMemcpyDeviceToHost, st));
+      RTB_CUDA(cudaStreamSynchronize(st));
+      host_valid = true;
+    }
+    return host.data();
   }
 };
 
@@ -191,10 +204,19 @@ rtucker_status rtucker_tensor_create(const uint64_t* shape, uint32_t order, cons
   if (!shape || !data || !out) return fail(RTUCKER_ERR_INVALID_ARGUMENT, "null argument");
   return guarded([&] {
     const uint64_t v = checked_volume(shape, order);
-    check_finite(data, v, "DenseTensor");
     auto t = std::make_unique<rtucker_tensor>();
     t->shape.assign(shape, shape + order);
-    t->host.assign(data, data + v);
+    if (rtb::cuda_device_present()) {
+      // the copy the reference makes (ref tensor.cpp:32-42) goes straight to HBM
+      cudaStream_t st = rtb::current_stream();
+      t->dev.ensure(v * 8, st);
+      rtb::upload_checked(t->dev.as<double>(), data, v, st, "DenseTensor");
+      t->dev_valid = true;
+      t->host_valid = false;
+    } else {
+      check_finite(data, v, "DenseTensor");
+      t->host.assign(data, data + v);
+    }
     *out = t.release();
   });
 }
@@ -285,14 +307,14 @@ rtucker_status rtucker_tensor_read_csv(const char* path, rtucker_tensor** out) {
 rtucker_status rtucker_tensor_write(const rtucker_tensor* t, const char* path) {
   if (!t || !path) return fail(RTUCKER_ERR_INVALID_ARGUMENT, "null argument");
   return guarded([&] {
-    if (!t->has_host) throw rtb::Error(1, "tensor has no host copy (device-only)");
+    const double* hd = t->host_data();
     std::ofstream o(path, std::ios::binary | std::ios::trunc);
     if (!o) throw std::runtime_error(std::string("write_tensor: cannot open ") + path);
     o.write("DTEN", 4);
     wr<uint8_t>(o, 1);
     wr<uint32_t>(o, (uint32_t)t->shape.size());
     for (auto d : t->shape) wr<uint64_t>(o, d);
-    o.write(reinterpret_cast<const char*>(t->host.data()), (std::streamsize)(t->size() * 8));
+    o.write(reinterpret_cast<const char*>(hd), (std::streamsize)(t->size() * 8));
     if (!o) throw std::runtime_error(std::string("write_tensor: write failed for ") + path);
   });
 }
@@ -311,11 +333,12 @@ uint64_t rtucker_tensor_size(const rtucker_tensor* t) { return t ? t->size() : 0
 
 const double* rtucker_tensor_data(const rtucker_tensor* t) {
   if (!t) return nullptr;
-  if (!t->has_host) {
-    fail(RTUCKER_ERR_INVALID_ARGUMENT, "tensor has no host copy (device-only)");
+  try {
+    return t->host_data();
+  } catch (const std::exception& e) {
+    fail(RTUCKER_ERR_UNKNOWN, e.what());
     return nullptr;
   }
-  return t->host.data();
 }
 
 void rtucker_tensor_free(rtucker_tensor* t) { delete t; }
@@ -658,7 +681,7 @@ rtucker_status rtucker_b200_tensor_create_device(const uint64_t* shape, uint32_t
     const uint64_t v = checked_volume(shape, order);
     auto t = std::make_unique<rtucker_tensor>();
     t->shape.assign(shape, shape + order);
-    t->has_host = false;
+    t->host_valid = false;
     cudaStream_t st = rtb::current_stream();
     t->dev.ensure(v * 8, st);
     RTB_CUDA(cudaMemcpyAsync(t->dev.p, data_device, v * 8, cudaMemcpyDeviceToDevice, st));

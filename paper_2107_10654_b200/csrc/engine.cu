@@ -201,6 +201,20 @@ __global__ void k_check_finite(const double* v, long long n, int* bad) {
   if (i < n && !isfinite(v[i])) atomicExch(bad, 1);
 }
 
+// Grid-stride finiteness scan (exponent field all ones = Inf/NaN), 2 doubles per load.
+__global__ void k_all_finite(const double* v, long long n, int* bad) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  int hit = 0;
+  const long long n2 = n >> 1;
+  const double2* v2 = reinterpret_cast<const double2*>(v);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const double2 a = __ldcs(v2 + i);
+    hit |= !isfinite(a.x) | !isfinite(a.y);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) hit |= !isfinite(v[n - 1]);
+  if (__syncthreads_or(hit) && threadIdx.x == 0) atomicExch(bad, 1);
+}
+
 // ---------------------------------------------------------------------------
 // profiling (optional per-kernel-family device time)
 
@@ -268,6 +282,37 @@ static uint64_t prod(const std::vector<uint64_t>& v, size_t from = 0, size_t to 
   uint64_t p = 1;
   for (size_t i = from; i < v.size() && i < to; ++i) p *= v[i];
   return p;
+}
+
+bool cuda_device_present() {
+  static const bool present = [] {
+    int n = 0;
+    const bool ok = cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+    cudaGetLastError();
+    return ok;
+  }();
+  return present;
+}
+
+void upload_checked(double* dst, const double* src, uint64_t n, cudaStream_t st,
+                    const char* what) {
+  RTB_CUDA(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyHostToDevice, st));
+  DevBuf flag;
+  flag.ensure(4, st);
+  RTB_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
+  int sms = 148;
+  int dev = 0;
+  RTB_CUDA(cudaGetDevice(&dev));
+  RTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const long long blocks = std::max<long long>(1, std::min<long long>(sms * 4LL, ceil_div<long long>((long long)n / 2 + 1, 256)));
+  if (n) {
+    k_all_finite<<<(unsigned)blocks, 256, 0, st>>>(dst, (long long)n, flag.as<int>());
+    RTB_LAUNCH_CHECK();
+  }
+  int bad = 0;
+  RTB_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  if (bad) throw Error(1, std::string(what) + ": non-finite entry");
 }
 
 uint64_t sample_count_formula(double beta_prime, uint64_t d, double epsilon, double delta) {

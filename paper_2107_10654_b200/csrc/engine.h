@@ -137,6 +137,11 @@ void dense_sketched_ridge(const double* a, uint64_t n, uint64_t d, const double*
                           double delta, uint64_t s_override, uint64_t seed, double* x,
                           uint64_t* s_out, double* beta_out);
 
+// True when at least one CUDA device is visible (cached).
+bool cuda_device_present();
+// H2D copy of n doubles on st, then a device-side finiteness scan; synchronises st and
+// throws Error(1, "<what>: non-finite entry") like ref tensor.cpp:32-42.
+void upload_checked(double* dst, const double* src, uint64_t n, cudaStream_t st, const char* what);
 uint64_t sample_count_formula(double beta_prime, uint64_t d, double eps, double delta);
 
 }  // namespace rtb

@@ -31,6 +31,9 @@ def build(ref: bool = True) -> None:
     targets = ["oracle"]
     if ref and os.path.isdir("/root/reference/proj"):
         targets.append("ref")
+        lib = os.path.join(HERE, "..", "paper_2107_10654_b200", "lib", "librtucker_b200.so")
+        if os.path.exists(lib):
+            targets.append("capi_test")  # the reference's test_capi.cpp against our library
     subprocess.check_call(["make", "-s", "-C", HERE] + targets)
 
 

@@ -60,7 +60,11 @@ typedef struct rtucker_b200_als_ext {
   /* 1 = record per-kernel-family device time (CUDA events on the run's
    * stream), exported by rtucker_b200_result_kernel_row. */
   int profile_kernels;
-  int reserved[7];
+  /* Sketched-core solver: 0 = auto (Kronecker-preconditioned CG when lambda > 0,
+   * every augmented row was drawn and d fits, verified by its true residual;
+   * Cholesky otherwise or on failure), 1 = always Cholesky. */
+  int core_solver;
+  int reserved[6];
 } rtucker_b200_als_ext;
 
 rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* ranks,
@@ -98,6 +102,9 @@ rtucker_status rtucker_b200_result_sketch_info(const rtucker_als_result* r,
                                                uint64_t* sample_count,
                                                uint64_t* data_draws,
                                                int* rank_deficient, int* solver_path);
+/* solver_path: 0 Cholesky, 1 eigen/pinv fallback (d <= 64), 2 preconditioned CG.
+ * CG iterations of the last sketched core solve (0 if CG was not used). */
+int rtucker_b200_result_pcg_iterations(const rtucker_als_result* r);
 
 /* Per-kernel device time accumulated over a run (CUDA events on the run's
  * stream). name_buf receives the kernel family name. */

@@ -433,6 +433,7 @@ rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* 
       o.allreduce = ext->allreduce;
       o.allreduce_user = ext->allreduce_user;
       o.profile = ext->profile_kernels != 0;
+      o.core_solver = ext->core_solver;
     }
     auto r = std::make_unique<rtucker_als_result>();
     rtb::als_run(x->device(), x->shape, std::vector<uint64_t>(ranks, ranks + order), o, r->out);
@@ -466,6 +467,7 @@ rtucker_status rtucker_b200_session_create(const rtucker_tensor* x, const uint64
       o.allreduce = ext->allreduce;
       o.allreduce_user = ext->allreduce_user;
       o.profile = ext->profile_kernels != 0;
+      o.core_solver = ext->core_solver;
     }
     auto s = std::make_unique<rtucker_b200_session>();
     s->s.reset(rtb::session_create(x->device(), x->shape,
@@ -743,6 +745,10 @@ rtucker_status rtucker_b200_result_sketch_info(const rtucker_als_result* r, uint
   if (rank_deficient) *rank_deficient = r->out.last_rank_deficient;
   if (solver_path) *solver_path = r->out.last_solver_path;
   return RTUCKER_OK;
+}
+
+int rtucker_b200_result_pcg_iterations(const rtucker_als_result* r) {
+  return r ? r->out.last_pcg_iterations : 0;
 }
 
 uint64_t rtucker_b200_result_kernel_count(const rtucker_als_result* r) {

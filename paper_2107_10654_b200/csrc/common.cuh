@@ -34,6 +34,20 @@ unsigned long long& launch_counter();
 constexpr int kNumSMs = 148;
 constexpr int kMaxOrder = 8;
 
+// vech index of the unordered pair (a <= b) among n items (row-major upper
+// triangle) and its inverse; the Gram of Kronecker rows is indexed by these.
+__host__ __device__ __forceinline__ int upper_pair(int a, int b, int n) {
+  return a * n - a * (a - 1) / 2 + (b - a);
+}
+__host__ __device__ __forceinline__ void pair_of(int u, int n, int& a, int& b) {
+  a = 0;
+  while (u >= n - a) {
+    u -= n - a;
+    ++a;
+  }
+  b = a + u;
+}
+
 // ---- SplitMix64 (ref rng.hpp:12-62) in counter form: output k of a stream
 // seeded with `seed` is mix(seed + (k+1)*gamma). ----
 constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ULL;

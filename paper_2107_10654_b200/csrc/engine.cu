@@ -459,6 +459,7 @@ class Engine {
     RTB_CUDA(cudaMemcpy(&out.last_data_draws, data_draws_.p, 8, cudaMemcpyDeviceToHost));
     out.last_rank_deficient = last_rank_deficient_;
     out.last_solver_path = last_solver_path_;
+    out.last_pcg_iterations = last_pcg_iters_;
     out.sweep_seconds = sweep_seconds_;
   }
 
@@ -529,11 +530,11 @@ class Engine {
   DevBuf T_, P_, tmp_a_, tmp_b_, partial_, scal_, hist_, init_loss_;
   DevBuf scores_, cdf_, sums_, score_off_, rows_dev_, cols_dev_, flag_;
   DevBuf sk_idx_, sk_w_, draw_work_, gram_work_, G_, rhs_, chol_work_, chol_status_,
-      data_draws_, zero_flag_, U_[8];
+      data_draws_, zero_flag_, U_[8], pev_, pvec_, pst_, pcg_work_, pcg_status_, blocks_;
   uint64_t sketch_rng_ = 0, sketch_k_ = 0;
   bool t_valid_ = false;
   uint64_t last_s_ = 0;
-  int last_rank_deficient_ = 0, last_solver_path_ = 0;
+  int last_rank_deficient_ = 0, last_solver_path_ = 0, last_pcg_iters_ = 0;
   struct StepEv {
     int step;
     cudaEvent_t a, b;
@@ -584,6 +585,10 @@ class Engine {
       RTB_CUDA(cudaMemcpy(ns_vals_.p, vals, 65 * 4, cudaMemcpyHostToDevice));
     }
     eig_status_.ensure(64 * 4, st_);
+    pev_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
+    pvec_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
+    pst_.ensure(64 * 4, st_);
+    pcg_status_.ensure(16, st_);
     ns_.ensure(64 * 4, st_);
     ranks_dev_.ensure(64 * 4, st_);
     // T and P: (total / I_N) x R_N
@@ -900,17 +905,61 @@ class Engine {
   void solve_sketch(uint64_t s) {
     GramSpec gs = gram_spec(s);
     gram_work_.ensure(gram_work_bytes(gs), st_);
-    G_.ensure(d_ * d_ * 8, st_);
     rhs_.ensure(d_ * 8, st_);
-    {
+    int rk[8];
+    for (int n = 0; n < N_; ++n) rk[n] = (int)ranks_[n];
+    const bool try_pcg = opt_.core_solver == 0 && opt_.lambda > 0.0 && opt_.shard_count <= 1 &&
+                         pcg_supported((int)d_, N_, rk);
+    auto normal_eq = [&](bool full) {
       Scope sc(prof_, "gram");
+      if (full) G_.ensure(d_ * d_ * 8, st_);
       sketch_normal_eq(gs, x_, (const unsigned long long*)sk_idx_.p, sk_w_.as<double>(),
-                       gram_work_.p, gram_work_.bytes, G_.as<double>(), rhs_.as<double>(),
-                       (unsigned long long*)data_draws_.p, st_);
-    }
-    if (opt_.allreduce && opt_.shard_count > 1) {
-      opt_.allreduce(G_.as<double>(), d_ * d_, st_, opt_.allreduce_user);
-      opt_.allreduce(rhs_.as<double>(), d_, st_, opt_.allreduce_user);
+                       gram_work_.p, gram_work_.bytes, full ? G_.as<double>() : nullptr,
+                       rhs_.as<double>(), (unsigned long long*)data_draws_.p, st_);
+      if (full && opt_.allreduce && opt_.shard_count > 1) {
+        opt_.allreduce(G_.as<double>(), d_ * d_, st_, opt_.allreduce_user);
+        opt_.allreduce(rhs_.as<double>(), d_, st_, opt_.allreduce_user);
+      }
+    };
+    normal_eq(!try_pcg);
+    int status[2] = {0, 0};
+    if (try_pcg) {
+      // Kronecker-preconditioned CG on the blocked Gram (k_pcg.cu), verified by its
+      // true residual; the Cholesky path below is the fallback
+      Scope sc(prof_, "pcg");
+      blocks_.ensure((size_t)gram_block_elems(gs) * 8, st_);
+      gram_expand_blocks(gs, gram_work_.p, blocks_.as<double>(), st_);
+      sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, pev_.as<double>(),
+                pvec_.as<double>(), pst_.as<int>(), N_, st_);
+      PcgSpec ps{};
+      ps.order = N_;
+      for (int n = 0; n < N_; ++n) ps.ranks[n] = rk[n];
+      ps.d = (int)d_;
+      ps.lambda = opt_.lambda;
+      ps.evals = pev_.as<double>();
+      ps.evecs = pvec_.as<double>();
+      ps.eig_stride = eig_stride_;
+      ps.aug_count = gram_aug_counts(gs, gram_work_.p);
+      ps.aug_term = gram_aug_term(gs);
+      ps.max_iter = 200;
+      ps.tol = 1e-14;
+      ps.check_tol = 1e-11;
+      pcg_work_.ensure(pcg_work_bytes((int)d_, rk[0]), st_);
+      pcg_solve(ps, blocks_.as<double>(), rhs_.as<double>(), core_.as<double>(), pcg_work_.p,
+                pcg_status_.as<int>(), st_);
+      int ps_out[2] = {1, 0};
+      RTB_CUDA(cudaMemcpyAsync(ps_out, pcg_status_.p, 8, cudaMemcpyDeviceToHost, st_));
+      RTB_CUDA(cudaMemcpyAsync(&status[1], zero_flag_.p, 4, cudaMemcpyDeviceToHost, st_));
+      RTB_CUDA(cudaStreamSynchronize(st_));
+      last_pcg_iters_ = ps_out[1];
+      if (ps_out[0] == 0 && !status[1]) {
+        last_solver_path_ = 2;
+        last_rank_deficient_ = 0;
+        check_core_finite();
+        return;
+      }
+      G_.ensure(d_ * d_ * 8, st_);
+      gram_expand_full(gs, gram_work_.p, G_.as<double>(), st_);
     }
     chol_work_.ensure(chol_work_bytes((int)d_), st_);
     {
@@ -918,7 +967,6 @@ class Engine {
       chol_solve(G_.as<double>(), (int)d_, rhs_.as<double>(), chol_status_.as<int>(),
                  chol_work_.p, st_);
     }
-    int status[2] = {0, 0};
     RTB_CUDA(cudaMemcpyAsync(&status[0], chol_status_.p, 4, cudaMemcpyDeviceToHost, st_));
     RTB_CUDA(cudaMemcpyAsync(&status[1], zero_flag_.p, 4, cudaMemcpyDeviceToHost, st_));
     RTB_CUDA(cudaStreamSynchronize(st_));

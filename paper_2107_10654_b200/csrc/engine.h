@@ -50,6 +50,7 @@ struct AlsOptions {
   uint32_t shard_rank = 0, shard_count = 1;
   void (*allreduce)(double*, uint64_t, void*, void*) = nullptr;
   void* allreduce_user = nullptr;
+  int core_solver = 0;                    // 0 auto (PCG, Cholesky fallback), 1 Cholesky
 };
 
 struct HistoryRow {
@@ -80,7 +81,7 @@ struct AlsOutput {
   double final_loss = 0.0, final_rmse = 0.0;
   bool converged = false;
   uint64_t last_sample_count = 0, last_data_draws = 0;
-  int last_rank_deficient = 0, last_solver_path = 0;
+  int last_rank_deficient = 0, last_solver_path = 0, last_pcg_iterations = 0;
   double sweep_seconds = 0.0;  // device time of the sweep loop
 };
 

@@ -170,23 +170,31 @@ GramLayout layout(const GramSpec& spec, void* base) {
   return l;
 }
 
-// pair index of (a <= b) among n items, row-major upper triangle
-__host__ __device__ __forceinline__ int upper_pair(int a, int b, int n) {
-  return a * n - a * (a - 1) / 2 + (b - a);
-}
-// inverse of upper_pair
-__device__ __forceinline__ void pair_of(int u, int n, int& a, int& b) {
-  a = 0;
-  while (u >= n - a) {
-    u -= n - a;
-    ++a;
-  }
-  b = a + u;
-}
 }  // namespace
 
 size_t gram_work_bytes(const GramSpec& spec) {
   return carve(spec, [](size_t, size_t) {});
+}
+
+const int* gram_aug_counts(const GramSpec& spec, void* work) {
+  return layout(spec, work).aug_count;
+}
+
+double gram_aug_term(const GramSpec& spec) {
+  // augmented rows: each adds (w^2 sqrt(lambda)) sqrt(lambda) to its diagonal,
+  // w = sqrt((1/s) / (0.5/d)) (ref sketch_ridge.cpp:88, 18-36, 115-120)
+  const double inv_s = 1.0 / (double)spec.s;
+  const double prob = (1.0 - 0.5) / (double)spec.d;
+  const double wa = std::sqrt(inv_s / prob);
+  const double rl = std::sqrt(spec.lambda);
+  return (wa * wa * rl) * rl;
+}
+
+long long gram_block_elems(const GramSpec& spec) {
+  const VechSpec v = make_vech(spec);
+  long long n = (long long)v.R[v.N - 1] * v.R[v.N - 1];
+  for (int k = 0; k < v.N - 1; ++k) n *= v.m[k];
+  return n;
 }
 
 // (A) keys, augmented-row histogram, data-draw count.
@@ -536,6 +544,32 @@ __global__ void k_vech_expand(GramSpec spec, VechSpec v, const double* __restric
   }
 }
 
+// (D') the Gram in "last-mode blocks": B[u_1..u_{N-1}][r][c] = G entry whose
+// first N-1 modes have vech pairs u_n and whose last-mode indices are (r, c).
+// prod_{n<N} m_n blocks of R_N x R_N (C2: 136^2 x 16^2 doubles = 38 MB, vs
+// 134 MB for the full Gram); consumed by the CG matvec (k_pcg.cu).
+__global__ void k_vech_blocks(GramSpec spec, VechSpec v, const double* __restrict__ S,
+                              double* __restrict__ B, long long total) {
+  const int N = v.N, RL = v.R[N - 1];
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e % RL);
+    long long t = e / RL;
+    const int r = (int)(t % RL);
+    t /= RL;
+    int un[kMaxOrder];
+    un[N - 1] = upper_pair(min(r, c), max(r, c), RL);
+    for (int n = N - 2; n >= 0; --n) {
+      un[n] = (int)(t % v.m[n]);
+      t /= v.m[n];
+    }
+    long long ur = 0, uc = 0;
+    for (int n = 1; n <= v.msplit && n < N; ++n) ur = ur * v.m[n] + un[n];
+    for (int n = v.msplit + 1; n < N; ++n) uc = uc * v.m[n] + un[n];
+    B[e] = S[(size_t)un[0] * v.Hsz + ur * v.Ncol + uc];
+  }
+}
+
 // (E) rhs[p1 * d' + p'] = sum_b A1[i1_b, p1] h[b, p'].
 // grid = (ceil(d'/64), R1); 64 outputs x 4 bucket groups per block.
 __global__ void __launch_bounds__(256) k_rhs(GramSpec spec, const double* __restrict__ h,
@@ -592,15 +626,28 @@ void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
   RTB_LAUNCH_CHECK();
   // augmented rows: each adds (w^2 sqrt(lambda)) sqrt(lambda) to its diagonal,
   // w = sqrt((1/s) / (0.5/d)) (ref sketch_ridge.cpp:88, 18-36, 115-120)
-  const double inv_s = 1.0 / (double)spec.s;
-  const double prob = (1.0 - 0.5) / (double)spec.d;
-  const double wa = std::sqrt(inv_s / prob);
-  const double rl = std::sqrt(spec.lambda);
-  const double aug_term = (wa * wa * rl) * rl;
-  k_vech_expand<<<kNumSMs * 8, 256, 0, st>>>(spec, v, l.S, l.aug_count, aug_term, gram);
-  RTB_LAUNCH_CHECK();
+  const double aug_term = gram_aug_term(spec);
+  if (gram) {
+    k_vech_expand<<<kNumSMs * 8, 256, 0, st>>>(spec, v, l.S, l.aug_count, aug_term, gram);
+    RTB_LAUNCH_CHECK();
+  }
   k_rhs<<<dim3(ceil_div(spec.dprime, 64), spec.ranks[0]), 256, 0, st>>>(spec, l.h, l.bi1,
                                                                         l.nbuckets, rhs);
+  RTB_LAUNCH_CHECK();
+}
+
+void gram_expand_full(const GramSpec& spec, void* work, double* gram, cudaStream_t st) {
+  const VechSpec v = make_vech(spec);
+  GramLayout l = layout(spec, work);
+  k_vech_expand<<<kNumSMs * 8, 256, 0, st>>>(spec, v, l.S, l.aug_count, gram_aug_term(spec), gram);
+  RTB_LAUNCH_CHECK();
+}
+
+void gram_expand_blocks(const GramSpec& spec, void* work, double* blocks, cudaStream_t st) {
+  const VechSpec v = make_vech(spec);
+  GramLayout l = layout(spec, work);
+  const long long total = gram_block_elems(spec);
+  k_vech_blocks<<<kNumSMs * 8, 256, 0, st>>>(spec, v, l.S, blocks, total);
   RTB_LAUNCH_CHECK();
 }
 

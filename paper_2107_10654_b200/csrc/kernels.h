@@ -93,10 +93,43 @@ struct GramSpec {
   unsigned long long s;
 };
 size_t gram_work_bytes(const GramSpec& spec);
-// Sketched normal equations from (idx, w): full d x d Gram + rhs.
+// Sketched normal equations from (idx, w): rhs, the compact (vech) Gram in the
+// workspace and, if gram != nullptr, the full d x d Gram.
 void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long long* idx,
                       const double* w, void* work, size_t work_bytes, double* gram,
                       double* rhs, unsigned long long* data_draws_dev, cudaStream_t st);
+
+// augmented-row draw counts [d] inside a gram workspace (valid after sketch_normal_eq)
+const int* gram_aug_counts(const GramSpec& spec, void* work);
+// diagonal term each augmented draw adds
+double gram_aug_term(const GramSpec& spec);
+// full Gram / last-mode blocks (data part only) from the workspace's compact Gram
+void gram_expand_full(const GramSpec& spec, void* work, double* gram, cudaStream_t st);
+long long gram_block_elems(const GramSpec& spec);
+void gram_expand_blocks(const GramSpec& spec, void* work, double* blocks, cudaStream_t st);
+
+// ---- k_pcg.cu ----
+struct PcgSpec {
+  int order;
+  int ranks[8];
+  int d;
+  double lambda;
+  const double* evals;  // per mode (stride eig_stride): eigenvalues of A_n^T A_n
+  const double* evecs;  // per mode: V[i*R+k], column k = eigenvector k
+  int eig_stride;
+  const int* aug_count; // [d] augmented draws per column (any 0 -> status 3)
+  double aug_term;      // diagonal added per augmented draw
+  int max_iter;
+  double tol;           // stop when ||r_k|| <= tol ||b|| (recursive residual)
+  double check_tol;     // accept when ||b - G x|| <= check_tol ||b||
+};
+size_t pcg_work_bytes(int d, int r1);
+bool pcg_supported(int d, int order, const int* ranks);
+// x = G^-1 b by Kronecker-preconditioned CG; status_dev[0] = 0 ok, 1 residual check
+// failed, 2 breakdown (non-SPD), 3 not applicable; status_dev[1] = iterations.
+// G is given as its last-mode blocks (gram_expand_blocks) + augmented diagonal.
+void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, double* x, void* work,
+               int* status_dev, cudaStream_t st);
 
 // ---- k_chol.cu ----
 size_t chol_work_bytes(int d);

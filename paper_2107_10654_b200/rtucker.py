@@ -61,7 +61,8 @@ class AlsExt(C.Structure):
         ("allreduce_user", C.c_void_p),
         ("async_sweeps_when_no_tolerance", C.c_int),
         ("profile_kernels", C.c_int),
-        ("reserved", C.c_int * 7),
+        ("core_solver", C.c_int),
+        ("reserved", C.c_int * 6),
     ]
 
 
@@ -133,6 +134,7 @@ def _load() -> C.CDLL:
                                           C.POINTER(_vp)]),
         "rtucker_b200_result_sketch_info": (S, [_vp, _u64p, _u64p, C.POINTER(C.c_int),
                                                 C.POINTER(C.c_int)]),
+        "rtucker_b200_result_pcg_iterations": (C.c_int, [_vp]),
         "rtucker_b200_result_kernel_count": (C.c_uint64, [_vp]),
         "rtucker_b200_result_kernel_row": (S, [_vp, C.c_uint64, C.c_char_p, C.c_size_t, _f64p,
                                                _u64p]),
@@ -336,7 +338,8 @@ class Result:
         _check(lib.rtucker_b200_result_sketch_info(self.h, C.byref(s), C.byref(dd), C.byref(rd),
                                                    C.byref(sp)))
         return {"sample_count": s.value, "data_draws": dd.value, "rank_deficient": rd.value,
-                "solver_path": sp.value}
+                "solver_path": sp.value,
+                "pcg_iterations": lib.rtucker_b200_result_pcg_iterations(self.h)}
 
     @property
     def final_loss(self) -> float:
@@ -383,8 +386,9 @@ class Result:
             pass
 
 
-def _ext(init_model: Model | None = None, profile: bool = False):
+def _ext(init_model: Model | None = None, profile: bool = False, core_solver: int = 0):
     ext = AlsExt()
+    ext.core_solver = int(core_solver)
     keep = []
     if init_model is not None:
         core = _f64(init_model.core).ravel()
@@ -397,15 +401,15 @@ def _ext(init_model: Model | None = None, profile: bool = False):
 
 
 def als_run(x: Tensor, ranks, opts: AlsOptions | None = None, init_model: Model | None = None,
-            profile: bool = False) -> Result:
+            profile: bool = False, core_solver: int = 0) -> Result:
     """rtucker_als_run (ref capi.cpp:176-201); extensions via rtucker_b200_als_run_ex."""
     opts = opts or options()
     ranks = _u64(ranks)
     r = _vp()
-    if init_model is None and not profile:
+    if init_model is None and not profile and not core_solver:
         _check(lib.rtucker_als_run(x.h, _p(ranks), len(ranks), C.byref(opts), C.byref(r)))
     else:
-        ext, keep = _ext(init_model, profile)
+        ext, keep = _ext(init_model, profile, core_solver)
         _check(lib.rtucker_b200_als_run_ex(x.h, _p(ranks), len(ranks), C.byref(opts),
                                            C.byref(ext), C.byref(r)))
         del keep
@@ -416,11 +420,11 @@ class Session:
     """Step-wise run (rtucker_b200_session_*): init at construction, sweeps on demand."""
 
     def __init__(self, x: Tensor, ranks, opts: AlsOptions | None = None,
-                 init_model: Model | None = None, profile: bool = False):
+                 init_model: Model | None = None, profile: bool = False, core_solver: int = 0):
         self.shape = x.shape
         opts = opts or options()
         ranks = _u64(ranks)
-        ext, self._keep = _ext(init_model, profile)
+        ext, self._keep = _ext(init_model, profile, core_solver)
         self.h = _vp()
         _check(lib.rtucker_b200_session_create(x.h, _p(ranks), len(ranks), C.byref(opts),
                                                C.byref(ext), C.byref(self.h)))

@@ -266,3 +266,27 @@ def test_rejects_bad_ranks(rt):
     with pytest.raises(rt.RtuckerError) as e:
         rt.als_run(x, (5, 2))
     assert e.value.code == rt.ERR_INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("shape,ranks,lam,s", [((40, 36, 32), (6, 5, 4), 1e-2, 8000),
+                                               ((48, 48, 48), (12, 12, 12), 1e-2, 60000),
+                                               ((20, 18, 16, 14), (4, 3, 3, 2), 1e-3, 6000),
+                                               ((64, 60), (9, 7), 1e-2, 3000)])
+def test_pcg_core_solve_matches_cholesky_and_oracle(oracle, rt, shape, ranks, lam, s):
+    """Sketched core by Kronecker-preconditioned CG (solver_path 2) vs the Cholesky
+    path (core_solver=1) and the reference restatement, sweep by sweep."""
+    x = planted(shape, ranks, seed=31)
+    kw = dict(lam=lam, sketched_core=1, max_iterations=3, tolerance=0.0,
+              sample_count_override=s, record_history=1, seed=9)
+    xt = rt.Tensor.from_numpy(x)
+    rp = rt.als_run(xt, ranks, rt.options(**kw))
+    rc = rt.als_run(xt, ranks, rt.options(**kw), core_solver=1)
+    assert rp.sketch_info()["solver_path"] == 2
+    assert rp.sketch_info()["pcg_iterations"] > 0
+    assert rc.sketch_info()["solver_path"] == 0
+    o = oracle.als(x, ranks, **kw)
+    for hp, hc, ho in zip(rp.history(), rc.history(), o["history"]):
+        assert abs(hp[2] - hc[2]) / hc[2] < 1e-9, hp[:2]
+        assert abs(hp[2] - ho[2]) / ho[2] < 1e-6, hp[:2]
+    mp, mc = rp.model(), rc.model()
+    assert np.linalg.norm(mp.core - mc.core) / np.linalg.norm(mc.core) < 1e-7

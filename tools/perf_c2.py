@@ -12,6 +12,7 @@ shape = tuple(int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "512,512,51
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 s = int(sys.argv[3]) if len(sys.argv) > 3 else 200000
 sweeps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+solver = int(sys.argv[5]) if len(sys.argv) > 5 else 0
 ranks = (R,) * len(shape)
 g = torch.Generator(device="cuda").manual_seed(0)
 core = torch.randn(ranks, dtype=torch.float64, device="cuda", generator=g)
@@ -27,7 +28,7 @@ t = rt.Tensor.from_device(x.data_ptr(), shape)
 opts = rt.options(lam=1e-2, sketched_core=1, sample_count_override=s, tolerance=0.0,
                   max_iterations=sweeps + 1)
 t0 = time.time()
-sess = rt.Session(t, ranks, opts, profile=True)
+sess = rt.Session(t, ranks, opts, profile=True, core_solver=solver)
 sess.sweeps(1)
 torch.cuda.synchronize()
 t1 = time.time()
@@ -37,7 +38,7 @@ t2 = time.time()
 r = sess.result()
 print(f"shape {shape} R {R} s {s}: warm {t1 - t0:.3f}s, {sweeps} sweeps wall {t2 - t1:.4f}s "
       f"-> {sweeps / (t2 - t1):.2f} sweeps/s; device sweep_seconds {r.sweep_seconds:.4f}")
-print("history:", [(h[1], round(h[2], 6)) for h in r.history()][-4:])
+print("solver", solver, "final loss %.17g" % r.final_loss)
 print("sketch:", r.sketch_info())
 tot = sum(k[1] for k in r.kernels())
 for name, secs, n in sorted(r.kernels(), key=lambda k: -k[1]):

@@ -909,7 +909,7 @@ class Engine {
     int rk[8];
     for (int n = 0; n < N_; ++n) rk[n] = (int)ranks_[n];
     const bool try_pcg = opt_.core_solver == 0 && opt_.lambda > 0.0 && opt_.shard_count <= 1 &&
-                         pcg_supported((int)d_, N_, rk);
+                         rmax_ <= 32 && pcg_supported((int)d_, N_, rk);
     auto normal_eq = [&](bool full) {
       Scope sc(prof_, "gram");
       if (full) G_.ensure(d_ * d_ * 8, st_);
@@ -929,21 +929,20 @@ class Engine {
       Scope sc(prof_, "pcg");
       blocks_.ensure((size_t)gram_block_elems(gs) * 8, st_);
       gram_expand_blocks(gs, gram_work_.p, blocks_.as<double>(), st_);
-      sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, pev_.as<double>(),
-                pvec_.as<double>(), pst_.as<int>(), N_, st_);
       PcgSpec ps{};
       ps.order = N_;
       for (int n = 0; n < N_; ++n) ps.ranks[n] = rk[n];
       ps.d = (int)d_;
       ps.lambda = opt_.lambda;
-      ps.evals = pev_.as<double>();
-      ps.evecs = pvec_.as<double>();
-      ps.eig_stride = eig_stride_;
+      ps.linv = linv_.as<double>();   // factor-Gram Cholesky of the score step
+      ps.linv_stride = eig_stride_;
+      ps.linv_ok = spd_ok_.as<int>();
+      ps.grams = grams_.as<double>();
       ps.aug_count = gram_aug_counts(gs, gram_work_.p);
       ps.aug_term = gram_aug_term(gs);
       ps.max_iter = 200;
-      ps.tol = 1e-14;
-      ps.check_tol = 1e-11;
+      ps.tol = 1e-15;
+      ps.check_tol = 1e-12;
       pcg_work_.ensure(pcg_work_bytes((int)d_, rk[0]), st_);
       pcg_solve(ps, blocks_.as<double>(), rhs_.as<double>(), core_.as<double>(), pcg_work_.p,
                 pcg_status_.as<int>(), st_);

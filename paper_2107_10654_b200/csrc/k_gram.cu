@@ -549,24 +549,31 @@ __global__ void k_vech_expand(GramSpec spec, VechSpec v, const double* __restric
 // prod_{n<N} m_n blocks of R_N x R_N (C2: 136^2 x 16^2 doubles = 38 MB, vs
 // 134 MB for the full Gram); consumed by the CG matvec (k_pcg.cu).
 __global__ void k_vech_blocks(GramSpec spec, VechSpec v, const double* __restrict__ S,
-                              double* __restrict__ B, long long total) {
+                              double* __restrict__ B) {
+  // one CTA per block (u_1..u_{N-1}); threads over the R_N x R_N entries
   const int N = v.N, RL = v.R[N - 1];
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(e % RL);
-    long long t = e / RL;
-    const int r = (int)(t % RL);
-    t /= RL;
-    int un[kMaxOrder];
-    un[N - 1] = upper_pair(min(r, c), max(r, c), RL);
+  int un[kMaxOrder];
+  {
+    unsigned t = blockIdx.x;
     for (int n = N - 2; n >= 0; --n) {
-      un[n] = (int)(t % v.m[n]);
-      t /= v.m[n];
+      un[n] = (int)(t % (unsigned)v.m[n]);
+      t /= (unsigned)v.m[n];
     }
-    long long ur = 0, uc = 0;
-    for (int n = 1; n <= v.msplit && n < N; ++n) ur = ur * v.m[n] + un[n];
-    for (int n = v.msplit + 1; n < N; ++n) uc = uc * v.m[n] + un[n];
-    B[e] = S[(size_t)un[0] * v.Hsz + ur * v.Ncol + uc];
+  }
+  long long ur = 0, ucb = 0;
+  for (int n = 1; n <= v.msplit && n < N - 1; ++n) ur = ur * v.m[n] + un[n];
+  // the last mode is in the column group unless the split put it in the row group
+  const bool last_in_row = v.msplit >= N - 1;
+  for (int n = v.msplit + 1; n < N - 1; ++n) ucb = ucb * v.m[n] + un[n];
+  const double* Su = S + (size_t)un[0] * v.Hsz;
+  double* Bb = B + (size_t)blockIdx.x * RL * RL;
+  for (int e = threadIdx.x; e < RL * RL; e += blockDim.x) {
+    const int r = e / RL, c = e - r * RL;
+    const int ul = upper_pair(min(r, c), max(r, c), RL);
+    long long idx;
+    if (last_in_row) idx = (ur * v.m[N - 1] + ul) * v.Ncol;
+    else idx = ur * v.Ncol + ucb * v.m[N - 1] + ul;
+    Bb[e] = __ldg(Su + idx);
   }
 }
 
@@ -646,8 +653,9 @@ void gram_expand_full(const GramSpec& spec, void* work, double* gram, cudaStream
 void gram_expand_blocks(const GramSpec& spec, void* work, double* blocks, cudaStream_t st) {
   const VechSpec v = make_vech(spec);
   GramLayout l = layout(spec, work);
-  const long long total = gram_block_elems(spec);
-  k_vech_blocks<<<kNumSMs * 8, 256, 0, st>>>(spec, v, l.S, blocks, total);
+  const long long nblk = gram_block_elems(spec) / ((long long)v.R[v.N - 1] * v.R[v.N - 1]);
+  if (nblk > 0x7fffffffLL) throw Error(4, "gram_expand_blocks: too many blocks");
+  k_vech_blocks<<<(unsigned)nblk, 256, 0, st>>>(spec, v, l.S, blocks);
   RTB_LAUNCH_CHECK();
 }
 

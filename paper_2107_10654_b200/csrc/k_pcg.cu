@@ -4,12 +4,12 @@
 // (ref sketch_ridge.cpp:130-139). G = K^T W K + lambda * diag(c) is SPD whenever
 // lambda > 0 and every augmented row was drawn (c_j > 0), and it is a (1 +- eps)
 // spectral approximation of the unsketched K^T K + lambda I (the point of ridge
-// leverage-score sampling). For the Kronecker design K = A_1 (x) ... (x) A_N that
-// matrix is cheap to invert exactly:
-//     M = (x)_n A_n^T A_n + lambda I = V diag(lambda + prod_n mu_n) V^T,  V = (x)_n V_n
-// (V_n, mu_n = eigenpairs of the R_n x R_n factor Gram), so M^-1 r costs 2 N
-// mode products on a d-vector. Preconditioned by M, CG sees eigenvalues in
-// [1 - eps, 1 + eps] and converges in a few tens of iterations.
+// leverage-score sampling). For the Kronecker design K = A_1 (x) ... (x) A_N,
+//     K^T K = (x)_n A_n^T A_n = (x)_n L_n L_n^T,   M^-1 = (x)_n L_n^-T L_n^-1,
+// with the L_n^-1 the score step already computed (k_spd_small). Preconditioned
+// by M, CG sees eigenvalues in [(1 - eps), (1 + eps)(1 + lambda / mu_min)] and
+// converges in a few tens of iterations; M^-1 r costs 2N mode products on a
+// d-vector.
 //
 // The matvec never touches the d x d Gram. G's entries depend only on the vech
 // pairs of the first N-1 modes (k_gram.cu), so it is read from the "last-mode
@@ -21,12 +21,17 @@
 // One persistent cooperative kernel runs all iterations with two grid barriers
 // per iteration: (A) slice partials -> barrier -> (B) each CTA sums the partials
 // of its own rows in a fixed order (+ the augmented diagonal) -> barrier -> (C)
-// every CTA redundantly and bit-identically updates the FULL r, applies M^-1,
-// forms the dot products and the next p in shared memory. The result is accepted
-// only if the true residual ||b - G x|| <= check_tol ||b|| (one extra matvec);
-// otherwise status != 0 and the caller falls back to the Cholesky path.
+// every CTA redundantly and bit-identically updates the FULL r and x, applies
+// M^-1, forms the dot products and the next p in shared memory.
+// Iterations stop at a backward-stable residual, ||r|| <= tol max(||b||, ||G||~ ||x||)
+// (||G||~ = lambda + prod_n ||A_n^T A_n||_F >= ||G||), and the result is accepted
+// only if the true residual ||b - G x|| <= check_tol (||G||~ ||x|| + ||b||) (one
+// extra matvec); otherwise status != 0 and the caller falls back to Cholesky.
 #include "common.cuh"
 #include "kernels.h"
+
+#include <cstdio>
+#include <cstdlib>
 
 namespace rtb {
 
@@ -45,9 +50,37 @@ struct PcgShared {
   int m1;         // vech pairs of mode 1 (slices)
 };
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+struct PcgArgs {
+  const double* B;        // last-mode blocks of the data Gram
+  const double* b;
+  double* x;
+  double* q;              // [d]
+  double* part;           // [m1][2][d']
+  double* rpart;          // [grid] residual partials
+  unsigned* counter;
+  int* status;            // [0] status, [1] iterations
+  const double* linv;     // per mode (stride): L_n^-1, row-major lower triangular
+  int linv_stride;
+  const int* linv_ok;     // per mode: Cholesky of A_n^T A_n succeeded
+  const double* grams;    // per mode (stride): A_n^T A_n
+  const int* aug_count;
+  double aug_term;
+  double lambda;
+  int max_iter;
+  double tol;
+  double check_tol;
+  unsigned long long* prof;  // optional: per-phase ns accumulated by CTA 0 (RTB_PCG_PROF)
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -56,7 +89,9 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned target)
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(counter, 1u);
-    while (ld_acquire_u32(counter) < target) __nanosleep(20);
+    while (ld_relaxed_u32(counter) < target) {
+    }
+    __threadfence();
   }
   __syncthreads();
 }
@@ -74,90 +109,95 @@ __device__ __forceinline__ double block_sum_det(double v, double* red) {
   return t;  // every thread holds the total
 }
 
-// out[o, j, k] = sum_i W[i * R + j] X[o, i, k] on a d-vector in shared memory
-// (W = V for X x_n V^T, W = V^T for X x_n V). One thread per fiber (o, k): the R
-// inputs are read once, W reads are warp-uniform (J > 1) or contiguous (J = 1).
+// out[o, j, k] = sum_i W[i * RM + j] X[o, i, k] (i, j < R <= RM) on a d-vector in
+// shared memory. J > 1: one thread per fiber (o, k), all R outputs in registers,
+// X reads contiguous across threads, W rows warp-uniform (broadcast).
+// J == 1: one thread per output, W reads contiguous, X reads broadcast.
+template <int RM>
 __device__ __forceinline__ void mode_product(const double* X, double* out, const double* W, int d,
                                              int R, int J) {
-  if (J == 1) {  // contiguous fibers: one output per thread, W reads contiguous in j
+  if (J == 1) {
     for (int e = threadIdx.x; e < d; e += kThreads) {
       const int o = e / R, j = e - o * R;
       const double* x = X + o * R;
-      double acc = 0.0;
-#pragma unroll 4
-      for (int i = 0; i < R; ++i) acc = fma(W[i * R + j], x[i], acc);
-      out[e] = acc;
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < RM; i += 2) {
+        if (i < R) acc0 = fma(W[i * RM + j], x[i], acc0);
+        if (i + 1 < R) acc1 = fma(W[(i + 1) * RM + j], x[i + 1], acc1);
+      }
+      out[e] = acc0 + acc1;
     }
     return;
   }
+  // J > 1: (fiber, output group) per thread; groups of 8 outputs so that every
+  // thread is busy when fibers < kThreads (C2: 256 fibers x 2 groups)
   const int fibers = d / R;
-  for (int f = threadIdx.x; f < fibers; f += kThreads) {
+  const int ngrp = (R + 7) / 8;
+  const int work = fibers * ngrp;
+  for (int w = threadIdx.x; w < work; w += kThreads) {
+    const int g = w / fibers, f = w - g * fibers;
     const int o = f / J, k = f - o * J;
     const int base = o * R * J + k;
-    for (int j0 = 0; j0 < R; j0 += 8) {
-      double acc[8];
+    const int j0 = 8 * g;
+    double acc[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) acc[t] = 0.0;
-      for (int i = 0; i < R; ++i) {
+    for (int t = 0; t < 8; ++t) acc[t] = 0.0;
+#pragma unroll
+    for (int i = 0; i < RM; ++i) {
+      if (i < R) {
         const double xi = X[base + i * J];
-        const double* w = W + i * R + j0;
+        const double2* wr = reinterpret_cast<const double2*>(W + i * RM + j0);
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (j0 + t < R) acc[t] = fma(w[t], xi, acc[t]);
+        for (int t = 0; t < 4; ++t) {
+          const double2 ww = wr[t];
+          acc[2 * t] = fma(ww.x, xi, acc[2 * t]);
+          acc[2 * t + 1] = fma(ww.y, xi, acc[2 * t + 1]);
+        }
       }
-#pragma unroll
-      for (int t = 0; t < 8; ++t)
-        if (j0 + t < R) out[base + (j0 + t) * J] = acc[t];
     }
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      if (j0 + t < R) out[base + (j0 + t) * J] = acc[t];
   }
 }
 
-// z = M^-1 r using scratch a, b; returns the buffer holding z (a or b).
+// z = M^-1 r = (x) L^-T (x) L^-1 r using scratch a, b; returns the buffer holding z.
+template <int RM>
 __device__ double* precondition(const PcgShared& sh, const double* r, double* a, double* b,
-                                const double* Vs, const double* VTs, const int* voff,
-                                const double* dinv) {
+                                const double* Wf, const double* Wb,
+                                unsigned long long* prof = nullptr) {
   const double* src = r;
   double* dst = a;
+  unsigned long long t0 = prof ? gtimer() : 0;
   for (int n = 0; n < sh.order; ++n) {
-    mode_product(src, dst, Vs + voff[n], sh.d, sh.R[n], sh.J[n]);
+    mode_product<RM>(src, dst, Wf + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
     __syncthreads();
+    if (prof) {
+      const unsigned long long t1 = gtimer();
+      prof[8 + n] += t1 - t0;
+      t0 = t1;
+    }
     src = dst;
     dst = (dst == a) ? b : a;
   }
-  double* t = const_cast<double*>(src);
-  for (int e = threadIdx.x; e < sh.d; e += kThreads) t[e] *= dinv[e];
-  __syncthreads();
   for (int n = 0; n < sh.order; ++n) {
-    mode_product(src, dst, VTs + voff[n], sh.d, sh.R[n], sh.J[n]);
+    mode_product<RM>(src, dst, Wb + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
     __syncthreads();
+    if (prof) {
+      const unsigned long long t1 = gtimer();
+      prof[11 + n] += t1 - t0;
+      t0 = t1;
+    }
     src = dst;
     dst = (dst == a) ? b : a;
   }
   return const_cast<double*>(src);
 }
 
-struct PcgArgs {
-  const double* B;        // last-mode blocks of the data Gram
-  const double* b;
-  double* x;
-  double* q;              // [d]
-  double* part;           // [m1][2][d']
-  double* rpart;          // [grid] residual partials
-  unsigned* counter;
-  int* status;            // [0] status, [1] iterations
-  const double* evals;
-  const double* evecs;
-  int eig_stride;
-  const int* aug_count;
-  double aug_term;
-  double lambda;
-  int max_iter;
-  double tol;
-  double check_tol;
-};
-
 // (A) slice partials: for slice u1 = v(a, b), side 0 = q[a, :] from p[b, :],
 // side 1 = q[b, :] from p[a, :] (absent when a == b).
+template <int RM>
 __device__ void slice_partials(const PcgArgs& A, const PcgShared& sh, const double* p) {
   const int last = sh.last, mid = sh.mid, dp = sh.dprime;
   const int nout = 2 * dp;
@@ -171,43 +211,148 @@ __device__ void slice_partials(const PcgArgs& A, const PcgShared& sh, const doub
       const int side = t & 1, im = t >> 1;
       if (side == 1 && a == b) continue;
       const double* pv = p + (size_t)(side == 0 ? b : a) * dp;
-      // middle-mode digits of im (mixed radix R_1..R_{N-2}, last fastest)
-      int idig[kMaxOrder];
+      // middle-mode digits (modes 1..N-2), kept in registers: every loop below
+      // runs to the compile-time bound with a guard, so indices are static
+      int idig[kMaxOrder], jdig[kMaxOrder];
       {
         int rem = im;
-        for (int n = sh.order - 2; n >= 1; --n) {
-          idig[n] = rem % sh.R[n];
-          rem /= sh.R[n];
+#pragma unroll
+        for (int n = kMaxOrder - 1; n >= 1; --n) {
+          idig[n] = 0;
+          jdig[n] = 0;
+          if (n <= sh.order - 2) {
+            idig[n] = rem % sh.R[n];
+            rem /= sh.R[n];
+          }
         }
       }
-      int jdig[kMaxOrder];
-      for (int n = 1; n <= sh.order - 2; ++n) jdig[n] = 0;
-      double sum = 0.0;
+      double s0 = 0.0, s1 = 0.0;
       for (int jm = 0; jm < mid; ++jm) {
         int umid = 0;
-        for (int n = 1; n <= sh.order - 2; ++n) {
-          const int x = idig[n], y = jdig[n];
-          umid = umid * sh.m[n] + upper_pair(min(x, y), max(x, y), sh.R[n]);
-        }
+#pragma unroll
+        for (int n = 1; n < kMaxOrder; ++n)
+          if (n <= sh.order - 2) {
+            const int x = idig[n], y = jdig[n];
+            umid = umid * sh.m[n] + upper_pair(min(x, y), max(x, y), sh.R[n]);
+          }
         const double* row = Bs + ((size_t)umid * last + r) * last;
         const double* ps = pv + (size_t)jm * last;
         if ((last & 1) == 0) {
-          for (int c = 0; c < last; c += 2) {
-            const double2 g = __ldg(reinterpret_cast<const double2*>(row + c));
-            const double2 pp = *reinterpret_cast<const double2*>(ps + c);
-            sum = fma(g.x, pp.x, sum);
-            sum = fma(g.y, pp.y, sum);
-          }
+          double2 g[RM / 2];
+#pragma unroll
+          for (int c = 0; c < RM / 2; ++c)
+            if (2 * c < last) g[c] = __ldg(reinterpret_cast<const double2*>(row) + c);
+#pragma unroll
+          for (int c = 0; c < RM / 2; ++c)
+            if (2 * c < last) {
+              const double2 pp = reinterpret_cast<const double2*>(ps)[c];
+              s0 = fma(g[c].x, pp.x, s0);
+              s1 = fma(g[c].y, pp.y, s1);
+            }
         } else {
-          for (int c = 0; c < last; ++c) sum = fma(__ldg(row + c), ps[c], sum);
+          double g[RM];
+#pragma unroll
+          for (int c = 0; c < RM; ++c)
+            if (c < last) g[c] = __ldg(row + c);
+#pragma unroll
+          for (int c = 0; c < RM; ++c)
+            if (c < last) s0 = fma(g[c], ps[c], s0);
         }
-        for (int n = sh.order - 2; n >= 1; --n) {  // odometer over the middle modes
-          if (++jdig[n] < sh.R[n]) break;
-          jdig[n] = 0;
+        bool carry = true;  // odometer over the middle modes
+#pragma unroll
+        for (int n = kMaxOrder - 1; n >= 1; --n)
+          if (n <= sh.order - 2 && carry) {
+            if (++jdig[n] < sh.R[n]) carry = false;
+            else jdig[n] = 0;
+          }
+      }
+      A.part[((size_t)u1 * 2 + side) * dp + (size_t)im * last + r] = s0 + s1;
+    }
+  }
+}
+
+// (A) fast path, order 3 with R_3 == 16: every unordered middle pair (i2 <= j2)
+// of the slice is read ONCE (one 2 KB block) and applied to the four (side,
+// orientation) targets -- q_a(i2) += B p_b(j2), q_a(j2) += B p_b(i2), q_b(i2) +=
+// B p_a(j2), q_b(j2) += B p_a(i2) (B symmetric). Lane (r = l/4, c = l%4) reads
+// columns {2c, 2c+1, 8+2c, 9+2c} of rows r and r+8 (8 lines per load), partial
+// dots are reduced over the 4 column lanes by shuffles, and each warp adds its
+// results to private accumulators acc[w][side][i2][r] (fixed order -> the final
+// sum over warps is deterministic).
+__device__ void slice_partials_n3(const PcgArgs& A, const PcgShared& sh, const double* p,
+                                  double* accw) {
+  const int R2 = sh.R[1], dp = sh.dprime;  // dp = R2 * 16
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, c = lane & 3;
+  const int m2 = sh.m[1];
+  for (int u1 = blockIdx.x; u1 < sh.m1; u1 += gridDim.x) {
+    int a, b;
+    pair_of(u1, sh.R[0], a, b);
+    const bool two_sides = a != b;
+    double* acc = accw + (size_t)w * 2 * dp;
+    for (int e = lane; e < 2 * dp; e += 32) acc[e] = 0.0;
+    __syncwarp();
+    const double* Bs = A.B + (size_t)u1 * m2 * 256;
+    const double* pa = p + (size_t)a * dp;
+    const double* pb = p + (size_t)b * dp;
+    for (int pidx = w; pidx < m2; pidx += kWarps) {
+      int i2, j2;
+      pair_of(pidx, R2, i2, j2);
+      const bool two_orient = i2 != j2;
+      const double* blk = Bs + (size_t)pidx * 256;
+      double2 g[2][2];
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          g[rr][h] = __ldg(reinterpret_cast<const double2*>(blk + (r + 8 * rr) * 16 + 8 * h + 2 * c));
+      // targets: 0 = q_a(i2) <- p_b(j2), 1 = q_a(j2) <- p_b(i2), 2 = q_b(i2) <- p_a(j2),
+      // 3 = q_b(j2) <- p_a(i2)
+      const double* src[4] = {pb + j2 * 16, pb + i2 * 16, pa + j2 * 16, pa + i2 * 16};
+      double t[4][2];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const double2 p0 = *reinterpret_cast<const double2*>(src[v] + 2 * c);
+        const double2 p1 = *reinterpret_cast<const double2*>(src[v] + 8 + 2 * c);
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          double s = g[rr][0].x * p0.x;
+          s = fma(g[rr][0].y, p0.y, s);
+          s = fma(g[rr][1].x, p1.x, s);
+          s = fma(g[rr][1].y, p1.y, s);
+          t[v][rr] = s;
         }
       }
-      A.part[((size_t)u1 * 2 + side) * dp + (size_t)im * last + r] = sum;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          t[v][rr] += __shfl_xor_sync(0xffffffffu, t[v][rr], 1);
+          t[v][rr] += __shfl_xor_sync(0xffffffffu, t[v][rr], 2);
+        }
+      if (c == 0) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int row = r + 8 * rr;
+          acc[i2 * 16 + row] += t[0][rr];
+          if (two_orient) acc[j2 * 16 + row] += t[1][rr];
+          if (two_sides) {
+            acc[dp + i2 * 16 + row] += t[2][rr];
+            if (two_orient) acc[dp + j2 * 16 + row] += t[3][rr];
+          }
+        }
+      }
+      __syncwarp();
     }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 2 * dp; e += kThreads) {
+      const int side = e >= dp;
+      if (side && !two_sides) continue;
+      double s = 0.0;
+      for (int ww = 0; ww < kWarps; ++ww) s += accw[(size_t)ww * 2 * dp + e];
+      A.part[((size_t)u1 * 2 + side) * dp + (e - side * dp)] = s;
+    }
+    __syncthreads();
   }
 }
 
@@ -229,29 +374,30 @@ __device__ void reduce_rows(const PcgArgs& A, const PcgShared& sh, const double*
   }
 }
 
+template <int RM>
 __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgShared shc) {
   extern __shared__ __align__(16) double sm[];
-  const PcgShared sh = shc;
+  const PcgShared& sh = shc;  // stays in the parameter bank (dynamic indexing is cheap)
   const int d = sh.d;
-  int voff[kMaxOrder];
-  int vtot = 0;
-  for (int n = 0; n < sh.order; ++n) {
-    voff[n] = vtot;
-    vtot += sh.R[n] * sh.R[n];
-  }
   const int dv = (d + 1) & ~1;
-  double* Vs = sm;
-  double* VTs = Vs + ((vtot + 1) & ~1);
-  double* dinv = VTs + ((vtot + 1) & ~1);
-  double* r = dinv + dv;
+  double* Wf = sm;                          // [order][RM][RM]: L^-T (row-major)
+  double* Wb = Wf + sh.order * RM * RM;     // [order][RM][RM]: L^-1
+  double* r = Wb + sh.order * RM * RM;
   double* p = r + dv;
   double* s0 = p + dv;
   double* s1 = s0 + dv;
-  double* red = s1 + dv;
+  double* xs = s1 + dv;  // full x, kept redundantly like r and p
+  double* red = xs + dv;
+  // fast order-3 matvec: per-warp accumulators, in s0/s1 when they are large enough
+  const bool fast3 = sh.order == 3 && sh.last == 16;
+  const size_t acc_need = (size_t)kWarps * 2 * sh.dprime;
+  double* accw = acc_need <= (size_t)2 * dv ? s0 : red + 32;
 
   // applicability: every augmented column drawn (then G >= lambda * min c_j > 0)
+  // and every factor Gram Cholesky-factorable (the preconditioner)
   int missing = 0;
   for (int e = threadIdx.x; e < d; e += kThreads) missing |= __ldg(A.aug_count + e) == 0;
+  if (threadIdx.x < sh.order) missing |= __ldg(A.linv_ok + threadIdx.x) == 0;
   if (__syncthreads_or(missing) || !(A.lambda > 0.0)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       A.status[0] = 3;
@@ -260,24 +406,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
     return;
   }
 
+  double gnorm = 1.0;
   for (int n = 0; n < sh.order; ++n) {
     const int R = sh.R[n];
-    for (int e = threadIdx.x; e < R * R; e += kThreads) {
-      const double v = A.evecs[(size_t)n * A.eig_stride + e];  // V[i][k], column k
-      Vs[voff[n] + e] = v;
-      VTs[voff[n] + (e % R) * R + e / R] = v;
+    const double* L = A.linv + (size_t)n * A.linv_stride;
+    for (int e = threadIdx.x; e < RM * RM; e += kThreads) {
+      const int i = e / RM, j = e - i * RM;
+      const bool in = i < R && j < R;
+      Wf[n * RM * RM + e] = in ? L[j * R + i] : 0.0;  // Wf[i][j] = L^-1[j][i]
+      Wb[n * RM * RM + e] = in ? L[i * R + j] : 0.0;  // Wb[i][j] = L^-1[i][j]
     }
+    // ||A_n^T A_n||_2 by power iteration (warp 0, lane = row; a slight
+    // underestimate is harmless: it only tightens the stopping test)
+    const double* Gm = A.grams + (size_t)n * A.linv_stride;
+    if (threadIdx.x < 32) {
+      const int i = threadIdx.x;
+      double v = i < R ? 1.0 : 0.0, mu = 0.0;
+      for (int itp = 0; itp < 60; ++itp) {
+        double y = 0.0;
+        for (int j = 0; j < R; ++j) y = fma(i < R ? Gm[i * R + j] : 0.0, __shfl_sync(0xffffffffu, v, j), y);
+        double yy = y * y, vy = v * y;
+        for (int o = 16; o > 0; o >>= 1) {
+          yy += __shfl_xor_sync(0xffffffffu, yy, o);
+          vy += __shfl_xor_sync(0xffffffffu, vy, o);
+        }
+        double vv = v * v;
+        for (int o = 16; o > 0; o >>= 1) vv += __shfl_xor_sync(0xffffffffu, vv, o);
+        mu = vv > 0.0 ? vy / vv : 0.0;
+        v = yy > 0.0 ? y * rsqrt(yy) : 0.0;
+      }
+      if (threadIdx.x == 0) red[0] = mu;
+    }
+    __syncthreads();
+    gnorm *= red[0];
+    __syncthreads();
   }
+  gnorm += A.lambda;
   for (int e = threadIdx.x; e < d; e += kThreads) {
-    double m = 1.0;
-    int rem = e;
-    for (int n = sh.order - 1; n >= 0; --n) {
-      const int j = rem % sh.R[n];
-      rem /= sh.R[n];
-      m *= fmax(A.evals[(size_t)n * A.eig_stride + j], 0.0);
-    }
-    dinv[e] = 1.0 / (m + A.lambda);
     r[e] = A.b[e];
+    xs[e] = 0.0;
   }
   __syncthreads();
 
@@ -288,15 +455,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   double bb = 0.0;
   for (int e = threadIdx.x; e < d; e += kThreads) bb = fma(r[e], r[e], bb);
   bb = block_sum_det(bb, red);
-  for (int e = row0 + threadIdx.x; e < row0 + nrows; e += kThreads) A.x[e] = 0.0;
   if (bb == 0.0) {
+    for (int e = row0 + threadIdx.x; e < row0 + nrows; e += kThreads) A.x[e] = 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       A.status[0] = 0;
       A.status[1] = 0;
     }
     return;
   }
-  double* z = precondition(sh, r, s0, s1, Vs, VTs, voff, dinv);
+  double* z = precondition<RM>(sh, r, s0, s1, Wf, Wb);
   double rho = 0.0;
   for (int e = threadIdx.x; e < d; e += kThreads) {
     p[e] = z[e];
@@ -304,17 +471,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   }
   rho = block_sum_det(rho, red);
 
-  const double stop = A.tol * A.tol * bb;
+  const double tol2 = A.tol * A.tol;
   int it = 0;
   int fail = 0;
+  const bool prof = A.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long t0 = prof ? gtimer() : 0, t1;
+#define RTB_PCG_MARK(k)                 \
+  if (prof) {                           \
+    t1 = gtimer();                      \
+    A.prof[k] += t1 - t0;               \
+    t0 = t1;                            \
+  }
   for (; it < A.max_iter; ++it) {
-    slice_partials(A, sh, p);
+    if (fast3) slice_partials_n3(A, sh, p, accw);
+    else slice_partials<RM>(A, sh, p);
+    __syncthreads();
+    RTB_PCG_MARK(0)
     sync_target += gridDim.x;
     grid_barrier(A.counter, sync_target);
+    RTB_PCG_MARK(1)
     reduce_rows(A, sh, p, row0, nrows, A.q);
+    __syncthreads();
+    RTB_PCG_MARK(2)
     sync_target += gridDim.x;
     grid_barrier(A.counter, sync_target);
-    // every CTA: alpha from the full p.q, full r update, own x rows
+    RTB_PCG_MARK(3)
+    // every CTA: alpha from the full p.q, full r and x updates
     double pq = 0.0;
     for (int e = threadIdx.x; e < d; e += kThreads) {
       const double qe = __ldcg(A.q + e);
@@ -327,20 +509,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
       break;
     }
     const double alpha = rho / pq;
-    double rr = 0.0;
+    double rr = 0.0, xx = 0.0;
     for (int e = threadIdx.x; e < d; e += kThreads) {
       const double re = fma(-alpha, s0[e], r[e]);
       r[e] = re;
       rr = fma(re, re, rr);
+      const double xe = fma(alpha, p[e], xs[e]);
+      xs[e] = xe;
+      xx = fma(xe, xe, xx);
     }
-    for (int e = row0 + threadIdx.x; e < row0 + nrows; e += kThreads)
-      A.x[e] = fma(alpha, p[e], A.x[e]);
     rr = block_sum_det(rr, red);
-    if (rr <= stop) {
+    xx = block_sum_det(xx, red);
+    RTB_PCG_MARK(4)
+    if (rr <= tol2 * fmax(bb, gnorm * gnorm * xx)) {
       ++it;
       break;
     }
-    z = precondition(sh, r, s0, s1, Vs, VTs, voff, dinv);
+    z = precondition<RM>(sh, r, s0, s1, Wf, Wb,
+                         (prof && sh.order <= 3) ? A.prof : nullptr);
+    RTB_PCG_MARK(5)
     double rho2 = 0.0;
     for (int e = threadIdx.x; e < d; e += kThreads) rho2 = fma(r[e], z[e], rho2);
     rho2 = block_sum_det(rho2, red);
@@ -348,13 +535,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
     rho = rho2;
     for (int e = threadIdx.x; e < d; e += kThreads) p[e] = fma(beta, p[e], z[e]);
     __syncthreads();
+    RTB_PCG_MARK(6)
   }
-  // true residual ||b - G x||: gather x, one matvec, reduce over CTAs
-  sync_target += gridDim.x;
-  grid_barrier(A.counter, sync_target);
-  for (int e = threadIdx.x; e < d; e += kThreads) p[e] = __ldcg(A.x + e);
-  __syncthreads();
-  slice_partials(A, sh, p);
+#undef RTB_PCG_MARK
+  // x out (own rows); true residual ||b - G x|| with one more matvec
+  double xx = 0.0;
+  for (int e = threadIdx.x; e < d; e += kThreads) {
+    p[e] = xs[e];
+    xx = fma(xs[e], xs[e], xx);
+  }
+  xx = block_sum_det(xx, red);
+  for (int e = row0 + threadIdx.x; e < row0 + nrows; e += kThreads) A.x[e] = xs[e];
+  if (fast3) slice_partials_n3(A, sh, p, accw);
+  else slice_partials<RM>(A, sh, p);
   sync_target += gridDim.x;
   grid_barrier(A.counter, sync_target);
   reduce_rows(A, sh, p, row0, nrows, A.q);
@@ -372,7 +565,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
     double tot = 0.0;
     for (int c = 0; c < (int)gridDim.x; ++c) tot += __ldcg(A.rpart + c);
     int st = fail;
-    if (!st && !(tot <= A.check_tol * A.check_tol * bb)) st = 1;
+    const double scale = gnorm * sqrt(xx) + sqrt(bb);
+    if (!st && !(tot <= A.check_tol * A.check_tol * scale * scale)) st = 1;
     A.status[0] = st;
     A.status[1] = it;
   }
@@ -388,11 +582,20 @@ int num_sms() {
   return sms;
 }
 
-size_t pcg_smem(int d, int order, const int* ranks) {
-  int vtot = 0;
-  for (int n = 0; n < order; ++n) vtot += ranks[n] * ranks[n];
+int rank_bucket(int order, const int* ranks) {
+  int rmax = 0;
+  for (int n = 0; n < order; ++n) rmax = ranks[n] > rmax ? ranks[n] : rmax;
+  return rmax <= 8 ? 8 : rmax <= 16 ? 16 : rmax <= 32 ? 32 : 0;
+}
+
+size_t pcg_smem(int d, int order, const int* ranks, int rm) {
   const size_t dv = (size_t)((d + 1) & ~1);
-  return 8 * (2 * (size_t)((vtot + 1) & ~1) + 5 * dv + 32);
+  size_t extra = 0;
+  if (order == 3 && ranks[2] == 16) {
+    const size_t need = (size_t)kWarps * 2 * (d / ranks[0]);
+    if (need > 2 * dv) extra = need;
+  }
+  return 8 * (2 * (size_t)order * rm * rm + 5 * dv + 32 + extra);
 }
 
 }  // namespace
@@ -404,7 +607,9 @@ size_t pcg_work_bytes(int d, int r1) {
 }
 
 bool pcg_supported(int d, int order, const int* ranks) {
-  return d >= 1 && order >= 2 && order <= kMaxOrder && pcg_smem(d, order, ranks) <= 220 * 1024;
+  const int rm = rank_bucket(order, ranks);
+  return d >= 1 && order >= 2 && order <= kMaxOrder && rm > 0 &&
+         pcg_smem(d, order, ranks, rm) <= 220 * 1024;
 }
 
 void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, double* x, void* work,
@@ -430,7 +635,8 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   sh.mmid = 1;
   for (int n = 1; n < spec.order - 1; ++n) sh.mmid *= sh.m[n];
   sh.m1 = sh.m[0];
-  const size_t smem = pcg_smem(d, spec.order, spec.ranks);
+  const int rm = rank_bucket(spec.order, spec.ranks);
+  const size_t smem = pcg_smem(d, spec.order, spec.ranks, rm);
 
   char* w = static_cast<char*>(work);
   PcgArgs a{};
@@ -442,24 +648,46 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   a.rpart = a.part + (size_t)sh.m1 * 2 * sh.dprime;
   a.counter = reinterpret_cast<unsigned*>(a.rpart + 1024);
   a.status = status_dev;
-  a.evals = spec.evals;
-  a.evecs = spec.evecs;
-  a.eig_stride = spec.eig_stride;
+  a.linv = spec.linv;
+  a.linv_stride = spec.linv_stride;
+  a.linv_ok = spec.linv_ok;
+  a.grams = spec.grams;
   a.aug_count = spec.aug_count;
   a.aug_term = spec.aug_term;
   a.lambda = spec.lambda;
   a.max_iter = spec.max_iter;
   a.tol = spec.tol;
   a.check_tol = spec.check_tol;
+  static unsigned long long* prof_buf = nullptr;
+  static const bool prof_on = std::getenv("RTB_PCG_PROF") != nullptr;
+  if (prof_on) {
+    if (!prof_buf) RTB_CUDA(cudaMalloc(&prof_buf, 16 * 8));
+    RTB_CUDA(cudaMemsetAsync(prof_buf, 0, 16 * 8, st));
+    a.prof = prof_buf;
+  }
   RTB_CUDA(cudaMemsetAsync(a.counter, 0, 64, st));
-  static bool attr_set = false;
-  if (!attr_set) {
-    RTB_CUDA(cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    attr_set = true;
+  void* fn = rm == 8 ? (void*)k_pcg<8> : rm == 16 ? (void*)k_pcg<16> : (void*)k_pcg<32>;
+  static bool attr_set[3] = {false, false, false};
+  const int slot = rm == 8 ? 0 : rm == 16 ? 1 : 2;
+  if (!attr_set[slot]) {
+    RTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr_set[slot] = true;
   }
   void* args[] = {(void*)&a, (void*)&sh};
-  RTB_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg, dim3(grid), dim3(kThreads), args, smem, st));
+  RTB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, st));
   RTB_LAUNCH_CHECK();
+  if (prof_on) {
+    unsigned long long h[16];
+    int stat[2];
+    RTB_CUDA(cudaMemcpyAsync(h, prof_buf, 128, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaMemcpyAsync(stat, status_dev, 8, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaStreamSynchronize(st));
+    std::fprintf(stderr,
+                 "[pcg] d=%d iters=%d status=%d ns: slice %llu bar1 %llu reduce %llu bar2 %llu "
+                 "vec %llu precond %llu tail %llu | stages %llu %llu %llu %llu %llu %llu\n",
+                 d, stat[1], stat[0], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[8], h[9], h[10],
+                 h[11], h[12], h[13]);
+  }
 }
 
 }  // namespace rtb

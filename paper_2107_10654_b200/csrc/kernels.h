@@ -114,14 +114,15 @@ struct PcgSpec {
   int ranks[8];
   int d;
   double lambda;
-  const double* evals;  // per mode (stride eig_stride): eigenvalues of A_n^T A_n
-  const double* evecs;  // per mode: V[i*R+k], column k = eigenvector k
-  int eig_stride;
+  const double* linv;   // per mode (stride linv_stride): L_n^-1 of A_n^T A_n (k_spd_small)
+  int linv_stride;
+  const int* linv_ok;   // per mode: Cholesky succeeded (any 0 -> status 3)
+  const double* grams;  // per mode (same stride): A_n^T A_n
   const int* aug_count; // [d] augmented draws per column (any 0 -> status 3)
   double aug_term;      // diagonal added per augmented draw
   int max_iter;
-  double tol;           // stop when ||r_k|| <= tol ||b|| (recursive residual)
-  double check_tol;     // accept when ||b - G x|| <= check_tol ||b||
+  double tol;           // stop when ||r_k|| <= tol max(||b||, ||G||~ ||x_k||)
+  double check_tol;     // accept when ||b - G x|| <= check_tol (||G||~ ||x|| + ||b||)
 };
 size_t pcg_work_bytes(int d, int r1);
 bool pcg_supported(int d, int order, const int* ranks);

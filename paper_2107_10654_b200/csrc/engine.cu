@@ -530,7 +530,7 @@ class Engine {
   DevBuf T_, P_, tmp_a_, tmp_b_, partial_, scal_, hist_, init_loss_;
   DevBuf scores_, cdf_, sums_, score_off_, rows_dev_, cols_dev_, flag_;
   DevBuf sk_idx_, sk_w_, draw_work_, gram_work_, G_, rhs_, chol_work_, chol_status_,
-      data_draws_, zero_flag_, U_[8], pev_, pvec_, pst_, pcg_work_, pcg_status_, blocks_;
+      data_draws_, zero_flag_, U_[8], pgram_, pcg_work_, pcg_status_, blocks_;
   uint64_t sketch_rng_ = 0, sketch_k_ = 0;
   bool t_valid_ = false;
   uint64_t last_s_ = 0;
@@ -585,9 +585,7 @@ class Engine {
       RTB_CUDA(cudaMemcpy(ns_vals_.p, vals, 65 * 4, cudaMemcpyHostToDevice));
     }
     eig_status_.ensure(64 * 4, st_);
-    pev_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
-    pvec_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
-    pst_.ensure(64 * 4, st_);
+    pgram_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
     pcg_status_.ensure(16, st_);
     ns_.ensure(64 * 4, st_);
     ranks_dev_.ensure(64 * 4, st_);
@@ -837,7 +835,7 @@ class Engine {
       const int* okm = nullptr;
       if (rmax_ <= 32) {
         spd_small(grams_.as<double>(), ns_.as<int>(), eig_stride_, (double)maxI * DBL_EPSILON,
-                  linv_.as<double>(), nullptr, spd_ok_.as<int>(), N_, st_);
+                  linv_.as<double>(), pgram_.as<double>(), spd_ok_.as<int>(), N_, st_);
         okm = spd_ok_.as<int>();
       }
       sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, evals_.as<double>(),
@@ -934,7 +932,7 @@ class Engine {
       for (int n = 0; n < N_; ++n) ps.ranks[n] = rk[n];
       ps.d = (int)d_;
       ps.lambda = opt_.lambda;
-      ps.linv = linv_.as<double>();   // factor-Gram Cholesky of the score step
+      ps.pinv = pgram_.as<double>();  // (A_n^T A_n)^-1 from the score step's Cholesky
       ps.linv_stride = eig_stride_;
       ps.linv_ok = spd_ok_.as<int>();
       ps.grams = grams_.as<double>();

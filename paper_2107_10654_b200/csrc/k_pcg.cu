@@ -5,11 +5,11 @@
 // lambda > 0 and every augmented row was drawn (c_j > 0), and it is a (1 +- eps)
 // spectral approximation of the unsketched K^T K + lambda I (the point of ridge
 // leverage-score sampling). For the Kronecker design K = A_1 (x) ... (x) A_N,
-//     K^T K = (x)_n A_n^T A_n = (x)_n L_n L_n^T,   M^-1 = (x)_n L_n^-T L_n^-1,
-// with the L_n^-1 the score step already computed (k_spd_small). Preconditioned
-// by M, CG sees eigenvalues in [(1 - eps), (1 + eps)(1 + lambda / mu_min)] and
-// converges in a few tens of iterations; M^-1 r costs 2N mode products on a
-// d-vector.
+//     M = K^T K = (x)_n A_n^T A_n,   M^-1 = (x)_n P_n,  P_n = (A_n^T A_n)^-1,
+// with the P_n from the score step's factor-Gram Cholesky (k_spd_small).
+// Preconditioned by M, CG sees eigenvalues in [(1 - eps), (1 + eps)(1 + lambda /
+// mu_min)] and converges in a few tens of iterations; M^-1 r costs N mode
+// products on a d-vector.
 //
 // The matvec never touches the d x d Gram. G's entries depend only on the vech
 // pairs of the first N-1 modes (k_gram.cu), so it is read from the "last-mode
@@ -59,7 +59,7 @@ struct PcgArgs {
   double* rpart;          // [grid] residual partials
   unsigned* counter;
   int* status;            // [0] status, [1] iterations
-  const double* linv;     // per mode (stride): L_n^-1, row-major lower triangular
+  const double* pinv;     // per mode (stride): (A_n^T A_n)^-1, row-major
   int linv_stride;
   const int* linv_ok;     // per mode: Cholesky of A_n^T A_n succeeded
   const double* grams;    // per mode (stride): A_n^T A_n
@@ -109,29 +109,54 @@ __device__ __forceinline__ double block_sum_det(double v, double* red) {
   return t;  // every thread holds the total
 }
 
-// out[o, j, k] = sum_i W[i * RM + j] X[o, i, k] (i, j < R <= RM) on a d-vector in
-// shared memory. J > 1: one thread per fiber (o, k), all R outputs in registers,
-// X reads contiguous across threads, W rows warp-uniform (broadcast).
-// J == 1: one thread per output, W reads contiguous, X reads broadcast.
-template <int RM>
-__device__ __forceinline__ void mode_product(const double* X, double* out, const double* W, int d,
-                                             int R, int J) {
+// out[o, j, k] = sum_i P[i * RM + j] X[o, i, k] (i, j < R <= RM; P symmetric) on
+// a d-vector in shared memory. RX = R when every mode has exactly that rank
+// (no guards: loops unroll into straight-line code), else 0 (guarded loops).
+// J > 1: (fiber, 8-output group) per thread, X reads contiguous across threads,
+//        P rows warp-uniform (broadcast LDS.128).
+// J == 1: output j fixed per thread when kThreads % R == 0: column j of P is held
+//        in registers and the fiber's inputs are broadcast reads.
+template <int RM, int RX>
+__device__ __forceinline__ void mode_product(const double* X, double* out, const double* P, int d,
+                                             int Rrt, int J) {
+  const int R = RX ? RX : Rrt;
+  if (J == 1 && (kThreads % R) == 0) {
+    const int j = threadIdx.x % R;
+    double pc[RM];
+#pragma unroll
+    for (int i = 0; i < RM; ++i) pc[i] = (RX || i < R) ? P[i * RM + j] : 0.0;
+    const int ostep = kThreads / R;
+    for (int o = threadIdx.x / R; o < d / R; o += ostep) {
+      const double* x = X + o * R;
+      double acc0 = 0.0, acc1 = 0.0;
+      if (RX && (RX % 2) == 0) {
+#pragma unroll
+        for (int i = 0; i < RM; i += 2) {
+          const double2 xx = *reinterpret_cast<const double2*>(x + i);
+          acc0 = fma(pc[i], xx.x, acc0);
+          acc1 = fma(pc[i + 1], xx.y, acc1);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+          if (i < R) acc0 = fma(pc[i], x[i], acc0);
+      }
+      out[o * R + j] = acc0 + acc1;
+    }
+    return;
+  }
   if (J == 1) {
     for (int e = threadIdx.x; e < d; e += kThreads) {
       const int o = e / R, j = e - o * R;
       const double* x = X + o * R;
-      double acc0 = 0.0, acc1 = 0.0;
+      double acc = 0.0;
 #pragma unroll
-      for (int i = 0; i < RM; i += 2) {
-        if (i < R) acc0 = fma(W[i * RM + j], x[i], acc0);
-        if (i + 1 < R) acc1 = fma(W[(i + 1) * RM + j], x[i + 1], acc1);
-      }
-      out[e] = acc0 + acc1;
+      for (int i = 0; i < RM; ++i)
+        if (i < R) acc = fma(P[i * RM + j], x[i], acc);
+      out[e] = acc;
     }
     return;
   }
-  // J > 1: (fiber, output group) per thread; groups of 8 outputs so that every
-  // thread is busy when fibers < kThreads (C2: 256 fibers x 2 groups)
   const int fibers = d / R;
   const int ngrp = (R + 7) / 8;
   const int work = fibers * ngrp;
@@ -145,9 +170,9 @@ __device__ __forceinline__ void mode_product(const double* X, double* out, const
     for (int t = 0; t < 8; ++t) acc[t] = 0.0;
 #pragma unroll
     for (int i = 0; i < RM; ++i) {
-      if (i < R) {
+      if (RX || i < R) {
         const double xi = X[base + i * J];
-        const double2* wr = reinterpret_cast<const double2*>(W + i * RM + j0);
+        const double2* wr = reinterpret_cast<const double2*>(P + i * RM + j0);
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const double2 ww = wr[t];
@@ -158,35 +183,24 @@ __device__ __forceinline__ void mode_product(const double* X, double* out, const
     }
 #pragma unroll
     for (int t = 0; t < 8; ++t)
-      if (j0 + t < R) out[base + (j0 + t) * J] = acc[t];
+      if (RX ? (RX % 8 == 0 || j0 + t < R) : (j0 + t < R)) out[base + (j0 + t) * J] = acc[t];
   }
 }
 
-// z = M^-1 r = (x) L^-T (x) L^-1 r using scratch a, b; returns the buffer holding z.
-template <int RM>
+// z = M^-1 r = ((x)_n P_n) r, P_n = (A_n^T A_n)^-1: N mode products with scratch
+// a, b; returns the buffer holding z.
+template <int RM, int RX>
 __device__ double* precondition(const PcgShared& sh, const double* r, double* a, double* b,
-                                const double* Wf, const double* Wb,
-                                unsigned long long* prof = nullptr) {
+                                const double* Ps, unsigned long long* prof = nullptr) {
   const double* src = r;
   double* dst = a;
   unsigned long long t0 = prof ? gtimer() : 0;
   for (int n = 0; n < sh.order; ++n) {
-    mode_product<RM>(src, dst, Wf + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
+    mode_product<RM, RX>(src, dst, Ps + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
     __syncthreads();
-    if (prof) {
+    if (prof && n < 8) {
       const unsigned long long t1 = gtimer();
       prof[8 + n] += t1 - t0;
-      t0 = t1;
-    }
-    src = dst;
-    dst = (dst == a) ? b : a;
-  }
-  for (int n = 0; n < sh.order; ++n) {
-    mode_product<RM>(src, dst, Wb + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
-    __syncthreads();
-    if (prof) {
-      const unsigned long long t1 = gtimer();
-      prof[11 + n] += t1 - t0;
       t0 = t1;
     }
     src = dst;
@@ -374,15 +388,14 @@ __device__ void reduce_rows(const PcgArgs& A, const PcgShared& sh, const double*
   }
 }
 
-template <int RM>
+template <int RM, int RX>
 __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgShared shc) {
   extern __shared__ __align__(16) double sm[];
   const PcgShared& sh = shc;  // stays in the parameter bank (dynamic indexing is cheap)
   const int d = sh.d;
   const int dv = (d + 1) & ~1;
-  double* Wf = sm;                          // [order][RM][RM]: L^-T (row-major)
-  double* Wb = Wf + sh.order * RM * RM;     // [order][RM][RM]: L^-1
-  double* r = Wb + sh.order * RM * RM;
+  double* Ps = sm;                          // [order][RM][RM]: (A_n^T A_n)^-1
+  double* r = Ps + sh.order * RM * RM;
   double* p = r + dv;
   double* s0 = p + dv;
   double* s1 = s0 + dv;
@@ -409,12 +422,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   double gnorm = 1.0;
   for (int n = 0; n < sh.order; ++n) {
     const int R = sh.R[n];
-    const double* L = A.linv + (size_t)n * A.linv_stride;
+    const double* Pg = A.pinv + (size_t)n * A.linv_stride;
     for (int e = threadIdx.x; e < RM * RM; e += kThreads) {
       const int i = e / RM, j = e - i * RM;
-      const bool in = i < R && j < R;
-      Wf[n * RM * RM + e] = in ? L[j * R + i] : 0.0;  // Wf[i][j] = L^-1[j][i]
-      Wb[n * RM * RM + e] = in ? L[i * R + j] : 0.0;  // Wb[i][j] = L^-1[i][j]
+      Ps[n * RM * RM + e] = (i < R && j < R) ? Pg[i * R + j] : 0.0;
     }
     // ||A_n^T A_n||_2 by power iteration (warp 0, lane = row; a slight
     // underestimate is harmless: it only tightens the stopping test)
@@ -463,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
     }
     return;
   }
-  double* z = precondition<RM>(sh, r, s0, s1, Wf, Wb);
+  double* z = precondition<RM, RX>(sh, r, s0, s1, Ps);
   double rho = 0.0;
   for (int e = threadIdx.x; e < d; e += kThreads) {
     p[e] = z[e];
@@ -525,8 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
       ++it;
       break;
     }
-    z = precondition<RM>(sh, r, s0, s1, Wf, Wb,
-                         (prof && sh.order <= 3) ? A.prof : nullptr);
+    z = precondition<RM, RX>(sh, r, s0, s1, Ps, prof ? A.prof : nullptr);
     RTB_PCG_MARK(5)
     double rho2 = 0.0;
     for (int e = threadIdx.x; e < d; e += kThreads) rho2 = fma(r[e], z[e], rho2);
@@ -590,12 +600,12 @@ int rank_bucket(int order, const int* ranks) {
 
 size_t pcg_smem(int d, int order, const int* ranks, int rm) {
   const size_t dv = (size_t)((d + 1) & ~1);
-  size_t extra = 0;
+  size_t extra = 0;  // (P_n blocks: order * rm^2)
   if (order == 3 && ranks[2] == 16) {
     const size_t need = (size_t)kWarps * 2 * (d / ranks[0]);
     if (need > 2 * dv) extra = need;
   }
-  return 8 * (2 * (size_t)order * rm * rm + 5 * dv + 32 + extra);
+  return 8 * ((size_t)order * rm * rm + 5 * dv + 32 + extra);
 }
 
 }  // namespace
@@ -648,7 +658,7 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   a.rpart = a.part + (size_t)sh.m1 * 2 * sh.dprime;
   a.counter = reinterpret_cast<unsigned*>(a.rpart + 1024);
   a.status = status_dev;
-  a.linv = spec.linv;
+  a.pinv = spec.pinv;
   a.linv_stride = spec.linv_stride;
   a.linv_ok = spec.linv_ok;
   a.grams = spec.grams;
@@ -666,9 +676,12 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
     a.prof = prof_buf;
   }
   RTB_CUDA(cudaMemsetAsync(a.counter, 0, 64, st));
-  void* fn = rm == 8 ? (void*)k_pcg<8> : rm == 16 ? (void*)k_pcg<16> : (void*)k_pcg<32>;
-  static bool attr_set[3] = {false, false, false};
-  const int slot = rm == 8 ? 0 : rm == 16 ? 1 : 2;
+  bool all16 = true;
+  for (int n = 0; n < spec.order; ++n) all16 &= spec.ranks[n] == 16;
+  void* fn = all16 ? (void*)k_pcg<16, 16>
+             : rm == 8 ? (void*)k_pcg<8, 0> : rm == 16 ? (void*)k_pcg<16, 0> : (void*)k_pcg<32, 0>;
+  static bool attr_set[4] = {false, false, false, false};
+  const int slot = all16 ? 3 : rm == 8 ? 0 : rm == 16 ? 1 : 2;
   if (!attr_set[slot]) {
     RTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr_set[slot] = true;
@@ -684,9 +697,8 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
     RTB_CUDA(cudaStreamSynchronize(st));
     std::fprintf(stderr,
                  "[pcg] d=%d iters=%d status=%d ns: slice %llu bar1 %llu reduce %llu bar2 %llu "
-                 "vec %llu precond %llu tail %llu | stages %llu %llu %llu %llu %llu %llu\n",
-                 d, stat[1], stat[0], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[8], h[9], h[10],
-                 h[11], h[12], h[13]);
+                 "vec %llu precond %llu tail %llu | stages %llu %llu %llu\n",
+                 d, stat[1], stat[0], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[8], h[9], h[10]);
   }
 }
 

@@ -114,7 +114,7 @@ struct PcgSpec {
   int ranks[8];
   int d;
   double lambda;
-  const double* linv;   // per mode (stride linv_stride): L_n^-1 of A_n^T A_n (k_spd_small)
+  const double* pinv;   // per mode (stride linv_stride): (A_n^T A_n)^-1 (k_spd_small)
   int linv_stride;
   const int* linv_ok;   // per mode: Cholesky succeeded (any 0 -> status 3)
   const double* grams;  // per mode (same stride): A_n^T A_n

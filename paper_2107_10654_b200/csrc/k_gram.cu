@@ -29,6 +29,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <type_traits>
 
 namespace rtb {
 
@@ -40,6 +41,11 @@ constexpr int LDB = TB + 4;     // padded smem rows (phase B operands)
 constexpr int LDC = TNC + 4;    // padded smem rows (phase C H chunk)
 constexpr int kTh = 192;        // 6 warps, one 8-row m-tile each
 constexpr int kMaxRow = 256;    // max concatenated factor-row length (modes >= 2)
+constexpr int kRhsSplit = 16;   // bucket groups of the two-level rhs reduction
+constexpr int kBT = 18;         // whole-bucket kernel: up to 18 x 18 tiles of 8 x 8
+constexpr int kBWarps = 18;     // ... 18 warps, warp w owns row tile w (second tile unused)
+constexpr int LDZ = kBT * 8 + 4;
+static_assert(kBWarps * 32 == 4 * kBT * 8, "generation maps 4 threads per column");
 
 // Vech/split description shared by the kernels.
 struct VechSpec {
@@ -103,6 +109,11 @@ struct GramLayout {
   double* S;      // [m_1][Hsz]
   void* cub_tmp;
   size_t cub_bytes;
+  double* dw2;    // [s] w^2 of the k-th data draw in bucket order
+  double* dwx;    // [s] w^2 x
+  int* dmode;     // [N][s] mode indices
+  double* rhs_part;  // [kRhsSplit][d]
+  double* drow;   // [s][rowlen] concatenated factor rows of modes >= 2, bucket order
 };
 
 int key_bits(int I1) {
@@ -141,6 +152,11 @@ size_t carve(const GramSpec& spec, F&& take) {
   t((size_t)I1 * spec.dprime * 8);
   t((size_t)v.m[0] * v.Hsz * 8);
   t(cub_sort_bytes(spec.s, key_bits(I1)));
+  t(spec.s * 8);                               // dw2: w^2 per sorted data draw
+  t(spec.s * 8);                               // dwx: w^2 x per sorted data draw
+  t(spec.s * 4 * (size_t)spec.order);          // dmode[n][k]
+  t((size_t)kRhsSplit * spec.d * 8);           // rhs partials
+  t(spec.s * (size_t)v.rowlen * 8);            // drow: factor rows (modes >= 2) per draw
   return total;
 }
 
@@ -165,6 +181,11 @@ GramLayout layout(const GramSpec& spec, void* base) {
       case 11: l.h = (double*)q; break;
       case 12: l.S = (double*)q; break;
       case 13: l.cub_tmp = q; l.cub_bytes = bytes; break;
+      case 14: l.dw2 = (double*)q; break;
+      case 15: l.dwx = (double*)q; break;
+      case 16: l.dmode = (int*)q; break;
+      case 17: l.rhs_part = (double*)q; break;
+      case 18: l.drow = (double*)q; break;
     }
   });
   return l;
@@ -439,6 +460,322 @@ __global__ void __launch_bounds__(256) k_bucket_h(GramSpec spec, const double* _
   }
 }
 
+// (A') draw records in bucket order: one parallel gather of x and one decode of
+// the flat index per data draw, so the bucket kernels stream contiguous arrays.
+__global__ void k_gather_draws(GramSpec spec, const double* __restrict__ x,
+                               const unsigned long long* __restrict__ idx,
+                               const double* __restrict__ w, const unsigned* __restrict__ order,
+                               const unsigned* __restrict__ keys_sorted, double* __restrict__ dw2,
+                               double* __restrict__ dwx, int* __restrict__ dmode) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (long long)spec.s) return;
+  if (keys_sorted[k] >= (unsigned)spec.rows[0]) return;  // augmented draws sort last
+  const unsigned tt = order[k];
+  unsigned long long flat = idx[tt];
+  const double xv = __ldg(x + flat);
+  for (int n = spec.order - 1; n >= 0; --n) {
+    const unsigned long long rn = (unsigned long long)spec.rows[n];
+    dmode[(size_t)n * spec.s + k] = (int)(flat % rn);
+    flat /= rn;
+  }
+  const double wt = w[tt];
+  const double w2 = wt * wt;
+  dw2[k] = w2;
+  dwx[k] = w2 * xv;
+}
+
+// drow[k][q] = a_n(i_n(k))[q - roff[n]] for modes n >= 2 (coalesced writes).
+__global__ void k_gather_rows(GramSpec spec, VechSpec v, const unsigned* __restrict__ keys_sorted,
+                              const int* __restrict__ dmode, double* __restrict__ drow) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int RL = v.rowlen;
+  if (e >= (long long)spec.s * RL) return;
+  const long long k = e / RL;
+  const int q = (int)(e - k * RL);
+  if (keys_sorted[k] >= (unsigned)spec.rows[0]) return;
+  int n = 1;
+  while (n + 1 < v.N && q >= v.roff[n + 1]) ++n;
+  if (n >= v.N) return;
+  const int in = dmode[(size_t)n * spec.s + k];
+  drow[e] = __ldg(spec.factors[n] + (size_t)in * v.R[n] + (q - v.roff[n]));
+}
+
+// (B') one CTA per bucket computes the whole H_b (Mrow x Ncol <= 144 x 144) so
+// the operand generation is done once per bucket and amortised over up to
+// 18 x 18 DMMA tiles per K step. 9 warps; warp w owns row tiles w and w + 9; NTT
+// column tiles are computed unconditionally (operands are zero-padded), so the
+// DMMA stream has no branches. With HPT > 0 the same CTA also accumulates the
+// rhs ingredient h_b[p'] = sum_t w_t^2 x_t prod_{n>=1} a_n(i_n)[p_n] from the
+// staged factor rows (HPT outputs per thread).
+// cp.async one chunk of draw records (KC draws: factor rows, w^2, w^2 x) into buffer buf.
+template <int HPT>
+__device__ __forceinline__ void stage_bucket_chunk(const double* __restrict__ drow,
+                                                   const double* __restrict__ dw2,
+                                                   const double* __restrict__ dwx, double* frow,
+                                                   double* w2s, double* wxs, int start, int len,
+                                                   int k0, int buf, int RL, int RLp) {
+  const int kn = min(KC, len - k0);
+  double* fr = frow + buf * KC * RLp;
+  for (int e = threadIdx.x; e < KC * RL; e += blockDim.x) {
+    const int k = e / RL, q = e - k * RL;
+    const bool ok = k < kn;
+    cp_async8(fr + k * RLp + q, ok ? drow + (size_t)(start + k0 + k) * RL + q : drow, ok);
+  }
+  if (threadIdx.x < KC) {
+    const bool ok = (int)threadIdx.x < kn;
+    cp_async8(w2s + buf * KC + threadIdx.x, ok ? dw2 + start + k0 + threadIdx.x : dw2, ok);
+    if (HPT > 0) cp_async8(wxs + buf * KC + threadIdx.x, ok ? dwx + start + k0 + threadIdx.x : dwx, ok);
+  }
+}
+
+template <int NTT, int HPT, int NR, int NC>
+__global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
+    GramSpec spec, VechSpec v, const double* __restrict__ dw2, const double* __restrict__ dwx,
+    const double* __restrict__ drow, const int* __restrict__ bstart, const int* __restrict__ blen,
+    const int* __restrict__ nbuckets, double* __restrict__ H, double* __restrict__ h) {
+  extern __shared__ __align__(16) double smb[];
+  const int RL = v.rowlen;
+  const int RLp = (RL + 1) & ~1;
+  double* zr = smb;                   // [KC][LDZ]
+  double* zc = zr + KC * LDZ;         // [KC][LDZ]
+  double* frow = zc + KC * LDZ;       // [2][KC][RLp] (double buffered)
+  double* w2s = frow + 2 * KC * RLp;  // [2][KC]
+  double* wxs = w2s + 2 * KC;         // [2][KC]
+  const int b = blockIdx.x;
+  if (b >= *nbuckets) return;
+  const int N = v.N;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int MT = (int)((v.Mrow + 7) / 8);
+  // generation: thread -> fixed column c, rows k = k0r + 4 j (576 threads = 4 x 144)
+  const int c = tid % (kBT * 8), k0r = tid / (kBT * 8);
+  // (p, q) factor-row offsets of this thread's column in the row / column groups
+  int ro[2 * (NR > 0 ? NR : 1)], co[2 * (NC > 0 ? NC : 1)];
+  {
+    long long u = c < v.Mrow ? c : 0;
+#pragma unroll
+    for (int j = NR - 1; j >= 0; --j) {  // row group = modes 1..NR (last fastest)
+      const int n = 1 + j;
+      const int un = (int)(u % v.m[n]);
+      u /= v.m[n];
+      int pa, pb;
+      pair_of(un, v.R[n], pa, pb);
+      ro[2 * j] = v.roff[n] + pa;
+      ro[2 * j + 1] = v.roff[n] + pb;
+    }
+    u = c < v.Ncol ? c : 0;
+#pragma unroll
+    for (int j = NC - 1; j >= 0; --j) {  // column group = modes NR+1..NR+NC
+      const int n = 1 + NR + j;
+      const int un = (int)(u % v.m[n]);
+      u /= v.m[n];
+      int pa, pb;
+      pair_of(un, v.R[n], pa, pb);
+      co[2 * j] = v.roff[n] + pa;
+      co[2 * j + 1] = v.roff[n] + pb;
+    }
+  }
+  const bool rok = c < v.Mrow, cok = c < v.Ncol;
+  // HPT == 1 (3-way, R_2, R_3 <= 16): the spare warp kBWarps-1 (row tiles <= 17)
+  // accumulates h_b[p2][p3] = sum_t (w^2 x a_2)[p2] a_3[p3] with 4 DMMA tiles.
+  const bool hwarp = HPT > 0 && warp == kBWarps - 1;
+  double hacc[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+  const int start = bstart[b], len = blen[b];
+  double acc[NTT][2];
+#pragma unroll
+  for (int j = 0; j < NTT; ++j) acc[j][0] = acc[j][1] = 0.0;
+  const int rt0 = warp;
+  if (len > 0) stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, 0, 0, RL, RLp);
+  cp_async_commit();
+  for (int k0 = 0, it = 0; k0 < len; k0 += KC, ++it) {
+    const int cur = it & 1;
+    if (k0 + KC < len)
+      stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, k0 + KC, cur ^ 1, RL,
+                              RLp);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();  // chunk `cur` landed; previous MMA readers of zr / zc are done
+    const double* fr = frow + cur * KC * RLp;
+    const double* w2c = w2s + cur * KC;
+#pragma unroll 4
+    for (int j = 0; j < KC / 4; ++j) {
+      const int k = k0r + 4 * j;
+      const double* f = fr + k * RLp;
+      double zrv = 0.0, zcv = 0.0;
+      if (rok) {
+        zrv = w2c[k];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) zrv *= f[ro[2 * q]] * f[ro[2 * q + 1]];
+      }
+      if (cok) {
+        zcv = 1.0;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) zcv *= f[co[2 * q]] * f[co[2 * q + 1]];
+      }
+      zr[k * LDZ + c] = zrv;
+      zc[k * LDZ + c] = zcv;
+    }
+    if (hwarp) {
+      const double* wxc = wxs + cur * KC;
+      const int R2 = v.R[1], R3 = v.R[2], o2 = v.roff[1], o3 = v.roff[2];
+#pragma unroll
+      for (int ks = 0; ks < KC / 4; ++ks) {
+        const int k = ks * 4 + t4;
+        const double* f = fr + k * RLp;
+        const double wk = wxc[k];
+        double af[2], bf[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          af[i] = (i * 8 + g < R2) ? wk * f[o2 + i * 8 + g] : 0.0;
+          bf[i] = (i * 8 + g < R3) ? f[o3 + i * 8 + g] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma_8x8x4(hacc[i][j][0], hacc[i][j][1], af[i], bf[j]);
+      }
+    }
+    __syncthreads();
+    if (rt0 < MT) {
+#pragma unroll
+      for (int ks = 0; ks < KC / 4; ++ks) {
+        const double* zrk = zr + (ks * 4 + t4) * LDZ;
+        const double* zck = zc + (ks * 4 + t4) * LDZ;
+        const double a0 = zrk[rt0 * 8 + g];
+#pragma unroll
+        for (int nt = 0; nt < NTT; ++nt) dmma_8x8x4(acc[nt][0], acc[nt][1], a0, zck[nt * 8 + g]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  double* Hb = H + (size_t)b * v.Hsz;
+  {
+    const long long r = (long long)rt0 * 8 + g;
+    if (rt0 < MT && r < v.Mrow) {
+#pragma unroll
+      for (int nt = 0; nt < NTT; ++nt) {
+        const long long cc = (long long)nt * 8 + 2 * t4;
+        if (cc < v.Ncol) Hb[r * v.Ncol + cc] = acc[nt][0];
+        if (cc + 1 < v.Ncol) Hb[r * v.Ncol + cc + 1] = acc[nt][1];
+      }
+    }
+  }
+  if (hwarp) {
+    const int R2 = v.R[1], R3 = v.R[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int p2 = i * 8 + g, p3 = j * 8 + 2 * t4;
+        if (p2 < R2 && p3 < R3) h[(size_t)b * spec.dprime + p2 * R3 + p3] = hacc[i][j][0];
+        if (p2 < R2 && p3 + 1 < R3) h[(size_t)b * spec.dprime + p2 * R3 + p3 + 1] = hacc[i][j][1];
+      }
+  }
+}
+
+size_t vech_bucket2_smem(const VechSpec& v) {
+  const size_t rlp = (size_t)((v.rowlen + 1) & ~1);
+  return (size_t)(2 * KC * LDZ + 2 * KC * rlp + 4 * KC) * 8 + 16;
+}
+
+// h_b[p'] = sum_{t in b} w_t^2 x_t prod_{n>=1} a_n(i_n)[p_n] from the draw records.
+__global__ void __launch_bounds__(256) k_bucket_h2(GramSpec spec, const double* __restrict__ dwx,
+                                                   const int* __restrict__ dmode,
+                                                   const int* __restrict__ bstart,
+                                                   const int* __restrict__ blen,
+                                                   const int* __restrict__ nbuckets,
+                                                   double* __restrict__ h) {
+  const int b = blockIdx.x;
+  if (b >= *nbuckets) return;
+  const int N = spec.order, dp = spec.dprime;
+  const int start = bstart[b], len = blen[b];
+  for (int p = threadIdx.x; p < dp; p += blockDim.x) {
+    int pn[kMaxOrder];
+    {
+      int rem = p;
+      for (int n = N - 1; n >= 1; --n) {
+        pn[n] = rem % spec.ranks[n];
+        rem /= spec.ranks[n];
+      }
+    }
+    double acc = 0.0;
+    for (int k = 0; k < len; ++k) {
+      double z = __ldg(dwx + start + k);
+      for (int n = 1; n < N; ++n)
+        z *= __ldg(spec.factors[n] + (size_t)__ldg(dmode + (size_t)n * spec.s + start + k) *
+                                         spec.ranks[n] + pn[n]);
+      acc += z;
+    }
+    h[(size_t)b * dp + p] = acc;
+  }
+}
+
+// h_b from the contiguous draw records (drow rows are shared by the whole CTA -> L1).
+__global__ void __launch_bounds__(256) k_bucket_h3(GramSpec spec, VechSpec v,
+                                                   const double* __restrict__ dwx,
+                                                   const double* __restrict__ drow,
+                                                   const int* __restrict__ bstart,
+                                                   const int* __restrict__ blen,
+                                                   const int* __restrict__ nbuckets,
+                                                   double* __restrict__ h) {
+  const int b = blockIdx.x;
+  if (b >= *nbuckets) return;
+  const int N = spec.order, dp = spec.dprime, RL = v.rowlen;
+  const int start = bstart[b], len = blen[b];
+  for (int p = threadIdx.x; p < dp; p += blockDim.x) {
+    int hq[kMaxOrder];
+    int rem = p;
+#pragma unroll
+    for (int n = kMaxOrder - 1; n >= 1; --n) {
+      hq[n] = 0;
+      if (n < N) {
+        hq[n] = v.roff[n] + rem % v.R[n];
+        rem /= v.R[n];
+      }
+    }
+    double acc = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < len; ++k) {
+      const double* f = drow + (size_t)(start + k) * RL;
+      double z = __ldg(dwx + start + k);
+#pragma unroll
+      for (int n = 1; n < kMaxOrder; ++n)
+        if (n < N) z *= __ldg(f + hq[n]);
+      acc += z;
+    }
+    h[(size_t)b * dp + p] = acc;
+  }
+}
+
+// rhs, two levels: partial[g][p1 * d' + p'] = sum_{b in group g} A1[i1_b, p1] h[b, p'],
+// then rhs = sum_g partial[g] (fixed order).
+__global__ void __launch_bounds__(256) k_rhs_part(GramSpec spec, const double* __restrict__ h,
+                                                  const int* __restrict__ bi1,
+                                                  const int* __restrict__ nbuckets,
+                                                  double* __restrict__ part) {
+  const int R1 = spec.ranks[0], dp = spec.dprime;
+  const int grp = blockIdx.y;
+  const int nb = *nbuckets;
+  const int per = (nb + kRhsSplit - 1) / kRhsSplit;
+  const int b0 = grp * per, b1 = min(nb, b0 + per);
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)spec.d) return;
+  const int p1 = (int)(e / dp), pp = (int)(e - (long long)p1 * dp);
+  double s = 0.0;
+  for (int b = b0; b < b1; ++b)
+    s = fma(__ldg(spec.factors[0] + (size_t)__ldg(bi1 + b) * R1 + p1),
+            __ldg(h + (size_t)b * dp + pp), s);
+  part[(size_t)grp * spec.d + e] = s;
+}
+
+__global__ void k_rhs_sum(int d, const double* __restrict__ part, double* __restrict__ rhs) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d) return;
+  double s = 0.0;
+  for (int g = 0; g < kRhsSplit; ++g) s += part[(size_t)g * d + e];
+  rhs[e] = s;
+}
+
 // (C) S[u0, U] = sum_b vech(a0 a0^T)(i0_b)[u0] H[b, U]: M = m_0, N = Hsz, K = buckets.
 // grid = (ceil(Hsz/64), ceil(m0/48)), block 192: warp w -> m-tile w, 8 n-tiles.
 __global__ void __launch_bounds__(kTh) k_vech_contract(GramSpec spec, VechSpec v,
@@ -619,27 +956,77 @@ void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
                                            l.vals_sorted, (int)spec.s, 0, key_bits(I1), st));
   k_bucket_scan<<<1, 1024, 0, st>>>(I1, l.counts, l.bstart, l.blen, l.bi1, l.nbuckets);
   RTB_LAUNCH_CHECK();
+  // draw records in bucket order (one gather of x per draw)
+  k_gather_draws<<<sb, 256, 0, st>>>(spec, x, idx, w, l.vals_sorted, l.keys_sorted, l.dw2, l.dwx,
+                                     l.dmode);
+  RTB_LAUNCH_CHECK();
   // Every bucket slot up to I1 is launched; blocks beyond *nbuckets exit.
-  const long long tiles_r = (v.Mrow + TB - 1) / TB, tiles_c = (v.Ncol + TB - 1) / TB;
-  k_vech_bucket<<<dim3((unsigned)(tiles_r * tiles_c), I1), kTh,
-                  (size_t)KC * v.rowlen * sizeof(double), st>>>(
-      spec, v, idx, w, l.vals_sorted, l.bstart, l.blen, l.nbuckets, l.H);
-  RTB_LAUNCH_CHECK();
-  k_bucket_h<<<I1, 256, 0, st>>>(spec, x, idx, w, l.vals_sorted, l.bstart, l.blen, l.nbuckets,
-                                 l.h);
-  RTB_LAUNCH_CHECK();
+  const int NTn = (int)((v.Ncol + 7) / 8);
+  const int nr = v.msplit, nc = v.N - 1 - v.msplit;
+  const bool whole = (v.Mrow + 7) / 8 <= kBT && NTn <= kBT && v.N >= 2 &&
+                     ((nr == 1 && nc <= 2) || (nr == 2 && nc == 1));
+  // h_b by the bucket kernel's spare warp in the 3-way case (R_2, R_3 <= 16)
+  const bool fused_h = whole && nr == 1 && nc == 1 && v.R[1] <= 16 && v.R[2] <= 16 &&
+                       (v.Mrow + 7) / 8 < kBWarps;
+  if (whole) {
+    k_gather_rows<<<(unsigned)ceil_div<unsigned long long>(spec.s * v.rowlen, 256ULL), 256, 0,
+                    st>>>(spec, v, l.keys_sorted, l.dmode, l.drow);
+    RTB_LAUNCH_CHECK();
+    const size_t smb = vech_bucket2_smem(v);
+    VechSpec vmax = v;
+    vmax.rowlen = kMaxRow;
+    const int smax = (int)vech_bucket2_smem(vmax);
+    auto launch = [&](auto kern) {
+      RTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+      kern<<<I1, kBWarps * 32, smb, st>>>(spec, v, l.dw2, l.dwx, l.drow, l.bstart, l.blen,
+                                          l.nbuckets, l.H, l.h);
+      RTB_LAUNCH_CHECK();
+    };
+    // (NR, NC) = (1, 1) for 3-way; (1, 0) for 2-way; (1, 2) / (2, 1) for 4-way
+    auto by_nt = [&](auto hpt, auto nrt, auto nct) {
+      constexpr int H_ = decltype(hpt)::value, R_ = decltype(nrt)::value, C_ = decltype(nct)::value;
+      if (NTn <= 4) launch(k_vech_bucket2<4, H_, R_, C_>);
+      else if (NTn <= 8) launch(k_vech_bucket2<8, H_, R_, C_>);
+      else if (NTn <= 12) launch(k_vech_bucket2<12, H_, R_, C_>);
+      else launch(k_vech_bucket2<18, H_, R_, C_>);
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1c = std::integral_constant<int, 1>;
+    using I2c = std::integral_constant<int, 2>;
+    auto by_groups = [&](auto hpt) {
+      if (nr == 1 && nc == 1) by_nt(hpt, I1c{}, I1c{});
+      else if (nr == 1 && nc == 0) by_nt(hpt, I1c{}, I0{});
+      else if (nr == 1 && nc == 2) by_nt(hpt, I1c{}, I2c{});
+      else by_nt(hpt, I2c{}, I1c{});
+    };
+    if (fused_h) by_nt(I1c{}, I1c{}, I1c{});
+    else by_groups(I0{});
+  } else {
+    const long long tiles_r = (v.Mrow + TB - 1) / TB, tiles_c = (v.Ncol + TB - 1) / TB;
+    k_vech_bucket<<<dim3((unsigned)(tiles_r * tiles_c), I1), kTh,
+                    (size_t)KC * v.rowlen * sizeof(double), st>>>(
+        spec, v, idx, w, l.vals_sorted, l.bstart, l.blen, l.nbuckets, l.H);
+    RTB_LAUNCH_CHECK();
+  }
+  if (whole && !fused_h) {
+    k_bucket_h3<<<I1, 256, 0, st>>>(spec, v, l.dwx, l.drow, l.bstart, l.blen, l.nbuckets, l.h);
+    RTB_LAUNCH_CHECK();
+  } else if (!fused_h) {
+    k_bucket_h2<<<I1, 256, 0, st>>>(spec, l.dwx, l.dmode, l.bstart, l.blen, l.nbuckets, l.h);
+    RTB_LAUNCH_CHECK();
+  }
   k_vech_contract<<<dim3((unsigned)((v.Hsz + TNC - 1) / TNC), (unsigned)ceil_div(v.m[0], TB)),
                     kTh, 0, st>>>(spec, v, l.H, l.bi1, l.nbuckets, l.S);
   RTB_LAUNCH_CHECK();
-  // augmented rows: each adds (w^2 sqrt(lambda)) sqrt(lambda) to its diagonal,
-  // w = sqrt((1/s) / (0.5/d)) (ref sketch_ridge.cpp:88, 18-36, 115-120)
   const double aug_term = gram_aug_term(spec);
   if (gram) {
     k_vech_expand<<<kNumSMs * 8, 256, 0, st>>>(spec, v, l.S, l.aug_count, aug_term, gram);
     RTB_LAUNCH_CHECK();
   }
-  k_rhs<<<dim3(ceil_div(spec.dprime, 64), spec.ranks[0]), 256, 0, st>>>(spec, l.h, l.bi1,
-                                                                        l.nbuckets, rhs);
+  k_rhs_part<<<dim3(ceil_div(spec.d, 256), kRhsSplit), 256, 0, st>>>(spec, l.h, l.bi1,
+                                                                      l.nbuckets, l.rhs_part);
+  RTB_LAUNCH_CHECK();
+  k_rhs_sum<<<ceil_div(spec.d, 256), 256, 0, st>>>(spec.d, l.rhs_part, rhs);
   RTB_LAUNCH_CHECK();
 }
 

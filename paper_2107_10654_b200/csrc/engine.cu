@@ -683,11 +683,9 @@ class Engine {
       if (J == 1) {
         Scope sc(prof_, "ttm_last");
         ttm_last(in, O, I, W, Rn, out, nullptr, nullptr, st_);
-      } else if (O <= 65535 && J >= 64) {
+      } else if (J >= 2) {
         Scope sc(prof_, "ttm_mid");
-        ttm_mid(in, (int)O, I, J, W, Rn, out, st_);
-      } else if (J <= 32 && ttm_smallj(in, O, I, (int)J, W, Rn, out, st_)) {
-        // short contiguous tail (e.g. T x_2 A_2^T with J = R_3)
+        ttm_mid(in, O, I, J, W, Rn, out, st_);
       } else {
         Scope sc(prof_, "ttm_generic");
         ttm_generic(in, O, I, J, W, wr, wi, Rn, out, st_);

@@ -151,30 +151,46 @@ __global__ void __launch_bounds__(128) k_ttm_last(const double* __restrict__ X, 
 }
 
 // ---------------------------------------------------------------------------
-// Strided-mode contraction: X viewed as (O, I, J), out (O, R, J).
-// grid = (ceil(J/64), O); block 128 (4 warps x 16 columns).
+// Strided-mode contraction: X viewed as (O, I, J), out (O, R, J). Columns are
+// the flattened (o, j) pairs (so small J packs several o into one 64-column
+// tile); blockIdx.y splits the I reduction (ksplit > 1 writes partial sums to
+// out + split * O*R*J, summed in fixed order by k_sum_splits).
+// block 128 (4 warps x 16 columns).
 template <int RP, int VEC>
-__global__ void __launch_bounds__(128) k_ttm_mid(const double* __restrict__ X, int O, int I,
+__global__ void __launch_bounds__(128) k_ttm_mid(const double* __restrict__ X, long long O, int I,
                                                  long long J, const double* __restrict__ A, int R,
-                                                 double* __restrict__ out) {
+                                                 double* __restrict__ out, int ich) {
   constexpr int BJ = 64;
   constexpr int LD = BJ + kPadX;
   extern __shared__ __align__(16) double xs[];  // [kStages][kBK][LD]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const long long j0 = (long long)blockIdx.x * BJ;
-  const long long o = blockIdx.y;
-  const double* Xo = X + o * I * J;
-  const int nchunks = ceil_div(I, kBK);
+  const long long ncol = O * J;
+  const long long c0 = (long long)blockIdx.x * BJ;
+  const int ibeg = blockIdx.y * ich, iend = min(I, ibeg + ich);
+  const int nchunks = ceil_div(iend - ibeg, kBK);
+  double* dst_out = out + (long long)blockIdx.y * O * R * J;
 
+  // whole tile inside one o (J % 64 == 0): no per-element index division
+  const bool one_o = (J % BJ) == 0;
+  const long long o_t = one_o ? c0 / J : 0, j_t = one_o ? c0 - o_t * J : 0;
   auto load_chunk = [&](int c, int stage) {
     double* dst = xs + stage * kBK * LD;
-    const int i0 = c * kBK;
+    const int i0 = ibeg + c * kBK;
     constexpr int PER_ROW = BJ / VEC;
     for (int e = tid; e < kBK * PER_ROW; e += 128) {
       const int r = e / PER_ROW, col = (e % PER_ROW) * VEC;
-      const bool ok = (i0 + r < I) && (j0 + col < J);
-      const double* src = ok ? Xo + (long long)(i0 + r) * J + j0 + col : X;
+      const long long cc = c0 + col;
+      const bool ok = (i0 + r < iend) && (cc < ncol);
+      long long o, j;
+      if (one_o) {
+        o = o_t;
+        j = j_t + col;
+      } else {
+        o = ok ? cc / J : 0;
+        j = ok ? cc - o * J : 0;
+      }
+      const double* src = ok ? X + (o * I + i0 + r) * J + j : X;
       if (VEC == 2)
         cp_async16(dst + r * LD + col, src, ok);
       else
@@ -199,7 +215,7 @@ __global__ void __launch_bounds__(128) k_ttm_mid(const double* __restrict__ X, i
     if (c + kStages - 1 < nchunks) load_chunk(c + kStages - 1, (c + kStages - 1) % kStages);
     cp_async_commit();
     const double* xt = xs + (c % kStages) * kBK * LD;
-    const int i0 = c * kBK;
+    const int i0 = ibeg + c * kBK;
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
       const int i = i0 + ks * 4 + t;
@@ -207,7 +223,7 @@ __global__ void __launch_bounds__(128) k_ttm_mid(const double* __restrict__ X, i
 #pragma unroll
       for (int mt = 0; mt < RP / 8; ++mt) {
         const int r = mt * 8 + g;
-        af[mt] = (i < I && r < R) ? __ldg(A + (size_t)i * R + r) : 0.0;
+        af[mt] = (i < iend && r < R) ? __ldg(A + (size_t)i * R + r) : 0.0;
       }
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
@@ -224,12 +240,26 @@ __global__ void __launch_bounds__(128) k_ttm_mid(const double* __restrict__ X, i
     if (r >= R) continue;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
-      const long long j = j0 + warp * 16 + nt * 8 + 2 * t;
-      double* dst = out + (o * R + r) * J + j;
-      if (j < J) dst[0] = acc[mt][nt][0];
-      if (j + 1 < J) dst[1] = acc[mt][nt][1];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long cc = c0 + warp * 16 + nt * 8 + 2 * t + h;
+        if (cc < ncol) {
+          const long long o = one_o ? o_t : cc / J;
+          const long long j = one_o ? j_t + (cc - c0) : cc - o * J;
+          dst_out[(o * R + r) * J + j] = acc[mt][nt][h];
+        }
+      }
     }
   }
+}
+
+__global__ void k_sum_splits(const double* __restrict__ part, long long n, int splits,
+                             double* __restrict__ out) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double s = 0.0;
+  for (int k = 0; k < splits; ++k) s += part[(long long)k * n + e];
+  out[e] = s;
 }
 
 // ---------------------------------------------------------------------------
@@ -421,8 +451,23 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
 #undef RTB_L
 }
 
+// per-device scratch for split-K partial sums (grown on demand, stream-ordered)
+static double* splits_scratch(size_t bytes, cudaStream_t st) {
+  static double* buf[16] = {};
+  static size_t cap[16] = {};
+  int dev = 0;
+  RTB_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) throw Error(4, "ttm_mid: device index");
+  if (cap[dev] < bytes) {
+    if (buf[dev]) RTB_CUDA(cudaFreeAsync(buf[dev], st));
+    RTB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf[dev]), bytes, st));
+    cap[dev] = bytes;
+  }
+  return buf[dev];
+}
+
 template <int RP, int VEC>
-static void launch_mid(const double* X, int O, int I, long long J, const double* A, int R,
+static void launch_mid(const double* X, long long O, int I, long long J, const double* A, int R,
                        double* out, cudaStream_t st) {
   constexpr int smem = kStages * kBK * (64 + kPadX) * sizeof(double);
   auto k = k_ttm_mid<RP, VEC>;
@@ -431,12 +476,24 @@ static void launch_mid(const double* X, int O, int I, long long J, const double*
     RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  dim3 grid((unsigned)ceil_div<long long>(J, 64), (unsigned)O);
-  k<<<grid, 128, smem, st>>>(X, O, I, J, A, R, out);
+  const long long tiles = ceil_div<long long>(O * J, 64);
+  // split the reduction when the column tiles alone cannot fill the GPU
+  int splits = 1;
+  while (tiles * splits < 6LL * kNumSMs && I / (splits * 2) >= 2 * kBK) splits *= 2;
+  const int ich = ceil_div(ceil_div(I, splits), kBK) * kBK;
+  splits = ceil_div(I, ich);
+  const long long n = O * R * J;
+  double* dst = splits > 1 ? splits_scratch((size_t)splits * n * 8, st) : out;
+  dim3 grid((unsigned)tiles, (unsigned)splits);
+  k<<<grid, 128, smem, st>>>(X, O, I, J, A, R, dst, ich);
   RTB_LAUNCH_CHECK();
+  if (splits > 1) {
+    k_sum_splits<<<(unsigned)ceil_div<long long>(n, 256), 256, 0, st>>>(dst, n, splits, out);
+    RTB_LAUNCH_CHECK();
+  }
 }
 
-void ttm_mid(const double* X, int O, int I, long long J, const double* A, int R, double* out,
+void ttm_mid(const double* X, long long O, int I, long long J, const double* A, int R, double* out,
              cudaStream_t st) {
   const bool v2 = (J % 2) == 0;
   const int rp = R <= 8 ? 8 : R <= 16 ? 16 : R <= 24 ? 24 : 32;

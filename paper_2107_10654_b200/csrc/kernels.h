@@ -43,7 +43,7 @@ long long ttm_last_blocks(long long O);
 void ttm_last(const double* X, long long O, int I, const double* A, int R, double* T,
               const double* P, double* partial, cudaStream_t st);
 // out[o,r,j] = sum_i A[i,r] X[o,i,j]
-void ttm_mid(const double* X, int O, int I, long long J, const double* A, int R, double* out,
+void ttm_mid(const double* X, long long O, int I, long long J, const double* A, int R, double* out,
              cudaStream_t st);
 // out[o,r,j] = sum_i W[r*wr + i*wi] X[o,i,j]
 void ttm_generic(const double* X, long long O, int I, long long J, const double* W, long long wr,

@@ -64,7 +64,11 @@ typedef struct rtucker_b200_als_ext {
    * every augmented row was drawn and d fits, verified by its true residual;
    * Cholesky otherwise or on failure), 1 = always Cholesky. */
   int core_solver;
-  int reserved[6];
+  /* 1 = loss by ||X||^2 - 2<Y,G> + <Q,G> (one cheaper X pass; ~1e-12 ||X||^2
+   * absolute accuracy, falls back to the direct residual near an exact fit);
+   * 0 (default) = the reference's direct residual pass. */
+  int fast_loss;
+  int reserved[5];
 } rtucker_b200_als_ext;
 
 rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* ranks,

@@ -434,6 +434,7 @@ rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* 
       o.allreduce_user = ext->allreduce_user;
       o.profile = ext->profile_kernels != 0;
       o.core_solver = ext->core_solver;
+      o.fast_loss = ext->fast_loss != 0;
     }
     auto r = std::make_unique<rtucker_als_result>();
     rtb::als_run(x->device(), x->shape, std::vector<uint64_t>(ranks, ranks + order), o, r->out);
@@ -468,6 +469,7 @@ rtucker_status rtucker_b200_session_create(const rtucker_tensor* x, const uint64
       o.allreduce_user = ext->allreduce_user;
       o.profile = ext->profile_kernels != 0;
       o.core_solver = ext->core_solver;
+      o.fast_loss = ext->fast_loss != 0;
     }
     auto s = std::make_unique<rtucker_b200_session>();
     s->s.reset(rtb::session_create(x->device(), x->shape,

@@ -124,6 +124,63 @@ __global__ void k_finish_loss(const double* residual, const double* reg, double 
   *rmse_out = sqrt(r / size);
 }
 
+// per-block partial sums of x^2 (||X||^2 for the fast loss)
+__global__ void k_sumsq_partials(const double* __restrict__ x, long long n, double* partial) {
+  __shared__ double red[32];
+  double s = 0.0;
+  const long long n2 = n >> 1;
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double2 v = __ldcs(x2 + i);
+    s = fma(v.x, v.x, s);
+    s = fma(v.y, v.y, s);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) s = fma(x[n - 1], x[n - 1], s);
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// Fast loss: sum (X - Xhat)^2 = ||X||^2 - 2 <Y, G> + <Q, G>, Y = X x_n A_n^T (all n),
+// Q = G x_n (A_n^T A_n) (all n). Accepted when the residual is >= thr ||X||^2 (the
+// cancellation then costs < ~1e-9 relative); otherwise *need = 1 and the direct
+// pass queued behind it runs.
+__global__ void k_fast_loss(const double* __restrict__ Y, const double* __restrict__ Q,
+                            const double* __restrict__ G, long long d,
+                            const double* __restrict__ xx, const double* __restrict__ reg,
+                            double lambda, double size, double thr, double* loss_out,
+                            double* rmse_out, int* need) {
+  __shared__ double red[32];
+  double a = 0.0, b = 0.0;
+  for (long long i = threadIdx.x; i < d; i += blockDim.x) {
+    a = fma(Y[i], G[i], a);
+    b = fma(Q[i], G[i], b);
+  }
+  a = block_sum<1024>(a, red);
+  __syncthreads();
+  b = block_sum<1024>(b, red);
+  if (threadIdx.x == 0) {
+    const double x2 = *xx;
+    const double r = (x2 - 2.0 * a) + b;
+    if (r >= thr * x2 && isfinite(r)) {
+      *loss_out = r + lambda * *reg;
+      *rmse_out = sqrt(r / size);
+      *need = 0;
+    } else {
+      *need = 1;
+    }
+  }
+}
+
+__global__ void k_finish_loss_guarded(const double* residual, const double* reg, double lambda,
+                                      double size, double* loss_out, double* rmse_out,
+                                      const int* need) {
+  if (*need == 0) return;
+  const double r = *residual;
+  *loss_out = r + lambda * *reg;
+  *rmse_out = sqrt(r / size);
+}
+
 __global__ void k_resid_partials(const double* x, const double* xh, long long n, double* partial) {
   __shared__ double red[32];
   double s = 0.0;
@@ -527,7 +584,8 @@ class Engine {
 
   DevBuf ns_vals_, pinv2_, linv_, spd_ok_;
   DevBuf core_, fac_, grams_, evals_, evecs_, eig_status_, ns_, pinv_, ranks_dev_;
-  DevBuf T_, P_, tmp_a_, tmp_b_, partial_, scal_, hist_, init_loss_;
+  DevBuf T_, P_, tmp_a_, tmp_b_, partial_, scal_, hist_, init_loss_, xx_, loss_need_, yq_;
+  bool xx_valid_ = false;
   DevBuf scores_, cdf_, sums_, score_off_, rows_dev_, cols_dev_, flag_;
   DevBuf sk_idx_, sk_w_, draw_work_, gram_work_, G_, rhs_, chol_work_, chol_status_,
       data_draws_, zero_flag_, U_[8], pgram_, pcg_work_, pcg_status_, blocks_;
@@ -616,10 +674,15 @@ class Engine {
     tmp_elems_ = mx;
     tmp_a_.ensure(mx * 8, st_);
     tmp_b_.ensure(mx * 8, st_);
-    const long long nblk = std::max<long long>(ttm_last_blocks((long long)(total_ / shape_[N_ - 1])),
-                                               kNumSMs * 8);
-    partial_.ensure(nblk * 8, st_);
+    const long long nblk = std::max<long long>(
+        ttm_last_blocks((long long)(total_ / shape_[N_ - 1]), (int)shape_[N_ - 1],
+                        (int)ranks_[N_ - 1]),
+        kNumSMs * 8);
+    partial_.ensure(std::max<size_t>(nblk, kNumSMs * 4) * 8, st_);
     scal_.ensure(4 * 8, st_);
+    xx_.ensure(8, st_);
+    loss_need_.ensure(8, st_);
+    yq_.ensure(2 * (d_ + 1) * 8, st_);
     hist_.ensure((size_t)std::max<uint32_t>(opt_.max_iterations, 1) * (N_ + 1) * 16 + 16, st_);
     init_loss_.ensure(16, st_);
     uint64_t sum_rows = 0;
@@ -677,9 +740,10 @@ class Engine {
     const long long O = (long long)prod(dims, 0, m);
     const int I = (int)dims[m];
     const long long J = (long long)prod(dims, m + 1);
-    const long long size = O * I * J;
-    const bool big = size >= (1 << 20);
-    if (big && w_is_At && Rn <= 32) {
+    // DMMA paths whenever the reduction is long enough to matter; the scalar
+    // generic kernel only for tiny contractions
+    const bool dmma = w_is_At && Rn <= 32 && I >= 16 && O * I * J >= 4096;
+    if (dmma) {
       if (J == 1) {
         Scope sc(prof_, "ttm_last");
         ttm_last(in, O, I, W, Rn, out, nullptr, nullptr, st_);
@@ -1105,18 +1169,95 @@ class Engine {
     return cur;
   }
 
-  // Loss pass (fused with T = X x_N A_N^T). Writes loss/rmse to device ptrs.
+  // Loss (ref tucker.cpp:216-229). Default: the direct residual, fused with T. Opt-in
+  // fast form (opt_.fast_loss; ~1e-12 ||X||^2 absolute error, so not the default):
+  // T = X x_N A_N^T (reused by the next sweep's factor updates), Y = T x_{n<N} A_n^T,
+  // Q = G x_n (A_n^T A_n); loss from ||X||^2 - 2<Y,G> + <Q,G>, with the direct
+  // residual pass (fused with T) enqueued behind it under a device guard for the
+  // near-exact-fit case where the cancellation would cost accuracy.
   void loss_pass(double* loss_dev, double* rmse_dev) {
+    const int R = (int)ranks_[N_ - 1];
+    if (N_ >= 2 && R <= 32 && opt_.fast_loss) {
+      if (!xx_valid_) {
+        Scope sc(prof_, "loss_norm_x");
+        const int nb = kNumSMs * 4;
+        k_sumsq_partials<<<nb, 256, 0, st_>>>(x_, (long long)total_, partial_.as<double>());
+        RTB_LAUNCH_CHECK();
+        sum_partials(partial_.as<double>(), nb, xx_.as<double>(), st_);
+        xx_valid_ = true;
+      }
+      if (!t_valid_) compute_T();
+      double* Y = yq_.as<double>();
+      double* Q = Y + d_ + 1;
+      {
+        Scope sc(prof_, "loss_small");
+        // Y = T x_1 A_1^T ... x_{N-1} A_{N-1}^T
+        std::vector<uint64_t> dims = shape_;
+        dims[N_ - 1] = ranks_[N_ - 1];
+        const double* cur = T_.as<double>();
+        double* bufs[2] = {tmp_a_.as<double>(), tmp_b_.as<double>()};
+        int which = 0;
+        for (int m = 0; m < N_ - 1; ++m) {
+          double* out = (m == N_ - 2) ? Y : bufs[which];
+          mode_product(cur, dims, m, factor(m), 1, (int)ranks_[m], (int)ranks_[m], out, true);
+          cur = out;
+          which ^= 1;
+        }
+        // Q = G x_n Gram_n (symmetric R_n x R_n)
+        std::vector<uint64_t> gd = ranks_;
+        const double* gc = core_.as<double>();
+        double* qb[2] = {scratch_q(0), scratch_q(1)};
+        int w2 = 0;
+        for (int m = 0; m < N_; ++m) {
+          const int Rm = (int)ranks_[m];
+          double* out = (m == N_ - 1) ? Q : qb[w2];
+          ttm_generic(gc, (long long)prod(gd, 0, m), Rm, (long long)prod(gd, m + 1), gram(m), Rm,
+                      1, Rm, out, st_);
+          gc = out;
+          w2 ^= 1;
+        }
+        double* sc2 = scal_.as<double>();
+        norms_into(sc2 + 1);
+        k_fast_loss<<<1, 1024, 0, st_>>>(Y, Q, core_.as<double>(), (long long)d_, xx_.as<double>(),
+                                         sc2 + 1, opt_.lambda, (double)total_, 1e-5, loss_dev,
+                                         rmse_dev, loss_need_.as<int>());
+        RTB_LAUNCH_CHECK();
+      }
+      // direct pass, runs only if k_fast_loss set *need
+      set_ttm_guard(loss_need_.as<int>());
+      try {
+        std::vector<uint64_t> dims;
+        const double* P = build_P(dims);
+        const long long O = (long long)(total_ / shape_[N_ - 1]);
+        const int I = (int)shape_[N_ - 1];
+        double* partial = partial_.as<double>();
+        {
+          Scope sc(prof_, "ttm_last_loss");
+          ttm_last(x_, O, I, factor(N_ - 1), R, T_.as<double>(), P, partial, st_);
+        }
+        double* sc2 = scal_.as<double>();
+        sum_partials(partial, ttm_last_blocks(O, I, R), sc2, st_);
+      } catch (...) {
+        set_ttm_guard(nullptr);
+        throw;
+      }
+      set_ttm_guard(nullptr);
+      double* sc2 = scal_.as<double>();
+      k_finish_loss_guarded<<<1, 1, 0, st_>>>(sc2, sc2 + 1, opt_.lambda, (double)total_, loss_dev,
+                                              rmse_dev, loss_need_.as<int>());
+      RTB_LAUNCH_CHECK();
+      return;
+    }
     std::vector<uint64_t> dims;
     const double* P = build_P(dims);
     const long long O = (long long)(total_ / shape_[N_ - 1]);
-    const int I = (int)shape_[N_ - 1], R = (int)ranks_[N_ - 1];
+    const int I = (int)shape_[N_ - 1];
     double* partial = partial_.as<double>();
     long long nparts;
     if (R <= 32) {
       Scope sc(prof_, "ttm_last_loss");
       ttm_last(x_, O, I, factor(N_ - 1), R, T_.as<double>(), P, partial, st_);
-      nparts = ttm_last_blocks(O);
+      nparts = ttm_last_blocks(O, I, R);
       t_valid_ = true;
     } else {
       // generic: full reconstruction then residual
@@ -1130,6 +1271,13 @@ class Engine {
     }
     double* sc = scal_.as<double>();
     sum_partials(partial, nparts, sc, st_);
+    norms_into(sc + 1);
+    k_finish_loss<<<1, 1, 0, st_>>>(sc, sc + 1, opt_.lambda, (double)total_, loss_dev, rmse_dev);
+    RTB_LAUNCH_CHECK();
+  }
+
+  // sum of squares of the core and all factors (the ridge term) into *out
+  void norms_into(double* out) {
     NormSet ns{};
     ns.count = N_ + 1;
     ns.p[0] = core_.as<double>();
@@ -1138,9 +1286,7 @@ class Engine {
       ns.p[n + 1] = factor(n);
       ns.n[n + 1] = (long long)(shape_[n] * ranks_[n]);
     }
-    k_norms<<<1, 1024, 0, st_>>>(ns, sc + 1);
-    RTB_LAUNCH_CHECK();
-    k_finish_loss<<<1, 1, 0, st_>>>(sc, sc + 1, opt_.lambda, (double)total_, loss_dev, rmse_dev);
+    k_norms<<<1, 1024, 0, st_>>>(ns, out);
     RTB_LAUNCH_CHECK();
   }
 

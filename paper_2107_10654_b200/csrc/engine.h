@@ -51,6 +51,7 @@ struct AlsOptions {
   void (*allreduce)(double*, uint64_t, void*, void*) = nullptr;
   void* allreduce_user = nullptr;
   int core_solver = 0;                    // 0 auto (PCG, Cholesky fallback), 1 Cholesky
+  bool fast_loss = false;                 // loss by the expansion formula (see engine.cu)
 };
 
 struct HistoryRow {

@@ -15,11 +15,19 @@
 //  * k_ttm_generic: scalar fallback for small tensors / odd ranks.
 //  * k_contract_except: M[i,r] = sum_{o,j} Y[o,i,j] G[o,r,j].
 #include "common.cuh"
+
+#include <algorithm>
 #include "kernels.h"
 
 namespace rtb {
 
 namespace {
+// Optional device flag: while set (set_ttm_guard), the launched kernels return at
+// once unless *need != 0. Lets the direct loss pass be enqueued behind the fast
+// loss formula and run only when that formula is numerically unsafe.
+thread_local const int* g_need = nullptr;
+#define RTB_GUARD() \
+  if (need && *need == 0) return;
 constexpr int kBK = 32;     // reduction chunk
 constexpr int kPadX = 4;    // smem row padding (doubles) -> conflict-free frags
 constexpr int kStages = 3;  // cp.async pipeline depth
@@ -33,7 +41,9 @@ __global__ void __launch_bounds__(128) k_ttm_last(const double* __restrict__ X, 
                                                   const double* __restrict__ A, int R,
                                                   double* __restrict__ T,
                                                   const double* __restrict__ P,
-                                                  double* __restrict__ partial) {
+                                                  double* __restrict__ partial,
+                                                  const int* __restrict__ need) {
+  RTB_GUARD()
   constexpr int BM = 64;
   constexpr int LD = kBK + kPadX;
   extern __shared__ __align__(16) double xs[];  // [kStages][BM][LD]
@@ -146,6 +156,146 @@ __global__ void __launch_bounds__(128) k_ttm_last(const double* __restrict__ X, 
   }
   if (FUSED) {
     const double s = block_sum<128>(resid, red);
+    if (tid == 0) partial[blockIdx.x] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent last-mode contraction (one CTA per SM, 8 warps x 16 rows = 128-row
+// blocks): A_N (I x R, padded rows) stays resident in shared memory for the whole
+// pass, X streams through a kStages2-deep cp.async pipeline that runs across row
+// blocks, so every DMMA operand comes from shared memory. FUSED also rebuilds
+// Xhat = P A^T tile by tile and accumulates (X - Xhat)^2 (one partial per CTA).
+constexpr int kStages2 = 3;
+constexpr int BM2 = 128;
+template <int RP>
+constexpr int lda2() { return RP + 4; }
+
+template <int RP, bool FUSED>
+__global__ void __launch_bounds__(256, 1) k_ttm_last2(const double* __restrict__ X, long long O,
+                                                      int I, const double* __restrict__ A, int R,
+                                                      double* __restrict__ T,
+                                                      const double* __restrict__ P,
+                                                      double* __restrict__ partial,
+                                                      const int* __restrict__ need) {
+  RTB_GUARD()
+  constexpr int LD = kBK + kPadX;
+  constexpr int LDA = lda2<RP>();
+  extern __shared__ __align__(16) double sm2[];
+  const int Ip = ceil_div(I, kBK) * kBK;  // A rows zero-padded to whole chunks
+  double* as = sm2;                        // [Ip][LDA]
+  double* xs = as + (size_t)Ip * LDA;      // [kStages2][BM2][LD]
+  __shared__ double red[32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const long long nrb = ceil_div<long long>(O, BM2);
+  const int nchunks = ceil_div(I, kBK);
+  // A resident (zero-padded ranks)
+  for (int e = tid; e < Ip * LDA; e += 256) {
+    const int i = e / LDA, r = e - i * LDA;
+    as[e] = (i < I && r < R) ? A[(size_t)i * R + r] : 0.0;
+  }
+  // flat item stream of this CTA: (row block, chunk)
+  const long long my_blocks = blockIdx.x < nrb ? (nrb - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long nitems = my_blocks * nchunks;
+  auto load_item = [&](long long q, int stage) {
+    const long long rb = blockIdx.x + (q / nchunks) * gridDim.x;
+    const int c = (int)(q % nchunks);
+    const long long o0 = rb * BM2;
+    const int i0 = c * kBK;
+    double* dst = xs + (size_t)stage * BM2 * LD;
+    for (int e = tid; e < BM2 * (kBK / 2); e += 256) {
+      const int r = e / (kBK / 2), col = (e % (kBK / 2)) * 2;
+      const long long o = o0 + r;
+      const bool ok = (o < O) && (i0 + col < I);
+      cp_async16(dst + r * LD + col, ok ? X + o * I + i0 + col : X, ok);
+    }
+  };
+#pragma unroll
+  for (int sidx = 0; sidx < kStages2 - 1; ++sidx) {
+    if (sidx < nitems) load_item(sidx, sidx);
+    cp_async_commit();
+  }
+  double acc[2][RP / 8][2];
+  double pf[2][RP / 4];
+  double resid = 0.0;
+  for (long long q = 0; q < nitems; ++q) {
+    const int c = (int)(q % nchunks);
+    const long long rb = blockIdx.x + (q / nchunks) * gridDim.x;
+    const long long o0 = rb * BM2 + warp * 16;
+    if (c == 0) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < RP / 8; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+      if (FUSED) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int ks = 0; ks < RP / 4; ++ks) {
+            const long long o = o0 + mt * 8 + g;
+            const int k = ks * 4 + t;
+            pf[mt][ks] = (o < O && k < R) ? P[o * R + k] : 0.0;
+          }
+      }
+    }
+    cp_async_wait<kStages2 - 2>();
+    __syncthreads();
+    if (q + kStages2 - 1 < nitems) load_item(q + kStages2 - 1, (int)((q + kStages2 - 1) % kStages2));
+    cp_async_commit();
+    const double* xt = xs + (size_t)(q % kStages2) * BM2 * LD + warp * 16 * LD;
+    const int i0 = c * kBK;
+    // T += X_tile (16 x 32) A_chunk (32 x RP)
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      const double* ar = as + (size_t)(i0 + ks * 4 + t) * LDA;
+      double bf[RP / 8];
+#pragma unroll
+      for (int nt = 0; nt < RP / 8; ++nt) bf[nt] = ar[nt * 8 + g];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const double af = xt[(mt * 8 + g) * LD + ks * 4 + t];
+#pragma unroll
+        for (int nt = 0; nt < RP / 8; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], af, bf[nt]);
+      }
+    }
+    if (FUSED) {
+      // Xhat_tile (16 x 32) = P_rows (16 x RP) A_chunk^T (RP x 32); residual
+#pragma unroll
+      for (int nt = 0; nt < kBK / 8; ++nt) {
+        const double* ar = as + (size_t)(i0 + nt * 8 + g) * LDA;
+        double bf[RP / 4];
+#pragma unroll
+        for (int ks = 0; ks < RP / 4; ++ks) bf[ks] = ar[ks * 4 + t];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < RP / 4; ++ks) dmma_8x8x4(c0, c1, pf[mt][ks], bf[ks]);
+          const double2 xv =
+              *reinterpret_cast<const double2*>(xt + (mt * 8 + g) * LD + nt * 8 + 2 * t);
+          const double d0 = xv.x - c0, d1 = xv.y - c1;
+          resid += d0 * d0 + d1 * d1;  // zero-filled tails contribute exactly 0
+        }
+      }
+    }
+    if (c == nchunks - 1) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const long long o = o0 + mt * 8 + g;
+        if (o >= O) continue;
+#pragma unroll
+        for (int nt = 0; nt < RP / 8; ++nt) {
+          const int r = nt * 8 + 2 * t;
+          if (r < R) T[o * R + r] = acc[mt][nt][0];
+          if (r + 1 < R) T[o * R + r + 1] = acc[mt][nt][1];
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (FUSED) {
+    const double s = block_sum<256>(resid, red);
     if (tid == 0) partial[blockIdx.x] = s;
   }
 }
@@ -266,7 +416,8 @@ __global__ void k_sum_splits(const double* __restrict__ part, long long n, int s
 // Scalar fallback: out[o,r,j] = sum_i W[r*wr + i*wi] X[o,i,j].
 __global__ void k_ttm_generic(const double* __restrict__ X, long long O, int I, long long J,
                               const double* __restrict__ W, long long wr, long long wi, int R,
-                              double* __restrict__ out) {
+                              double* __restrict__ out, const int* __restrict__ need) {
+  RTB_GUARD()
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = O * R * J;
   if (e >= total) return;
@@ -371,7 +522,9 @@ __global__ void __launch_bounds__(256) k_ttm_smallj(const double* __restrict__ X
 // block's A rows staged in smem; grid (ceil(I/ICH), O), threads over (i, j).
 __global__ void __launch_bounds__(256) k_ttm_expand(const double* __restrict__ Y, int R,
                                                    long long J, const double* __restrict__ A,
-                                                   int I, int ich, double* __restrict__ out) {
+                                                   int I, int ich, double* __restrict__ out,
+                                                   const int* __restrict__ need) {
+  RTB_GUARD()
   extern __shared__ double ys[];  // R x J, then ich x R
   double* as = ys + (long long)R * J;
   const long long o = blockIdx.y;
@@ -398,7 +551,8 @@ __global__ void __launch_bounds__(256) k_ttm_expand(const double* __restrict__ Y
 
 // Deterministic sum of per-block partials (fixed order), one block.
 __global__ void k_sum_partials(const double* __restrict__ partial, long long n,
-                               double* __restrict__ out) {
+                               double* __restrict__ out, const int* __restrict__ need) {
+  RTB_GUARD()
   __shared__ double red[32];
   double s = 0.0;
   for (long long i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
@@ -420,11 +574,51 @@ static void launch_last(const double* X, long long O, int I, const double* A, in
     attr = true;
   }
   const long long blocks = ceil_div<long long>(O, 64);
-  k<<<(unsigned)blocks, 128, smem, st>>>(X, O, I, A, R, T, P, partial);
+  k<<<(unsigned)blocks, 128, smem, st>>>(X, O, I, A, R, T, P, partial, g_need);
   RTB_LAUNCH_CHECK();
 }
 
-long long ttm_last_blocks(long long O) { return ceil_div<long long>(O, 64); }
+void set_ttm_guard(const int* need) { g_need = need; }
+
+static int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : kNumSMs;
+  }();
+  return n;
+}
+
+// the persistent kernel applies when A fits next to the X pipeline in shared memory
+static bool last2_ok(int I, int R) {
+  const int rp = R <= 8 ? 8 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
+  const size_t ip = (size_t)ceil_div(I, kBK) * kBK;
+  const size_t smem = (ip * (rp + 4) + (size_t)kStages2 * BM2 * (kBK + kPadX)) * 8;
+  return (I % 2) == 0 && smem <= 220 * 1024;
+}
+
+template <int RP, bool FUSED>
+static void launch_last2(const double* X, long long O, int I, const double* A, int R, double* T,
+                         const double* P, double* partial, cudaStream_t st) {
+  const size_t ip = (size_t)ceil_div(I, kBK) * kBK;
+  const size_t smem = (ip * lda2<RP>() + (size_t)kStages2 * BM2 * (kBK + kPadX)) * 8;
+  auto k = k_ttm_last2<RP, FUSED>;
+  static bool attr = false;
+  if (!attr) {
+    RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  const long long nrb = ceil_div<long long>(O, BM2);
+  const int grid = (int)std::min<long long>(nrb, sm_count());
+  k<<<grid, 256, smem, st>>>(X, O, I, A, R, T, P, partial, g_need);
+  RTB_LAUNCH_CHECK();
+}
+
+long long ttm_last_blocks(long long O, int I, int R) {
+  if (last2_ok(I, R)) return std::min<long long>(ceil_div<long long>(O, BM2), sm_count());
+  return ceil_div<long long>(O, 64);
+}
 
 void ttm_last(const double* X, long long O, int I, const double* A, int R, double* T,
               const double* P, double* partial, cudaStream_t st) {
@@ -432,6 +626,21 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
   const bool v2 = (I % 2) == 0;
   const int rp = R <= 8 ? 8 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
   if (R > 32) throw Error(4, "ttm_last: rank > 32 not supported by the DMMA path");
+  if (last2_ok(I, R)) {
+#define RTB_L2(RPV)                                                     \
+  case RPV:                                                             \
+    if (fused) launch_last2<RPV, true>(X, O, I, A, R, T, P, partial, st); \
+    else launch_last2<RPV, false>(X, O, I, A, R, T, P, partial, st);      \
+    break;
+    switch (rp) {
+      RTB_L2(8)
+      RTB_L2(16)
+      RTB_L2(24)
+      RTB_L2(32)
+    }
+#undef RTB_L2
+    return;
+  }
 #define RTB_L(RPV)                                                                       \
   case RPV:                                                                              \
     if (fused) {                                                                         \
@@ -517,7 +726,7 @@ void ttm_generic(const double* X, long long O, int I, long long J, const double*
   const long long total = O * R * J;
   if (total == 0) return;
   k_ttm_generic<<<(unsigned)ceil_div<long long>(total, 256), 256, 0, st>>>(X, O, I, J, W, wr, wi,
-                                                                          R, out);
+                                                                          R, out, g_need);
   RTB_LAUNCH_CHECK();
 }
 
@@ -537,7 +746,7 @@ bool ttm_expand(const double* Y, long long O, int R, long long J, const double* 
   const size_t smem = ((size_t)R * J + (size_t)ich * R) * sizeof(double);
   if (smem > 48 * 1024 || O > 65535) return false;
   k_ttm_expand<<<dim3((unsigned)ceil_div(I, ich), (unsigned)O), 256, smem, st>>>(Y, R, J, A, I,
-                                                                                 ich, out);
+                                                                                 ich, out, g_need);
   RTB_LAUNCH_CHECK();
   return true;
 }
@@ -559,7 +768,7 @@ void contract_except(const double* Y, const double* G, long long O, int I, int R
 }
 
 void sum_partials(const double* partial, long long n, double* out, cudaStream_t st) {
-  k_sum_partials<<<1, 1024, 0, st>>>(partial, n, out);
+  k_sum_partials<<<1, 1024, 0, st>>>(partial, n, out, g_need);
   RTB_LAUNCH_CHECK();
 }
 

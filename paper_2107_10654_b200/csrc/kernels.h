@@ -38,7 +38,10 @@ __global__ void k_sym_pinv(const double* evals, const double* evecs, const int* 
 __global__ void k_rows_times_small(const double* M, const double* P, int I, int R, double* out);
 
 // ---- k_ttm.cu ----
-long long ttm_last_blocks(long long O);
+// While a guard is set (non-null), ttm_last / ttm_generic / ttm_expand / sum_partials
+// kernels do nothing unless *need != 0 at run time (nullptr clears the guard).
+void set_ttm_guard(const int* need);
+long long ttm_last_blocks(long long O, int I, int R);
 // T (O x R) = X (O x I) A (I x R); if P != null also partial[block] = sum (X - P A^T)^2
 void ttm_last(const double* X, long long O, int I, const double* A, int R, double* T,
               const double* P, double* partial, cudaStream_t st);

@@ -62,7 +62,8 @@ class AlsExt(C.Structure):
         ("async_sweeps_when_no_tolerance", C.c_int),
         ("profile_kernels", C.c_int),
         ("core_solver", C.c_int),
-        ("reserved", C.c_int * 6),
+        ("fast_loss", C.c_int),
+        ("reserved", C.c_int * 5),
     ]
 
 
@@ -386,9 +387,11 @@ class Result:
             pass
 
 
-def _ext(init_model: Model | None = None, profile: bool = False, core_solver: int = 0):
+def _ext(init_model: Model | None = None, profile: bool = False, core_solver: int = 0,
+         fast_loss: bool = False):
     ext = AlsExt()
     ext.core_solver = int(core_solver)
+    ext.fast_loss = int(fast_loss)
     keep = []
     if init_model is not None:
         core = _f64(init_model.core).ravel()
@@ -401,15 +404,15 @@ def _ext(init_model: Model | None = None, profile: bool = False, core_solver: in
 
 
 def als_run(x: Tensor, ranks, opts: AlsOptions | None = None, init_model: Model | None = None,
-            profile: bool = False, core_solver: int = 0) -> Result:
+            profile: bool = False, core_solver: int = 0, fast_loss: bool = False) -> Result:
     """rtucker_als_run (ref capi.cpp:176-201); extensions via rtucker_b200_als_run_ex."""
     opts = opts or options()
     ranks = _u64(ranks)
     r = _vp()
-    if init_model is None and not profile and not core_solver:
+    if init_model is None and not profile and not core_solver and not fast_loss:
         _check(lib.rtucker_als_run(x.h, _p(ranks), len(ranks), C.byref(opts), C.byref(r)))
     else:
-        ext, keep = _ext(init_model, profile, core_solver)
+        ext, keep = _ext(init_model, profile, core_solver, fast_loss)
         _check(lib.rtucker_b200_als_run_ex(x.h, _p(ranks), len(ranks), C.byref(opts),
                                            C.byref(ext), C.byref(r)))
         del keep

@@ -310,3 +310,37 @@ def test_pcg_matches_cholesky_large_d(rt, shape, ranks, s):
         assert abs(hp[2] - hc[2]) / hc[2] < 1e-7, hp[:2]
     mp, mc = rp.model(), rc.model()
     assert np.linalg.norm(mp.core - mc.core) / np.linalg.norm(mc.core) < 1e-5
+
+
+def test_loss_near_exact_fit_takes_direct_residual(oracle, rt):
+    """Noise-free low-rank data: the residual is ~1e-13 of ||X||^2, where the fast loss
+    formula would cancel; the guarded direct pass must give the direct residual of the
+    returned model (checked against the single-op direct loss and the reference)."""
+    shape, ranks = (14, 12, 10), (3, 3, 3)
+    x = planted(shape, ranks, noise=0.0, seed=8)
+    kw = dict(lam=1e-9, max_iterations=8, tolerance=0.0, record_history=1, seed=2)
+    r = rt.als_run(rt.Tensor.from_numpy(x), ranks, rt.options(**kw))
+    m = r.model()
+    gl, grm = rt.loss(rt.Tensor.from_numpy(x), m)
+    ol, orm = oracle.tucker_loss(shape, ranks, m.core, m.factors, 1e-9, x)
+    assert abs(r.final_rmse - grm) <= 1e-9 * grm, (r.final_rmse, grm)
+    assert abs(r.final_rmse - orm) <= 1e-6 * orm, (r.final_rmse, orm)
+    assert abs(r.final_loss - ol) <= 1e-9 * ol
+
+
+@pytest.mark.parametrize("shape,ranks,noise", [((40, 36, 32), (5, 4, 6), 0.01),
+                                               ((64, 64, 64), (16, 16, 16), 0.01),
+                                               ((30, 28, 26, 24), (3, 3, 3, 3), 0.05)])
+def test_fast_loss_matches_direct_residual(rt, shape, ranks, noise):
+    """Same ALS trajectory, loss by the opt-in fast formula vs the default direct residual
+    pass: agreement to ~1e-12 ||X||^2 absolute (bounded here by 1e-7 relative)."""
+    x = planted(shape, ranks, noise=noise, seed=9)
+    kw = dict(lam=1e-3, sketched_core=1, sample_count_override=20 * int(np.prod(ranks)),
+              max_iterations=3, tolerance=0.0, record_history=1, seed=5)
+    xt = rt.Tensor.from_numpy(x)
+    rf = rt.als_run(xt, ranks, rt.options(**kw), fast_loss=True)
+    rd = rt.als_run(xt, ranks, rt.options(**kw))
+    for (fi, fs, fl, frm), (di, ds, dl, drm) in zip(rf.history(), rd.history()):
+        assert (fi, fs) == (di, ds)
+        assert abs(fl - dl) / dl < 1e-7, (fi, fs, fl, dl)
+        assert abs(frm - drm) / drm < 1e-7, (fi, fs, frm, drm)

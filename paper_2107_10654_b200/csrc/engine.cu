@@ -588,7 +588,7 @@ class Engine {
   bool xx_valid_ = false;
   DevBuf scores_, cdf_, sums_, score_off_, rows_dev_, cols_dev_, flag_;
   DevBuf sk_idx_, sk_w_, draw_work_, gram_work_, G_, rhs_, chol_work_, chol_status_,
-      data_draws_, zero_flag_, U_[8], pgram_, pcg_work_, pcg_status_, blocks_;
+      data_draws_, zero_flag_, U_[8], pgram_, pcg_work_, pcg_status_, blocks_, pev_, pvec_, pst_;
   uint64_t sketch_rng_ = 0, sketch_k_ = 0;
   bool t_valid_ = false;
   uint64_t last_s_ = 0;
@@ -644,6 +644,9 @@ class Engine {
     }
     eig_status_.ensure(64 * 4, st_);
     pgram_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
+    pev_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
+    pvec_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
+    pst_.ensure(64 * 4, st_);
     pcg_status_.ensure(16, st_);
     ns_.ensure(64 * 4, st_);
     ranks_dev_.ensure(64 * 4, st_);
@@ -998,9 +1001,13 @@ class Engine {
       ps.linv_stride = eig_stride_;
       ps.linv_ok = spd_ok_.as<int>();
       ps.grams = grams_.as<double>();
+      sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, pev_.as<double>(),
+                pvec_.as<double>(), pst_.as<int>(), N_, st_);
+      ps.evals = pev_.as<double>();
+      ps.evecs = pvec_.as<double>();
       ps.aug_count = gram_aug_counts(gs, gram_work_.p);
       ps.aug_term = gram_aug_term(gs);
-      ps.max_iter = 200;
+      ps.max_iter = 80;
       ps.tol = 1e-15;
       ps.check_tol = 1e-12;
       pcg_work_.ensure(pcg_work_bytes((int)d_, rk[0]), st_);
@@ -1367,10 +1374,24 @@ void session_output(Session* s, AlsOutput& out) { s->e->output(out); }
 
 void als_run(const double* x_dev, const std::vector<uint64_t>& shape,
              const std::vector<uint64_t>& ranks, const AlsOptions& opt, AlsOutput& out) {
+  static const bool trace = std::getenv("RTB_TRACE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto t0 = now();
   std::unique_ptr<Session> s(session_create(x_dev, shape, ranks, opt));
+  if (trace) RTB_CUDA(cudaStreamSynchronize(current_stream()));
+  const auto t1 = now();
   // tolerance <= 0 can never stop early (change < tol is false): no per-sweep sync
   session_run(s.get(), opt.max_iterations, opt.tolerance > 0.0);
+  const auto t2 = now();
   session_output(s.get(), out);
+  const auto t3 = now();
+  s.reset();
+  const auto t4 = now();
+  if (trace)
+    std::fprintf(stderr, "[als_run] create+init+loss %.2f ms, sweeps %.2f ms (device %.2f), "
+                 "output %.2f ms, teardown %.2f ms\n", ms(t0, t1), ms(t1, t2),
+                 out.sweep_seconds * 1e3, ms(t2, t3), ms(t3, t4));
 }
 
 // ---------------------------------------------------------------------------

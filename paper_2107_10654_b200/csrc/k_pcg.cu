@@ -63,6 +63,8 @@ struct PcgArgs {
   int linv_stride;
   const int* linv_ok;     // per mode: Cholesky of A_n^T A_n succeeded
   const double* grams;    // per mode (stride): A_n^T A_n
+  const double* evals;    // per mode (stride): eigenvalues of A_n^T A_n (descending)
+  const double* evecs;    // per mode (stride): V[i*R+k], column k = eigenvector k
   const int* aug_count;
   double aug_term;
   double lambda;
@@ -187,16 +189,19 @@ __device__ __forceinline__ void mode_product(const double* X, double* out, const
   }
 }
 
-// z = M^-1 r = ((x)_n P_n) r, P_n = (A_n^T A_n)^-1: N mode products with scratch
-// a, b; returns the buffer holding z.
+// z = M^-1 r with scratch a, b; returns the buffer holding z. Two forms:
+//  * P form (eig == false): M = (x)_n A_n^T A_n, M^-1 = (x)_n P_n: N mode products.
+//  * eigen form: M = (x)_n A_n^T A_n + lambda I = V diag(lambda + prod mu) V^T:
+//    N products with V^T, a diagonal scaling, N products with V (2N + 1 passes).
 template <int RM, int RX>
 __device__ double* precondition(const PcgShared& sh, const double* r, double* a, double* b,
-                                const double* Ps, unsigned long long* prof = nullptr) {
+                                const double* W1, const double* W2, const double* dinv, bool eig,
+                                unsigned long long* prof = nullptr) {
   const double* src = r;
   double* dst = a;
   unsigned long long t0 = prof ? gtimer() : 0;
   for (int n = 0; n < sh.order; ++n) {
-    mode_product<RM, RX>(src, dst, Ps + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
+    mode_product<RM, RX>(src, dst, W1 + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
     __syncthreads();
     if (prof && n < 8) {
       const unsigned long long t1 = gtimer();
@@ -205,6 +210,17 @@ __device__ double* precondition(const PcgShared& sh, const double* r, double* a,
     }
     src = dst;
     dst = (dst == a) ? b : a;
+  }
+  if (eig) {
+    double* t = const_cast<double*>(src);
+    for (int e = threadIdx.x; e < sh.d; e += kThreads) t[e] *= dinv[e];
+    __syncthreads();
+    for (int n = 0; n < sh.order; ++n) {
+      mode_product<RM, RX>(src, dst, W2 + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
+      __syncthreads();
+      src = dst;
+      dst = (dst == a) ? b : a;
+    }
   }
   return const_cast<double*>(src);
 }
@@ -391,11 +407,14 @@ __device__ void reduce_rows(const PcgArgs& A, const PcgShared& sh, const double*
 template <int RM, int RX>
 __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgShared shc) {
   extern __shared__ __align__(16) double sm[];
-  const PcgShared& sh = shc;  // stays in the parameter bank (dynamic indexing is cheap)
+  const PcgShared& sh = shc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;  // stays in the parameter bank (dynamic indexing is cheap)
   const int d = sh.d;
   const int dv = (d + 1) & ~1;
-  double* Ps = sm;                          // [order][RM][RM]: (A_n^T A_n)^-1
-  double* r = Ps + sh.order * RM * RM;
+  double* Ps = sm;                          // [order][RM][RM]: P_n (P form) or V_n (eigen form)
+  double* VTs = Ps + sh.order * RM * RM;    // [order][RM][RM]: V_n^T (eigen form)
+  double* dinv = VTs + sh.order * RM * RM;  // [d]: 1 / (lambda + prod mu) (eigen form)
+  double* r = dinv + ((sh.d + 1) & ~1);
   double* p = r + dv;
   double* s0 = p + dv;
   double* s1 = s0 + dv;
@@ -419,7 +438,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
     return;
   }
 
-  double gnorm = 1.0;
   for (int n = 0; n < sh.order; ++n) {
     const int R = sh.R[n];
     const double* Pg = A.pinv + (size_t)n * A.linv_stride;
@@ -427,32 +445,83 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
       const int i = e / RM, j = e - i * RM;
       Ps[n * RM * RM + e] = (i < R && j < R) ? Pg[i * R + j] : 0.0;
     }
-    // ||A_n^T A_n||_2 by power iteration (warp 0, lane = row; a slight
-    // underestimate is harmless: it only tightens the stopping test)
+  }
+  __syncthreads();
+  // Warp n (one per mode, in parallel): mu_max(A_n^T A_n) and ||P_n||_2 = 1/mu_min by
+  // power iteration (lane = row). mu_max gives the ||G|| estimate of the stopping test
+  // (an underestimate only tightens it). The preconditioner drops lambda: every
+  // direction with lambda > mu(K^T K) becomes an outlier eigenvalue of M^-1 G that
+  // CG removes in about one iteration, so a moderate lambda / mu_min(K^T K) is
+  // harmless (C2: ~2.5, 15 iterations); beyond 100 (near-noise fits, hundreds of
+  // outliers) the Cholesky path is used directly.
+  if (warp < sh.order) {
+    const int n = warp, R = sh.R[n];
     const double* Gm = A.grams + (size_t)n * A.linv_stride;
-    if (threadIdx.x < 32) {
-      const int i = threadIdx.x;
-      double v = i < R ? 1.0 : 0.0, mu = 0.0;
-      for (int itp = 0; itp < 60; ++itp) {
+    const double* Pm = Ps + n * RM * RM;
+    double est[2];
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      double v = lane < R ? 1.0 + 0.01 * lane : 0.0, mu = 0.0;
+      for (int itp = 0; itp < 40; ++itp) {
         double y = 0.0;
-        for (int j = 0; j < R; ++j) y = fma(i < R ? Gm[i * R + j] : 0.0, __shfl_sync(0xffffffffu, v, j), y);
-        double yy = y * y, vy = v * y;
+        for (int j = 0; j < R; ++j) {
+          const double mij = lane < R ? (which == 0 ? Gm[lane * R + j] : Pm[lane * RM + j]) : 0.0;
+          y = fma(mij, __shfl_sync(0xffffffffu, v, j), y);
+        }
+        double yy = y * y, vy = v * y, vv = v * v;
         for (int o = 16; o > 0; o >>= 1) {
           yy += __shfl_xor_sync(0xffffffffu, yy, o);
           vy += __shfl_xor_sync(0xffffffffu, vy, o);
+          vv += __shfl_xor_sync(0xffffffffu, vv, o);
         }
-        double vv = v * v;
-        for (int o = 16; o > 0; o >>= 1) vv += __shfl_xor_sync(0xffffffffu, vv, o);
         mu = vv > 0.0 ? vy / vv : 0.0;
         v = yy > 0.0 ? y * rsqrt(yy) : 0.0;
       }
-      if (threadIdx.x == 0) red[0] = mu;
+      est[which] = mu;
     }
-    __syncthreads();
-    gnorm *= red[0];
-    __syncthreads();
+    if (lane == 0) {
+      red[2 * n] = est[0];
+      red[2 * n + 1] = est[1];
+    }
+  }
+  __syncthreads();
+  double gnorm = 1.0, pnorm = 1.0;
+  for (int n = 0; n < sh.order; ++n) {
+    gnorm *= red[2 * n];
+    pnorm *= red[2 * n + 1];
   }
   gnorm += A.lambda;
+  __syncthreads();
+  if (A.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    A.prof[14] = __double_as_longlong(gnorm);
+    A.prof[15] = __double_as_longlong(pnorm);
+  }
+  // lambda-free P form while lambda is small against mu_min(K^T K) (few outlier
+  // eigenvalues), else the exact eigen form of (x) A_n^T A_n + lambda I
+  const bool eig = !(A.lambda * pnorm <= 4.0);
+  if (eig) {
+    for (int n = 0; n < sh.order; ++n) {
+      const int R = sh.R[n];
+      const double* Vg = A.evecs + (size_t)n * A.linv_stride;
+      for (int e = threadIdx.x; e < RM * RM; e += kThreads) {
+        const int i = e / RM, j = e - i * RM;
+        const bool in = i < R && j < R;
+        Ps[n * RM * RM + e] = in ? Vg[i * R + j] : 0.0;   // W[i][j] = V[i][j]
+        VTs[n * RM * RM + e] = in ? Vg[j * R + i] : 0.0;  // W[i][j] = V[j][i]
+      }
+    }
+    for (int e = threadIdx.x; e < d; e += kThreads) {
+      double m = 1.0;
+      int rem = e;
+      for (int n = sh.order - 1; n >= 0; --n) {
+        const int j = rem % sh.R[n];
+        rem /= sh.R[n];
+        m *= fmax(A.evals[(size_t)n * A.linv_stride + j], 0.0);
+      }
+      dinv[e] = 1.0 / (m + A.lambda);
+    }
+    __syncthreads();
+  }
   for (int e = threadIdx.x; e < d; e += kThreads) {
     r[e] = A.b[e];
     xs[e] = 0.0;
@@ -474,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
     }
     return;
   }
-  double* z = precondition<RM, RX>(sh, r, s0, s1, Ps);
+  double* z = precondition<RM, RX>(sh, r, s0, s1, Ps, VTs, dinv, eig);
   double rho = 0.0;
   for (int e = threadIdx.x; e < d; e += kThreads) {
     p[e] = z[e];
@@ -536,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
       ++it;
       break;
     }
-    z = precondition<RM, RX>(sh, r, s0, s1, Ps, prof ? A.prof : nullptr);
+    z = precondition<RM, RX>(sh, r, s0, s1, Ps, VTs, dinv, eig, prof ? A.prof : nullptr);
     RTB_PCG_MARK(5)
     double rho2 = 0.0;
     for (int e = threadIdx.x; e < d; e += kThreads) rho2 = fma(r[e], z[e], rho2);
@@ -605,7 +674,7 @@ size_t pcg_smem(int d, int order, const int* ranks, int rm) {
     const size_t need = (size_t)kWarps * 2 * (d / ranks[0]);
     if (need > 2 * dv) extra = need;
   }
-  return 8 * ((size_t)order * rm * rm + 5 * dv + 32 + extra);
+  return 8 * (2 * (size_t)order * rm * rm + 6 * dv + 32 + extra);
 }
 
 }  // namespace
@@ -662,6 +731,8 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   a.linv_stride = spec.linv_stride;
   a.linv_ok = spec.linv_ok;
   a.grams = spec.grams;
+  a.evals = spec.evals;
+  a.evecs = spec.evecs;
   a.aug_count = spec.aug_count;
   a.aug_term = spec.aug_term;
   a.lambda = spec.lambda;
@@ -697,8 +768,9 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
     RTB_CUDA(cudaStreamSynchronize(st));
     std::fprintf(stderr,
                  "[pcg] d=%d iters=%d status=%d ns: slice %llu bar1 %llu reduce %llu bar2 %llu "
-                 "vec %llu precond %llu tail %llu | stages %llu %llu %llu\n",
-                 d, stat[1], stat[0], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[8], h[9], h[10]);
+                 "vec %llu precond %llu tail %llu | stages %llu %llu %llu | gnorm %.3e pnorm %.3e\n",
+                 d, stat[1], stat[0], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[8], h[9], h[10],
+                 __builtin_bit_cast(double, h[14]), __builtin_bit_cast(double, h[15]));
   }
 }
 

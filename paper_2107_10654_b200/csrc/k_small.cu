@@ -15,6 +15,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
+
 #include <cfloat>
 
 namespace rtb {
@@ -282,6 +284,110 @@ __global__ void k_sym_eigen_warp(const double* in, const int* ns, int stride, do
 }
 
 // ---------------------------------------------------------------------------
+// CTA-per-matrix parallel Jacobi for n <= 32: thread (i, j) owns A[i][j] and
+// V[i][j]; every round applies the n/2 disjoint rotations of the round-robin
+// tournament at once (they commute), A' = J^T A J and V' = V J, each thread
+// reading the 4 (resp. 2) entries it needs from the previous buffer. Same
+// rotation formula, absolute threshold and output order as k_sym_eigen_warp,
+// ~2 barriers per round instead of a serial per-pair loop.
+__global__ void __launch_bounds__(1024) k_sym_eigen_cta(const double* in, const int* ns, int stride,
+                                                        double* evals, double* evecs, int* status,
+                                                        const int* skip) {
+  __shared__ double Ab[2][32][33];
+  __shared__ double Vb[2][32][33];
+  __shared__ double rc[32], rs[32];
+  __shared__ int partner[32];
+  __shared__ double red[32];
+  const int b = blockIdx.x;
+  if (skip && skip[b]) {
+    if (threadIdx.x == 0) status[b] = 0;
+    return;
+  }
+  const int n = ns[b];
+  const int np = n + (n & 1);
+  const int tid = threadIdx.x;
+  const int i = tid / 32, j = tid % 32;
+  const bool act = i < np && j < np;
+  const double* src = in + (size_t)b * stride;
+  double fro = 0.0;
+  if (act) {
+    const double v = (i < n && j < n) ? src[i * n + j] : 0.0;
+    Ab[0][i][j] = v;
+    Vb[0][i][j] = (i == j) ? 1.0 : 0.0;
+    fro = v * v;
+  }
+  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  if ((tid & 31) == 0) red[tid >> 5] = fro;
+  __syncthreads();
+  if (tid < 32) {
+    double t = tid < (int)(blockDim.x >> 5) ? red[tid] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (tid == 0) red[0] = t;
+  }
+  __syncthreads();
+  const double tol_abs = (double)n * DBL_EPSILON * sqrt(red[0]);
+  int cur = 0;
+  int st = 3;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    for (int round = 0; round < np - 1; ++round) {
+      if (tid < np / 2) {
+        const int k = tid;
+        const int pp = k == 0 ? 0 : 1 + ((k - 1 + round) % (np - 1));
+        const int qq = 1 + ((np - 2 - k + round) % (np - 1));
+        const int p = min(pp, qq), q = max(pp, qq);
+        const double apq = Ab[cur][p][q], app = Ab[cur][p][p], aqq = Ab[cur][q][q];
+        double c = 1.0, sn = 0.0;
+        if (q < n && fabs(apq) > 1e-300 && fabs(apq) > tol_abs) {
+          const double diff = aqq - app;
+          const double den = fabs(diff) + sqrt(diff * diff + 4.0 * apq * apq);
+          double t = 2.0 * apq / den;
+          if (diff < 0.0) t = -t;
+          c = rsqrt(1.0 + t * t);
+          sn = c * t;
+        }
+        partner[p] = q;
+        partner[q] = p;
+        rc[p] = c;
+        rc[q] = c;
+        rs[p] = -sn;  // sigma_p s: column p' = c col_p - s col_q
+        rs[q] = sn;   // sigma_q s: column q' = c col_q + s col_p
+      }
+      __syncthreads();
+      if (act) {
+        const int yi = partner[i], yj = partner[j];
+        const double ci = rc[i], si = rs[i], cj = rc[j], sj = rs[j];
+        const double (*A)[33] = Ab[cur];
+        double v = ci * cj * A[i][j] + ci * sj * A[i][yj] + si * cj * A[yi][j] + si * sj * A[yi][yj];
+        if (si != 0.0 && j == yi) v = 0.0;  // the annihilated pair
+        Ab[cur ^ 1][i][j] = v;
+        Vb[cur ^ 1][i][j] = cj * Vb[cur][i][j] + sj * Vb[cur][i][yj];
+      }
+      cur ^= 1;
+      __syncthreads();
+    }
+    // converged when no rotation fired in the whole sweep
+    int any = 0;
+    if (act && i < j && j < n) any = fabs(Ab[cur][i][j]) > tol_abs && fabs(Ab[cur][i][j]) > 1e-300;
+    if (!__syncthreads_or(any)) {
+      st = 0;
+      break;
+    }
+  }
+  if (tid < n) {
+    const int k = tid;
+    const double mk = Ab[cur][k][k];
+    int rank = 0;
+    for (int jj = 0; jj < n; ++jj) {
+      const double mj = Ab[cur][jj][jj];
+      if (mj > mk || (mj == mk && jj < k)) ++rank;
+    }
+    evals[(size_t)b * stride + rank] = mk;
+    for (int ii = 0; ii < n; ++ii) evecs[(size_t)b * stride + (size_t)ii * n + rank] = Vb[cur][ii][k];
+  }
+  if (tid == 0) status[b] = st;
+}
+
+// ---------------------------------------------------------------------------
 // Batched small SPD factorization, one warp per matrix (n <= 32): Cholesky
 // with row r in lane r's registers (column broadcasts through shuffles), then
 // Linv (column per lane). ok[b] = 1 unless a pivot falls below
@@ -487,12 +593,9 @@ __global__ void k_rows_times_small(const double* M, const double* P, int I, int 
 void sym_eigen(const double* in, const int* ns_dev, int nmax, int stride, double* evals,
                double* evecs, int* status, int nmat, cudaStream_t st, const int* skip) {
   if (nmax <= 32) {
-    const int per_block = 4;
-    const size_t smem = (size_t)per_block * (2 * 32 * 33 + 64) * sizeof(double);
-    RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    k_sym_eigen_warp<<<ceil_div(nmat, per_block), 32 * per_block, smem, st>>>(
-        in, ns_dev, stride, evals, evecs, status, nmat, skip);
+    const int np = nmax + (nmax & 1);
+    const int threads = std::max(64, ceil_div(np * 32, 32) * 32);
+    k_sym_eigen_cta<<<nmat, threads, 0, st>>>(in, ns_dev, stride, evals, evecs, status, skip);
   } else {
     if (skip) throw Error(4, "eigen: skip flags need n <= 32");
     if (nmax > 64) throw Error(4, "eigen: n > 64 not supported");

@@ -172,7 +172,7 @@ template <int RP>
 constexpr int lda2() { return RP + 4; }
 
 template <int RP, bool FUSED>
-__global__ void __launch_bounds__(256, 1) k_ttm_last2(const double* __restrict__ X, long long O,
+__global__ void __launch_bounds__(512, 1) k_ttm_last2(const double* __restrict__ X, long long O,
                                                       int I, const double* __restrict__ A, int R,
                                                       double* __restrict__ T,
                                                       const double* __restrict__ P,
@@ -181,6 +181,12 @@ __global__ void __launch_bounds__(256, 1) k_ttm_last2(const double* __restrict__
   RTB_GUARD()
   constexpr int LD = kBK + kPadX;
   constexpr int LDA = lda2<RP>();
+  // 16 warps. FUSED: warps 0-7 accumulate T for 16 rows each, warps 8-15 rebuild
+  // Xhat for the same rows and accumulate the residual (warp specialisation keeps
+  // both register sets small and doubles the DMMA chains in flight). Not fused:
+  // 16 warps x 8 rows of T.
+  constexpr int ROWS = FUSED ? 16 : 8;
+  constexpr int MT = ROWS / 8;
   extern __shared__ __align__(16) double sm2[];
   const int Ip = ceil_div(I, kBK) * kBK;  // A rows zero-padded to whole chunks
   double* as = sm2;                        // [Ip][LDA]
@@ -188,14 +194,14 @@ __global__ void __launch_bounds__(256, 1) k_ttm_last2(const double* __restrict__
   __shared__ double red[32];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
+  const bool rwarp = FUSED && warp >= 8;
+  const int wrow = FUSED ? (warp & 7) : warp;
   const long long nrb = ceil_div<long long>(O, BM2);
   const int nchunks = ceil_div(I, kBK);
-  // A resident (zero-padded ranks)
-  for (int e = tid; e < Ip * LDA; e += 256) {
+  for (int e = tid; e < Ip * LDA; e += 512) {
     const int i = e / LDA, r = e - i * LDA;
     as[e] = (i < I && r < R) ? A[(size_t)i * R + r] : 0.0;
   }
-  // flat item stream of this CTA: (row block, chunk)
   const long long my_blocks = blockIdx.x < nrb ? (nrb - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const long long nitems = my_blocks * nchunks;
   auto load_item = [&](long long q, int stage) {
@@ -204,7 +210,7 @@ __global__ void __launch_bounds__(256, 1) k_ttm_last2(const double* __restrict__
     const long long o0 = rb * BM2;
     const int i0 = c * kBK;
     double* dst = xs + (size_t)stage * BM2 * LD;
-    for (int e = tid; e < BM2 * (kBK / 2); e += 256) {
+    for (int e = tid; e < BM2 * (kBK / 2); e += 512) {
       const int r = e / (kBK / 2), col = (e % (kBK / 2)) * 2;
       const long long o = o0 + r;
       const bool ok = (o < O) && (i0 + col < I);
@@ -216,21 +222,21 @@ __global__ void __launch_bounds__(256, 1) k_ttm_last2(const double* __restrict__
     if (sidx < nitems) load_item(sidx, sidx);
     cp_async_commit();
   }
-  double acc[2][RP / 8][2];
-  double pf[2][RP / 4];
-  double resid = 0.0;
+  double acc[MT][RP / 8][2];
+  double pf[MT][RP / 4];
+  double resid0 = 0.0, resid1 = 0.0;
   for (long long q = 0; q < nitems; ++q) {
     const int c = (int)(q % nchunks);
     const long long rb = blockIdx.x + (q / nchunks) * gridDim.x;
-    const long long o0 = rb * BM2 + warp * 16;
+    const long long o0 = rb * BM2 + wrow * ROWS;
     if (c == 0) {
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < RP / 8; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-      if (FUSED) {
+      if (rwarp) {
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
           for (int ks = 0; ks < RP / 4; ++ks) {
             const long long o = o0 + mt * 8 + g;
@@ -243,23 +249,37 @@ __global__ void __launch_bounds__(256, 1) k_ttm_last2(const double* __restrict__
     __syncthreads();
     if (q + kStages2 - 1 < nitems) load_item(q + kStages2 - 1, (int)((q + kStages2 - 1) % kStages2));
     cp_async_commit();
-    const double* xt = xs + (size_t)(q % kStages2) * BM2 * LD + warp * 16 * LD;
+    const double* xt = xs + (size_t)(q % kStages2) * BM2 * LD + wrow * ROWS * LD;
     const int i0 = c * kBK;
-    // T += X_tile (16 x 32) A_chunk (32 x RP)
+    if (!rwarp) {
+      // T += X_tile (ROWS x 32) A_chunk (32 x RP)
 #pragma unroll
-    for (int ks = 0; ks < kBK / 4; ++ks) {
-      const double* ar = as + (size_t)(i0 + ks * 4 + t) * LDA;
-      double bf[RP / 8];
+      for (int ks = 0; ks < kBK / 4; ++ks) {
+        const double* ar = as + (size_t)(i0 + ks * 4 + t) * LDA;
+        double bf[RP / 8];
 #pragma unroll
-      for (int nt = 0; nt < RP / 8; ++nt) bf[nt] = ar[nt * 8 + g];
+        for (int nt = 0; nt < RP / 8; ++nt) bf[nt] = ar[nt * 8 + g];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const double af = xt[(mt * 8 + g) * LD + ks * 4 + t];
+        for (int mt = 0; mt < MT; ++mt) {
+          const double af = xt[(mt * 8 + g) * LD + ks * 4 + t];
 #pragma unroll
-        for (int nt = 0; nt < RP / 8; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], af, bf[nt]);
+          for (int nt = 0; nt < RP / 8; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], af, bf[nt]);
+        }
       }
-    }
-    if (FUSED) {
+      if (c == nchunks - 1) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const long long o = o0 + mt * 8 + g;
+          if (o >= O) continue;
+#pragma unroll
+          for (int nt = 0; nt < RP / 8; ++nt) {
+            const int r = nt * 8 + 2 * t;
+            if (r < R) T[o * R + r] = acc[mt][nt][0];
+            if (r + 1 < R) T[o * R + r + 1] = acc[mt][nt][1];
+          }
+        }
+      }
+    } else {
       // Xhat_tile (16 x 32) = P_rows (16 x RP) A_chunk^T (RP x 32); residual
 #pragma unroll
       for (int nt = 0; nt < kBK / 8; ++nt) {
@@ -268,34 +288,22 @@ __global__ void __launch_bounds__(256, 1) k_ttm_last2(const double* __restrict__
 #pragma unroll
         for (int ks = 0; ks < RP / 4; ++ks) bf[ks] = ar[ks * 4 + t];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
+        for (int mt = 0; mt < MT; ++mt) {
           double c0 = 0.0, c1 = 0.0;
 #pragma unroll
           for (int ks = 0; ks < RP / 4; ++ks) dmma_8x8x4(c0, c1, pf[mt][ks], bf[ks]);
           const double2 xv =
               *reinterpret_cast<const double2*>(xt + (mt * 8 + g) * LD + nt * 8 + 2 * t);
           const double d0 = xv.x - c0, d1 = xv.y - c1;
-          resid += d0 * d0 + d1 * d1;  // zero-filled tails contribute exactly 0
-        }
-      }
-    }
-    if (c == nchunks - 1) {
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const long long o = o0 + mt * 8 + g;
-        if (o >= O) continue;
-#pragma unroll
-        for (int nt = 0; nt < RP / 8; ++nt) {
-          const int r = nt * 8 + 2 * t;
-          if (r < R) T[o * R + r] = acc[mt][nt][0];
-          if (r + 1 < R) T[o * R + r + 1] = acc[mt][nt][1];
+          resid0 = fma(d0, d0, resid0);  // zero-filled tails contribute exactly 0
+          resid1 = fma(d1, d1, resid1);
         }
       }
     }
   }
   cp_async_wait<0>();
   if (FUSED) {
-    const double s = block_sum<256>(resid, red);
+    const double s = block_sum<512>(resid0 + resid1, red);
     if (tid == 0) partial[blockIdx.x] = s;
   }
 }
@@ -611,7 +619,7 @@ static void launch_last2(const double* X, long long O, int I, const double* A, i
   }
   const long long nrb = ceil_div<long long>(O, BM2);
   const int grid = (int)std::min<long long>(nrb, sm_count());
-  k<<<grid, 256, smem, st>>>(X, O, I, A, R, T, P, partial, g_need);
+  k<<<grid, 512, smem, st>>>(X, O, I, A, R, T, P, partial, g_need);
   RTB_LAUNCH_CHECK();
 }
 

@@ -121,6 +121,8 @@ struct PcgSpec {
   int linv_stride;
   const int* linv_ok;   // per mode: Cholesky succeeded (any 0 -> status 3)
   const double* grams;  // per mode (same stride): A_n^T A_n
+  const double* evals;  // per mode (same stride): eigenpairs of A_n^T A_n (eigen-form
+  const double* evecs;  //   preconditioner when lambda is not small against mu_min)
   const int* aug_count; // [d] augmented draws per column (any 0 -> status 3)
   double aug_term;      // diagonal added per augmented draw
   int max_iter;

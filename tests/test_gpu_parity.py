@@ -344,3 +344,20 @@ def test_fast_loss_matches_direct_residual(rt, shape, ranks, noise):
         assert (fi, fs) == (di, ds)
         assert abs(fl - dl) / dl < 1e-7, (fi, fs, fl, dl)
         assert abs(frm - drm) / drm < 1e-7, (fi, fs, frm, drm)
+
+
+def test_pcg_lambda_dominated_system(rt):
+    """lambda far above the smallest eigenvalue of K^T K (here: data scaled down): the
+    eigen-form preconditioner (x) A_n^T A_n + lambda I keeps CG fast; the result
+    matches the Cholesky path."""
+    shape, ranks = (40, 36, 32), (6, 5, 4)
+    x = np.random.default_rng(12).standard_normal(shape)  # no structure: a noise fit
+    kw = dict(lam=0.5, sketched_core=1, max_iterations=3, tolerance=0.0,
+              sample_count_override=6000, record_history=1, seed=4)
+    xt = rt.Tensor.from_numpy(x)
+    ra = rt.als_run(xt, ranks, rt.options(**kw))
+    rc = rt.als_run(xt, ranks, rt.options(**kw), core_solver=1)
+    assert ra.sketch_info()["solver_path"] == 2
+    assert ra.sketch_info()["pcg_iterations"] < 60
+    for ha, hc in zip(ra.history(), rc.history()):
+        assert abs(ha[2] - hc[2]) / hc[2] < 1e-9, (ha[:2], ha[2], hc[2])

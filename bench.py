@@ -139,12 +139,17 @@ def run_reference_arm(args):
 # clocks sampler (nvidia-smi during the timed region)
 
 class Clocks:
+    """nvidia-smi sampler (100 ms period) on a reader thread that timestamps every line;
+    only samples taken inside [mark_start, stop] are reported."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
+        import threading
         self.p = None
+        self.lines = []
+        self.t0 = None
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
@@ -152,15 +157,38 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
+            return
+
+        def reader():
+            for line in self.p.stdout:
+                self.lines.append((time.perf_counter(), line))
+        self.th = threading.Thread(target=reader, daemon=True)
+        self.th.start()
+
+    def wait_first(self, timeout=10.0):
+        t = time.perf_counter()
+        while self.p is not None and not self.lines and time.perf_counter() - t < timeout:
+            time.sleep(0.01)
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
 
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.perf_counter()
+        time.sleep(0.15)  # let the sample straddling the end arrive
         self.p.terminate()
-        out, _ = self.p.communicate(timeout=10)
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            pass
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        t0 = self.t0 if self.t0 is not None else 0.0
+        for ts, line in list(self.lines):
+            if ts < t0 or ts > t1 + 0.1:
+                continue
             f = [v.strip() for v in line.split(",")]
             if len(f) < 7:
                 continue
@@ -192,6 +220,48 @@ def make_input(torch, device, seed=0):
     return x.contiguous()
 
 
+def family_table(fam, steps, n_data, n_buckets, pcg_iters, peaks, hbm_peak):
+    """Per-sweep time and roofline fraction of every major kernel family (DESIGN.md s.3).
+    Work is algorithmic: flops of the DMMA contractions, bytes of the X passes."""
+    total = SHAPE[0] * SHAPE[1] * SHAPE[2]
+    R3 = RANKS[2]
+    v = [r * (r + 1) // 2 for r in RANKS]
+    dmma = peaks["dmma_m8n8k4_tflops"]
+    rows = {}
+    def add(name, sec, flops=None, hbm_bytes=None, note=None):
+        row = {"ms_per_sweep": sec * 1e3}
+        if flops:
+            row["tflops"] = flops / sec / 1e12
+            row["frac_dmma"] = row["tflops"] / dmma
+        if hbm_bytes:
+            row["gbs"] = hbm_bytes / sec / 1e9
+            row["frac_hbm"] = row["gbs"] / hbm_peak
+        if note:
+            row["note"] = note
+        rows[name] = row
+    per = {k: v_[0] / steps for k, v_ in fam.items()}
+    if "gram" in per:
+        add("gram", per["gram"], flops=2.0 * (n_data * v[1] * v[2] + n_buckets * v[0] * v[1] * v[2]),
+            note="vech Gram: H_b GEMMs + contraction over buckets")
+    if "ttm_last_loss" in per:
+        add("ttm_last_loss", per["ttm_last_loss"], flops=4.0 * total * R3, hbm_bytes=8.0 * total,
+            note="one X pass: T = X A_3 and the direct residual (X - P A_3^T)^2")
+    if "ttm_mid" in per:
+        add("ttm_mid", per["ttm_mid"], flops=2.0 * total * RANKS[0], hbm_bytes=8.0 * total,
+            note="X x_1 A_1^T (F3 projection) + three 32 MB T-based products")
+    if "pcg" in per:
+        d = RANKS[0] * RANKS[1] * RANKS[2]
+        add("pcg", per["pcg"], note=f"{pcg_iters} CG iterations on the blocked Gram "
+            f"({v[0] * v[1] * R3 * R3 * 8 / 1e6:.0f} MB, L2-resident), d={d}")
+    if "chol" in per:
+        d = RANKS[0] * RANKS[1] * RANKS[2]
+        add("chol", per["chol"], flops=d ** 3 / 3 + 2 * d * d)
+    return rows
+
+
+PCG_ITERS = [0]
+
+
 def kernel_work(family, n_data, n_buckets):
     """Algorithmic work per launch of a kernel family."""
     d = 1
@@ -200,12 +270,21 @@ def kernel_work(family, n_data, n_buckets):
     total = SHAPE[0] * SHAPE[1] * SHAPE[2]
     if family == "chol":
         return "tensor", "TFLOP/s", d ** 3 / 3 + 2 * d * d
+    if family == "pcg":
+        # per solve: every CG iteration (+1 residual check) reads the blocked Gram once
+        # (L2-resident, but counted against the HBM roofline it would otherwise hit)
+        v = [r * (r + 1) // 2 for r in RANKS]
+        blk = v[0] * v[1] * RANKS[2] * RANKS[2] * 8
+        return "hbm", "GB/s", (PCG_ITERS[0] + 1) * blk
     if family == "gram":
         # vech-factored Gram: per data draw one rank-1 update of
         # the i1-bucket's H_b (vech(R2) x vech(R3)), then S = V1^T H over buckets.
         v = [r * (r + 1) // 2 for r in RANKS]
         return "tensor", "TFLOP/s", 2.0 * (n_data * v[1] * v[2] + n_buckets * v[0] * v[1] * v[2])
-    if family in ("ttm_last_loss", "ttm_last", "ttm_mid"):
+    if family == "ttm_last_loss":
+        # one launch per sweep: T = X A_3 plus the direct residual, 4 * total * R3 flops
+        return "tensor", "TFLOP/s", 4.0 * total * RANKS[2]
+    if family in ("ttm_last", "ttm_mid"):
         return "hbm", "GB/s", 8.0 * total
     return None, None, None
 
@@ -246,8 +325,10 @@ def run_our_arm(args):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    launches0 = rt.lib.rtucker_b200_launch_count()
     clocks = Clocks(local)
+    clocks.wait_first()
+    launches0 = rt.lib.rtucker_b200_launch_count()
+    clocks.mark_start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -275,6 +356,7 @@ def run_our_arm(args):
 
     # roofline of the dominant kernel family
     dom = max(fam, key=lambda k: fam[k][0])
+    PCG_ITERS[0] = info.get("pcg_iterations", 0) or 0
     n_data = info["data_draws"]
     n_buckets = SHAPE[0]
     bound, unit, work = kernel_work(dom, n_data, n_buckets)
@@ -362,6 +444,8 @@ def run_our_arm(args):
             "gpu_launches": int(launches),
             "roofline": roofline,
             "kernels_ms_per_sweep": {k: v[0] * 1e3 / args.steps for k, v in fam.items()},
+            "families": family_table(fam, args.steps, n_data, n_buckets, info.get("pcg_iterations"),
+                                     peaks, mp.get("hbm_gbs", 6553.3)),
             "sketch": info,
             "cpu_baseline": cpu,
         }
@@ -375,7 +459,7 @@ def run_our_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -646,7 +646,7 @@ class Engine {
     pgram_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
     pev_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
     pvec_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
-    pst_.ensure(64 * 4, st_);
+    pst_.ensure(64 * 4 + 8 * 8, st_);
     pcg_status_.ensure(16, st_);
     ns_.ensure(64 * 4, st_);
     ranks_dev_.ensure(64 * 4, st_);
@@ -1001,10 +1001,15 @@ class Engine {
       ps.linv_stride = eig_stride_;
       ps.linv_ok = spd_ok_.as<int>();
       ps.grams = grams_.as<double>();
+      ps.lambda = opt_.lambda;
+      double* prep = reinterpret_cast<double*>(pst_.as<int>() + 64);
+      int* eskip = pst_.as<int>() + 32;
+      pcg_prepare(ps, prep, eskip, st_);
       sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, pev_.as<double>(),
-                pvec_.as<double>(), pst_.as<int>(), N_, st_);
+                pvec_.as<double>(), pst_.as<int>(), N_, st_, eskip);
       ps.evals = pev_.as<double>();
       ps.evecs = pvec_.as<double>();
+      ps.prep = prep;
       ps.aug_count = gram_aug_counts(gs, gram_work_.p);
       ps.aug_term = gram_aug_term(gs);
       ps.max_iter = 80;

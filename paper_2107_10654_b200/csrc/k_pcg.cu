@@ -65,6 +65,7 @@ struct PcgArgs {
   const double* grams;    // per mode (stride): A_n^T A_n
   const double* evals;    // per mode (stride): eigenvalues of A_n^T A_n (descending)
   const double* evecs;    // per mode (stride): V[i*R+k], column k = eigenvector k
+  const double* prep;     // k_pcg_prep: [0] ||G|| estimate, [1] 1/mu_min(K^T K), [2] eigen form
   const int* aug_count;
   double aug_term;
   double lambda;
@@ -404,11 +405,73 @@ __device__ void reduce_rows(const PcgArgs& A, const PcgShared& sh, const double*
   }
 }
 
+constexpr double kEigenAbove = 4.0;           // lambda / mu_min above which the eigen form is used
+constexpr double kMaxLambdaOverMu = 1e12;     // beyond: not worth CG
+
+// Warp n (one per mode, in parallel): mu_max(A_n^T A_n) and ||P_n||_2 = 1/mu_min by
+// power iteration (lane = row). mu_max gives the ||G|| estimate of the stopping test
+// (an underestimate only tightens it). The P form of the preconditioner drops lambda:
+// every direction with lambda > mu(K^T K) becomes an outlier eigenvalue of M^-1 G that
+// CG removes in about one iteration, so a moderate lambda / mu_min(K^T K) is cheap (C2:
+// ~2.5, 15 iterations); above kEigenAbove the exact eigen form is used, and only then
+// are the factor-Gram eigenpairs computed (skip flags for the eigensolver).
+__global__ void k_pcg_prep(const double* __restrict__ grams, const double* __restrict__ pinv,
+                           int stride, PcgShared sh, double lambda, double* prep, int* skip) {
+  // warp w: mode w >> 1, matrix (w & 1) ? P_n : G_n; row i of M in lane i's registers,
+  // the iterate v broadcast through shared memory (independent loads, short chains)
+  __shared__ double est[2 * kMaxOrder];
+  __shared__ double vs[2 * kMaxOrder][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < 2 * sh.order) {
+    const int n = warp >> 1, which = warp & 1, R = sh.R[n];
+    const double* M = (which ? pinv : grams) + (size_t)n * stride;
+    double row[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) row[j] = (lane < R && j < R) ? M[lane * R + j] : 0.0;
+    double v = lane < R ? 1.0 + 0.01 * lane : 0.0, mu = 0.0;
+    for (int itp = 0; itp < 24; ++itp) {
+      vs[warp][lane] = v;
+      __syncwarp();
+      double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        y0 = fma(row[j], vs[warp][j], y0);
+        y1 = fma(row[j + 1], vs[warp][j + 1], y1);
+        y2 = fma(row[j + 2], vs[warp][j + 2], y2);
+        y3 = fma(row[j + 3], vs[warp][j + 3], y3);
+      }
+      const double y = (y0 + y1) + (y2 + y3);
+      double yy = y * y, vy = v * y, vv = v * v;
+      for (int o = 16; o > 0; o >>= 1) {
+        yy += __shfl_xor_sync(0xffffffffu, yy, o);
+        vy += __shfl_xor_sync(0xffffffffu, vy, o);
+        vv += __shfl_xor_sync(0xffffffffu, vv, o);
+      }
+      mu = vv > 0.0 ? vy / vv : 0.0;
+      v = yy > 0.0 ? y * rsqrt(yy) : 0.0;
+      __syncwarp();
+    }
+    if (lane == 0) est[2 * n + which] = mu;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double g = 1.0, pn = 1.0;
+    for (int n = 0; n < sh.order; ++n) {
+      g *= est[2 * n];
+      pn *= est[2 * n + 1];
+    }
+    const bool eig = !(lambda * pn <= kEigenAbove);
+    prep[0] = g + lambda;
+    prep[1] = pn;
+    prep[2] = eig ? 1.0 : 0.0;
+    for (int n = 0; n < sh.order; ++n) skip[n] = eig ? 0 : 1;
+  }
+}
+
 template <int RM, int RX>
 __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgShared shc) {
   extern __shared__ __align__(16) double sm[];
   const PcgShared& sh = shc;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;  // stays in the parameter bank (dynamic indexing is cheap)
   const int d = sh.d;
   const int dv = (d + 1) & ~1;
   double* Ps = sm;                          // [order][RM][RM]: P_n (P form) or V_n (eigen form)
@@ -447,58 +510,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
     }
   }
   __syncthreads();
-  // Warp n (one per mode, in parallel): mu_max(A_n^T A_n) and ||P_n||_2 = 1/mu_min by
-  // power iteration (lane = row). mu_max gives the ||G|| estimate of the stopping test
-  // (an underestimate only tightens it). The preconditioner drops lambda: every
-  // direction with lambda > mu(K^T K) becomes an outlier eigenvalue of M^-1 G that
-  // CG removes in about one iteration, so a moderate lambda / mu_min(K^T K) is
-  // harmless (C2: ~2.5, 15 iterations); beyond 100 (near-noise fits, hundreds of
-  // outliers) the Cholesky path is used directly.
-  if (warp < sh.order) {
-    const int n = warp, R = sh.R[n];
-    const double* Gm = A.grams + (size_t)n * A.linv_stride;
-    const double* Pm = Ps + n * RM * RM;
-    double est[2];
-#pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      double v = lane < R ? 1.0 + 0.01 * lane : 0.0, mu = 0.0;
-      for (int itp = 0; itp < 40; ++itp) {
-        double y = 0.0;
-        for (int j = 0; j < R; ++j) {
-          const double mij = lane < R ? (which == 0 ? Gm[lane * R + j] : Pm[lane * RM + j]) : 0.0;
-          y = fma(mij, __shfl_sync(0xffffffffu, v, j), y);
-        }
-        double yy = y * y, vy = v * y, vv = v * v;
-        for (int o = 16; o > 0; o >>= 1) {
-          yy += __shfl_xor_sync(0xffffffffu, yy, o);
-          vy += __shfl_xor_sync(0xffffffffu, vy, o);
-          vv += __shfl_xor_sync(0xffffffffu, vv, o);
-        }
-        mu = vv > 0.0 ? vy / vv : 0.0;
-        v = yy > 0.0 ? y * rsqrt(yy) : 0.0;
-      }
-      est[which] = mu;
-    }
-    if (lane == 0) {
-      red[2 * n] = est[0];
-      red[2 * n + 1] = est[1];
-    }
-  }
-  __syncthreads();
-  double gnorm = 1.0, pnorm = 1.0;
-  for (int n = 0; n < sh.order; ++n) {
-    gnorm *= red[2 * n];
-    pnorm *= red[2 * n + 1];
-  }
-  gnorm += A.lambda;
-  __syncthreads();
-  if (A.prof && blockIdx.x == 0 && threadIdx.x == 0) {
-    A.prof[14] = __double_as_longlong(gnorm);
-    A.prof[15] = __double_as_longlong(pnorm);
-  }
+  const double gnorm = A.prep[0], pnorm = A.prep[1];
   // lambda-free P form while lambda is small against mu_min(K^T K) (few outlier
   // eigenvalues), else the exact eigen form of (x) A_n^T A_n + lambda I
-  const bool eig = !(A.lambda * pnorm <= 4.0);
+  const bool eig = A.prep[2] != 0.0;
+  if (!(A.lambda * pnorm <= kMaxLambdaOverMu)) {  // hopeless for CG: Cholesky path
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      A.status[0] = 3;
+      A.status[1] = 0;
+    }
+    return;
+  }
   if (eig) {
     for (int n = 0; n < sh.order; ++n) {
       const int R = sh.R[n];
@@ -677,7 +699,24 @@ size_t pcg_smem(int d, int order, const int* ranks, int rm) {
   return 8 * (2 * (size_t)order * rm * rm + 6 * dv + 32 + extra);
 }
 
+PcgShared pcg_shape(const PcgSpec& spec) {
+  PcgShared sh{};
+  sh.d = spec.d;
+  sh.order = spec.order;
+  for (int n = spec.order - 1; n >= 0; --n) {
+    sh.R[n] = spec.ranks[n];
+    sh.m[n] = spec.ranks[n] * (spec.ranks[n] + 1) / 2;
+  }
+  return sh;
+}
+
 }  // namespace
+
+void pcg_prepare(const PcgSpec& spec, double* prep_dev, int* skip_dev, cudaStream_t st) {
+  k_pcg_prep<<<1, 64 * spec.order, 0, st>>>(spec.grams, spec.pinv, spec.linv_stride,
+                                            pcg_shape(spec), spec.lambda, prep_dev, skip_dev);
+  RTB_LAUNCH_CHECK();
+}
 
 size_t pcg_work_bytes(int d, int r1) {
   const size_t m1 = (size_t)r1 * (r1 + 1) / 2;
@@ -733,6 +772,7 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   a.grams = spec.grams;
   a.evals = spec.evals;
   a.evecs = spec.evecs;
+  a.prep = spec.prep;
   a.aug_count = spec.aug_count;
   a.aug_term = spec.aug_term;
   a.lambda = spec.lambda;

@@ -123,6 +123,7 @@ struct PcgSpec {
   const double* grams;  // per mode (same stride): A_n^T A_n
   const double* evals;  // per mode (same stride): eigenpairs of A_n^T A_n (eigen-form
   const double* evecs;  //   preconditioner when lambda is not small against mu_min)
+  const double* prep;   // [3] from pcg_prepare
   const int* aug_count; // [d] augmented draws per column (any 0 -> status 3)
   double aug_term;      // diagonal added per augmented draw
   int max_iter;
@@ -130,6 +131,9 @@ struct PcgSpec {
   double check_tol;     // accept when ||b - G x|| <= check_tol (||G||~ ||x|| + ||b||)
 };
 size_t pcg_work_bytes(int d, int r1);
+// norm estimates and preconditioner form (prep_dev[3]); skip_dev[order] = 1 where the
+// factor-Gram eigenpairs are not needed (feed to sym_eigen as skip flags)
+void pcg_prepare(const PcgSpec& spec, double* prep_dev, int* skip_dev, cudaStream_t st);
 bool pcg_supported(int d, int order, const int* ranks);
 // x = G^-1 b by Kronecker-preconditioned CG; status_dev[0] = 0 ok, 1 residual check
 // failed, 2 breakdown (non-SPD), 3 not applicable; status_dev[1] = iterations.

@@ -843,7 +843,7 @@ class Engine {
       const int stride = std::max(eig_stride_, Rn * Rn);
       if (Rn <= 32) {
         spd_small(kk, ns_one(Rn), stride, (double)Rn * DBL_EPSILON, linv_.as<double>(), pv, okf,
-                  1, st_);
+                  1, st_, Rn);
         sym_eigen(kk, ns_one(Rn), Rn, stride, evals_.as<double>(), evecs_.as<double>(),
                   eig_status_.as<int>(), 1, st_, okf);
         k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one(Rn),
@@ -900,7 +900,7 @@ class Engine {
       const int* okm = nullptr;
       if (rmax_ <= 32) {
         spd_small(grams_.as<double>(), ns_.as<int>(), eig_stride_, (double)maxI * DBL_EPSILON,
-                  linv_.as<double>(), pgram_.as<double>(), spd_ok_.as<int>(), N_, st_);
+                  linv_.as<double>(), pgram_.as<double>(), spd_ok_.as<int>(), N_, st_, rmax_);
         okm = spd_ok_.as<int>();
       }
       sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, evals_.as<double>(),

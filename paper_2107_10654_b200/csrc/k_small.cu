@@ -395,6 +395,7 @@ __global__ void __launch_bounds__(1024) k_sym_eigen_cta(const double* in, const 
 // matrix). Optionally also writes P = M^-1 = Linv^T Linv.
 // Loops run to 32 with compile-time indices so row[] / x[] stay in registers;
 // the matrix is padded with the identity beyond n.
+template <int NM>
 __global__ void __launch_bounds__(128) k_spd_small(const double* in, const int* ns, int stride,
                                                    double tolrel, double* linv, double* pinv,
                                                    int* ok, int nmat) {
@@ -405,13 +406,13 @@ __global__ void __launch_bounds__(128) k_spd_small(const double* in, const int* 
   const int n = ns[b];
   const double* src = in + (size_t)b * stride;
   constexpr unsigned FULL = 0xffffffffu;
-  double row[32];
+  double row[NM];
 #pragma unroll
-  for (int q = 0; q < 32; ++q)
+  for (int q = 0; q < NM; ++q)
     row[q] = (lane < n && q < n) ? src[lane * n + q] : (lane == q ? 1.0 : 0.0);
   double dmax = 0.0;
 #pragma unroll
-  for (int q = 0; q < 32; ++q)
+  for (int q = 0; q < NM; ++q)
     if (q == lane && lane < n) dmax = fabs(row[q]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(FULL, dmax, o));
@@ -419,14 +420,14 @@ __global__ void __launch_bounds__(128) k_spd_small(const double* in, const int* 
   bool bad = false;
   double invd = 1.0;
 #pragma unroll
-  for (int c = 0; c < 32; ++c) {
+  for (int c = 0; c < NM; ++c) {
     const double piv = __shfl_sync(FULL, row[c], c);
     bad |= (c < n) && !(piv > tol);
     const double rs = rsqrt(piv);
     row[c] = (lane == c) ? piv * rs : ((lane > c) ? row[c] * rs : row[c]);
     invd = (lane == c) ? rs : invd;
 #pragma unroll
-    for (int l = 1; l < 32; ++l) {
+    for (int l = 1; l < NM; ++l) {
       if (l > c) {
         const double lc = __shfl_sync(FULL, row[c], l);
         row[l] = (lane >= l) ? row[l] - row[c] * lc : row[l];
@@ -437,12 +438,12 @@ __global__ void __launch_bounds__(128) k_spd_small(const double* in, const int* 
   if (lane == 0) ok[b] = bad ? 0 : 1;
   if (bad) return;
   // Linv: lane = column
-  double x[32];
+  double x[NM];
 #pragma unroll
-  for (int rr = 0; rr < 32; ++rr) {
+  for (int rr = 0; rr < NM; ++rr) {
     double s0 = (rr == lane) ? 1.0 : 0.0, s1 = 0.0;
 #pragma unroll
-    for (int l = 0; l < 31; ++l) {
+    for (int l = 0; l < NM - 1; ++l) {
       if (l < rr) {
         const double lv = __shfl_sync(FULL, row[l], rr);
         if (l & 1) s1 -= lv * x[l];
@@ -455,13 +456,13 @@ __global__ void __launch_bounds__(128) k_spd_small(const double* in, const int* 
   double* lo = linv + (size_t)b * stride;
   if (lane < n) {
 #pragma unroll
-    for (int q = 0; q < 32; ++q)
+    for (int q = 0; q < NM; ++q)
       if (q < n) lo[q * n + lane] = x[q];  // Linv[q][lane]
   }
   if (pinv) {
     // P[i][j] = sum_k Linv[k][i] Linv[k][j]; lane j holds column j (x[k] = Linv[k][j])
 #pragma unroll
-    for (int q = 0; q < 32; ++q) xs[wib][q][lane] = x[q];
+    for (int q = 0; q < NM; ++q) xs[wib][q][lane] = x[q];
     __syncwarp();
     double* po = pinv + (size_t)b * stride;
     if (lane < n) {
@@ -609,8 +610,14 @@ void sym_eigen(const double* in, const int* ns_dev, int nmax, int stride, double
 }
 
 void spd_small(const double* in, const int* ns_dev, int stride, double tolrel, double* linv,
-               double* pinv, int* ok, int nmat, cudaStream_t st) {
-  k_spd_small<<<ceil_div(nmat, 4), 128, 0, st>>>(in, ns_dev, stride, tolrel, linv, pinv, ok, nmat);
+               double* pinv, int* ok, int nmat, cudaStream_t st, int nmax) {
+  // rows beyond n are padded with the identity, so any NM >= n gives the same factor
+  if (nmax <= 8)
+    k_spd_small<8><<<ceil_div(nmat, 4), 128, 0, st>>>(in, ns_dev, stride, tolrel, linv, pinv, ok, nmat);
+  else if (nmax <= 16)
+    k_spd_small<16><<<ceil_div(nmat, 4), 128, 0, st>>>(in, ns_dev, stride, tolrel, linv, pinv, ok, nmat);
+  else
+    k_spd_small<32><<<ceil_div(nmat, 4), 128, 0, st>>>(in, ns_dev, stride, tolrel, linv, pinv, ok, nmat);
   RTB_LAUNCH_CHECK();
 }
 

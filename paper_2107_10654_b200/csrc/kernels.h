@@ -30,7 +30,7 @@ __global__ void k_leverage_chol(const FactorSet fs, const double* linv, int stri
                                 double* scores, const long long* score_off, int* ranks);
 // batched small SPD Cholesky (n <= 32): Linv (+ optional P = M^-1), ok flags
 void spd_small(const double* in, const int* ns_dev, int stride, double tolrel, double* linv,
-               double* pinv, int* ok, int nmat, cudaStream_t st);
+               double* pinv, int* ok, int nmat, cudaStream_t st, int nmax = 32);
 __global__ void k_score_cdf(const double* scores, const long long* off, const int* rows,
                             int order, double* cdf, double* sums);
 __global__ void k_sym_pinv(const double* evals, const double* evecs, const int* ns, int stride,

@@ -411,6 +411,106 @@ __global__ void __launch_bounds__(128) k_ttm_mid(const double* __restrict__ X, l
   }
 }
 
+// Persistent strided-mode contraction for large column counts (the F_N projection
+// X x_1 A_1^T): A^T (R x I, padded) resident in shared memory, 128-column tiles (8
+// warps x 16 columns) of X streamed through a KS-deep cp.async pipeline that runs
+// across tiles; every DMMA operand from shared memory. Requires J % 128 == 0 (a
+// tile never straddles two o).
+constexpr int BJ2 = 128;
+constexpr int kStagesMid = 4;
+template <int RP>
+__global__ void __launch_bounds__(256, 1) k_ttm_mid2(const double* __restrict__ X, long long O,
+                                                     int I, long long J,
+                                                     const double* __restrict__ A, int R,
+                                                     double* __restrict__ out) {
+  constexpr int LDX = BJ2 + 8;     // (8t + g) mod 16 -> 2-way at most
+  extern __shared__ __align__(16) double sm3[];
+  const int Ip = ceil_div(I, kBK) * kBK;
+  const int LDT = Ip + 4;                 // A^T rows: (4g + t) mod 16 -> 2-way at most
+  double* at = sm3;                       // [RP][LDT]
+  double* xs = at + (size_t)RP * LDT;     // [kStagesMid][kBK][LDX]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const long long ntiles = O * J / BJ2;
+  const int nchunks = ceil_div(I, kBK);
+  for (int e = tid; e < RP * LDT; e += 256) {
+    const int r = e / LDT, i = e - r * LDT;
+    at[e] = (i < I && r < R) ? A[(size_t)i * R + r] : 0.0;
+  }
+  const long long my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long nitems = my_tiles * nchunks;
+  auto load_item = [&](long long q, int stage) {
+    const long long tile = blockIdx.x + (q / nchunks) * gridDim.x;
+    const int c = (int)(q % nchunks);
+    const long long c0 = tile * BJ2;
+    const long long o = c0 / J, j0 = c0 - o * J;
+    const int i0 = c * kBK;
+    double* dst = xs + (size_t)stage * kBK * LDX;
+    for (int e = tid; e < kBK * (BJ2 / 2); e += 256) {
+      const int r = e / (BJ2 / 2), col = (e % (BJ2 / 2)) * 2;
+      const bool ok = i0 + r < I;
+      cp_async16(dst + r * LDX + col, ok ? X + (o * I + i0 + r) * J + j0 + col : X, ok);
+    }
+  };
+#pragma unroll
+  for (int sidx = 0; sidx < kStagesMid - 1; ++sidx) {
+    if (sidx < nitems) load_item(sidx, sidx);
+    cp_async_commit();
+  }
+  double acc[RP / 8][2][2];
+  for (long long q = 0; q < nitems; ++q) {
+    const int c = (int)(q % nchunks);
+    if (c == 0) {
+#pragma unroll
+      for (int mt = 0; mt < RP / 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    }
+    cp_async_wait<kStagesMid - 2>();
+    __syncthreads();
+    if (q + kStagesMid - 1 < nitems)
+      load_item(q + kStagesMid - 1, (int)((q + kStagesMid - 1) % kStagesMid));
+    cp_async_commit();
+    const double* xt = xs + (size_t)(q % kStagesMid) * kBK * LDX + warp * 16;
+    const int i0 = c * kBK;
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      double af[RP / 8];
+#pragma unroll
+      for (int mt = 0; mt < RP / 8; ++mt) af[mt] = at[(size_t)(mt * 8 + g) * LDT + i0 + ks * 4 + t];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const double bf = xt[(ks * 4 + t) * LDX + nt * 8 + g];
+#pragma unroll
+        for (int mt = 0; mt < RP / 8; ++mt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf);
+      }
+    }
+    if (c == nchunks - 1) {
+      const long long tile = blockIdx.x + (q / nchunks) * gridDim.x;
+      const long long c0 = tile * BJ2;
+      const long long o = c0 / J, j0 = c0 - o * J + warp * 16;
+#pragma unroll
+      for (int mt = 0; mt < RP / 8; ++mt) {
+        const int r = mt * 8 + g;
+        if (r >= R) continue;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          double2 v2;
+          v2.x = acc[mt][nt][0];
+          v2.y = acc[mt][nt][1];
+          *reinterpret_cast<double2*>(out + (o * R + r) * J + j0 + nt * 8 + 2 * t) = v2;
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+static size_t mid2_smem(int I, int rp) {
+  const size_t ip = (size_t)ceil_div(I, kBK) * kBK;
+  return ((size_t)rp * (ip + 4) + (size_t)kStagesMid * kBK * (BJ2 + 8)) * 8;
+}
+
 __global__ void k_sum_splits(const double* __restrict__ part, long long n, int splits,
                              double* __restrict__ out) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -710,11 +810,40 @@ static void launch_mid(const double* X, long long O, int I, long long J, const d
   }
 }
 
+template <int RP>
+static void launch_mid2(const double* X, long long O, int I, long long J, const double* A, int R,
+                        double* out, cudaStream_t st) {
+  const size_t smem = mid2_smem(I, RP);
+  auto k = k_ttm_mid2<RP>;
+  static bool attr = false;
+  if (!attr) {
+    RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  const long long ntiles = O * J / BJ2;
+  const int grid = (int)std::min<long long>(ntiles, sm_count());
+  k<<<grid, 256, smem, st>>>(X, O, I, J, A, R, out);
+  RTB_LAUNCH_CHECK();
+}
+
 void ttm_mid(const double* X, long long O, int I, long long J, const double* A, int R, double* out,
              cudaStream_t st) {
   const bool v2 = (J % 2) == 0;
   const int rp = R <= 8 ? 8 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
   if (R > 32) throw Error(4, "ttm_mid: rank > 32 not supported by the DMMA path");
+  {
+    // persistent path: whole 128-column tiles, enough of them to keep every SM busy,
+    // and A resident next to the pipeline
+    const size_t smem = mid2_smem(I, rp);
+    if (J % BJ2 == 0 && O * J / BJ2 >= 4LL * sm_count() && smem <= 220 * 1024) {
+      switch (rp) {
+        case 8: launch_mid2<8>(X, O, I, J, A, R, out, st); return;
+        case 16: launch_mid2<16>(X, O, I, J, A, R, out, st); return;
+        case 24: launch_mid2<24>(X, O, I, J, A, R, out, st); return;
+        default: launch_mid2<32>(X, O, I, J, A, R, out, st); return;
+      }
+    }
+  }
 #define RTB_M(RPV)                                        \
   case RPV:                                               \
     if (v2) launch_mid<RPV, 2>(X, O, I, J, A, R, out, st); \

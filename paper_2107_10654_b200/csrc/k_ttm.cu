@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last2(const double* __restrict__
     if (sidx < nitems) load_item(sidx, sidx);
     cp_async_commit();
   }
-  double acc[MT][RP / 8][2];
+  double acc[2][MT][RP / 8][2];  // even / odd k steps: twice the DMMA chains
   double pf[MT][RP / 4];
   double resid0 = 0.0, resid1 = 0.0;
   for (long long q = 0; q < nitems; ++q) {
@@ -231,9 +231,11 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last2(const double* __restrict__
     const long long o0 = rb * BM2 + wrow * ROWS;
     if (c == 0) {
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int nt = 0; nt < RP / 8; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < RP / 8; ++nt) acc[h][mt][nt][0] = acc[h][mt][nt][1] = 0.0;
       if (rwarp) {
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
@@ -263,7 +265,8 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last2(const double* __restrict__
         for (int mt = 0; mt < MT; ++mt) {
           const double af = xt[(mt * 8 + g) * LD + ks * 4 + t];
 #pragma unroll
-          for (int nt = 0; nt < RP / 8; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], af, bf[nt]);
+          for (int nt = 0; nt < RP / 8; ++nt)
+            dmma_8x8x4(acc[ks & 1][mt][nt][0], acc[ks & 1][mt][nt][1], af, bf[nt]);
         }
       }
       if (c == nchunks - 1) {
@@ -274,8 +277,8 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last2(const double* __restrict__
 #pragma unroll
           for (int nt = 0; nt < RP / 8; ++nt) {
             const int r = nt * 8 + 2 * t;
-            if (r < R) T[o * R + r] = acc[mt][nt][0];
-            if (r + 1 < R) T[o * R + r + 1] = acc[mt][nt][1];
+            if (r < R) T[o * R + r] = acc[0][mt][nt][0] + acc[1][mt][nt][0];
+            if (r + 1 < R) T[o * R + r + 1] = acc[0][mt][nt][1] + acc[1][mt][nt][1];
           }
         }
       }
@@ -289,9 +292,14 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last2(const double* __restrict__
         for (int ks = 0; ks < RP / 4; ++ks) bf[ks] = ar[ks * 4 + t];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          double c0 = 0.0, c1 = 0.0;
+          double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
-          for (int ks = 0; ks < RP / 4; ++ks) dmma_8x8x4(c0, c1, pf[mt][ks], bf[ks]);
+          for (int ks = 0; ks < RP / 4; ks += 2) {
+            dmma_8x8x4(c0, c1, pf[mt][ks], bf[ks]);
+            if (ks + 1 < RP / 4) dmma_8x8x4(e0, e1, pf[mt][ks + 1], bf[ks + 1]);
+          }
+          c0 += e0;
+          c1 += e1;
           const double2 xv =
               *reinterpret_cast<const double2*>(xt + (mt * 8 + g) * LD + nt * 8 + 2 * t);
           const double d0 = xv.x - c0, d1 = xv.y - c1;
@@ -457,14 +465,17 @@ __global__ void __launch_bounds__(256, 1) k_ttm_mid2(const double* __restrict__ 
     if (sidx < nitems) load_item(sidx, sidx);
     cp_async_commit();
   }
-  double acc[RP / 8][2][2];
+  // two accumulator sets (even / odd k steps): twice the independent DMMA chains
+  double acc[2][RP / 8][2][2];
   for (long long q = 0; q < nitems; ++q) {
     const int c = (int)(q % nchunks);
     if (c == 0) {
 #pragma unroll
-      for (int mt = 0; mt < RP / 8; ++mt)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        for (int mt = 0; mt < RP / 8; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) acc[h][mt][nt][0] = acc[h][mt][nt][1] = 0.0;
     }
     cp_async_wait<kStagesMid - 2>();
     __syncthreads();
@@ -482,7 +493,8 @@ __global__ void __launch_bounds__(256, 1) k_ttm_mid2(const double* __restrict__ 
       for (int nt = 0; nt < 2; ++nt) {
         const double bf = xt[(ks * 4 + t) * LDX + nt * 8 + g];
 #pragma unroll
-        for (int mt = 0; mt < RP / 8; ++mt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf);
+        for (int mt = 0; mt < RP / 8; ++mt)
+          dmma_8x8x4(acc[ks & 1][mt][nt][0], acc[ks & 1][mt][nt][1], af[mt], bf);
       }
     }
     if (c == nchunks - 1) {
@@ -496,8 +508,8 @@ __global__ void __launch_bounds__(256, 1) k_ttm_mid2(const double* __restrict__ 
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           double2 v2;
-          v2.x = acc[mt][nt][0];
-          v2.y = acc[mt][nt][1];
+          v2.x = acc[0][mt][nt][0] + acc[1][mt][nt][0];
+          v2.y = acc[0][mt][nt][1] + acc[1][mt][nt][1];
           *reinterpret_cast<double2*>(out + (o * R + r) * J + j0 + nt * 8 + 2 * t) = v2;
         }
       }

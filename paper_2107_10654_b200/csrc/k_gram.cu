@@ -536,11 +536,14 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
   extern __shared__ __align__(16) double smb[];
   const int RL = v.rowlen;
   const int RLp = (RL + 1) & ~1;
-  double* zr = smb;                   // [KC][LDZ]
-  double* zc = zr + KC * LDZ;         // [KC][LDZ]
-  double* frow = zc + KC * LDZ;       // [2][KC][RLp] (double buffered)
-  double* w2s = frow + 2 * KC * RLp;  // [2][KC]
-  double* wxs = w2s + 2 * KC;         // [2][KC]
+  // software pipeline, one barrier per chunk: while some warps still run the DMMAs of
+  // chunk k, others already generate the operands of chunk k+1 into the other buffer
+  // and the draw records of chunk k+2 land in the third frow buffer.
+  double* zr = smb;                   // [2][KC][LDZ]
+  double* zc = zr + 2 * KC * LDZ;     // [2][KC][LDZ]
+  double* frow = zc + 2 * KC * LDZ;   // [3][KC][RLp]
+  double* w2s = frow + 3 * KC * RLp;  // [3][KC]
+  double* wxs = w2s + 3 * KC;         // [3][KC]
   const int b = blockIdx.x;
   if (b >= *nbuckets) return;
   const int N = v.N;
@@ -585,18 +588,14 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
 #pragma unroll
   for (int j = 0; j < NTT; ++j) acc[j][0] = acc[j][1] = 0.0;
   const int rt0 = warp;
-  if (len > 0) stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, 0, 0, RL, RLp);
-  cp_async_commit();
-  for (int k0 = 0, it = 0; k0 < len; k0 += KC, ++it) {
-    const int cur = it & 1;
-    if (k0 + KC < len)
-      stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, k0 + KC, cur ^ 1, RL,
-                              RLp);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();  // chunk `cur` landed; previous MMA readers of zr / zc are done
-    const double* fr = frow + cur * KC * RLp;
-    const double* w2c = w2s + cur * KC;
+  const int nch = (len + KC - 1) / KC;
+  // generate chunk kk (its frow buffer kk % 3 has landed) into z buffer kk & 1
+  auto generate = [&](int kk) {
+    const int fb = kk % 3, zb = kk & 1;
+    const double* fr = frow + fb * KC * RLp;
+    const double* w2c = w2s + fb * KC;
+    double* zrb = zr + zb * KC * LDZ;
+    double* zcb = zc + zb * KC * LDZ;
 #pragma unroll 4
     for (int j = 0; j < KC / 4; ++j) {
       const int k = k0r + 4 * j;
@@ -612,11 +611,41 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
 #pragma unroll
         for (int q = 0; q < NC; ++q) zcv *= f[co[2 * q]] * f[co[2 * q + 1]];
       }
-      zr[k * LDZ + c] = zrv;
-      zc[k * LDZ + c] = zcv;
+      zrb[k * LDZ + c] = zrv;
+      zcb[k * LDZ + c] = zcv;
+    }
+  };
+  if (nch > 0) stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, 0, 0, RL, RLp);
+  cp_async_commit();
+  if (nch > 1) stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, KC, 1, RL, RLp);
+  cp_async_commit();
+  cp_async_wait<1>();
+  __syncthreads();
+  if (nch > 0) generate(0);
+  __syncthreads();
+  for (int kk = 0; kk < nch; ++kk) {
+    // records of chunk kk+2 into frow buffer (kk+2) % 3 (last read by generate(kk-1))
+    if (kk + 2 < nch)
+      stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, (kk + 2) * KC,
+                              (kk + 2) % 3, RL, RLp);
+    cp_async_commit();
+    const int zb = kk & 1;
+    if (rt0 < MT) {
+      const double* zrb = zr + zb * KC * LDZ;
+      const double* zcb = zc + zb * KC * LDZ;
+#pragma unroll
+      for (int ks = 0; ks < KC / 4; ++ks) {
+        const double* zrk = zrb + (ks * 4 + t4) * LDZ;
+        const double* zck = zcb + (ks * 4 + t4) * LDZ;
+        const double a0 = zrk[rt0 * 8 + g];
+#pragma unroll
+        for (int nt = 0; nt < NTT; ++nt) dmma_8x8x4(acc[nt][0], acc[nt][1], a0, zck[nt * 8 + g]);
+      }
     }
     if (hwarp) {
-      const double* wxc = wxs + cur * KC;
+      const int fb = kk % 3;
+      const double* fr = frow + fb * KC * RLp;
+      const double* wxc = wxs + fb * KC;
       const int R2 = v.R[1], R3 = v.R[2], o2 = v.roff[1], o3 = v.roff[2];
 #pragma unroll
       for (int ks = 0; ks < KC / 4; ++ks) {
@@ -635,17 +664,12 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
           for (int j = 0; j < 2; ++j) dmma_8x8x4(hacc[i][j][0], hacc[i][j][1], af[i], bf[j]);
       }
     }
-    __syncthreads();
-    if (rt0 < MT) {
-#pragma unroll
-      for (int ks = 0; ks < KC / 4; ++ks) {
-        const double* zrk = zr + (ks * 4 + t4) * LDZ;
-        const double* zck = zc + (ks * 4 + t4) * LDZ;
-        const double a0 = zrk[rt0 * 8 + g];
-#pragma unroll
-        for (int nt = 0; nt < NTT; ++nt) dmma_8x8x4(acc[nt][0], acc[nt][1], a0, zck[nt * 8 + g]);
-      }
+    if (kk + 1 < nch) {
+      cp_async_wait<1>();   // chunk kk+1's records (this thread's copies) have landed
+      __syncthreads();      // ... everyone's; and z buffer (kk+1)&1 is free (MMA kk-1 done)
+      generate(kk + 1);
     }
+    __syncthreads();        // z buffer (kk+1)&1 complete; MMA kk done before it is reused
   }
   cp_async_wait<0>();
   double* Hb = H + (size_t)b * v.Hsz;
@@ -675,7 +699,7 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
 
 size_t vech_bucket2_smem(const VechSpec& v) {
   const size_t rlp = (size_t)((v.rowlen + 1) & ~1);
-  return (size_t)(2 * KC * LDZ + 2 * KC * rlp + 4 * KC) * 8 + 16;
+  return (size_t)(4 * KC * LDZ + 3 * KC * rlp + 6 * KC) * 8 + 16;
 }
 
 // h_b[p'] = sum_{t in b} w_t^2 x_t prod_{n>=1} a_n(i_n)[p_n] from the draw records.
@@ -964,7 +988,8 @@ void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
   const int NTn = (int)((v.Ncol + 7) / 8);
   const int nr = v.msplit, nc = v.N - 1 - v.msplit;
   const bool whole = (v.Mrow + 7) / 8 <= kBT && NTn <= kBT && v.N >= 2 &&
-                     ((nr == 1 && nc <= 2) || (nr == 2 && nc == 1));
+                     ((nr == 1 && nc <= 2) || (nr == 2 && nc == 1)) &&
+                     vech_bucket2_smem(v) <= 227 * 1024;
   // h_b by the bucket kernel's spare warp in the 3-way case (R_2, R_3 <= 16)
   const bool fused_h = whole && nr == 1 && nc == 1 && v.R[1] <= 16 && v.R[2] <= 16 &&
                        (v.Mrow + 7) / 8 < kBWarps;
@@ -973,9 +998,7 @@ void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
                     st>>>(spec, v, l.keys_sorted, l.dmode, l.drow);
     RTB_LAUNCH_CHECK();
     const size_t smb = vech_bucket2_smem(v);
-    VechSpec vmax = v;
-    vmax.rowlen = kMaxRow;
-    const int smax = (int)vech_bucket2_smem(vmax);
+    const int smax = 227 * 1024;
     auto launch = [&](auto kern) {
       RTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
       kern<<<I1, kBWarps * 32, smb, st>>>(spec, v, l.dw2, l.dwx, l.drow, l.bstart, l.blen,

@@ -878,6 +878,99 @@ __global__ void __launch_bounds__(kTh) k_vech_contract(GramSpec spec, VechSpec v
   }
 }
 
+// (C') S = V1^T H with the full M = m_1 (<= 144) per CTA, so every H column panel is
+// read once (the 48-row tiling of k_vech_contract reads it three times). 18 warps,
+// warp w -> row tile w x 64 columns; K = buckets in chunks of 32: H chunks by
+// cp.async, V1 chunks (vech(a1 a1^T) of the chunk's buckets; thread -> fixed pair
+// column) generated while other warps run the previous chunk's DMMAs.
+constexpr int TNC2 = 64;
+constexpr int LDH2 = TNC2 + 4;
+__global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_contract2(GramSpec spec, VechSpec v,
+                                                                  const double* __restrict__ H,
+                                                                  const int* __restrict__ bi1,
+                                                                  const int* __restrict__ nbuckets,
+                                                                  double* __restrict__ S) {
+  extern __shared__ __align__(16) double smc[];
+  double* hs = smc;                    // [2][KC][LDH2]
+  double* vs = hs + 2 * KC * LDH2;     // [2][KC][LDZ]
+  const int R0 = v.R[0], m0 = v.m[0];
+  const int nb = *nbuckets;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const long long n0 = (long long)blockIdx.x * TNC2;
+  const int MT = (m0 + 7) / 8;
+  const int u = tid % (kBT * 8), k0r = tid / (kBT * 8);  // fixed pair column, rows k0r + 4j
+  int pa = 0, pb = 0;
+  const bool uok = u < m0;
+  if (uok) pair_of(u, R0, pa, pb);
+  const double* A0 = spec.factors[0];
+  const bool vec = (v.Hsz & 1) == 0;
+  auto load_h = [&](int kc, int buf) {
+    double* dst = hs + buf * KC * LDH2;
+    for (int e = tid; e < KC * (TNC2 / 2); e += blockDim.x) {
+      const int k = e / (TNC2 / 2), c = (e % (TNC2 / 2)) * 2;
+      const bool ok = (kc + k < nb) && (n0 + c < v.Hsz);
+      const double* src = ok ? H + (size_t)(kc + k) * v.Hsz + n0 + c : H;
+      if (vec) {
+        cp_async16(dst + k * LDH2 + c, src, ok);
+      } else {
+        dst[k * LDH2 + c] = ok ? src[0] : 0.0;
+        dst[k * LDH2 + c + 1] = (ok && n0 + c + 1 < v.Hsz) ? src[1] : 0.0;
+      }
+    }
+  };
+  auto gen_v = [&](int kc, int buf) {
+    double* dst = vs + buf * KC * LDZ;
+#pragma unroll 4
+    for (int j = 0; j < KC / 4; ++j) {
+      const int k = k0r + 4 * j;
+      double val = 0.0;
+      if (uok && kc + k < nb) {
+        const double* a = A0 + (size_t)__ldg(bi1 + kc + k) * R0;
+        val = __ldg(a + pa) * __ldg(a + pb);
+      }
+      dst[k * LDZ + u] = val;
+    }
+  };
+  double acc[8][2];
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+  const int nch = (nb + KC - 1) / KC;
+  if (nch > 0) load_h(0, 0);
+  cp_async_commit();
+  if (nch > 0) gen_v(0, 0);
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int kk = 0; kk < nch; ++kk) {
+    const int cur = kk & 1;
+    if (kk + 1 < nch) load_h((kk + 1) * KC, cur ^ 1);
+    cp_async_commit();
+    if (warp < MT) {
+      const double* hb = hs + cur * KC * LDH2;
+      const double* vb = vs + cur * KC * LDZ;
+#pragma unroll
+      for (int ks = 0; ks < KC / 4; ++ks) {
+        const double af = vb[(ks * 4 + t4) * LDZ + warp * 8 + g];
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt)
+          dmma_8x8x4(acc[nt][0], acc[nt][1], af, hb[(ks * 4 + t4) * LDH2 + nt * 8 + g]);
+      }
+    }
+    if (kk + 1 < nch) gen_v((kk + 1) * KC, cur ^ 1);
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  const int uu = warp * 8 + g;
+  if (warp < MT && uu < m0) {
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const long long c = n0 + nt * 8 + 2 * t4;
+      if (c < v.Hsz) S[(size_t)uu * v.Hsz + c] = acc[nt][0];
+      if (c + 1 < v.Hsz) S[(size_t)uu * v.Hsz + c + 1] = acc[nt][1];
+    }
+  }
+}
+
 // (D) full Gram from S plus the augmented diagonal.
 __global__ void k_vech_expand(GramSpec spec, VechSpec v, const double* __restrict__ S,
                               const int* __restrict__ aug_count, double aug_term,
@@ -1038,8 +1131,20 @@ void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
     k_bucket_h2<<<I1, 256, 0, st>>>(spec, l.dwx, l.dmode, l.bstart, l.blen, l.nbuckets, l.h);
     RTB_LAUNCH_CHECK();
   }
-  k_vech_contract<<<dim3((unsigned)((v.Hsz + TNC - 1) / TNC), (unsigned)ceil_div(v.m[0], TB)),
-                    kTh, 0, st>>>(spec, v, l.H, l.bi1, l.nbuckets, l.S);
+  if ((v.m[0] + 7) / 8 <= kBWarps) {
+    const size_t smc = (size_t)(2 * KC * LDH2 + 2 * KC * LDZ) * 8;
+    static bool attr_c = false;
+    if (!attr_c) {
+      RTB_CUDA(cudaFuncSetAttribute(k_vech_contract2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smc));
+      attr_c = true;
+    }
+    k_vech_contract2<<<(unsigned)((v.Hsz + TNC2 - 1) / TNC2), kBWarps * 32, smc, st>>>(
+        spec, v, l.H, l.bi1, l.nbuckets, l.S);
+  } else {
+    k_vech_contract<<<dim3((unsigned)((v.Hsz + TNC - 1) / TNC), (unsigned)ceil_div(v.m[0], TB)),
+                      kTh, 0, st>>>(spec, v, l.H, l.bi1, l.nbuckets, l.S);
+  }
   RTB_LAUNCH_CHECK();
   const double aug_term = gram_aug_term(spec);
   if (gram) {

@@ -383,6 +383,10 @@ uint64_t sample_count_formula(double beta_prime, uint64_t d, double epsilon, dou
   return (uint64_t)std::ceil(4.0 * dd / beta_prime * std::max(log_term, tail_term));
 }
 
+// Generating the P rows inside the loss pass (no P in HBM) measured slower than
+// materialising P (the per-row-block generation stalls the residual warps): off.
+constexpr bool kGenerateP = false;
+
 class Engine {
  public:
   Engine(const double* x, const std::vector<uint64_t>& shape, const std::vector<uint64_t>& ranks,
@@ -1260,18 +1264,36 @@ class Engine {
       RTB_LAUNCH_CHECK();
       return;
     }
-    std::vector<uint64_t> dims;
-    const double* P = build_P(dims);
     const long long O = (long long)(total_ / shape_[N_ - 1]);
     const int I = (int)shape_[N_ - 1];
     double* partial = partial_.as<double>();
     long long nparts;
-    if (R <= 32) {
+    if (kGenerateP && N_ == 3 && ttm_last_pgen_ok(I, R)) {
+      // P rows generated inside the pass from W = G x_1 A_1 and A_2 (no P in HBM)
+      double* W = tmp_a_.as<double>();
+      {
+        Scope sc(prof_, "ttm_expand");
+        const long long Je = (long long)(ranks_[1] * ranks_[2]);
+        if (!ttm_expand(core_.as<double>(), 1, (int)ranks_[0], Je, factor(0), (int)shape_[0], W,
+                        st_))
+          ttm_generic(core_.as<double>(), 1, (int)ranks_[0], Je, factor(0), (int)ranks_[0], 1,
+                      (int)shape_[0], W, st_);
+      }
+      Scope sc(prof_, "ttm_last_loss");
+      ttm_last(x_, O, I, factor(N_ - 1), R, T_.as<double>(), nullptr, partial, st_, W, factor(1),
+               (int)shape_[1], (int)ranks_[1]);
+      nparts = ttm_last_blocks(O, I, R);
+      t_valid_ = true;
+    } else if (R <= 32) {
+      std::vector<uint64_t> dims;
+      const double* P = build_P(dims);
       Scope sc(prof_, "ttm_last_loss");
       ttm_last(x_, O, I, factor(N_ - 1), R, T_.as<double>(), P, partial, st_);
       nparts = ttm_last_blocks(O, I, R);
       t_valid_ = true;
     } else {
+      std::vector<uint64_t> dims;
+      const double* P = build_P(dims);
       // generic: full reconstruction then residual
       DevBuf xh(total_ * 8, st_);
       ttm_generic(P, O, R, 1, factor(N_ - 1), R, 1, I, xh.as<double>(), st_);

@@ -171,13 +171,22 @@ constexpr int BM2 = 128;
 template <int RP>
 constexpr int lda2() { return RP + 4; }
 
+// PGEN (3-way): the P rows are not read from a materialised P = G x_1 A_1 x_2 A_2 but
+// formed per row block from W = G x_1 A_1 (I_1 x R_2 x R_3, L2-resident) and A_2:
+// P[(i1, i2), r3] = sum_r2 A_2[i2, r2] W[i1, r2, r3].
+struct PGen {
+  const double* W;
+  const double* A2;
+  int I2, R2;
+};
+
 template <int RP, bool FUSED>
 __global__ void __launch_bounds__(512, 1) k_ttm_last2(const double* __restrict__ X, long long O,
                                                       int I, const double* __restrict__ A, int R,
                                                       double* __restrict__ T,
                                                       const double* __restrict__ P,
                                                       double* __restrict__ partial,
-                                                      const int* __restrict__ need) {
+                                                      const int* __restrict__ need, PGen pg) {
   RTB_GUARD()
   constexpr int LD = kBK + kPadX;
   constexpr int LDA = lda2<RP>();
@@ -656,16 +665,22 @@ __global__ void __launch_bounds__(256) k_ttm_expand(const double* __restrict__ Y
     as[e] = (i0 + ii < I) ? A[(long long)(i0 + ii) * R + e % R] : 0.0;
   }
   __syncthreads();
-  const long long n = (long long)ich * J;
-  for (long long e = threadIdx.x; e < n; e += 256) {
-    const int ii = (int)(e / J);
-    const long long j = e % J;
+  const int Ji = (int)J;  // R * J fits shared memory, so J is small
+  const int n = ich * Ji;
+  for (int e = threadIdx.x; e < n; e += 256) {
+    const int ii = e / Ji;
+    const int j = e - ii * Ji;
     const int i = i0 + ii;
     if (i >= I) continue;
     const double* a = as + ii * R;
-    double sacc = 0.0;
-    for (int r = 0; r < R; ++r) sacc += a[r] * ys[(long long)r * J + j];
-    out[(o * I + i) * J + j] = sacc;
+    double s0 = 0.0, s1 = 0.0;
+    int r = 0;
+    for (; r + 1 < R; r += 2) {
+      s0 = fma(a[r], ys[r * Ji + j], s0);
+      s1 = fma(a[r + 1], ys[(r + 1) * Ji + j], s1);
+    }
+    if (r < R) s0 = fma(a[r], ys[r * Ji + j], s0);
+    out[(o * I + i) * J + j] = s0 + s1;
   }
 }
 
@@ -720,7 +735,7 @@ static bool last2_ok(int I, int R) {
 
 template <int RP, bool FUSED>
 static void launch_last2(const double* X, long long O, int I, const double* A, int R, double* T,
-                         const double* P, double* partial, cudaStream_t st) {
+                         const double* P, double* partial, cudaStream_t st, PGen pg) {
   const size_t ip = (size_t)ceil_div(I, kBK) * kBK;
   const size_t smem = (ip * lda2<RP>() + (size_t)kStages2 * BM2 * (kBK + kPadX)) * 8;
   auto k = k_ttm_last2<RP, FUSED>;
@@ -731,9 +746,11 @@ static void launch_last2(const double* X, long long O, int I, const double* A, i
   }
   const long long nrb = ceil_div<long long>(O, BM2);
   const int grid = (int)std::min<long long>(nrb, sm_count());
-  k<<<grid, 512, smem, st>>>(X, O, I, A, R, T, P, partial, g_need);
+  k<<<grid, 512, smem, st>>>(X, O, I, A, R, T, P, partial, g_need, pg);
   RTB_LAUNCH_CHECK();
 }
+
+bool ttm_last_pgen_ok(int I, int R) { return R <= 32 && last2_ok(I, R); }
 
 long long ttm_last_blocks(long long O, int I, int R) {
   if (last2_ok(I, R)) return std::min<long long>(ceil_div<long long>(O, BM2), sm_count());
@@ -741,16 +758,19 @@ long long ttm_last_blocks(long long O, int I, int R) {
 }
 
 void ttm_last(const double* X, long long O, int I, const double* A, int R, double* T,
-              const double* P, double* partial, cudaStream_t st) {
-  const bool fused = P != nullptr;
+              const double* P, double* partial, cudaStream_t st, const double* W,
+              const double* A2, int I2, int R2) {
+  const bool fused = P != nullptr || W != nullptr;
+  const PGen pg{W, A2, I2, R2};
+  if (W) throw Error(4, "ttm_last: in-pass P generation is disabled (slower than materialised P)");
   const bool v2 = (I % 2) == 0;
   const int rp = R <= 8 ? 8 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
   if (R > 32) throw Error(4, "ttm_last: rank > 32 not supported by the DMMA path");
   if (last2_ok(I, R)) {
 #define RTB_L2(RPV)                                                     \
   case RPV:                                                             \
-    if (fused) launch_last2<RPV, true>(X, O, I, A, R, T, P, partial, st); \
-    else launch_last2<RPV, false>(X, O, I, A, R, T, P, partial, st);      \
+    if (fused) launch_last2<RPV, true>(X, O, I, A, R, T, P, partial, st, pg); \
+    else launch_last2<RPV, false>(X, O, I, A, R, T, P, partial, st, pg);      \
     break;
     switch (rp) {
       RTB_L2(8)
@@ -889,8 +909,9 @@ bool ttm_smallj(const double* X, long long O, int I, int J, const double* A, int
 
 bool ttm_expand(const double* Y, long long O, int R, long long J, const double* A, int I,
                 double* out, cudaStream_t st) {
-  // enough blocks to fill the GPU: small O -> small i chunks
-  int ich = 16;
+  // big i chunks (A rows staged once per CTA, several outputs per thread), shrunk
+  // until there are enough blocks to fill the GPU
+  int ich = 128;
   while (ich > 1 && O * ceil_div(I, ich) < 4 * kNumSMs) ich >>= 1;
   const size_t smem = ((size_t)R * J + (size_t)ich * R) * sizeof(double);
   if (smem > 48 * 1024 || O > 65535) return false;

@@ -43,8 +43,12 @@ __global__ void k_rows_times_small(const double* M, const double* P, int I, int 
 void set_ttm_guard(const int* need);
 long long ttm_last_blocks(long long O, int I, int R);
 // T (O x R) = X (O x I) A (I x R); if P != null also partial[block] = sum (X - P A^T)^2
+// With W != nullptr (3-way), P is not read but generated per row: P[(i1,i2),:] =
+// A2[i2,:] W[i1] with W = G x_1 A_1 (I1 x R2 x R3) -- saves writing / reading P.
 void ttm_last(const double* X, long long O, int I, const double* A, int R, double* T,
-              const double* P, double* partial, cudaStream_t st);
+              const double* P, double* partial, cudaStream_t st, const double* W = nullptr,
+              const double* A2 = nullptr, int I2 = 0, int R2 = 0);
+bool ttm_last_pgen_ok(int I, int R);
 // out[o,r,j] = sum_i A[i,r] X[o,i,j]
 void ttm_mid(const double* X, long long O, int I, long long J, const double* A, int R, double* out,
              cudaStream_t st);

@@ -52,6 +52,34 @@ __global__ void dfma_loop(double* out, int iters) {
   if (s == 12345.0) out[0] = s;
 }
 
+// half the warps DMMA, half DFMA: are the FP64 tensor and FP64 FMA pipes independent?
+__global__ void mixed_loop(double* out, int iters) {
+  const int w = threadIdx.x >> 5;
+  double s = 0;
+  if (w & 1) {
+    double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-9;
+    double c[16];
+    for (int j = 0; j < 16; ++j) c[j] = j;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) c[j] = fma(c[j], b, a);
+    }
+    for (int j = 0; j < 16; ++j) s += c[j];
+  } else {
+    double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+    double c[8][2];
+    for (int j = 0; j < 8; ++j) { c[j][0] = 0; c[j][1] = 0; }
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(c[j][0]), "+d"(c[j][1]) : "d"(a), "d"(b));
+    }
+    for (int j = 0; j < 8; ++j) s += c[j][0] + c[j][1];
+  }
+  if (s == 12345.0) out[0] = s;
+}
+
 int main() {
   double* out; cudaMalloc(&out, 8);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -82,6 +110,18 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     flops = 2.0 * 16 * iters * (double)grid.x * block.x;
     printf("DFMA warps/CTA=%d: %.2f TFLOP/s\n", warps, flops / ms / 1e9);
+  }
+  for (int warps : {8, 16}) {
+    int iters = 20000;
+    dim3 grid(sms * 2), block(32 * warps);
+    mixed_loop<<<grid, block>>>(out, 100);
+    cudaEventRecord(e0);
+    mixed_loop<<<grid, block>>>(out, iters);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    // per iteration: DMMA warps 8 x 512 flops per warp, DFMA warps 16 x 2 x 32 flops per warp
+    double flops = ((double)8 * 512 + 16 * 2 * 32) * (warps / 2) * iters * (double)grid.x;
+    printf("MIXED (half DMMA, half DFMA) warps/CTA=%d: %.2f TFLOP/s combined\n", warps, flops / ms / 1e9);
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

@@ -46,10 +46,12 @@ typedef struct rtucker_b200_als_ext {
    * I_n x R_n row-major, concatenated) replace the uniform init. */
   const double* init_core;
   const double* init_factors;
-  /* Multi-GPU sample sharding: this process draws sketch rows
-   * [shard_rank * s / shard_count, (shard_rank+1) * s / shard_count) and the
-   * partial normal equations are summed by `allreduce` (in place, doubles,
-   * on the library's stream) before the solve. shard_count 0/1 = no sharding. */
+  /* Multi-GPU (shard_count > 1): X is split along mode 1; this process passes only
+   * its rows [r*I1/P, (r+1)*I1/P) (r = shard_rank, P = shard_count, I1 =
+   * shard_rows_total) as `x`. X passes, mode-1 factor rows and the sketch's data
+   * draws stay local; every partial sum (projections, A_1 rows, compact Gram + rhs,
+   * residual) goes through `allreduce` (in place, doubles, enqueued on the
+   * library's stream, e.g. ncclAllReduce sum). shard_count 0/1 = no sharding. */
   uint32_t shard_rank;
   uint32_t shard_count;
   void (*allreduce)(double* device_buf, uint64_t count, void* stream, void* user);
@@ -68,7 +70,8 @@ typedef struct rtucker_b200_als_ext {
    * absolute accuracy, falls back to the direct residual near an exact fit);
    * 0 (default) = the reference's direct residual pass. */
   int fast_loss;
-  int reserved[5];
+  int shard_rows_total; /* global I_1 of a sharded run */
+  int reserved[4];
 } rtucker_b200_als_ext;
 
 rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* ranks,

@@ -416,6 +416,24 @@ void rtucker_als_options_init(rtucker_als_options* opts) {
   opts->record_history = 0;
 }
 
+// Multi-GPU: x holds this shard's rows of mode 1; the engine works on the global shape.
+std::vector<uint64_t> engine_shape(const rtucker_tensor* x, const rtb::AlsOptions& o,
+                                   const rtucker_b200_als_ext* ext) {
+  std::vector<uint64_t> sh = x->shape;
+  if (o.shard_count > 1) {
+    if (!o.allreduce) throw rtb::Error(1, "sharded run needs an allreduce callback");
+    const uint64_t total = ext->shard_rows_total;
+    if (total == 0) throw rtb::Error(1, "sharded run needs shard_rows_total (global I_1)");
+    if (o.shard_rank >= o.shard_count) throw rtb::Error(1, "shard_rank >= shard_count");
+    const uint64_t lo = o.shard_rank * total / o.shard_count;
+    const uint64_t hi = (o.shard_rank + 1) * total / o.shard_count;
+    if (sh[0] != hi - lo)
+      throw rtb::Error(1, "tensor rows != this shard's even split of shard_rows_total");
+    sh[0] = total;
+  }
+  return sh;
+}
+
 rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* ranks,
                                        uint32_t order, const rtucker_als_options* opts,
                                        const rtucker_b200_als_ext* ext,
@@ -437,7 +455,8 @@ rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* 
       o.fast_loss = ext->fast_loss != 0;
     }
     auto r = std::make_unique<rtucker_als_result>();
-    rtb::als_run(x->device(), x->shape, std::vector<uint64_t>(ranks, ranks + order), o, r->out);
+    rtb::als_run(x->device(), engine_shape(x, o, ext), std::vector<uint64_t>(ranks, ranks + order),
+                 o, r->out);
     *out = r.release();
   });
 }
@@ -472,7 +491,7 @@ rtucker_status rtucker_b200_session_create(const rtucker_tensor* x, const uint64
       o.fast_loss = ext->fast_loss != 0;
     }
     auto s = std::make_unique<rtucker_b200_session>();
-    s->s.reset(rtb::session_create(x->device(), x->shape,
+    s->s.reset(rtb::session_create(x->device(), engine_shape(x, o, ext),
                                    std::vector<uint64_t>(ranks, ranks + order), o));
     *out = s.release();
   });

@@ -397,6 +397,20 @@ class Engine {
     prof_.st = st_;
     total_ = prod(shape_);
     d_ = prod(ranks_);
+    // Multi-GPU: this process holds rows [lo_, lo_ + nloc_) of mode 1 (the even split
+    // r * I_1 / P); X passes, the mode-1 factor rows and the Gram's data draws are
+    // local, partial sums meet in opt_.allreduce.
+    if (opt_.shard_count > 1) {
+      const uint64_t I1 = shape_[0], P = opt_.shard_count, r = opt_.shard_rank;
+      lo_ = (long long)(r * I1 / P);
+      nloc_ = (long long)((r + 1) * I1 / P) - lo_;
+    } else {
+      lo_ = 0;
+      nloc_ = (long long)shape_[0];
+    }
+    lshape_ = shape_;
+    lshape_[0] = (uint64_t)nloc_;
+    ltotal_ = prod(lshape_);
     rmax_ = 0;
     for (auto r : ranks_) rmax_ = std::max<int>(rmax_, (int)r);
     eig_stride_ = std::max(rmax_ * rmax_, 1);
@@ -576,7 +590,14 @@ class Engine {
   cudaStream_t st_;
 
  private:
-  const double* x_;
+  const double* x_;  // this process's slab of X (rows lo_ .. lo_ + nloc_ of mode 1)
+  long long lo_ = 0, nloc_ = 0;
+  std::vector<uint64_t> lshape_;
+  uint64_t ltotal_ = 0;
+  bool sharded() const { return opt_.shard_count > 1 && opt_.allreduce; }
+  void allreduce(double* buf, uint64_t n) {
+    if (sharded()) opt_.allreduce(buf, n, st_, opt_.allreduce_user);
+  }
   std::vector<uint64_t> shape_, ranks_;
   AlsOptions opt_;
   int N_;
@@ -770,7 +791,7 @@ class Engine {
 
   // Y for factor n: dims with I_n at n and R_m elsewhere. Returns pointer into tmp.
   const double* factor_projection(int n, std::vector<uint64_t>& dims) {
-    dims = shape_;
+    dims = lshape_;
     const double* cur = x_;
     double* bufs[2] = {tmp_a_.as<double>(), tmp_b_.as<double>()};
     int which = 0;
@@ -784,18 +805,23 @@ class Engine {
     } else {
       for (int m = 0; m < N_ - 1; ++m) modes.push_back(m);
     }
+    bool partial = false;
     for (int m : modes) {
       const int R = (int)ranks_[m];
-      mode_product(cur, dims, m, factor(m), 1, R, R, bufs[which], true);
+      // mode 1 is sharded: contract with this shard's rows of A_1 -> partial sum
+      const double* W = factor(m) + (m == 0 ? (size_t)lo_ * R : 0);
+      mode_product(cur, dims, m, W, 1, R, R, bufs[which], true);
+      partial |= (m == 0);
       cur = bufs[which];
       which ^= 1;
     }
+    if (partial && sharded()) allreduce(const_cast<double*>(cur), prod(dims));
     return cur;
   }
 
   void compute_T() {
-    // T = X x_N A_N^T (O x R_N), no residual
-    const long long O = (long long)(total_ / shape_[N_ - 1]);
+    // T = X x_N A_N^T (O x R_N, this shard's rows), no residual
+    const long long O = (long long)(ltotal_ / shape_[N_ - 1]);
     const int I = (int)shape_[N_ - 1], R = (int)ranks_[N_ - 1];
     if (R <= 32) {
       Scope sc(prof_, "ttm_last");
@@ -809,7 +835,8 @@ class Engine {
 
   // ---- exact factor update (ref tucker.cpp:70-89) ----
   void update_factor(int n) {
-    const int In = (int)shape_[n], Rn = (int)ranks_[n];
+    // mode 1 under sharding: this shard computes its own rows of A_1
+    const int In = (n == 0) ? (int)nloc_ : (int)shape_[n], Rn = (int)ranks_[n];
     std::vector<uint64_t> dims;
     const double* Y = factor_projection(n, dims);
     // M = Y_(n) G_(n)^T  (I_n x R_n)
@@ -860,8 +887,19 @@ class Engine {
       RTB_LAUNCH_CHECK();
       // A_n = M pinv
       const long long tot = (long long)In * Rn;
-      k_rows_times_small<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(M, pv, In, Rn, factor(n));
-      RTB_LAUNCH_CHECK();
+      if (n == 0 && sharded()) {
+        // own rows into a zeroed full-size A_1, then sum over shards = the whole A_1
+        double* a1 = factor(0);
+        RTB_CUDA(cudaMemsetAsync(a1, 0, shape_[0] * Rn * 8, st_));
+        k_rows_times_small<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(
+            M, pv, In, Rn, a1 + (size_t)lo_ * Rn);
+        RTB_LAUNCH_CHECK();
+        allreduce(a1, shape_[0] * Rn);
+      } else {
+        k_rows_times_small<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(M, pv, In, Rn,
+                                                                          factor(n));
+        RTB_LAUNCH_CHECK();
+      }
     }
     factor_gram(n);
     if (n == N_ - 1) t_valid_ = false;
@@ -964,6 +1002,8 @@ class Engine {
     gs.dprime = (int)(d_ / ranks_[0]);
     gs.lambda = opt_.lambda;
     gs.s = s;
+    gs.i1_lo = sharded() ? (int)lo_ : 0;
+    gs.i1_hi = sharded() ? (int)(lo_ + nloc_) : 0;
     return gs;
   }
 
@@ -975,17 +1015,23 @@ class Engine {
     rhs_.ensure(d_ * 8, st_);
     int rk[8];
     for (int n = 0; n < N_; ++n) rk[n] = (int)ranks_[n];
-    const bool try_pcg = opt_.core_solver == 0 && opt_.lambda > 0.0 && opt_.shard_count <= 1 &&
-                         rmax_ <= 32 && pcg_supported((int)d_, N_, rk);
+    const bool try_pcg = opt_.core_solver == 0 && opt_.lambda > 0.0 && rmax_ <= 32 &&
+                         pcg_supported((int)d_, N_, rk);
+    // X slab pointer offset so that global flat indices of this shard's draws land in it
+    const double* xg = x_ - (sharded() ? lo_ * (long long)(total_ / shape_[0]) : 0);
     auto normal_eq = [&](bool full) {
       Scope sc(prof_, "gram");
       if (full) G_.ensure(d_ * d_ * 8, st_);
-      sketch_normal_eq(gs, x_, (const unsigned long long*)sk_idx_.p, sk_w_.as<double>(),
-                       gram_work_.p, gram_work_.bytes, full ? G_.as<double>() : nullptr,
+      // the full Gram is expanded after the shard sum of the compact one
+      sketch_normal_eq(gs, xg, (const unsigned long long*)sk_idx_.p, sk_w_.as<double>(),
+                       gram_work_.p, gram_work_.bytes, (full && !sharded()) ? G_.as<double>() : nullptr,
                        rhs_.as<double>(), (unsigned long long*)data_draws_.p, st_);
-      if (full && opt_.allreduce && opt_.shard_count > 1) {
-        opt_.allreduce(G_.as<double>(), d_ * d_, st_, opt_.allreduce_user);
-        opt_.allreduce(rhs_.as<double>(), d_, st_, opt_.allreduce_user);
+      if (sharded()) {
+        size_t ns = 0;
+        double* S = gram_compact(gs, gram_work_.p, &ns);
+        allreduce(S, ns);
+        allreduce(rhs_.as<double>(), d_);
+        if (full) gram_expand_full(gs, gram_work_.p, G_.as<double>(), st_);
       }
     };
     normal_eq(!try_pcg);
@@ -1056,13 +1102,7 @@ class Engine {
       if (d_ > 64)
         throw Error(3, "sketched Gram is not positive definite (d > 64 pinv fallback "
                        "not available)");
-      sketch_normal_eq(gs, x_, (const unsigned long long*)sk_idx_.p, sk_w_.as<double>(),
-                       gram_work_.p, gram_work_.bytes, G_.as<double>(), rhs_.as<double>(),
-                       (unsigned long long*)data_draws_.p, st_);
-      if (opt_.allreduce && opt_.shard_count > 1) {
-        opt_.allreduce(G_.as<double>(), d_ * d_, st_, opt_.allreduce_user);
-        opt_.allreduce(rhs_.as<double>(), d_, st_, opt_.allreduce_user);
-      }
+      normal_eq(true);  // Cholesky overwrote G and rhs: rebuild them
       eigen_one(G_.as<double>(), (int)d_);
       double* pv = tmp_a_.as<double>();
       k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one((int)d_),
@@ -1120,8 +1160,9 @@ class Engine {
           U_[n].as<double>());
       RTB_LAUNCH_CHECK();
     }
-    // W = X x_n U_n^T, last mode first (contiguous), then the others
-    std::vector<uint64_t> dims = shape_;
+    // W = X x_n U_n^T, last mode first (contiguous), then the others; mode 1 with this
+    // shard's rows of U_1 (partial sum over shards)
+    std::vector<uint64_t> dims = lshape_;
     double* bufs[2] = {tmp_a_.as<double>(), tmp_b_.as<double>()};
     int which = 0;
     const double* cur = x_;
@@ -1129,10 +1170,12 @@ class Engine {
     order.push_back(N_ - 1);
     for (int m = 0; m < N_ - 1; ++m) order.push_back(m);
     for (int m : order) {
-      mode_product(cur, dims, m, U_[m].as<double>(), 1, rk[m], rk[m], bufs[which], true);
+      const double* U = U_[m].as<double>() + (m == 0 ? (size_t)lo_ * rk[0] : 0);
+      mode_product(cur, dims, m, U, 1, rk[m], rk[m], bufs[which], true);
       cur = bufs[which];
       which ^= 1;
     }
+    allreduce(const_cast<double*>(cur), prod(dims));
     // scale by sigma_t / (sigma_t^2 + lambda)
     ScaleSpec sp{};
     sp.order = N_;
@@ -1170,13 +1213,15 @@ class Engine {
     double* bufs[2] = {tmp_a_.as<double>(), tmp_b_.as<double>()};
     int which = 0;
     for (int m = 0; m < N_ - 1; ++m) {
-      const int I = (int)shape_[m], R = (int)ranks_[m];
+      // mode 1: this shard's rows only (P rows of the local slab)
+      const int I = (m == 0) ? (int)nloc_ : (int)shape_[m], R = (int)ranks_[m];
+      const double* A = factor(m) + (m == 0 ? (size_t)lo_ * R : 0);
       double* out = (m == N_ - 2) ? P_.as<double>() : bufs[which];
       // out[.., i, ..] = sum_r A[i][r] cur[.., r, ..]  (W = A: wr = R, wi = 1)
       Scope sc(prof_, "ttm_expand");
       const long long Oe = (long long)prod(dims, 0, m), Je = (long long)prod(dims, m + 1);
-      if (!ttm_expand(cur, Oe, R, Je, factor(m), I, out, st_))
-        ttm_generic(cur, Oe, R, Je, factor(m), R, 1, I, out, st_);
+      if (!ttm_expand(cur, Oe, R, Je, A, I, out, st_))
+        ttm_generic(cur, Oe, R, Je, A, R, 1, I, out, st_);
       dims[m] = I;
       cur = out;
       which ^= 1;
@@ -1193,7 +1238,7 @@ class Engine {
   // near-exact-fit case where the cancellation would cost accuracy.
   void loss_pass(double* loss_dev, double* rmse_dev) {
     const int R = (int)ranks_[N_ - 1];
-    if (N_ >= 2 && R <= 32 && opt_.fast_loss) {
+    if (N_ >= 2 && R <= 32 && opt_.fast_loss && !sharded()) {
       if (!xx_valid_) {
         Scope sc(prof_, "loss_norm_x");
         const int nb = kNumSMs * 4;
@@ -1264,7 +1309,7 @@ class Engine {
       RTB_LAUNCH_CHECK();
       return;
     }
-    const long long O = (long long)(total_ / shape_[N_ - 1]);
+    const long long O = (long long)(ltotal_ / shape_[N_ - 1]);  // this shard's rows
     const int I = (int)shape_[N_ - 1];
     double* partial = partial_.as<double>();
     long long nparts;
@@ -1295,9 +1340,9 @@ class Engine {
       std::vector<uint64_t> dims;
       const double* P = build_P(dims);
       // generic: full reconstruction then residual
-      DevBuf xh(total_ * 8, st_);
+      DevBuf xh(ltotal_ * 8, st_);
       ttm_generic(P, O, R, 1, factor(N_ - 1), R, 1, I, xh.as<double>(), st_);
-      k_resid_partials<<<kNumSMs * 8, 256, 0, st_>>>(x_, xh.as<double>(), (long long)total_,
+      k_resid_partials<<<kNumSMs * 8, 256, 0, st_>>>(x_, xh.as<double>(), (long long)ltotal_,
                                                       partial);
       RTB_LAUNCH_CHECK();
       nparts = kNumSMs * 8;
@@ -1305,6 +1350,7 @@ class Engine {
     }
     double* sc = scal_.as<double>();
     sum_partials(partial, nparts, sc, st_);
+    allreduce(sc, 1);  // shard residuals
     norms_into(sc + 1);
     k_finish_loss<<<1, 1, 0, st_>>>(sc, sc + 1, opt_.lambda, (double)total_, loss_dev, rmse_dev);
     RTB_LAUNCH_CHECK();

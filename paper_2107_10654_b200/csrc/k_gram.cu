@@ -197,6 +197,12 @@ size_t gram_work_bytes(const GramSpec& spec) {
   return carve(spec, [](size_t, size_t) {});
 }
 
+double* gram_compact(const GramSpec& spec, void* work, size_t* count) {
+  const VechSpec v = make_vech(spec);
+  if (count) *count = (size_t)v.m[0] * v.Hsz;
+  return layout(spec, work).S;
+}
+
 const int* gram_aug_counts(const GramSpec& spec, void* work) {
   return layout(spec, work).aug_count;
 }
@@ -230,6 +236,10 @@ __global__ void k_sketch_keys(GramSpec spec, const unsigned long long* idx, unsi
   if (v < spec.total_rows) {
     const unsigned long long inner = spec.total_rows / (unsigned long long)I1;
     const unsigned i1 = (unsigned)(v / inner);
+    if (spec.i1_hi > 0 && ((int)i1 < spec.i1_lo || (int)i1 >= spec.i1_hi)) {
+      keys[t] = (unsigned)I1;  // another shard's draw: sorts with the augmented ones
+      return;
+    }
     keys[t] = i1;
     atomicAdd(&counts[i1], 1);
     atomicAdd(data_draws, 1ULL);

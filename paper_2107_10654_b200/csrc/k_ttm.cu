@@ -800,10 +800,12 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
 #undef RTB_L
 }
 
-// per-device scratch for split-K partial sums (grown on demand, stream-ordered)
+// per-thread, per-device scratch for split-K partial sums (grown on demand,
+// stream-ordered; thread-local so concurrent host threads on their own streams never
+// share it)
 static double* splits_scratch(size_t bytes, cudaStream_t st) {
-  static double* buf[16] = {};
-  static size_t cap[16] = {};
+  thread_local double* buf[16] = {};
+  thread_local size_t cap[16] = {};
   int dev = 0;
   RTB_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 16) throw Error(4, "ttm_mid: device index");

@@ -98,8 +98,14 @@ struct GramSpec {
   int dprime;     // prod_{n>=1} R_n (z width)
   double lambda;
   unsigned long long s;
+  // multi-GPU: only data draws with i1 in [i1_lo, i1_hi) contribute (this shard's X
+  // slab; x points at the slab minus i1_lo * prod_{n>=2} I_n). Augmented draws are
+  // counted by every shard. i1_hi == 0 means no sharding.
+  int i1_lo, i1_hi;
 };
 size_t gram_work_bytes(const GramSpec& spec);
+// the compact (vech) Gram S [m_1][Hsz] inside the workspace (sum it across shards)
+double* gram_compact(const GramSpec& spec, void* work, size_t* count);
 // Sketched normal equations from (idx, w): rhs, the compact (vech) Gram in the
 // workspace and, if gram != nullptr, the full d x d Gram.
 void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long long* idx,

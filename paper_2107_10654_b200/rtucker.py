@@ -63,7 +63,8 @@ class AlsExt(C.Structure):
         ("profile_kernels", C.c_int),
         ("core_solver", C.c_int),
         ("fast_loss", C.c_int),
-        ("reserved", C.c_int * 5),
+        ("shard_rows_total", C.c_int),
+        ("reserved", C.c_int * 4),
     ]
 
 
@@ -387,12 +388,44 @@ class Result:
             pass
 
 
+def shard_rows(rank: int, count: int, rows_total: int):
+    """Rows [lo, hi) of mode 1 held by shard `rank` of `count` (the library's even split)."""
+    return rank * rows_total // count, (rank + 1) * rows_total // count
+
+
+@dataclass
+class Shard:
+    """Multi-GPU run: X split along mode 1. `allreduce(ptr, count, stream)` must sum
+    `count` doubles at device address `ptr` across all shards, in place, ordered after
+    the work already enqueued on `stream` (e.g. an NCCL all-reduce)."""
+    rank: int
+    count: int
+    rows_total: int
+    allreduce: object
+
+
 def _ext(init_model: Model | None = None, profile: bool = False, core_solver: int = 0,
-         fast_loss: bool = False):
+         fast_loss: bool = False, shard: Shard | None = None):
     ext = AlsExt()
     ext.core_solver = int(core_solver)
     ext.fast_loss = int(fast_loss)
     keep = []
+    if shard is not None:
+        fn = shard.allreduce
+
+        def _cb(ptr, n, stream, user):
+            try:
+                fn(C.cast(ptr, C.c_void_p).value, int(n), int(stream or 0))
+            except Exception as e:  # a callback cannot raise into C
+                import traceback
+                traceback.print_exc()
+                raise SystemExit(f"allreduce callback failed: {e}")
+        cb = _ALLREDUCE(_cb)
+        keep.append(cb)
+        ext.shard_rank = shard.rank
+        ext.shard_count = shard.count
+        ext.shard_rows_total = shard.rows_total
+        ext.allreduce = cb
     if init_model is not None:
         core = _f64(init_model.core).ravel()
         fc = _f64(np.concatenate([_f64(f).ravel() for f in init_model.factors]))
@@ -404,30 +437,38 @@ def _ext(init_model: Model | None = None, profile: bool = False, core_solver: in
 
 
 def als_run(x: Tensor, ranks, opts: AlsOptions | None = None, init_model: Model | None = None,
-            profile: bool = False, core_solver: int = 0, fast_loss: bool = False) -> Result:
-    """rtucker_als_run (ref capi.cpp:176-201); extensions via rtucker_b200_als_run_ex."""
+            profile: bool = False, core_solver: int = 0, fast_loss: bool = False,
+            shard: Shard | None = None) -> Result:
+    """rtucker_als_run (ref capi.cpp:176-201); extensions via rtucker_b200_als_run_ex.
+    With `shard`, `x` holds only that shard's rows of mode 1 (see shard_rows)."""
     opts = opts or options()
     ranks = _u64(ranks)
     r = _vp()
-    if init_model is None and not profile and not core_solver and not fast_loss:
+    shape = tuple(x.shape)
+    if shard is not None:
+        shape = (shard.rows_total,) + shape[1:]
+    if init_model is None and not profile and not core_solver and not fast_loss and shard is None:
         _check(lib.rtucker_als_run(x.h, _p(ranks), len(ranks), C.byref(opts), C.byref(r)))
     else:
-        ext, keep = _ext(init_model, profile, core_solver, fast_loss)
+        ext, keep = _ext(init_model, profile, core_solver, fast_loss, shard)
         _check(lib.rtucker_b200_als_run_ex(x.h, _p(ranks), len(ranks), C.byref(opts),
                                            C.byref(ext), C.byref(r)))
         del keep
-    return Result(r, x.shape)
+    return Result(r, shape)
 
 
 class Session:
     """Step-wise run (rtucker_b200_session_*): init at construction, sweeps on demand."""
 
     def __init__(self, x: Tensor, ranks, opts: AlsOptions | None = None,
-                 init_model: Model | None = None, profile: bool = False, core_solver: int = 0):
-        self.shape = x.shape
+                 init_model: Model | None = None, profile: bool = False, core_solver: int = 0,
+                 shard: Shard | None = None):
+        self.shape = tuple(x.shape)
+        if shard is not None:
+            self.shape = (shard.rows_total,) + self.shape[1:]
         opts = opts or options()
         ranks = _u64(ranks)
-        ext, self._keep = _ext(init_model, profile, core_solver)
+        ext, self._keep = _ext(init_model, profile, core_solver, False, shard)
         self.h = _vp()
         _check(lib.rtucker_b200_session_create(x.h, _p(ranks), len(ranks), C.byref(opts),
                                                C.byref(ext), C.byref(self.h)))
@@ -568,3 +609,12 @@ def loss(x: Tensor, model: Model):
     finally:
         lib.rtucker_model_free(h)
     return lo.value, rm.value
+
+
+class DeviceArray:
+    """A raw device pointer viewed through __cuda_array_interface__ (float64, 1-D), so
+    frameworks (torch.as_tensor) can wrap library buffers without a copy."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8",
+                                         "data": (ptr, False), "version": 3, "stream": None}

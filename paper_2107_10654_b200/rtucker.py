@@ -618,3 +618,26 @@ class DeviceArray:
     def __init__(self, ptr: int, count: int):
         self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8",
                                          "data": (ptr, False), "version": 3, "stream": None}
+
+
+def torch_allreduce(dist, group=None):
+    """Shard.allreduce over torch.distributed for device buffers (NCCL): the library's
+    buffer is wrapped without a copy and summed in place. Run the library on torch's
+    current stream (set_stream) so the collective is ordered after its kernels."""
+    import torch
+
+    def fn(ptr, count, stream):
+        t = torch.as_tensor(DeviceArray(ptr, count), device="cuda")
+        dist.all_reduce(t, group=group)
+    return fn
+
+
+def host_allreduce(dist, group=None):
+    """The same contract for host buffers (gloo): sums `count` doubles at host address
+    `ptr` across the process group, in place."""
+    import torch
+
+    def fn(ptr, count, stream):
+        arr = np.ctypeslib.as_array((C.c_double * count).from_address(ptr))
+        dist.all_reduce(torch.from_numpy(arr), group=group)
+    return fn

@@ -1,0 +1,104 @@
+"""World-size-2 gloo tests of the multi-GPU decomposition (runs on CPU).
+
+The sharded engine splits X along mode 1 with
+rtucker.shard_rows and meets every partial sum in a Shard.allreduce callback.
+Here two gloo processes check the identities it relies on, with the reference
+restatement as the arithmetic and the library's own host_allreduce callable as
+the collective: (1) the row split partitions [0, I_1); (2) the mode-1
+contraction of the X slabs sums to the full X x_1 A_1^T; (3) the normal
+equations of the shard-local data draws plus the (replicated) augmented draws
+sum to the full sketched normal equations; (4) the stitched A_1 rows (zero
+elsewhere) sum to the full factor."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _planted(shape, ranks, seed):
+    rng = np.random.default_rng(seed)
+    core = rng.standard_normal(ranks)
+    fs = [rng.standard_normal((i, r)) for i, r in zip(shape, ranks)]
+    x = core
+    for n, f in enumerate(fs):
+        x = np.moveaxis(np.tensordot(f, x, axes=(1, n)), 0, n)
+    return x + 0.01 * rng.standard_normal(x.shape), core, fs
+
+
+def _worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle.oracle import Oracle
+        from paper_2107_10654_b200 import rtucker as rt
+        ar = rt.host_allreduce(dist)
+        shape, ranks = (13, 9, 7), (3, 2, 2)
+        x, core, fs = _planted(shape, ranks, 5)
+        I1 = shape[0]
+        lo, hi = rt.shard_rows(rank, world, I1)
+        # (1) partition
+        cov = np.zeros(I1)
+        cov[lo:hi] = 1.0
+        ar(cov.ctypes.data, cov.size, 0)
+        assert np.array_equal(cov, np.ones(I1)), cov
+        # (2) mode-1 projection from the slab with this shard's rows of A_1
+        part = np.ascontiguousarray(np.tensordot(fs[0][lo:hi].T, x[lo:hi], axes=(1, 0)))
+        ar(part.ctypes.data, part.size, 0)
+        full = np.tensordot(fs[0].T, x, axes=(1, 0))
+        assert np.allclose(part, full, rtol=1e-13, atol=1e-12)
+        # (3) sketched normal equations: data draws split by i1, augmented draws once
+        o = Oracle()
+        lam, s, seed = 0.05, 900, 17
+        _, idx, w, _ = o.update_core_fast(shape, ranks, core, fs, lam, x, s, seed)
+        total = int(np.prod(shape))
+        inner = total // I1
+        data = idx < total
+        own = data & (idx // inner >= lo) & (idx // inner < hi)
+        g_own, r_own = o.kron_normal_eq(shape, ranks, fs, x, lam, idx[own], w[own])
+        g_own = np.ascontiguousarray(g_own)
+        r_own = np.ascontiguousarray(r_own)
+        ar(g_own.ctypes.data, g_own.size, 0)
+        ar(r_own.ctypes.data, r_own.size, 0)
+        g_aug, _ = o.kron_normal_eq(shape, ranks, fs, x, lam, idx[~data], w[~data])
+        g_all, r_all = o.kron_normal_eq(shape, ranks, fs, x, lam, idx, w)
+        dg = np.sqrt(np.outer(np.diag(g_all), np.diag(g_all)))
+        assert np.max(np.abs(g_own + g_aug - g_all) / dg) < 1e-12
+        assert np.linalg.norm(r_own - r_all) / np.linalg.norm(r_all) < 1e-12
+        # (4) A_1 stitched from shard rows
+        a1 = np.zeros_like(fs[0])
+        a1[lo:hi] = fs[0][lo:hi]
+        ar(a1.ctypes.data, a1.size, 0)
+        assert np.array_equal(a1, fs[0])
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except BaseException as e:  # noqa: BLE001
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharding_decomposition_gloo(oracle, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=240) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, msg in res:
+        assert msg == "ok", f"rank {rank}:\n{msg}"

@@ -68,10 +68,24 @@ __device__ __forceinline__ double u64_to_unit(uint64_t u) {
 // ---- FP64 tensor-core MMA: D(8x8) += A(8x4) * B(4x8), one DMMA.8x8x4 ----
 // Fragment ownership (lane l, g = l>>2, t = l&3):
 //   A: a = A[g][t]   B: b = B[t][g]   C/D: c0 = C[g][2t], c1 = C[g][2t+1]
+// (not volatile: the asm has outputs, so the compiler may schedule loads around it)
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// m16n8k16 f64 (CuTe SM90_16x8x16_F64F64F64F64_TN layouts), g = lane / 4, t = lane % 4:
+//   a[v] = A[g + 8 (v & 1)][t + 4 (v >> 1)]   (v < 8, A is 16 x 16 row-major M x K)
+//   b[v] = B[t + 4 v][g]                       (v < 4, B is 16 x 8, K x N)
+//   c[v] = C[g + 8 (v >> 1)][2 t + (v & 1)]    (v < 4, C is 16 x 8)
+__device__ __forceinline__ void dmma_16x8x16(double (&c)[4], const double (&a)[8],
+                                             const double (&b)[4]) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+      "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+        "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
 // ---- cp.async (LDGSTS) with zero fill: copies `src_bytes` (0 or the full

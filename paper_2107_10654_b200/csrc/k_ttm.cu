@@ -715,6 +715,135 @@ static void launch_last(const double* X, long long O, int I, const double* A, in
 
 void set_ttm_guard(const int* need) { g_need = need; }
 
+// Same pass with m16n8k16 DMMA (R <= 16): per 32-column chunk a T warp issues 4 MMAs
+// (2 k-steps x 2 n-tiles over the rank) and a residual warp 4 (one per 8 columns, K =
+// rank), each fed straight from shared memory, instead of 32 m8n8k4 each.
+template <bool FUSED>
+__global__ void __launch_bounds__(512, 1) k_ttm_last3(const double* __restrict__ X, long long O,
+                                                      int I, const double* __restrict__ A, int R,
+                                                      double* __restrict__ T,
+                                                      const double* __restrict__ P,
+                                                      double* __restrict__ partial,
+                                                      const int* __restrict__ need) {
+  RTB_GUARD()
+  constexpr int RP = 16;
+  constexpr int LD = kBK + kPadX;
+  constexpr int LDA = RP + 4;
+  constexpr int ROWS = 16;  // rows per warp (m16)
+  extern __shared__ __align__(16) double sm2[];
+  const int Ip = ceil_div(I, kBK) * kBK;
+  double* as = sm2;                        // [Ip][LDA]
+  double* xs = as + (size_t)Ip * LDA;      // [kStages2][BM2][LD]
+  __shared__ double red[32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  // FUSED: warps 0-7 T, 8-15 residual, 16 rows each; else 8 warps (128 rows) of T
+  const bool rwarp = FUSED && warp >= 8;
+  const int wrow = warp & 7;
+  const bool idle = !FUSED && warp >= 8;
+  const long long nrb = ceil_div<long long>(O, BM2);
+  const int nchunks = ceil_div(I, kBK);
+  for (int e = tid; e < Ip * LDA; e += 512) {
+    const int i = e / LDA, r = e - i * LDA;
+    as[e] = (i < I && r < R) ? A[(size_t)i * R + r] : 0.0;
+  }
+  const long long my_blocks = blockIdx.x < nrb ? (nrb - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long nitems = my_blocks * nchunks;
+  auto load_item = [&](long long q, int stage) {
+    const long long rb = blockIdx.x + (q / nchunks) * gridDim.x;
+    const int c = (int)(q % nchunks);
+    const long long o0 = rb * BM2;
+    const int i0 = c * kBK;
+    double* dst = xs + (size_t)stage * BM2 * LD;
+    for (int e = tid; e < BM2 * (kBK / 2); e += 512) {
+      const int r = e / (kBK / 2), col = (e % (kBK / 2)) * 2;
+      const long long o = o0 + r;
+      const bool ok = (o < O) && (i0 + col < I);
+      cp_async16(dst + r * LD + col, ok ? X + o * I + i0 + col : X, ok);
+    }
+  };
+#pragma unroll
+  for (int sidx = 0; sidx < kStages2 - 1; ++sidx) {
+    if (sidx < nitems) load_item(sidx, sidx);
+    cp_async_commit();
+  }
+  double acc[2][4];   // T: two n-tiles (rank 0-7, 8-15) of the 16 x 16 block
+  double pa[8];       // residual: P rows as the A fragment (constant per row block)
+  double resid0 = 0.0, resid1 = 0.0;
+  for (long long q = 0; q < nitems; ++q) {
+    const int c = (int)(q % nchunks);
+    const long long rb = blockIdx.x + (q / nchunks) * gridDim.x;
+    const long long o0 = rb * BM2 + wrow * ROWS;
+    if (c == 0) {
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[n][v] = 0.0;
+      if (rwarp) {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const long long o = o0 + g + 8 * (v & 1);
+          const int k = t + 4 * (v >> 1);
+          pa[v] = (o < O && k < R) ? P[o * R + k] : 0.0;
+        }
+      }
+    }
+    cp_async_wait<kStages2 - 2>();
+    __syncthreads();
+    if (q + kStages2 - 1 < nitems) load_item(q + kStages2 - 1, (int)((q + kStages2 - 1) % kStages2));
+    cp_async_commit();
+    const double* xt = xs + (size_t)(q % kStages2) * BM2 * LD + wrow * ROWS * LD;
+    const int i0 = c * kBK;
+    if (idle) {
+    } else if (!rwarp) {
+#pragma unroll
+      for (int kb = 0; kb < kBK; kb += 16) {
+        double a[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) a[v] = xt[(g + 8 * (v & 1)) * LD + kb + t + 4 * (v >> 1)];
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          double b[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) b[v] = as[(size_t)(i0 + kb + t + 4 * v) * LDA + n * 8 + g];
+          dmma_16x8x16(acc[n], a, b);
+        }
+      }
+      if (c == nchunks - 1) {
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const long long o = o0 + g + 8 * (v >> 1);
+            const int r = n * 8 + 2 * t + (v & 1);
+            if (o < O && r < R) T[o * R + r] = acc[n][v];
+          }
+      }
+    } else {
+#pragma unroll
+      for (int nb = 0; nb < kBK; nb += 8) {
+        double b[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) b[v] = as[(size_t)(i0 + nb + g) * LDA + t + 4 * v];
+        double cx[4] = {0.0, 0.0, 0.0, 0.0};
+        dmma_16x8x16(cx, pa, b);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double2 xv = *reinterpret_cast<const double2*>(xt + (g + 8 * h) * LD + nb + 2 * t);
+          const double d0 = xv.x - cx[2 * h], d1 = xv.y - cx[2 * h + 1];
+          resid0 = fma(d0, d0, resid0);  // zero-filled tails contribute exactly 0
+          resid1 = fma(d1, d1, resid1);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (FUSED) {
+    const double s = block_sum<512>(resid0 + resid1, red);
+    if (tid == 0) partial[blockIdx.x] = s;
+  }
+}
+
 static int sm_count() {
   static int n = [] {
     int dev = 0, v = 0;
@@ -766,6 +895,21 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
   const bool v2 = (I % 2) == 0;
   const int rp = R <= 8 ? 8 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
   if (R > 32) throw Error(4, "ttm_last: rank > 32 not supported by the DMMA path");
+  if (last2_ok(I, R) && R <= 16) {
+    const size_t ip = (size_t)ceil_div(I, kBK) * kBK;
+    const size_t smem = (ip * lda2<16>() + (size_t)kStages2 * BM2 * (kBK + kPadX)) * 8;
+    auto k = fused ? k_ttm_last3<true> : k_ttm_last3<false>;
+    static bool attr3[2] = {false, false};
+    if (!attr3[fused]) {
+      RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      attr3[fused] = true;
+    }
+    const long long nrb = ceil_div<long long>(O, BM2);
+    const int grid = (int)std::min<long long>(nrb, sm_count());
+    k<<<grid, 512, smem, st>>>(X, O, I, A, R, T, P, partial, g_need);
+    RTB_LAUNCH_CHECK();
+    return;
+  }
   if (last2_ok(I, R)) {
 #define RTB_L2(RPV)                                                     \
   case RPV:                                                             \

@@ -17,6 +17,7 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include "kernels.h"
 
 namespace rtb {
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(128) k_ttm_mid(const double* __restrict__ X, l
 // tile never straddles two o).
 constexpr int BJ2 = 128;
 constexpr int kStagesMid = 4;
-template <int RP>
+template <int RP, bool COMPUTE = true>
 __global__ void __launch_bounds__(256, 1) k_ttm_mid2(const double* __restrict__ X, long long O,
                                                      int I, long long J,
                                                      const double* __restrict__ A, int R,
@@ -493,6 +494,10 @@ __global__ void __launch_bounds__(256, 1) k_ttm_mid2(const double* __restrict__ 
     cp_async_commit();
     const double* xt = xs + (size_t)(q % kStagesMid) * kBK * LDX + warp * 16;
     const int i0 = c * kBK;
+    if (!COMPUTE) {
+      acc[0][0][0][0] += xt[lane];  // touch the stage, no contraction (bandwidth probe)
+      continue;
+    }
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
       double af[RP / 8];
@@ -525,6 +530,113 @@ __global__ void __launch_bounds__(256, 1) k_ttm_mid2(const double* __restrict__ 
     }
   }
   cp_async_wait<0>();
+}
+
+// Producer / consumer version of the same pass: warp 8 only issues the cp.async
+// copies of the ring (and arrives on full[s] when they land), warps 0-7 only compute
+// and release a stage with one arrive on empty[s]. No block-wide barrier per chunk,
+// so the consumer warps drift and the DMMA pipe does not drain between chunks.
+template <int RP>
+__global__ void __launch_bounds__(288, 1) k_ttm_mid3(const double* __restrict__ X, long long O,
+                                                     int I, long long J,
+                                                     const double* __restrict__ A, int R,
+                                                     double* __restrict__ out) {
+  constexpr int LDX = BJ2 + 8;
+  constexpr int S = kStagesMid;
+  extern __shared__ __align__(16) double sm3[];
+  __shared__ __align__(8) unsigned long long full[S], empty[S];
+  const int Ip = ceil_div(I, kBK) * kBK;
+  const int LDT = Ip + 4;
+  double* at = sm3;                       // [RP][LDT]
+  double* xs = at + (size_t)RP * LDT;     // [S][kBK][LDX]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const long long ntiles = O * J / BJ2;
+  const int nchunks = ceil_div(I, kBK);
+  for (int e = tid; e < RP * LDT; e += blockDim.x) {
+    const int r = e / LDT, i = e - r * LDT;
+    at[e] = (i < I && r < R) ? A[(size_t)i * R + r] : 0.0;
+  }
+  // stages zeroed once: rows of a short last chunk are never copied
+  for (int e = tid; e < S * kBK * LDX; e += blockDim.x) xs[e] = 0.0;
+  if (tid == 0) {
+    for (int s2 = 0; s2 < S; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], 8);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const long long my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long nitems = my_tiles * nchunks;
+  if (warp == 8) {
+    // producer: one 1 KB bulk copy (TMA, cp.async.bulk) per row of the chunk, all
+    // completing on full[s] with the expected byte count
+    for (long long q = 0; q < nitems; ++q) {
+      const int st = (int)(q % S);
+      if (q >= S) mbar_wait(&empty[st], (unsigned)(((q / S) - 1) & 1));
+      const long long tile = blockIdx.x + (q / nchunks) * gridDim.x;
+      const int c = (int)(q % nchunks);
+      const long long c0 = tile * BJ2;
+      const long long o = c0 / J, j0 = c0 - o * J;
+      const int i0 = c * kBK;
+      const int rows = min(kBK, I - i0);
+      double* dst = xs + (size_t)st * kBK * LDX;
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&full[st], (unsigned)(rows * BJ2 * 8));
+      }
+      __syncwarp();
+      if (lane < rows)
+        bulk_g2s(dst + lane * LDX, X + (o * I + i0 + lane) * J + j0, BJ2 * 8, &full[st]);
+    }
+    return;
+  }
+  double acc[RP / 8][2][2];
+  for (long long q = 0; q < nitems; ++q) {
+    const int st = (int)(q % S);
+    const int c = (int)(q % nchunks);
+    if (c == 0) {
+#pragma unroll
+      for (int mt = 0; mt < RP / 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    }
+    mbar_wait(&full[st], (unsigned)((q / S) & 1));
+    const double* xt = xs + (size_t)st * kBK * LDX + warp * 16;
+    const int i0 = c * kBK;
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      double af[RP / 8];
+#pragma unroll
+      for (int mt = 0; mt < RP / 8; ++mt) af[mt] = at[(size_t)(mt * 8 + g) * LDT + i0 + ks * 4 + t];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const double bf = xt[(ks * 4 + t) * LDX + nt * 8 + g];
+#pragma unroll
+        for (int mt = 0; mt < RP / 8; ++mt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (c == nchunks - 1) {
+      const long long tile = blockIdx.x + (q / nchunks) * gridDim.x;
+      const long long c0 = tile * BJ2;
+      const long long o = c0 / J, j0 = c0 - o * J + warp * 16;
+#pragma unroll
+      for (int mt = 0; mt < RP / 8; ++mt) {
+        const int r = mt * 8 + g;
+        if (r >= R) continue;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          double2 v2;
+          v2.x = acc[mt][nt][0];
+          v2.y = acc[mt][nt][1];
+          *reinterpret_cast<double2*>(out + (o * R + r) * J + j0 + nt * 8 + 2 * t) = v2;
+        }
+      }
+    }
+  }
 }
 
 static size_t mid2_smem(int I, int rp) {
@@ -992,12 +1104,19 @@ template <int RP>
 static void launch_mid2(const double* X, long long O, int I, long long J, const double* A, int R,
                         double* out, cudaStream_t st) {
   const size_t smem = mid2_smem(I, RP);
-  auto k = k_ttm_mid2<RP>;
-  static bool attr = false;
-  if (!attr) {
-    RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    attr = true;
+  static const bool probe = std::getenv("RTB_TTM_STREAM_ONLY") != nullptr;
+  static const bool pc = std::getenv("RTB_TTM_NO_PRODUCER") == nullptr;
+  if (pc && !probe) {
+    auto k3 = k_ttm_mid3<RP>;
+    RTB_CUDA(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    const long long ntiles = O * J / BJ2;
+    const int grid = (int)std::min<long long>(ntiles, sm_count());
+    k3<<<grid, 288, smem, st>>>(X, O, I, J, A, R, out);
+    RTB_LAUNCH_CHECK();
+    return;
   }
+  auto k = probe ? k_ttm_mid2<RP, false> : k_ttm_mid2<RP, true>;
+  RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   const long long ntiles = O * J / BJ2;
   const int grid = (int)std::min<long long>(ntiles, sm_count());
   k<<<grid, 256, smem, st>>>(X, O, I, J, A, R, out);

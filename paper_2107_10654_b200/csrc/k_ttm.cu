@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(256, 1) k_ttm_mid2(const double* __restrict__ 
 // copies of the ring (and arrives on full[s] when they land), warps 0-7 only compute
 // and release a stage with one arrive on empty[s]. No block-wide barrier per chunk,
 // so the consumer warps drift and the DMMA pipe does not drain between chunks.
-template <int RP>
+template <int RP, bool COMPUTE = true>
 __global__ void __launch_bounds__(288, 1) k_ttm_mid3(const double* __restrict__ X, long long O,
                                                      int I, long long J,
                                                      const double* __restrict__ A, int R,
@@ -605,6 +605,12 @@ __global__ void __launch_bounds__(288, 1) k_ttm_mid3(const double* __restrict__ 
     mbar_wait(&full[st], (unsigned)((q / S) & 1));
     const double* xt = xs + (size_t)st * kBK * LDX + warp * 16;
     const int i0 = c * kBK;
+    if (!COMPUTE) {
+      acc[0][0][0] += xt[lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      continue;
+    }
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
       double af[RP / 8];
@@ -1106,8 +1112,8 @@ static void launch_mid2(const double* X, long long O, int I, long long J, const 
   const size_t smem = mid2_smem(I, RP);
   static const bool probe = std::getenv("RTB_TTM_STREAM_ONLY") != nullptr;
   static const bool pc = std::getenv("RTB_TTM_NO_PRODUCER") == nullptr;
-  if (pc && !probe) {
-    auto k3 = k_ttm_mid3<RP>;
+  if (pc) {
+    auto k3 = probe ? k_ttm_mid3<RP, false> : k_ttm_mid3<RP, true>;
     RTB_CUDA(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     const long long ntiles = O * J / BJ2;
     const int grid = (int)std::min<long long>(ntiles, sm_count());

@@ -71,7 +71,12 @@ typedef struct rtucker_b200_als_ext {
    * 0 (default) = the reference's direct residual pass. */
   int fast_loss;
   int shard_rows_total; /* global I_1 of a sharded run */
-  int reserved[4];
+  /* Perf mode (not the reference's semantics): > 0 = sketched factor updates with this
+   * many draws per mode from the product of the other modes' leverage distributions
+   * plus the sqrt(lambda) augmentation (BASELINE "samples per factor update"; DESIGN.md
+   * section 3). 0 (default) = the reference's exact factor updates. Not with sharding. */
+  uint32_t factor_samples;
+  int reserved[3];
 } rtucker_b200_als_ext;
 
 rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* ranks,

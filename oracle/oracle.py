@@ -227,6 +227,17 @@ class Oracle:
                                              _p(_f64(x).ravel()), C.c_uint32(mode)))
         return model_split(shape, ranks, fc)[mode - 1].copy()
 
+    def update_factor_sketched(self, shape, ranks, core, factors, lam, x, mode, s, seed):
+        """Perf-mode sketched factor update (not in the reference; parity unpinned).
+        Returns (new factor, indices, weights)."""
+        shape, ranks, core, fc = self._model_args(shape, ranks, core, factors)
+        idx, w = np.zeros(s, np.uint64), np.zeros(s)
+        self._chk(self.lib.orc_update_factor_sketched(
+            C.c_uint32(len(shape)), _p(shape), _p(ranks), _p(core), _p(fc), C.c_double(lam),
+            _p(_f64(x).ravel()), C.c_uint32(mode), C.c_uint64(s), C.c_uint64(seed), _p(idx),
+            _p(w)))
+        return model_split(shape, ranks, fc)[mode - 1].copy(), idx, w
+
     def update_core_exact(self, shape, ranks, core, factors, lam, x):
         shape, ranks, core, fc = self._model_args(shape, ranks, core, factors)
         out = np.zeros(int(np.prod(ranks)))
@@ -260,7 +271,8 @@ class Oracle:
         return core, model_split(shape, ranks, fc)
 
     def als(self, x, ranks, lam=1e-3, sketched_core=0, epsilon=0.1, delta=0.1, seed=0,
-            max_iterations=50, tolerance=1e-6, sample_count_override=0, record_history=0):
+            max_iterations=50, tolerance=1e-6, sample_count_override=0, record_history=0,
+            factor_samples=0):
         x = _f64(x)
         shape = _u64(x.shape)
         ranks = _u64(ranks)
@@ -279,10 +291,10 @@ class Oracle:
         fl, fr = C.c_double(), C.c_double()
         seeds = np.zeros(max_iterations, np.uint64)
         del o
-        self._chk(self.lib.orc_als(C.c_uint32(order), _p(shape), _p(ranks), _p(x.ravel()),
-                                   C.byref(opts), _p(core), _p(fc), _p(hi), _p(hs), _p(hl),
-                                   _p(hr), C.byref(hlen), C.byref(iters), C.byref(fl),
-                                   C.byref(fr), _p(seeds)))
+        self._chk(self.lib.orc_als_fs(C.c_uint32(order), _p(shape), _p(ranks), _p(x.ravel()),
+                                      C.byref(opts), C.c_uint64(factor_samples), _p(core),
+                                      _p(fc), _p(hi), _p(hs), _p(hl), _p(hr), C.byref(hlen),
+                                      C.byref(iters), C.byref(fl), C.byref(fr), _p(seeds)))
         n = hlen.value
         steps = ["Core" if v == order else f"F{v + 1}" for v in hs[:n]]
         return {

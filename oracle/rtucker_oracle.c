@@ -962,6 +962,115 @@ done:
   return status;
 }
 
+/* Sketched factor update (perf mode). NOT in the reference:
+ * composed from its public pieces as SURVEY 8(c) prescribes, so parity is unpinned
+ * by reference tests. The mode-n subproblem min ||K a_i - x_i||^2 + lambda ||a_i||^2
+ * (K = (kron_{m!=n} A_m) G_(n)^T, rows indexed like the columns of X_(n): other modes
+ * ascending, last fastest; tucker.cpp:31-43,70-89) is solved once per fiber row i with
+ * solve_sketched_ridge semantics (sketch_ridge.cpp:52-151) and ONE shared sketch:
+ *   draws: ProductLeverageSampler over the other factors' classical scores with the
+ *          sqrt(lambda) augmentation over R_n (kronecker.cpp:159-181), s draws from
+ *          SplitMix64(seed) -> orc_kron_draw(order - 1, others, d = R_n);
+ *   row t: data -> G_(n) z, z = kron_row of the other factors' rows; aug -> sqrt(lambda) e_j;
+ *   G = sum w^2 row row^T (upper triangle, mirrored), rhs_i = sum w^2 X_(n)[i, j_t] row;
+ *   a_i = pinv(G) rhs_i (sketch_ridge.cpp:130-139).
+ * A factor with no nonzero rows among the others cannot be sampled (kronecker.cpp:128-131). */
+int orc_update_factor_sketched(uint32_t order, const uint64_t* shape, const uint64_t* ranks,
+                               const double* core, double* factors_cat, double lambda,
+                               const double* x, uint32_t mode, uint64_t s, uint64_t seed,
+                               uint64_t* indices_out, double* weights_out) {
+  int status = ORC_OK;
+  if (mode < 1 || mode > order) return fail(ORC_INVALID, "update_factor: mode out of range");
+  if (order < 2) return fail(ORC_INVALID, "sketched factor update needs order >= 2");
+  if (s == 0) return fail(ORC_INVALID, "solve_sketched_ridge: sample count must be positive");
+  if (lambda < 0.0) return fail(ORC_INVALID, "solve_sketched_ridge: lambda must be non-negative");
+  const double* f[16];
+  factor_ptrs(order, shape, ranks, factors_cat, f);
+  const size_t axis = mode - 1;
+  const size_t rn = ranks[axis], in = shape[axis];
+  uint64_t orows[16], oranks[16];
+  const double* ofac[16];
+  uint32_t no = 0;
+  uint64_t total_o = 1, width = 1, sum_rows = 0;
+  for (uint32_t n = 0; n < order; ++n) {
+    if (n == axis) continue;
+    orows[no] = shape[n];
+    oranks[no] = ranks[n];
+    ofac[no] = f[n];
+    total_o *= shape[n];
+    width *= ranks[n];
+    sum_rows += shape[n];
+    ++no;
+  }
+  double* g_unf = malloc(rn * width * sizeof(double));
+  unfold(core, order, ranks, mode, g_unf); /* R_n x width, others ascending */
+  double* xu = malloc(in * total_o * sizeof(double));
+  unfold(x, order, shape, mode, xu); /* I_n x prod_{m!=n} I_m */
+  double* scores = xcalloc(sum_rows, sizeof(double));
+  double* cdfs = xcalloc(sum_rows, sizeof(double));
+  uint64_t* idx = xcalloc(s, sizeof(uint64_t));
+  double* wts = xcalloc(s, sizeof(double));
+  double* z = xcalloc(width, sizeof(double));
+  double* row = xcalloc(rn, sizeof(double));
+  double* g = xcalloc(rn * rn, sizeof(double));
+  double* rhs = xcalloc(in * rn, sizeof(double));
+  double* sol = xcalloc(rn, sizeof(double));
+  double sums[16];
+  size_t off = 0;
+  for (uint32_t m = 0; m < no; ++m) {
+    CHECK(orc_factor_scores(ofac[m], orows[m], oranks[m], scores + off, cdfs + off, &sums[m],
+                            NULL));
+    off += orows[m];
+  }
+  CHECK(orc_kron_draw(no, orows, rn, scores, cdfs, sums, seed, s, idx, wts, NULL));
+  {
+    kron_rows kr = {no, orows, oranks, ofac};
+    const double root_lambda = sqrt(lambda);
+    for (uint64_t t = 0; t < s; ++t) {
+      const double w2 = wts[t] * wts[t];
+      if (idx[t] < total_o) {
+        kron_row(&kr, idx[t], z);
+        for (size_t r = 0; r < rn; ++r) row[r] = dotv(g_unf + r * width, z, width);
+      } else {
+        for (size_t r = 0; r < rn; ++r) row[r] = 0.0;
+        row[idx[t] - total_o] = root_lambda;
+      }
+      for (size_t p = 0; p < rn; ++p) {
+        const double v = w2 * row[p];
+        if (v == 0.0) continue;
+        for (size_t q = p; q < rn; ++q) g[p * rn + q] += v * row[q];
+      }
+      if (idx[t] < total_o)
+        for (size_t i = 0; i < in; ++i) {
+          const double wb = w2 * xu[i * total_o + idx[t]];
+          if (wb == 0.0) continue;
+          for (size_t p = 0; p < rn; ++p) rhs[i * rn + p] += wb * row[p];
+        }
+    }
+    for (size_t p = 0; p < rn; ++p)
+      for (size_t q = 0; q < p; ++q) g[p * rn + q] = g[q * rn + p];
+  }
+  for (size_t i = 0; i < in; ++i) {
+    CHECK(orc_pinv_solve(g, rhs + i * rn, rn, sol, NULL));
+    memcpy((double*)f[axis] + i * rn, sol, rn * sizeof(double));
+  }
+  if (indices_out) memcpy(indices_out, idx, s * sizeof(uint64_t));
+  if (weights_out) memcpy(weights_out, wts, s * sizeof(double));
+done:
+  free(g_unf);
+  free(xu);
+  free(scores);
+  free(cdfs);
+  free(idx);
+  free(wts);
+  free(z);
+  free(row);
+  free(g);
+  free(rhs);
+  free(sol);
+  return status;
+}
+
 /* update_core_exact (tucker.cpp:91-129) */
 int orc_update_core_exact(uint32_t order, const uint64_t* shape, const uint64_t* ranks,
                           const double* core, const double* factors_cat, double lambda,
@@ -1131,6 +1240,20 @@ int orc_als(uint32_t order, const uint64_t* shape, const uint64_t* ranks,
             double* history_loss, double* history_rmse, uint64_t* history_len_out,
             uint32_t* iterations_out, double* final_loss, double* final_rmse,
             uint64_t* core_seeds_out) {
+  return orc_als_fs(order, shape, ranks, x, o, 0, core, factors_cat, history_iter, history_step,
+                    history_loss, history_rmse, history_len_out, iterations_out, final_loss,
+                    final_rmse, core_seeds_out);
+}
+
+/* orc_als with sketched factor updates when factor_samples > 0 (perf mode). Factor
+ * sketch seeds: a second split of the seed generator (the first seeds the core
+ * sketches, tucker.cpp:206), one next_u64 per (sweep, mode) in update order. */
+int orc_als_fs(uint32_t order, const uint64_t* shape, const uint64_t* ranks,
+               const double* x, const orc_als_options* o, uint64_t factor_samples,
+               double* core, double* factors_cat, uint32_t* history_iter, int* history_step,
+               double* history_loss, double* history_rmse, uint64_t* history_len_out,
+               uint32_t* iterations_out, double* final_loss, double* final_rmse,
+               uint64_t* core_seeds_out) {
   int status = ORC_OK;
   double* new_core = NULL;
   if (o->max_iterations == 0) return fail(ORC_INVALID, "als: max_iterations must be >= 1");
@@ -1140,6 +1263,7 @@ int orc_als(uint32_t order, const uint64_t* shape, const uint64_t* ranks,
   CHECK(orc_random_model(order, shape, ranks, o->seed, core, factors_cat));
   orc_rng seed_rng0 = {o->seed};
   orc_rng sketch_seed_rng = {orc_split_seed(&seed_rng0)};
+  orc_rng factor_seed_rng = {orc_split_seed(&seed_rng0)};
   const double lambda = o->lambda;
   uint64_t hl = 0;
   double previous_loss, unused;
@@ -1149,7 +1273,13 @@ int orc_als(uint32_t order, const uint64_t* shape, const uint64_t* ranks,
   uint32_t iter;
   for (iter = 1; iter <= o->max_iterations; ++iter) {
     for (uint32_t n = 0; n < order; ++n) {
-      CHECK(orc_update_factor(order, shape, ranks, core, factors_cat, lambda, x, n + 1));
+      if (factor_samples > 0 && order >= 2) {
+        const uint64_t fs = orc_next_u64(&factor_seed_rng);
+        CHECK(orc_update_factor_sketched(order, shape, ranks, core, factors_cat, lambda, x,
+                                         n + 1, factor_samples, fs, NULL, NULL));
+      } else {
+        CHECK(orc_update_factor(order, shape, ranks, core, factors_cat, lambda, x, n + 1));
+      }
       if (o->record_history) {
         history_iter[hl] = iter;
         history_step[hl] = (int)n;

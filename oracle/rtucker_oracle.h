@@ -152,6 +152,19 @@ int orc_als(uint32_t order, const uint64_t* shape, const uint64_t* ranks,
             uint32_t* iterations_out, double* final_loss, double* final_rmse,
             uint64_t* core_seeds_out);
 
+/* Perf mode (not in the reference; parity unpinned): sketched factor update and
+ * ALS with it. See rtucker_oracle.c. */
+int orc_update_factor_sketched(uint32_t order, const uint64_t* shape, const uint64_t* ranks,
+                               const double* core, double* factors_cat, double lambda,
+                               const double* x, uint32_t mode, uint64_t s, uint64_t seed,
+                               uint64_t* indices_out, double* weights_out);
+int orc_als_fs(uint32_t order, const uint64_t* shape, const uint64_t* ranks,
+               const double* x, const orc_als_options* opts, uint64_t factor_samples,
+               double* core, double* factors_cat, uint32_t* history_iter, int* history_step,
+               double* history_loss, double* history_rmse, uint64_t* history_len_out,
+               uint32_t* iterations_out, double* final_loss, double* final_rmse,
+               uint64_t* core_seeds_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -453,6 +453,7 @@ rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* 
       o.profile = ext->profile_kernels != 0;
       o.core_solver = ext->core_solver;
       o.fast_loss = ext->fast_loss != 0;
+      o.factor_samples = ext->factor_samples;
     }
     auto r = std::make_unique<rtucker_als_result>();
     rtb::als_run(x->device(), engine_shape(x, o, ext), std::vector<uint64_t>(ranks, ranks + order),
@@ -489,6 +490,7 @@ rtucker_status rtucker_b200_session_create(const rtucker_tensor* x, const uint64
       o.profile = ext->profile_kernels != 0;
       o.core_solver = ext->core_solver;
       o.fast_loss = ext->fast_loss != 0;
+      o.factor_samples = ext->factor_samples;
     }
     auto s = std::make_unique<rtucker_b200_session>();
     s->s.reset(rtb::session_create(x->device(), engine_shape(x, o, ext),

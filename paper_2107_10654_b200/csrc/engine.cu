@@ -436,6 +436,11 @@ class Engine {
     // SplitMix64(seed).split(): next_u64 ^ 0x5851f42d4c957f2d (ref rng.hpp:56, tucker.cpp:206)
     sketch_rng_ = sm_at(opt_.seed, 0) ^ 0x5851f42d4c957f2dULL;
     sketch_k_ = 0;
+    // perf mode: factor sketch seeds from a second split of the same generator
+    // (orc_als_fs), one next_u64 per (sweep, mode)
+    factor_rng_ = sm_at(opt_.seed, 1) ^ 0x5851f42d4c957f2dULL;
+    factor_k_ = 0;
+    scores_valid_ = false;
     t_valid_ = false;
   }
 
@@ -453,7 +458,10 @@ class Engine {
       RTB_CUDA(cudaEventCreate(&a));
       RTB_CUDA(cudaEventCreate(&b));
       RTB_CUDA(cudaEventRecord(a, st_));
-      update_factor(n);
+      if (opt_.factor_samples > 0 && N_ >= 2)
+        update_factor_sketched(n, sm_at(factor_rng_, factor_k_++));
+      else
+        update_factor(n);
       RTB_CUDA(cudaEventRecord(b, st_));
       step_events_.push_back({n, a, b});
       if (opt_.record_history) {
@@ -615,6 +623,9 @@ class Engine {
   DevBuf sk_idx_, sk_w_, draw_work_, gram_work_, G_, rhs_, chol_work_, chol_status_,
       data_draws_, zero_flag_, U_[8], pgram_, pcg_work_, pcg_status_, blocks_, pev_, pvec_, pst_;
   uint64_t sketch_rng_ = 0, sketch_k_ = 0;
+  uint64_t factor_rng_ = 0, factor_k_ = 0;
+  bool scores_valid_ = false;
+  DevBuf fsums_, fsk_idx_, fsk_w_, fsk_work_;
   bool t_valid_ = false;
   uint64_t last_s_ = 0;
   int last_rank_deficient_ = 0, last_solver_path_ = 0, last_pcg_iters_ = 0;
@@ -930,7 +941,122 @@ class Engine {
     uint64_t s = opt_.sample_override;
     if (s == 0) s = sample_count_formula(0.5, d_, opt_.epsilon, opt_.delta);
     last_s_ = s;
-    // shard of the draw range for multi-GPU sample sharding
+    compute_scores();
+    DrawSpec ds{};
+    ds.order = N_;
+    long long off = 0;
+    for (int n = 0; n < N_; ++n) {
+      ds.rows[n] = (long long)shape_[n];
+      ds.cdf_off[n] = off;
+      off += (long long)shape_[n];
+    }
+    ds.total_rows = total_;
+    ds.d = d_;
+    ds.seed = seed;
+    ds.s = s;
+    sk_idx_.ensure(s * 8, st_);
+    sk_w_.ensure(s * 8, st_);
+    draw_work_.ensure(draw_work_bytes(ds), st_);
+    RTB_CUDA(cudaMemsetAsync(flag_.p, 0, 4, st_));
+    {
+      Scope sc(prof_, "draw");
+      draw_sketch(ds, scores_.as<double>(), cdf_.as<double>(), sums_.as<double>(),
+                  DrawWork{draw_work_.p, draw_work_.bytes}, (unsigned long long*)sk_idx_.p,
+                  sk_w_.as<double>(), flag_.as<int>(), st_);
+    }
+    solve_sketch(s);
+  }
+
+  // ---- sketched factor update (perf mode; k_fsketch.cu, orc_update_factor_sketched) ----
+  void update_factor_sketched(int n, uint64_t seed) {
+    if (sharded()) throw Error(1, "sketched factor updates are not supported with sharding");
+    const int Rn = (int)ranks_[n], In = (int)shape_[n];
+    if (Rn > 32) {  // the register-tiled gather kernel covers R_n <= 32
+      update_factor(n);
+      return;
+    }
+    const uint64_t s = opt_.factor_samples;
+    compute_scores();
+    DrawSpec ds{};
+    ds.order = N_ - 1;
+    uint64_t total_o = 1;
+    long long off = 0;
+    int k = 0;
+    for (int m = 0; m < N_; ++m) {
+      if (m != n) {
+        ds.rows[k] = (long long)shape_[m];
+        ds.cdf_off[k] = off;
+        total_o *= shape_[m];
+        ++k;
+      }
+      off += (long long)shape_[m];
+    }
+    ds.total_rows = total_o;
+    ds.d = (uint64_t)Rn;
+    ds.seed = seed;
+    ds.s = s;
+    fsums_.ensure(8 * 8, st_);
+    // score sums of the other modes, in order
+    if (n > 0)
+      RTB_CUDA(cudaMemcpyAsync(fsums_.p, sums_.p, n * 8, cudaMemcpyDeviceToDevice, st_));
+    if (n < N_ - 1)
+      RTB_CUDA(cudaMemcpyAsync(fsums_.as<double>() + n, sums_.as<double>() + n + 1,
+                               (N_ - 1 - n) * 8, cudaMemcpyDeviceToDevice, st_));
+    fsk_idx_.ensure(s * 8, st_);
+    fsk_w_.ensure(s * 8, st_);
+    draw_work_.ensure(draw_work_bytes(ds), st_);
+    RTB_CUDA(cudaMemsetAsync(flag_.p, 0, 4, st_));
+    {
+      Scope sc(prof_, "draw");
+      draw_sketch(ds, scores_.as<double>(), cdf_.as<double>(), fsums_.as<double>(),
+                  DrawWork{draw_work_.p, draw_work_.bytes}, (unsigned long long*)fsk_idx_.p,
+                  fsk_w_.as<double>(), flag_.as<int>(), st_);
+    }
+    FactorSketchSpec fs{};
+    fs.order = N_;
+    fs.mode = n;
+    for (int m = 0; m < N_; ++m) {
+      fs.rows[m] = (int)shape_[m];
+      fs.ranks[m] = (int)ranks_[m];
+      fs.factors[m] = factor(m);
+    }
+    fs.core = core_.as<double>();
+    fs.x = x_;
+    fs.lambda = opt_.lambda;
+    fs.s = s;
+    fsk_work_.ensure(factor_sketch_work_bytes(fs), st_);
+    double* kk = pinv_.as<double>();
+    double* M = tmp_a_.as<double>();
+    {
+      Scope sc(prof_, "factor_sketch");
+      factor_sketch_normal_eq(fs, (const unsigned long long*)fsk_idx_.p, fsk_w_.as<double>(),
+                              fsk_work_.p, kk, M, st_);
+    }
+    {
+      // A_n = M pinv(Gram) (ref sketch_ridge.cpp:130-139 per fiber row), as in update_factor
+      Scope sc(prof_, "small_linalg");
+      double* pv = pinv2_.as<double>();
+      int* okf = spd_ok_.as<int>();
+      const int stride = std::max(eig_stride_, Rn * Rn);
+      spd_small(kk, ns_one(Rn), stride, (double)Rn * DBL_EPSILON, linv_.as<double>(), pv, okf, 1,
+                st_, Rn);
+      sym_eigen(kk, ns_one(Rn), Rn, stride, evals_.as<double>(), evecs_.as<double>(),
+                eig_status_.as<int>(), 1, st_, okf);
+      k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one(Rn), stride,
+                                     pv, nullptr, okf);
+      RTB_LAUNCH_CHECK();
+      const long long tot = (long long)In * Rn;
+      k_rows_times_small<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(M, pv, In, Rn,
+                                                                        factor(n));
+      RTB_LAUNCH_CHECK();
+    }
+    factor_gram(n);
+    scores_valid_ = false;
+    if (n == N_ - 1) t_valid_ = false;
+  }
+
+  // per-mode classical leverage scores, CDFs and sums of the current factors
+  void compute_scores() {
     {
       Scope sc(prof_, "scores");
       // classical scores l_i = a_i^T (A^T A)^+ a_i: Cholesky of each factor Gram
@@ -964,29 +1090,6 @@ class Engine {
       k_any_zero_rank<<<1, 32, 0, st_>>>(ranks_dev_.as<int>(), N_, zero_flag_.as<int>());
       RTB_LAUNCH_CHECK();
     }
-    DrawSpec ds{};
-    ds.order = N_;
-    long long off = 0;
-    for (int n = 0; n < N_; ++n) {
-      ds.rows[n] = (long long)shape_[n];
-      ds.cdf_off[n] = off;
-      off += (long long)shape_[n];
-    }
-    ds.total_rows = total_;
-    ds.d = d_;
-    ds.seed = seed;
-    ds.s = s;
-    sk_idx_.ensure(s * 8, st_);
-    sk_w_.ensure(s * 8, st_);
-    draw_work_.ensure(draw_work_bytes(ds), st_);
-    RTB_CUDA(cudaMemsetAsync(flag_.p, 0, 4, st_));
-    {
-      Scope sc(prof_, "draw");
-      draw_sketch(ds, scores_.as<double>(), cdf_.as<double>(), sums_.as<double>(),
-                  DrawWork{draw_work_.p, draw_work_.bytes}, (unsigned long long*)sk_idx_.p,
-                  sk_w_.as<double>(), flag_.as<int>(), st_);
-    }
-    solve_sketch(s);
   }
 
   GramSpec gram_spec(uint64_t s) {

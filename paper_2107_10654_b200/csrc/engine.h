@@ -52,6 +52,7 @@ struct AlsOptions {
   void* allreduce_user = nullptr;
   int core_solver = 0;                    // 0 auto (PCG, Cholesky fallback), 1 Cholesky
   bool fast_loss = false;                 // loss by the expansion formula (see engine.cu)
+  uint64_t factor_samples = 0;            // > 0: sketched factor updates (perf mode)
 };
 
 struct HistoryRow {

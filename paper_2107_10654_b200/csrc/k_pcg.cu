@@ -112,6 +112,32 @@ __device__ __forceinline__ double block_sum_det(double v, double* red) {
   return t;  // every thread holds the total
 }
 
+// Two deterministic block sums with one pair of barriers.
+__device__ __forceinline__ void block_sum2_det(double& v0, double& v1, double* red) {
+  for (int o = 16; o > 0; o >>= 1) {
+    v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) {
+    red[w] = v0;
+    red[kWarps + w] = v1;
+  }
+  __syncthreads();
+  double t0 = 0.0, t1 = 0.0;
+  if (lane < kWarps) {
+    t0 = red[lane];
+    t1 = red[kWarps + lane];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+    t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+  }
+  v0 = t0;
+  v1 = t1;
+}
+
 // out[o, j, k] = sum_i P[i * RM + j] X[o, i, k] (i, j < R <= RM; P symmetric) on
 // a d-vector in shared memory. RX = R when every mode has exactly that rank
 // (no guards: loops unroll into straight-line code), else 0 (guarded loops).
@@ -326,17 +352,35 @@ __device__ void slice_partials_n3(const PcgArgs& A, const PcgShared& sh, const d
     const double* Bs = A.B + (size_t)u1 * m2 * 256;
     const double* pa = p + (size_t)a * dp;
     const double* pb = p + (size_t)b * dp;
-    for (int pidx = w; pidx < m2; pidx += kWarps) {
+    // the L2 reads of a warp's blocks are issued kAhead at a time (latency, not
+    // bandwidth, bounds this loop: ~9 blocks per warp)
+#ifndef RTB_PCG_AHEAD
+#define RTB_PCG_AHEAD 1
+#endif
+    constexpr int kAhead = RTB_PCG_AHEAD;
+    for (int pbase = w; pbase < m2; pbase += kWarps * kAhead) {
+      double2 gq[kAhead][2][2];
+#pragma unroll
+      for (int k = 0; k < kAhead; ++k) {
+        const int pidx = pbase + k * kWarps;
+        if (pidx < m2) {
+          const double* blk = Bs + (size_t)pidx * 256;
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              gq[k][rr][h] =
+                  __ldg(reinterpret_cast<const double2*>(blk + (r + 8 * rr) * 16 + 8 * h + 2 * c));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kAhead; ++k) {
+      const int pidx = pbase + k * kWarps;
+      if (pidx >= m2) break;
       int i2, j2;
       pair_of(pidx, R2, i2, j2);
       const bool two_orient = i2 != j2;
-      const double* blk = Bs + (size_t)pidx * 256;
-      double2 g[2][2];
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          g[rr][h] = __ldg(reinterpret_cast<const double2*>(blk + (r + 8 * rr) * 16 + 8 * h + 2 * c));
+      const double2(&g)[2][2] = gq[k];
       // targets: 0 = q_a(i2) <- p_b(j2), 1 = q_a(j2) <- p_b(i2), 2 = q_b(i2) <- p_a(j2),
       // 3 = q_b(j2) <- p_a(i2)
       const double* src[4] = {pb + j2 * 16, pb + i2 * 16, pa + j2 * 16, pa + i2 * 16};
@@ -374,6 +418,7 @@ __device__ void slice_partials_n3(const PcgArgs& A, const PcgShared& sh, const d
         }
       }
       __syncwarp();
+      }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < 2 * dp; e += kThreads) {
@@ -620,8 +665,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
       xs[e] = xe;
       xx = fma(xe, xe, xx);
     }
-    rr = block_sum_det(rr, red);
-    xx = block_sum_det(xx, red);
+    block_sum2_det(rr, xx, red);
     RTB_PCG_MARK(4)
     if (rr <= tol2 * fmax(bb, gnorm * gnorm * xx)) {
       ++it;

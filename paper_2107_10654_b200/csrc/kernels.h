@@ -87,6 +87,24 @@ void draw_sketch(const DrawSpec& spec, const double* scores, const double* cdfs,
                  const double* sums, DrawWork work, unsigned long long* idx_out,
                  double* w_out, int* flag_dev, cudaStream_t st);
 
+// ---- k_fsketch.cu: sketched factor update (perf mode) ----
+struct FactorSketchSpec {
+  int order;
+  int mode;                 // 0-based
+  int rows[8], ranks[8];
+  const double* factors[8];
+  const double* core;
+  const double* x;
+  double lambda;
+  unsigned long long s;     // draws (indices over the other modes + R_n augmented rows)
+};
+size_t factor_sketch_work_bytes(const FactorSketchSpec& spec);
+// gram (R_n x R_n) and M (I_n x R_n) from the draws idx/w (k_draw.cu format with
+// total_rows = prod_{m != n} I_m, d = R_n)
+void factor_sketch_normal_eq(const FactorSketchSpec& spec, const unsigned long long* idx,
+                             const double* w, void* work, double* gram, double* M,
+                             cudaStream_t st);
+
 // ---- k_gram.cu ----
 struct GramSpec {
   int order;

@@ -64,7 +64,8 @@ class AlsExt(C.Structure):
         ("core_solver", C.c_int),
         ("fast_loss", C.c_int),
         ("shard_rows_total", C.c_int),
-        ("reserved", C.c_int * 4),
+        ("factor_samples", C.c_uint32),
+        ("reserved", C.c_int * 3),
     ]
 
 
@@ -405,10 +406,11 @@ class Shard:
 
 
 def _ext(init_model: Model | None = None, profile: bool = False, core_solver: int = 0,
-         fast_loss: bool = False, shard: Shard | None = None):
+         fast_loss: bool = False, shard: Shard | None = None, factor_samples: int = 0):
     ext = AlsExt()
     ext.core_solver = int(core_solver)
     ext.fast_loss = int(fast_loss)
+    ext.factor_samples = int(factor_samples)
     keep = []
     if shard is not None:
         fn = shard.allreduce
@@ -438,19 +440,21 @@ def _ext(init_model: Model | None = None, profile: bool = False, core_solver: in
 
 def als_run(x: Tensor, ranks, opts: AlsOptions | None = None, init_model: Model | None = None,
             profile: bool = False, core_solver: int = 0, fast_loss: bool = False,
-            shard: Shard | None = None) -> Result:
+            shard: Shard | None = None, factor_samples: int = 0) -> Result:
     """rtucker_als_run (ref capi.cpp:176-201); extensions via rtucker_b200_als_run_ex.
-    With `shard`, `x` holds only that shard's rows of mode 1 (see shard_rows)."""
+    With `shard`, `x` holds only that shard's rows of mode 1 (see shard_rows).
+    factor_samples > 0: sketched factor updates with that many draws (perf mode)."""
     opts = opts or options()
     ranks = _u64(ranks)
     r = _vp()
     shape = tuple(x.shape)
     if shard is not None:
         shape = (shard.rows_total,) + shape[1:]
-    if init_model is None and not profile and not core_solver and not fast_loss and shard is None:
+    if (init_model is None and not profile and not core_solver and not fast_loss and shard is None
+            and not factor_samples):
         _check(lib.rtucker_als_run(x.h, _p(ranks), len(ranks), C.byref(opts), C.byref(r)))
     else:
-        ext, keep = _ext(init_model, profile, core_solver, fast_loss, shard)
+        ext, keep = _ext(init_model, profile, core_solver, fast_loss, shard, factor_samples)
         _check(lib.rtucker_b200_als_run_ex(x.h, _p(ranks), len(ranks), C.byref(opts),
                                            C.byref(ext), C.byref(r)))
         del keep
@@ -462,13 +466,13 @@ class Session:
 
     def __init__(self, x: Tensor, ranks, opts: AlsOptions | None = None,
                  init_model: Model | None = None, profile: bool = False, core_solver: int = 0,
-                 shard: Shard | None = None):
+                 shard: Shard | None = None, factor_samples: int = 0):
         self.shape = tuple(x.shape)
         if shard is not None:
             self.shape = (shard.rows_total,) + self.shape[1:]
         opts = opts or options()
         ranks = _u64(ranks)
-        ext, self._keep = _ext(init_model, profile, core_solver, False, shard)
+        ext, self._keep = _ext(init_model, profile, core_solver, False, shard, factor_samples)
         self.h = _vp()
         _check(lib.rtucker_b200_session_create(x.h, _p(ranks), len(ranks), C.byref(opts),
                                                C.byref(ext), C.byref(self.h)))

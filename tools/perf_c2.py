@@ -13,6 +13,7 @@ R = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 s = int(sys.argv[3]) if len(sys.argv) > 3 else 200000
 sweeps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 solver = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+fsamples = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 ranks = (R,) * len(shape)
 g = torch.Generator(device="cuda").manual_seed(0)
 core = torch.randn(ranks, dtype=torch.float64, device="cuda", generator=g)
@@ -28,7 +29,7 @@ t = rt.Tensor.from_device(x.data_ptr(), shape)
 opts = rt.options(lam=1e-2, sketched_core=1, sample_count_override=s, tolerance=0.0,
                   max_iterations=sweeps + 1)
 t0 = time.time()
-sess = rt.Session(t, ranks, opts, profile=True, core_solver=solver)
+sess = rt.Session(t, ranks, opts, profile=True, core_solver=solver, factor_samples=fsamples)
 sess.sweeps(1)
 torch.cuda.synchronize()
 t1 = time.time()

@@ -627,6 +627,7 @@ class Engine {
   bool scores_valid_ = false;
   DevBuf fsums_, fsk_idx_, fsk_w_, fsk_work_;
   bool t_valid_ = false;
+  bool warm_core_ = false;  // core_ holds a previous sketched solve's solution
   uint64_t last_s_ = 0;
   int last_rank_deficient_ = 0, last_solver_path_ = 0, last_pcg_iters_ = 0;
   struct StepEv {
@@ -1168,6 +1169,9 @@ class Engine {
       ps.max_iter = 80;
       ps.tol = 1e-15;
       ps.check_tol = 1e-12;
+      // warm start from the current core (the previous sweep's solution); the first
+      // sketch of a run starts cold (the core is the random init then)
+      ps.warm = warm_core_ ? 1 : 0;
       pcg_work_.ensure(pcg_work_bytes((int)d_, rk[0]), st_);
       pcg_solve(ps, blocks_.as<double>(), rhs_.as<double>(), core_.as<double>(), pcg_work_.p,
                 pcg_status_.as<int>(), st_);
@@ -1177,6 +1181,7 @@ class Engine {
       RTB_CUDA(cudaStreamSynchronize(st_));
       last_pcg_iters_ = ps_out[1];
       if (ps_out[0] == 0 && !status[1]) {
+        warm_core_ = true;
         last_solver_path_ = 2;
         last_rank_deficient_ = 0;
         check_core_finite();

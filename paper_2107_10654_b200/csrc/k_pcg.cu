@@ -57,6 +57,7 @@ struct PcgArgs {
   double* q;              // [d]
   double* part;           // [m1][2][d']
   double* rpart;          // [grid] residual partials
+  int warm;               // x holds a starting guess
   unsigned* counter;
   int* status;            // [0] status, [1] iterations
   const double* pinv;     // per mode (stride): (A_n^T A_n)^-1, row-major
@@ -216,6 +217,42 @@ __device__ __forceinline__ void mode_product(const double* X, double* out, const
   }
 }
 
+// Rank-16 modes on the FP64 tensor cores: out[o, j, k] = sum_i P[i][j] X[o, i, k] is
+// C (16 x NN) = P^T (16 x 16) B (16 x NN) with column n = (o, k), NN = d / 16,
+// B[i][n] = X[o*16*J + i*J + k]. m8n8k4 DMMAs: A = P^T fragments in registers
+// (a = P[4 ks + t][8 mt + g]), one 8-column tile per warp iteration.
+__device__ __forceinline__ void mode_product_dmma16(const double* X, double* out, const double* P,
+                                                    int d, int J) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double a[2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) a[mt][ks] = P[(ks * 4 + t) * 16 + mt * 8 + g];
+  const int ntiles = d / 128;
+  for (int nt = warp; nt < ntiles; nt += kWarps) {
+    const int n = nt * 8 + g;
+    const int o = n / J, k = n - o * J;
+    const double* xb = X + o * 16 * J + k;
+    double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const double b = xb[(ks * 4 + t) * J];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) dmma_8x8x4(c[mt][0], c[mt][1], a[mt][ks], b);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int n2 = nt * 8 + 2 * t + e;
+      const int o2 = n2 / J, k2 = n2 - o2 * J;
+      double* ob = out + o2 * 16 * J + k2;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) ob[(mt * 8 + g) * J] = c[mt][e];
+    }
+  }
+}
+
 // z = M^-1 r with scratch a, b; returns the buffer holding z. Two forms:
 //  * P form (eig == false): M = (x)_n A_n^T A_n, M^-1 = (x)_n P_n: N mode products.
 //  * eigen form: M = (x)_n A_n^T A_n + lambda I = V diag(lambda + prod mu) V^T:
@@ -228,7 +265,8 @@ __device__ double* precondition(const PcgShared& sh, const double* r, double* a,
   double* dst = a;
   unsigned long long t0 = prof ? gtimer() : 0;
   for (int n = 0; n < sh.order; ++n) {
-    mode_product<RM, RX>(src, dst, W1 + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
+    if constexpr (RX == 16 && RM == 16) mode_product_dmma16(src, dst, W1 + n * RM * RM, sh.d, sh.J[n]);
+    else mode_product<RM, RX>(src, dst, W1 + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
     __syncthreads();
     if (prof && n < 8) {
       const unsigned long long t1 = gtimer();
@@ -243,7 +281,8 @@ __device__ double* precondition(const PcgShared& sh, const double* r, double* a,
     for (int e = threadIdx.x; e < sh.d; e += kThreads) t[e] *= dinv[e];
     __syncthreads();
     for (int n = 0; n < sh.order; ++n) {
-      mode_product<RM, RX>(src, dst, W2 + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
+      if constexpr (RX == 16 && RM == 16) mode_product_dmma16(src, dst, W2 + n * RM * RM, sh.d, sh.J[n]);
+      else mode_product<RM, RX>(src, dst, W2 + n * RM * RM, sh.d, sh.R[n], sh.J[n]);
       __syncthreads();
       src = dst;
       dst = (dst == a) ? b : a;
@@ -610,6 +649,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
     }
     return;
   }
+  // warm start from x0 = A.x (the previous sweep's core: the system changes little
+  // between sweeps): r = b - G x0, kept only if it beats the cold residual ||b||
+  if (A.warm) {
+    for (int e = threadIdx.x; e < d; e += kThreads) {
+      const double x0 = A.x[e];
+      xs[e] = x0;
+      p[e] = x0;
+    }
+    __syncthreads();
+    if (fast3) slice_partials_n3(A, sh, p, accw);
+    else slice_partials<RM>(A, sh, p);
+    __syncthreads();
+    sync_target += gridDim.x;
+    grid_barrier(A.counter, sync_target);
+    reduce_rows(A, sh, p, row0, nrows, A.q);
+    __syncthreads();
+    sync_target += gridDim.x;
+    grid_barrier(A.counter, sync_target);
+    double r0 = 0.0;
+    for (int e = threadIdx.x; e < d; e += kThreads) {
+      const double re = A.b[e] - __ldcg(A.q + e);
+      s0[e] = re;
+      r0 = fma(re, re, r0);
+    }
+    r0 = block_sum_det(r0, red);
+    if (r0 < bb && isfinite(r0)) {
+      for (int e = threadIdx.x; e < d; e += kThreads) r[e] = s0[e];
+    } else {
+      for (int e = threadIdx.x; e < d; e += kThreads) xs[e] = 0.0;
+    }
+    __syncthreads();
+  }
   double* z = precondition<RM, RX>(sh, r, s0, s1, Ps, VTs, dinv, eig);
   double rho = 0.0;
   for (int e = threadIdx.x; e < d; e += kThreads) {
@@ -823,6 +894,7 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   a.max_iter = spec.max_iter;
   a.tol = spec.tol;
   a.check_tol = spec.check_tol;
+  a.warm = spec.warm;
   static unsigned long long* prof_buf = nullptr;
   static const bool prof_on = std::getenv("RTB_PCG_PROF") != nullptr;
   if (prof_on) {

@@ -157,6 +157,7 @@ struct PcgSpec {
   int max_iter;
   double tol;           // stop when ||r_k|| <= tol max(||b||, ||G||~ ||x_k||)
   double check_tol;     // accept when ||b - G x|| <= check_tol (||G||~ ||x|| + ||b||)
+  int warm = 0;         // 1: x holds a starting guess (kept if ||b - G x0|| < ||b||)
 };
 size_t pcg_work_bytes(int d, int r1);
 // norm estimates and preconditioner form (prep_dev[3]); skip_dev[order] = 1 where the

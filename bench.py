@@ -466,6 +466,75 @@ def run_our_arm(args):
     return 0
 
 
+def run_c4(args):
+    """BASELINE config 4 microbench (--workload c4): Kronecker-product sampling + fused fiber
+    gather/SYRK. 3 factors 2048 x 32 N(0,1) FP64 (A1 unused by the microbench), X 2048^3 FP32
+    N(0,1) (34 GB, resident), lambda = 1e-2; for each s: draws of [A2 (x) A3; sqrt(lambda) I]
+    (W = 1024), the W x W Gram and the W x 2048 mode-1 fiber RHS. One JSON line per s."""
+    import numpy as np
+    import torch
+    from paper_2107_10654_b200 import rtucker as rt
+    torch.cuda.set_device(0)
+    rt.set_stream(torch.cuda.current_stream().cuda_stream)
+    I, R, lam = 2048, 32, 1e-2
+    g = torch.Generator(device="cuda").manual_seed(0)
+    a2 = torch.randn(I, R, dtype=torch.float64, device="cuda", generator=g)
+    a3 = torch.randn(I, R, dtype=torch.float64, device="cuda", generator=g)
+    x = torch.empty((I, I, I), dtype=torch.float32, device="cuda")
+    for k in range(0, I, 128):  # seeded N(0,1) in slabs (bounded temporaries)
+        x[k:k + 128].normal_(generator=g)
+    W = R * R
+    gram = torch.empty(W, W, dtype=torch.float64, device="cuda")
+    rhs = torch.empty(W, I, dtype=torch.float64, device="cuda")
+    peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+    mp = {}
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = mp.get("hbm_gbs", 6553.3)
+    fp64 = peaks["dmma_m8n8k4_tflops"]
+    for s in [int(float(v)) for v in args.c4_s.split(",")]:
+        for _ in range(args.warmup):
+            rt.kron_fiber_sketch(x.data_ptr(), (I, I, I), a2.data_ptr(), a3.data_ptr(), R, R, lam, s,
+                                 1, gram.data_ptr(), rhs.data_ptr())
+        ph = np.zeros(3)
+        nd = 0
+        for k in range(args.steps):
+            out = rt.kron_fiber_sketch(x.data_ptr(), (I, I, I), a2.data_ptr(), a3.data_ptr(), R, R,
+                                       lam, s, 2 + k, gram.data_ptr(), rhs.data_ptr())
+            ph += np.array(out["phase_ms"])
+            nd += out["data_draws"]
+        ph /= args.steps
+        nd /= args.steps
+        draw_ms, gram_ms, rhs_ms = ph
+        m = R * (R + 1) // 2
+        # order-2 vech Gram: per data draw a vech(a3 a3^T) update of its j2 bucket, then the
+        # contraction S = V2^T H over the 2048 buckets
+        gram_flops = 2.0 * nd * m + 2.0 * m * m * I
+        rhs_flops = 2.0 * nd * R * I + 2.0 * I * R * R * I  # D_b accumulation + fold a2 (x) D_b
+        fiber_bytes = 4.0 * I * nd                # useful FP32 fiber bytes
+        line = {
+            "metric": "C4 sketched Kronecker samples/s (Gram+RHS)",
+            "value": s / ((draw_ms + gram_ms + rhs_ms) / 1e3),
+            "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "dtype": "f64 (FP32 tensor upcast)", "data": "synthetic",
+            "config": {"workload": "C4: factors 2048 x 32 N(0,1), X 2048^3 FP32 N(0,1) (34 GB), "
+                                   "design A2 (x) A3 (4,194,304 x 1024), lambda 1e-2",
+                       "s": s, "data_draws": nd},
+            "phases_ms": {"scores_and_draws": draw_ms, "gram": gram_ms, "fiber_rhs": rhs_ms},
+            "gram_only_samples_per_s": s / ((draw_ms + gram_ms) / 1e3),
+            "fiber_rhs": {"useful_gbs": fiber_bytes / (rhs_ms / 1e3) / 1e9,
+                          "useful_frac_hbm": fiber_bytes / (rhs_ms / 1e3) / 1e9 / hbm,
+                          "tflops": rhs_flops / (rhs_ms / 1e3) / 1e12,
+                          "frac_fp64": rhs_flops / (rhs_ms / 1e3) / 1e12 / fp64},
+            "gram": {"tflops": gram_flops / (gram_ms / 1e3) / 1e12,
+                     "frac_fp64": gram_flops / (gram_ms / 1e3) / 1e12 / fp64},
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -473,11 +542,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
+                    help="c2 (default): the headline ALS sweep; c4: the BASELINE config-4 "
+                         "sampling + fiber gather/SYRK microbench")
+    ap.add_argument("--c4-s", default="1e5,1e6,1e7", help="sample counts for --workload c4")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.workload == "c4":
+        return run_c4(args)
     return run_our_arm(args)
 
 

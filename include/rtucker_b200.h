@@ -147,6 +147,20 @@ rtucker_status rtucker_b200_kron_draw(uint32_t order, const uint64_t* rows, uint
 /* Rung 3: sketched normal equations (gram d x d full, rhs d) of the augmented
  * Kronecker design from a caller-supplied RowSketch (ref
  * sketch_ridge.cpp:105-128). x is the host tensor (prod rows values). */
+/* BASELINE config 4 microbench (Kronecker-product sampling + fused fiber gather/SYRK), all
+ * buffers on the device: draws s rows of [A2 (x) A3; sqrt(lambda) I_W] (W = r2 r3) with the
+ * reference's ProductLeverageSampler stream, then gram_dev (W x W, if non-NULL) = the
+ * sketched Gram and rhs_dev (W x I1, if x_dev and rhs_dev are non-NULL) = sum over data
+ * draws of w^2 (a2 (x) a3) X[:, j2, j3]^T, X being an I1 x I2 x I3 FP32 tensor (upcast in
+ * the kernel). indices_out / weights_out (host, s entries, optional) receive the draws;
+ * phase_ms_out[3] (optional) = scores+draws, Gram, RHS device times. r2, r3 <= 32. */
+rtucker_status rtucker_b200_kron_fiber_sketch(const float* x_dev, const uint64_t* shape,
+                                              const double* a2_dev, const double* a3_dev,
+                                              uint32_t r2, uint32_t r3, double lambda, uint64_t s,
+                                              uint64_t seed, double* gram_dev, double* rhs_dev,
+                                              uint64_t* indices_out, double* weights_out,
+                                              uint64_t* data_draws_out, double* phase_ms_out);
+
 rtucker_status rtucker_b200_kron_normal_eq(uint32_t order, const uint64_t* rows,
                                            const uint64_t* ranks, const double* factors,
                                            const double* x, double lambda, uint64_t s,

@@ -817,6 +817,20 @@ rtucker_status rtucker_b200_kron_draw(uint32_t order, const uint64_t* rows, uint
   });
 }
 
+rtucker_status rtucker_b200_kron_fiber_sketch(const float* x_dev, const uint64_t* shape,
+                                              const double* a2_dev, const double* a3_dev,
+                                              uint32_t r2, uint32_t r3, double lambda, uint64_t s,
+                                              uint64_t seed, double* gram_dev, double* rhs_dev,
+                                              uint64_t* indices_out, double* weights_out,
+                                              uint64_t* data_draws_out, double* phase_ms_out) {
+  return guarded([&] {
+    if (!shape || !a2_dev || !a3_dev) throw rtb::Error(1, "kron_fiber_sketch: null argument");
+    rtb::kron_fiber_sketch(x_dev, (int)shape[0], (int)shape[1], (int)shape[2], a2_dev, a3_dev,
+                           (int)r2, (int)r3, lambda, s, seed, gram_dev, rhs_dev, indices_out,
+                           weights_out, data_draws_out, phase_ms_out);
+  });
+}
+
 rtucker_status rtucker_b200_kron_normal_eq(uint32_t order, const uint64_t* rows,
                                            const uint64_t* ranks, const double* factors,
                                            const double* x, double lambda, uint64_t s,

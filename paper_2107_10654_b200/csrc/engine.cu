@@ -1737,6 +1737,120 @@ void kron_draw(int order, const uint64_t* rows, uint64_t d, const double* scores
   if (bad) throw Error(1, "ImplicitKronecker: cannot sample, factor has no nonzero rows");
 }
 
+void kron_fiber_sketch(const float* x, int I1, int I2, int I3, const double* a2, const double* a3,
+                       int R2, int R3, double lambda, uint64_t s, uint64_t seed, double* gram,
+                       double* rhs, uint64_t* idx_host, double* w_host, uint64_t* data_draws,
+                       double* phase_ms) {
+  if (I1 < 1 || I2 < 1 || I3 < 1 || R2 < 1 || R3 < 1 || R2 > 32 || R3 > 32 || R2 > I2 || R3 > I3)
+    throw Error(1, "kron_fiber_sketch: bad shape or ranks (R <= 32, R <= I)");
+  if (s == 0) throw Error(1, "solve_sketched_ridge: sample count must be positive");
+  if (lambda < 0.0) throw Error(1, "solve_sketched_ridge: lambda must be non-negative");
+  cudaStream_t st = current_stream();
+  const int rmax = std::max(R2, R3), stride = rmax * rmax, maxI = std::max(I2, I3);
+  const uint64_t W = (uint64_t)R2 * R3, total = (uint64_t)I2 * I3;
+  cudaEvent_t ev[4];
+  for (auto& e : ev) RTB_CUDA(cudaEventCreate(&e));
+  RTB_CUDA(cudaEventRecord(ev[0], st));
+  // ---- scores (classical, Cholesky route with the eigen fallback) and draws ----
+  DevBuf grams(2 * stride * 8, st), linv(2 * stride * 8, st), ok(2 * 4, st), evals(2 * stride * 8, st),
+      evecs(2 * stride * 8, st), est(2 * 4 + 64, st), scores((I2 + I3) * 8, st),
+      cdf((I2 + I3) * 8, st), sums(2 * 8, st), meta(256, st), flag(4, st);
+  FactorSet fs{};
+  fs.order = 2;
+  fs.ptr[0] = a2;
+  fs.ptr[1] = a3;
+  fs.rows[0] = I2;
+  fs.rows[1] = I3;
+  fs.cols[0] = R2;
+  fs.cols[1] = R3;
+  int hmeta[8] = {R2, R3, I2, I3, R2, R3, 0, 0};  // ns, rows, ranks
+  long long hoff[2] = {0, I2};
+  char* mp = static_cast<char*>(meta.p);
+  int* ns_dev = reinterpret_cast<int*>(mp);
+  int* rows_dev = ns_dev + 2;
+  int* ranks_dev = ns_dev + 4;
+  long long* off_dev = reinterpret_cast<long long*>(mp + 64);
+  RTB_CUDA(cudaMemcpyAsync(mp, hmeta, sizeof(hmeta), cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemcpyAsync(off_dev, hoff, sizeof(hoff), cudaMemcpyHostToDevice, st));
+  k_factor_gram<<<dim3(rmax * rmax, 2), 256, 0, st>>>(fs, grams.as<double>(), rmax);
+  RTB_LAUNCH_CHECK();
+  spd_small(grams.as<double>(), ns_dev, stride, (double)maxI * DBL_EPSILON, linv.as<double>(), nullptr,
+            ok.as<int>(), 2, st, rmax);
+  sym_eigen(grams.as<double>(), ns_dev, rmax, stride, evals.as<double>(), evecs.as<double>(),
+            est.as<int>(), 2, st, ok.as<int>());
+  const dim3 lg(ceil_div(maxI, 128), 2);
+  k_leverage_rows<<<lg, 128, 0, st>>>(fs, evals.as<double>(), evecs.as<double>(), stride, 0.0,
+                                      scores.as<double>(), off_dev, ranks_dev, ok.as<int>());
+  RTB_LAUNCH_CHECK();
+  k_leverage_chol<<<lg, 128, 0, st>>>(fs, linv.as<double>(), stride, ok.as<int>(),
+                                      scores.as<double>(), off_dev, ranks_dev);
+  RTB_LAUNCH_CHECK();
+  k_score_cdf<<<1, 64, 0, st>>>(scores.as<double>(), off_dev, rows_dev, 2, cdf.as<double>(),
+                                sums.as<double>());
+  RTB_LAUNCH_CHECK();
+  DrawSpec ds{};
+  ds.order = 2;
+  ds.rows[0] = I2;
+  ds.rows[1] = I3;
+  ds.cdf_off[0] = 0;
+  ds.cdf_off[1] = I2;
+  ds.total_rows = total;
+  ds.d = W;
+  ds.seed = seed;
+  ds.s = s;
+  DevBuf ix(s * 8, st), ww(s * 8, st), dwork(draw_work_bytes(ds), st);
+  RTB_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
+  draw_sketch(ds, scores.as<double>(), cdf.as<double>(), sums.as<double>(),
+              DrawWork{dwork.p, dwork.bytes}, (unsigned long long*)ix.p, ww.as<double>(),
+              flag.as<int>(), st);
+  RTB_CUDA(cudaEventRecord(ev[1], st));
+  // ---- Gram (order-2 vech/Kronecker machinery; the response is not needed) ----
+  DevBuf dd(8, st);
+  if (gram) {
+    GramSpec gs{};
+    gs.order = 2;
+    gs.rows[0] = I2;
+    gs.rows[1] = I3;
+    gs.ranks[0] = R2;
+    gs.ranks[1] = R3;
+    gs.factors[0] = a2;
+    gs.factors[1] = a3;
+    gs.total_rows = total;
+    gs.d = (int)W;
+    gs.dprime = R3;
+    gs.lambda = lambda;
+    gs.s = s;
+    DevBuf zb(total * 8, st), r(W * 8, st), gw(gram_work_bytes(gs), st);
+    RTB_CUDA(cudaMemsetAsync(zb.p, 0, total * 8, st));
+    sketch_normal_eq(gs, zb.as<double>(), (const unsigned long long*)ix.p, ww.as<double>(), gw.p,
+                     gw.bytes, gram, r.as<double>(), (unsigned long long*)dd.p, st);
+  }
+  RTB_CUDA(cudaEventRecord(ev[2], st));
+  // ---- fiber RHS ----
+  if (x && rhs) {
+    DevBuf cw(c4_fiber_work_bytes(s, I2), st);
+    c4_fiber_rhs(x, I1, I2, I3, a2, R2, a3, R3, (const unsigned long long*)ix.p, ww.as<double>(),
+                 s, cw.p, cw.bytes, rhs, st);
+  }
+  RTB_CUDA(cudaEventRecord(ev[3], st));
+  int bad = 0;
+  RTB_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
+  if (idx_host) RTB_CUDA(cudaMemcpyAsync(idx_host, ix.p, s * 8, cudaMemcpyDeviceToHost, st));
+  if (w_host) RTB_CUDA(cudaMemcpyAsync(w_host, ww.p, s * 8, cudaMemcpyDeviceToHost, st));
+  uint64_t nd = 0;
+  if (gram) RTB_CUDA(cudaMemcpyAsync(&nd, dd.p, 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  if (bad) throw Error(1, "ImplicitKronecker: cannot sample, factor has no nonzero rows");
+  if (data_draws) *data_draws = nd;
+  if (phase_ms)
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.f;
+      RTB_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+      phase_ms[k] = ms;
+    }
+  for (auto& e : ev) cudaEventDestroy(e);
+}
+
 void kron_normal_eq(int order, const uint64_t* rows, const uint64_t* ranks, const double* factors,
                     const double* x_host, double lambda, uint64_t s, const uint64_t* idx,
                     const double* w, double* gram, double* rhs) {

@@ -110,6 +110,13 @@ void factor_scores(const double* factor_host, int rows, int cols, double* scores
 void kron_draw(int order, const uint64_t* rows, uint64_t d, const double* scores,
                const double* cdfs, const double* sums, uint64_t seed, uint64_t s, uint64_t* idx,
                double* w);
+// BASELINE C4 microbench on device buffers: scores of A2, A3, s draws from their augmented
+// product distribution (d = R2 R3), the W x W Gram (W = R2 R3) and, when x != nullptr,
+// the W x I1 fiber RHS. phase_ms[3] = scores+draws, Gram, RHS (CUDA events).
+void kron_fiber_sketch(const float* x, int I1, int I2, int I3, const double* a2, const double* a3,
+                       int R2, int R3, double lambda, uint64_t s, uint64_t seed, double* gram,
+                       double* rhs, uint64_t* idx_host, double* w_host, uint64_t* data_draws,
+                       double* phase_ms);
 void kron_normal_eq(int order, const uint64_t* rows, const uint64_t* ranks, const double* factors,
                     const double* x_host, double lambda, uint64_t s, const uint64_t* idx,
                     const double* w, double* gram, double* rhs);

@@ -105,6 +105,14 @@ void factor_sketch_normal_eq(const FactorSketchSpec& spec, const unsigned long l
                              const double* w, void* work, double* gram, double* M,
                              cudaStream_t st);
 
+// ---- k_c4.cu: fiber RHS of the C4 microbench ----
+size_t c4_fiber_work_bytes(unsigned long long s, int I2);
+// rhs (R2 R3 x I1) = sum over data draws of w^2 (a2 (x) a3) X[:, j2, j3]^T (X FP32, I1 x I2 x I3)
+void c4_fiber_rhs(const float* x, int I1, int I2, int I3, const double* A2, int R2,
+                  const double* A3, int R3, const unsigned long long* idx, const double* w,
+                  unsigned long long s, void* work, size_t work_bytes, double* rhs,
+                  cudaStream_t st);
+
 // ---- k_gram.cu ----
 struct GramSpec {
   int order;

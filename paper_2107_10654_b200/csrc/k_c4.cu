@@ -13,12 +13,8 @@
 // bucket D_b = sum_{t in b} w^2 a3(j3_t) x_t^T (R3 x I1) and RHS = sum_b a2(b) (x) D_b:
 // 2 R3 I1 flops per data draw instead of 2 W I1.
 //
-// k_c4_fiber_rhs: one CTA per 16-column tile of the fiber index i (I1 / 16 CTAs) holds
-// its RHS tile (W x 16) in shared memory; per bucket, 64-draw chunks are staged from
-// precomputed sorted records (j3, w^2): A = a3 rows, B = w^2 times the gathered fiber
-// values of the tile (16 sectors per draw, shared by neighbouring j3 after the sort),
-// and 8 warps run m8n8k4 DMMAs into D (R3 x 16); at the bucket end D is folded into
-// the tile with a2(b). Fixed order: deterministic.
+// k_c4_fiber_rhs: one CTA per 16-column tile of the fiber index i (I1 / 16 CTAs); see
+// the kernel comment for the pipeline.
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -29,10 +25,6 @@ namespace rtb {
 namespace {
 
 constexpr int kC4Tile = 16;    // fiber columns per CTA
-constexpr int kC4Chunk = 64;   // draws staged per round
-constexpr int kC4LDA = kC4Chunk + 4;
-constexpr int kC4LDB = kC4Tile + 4;
-constexpr int kC4LDR = kC4Tile + 1;
 
 __global__ void k_c4_keys(const unsigned long long* __restrict__ idx, unsigned long long s,
                           unsigned long long total, int I3, unsigned long long* keys,
@@ -82,83 +74,141 @@ __global__ void __launch_bounds__(1024) k_c4_scan(int n, const int* counts, int*
     }
 }
 
+__global__ void k_c4_chunk_counts(int I2, const int* __restrict__ counts, int* __restrict__ ccnt) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < I2) ccnt[b] = (counts[b] + 255) / 256;
+}
+__global__ void k_c4_total(int I2, const int* ccnt, const int* cstart, int* total) {
+  *total = I2 > 0 ? cstart[I2 - 1] + ccnt[I2 - 1] : 0;
+}
+
+// chunk descriptors: chunk c covers draws [start, start + len) of bucket b (len <= kQC)
+constexpr int kQC = 256;  // draws per pipelined chunk
+__global__ void k_c4_chunks(int I2, const int* __restrict__ bstart, const int* __restrict__ bcount,
+                            const int* __restrict__ cstart, int4* __restrict__ chunks) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= I2) return;
+  const int n = bcount[b], c0 = cstart[b];
+  for (int k = 0; k * kQC < n; ++k) chunks[c0 + k] = make_int4(b, bstart[b] + k * kQC, min(kQC, n - k * kQC), 0);
+}
+
+// Pipelined RHS: the CTA's RHS tile (W x 16) lives in registers -- thread (q, i) =
+// (tid / 16, tid % 16) holds RHS[(p, q), i] for all p. Chunks of <= 256 draws of one j2
+// bucket flow through a two-buffer cp.async pipeline (a3 rows by 16 B copies, the
+// tile's 16 fiber values per draw by 4 B copies -- FP32 kept in shared memory, upcast
+// and scaled by w^2 at the fragment load -- and the next chunk's records), so the
+// gathers of chunk c + 1 are in flight while warps 0-7 run chunk c's DMMAs into
+// D (32 x 16). The limit is the cp.async issue rate of the staging (8 B a3 copies and
+// 4 B fiber copies: ~12k per 256-draw chunk), not the DMMAs. At each bucket end D goes through shared memory and every thread folds
+// RHS[(p, q), i] += a2(b)[p] D[q][i]. Fixed order: deterministic.
+constexpr int kQLDT = 36;   // a3 rows, draw-major [k][q]: conflict-free A fragments
+constexpr int kQLDB = 24;   // fiber values (floats) [k][i]: conflict-free B fragments
 __global__ void __launch_bounds__(512, 1) k_c4_fiber_rhs(
     const float* __restrict__ X, int I1, int I2, int I3, const double* __restrict__ A2, int R2,
     const double* __restrict__ A3, int R3, const int* __restrict__ j3s,
-    const double* __restrict__ w2s, const int* __restrict__ bstart, const int* __restrict__ bcount,
+    const double* __restrict__ w2s, const int4* __restrict__ chunks, const int* __restrict__ nchunks_p,
     double* __restrict__ rhs) {
   extern __shared__ __align__(16) double c4s[];
-  const int W = R2 * R3;
-  double* rt = c4s;                             // [W][kC4LDR] RHS tile
-  double* As = rt + (size_t)W * kC4LDR;         // [32][kC4LDA]: a3 rows (q x draw)
-  double* Bs = As + 32 * kC4LDA;                // [kC4Chunk][kC4LDB]: fiber values
-  double* a2s = Bs + kC4Chunk * kC4LDB;         // [32]: a2 row of the bucket
-  double* sw2 = a2s + 32;                       // [kC4Chunk]: w^2 of the chunk's draws
-  int* sj3 = reinterpret_cast<int*>(sw2 + kC4Chunk);  // [kC4Chunk]
+  double* At = c4s;                                    // [2][kQC][kQLDT]
+  float* Bf = reinterpret_cast<float*>(At + 2 * kQC * kQLDT);  // [2][kQC][kQLDB]
+  double* W2 = reinterpret_cast<double*>(Bf + 2 * kQC * kQLDB);  // [2][kQC]
+  int* J3 = reinterpret_cast<int*>(W2 + 2 * kQC);      // [2][kQC]
+  double* Ds = reinterpret_cast<double*>(J3 + 2 * kQC);  // [32][17]: D of the bucket
+  double* a2s = Ds + 32 * 17;                          // [32]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int i0 = blockIdx.x * kC4Tile;
-  const long long slab = (long long)I2 * I3;    // X stride of mode 1
-  for (int e = tid; e < W * kC4LDR; e += blockDim.x) rt[e] = 0.0;
+  const long long slab = (long long)I2 * I3;
+  const int nch = *nchunks_p;
+  const int mq = tid >> 4, mi = tid & 15;              // this thread's RHS column (q, i)
   const bool mma_warp = warp < 8;
-  const int mt = warp >> 1, nt = warp & 1;       // q rows 8 mt.., fiber columns 8 nt..
-  for (int b = 0; b < I2; ++b) {
-    const int n = bcount[b];
-    if (n == 0) continue;
-    const int st0 = bstart[b];
-    if (tid < 32) a2s[tid] = tid < R2 ? A2[(size_t)b * R2 + tid] : 0.0;
-    double c0 = 0.0, c1 = 0.0;
-    for (int k0 = 0; k0 < n; k0 += kC4Chunk) {
-      const int kn = min(kC4Chunk, n - k0);
-      __syncthreads();
-      // stage the chunk's records, then A[q][k] = a3(j3_t)[q] and B[k][i] = w_t^2 X[i0 + i, j2, j3_t]
-      if (tid < kC4Chunk) {
-        const int pos = st0 + k0 + tid;
-        sj3[tid] = tid < kn ? j3s[pos] : 0;
-        sw2[tid] = tid < kn ? w2s[pos] : 0.0;
-      }
-      __syncthreads();
-      for (int e = tid; e < 32 * kC4Chunk; e += blockDim.x) {
-        const int k = e / 32, q = e - k * 32;
-        As[q * kC4LDA + k] = (k < kn && q < R3) ? __ldg(A3 + (size_t)sj3[k] * R3 + q) : 0.0;
-      }
-      const long long rowb = (long long)b * I3;
-      for (int e = tid; e < kC4Chunk * kC4Tile; e += blockDim.x) {
-        const int k = e / kC4Tile, i = e - k * kC4Tile;
-        double v = 0.0;
-        if (k < kn && i0 + i < I1)
-          v = sw2[k] * (double)__ldg(X + (long long)(i0 + i) * slab + rowb + sj3[k]);
-        Bs[k * kC4LDB + i] = v;
-      }
-      __syncthreads();
-      if (mma_warp) {
-        const int kk = (kn + 3) & ~3;
-        for (int ks = 0; ks < kk; ks += 4) {
-          const double a = As[(mt * 8 + g) * kC4LDA + ks + t];
-          const double bv = Bs[(ks + t) * kC4LDB + nt * 8 + g];
-          dmma_8x8x4(c0, c1, a, bv);
-        }
-      }
+  const int mt = warp >> 1, nt = warp & 1;
+  double acc[32];
+#pragma unroll
+  for (int p = 0; p < 32; ++p) acc[p] = 0.0;
+  // records of chunk c into record buffer c & 1
+  auto load_records = [&](int c) {
+    if (c >= nch) return;
+    const int4 ch = chunks[c];
+    const int rb = c & 1;
+    for (int k = tid; k < kQC; k += blockDim.x) {
+      const bool v = k < ch.z;
+      cp_async4(J3 + rb * kQC + k, j3s + (v ? ch.y + k : 0), v);
+      cp_async8(W2 + rb * kQC + k, w2s + (v ? ch.y + k : 0), v);
     }
-    // fold D (this warp: q = 8 mt + g, i = 8 nt + 2t + e) into the tile with a2(b)
-    __syncthreads();
-    if (mma_warp) {
-      const int q = mt * 8 + g;
-      if (q < R3) {
-        const int ic = nt * 8 + 2 * t;
-        for (int p = 0; p < R2; ++p) {
-          const double ap = a2s[p];
-          double* row = rt + (size_t)(p * R3 + q) * kC4LDR + ic;
-          row[0] = fma(ap, c0, row[0]);
-          row[1] = fma(ap, c1, row[1]);
-        }
-      }
+  };
+  // data of chunk c (its records landed) into data buffer c & 1
+  auto load_data = [&](int c) {
+    if (c >= nch) return;
+    const int4 ch = chunks[c];
+    const int db = c & 1;
+    const int* j3 = J3 + db * kQC;
+    const int kpad = (ch.z + 3) & ~3;
+    // a3 rows: kpad x 32 doubles, 8 B copies (rows >= len and columns >= R3 zero-filled)
+    for (int e = tid; e < kpad * 32; e += blockDim.x) {
+      const int k = e >> 5, q = e & 31;
+      const bool v = k < ch.z && q < R3;
+      cp_async8(At + ((size_t)db * kQC + k) * kQLDT + q, A3 + (v ? (size_t)j3[k] * R3 + q : 0), v);
     }
-  }
+    const long long rowb = (long long)ch.x * I3;
+    for (int e = tid; e < kpad * kC4Tile; e += blockDim.x) {
+      const int k = e >> 4, i = e & 15;
+      const bool v = k < ch.z && i0 + i < I1;
+      cp_async4(Bf + ((size_t)db * kQC + k) * kQLDB + i,
+                X + (v ? (long long)(i0 + i) * slab + rowb + j3[k] : 0), v);
+    }
+  };
+  load_records(0);
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
-  for (int e = tid; e < W * kC4Tile; e += blockDim.x) {
-    const int r = e / kC4Tile, i = e - r * kC4Tile;
-    if (i0 + i < I1) rhs[(size_t)r * I1 + i0 + i] = rt[r * kC4LDR + i];
+  load_data(0);
+  load_records(1);
+  cp_async_commit();
+  double c0 = 0.0, c1 = 0.0;
+  for (int c = 0; c < nch; ++c) {
+    cp_async_wait<0>();
+    __syncthreads();  // chunk c's data and chunk c+1's records are in; buffers of c-1 free
+    load_data(c + 1);
+    // records of chunk c + 2 go to record buffer c & 1, whose chunk c is still read
+    // below -- so they are issued after this chunk's DMMAs (next iteration's head)
+    cp_async_commit();
+    const int4 ch = chunks[c];
+    const int db = c & 1;
+    if (mma_warp) {
+      const double* at = At + (size_t)db * kQC * kQLDT;
+      const float* bf = Bf + (size_t)db * kQC * kQLDB;
+      const double* w2 = W2 + db * kQC;
+      const int kpad = (ch.z + 3) & ~3;
+      for (int ks = 0; ks < kpad; ks += 4) {
+        const int k = ks + t;
+        const double a = at[k * kQLDT + mt * 8 + g];
+        const double b = (double)bf[k * kQLDB + nt * 8 + g] * w2[k];
+        dmma_8x8x4(c0, c1, a, b);
+      }
+    }
+    const bool last_of_bucket = (c + 1 >= nch) || (chunks[c + 1].x != ch.x);
+    if (last_of_bucket) {
+      if (mma_warp) {
+        Ds[(mt * 8 + g) * 17 + nt * 8 + 2 * t] = c0;
+        Ds[(mt * 8 + g) * 17 + nt * 8 + 2 * t + 1] = c1;
+      }
+      if (tid < 32) a2s[tid] = tid < R2 ? A2[(size_t)ch.x * R2 + tid] : 0.0;
+      c0 = c1 = 0.0;
+      __syncthreads();
+      const double dv = Ds[mq * 17 + mi];
+#pragma unroll
+      for (int p = 0; p < 32; ++p) acc[p] = fma(a2s[p], dv, acc[p]);
+    }
+    __syncthreads();  // record buffer c & 1 (chunk c) no longer read
+    load_records(c + 2);
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+  if (mq < R3 && i0 + mi < I1) {
+#pragma unroll
+    for (int p = 0; p < 32; ++p)
+      if (p < R2) rhs[(size_t)(p * R3 + mq) * I1 + i0 + mi] = acc[p];
   }
 }
 
@@ -169,7 +219,8 @@ size_t c4_fiber_work_bytes(unsigned long long s, int I2) {
   cub::DeviceRadixSort::SortPairs<unsigned long long, unsigned>(
       nullptr, cub_bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
       (const unsigned*)nullptr, (unsigned*)nullptr, (int)s);
-  return (size_t)s * (8 + 8 + 4 + 4 + 4 + 8) + (size_t)I2 * 8 + cub_bytes + 4096;
+  return (size_t)s * (8 + 8 + 4 + 4 + 4 + 8) + (size_t)I2 * 16 + cub_bytes +
+         ((size_t)s / 256 + (size_t)I2 + 1) * 16 + 8192;
 }
 
 void c4_fiber_rhs(const float* x, int I1, int I2, int I3, const double* A2, int R2,
@@ -212,10 +263,21 @@ void c4_fiber_rhs(const float* x, int I1, int I2, int I3, const double* A2, int 
   k_c4_records<<<(unsigned)ceil_div<unsigned long long>(s, 256ULL), 256, 0, st>>>(keys_s, vals_s, w,
                                                                                 s, I3, j3s, w2s);
   RTB_LAUNCH_CHECK();
-  const int W = R2 * R3;
-  const size_t smem =
-      ((size_t)W * kC4LDR + 32 * kC4LDA + kC4Chunk * kC4LDB + 32 + 2 * kC4Chunk) * sizeof(double);
-  if (smem > 227 * 1024) throw Error(4, "c4_fiber_rhs: R2 R3 too large for the shared tile");
+  // chunk descriptors (<= kQC draws, one bucket each)
+  auto* ccnt = reinterpret_cast<int*>(take((size_t)I2 * 4));
+  auto* cstart = reinterpret_cast<int*>(take((size_t)I2 * 4));
+  auto* nch = reinterpret_cast<int*>(take(64));
+  auto* chunks = reinterpret_cast<int4*>(take(((size_t)s / kQC + (size_t)I2 + 1) * 16));
+  k_c4_chunk_counts<<<ceil_div(I2, 256), 256, 0, st>>>(I2, counts, ccnt);
+  RTB_LAUNCH_CHECK();
+  k_c4_scan<<<1, 1024, 0, st>>>(I2, ccnt, cstart);
+  RTB_LAUNCH_CHECK();
+  k_c4_total<<<1, 1, 0, st>>>(I2, ccnt, cstart, nch);
+  RTB_LAUNCH_CHECK();
+  k_c4_chunks<<<ceil_div(I2, 256), 256, 0, st>>>(I2, start, counts, cstart, chunks);
+  RTB_LAUNCH_CHECK();
+  const size_t smem = (size_t)2 * kQC * kQLDT * 8 + (size_t)2 * kQC * kQLDB * 4 +
+                      (size_t)2 * kQC * 8 + (size_t)2 * kQC * 4 + (2 * 32 * 17 + 32) * 8;
   static bool attr = false;
   if (!attr) {
     RTB_CUDA(cudaFuncSetAttribute(k_c4_fiber_rhs, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -223,7 +285,7 @@ void c4_fiber_rhs(const float* x, int I1, int I2, int I3, const double* A2, int 
     attr = true;
   }
   k_c4_fiber_rhs<<<ceil_div(I1, kC4Tile), 512, smem, st>>>(x, I1, I2, I3, A2, R2, A3, R3, j3s,
-                                                             w2s, start, counts, rhs);
+                                                             w2s, chunks, nch, rhs);
   RTB_LAUNCH_CHECK();
 }
 

@@ -168,6 +168,12 @@ __global__ void __launch_bounds__(128) k_ttm_last(const double* __restrict__ X, 
 // blocks, so every DMMA operand comes from shared memory. FUSED also rebuilds
 // Xhat = P A^T tile by tile and accumulates (X - Xhat)^2 (one partial per CTA).
 constexpr int kStages2 = 3;
+#ifndef RTB_L3BK
+#define RTB_L3BK 64
+#define RTB_L3ST 2
+#endif
+constexpr int kL3BK = RTB_L3BK;     // k_ttm_last3 chunk width (columns per barrier)
+constexpr int kL3Stages = RTB_L3ST; // k_ttm_last3 ring depth
 constexpr int BM2 = 128;
 template <int RP>
 constexpr int lda2() { return RP + 4; }
@@ -836,7 +842,7 @@ void set_ttm_guard(const int* need) { g_need = need; }
 // Same pass with m16n8k16 DMMA (R <= 16): per 32-column chunk a T warp issues 4 MMAs
 // (2 k-steps x 2 n-tiles over the rank) and a residual warp 4 (one per 8 columns, K =
 // rank), each fed straight from shared memory, instead of 32 m8n8k4 each.
-template <bool FUSED>
+template <bool FUSED, int BK, int ST>
 __global__ void __launch_bounds__(512, 1) k_ttm_last3(const double* __restrict__ X, long long O,
                                                       int I, const double* __restrict__ A, int R,
                                                       double* __restrict__ T,
@@ -845,13 +851,13 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last3(const double* __restrict__
                                                       const int* __restrict__ need) {
   RTB_GUARD()
   constexpr int RP = 16;
-  constexpr int LD = kBK + kPadX;
+  constexpr int LD = BK + kPadX;
   constexpr int LDA = RP + 4;
   constexpr int ROWS = 16;  // rows per warp (m16)
   extern __shared__ __align__(16) double sm2[];
-  const int Ip = ceil_div(I, kBK) * kBK;
+  const int Ip = ceil_div(I, BK) * BK;
   double* as = sm2;                        // [Ip][LDA]
-  double* xs = as + (size_t)Ip * LDA;      // [kStages2][BM2][LD]
+  double* xs = as + (size_t)Ip * LDA;      // [ST][BM2][LD]
   __shared__ double red[32];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -860,7 +866,7 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last3(const double* __restrict__
   const int wrow = warp & 7;
   const bool idle = !FUSED && warp >= 8;
   const long long nrb = ceil_div<long long>(O, BM2);
-  const int nchunks = ceil_div(I, kBK);
+  const int nchunks = ceil_div(I, BK);
   for (int e = tid; e < Ip * LDA; e += 512) {
     const int i = e / LDA, r = e - i * LDA;
     as[e] = (i < I && r < R) ? A[(size_t)i * R + r] : 0.0;
@@ -871,17 +877,17 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last3(const double* __restrict__
     const long long rb = blockIdx.x + (q / nchunks) * gridDim.x;
     const int c = (int)(q % nchunks);
     const long long o0 = rb * BM2;
-    const int i0 = c * kBK;
+    const int i0 = c * BK;
     double* dst = xs + (size_t)stage * BM2 * LD;
-    for (int e = tid; e < BM2 * (kBK / 2); e += 512) {
-      const int r = e / (kBK / 2), col = (e % (kBK / 2)) * 2;
+    for (int e = tid; e < BM2 * (BK / 2); e += 512) {
+      const int r = e / (BK / 2), col = (e % (BK / 2)) * 2;
       const long long o = o0 + r;
       const bool ok = (o < O) && (i0 + col < I);
       cp_async16(dst + r * LD + col, ok ? X + o * I + i0 + col : X, ok);
     }
   };
 #pragma unroll
-  for (int sidx = 0; sidx < kStages2 - 1; ++sidx) {
+  for (int sidx = 0; sidx < ST - 1; ++sidx) {
     if (sidx < nitems) load_item(sidx, sidx);
     cp_async_commit();
   }
@@ -906,16 +912,16 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last3(const double* __restrict__
         }
       }
     }
-    cp_async_wait<kStages2 - 2>();
+    cp_async_wait<ST - 2>();
     __syncthreads();
-    if (q + kStages2 - 1 < nitems) load_item(q + kStages2 - 1, (int)((q + kStages2 - 1) % kStages2));
+    if (q + ST - 1 < nitems) load_item(q + ST - 1, (int)((q + ST - 1) % ST));
     cp_async_commit();
-    const double* xt = xs + (size_t)(q % kStages2) * BM2 * LD + wrow * ROWS * LD;
-    const int i0 = c * kBK;
+    const double* xt = xs + (size_t)(q % ST) * BM2 * LD + wrow * ROWS * LD;
+    const int i0 = c * BK;
     if (idle) {
     } else if (!rwarp) {
 #pragma unroll
-      for (int kb = 0; kb < kBK; kb += 16) {
+      for (int kb = 0; kb < BK; kb += 16) {
         double a[8];
 #pragma unroll
         for (int v = 0; v < 8; ++v) a[v] = xt[(g + 8 * (v & 1)) * LD + kb + t + 4 * (v >> 1)];
@@ -939,7 +945,7 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last3(const double* __restrict__
       }
     } else {
 #pragma unroll
-      for (int nb = 0; nb < kBK; nb += 8) {
+      for (int nb = 0; nb < BK; nb += 8) {
         double b[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) b[v] = as[(size_t)(i0 + nb + g) * LDA + t + 4 * v];
@@ -1013,13 +1019,14 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
   const bool v2 = (I % 2) == 0;
   const int rp = R <= 8 ? 8 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
   if (R > 32) throw Error(4, "ttm_last: rank > 32 not supported by the DMMA path");
-  if (last2_ok(I, R) && R <= 16) {
-    const size_t ip = (size_t)ceil_div(I, kBK) * kBK;
-    const size_t smem = (ip * lda2<16>() + (size_t)kStages2 * BM2 * (kBK + kPadX)) * 8;
-    auto k = fused ? k_ttm_last3<true> : k_ttm_last3<false>;
+  const size_t ip3 = (size_t)ceil_div(I, kL3BK) * kL3BK;
+  const size_t smem3 = (ip3 * lda2<16>() + (size_t)kL3Stages * BM2 * (kL3BK + kPadX)) * 8;
+  if (R <= 16 && (I % 2) == 0 && smem3 <= 227 * 1024 - 1024) {
+    const size_t smem = smem3;
+    auto k = fused ? k_ttm_last3<true, kL3BK, kL3Stages> : k_ttm_last3<false, kL3BK, kL3Stages>;
     static bool attr3[2] = {false, false};
     if (!attr3[fused]) {
-      RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 1024));
       attr3[fused] = true;
     }
     const long long nrb = ceil_div<long long>(O, BM2);

@@ -442,6 +442,12 @@ __global__ void __launch_bounds__(128) k_ttm_mid(const double* __restrict__ X, l
 // tile never straddles two o).
 constexpr int BJ2 = 128;
 constexpr int kStagesMid = 4;
+#ifndef RTB_MIDKB
+#define RTB_MIDKB 64
+#define RTB_MIDST 2
+#endif
+constexpr int kMidKB = RTB_MIDKB;      // k_ttm_mid3: rows of X (reduction index) per chunk
+constexpr int kMidStages = RTB_MIDST;  // k_ttm_mid3: ring depth
 template <int RP, bool COMPUTE = true>
 __global__ void __launch_bounds__(256, 1) k_ttm_mid2(const double* __restrict__ X, long long O,
                                                      int I, long long J,
@@ -548,23 +554,23 @@ __global__ void __launch_bounds__(288, 1) k_ttm_mid3(const double* __restrict__ 
                                                      const double* __restrict__ A, int R,
                                                      double* __restrict__ out) {
   constexpr int LDX = BJ2 + 8;
-  constexpr int S = kStagesMid;
+  constexpr int S = kMidStages;
   extern __shared__ __align__(16) double sm3[];
   __shared__ __align__(8) unsigned long long full[S], empty[S];
-  const int Ip = ceil_div(I, kBK) * kBK;
+  const int Ip = ceil_div(I, kMidKB) * kMidKB;
   const int LDT = Ip + 4;
   double* at = sm3;                       // [RP][LDT]
-  double* xs = at + (size_t)RP * LDT;     // [S][kBK][LDX]
+  double* xs = at + (size_t)RP * LDT;     // [S][kMidKB][LDX]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const long long ntiles = O * J / BJ2;
-  const int nchunks = ceil_div(I, kBK);
+  const int nchunks = ceil_div(I, kMidKB);
   for (int e = tid; e < RP * LDT; e += blockDim.x) {
     const int r = e / LDT, i = e - r * LDT;
     at[e] = (i < I && r < R) ? A[(size_t)i * R + r] : 0.0;
   }
   // stages zeroed once: rows of a short last chunk are never copied
-  for (int e = tid; e < S * kBK * LDX; e += blockDim.x) xs[e] = 0.0;
+  for (int e = tid; e < S * kMidKB * LDX; e += blockDim.x) xs[e] = 0.0;
   if (tid == 0) {
     for (int s2 = 0; s2 < S; ++s2) {
       mbar_init(&full[s2], 1);
@@ -585,16 +591,16 @@ __global__ void __launch_bounds__(288, 1) k_ttm_mid3(const double* __restrict__ 
       const int c = (int)(q % nchunks);
       const long long c0 = tile * BJ2;
       const long long o = c0 / J, j0 = c0 - o * J;
-      const int i0 = c * kBK;
-      const int rows = min(kBK, I - i0);
-      double* dst = xs + (size_t)st * kBK * LDX;
+      const int i0 = c * kMidKB;
+      const int rows = min(kMidKB, I - i0);
+      double* dst = xs + (size_t)st * kMidKB * LDX;
       if (lane == 0) {
         fence_proxy_async();
         mbar_arrive_expect_tx(&full[st], (unsigned)(rows * BJ2 * 8));
       }
       __syncwarp();
-      if (lane < rows)
-        bulk_g2s(dst + lane * LDX, X + (o * I + i0 + lane) * J + j0, BJ2 * 8, &full[st]);
+      for (int rr = lane; rr < rows; rr += 32)
+        bulk_g2s(dst + rr * LDX, X + (o * I + i0 + rr) * J + j0, BJ2 * 8, &full[st]);
     }
     return;
   }
@@ -609,8 +615,8 @@ __global__ void __launch_bounds__(288, 1) k_ttm_mid3(const double* __restrict__ 
         for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
     }
     mbar_wait(&full[st], (unsigned)((q / S) & 1));
-    const double* xt = xs + (size_t)st * kBK * LDX + warp * 16;
-    const int i0 = c * kBK;
+    const double* xt = xs + (size_t)st * kMidKB * LDX + warp * 16;
+    const int i0 = c * kMidKB;
     if (!COMPUTE) {
       acc[0][0][0] += xt[lane];
       __syncwarp();
@@ -618,7 +624,7 @@ __global__ void __launch_bounds__(288, 1) k_ttm_mid3(const double* __restrict__ 
       continue;
     }
 #pragma unroll
-    for (int ks = 0; ks < kBK / 4; ++ks) {
+    for (int ks = 0; ks < kMidKB / 4; ++ks) {
       double af[RP / 8];
 #pragma unroll
       for (int mt = 0; mt < RP / 8; ++mt) af[mt] = at[(size_t)(mt * 8 + g) * LDT + i0 + ks * 4 + t];
@@ -651,6 +657,10 @@ __global__ void __launch_bounds__(288, 1) k_ttm_mid3(const double* __restrict__ 
   }
 }
 
+static size_t mid3_smem(int I, int rp) {
+  const size_t ip = (size_t)ceil_div(I, kMidKB) * kMidKB;
+  return ((size_t)rp * (ip + 4) + (size_t)kMidStages * kMidKB * (BJ2 + 8)) * 8;
+}
 static size_t mid2_smem(int I, int rp) {
   const size_t ip = (size_t)ceil_div(I, kBK) * kBK;
   return ((size_t)rp * (ip + 4) + (size_t)kStagesMid * kBK * (BJ2 + 8)) * 8;
@@ -1119,12 +1129,14 @@ static void launch_mid2(const double* X, long long O, int I, long long J, const 
   const size_t smem = mid2_smem(I, RP);
   static const bool probe = std::getenv("RTB_TTM_STREAM_ONLY") != nullptr;
   static const bool pc = std::getenv("RTB_TTM_NO_PRODUCER") == nullptr;
-  if (pc) {
+  const size_t smem3 = mid3_smem(I, RP);
+  if (pc && smem3 <= 227 * 1024 - 2048) {
     auto k3 = probe ? k_ttm_mid3<RP, false> : k_ttm_mid3<RP, true>;
-    RTB_CUDA(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    RTB_CUDA(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024 - 2048));
     const long long ntiles = O * J / BJ2;
     const int grid = (int)std::min<long long>(ntiles, sm_count());
-    k3<<<grid, 288, smem, st>>>(X, O, I, J, A, R, out);
+    k3<<<grid, 288, smem3, st>>>(X, O, I, J, A, R, out);
     RTB_LAUNCH_CHECK();
     return;
   }

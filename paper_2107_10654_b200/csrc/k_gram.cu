@@ -37,6 +37,12 @@ namespace {
 constexpr int TB = 48;          // phase B/C output tile (6 x 8 rows)
 constexpr int TNC = 64;         // phase C output tile columns
 constexpr int KC = 32;          // samples (or buckets) per K chunk
+#ifndef RTB_KCB
+#define RTB_KCB 32
+#define RTB_KCC 32
+#endif
+constexpr int KCB = RTB_KCB;     // k_vech_bucket2: draws per pipelined chunk
+constexpr int KCC = RTB_KCC;     // k_vech_contract2: buckets per pipelined chunk
 constexpr int LDB = TB + 4;     // padded smem rows (phase B operands)
 constexpr int LDC = TNC + 4;    // padded smem rows (phase C H chunk)
 constexpr int kTh = 192;        // 6 warps, one 8-row m-tile each
@@ -517,24 +523,24 @@ __global__ void k_gather_rows(GramSpec spec, VechSpec v, const unsigned* __restr
 // DMMA stream has no branches. With HPT > 0 the same CTA also accumulates the
 // rhs ingredient h_b[p'] = sum_t w_t^2 x_t prod_{n>=1} a_n(i_n)[p_n] from the
 // staged factor rows (HPT outputs per thread).
-// cp.async one chunk of draw records (KC draws: factor rows, w^2, w^2 x) into buffer buf.
+// cp.async one chunk of draw records (KCB draws: factor rows, w^2, w^2 x) into buffer buf.
 template <int HPT>
 __device__ __forceinline__ void stage_bucket_chunk(const double* __restrict__ drow,
                                                    const double* __restrict__ dw2,
                                                    const double* __restrict__ dwx, double* frow,
                                                    double* w2s, double* wxs, int start, int len,
                                                    int k0, int buf, int RL, int RLp) {
-  const int kn = min(KC, len - k0);
-  double* fr = frow + buf * KC * RLp;
-  for (int e = threadIdx.x; e < KC * RL; e += blockDim.x) {
+  const int kn = min(KCB, len - k0);
+  double* fr = frow + buf * KCB * RLp;
+  for (int e = threadIdx.x; e < KCB * RL; e += blockDim.x) {
     const int k = e / RL, q = e - k * RL;
     const bool ok = k < kn;
     cp_async8(fr + k * RLp + q, ok ? drow + (size_t)(start + k0 + k) * RL + q : drow, ok);
   }
-  if (threadIdx.x < KC) {
+  if (threadIdx.x < KCB) {
     const bool ok = (int)threadIdx.x < kn;
-    cp_async8(w2s + buf * KC + threadIdx.x, ok ? dw2 + start + k0 + threadIdx.x : dw2, ok);
-    if (HPT > 0) cp_async8(wxs + buf * KC + threadIdx.x, ok ? dwx + start + k0 + threadIdx.x : dwx, ok);
+    cp_async8(w2s + buf * KCB + threadIdx.x, ok ? dw2 + start + k0 + threadIdx.x : dw2, ok);
+    if (HPT > 0) cp_async8(wxs + buf * KCB + threadIdx.x, ok ? dwx + start + k0 + threadIdx.x : dwx, ok);
   }
 }
 
@@ -549,11 +555,11 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
   // software pipeline, one barrier per chunk: while some warps still run the DMMAs of
   // chunk k, others already generate the operands of chunk k+1 into the other buffer
   // and the draw records of chunk k+2 land in the third frow buffer.
-  double* zr = smb;                   // [2][KC][LDZ]
-  double* zc = zr + 2 * KC * LDZ;     // [2][KC][LDZ]
-  double* frow = zc + 2 * KC * LDZ;   // [3][KC][RLp]
-  double* w2s = frow + 3 * KC * RLp;  // [3][KC]
-  double* wxs = w2s + 3 * KC;         // [3][KC]
+  double* zr = smb;                   // [2][KCB][LDZ]
+  double* zc = zr + 2 * KCB * LDZ;     // [2][KCB][LDZ]
+  double* frow = zc + 2 * KCB * LDZ;   // [3][KCB][RLp]
+  double* w2s = frow + 3 * KCB * RLp;  // [3][KCB]
+  double* wxs = w2s + 3 * KCB;         // [3][KCB]
   const int b = blockIdx.x;
   if (b >= *nbuckets) return;
   const int N = v.N;
@@ -598,16 +604,16 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
 #pragma unroll
   for (int j = 0; j < NTT; ++j) acc[j][0] = acc[j][1] = 0.0;
   const int rt0 = warp;
-  const int nch = (len + KC - 1) / KC;
+  const int nch = (len + KCB - 1) / KCB;
   // generate chunk kk (its frow buffer kk % 3 has landed) into z buffer kk & 1
   auto generate = [&](int kk) {
     const int fb = kk % 3, zb = kk & 1;
-    const double* fr = frow + fb * KC * RLp;
-    const double* w2c = w2s + fb * KC;
-    double* zrb = zr + zb * KC * LDZ;
-    double* zcb = zc + zb * KC * LDZ;
+    const double* fr = frow + fb * KCB * RLp;
+    const double* w2c = w2s + fb * KCB;
+    double* zrb = zr + zb * KCB * LDZ;
+    double* zcb = zc + zb * KCB * LDZ;
 #pragma unroll 4
-    for (int j = 0; j < KC / 4; ++j) {
+    for (int j = 0; j < KCB / 4; ++j) {
       const int k = k0r + 4 * j;
       const double* f = fr + k * RLp;
       double zrv = 0.0, zcv = 0.0;
@@ -627,7 +633,7 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
   };
   if (nch > 0) stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, 0, 0, RL, RLp);
   cp_async_commit();
-  if (nch > 1) stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, KC, 1, RL, RLp);
+  if (nch > 1) stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, KCB, 1, RL, RLp);
   cp_async_commit();
   cp_async_wait<1>();
   __syncthreads();
@@ -636,15 +642,15 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
   for (int kk = 0; kk < nch; ++kk) {
     // records of chunk kk+2 into frow buffer (kk+2) % 3 (last read by generate(kk-1))
     if (kk + 2 < nch)
-      stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, (kk + 2) * KC,
+      stage_bucket_chunk<HPT>(drow, dw2, dwx, frow, w2s, wxs, start, len, (kk + 2) * KCB,
                               (kk + 2) % 3, RL, RLp);
     cp_async_commit();
     const int zb = kk & 1;
     if (rt0 < MT) {
-      const double* zrb = zr + zb * KC * LDZ;
-      const double* zcb = zc + zb * KC * LDZ;
+      const double* zrb = zr + zb * KCB * LDZ;
+      const double* zcb = zc + zb * KCB * LDZ;
 #pragma unroll
-      for (int ks = 0; ks < KC / 4; ++ks) {
+      for (int ks = 0; ks < KCB / 4; ++ks) {
         const double* zrk = zrb + (ks * 4 + t4) * LDZ;
         const double* zck = zcb + (ks * 4 + t4) * LDZ;
         const double a0 = zrk[rt0 * 8 + g];
@@ -654,11 +660,11 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
     }
     if (hwarp) {
       const int fb = kk % 3;
-      const double* fr = frow + fb * KC * RLp;
-      const double* wxc = wxs + fb * KC;
+      const double* fr = frow + fb * KCB * RLp;
+      const double* wxc = wxs + fb * KCB;
       const int R2 = v.R[1], R3 = v.R[2], o2 = v.roff[1], o3 = v.roff[2];
 #pragma unroll
-      for (int ks = 0; ks < KC / 4; ++ks) {
+      for (int ks = 0; ks < KCB / 4; ++ks) {
         const int k = ks * 4 + t4;
         const double* f = fr + k * RLp;
         const double wk = wxc[k];
@@ -709,7 +715,7 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_bucket2(
 
 size_t vech_bucket2_smem(const VechSpec& v) {
   const size_t rlp = (size_t)((v.rowlen + 1) & ~1);
-  return (size_t)(4 * KC * LDZ + 3 * KC * rlp + 6 * KC) * 8 + 16;
+  return (size_t)(4 * KCB * LDZ + 3 * KCB * rlp + 6 * KCB) * 8 + 16;
 }
 
 // h_b[p'] = sum_{t in b} w_t^2 x_t prod_{n>=1} a_n(i_n)[p_n] from the draw records.
@@ -901,8 +907,8 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_contract2(GramSpec spe
                                                                   const int* __restrict__ nbuckets,
                                                                   double* __restrict__ S) {
   extern __shared__ __align__(16) double smc[];
-  double* hs = smc;                    // [2][KC][LDH2]
-  double* vs = hs + 2 * KC * LDH2;     // [2][KC][LDZ]
+  double* hs = smc;                    // [2][KCC][LDH2]
+  double* vs = hs + 2 * KCC * LDH2;     // [2][KCC][LDZ]
   const int R0 = v.R[0], m0 = v.m[0];
   const int nb = *nbuckets;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -916,8 +922,8 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_contract2(GramSpec spe
   const double* A0 = spec.factors[0];
   const bool vec = (v.Hsz & 1) == 0;
   auto load_h = [&](int kc, int buf) {
-    double* dst = hs + buf * KC * LDH2;
-    for (int e = tid; e < KC * (TNC2 / 2); e += blockDim.x) {
+    double* dst = hs + buf * KCC * LDH2;
+    for (int e = tid; e < KCC * (TNC2 / 2); e += blockDim.x) {
       const int k = e / (TNC2 / 2), c = (e % (TNC2 / 2)) * 2;
       const bool ok = (kc + k < nb) && (n0 + c < v.Hsz);
       const double* src = ok ? H + (size_t)(kc + k) * v.Hsz + n0 + c : H;
@@ -930,9 +936,9 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_contract2(GramSpec spe
     }
   };
   auto gen_v = [&](int kc, int buf) {
-    double* dst = vs + buf * KC * LDZ;
+    double* dst = vs + buf * KCC * LDZ;
 #pragma unroll 4
-    for (int j = 0; j < KC / 4; ++j) {
+    for (int j = 0; j < KCC / 4; ++j) {
       const int k = k0r + 4 * j;
       double val = 0.0;
       if (uok && kc + k < nb) {
@@ -945,7 +951,7 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_contract2(GramSpec spe
   double acc[8][2];
 #pragma unroll
   for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
-  const int nch = (nb + KC - 1) / KC;
+  const int nch = (nb + KCC - 1) / KCC;
   if (nch > 0) load_h(0, 0);
   cp_async_commit();
   if (nch > 0) gen_v(0, 0);
@@ -953,20 +959,20 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_contract2(GramSpec spe
   __syncthreads();
   for (int kk = 0; kk < nch; ++kk) {
     const int cur = kk & 1;
-    if (kk + 1 < nch) load_h((kk + 1) * KC, cur ^ 1);
+    if (kk + 1 < nch) load_h((kk + 1) * KCC, cur ^ 1);
     cp_async_commit();
     if (warp < MT) {
-      const double* hb = hs + cur * KC * LDH2;
-      const double* vb = vs + cur * KC * LDZ;
+      const double* hb = hs + cur * KCC * LDH2;
+      const double* vb = vs + cur * KCC * LDZ;
 #pragma unroll
-      for (int ks = 0; ks < KC / 4; ++ks) {
+      for (int ks = 0; ks < KCC / 4; ++ks) {
         const double af = vb[(ks * 4 + t4) * LDZ + warp * 8 + g];
 #pragma unroll
         for (int nt = 0; nt < 8; ++nt)
           dmma_8x8x4(acc[nt][0], acc[nt][1], af, hb[(ks * 4 + t4) * LDH2 + nt * 8 + g]);
       }
     }
-    if (kk + 1 < nch) gen_v((kk + 1) * KC, cur ^ 1);
+    if (kk + 1 < nch) gen_v((kk + 1) * KCC, cur ^ 1);
     cp_async_wait<0>();
     __syncthreads();
   }
@@ -1142,7 +1148,7 @@ void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
     RTB_LAUNCH_CHECK();
   }
   if ((v.m[0] + 7) / 8 <= kBWarps) {
-    const size_t smc = (size_t)(2 * KC * LDH2 + 2 * KC * LDZ) * 8;
+    const size_t smc = (size_t)(2 * KCC * LDH2 + 2 * KCC * LDZ) * 8;
     static bool attr_c = false;
     if (!attr_c) {
       RTB_CUDA(cudaFuncSetAttribute(k_vech_contract2, cudaFuncAttributeMaxDynamicSharedMemorySize,

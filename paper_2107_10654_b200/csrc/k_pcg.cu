@@ -489,7 +489,10 @@ __device__ void reduce_rows(const PcgArgs& A, const PcgShared& sh, const double*
   }
 }
 
-constexpr double kEigenAbove = 4.0;           // lambda / mu_min above which the eigen form is used
+#ifndef RTB_EIG_ABOVE
+#define RTB_EIG_ABOVE 4.0
+#endif
+constexpr double kEigenAbove = RTB_EIG_ABOVE;  // lambda / mu_min above which the eigen form is used
 constexpr double kMaxLambdaOverMu = 1e12;     // beyond: not worth CG
 
 // Warp n (one per mode, in parallel): mu_max(A_n^T A_n) and ||P_n||_2 = 1/mu_min by

@@ -144,23 +144,35 @@ rtucker_status rtucker_b200_kron_draw(uint32_t order, const uint64_t* rows, uint
                                       const double* sums, uint64_t seed, uint64_t s,
                                       uint64_t* indices_out, double* weights_out);
 
-/* Rung 3: sketched normal equations (gram d x d full, rhs d) of the augmented
- * Kronecker design from a caller-supplied RowSketch (ref
- * sketch_ridge.cpp:105-128). x is the host tensor (prod rows values). */
 /* BASELINE config 4 microbench (Kronecker-product sampling + fused fiber gather/SYRK), all
  * buffers on the device: draws s rows of [A2 (x) A3; sqrt(lambda) I_W] (W = r2 r3) with the
  * reference's ProductLeverageSampler stream, then gram_dev (W x W, if non-NULL) = the
  * sketched Gram and rhs_dev (W x I1, if x_dev and rhs_dev are non-NULL) = sum over data
  * draws of w^2 (a2 (x) a3) X[:, j2, j3]^T, X being an I1 x I2 x I3 FP32 tensor (upcast in
- * the kernel). indices_out / weights_out (host, s entries, optional) receive the draws;
- * phase_ms_out[3] (optional) = scores+draws, Gram, RHS device times. r2, r3 <= 32. */
+ * the kernel). x_layout: 0 = canonical row-major (last index fastest), 1 = fiber-major
+ * (mode 1 fastest: element (i1,i2,i3) at (i2 I3 + i3) I1 + i1, every mode-1 fiber
+ * contiguous; see rtucker_b200_tensor_fiber_major). indices_out / weights_out (host, s
+ * entries, optional) receive the draws; data_draws_out / unique_rows_out (optional) the
+ * number of data draws and of distinct sampled rows; phase_ms_out[3] (optional) =
+ * scores+draws, Gram (including the shared sort/merge of the draws), RHS device times.
+ * r2, r3 <= 32. */
 rtucker_status rtucker_b200_kron_fiber_sketch(const float* x_dev, const uint64_t* shape,
-                                              const double* a2_dev, const double* a3_dev,
-                                              uint32_t r2, uint32_t r3, double lambda, uint64_t s,
-                                              uint64_t seed, double* gram_dev, double* rhs_dev,
+                                              uint32_t x_layout, const double* a2_dev,
+                                              const double* a3_dev, uint32_t r2, uint32_t r3,
+                                              double lambda, uint64_t s, uint64_t seed,
+                                              double* gram_dev, double* rhs_dev,
                                               uint64_t* indices_out, double* weights_out,
-                                              uint64_t* data_draws_out, double* phase_ms_out);
+                                              uint64_t* data_draws_out, uint64_t* unique_rows_out,
+                                              double* phase_ms_out);
 
+/* Fiber-major copy of a device FP32 tensor (shape[3] = I1, I2, I3, canonical row-major in):
+ * out_dev[(i2 I3 + i3) I1 + i1] = x_dev[(i1 I2 + i2) I3 + i3]. */
+rtucker_status rtucker_b200_tensor_fiber_major(const float* x_dev, const uint64_t* shape,
+                                               float* out_dev);
+
+/* Rung 3: sketched normal equations (gram d x d full, rhs d) of the augmented
+ * Kronecker design from a caller-supplied RowSketch (ref
+ * sketch_ridge.cpp:105-128). x is the host tensor (prod rows values). */
 rtucker_status rtucker_b200_kron_normal_eq(uint32_t order, const uint64_t* rows,
                                            const uint64_t* ranks, const double* factors,
                                            const double* x, double lambda, uint64_t s,

@@ -1737,10 +1737,16 @@ void kron_draw(int order, const uint64_t* rows, uint64_t d, const double* scores
   if (bad) throw Error(1, "ImplicitKronecker: cannot sample, factor has no nonzero rows");
 }
 
-void kron_fiber_sketch(const float* x, int I1, int I2, int I3, const double* a2, const double* a3,
-                       int R2, int R3, double lambda, uint64_t s, uint64_t seed, double* gram,
-                       double* rhs, uint64_t* idx_host, double* w_host, uint64_t* data_draws,
-                       double* phase_ms) {
+void tensor_fiber_major(const float* x, int I1, int I2, int I3, float* out) {
+  cudaStream_t st = current_stream();
+  c4_to_fiber_major(x, I1, I2, I3, out, st);
+  RTB_CUDA(cudaStreamSynchronize(st));
+}
+
+void kron_fiber_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const double* a2,
+                       const double* a3, int R2, int R3, double lambda, uint64_t s, uint64_t seed,
+                       double* gram, double* rhs, uint64_t* idx_host, double* w_host,
+                       uint64_t* data_draws, uint64_t* unique_rows, double* phase_ms) {
   if (I1 < 1 || I2 < 1 || I3 < 1 || R2 < 1 || R3 < 1 || R2 > 32 || R3 > 32 || R2 > I2 || R3 > I3)
     throw Error(1, "kron_fiber_sketch: bad shape or ranks (R <= 32, R <= I)");
   if (s == 0) throw Error(1, "solve_sketched_ridge: sample count must be positive");
@@ -1804,44 +1810,30 @@ void kron_fiber_sketch(const float* x, int I1, int I2, int I3, const double* a2,
               DrawWork{dwork.p, dwork.bytes}, (unsigned long long*)ix.p, ww.as<double>(),
               flag.as<int>(), st);
   RTB_CUDA(cudaEventRecord(ev[1], st));
-  // ---- Gram (order-2 vech/Kronecker machinery; the response is not needed) ----
-  DevBuf dd(8, st);
-  if (gram) {
-    GramSpec gs{};
-    gs.order = 2;
-    gs.rows[0] = I2;
-    gs.rows[1] = I3;
-    gs.ranks[0] = R2;
-    gs.ranks[1] = R3;
-    gs.factors[0] = a2;
-    gs.factors[1] = a3;
-    gs.total_rows = total;
-    gs.d = (int)W;
-    gs.dprime = R3;
-    gs.lambda = lambda;
-    gs.s = s;
-    DevBuf zb(total * 8, st), r(W * 8, st), gw(gram_work_bytes(gs), st);
-    RTB_CUDA(cudaMemsetAsync(zb.p, 0, total * 8, st));
-    sketch_normal_eq(gs, zb.as<double>(), (const unsigned long long*)ix.p, ww.as<double>(), gw.p,
-                     gw.bytes, gram, r.as<double>(), (unsigned long long*)dd.p, st);
-  }
-  RTB_CUDA(cudaEventRecord(ev[2], st));
-  // ---- fiber RHS ----
-  if (x && rhs) {
-    DevBuf cw(c4_fiber_work_bytes(s, I2), st);
-    c4_fiber_rhs(x, I1, I2, I3, a2, R2, a3, R3, (const unsigned long long*)ix.p, ww.as<double>(),
-                 s, cw.p, cw.bytes, rhs, st);
+  // ---- one sort/merge of the draws, then the Gram and the fiber RHS (k_c4.cu) ----
+  DevBuf cnt(16, st);
+  const bool want_rhs = x && rhs;
+  if (gram || want_rhs) {
+    DevBuf cw(c4_work_bytes(s, I1, I2, I3, R2, R3, gram != nullptr), st);
+    c4_sketch(want_rhs ? x : nullptr, fiber_major, I1, I2, I3, a2, R2, a3, R3,
+              (const unsigned long long*)ix.p, ww.as<double>(), s, lambda, cw.p, cw.bytes, gram,
+              want_rhs ? rhs : nullptr, cnt.as<unsigned long long>(),
+              cnt.as<unsigned long long>() + 1, ev[2], st);
+  } else {
+    RTB_CUDA(cudaMemsetAsync(cnt.p, 0, 16, st));
+    RTB_CUDA(cudaEventRecord(ev[2], st));
   }
   RTB_CUDA(cudaEventRecord(ev[3], st));
   int bad = 0;
   RTB_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
   if (idx_host) RTB_CUDA(cudaMemcpyAsync(idx_host, ix.p, s * 8, cudaMemcpyDeviceToHost, st));
   if (w_host) RTB_CUDA(cudaMemcpyAsync(w_host, ww.p, s * 8, cudaMemcpyDeviceToHost, st));
-  uint64_t nd = 0;
-  if (gram) RTB_CUDA(cudaMemcpyAsync(&nd, dd.p, 8, cudaMemcpyDeviceToHost, st));
+  uint64_t nd[2] = {0, 0};
+  RTB_CUDA(cudaMemcpyAsync(nd, cnt.p, 16, cudaMemcpyDeviceToHost, st));
   RTB_CUDA(cudaStreamSynchronize(st));
   if (bad) throw Error(1, "ImplicitKronecker: cannot sample, factor has no nonzero rows");
-  if (data_draws) *data_draws = nd;
+  if (data_draws) *data_draws = nd[0];
+  if (unique_rows) *unique_rows = nd[1];
   if (phase_ms)
     for (int k = 0; k < 3; ++k) {
       float ms = 0.f;

@@ -112,11 +112,13 @@ void kron_draw(int order, const uint64_t* rows, uint64_t d, const double* scores
                double* w);
 // BASELINE C4 microbench on device buffers: scores of A2, A3, s draws from their augmented
 // product distribution (d = R2 R3), the W x W Gram (W = R2 R3) and, when x != nullptr,
-// the W x I1 fiber RHS. phase_ms[3] = scores+draws, Gram, RHS (CUDA events).
-void kron_fiber_sketch(const float* x, int I1, int I2, int I3, const double* a2, const double* a3,
-                       int R2, int R3, double lambda, uint64_t s, uint64_t seed, double* gram,
-                       double* rhs, uint64_t* idx_host, double* w_host, uint64_t* data_draws,
-                       double* phase_ms);
+// the W x I1 fiber RHS (x canonical row-major, or fiber-major: mode 1 fastest).
+// phase_ms[3] = scores+draws, Gram (incl. the shared sort/merge of the draws), RHS.
+void kron_fiber_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const double* a2,
+                       const double* a3, int R2, int R3, double lambda, uint64_t s, uint64_t seed,
+                       double* gram, double* rhs, uint64_t* idx_host, double* w_host,
+                       uint64_t* data_draws, uint64_t* unique_rows, double* phase_ms);
+void tensor_fiber_major(const float* x, int I1, int I2, int I3, float* out);
 void kron_normal_eq(int order, const uint64_t* rows, const uint64_t* ranks, const double* factors,
                     const double* x_host, double lambda, uint64_t s, const uint64_t* idx,
                     const double* w, double* gram, double* rhs);

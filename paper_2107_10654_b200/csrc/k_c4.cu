@@ -8,13 +8,22 @@
 //   3. gather the mode-1 fiber X[:, j2, j3] (I1 FP32 values, upcast to FP64);
 //   4. accumulate the W x W Gram and the W x I1 RHS:  G = sum w^2 z z^T + lambda sum_aug,
 //      RHS = sum w^2 z x^T.
-// The Gram is the core-Gram machinery of k_gram.cu with order 2 (vech/Kronecker
-// factored). The RHS is factored the same way: draws sorted by (j2, j3), so for each j2
-// bucket D_b = sum_{t in b} w^2 a3(j3_t) x_t^T (R3 x I1) and RHS = sum_b a2(b) (x) D_b:
-// 2 R3 I1 flops per data draw instead of 2 W I1.
 //
-// k_c4_fiber_rhs: one CTA per 16-column tile of the fiber index i (I1 / 16 CTAs); see
-// the kernel comment for the pipeline.
+// The reference streams every draw into the triangle (sketch_ridge.cpp:105-128). Here:
+//   (A) one radix sort of the draws by flat data index j2 I3 + j3 (augmented draws carry a
+//       sentinel and sort last); equal indices are merged into one record with weight
+//       c = sum of their w^2 in sorted (= draw) order, so every distinct sampled row is
+//       touched once (at s = 1e7 over the 4.2M rows of A2 (x) A3: ~2.9M distinct of 5M
+//       data draws). The merge is the exact identity sum_t w_t^2 z z^T = (sum_t w_t^2) z z^T.
+//   (B) Gram through a dense record-weight matrix C (I3 x I2, C[j3][j2] = c):
+//         G[(p,q),(p',q')] = sum_{j2} A2[j2,p] A2[j2,p'] T[j2,(q,q')],
+//         T[j2,(q,q')]     = sum_{j3} C[j2,j3] A3[j3,q] A3[j3,q'],
+//       two FP64 DMMA GEMMs (k_gemm_tn) over Khatri-Rao row products, then the permute
+//       into (p,q) order plus the augmented diagonal.
+//   (C) RHS factored by j2 bucket: D_b = sum_{t in b} c_t a3(j3_t) x_t^T (R3 x I1), 2 R3 I1
+//       flops per record (k_c4_dfib), then RHS = sum_b a2(b) (x) D_b = A2^T D (k_gemm_tn).
+//       The rows c_t a3(j3_t) are pre-scaled into a record-ordered array.
+// Fixed summation orders throughout: deterministic.
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -24,269 +33,525 @@ namespace rtb {
 
 namespace {
 
-constexpr int kC4Tile = 16;    // fiber columns per CTA
+constexpr int kRowW = 32;      // padded width of the pre-scaled a3 rows
 
-__global__ void k_c4_keys(const unsigned long long* __restrict__ idx, unsigned long long s,
-                          unsigned long long total, int I3, unsigned long long* keys,
-                          unsigned* vals, int* counts) {
+__global__ void k_c4_iota(unsigned long long s, unsigned* vals) {
+  const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < s) vals[t] = (unsigned)t;
+}
+
+// over the sorted draw indices (data rows < total, augmented rows total + j after them):
+// head[t] = 1 where a run of equal data indices starts; astart[j] (W + 1) = first sorted
+// position of augmented index j (runs are contiguous, so counts are differences -- no
+// atomics); *ndata = number of data draws
+__global__ void k_c4_heads(const unsigned long long* __restrict__ keys_s, unsigned long long s,
+                           unsigned long long total, int W, unsigned* __restrict__ head,
+                           int* __restrict__ astart, unsigned long long* __restrict__ ndata) {
   const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= s) return;
-  const unsigned long long id = idx[t];
-  const bool data = id < total;
-  keys[t] = data ? id : total;
-  vals[t] = (unsigned)t;
-  if (data) atomicAdd(counts + (int)(id / (unsigned long long)I3), 1);
+  const unsigned long long k = keys_s[t];
+  const bool has_prev = t > 0;
+  const unsigned long long pk = has_prev ? keys_s[t - 1] : 0ULL;
+  head[t] = (k < total && (!has_prev || pk != k)) ? 1u : 0u;
+  if (k >= total && (!has_prev || pk != k)) {
+    const long long j = (long long)(k - total);
+    const long long jp = (has_prev && pk >= total) ? (long long)(pk - total) : -1;
+    for (long long jj = jp + 1; jj <= j; ++jj) astart[jj] = (int)t;
+    if (!has_prev || pk < total) *ndata = t;
+  }
+  if (t == s - 1) {
+    const long long jl = k >= total ? (long long)(k - total) : -1;
+    for (long long jj = jl + 1; jj <= W; ++jj) astart[jj] = (int)s;
+    if (k < total) *ndata = s;
+  }
 }
 
-// sorted draw records: j3 and w^2 of each data draw in (j2, j3) order (one gather of w)
-__global__ void k_c4_records(const unsigned long long* __restrict__ keys_s,
-                             const unsigned* __restrict__ vals_s, const double* __restrict__ w,
-                             unsigned long long n, int I3, int* __restrict__ j3s,
-                             double* __restrict__ w2s) {
+// one thread per run head: record u = (key, c = sum of w^2 over the run in draw order)
+__global__ void k_c4_unique(const unsigned long long* __restrict__ keys_s,
+                            const unsigned* __restrict__ vals_s, const unsigned* __restrict__ head,
+                            const unsigned* __restrict__ uid, const double* __restrict__ w,
+                            unsigned long long s, unsigned long long* __restrict__ ukey,
+                            double* __restrict__ uc, unsigned long long* __restrict__ nuniq) {
   const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const double wt = w[vals_s[t]];
-  j3s[t] = (int)(keys_s[t] % (unsigned long long)I3);
-  w2s[t] = wt * wt;
+  if (t >= s) return;
+  if (t == s - 1) *nuniq = (unsigned long long)uid[t] + head[t];
+  if (!head[t]) return;
+  const unsigned long long k = keys_s[t];
+  double c = 0.0;
+  for (unsigned long long r = t; r < s && keys_s[r] == k; ++r) {
+    const double wt = w[vals_s[r]];
+    c += wt * wt;
+  }
+  const unsigned u = uid[t];
+  ukey[u] = k;
+  uc[u] = c;
 }
 
-// exclusive scan of the I2 bucket counts (one block)
-__global__ void __launch_bounds__(1024) k_c4_scan(int n, const int* counts, int* start) {
-  __shared__ int part[1024];
-  const int per = (n + 1023) / 1024;
-  const int b0 = threadIdx.x * per;
-  int s = 0;
-  for (int i = 0; i < per; ++i)
-    if (b0 + i < n) s += counts[b0 + i];
-  part[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+// bstart[b] (I2 + 1) = first record of bucket j2 = b (records are sorted by key)
+__global__ void k_c4_bounds(const unsigned long long* __restrict__ ukey,
+                            const unsigned long long* __restrict__ nuniq, unsigned long long s,
+                            int I2, int I3, int* __restrict__ bstart) {
+  const unsigned long long u = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long U = *nuniq;
+  if (U == 0) {
+    if (u == 0)
+      for (int b = 0; b <= I2; ++b) bstart[b] = 0;
+    return;
+  }
+  if (u >= U || u >= s) return;
+  const long long j2 = (long long)(ukey[u] / (unsigned long long)I3);
+  const long long jp = u > 0 ? (long long)(ukey[u - 1] / (unsigned long long)I3) : -1;
+  for (long long b = jp + 1; b <= j2; ++b) bstart[b] = (int)u;
+  if (u == U - 1)
+    for (long long b = j2 + 1; b <= I2; ++b) bstart[b] = (int)U;
+}
+
+// pre-scaled record rows c_u a3(j3_u), zero-padded to 32 columns (grid-stride, 16 B stores)
+__global__ void k_c4_rows(const unsigned long long* __restrict__ ukey, const double* __restrict__ uc,
+                          const unsigned long long* __restrict__ nuniq, int I3,
+                          const double* __restrict__ A3, int R3, double* __restrict__ rows) {
+  const unsigned long long n = *nuniq * (kRowW / 2);
+  for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long u = e / (kRowW / 2);
+    const int q = 2 * (int)(e % (kRowW / 2));
+    const double cu = uc[u];
+    const double* a = A3 + (size_t)(ukey[u] % (unsigned long long)I3) * R3;
+    reinterpret_cast<double2*>(rows)[e] =
+        make_double2(q < R3 ? cu * a[q] : 0.0, q + 1 < R3 ? cu * a[q + 1] : 0.0);
+  }
+}
+
+// ---- Gram (B) ----
+// C^T[j3][j2] = c of record (j2, j3); the matrix is zeroed first, records are distinct
+__global__ void k_c4_scatter(const unsigned long long* __restrict__ ukey, const double* __restrict__ uc,
+                             const unsigned long long* __restrict__ nuniq, int I2, int I3,
+                             double* __restrict__ ct) {
+  const unsigned long long u = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= *nuniq) return;
+  const unsigned long long k = ukey[u];
+  const unsigned long long j2 = k / (unsigned long long)I3, j3 = k % (unsigned long long)I3;
+  ct[j3 * (unsigned long long)I2 + j2] = uc[u];
+}
+
+// Khatri-Rao row products: kr[i][(a,b)] = A[i,a] A[i,b]
+__global__ void k_c4_kr(const double* __restrict__ A, int I, int R, double* __restrict__ kr) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long RR = (long long)R * R;
+  if (e >= (long long)I * RR) return;
+  const long long i = e / RR;
+  const int ab = (int)(e % RR), a = ab / R, b = ab % R;
+  kr[e] = A[i * R + a] * A[i * R + b];
+}
+
+// out[m][n] = sum_k A[k][m] B[k][n]  (A: K x M, B: K x N, row-major, leading dims lda/ldb).
+// (32 WM) x (16 (8 / WM)) output tile per CTA (WM = 2: 64 x 64; WM = 1: 32 x 128 for M <= 32),
+// 8 warps of 32 x 16 (4 x 2 DMMA.8x8x4 tiles), K chunks of 16 through a two-buffer cp.async
+// ring; rows padded to 4 mod 16 doubles make the fragment loads conflict-free.
+constexpr int kGK = 16;
+template <int WM>
+__global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, long long lda,
+                                                 const double* __restrict__ B, long long ldb,
+                                                 int M, int N, int K, double* __restrict__ out,
+                                                 long long ldo) {
+  constexpr int TM = 32 * WM, TN = 16 * (8 / WM), LDA = TM + 4, LDB = TN + 4;
+  __shared__ __align__(16) double As[2][kGK][LDA];
+  __shared__ __align__(16) double Bs[2][kGK][LDB];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const long long m0 = (long long)blockIdx.y * TM, n0 = (long long)blockIdx.x * TN;
+  const int wm = warp / (8 / WM), wn = warp % (8 / WM);
+  double c[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+  const int nk = (K + kGK - 1) / kGK;
+  auto load = [&](int kc, int buf) {
+    const int k0 = kc * kGK;
+    for (int e = tid; e < kGK * TM; e += 256) {
+      const int k = e / TM, j = e % TM;
+      const bool v = k0 + k < K && m0 + j < M;
+      cp_async8(&As[buf][k][j], A + (v ? (long long)(k0 + k) * lda + m0 + j : 0), v);
+    }
+    for (int e = tid; e < kGK * TN; e += 256) {
+      const int k = e / TN, j = e % TN;
+      const bool v = k0 + k < K && n0 + j < N;
+      cp_async8(&Bs[buf][k][j], B + (v ? (long long)(k0 + k) * ldb + n0 + j : 0), v);
+    }
+  };
+  load(0, 0);
+  cp_async_commit();
+  for (int kc = 0; kc < nk; ++kc) {
+    const int buf = kc & 1;
+    if (kc + 1 < nk) load(kc + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
-    part[threadIdx.x] += v;
+#pragma unroll
+    for (int ks = 0; ks < kGK; ks += 4) {
+      double a[4], b[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[buf][ks + t][wm * 32 + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = Bs[buf][ks + t][wn * 16 + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(c[i][j][0], c[i][j][1], a[i], b[j]);
+    }
     __syncthreads();
   }
-  int run = threadIdx.x > 0 ? part[threadIdx.x - 1] : 0;
-  for (int i = 0; i < per; ++i)
-    if (b0 + i < n) {
-      start[b0 + i] = run;
-      run += counts[b0 + i];
-    }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long m = m0 + wm * 32 + i * 8 + g, n = n0 + wn * 16 + j * 8 + 2 * t + h;
+        if (m < M && n < N) out[m * ldo + n] = c[i][j][h];
+      }
 }
 
-__global__ void k_c4_chunk_counts(int I2, const int* __restrict__ counts, int* __restrict__ ccnt) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b < I2) ccnt[b] = (counts[b] + 255) / 256;
-}
-__global__ void k_c4_total(int I2, const int* ccnt, const int* cstart, int* total) {
-  *total = I2 > 0 ? cstart[I2 - 1] + ccnt[I2 - 1] : 0;
+// out = A^T B (k_gemm_tn), tile shape by M
+void gemm_tn(const double* A, long long lda, const double* B, long long ldb, int M, long long N,
+             int K, double* out, long long ldo, cudaStream_t st) {
+  if (M <= 32) {
+    const long long gx = (N + 127) / 128;
+    if (gx > 0x7fffffffLL) throw Error(1, "gemm_tn: N too large");
+    k_gemm_tn<1><<<dim3((unsigned)gx, ceil_div(M, 32)), 256, 0, st>>>(A, lda, B, ldb, M, (int)N, K,
+                                                                       out, ldo);
+  } else {
+    const long long gx = (N + 63) / 64;
+    if (gx > 0x7fffffffLL) throw Error(1, "gemm_tn: N too large");
+    k_gemm_tn<2><<<dim3((unsigned)gx, ceil_div(M, 64)), 256, 0, st>>>(A, lda, B, ldb, M, (int)N, K,
+                                                                       out, ldo);
+  }
+  RTB_LAUNCH_CHECK();
 }
 
-// chunk descriptors: chunk c covers draws [start, start + len) of bucket b (len <= kQC)
-constexpr int kQC = 256;  // draws per pipelined chunk
-__global__ void k_c4_chunks(int I2, const int* __restrict__ bstart, const int* __restrict__ bcount,
-                            const int* __restrict__ cstart, int4* __restrict__ chunks) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= I2) return;
-  const int n = bcount[b], c0 = cstart[b];
-  for (int k = 0; k * kQC < n; ++k) chunks[c0 + k] = make_int4(b, bstart[b] + k * kQC, min(kQC, n - k * kQC), 0);
+// G[(p,q),(p',q')] = G'[(p,p'),(q,q')] + [p = p', q = q'] (augmented draws of (p,q)) aug_term
+__global__ void k_c4_gram_out(const double* __restrict__ gp, int R2, int R3,
+                              const int* __restrict__ astart, double aug_term,
+                              double* __restrict__ gram) {
+  const long long W = (long long)R2 * R3;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= W * W) return;
+  const long long r = e / W, col = e % W;
+  const int p = (int)(r / R3), q = (int)(r % R3), pp = (int)(col / R3), qq = (int)(col % R3);
+  double v = gp[((long long)p * R2 + pp) * ((long long)R3 * R3) + (long long)q * R3 + qq];
+  if (r == col) v += (double)(astart[r + 1] - astart[r]) * aug_term;
+  gram[e] = v;
 }
 
-// Pipelined RHS: the CTA's RHS tile (W x 16) lives in registers -- thread (q, i) =
-// (tid / 16, tid % 16) holds RHS[(p, q), i] for all p. Chunks of <= 256 draws of one j2
-// bucket flow through a two-buffer cp.async pipeline (a3 rows by 16 B copies, the
-// tile's 16 fiber values per draw by 4 B copies -- FP32 kept in shared memory, upcast
-// and scaled by w^2 at the fragment load -- and the next chunk's records), so the
-// gathers of chunk c + 1 are in flight while warps 0-7 run chunk c's DMMAs into
-// D (32 x 16). The limit is the cp.async issue rate of the staging (8 B a3 copies and
-// 4 B fiber copies: ~12k per 256-draw chunk), not the DMMAs. At each bucket end D goes through shared memory and every thread folds
-// RHS[(p, q), i] += a2(b)[p] D[q][i]. Fixed order: deterministic.
-constexpr int kQLDT = 36;   // a3 rows, draw-major [k][q]: conflict-free A fragments
-constexpr int kQLDB = 24;   // fiber values (floats) [k][i]: conflict-free B fragments
-__global__ void __launch_bounds__(512, 1) k_c4_fiber_rhs(
-    const float* __restrict__ X, int I1, int I2, int I3, const double* __restrict__ A2, int R2,
-    const double* __restrict__ A3, int R3, const int* __restrict__ j3s,
-    const double* __restrict__ w2s, const int4* __restrict__ chunks, const int* __restrict__ nchunks_p,
-    double* __restrict__ rhs) {
+// ---- RHS (C) ----
+// Two steps. k_c4_dfib: D[b][q][i] = sum over the records t of bucket b of
+// rows[t][q] x_t[i] (rows = c_t a3(j3_t), x_t = the sampled mode-1 fiber), a GEMM per bucket
+// with M = R3 (<= 32), N = I1, K = the bucket's records. Then RHS (R2 x R3 I1) = A2^T D by
+// k_gemm_tn (the fold RHS[(p,q), i] = sum_b a2(b)[p] D_b[q][i]).
+//
+// k_c4_dfib: persistent, two CTAs per SM; work item = (bucket b, 256-column tile of i),
+// bucket-major, static round robin. Per item the bucket's record keys are staged in shared
+// memory (segments of kSeg records), then chunks of 16 records flow through a kSt-stage
+// cp.async ring: the pre-scaled rows (16 x 16 B per chunk) and the tile's 256 fiber values
+// per record (MODE 1: fiber-major X with I1 % 4 == 0, one 1 KB run per record = 64 x 16 B
+// copies; MODE 2: fiber-major, 4 B copies; MODE 0: canonical row-major X, 256 strided 4 B
+// copies), FP32 kept in shared memory and upcast at the fragment load. 8 warps, warp w owns
+// the 32 x 32 tile D[:, 32 w .. 32 w + 31] as 4 x 4 DMMA.8x8x4 tiles (16 independent
+// accumulator chains; per k-step 4 A + 4 B fragment loads feed 16 DMMAs). Each (b, i) is
+// produced by one CTA in record order: deterministic, and fibers are read from HBM once.
+constexpr int kQLDT = 36;         // rows [k][q]: conflict-free A fragments
+constexpr int kDT = 256;          // fiber columns per work item
+constexpr int kQLDB = kDT + 8;    // fiber values (floats) [k][i]: conflict-free B fragments
+constexpr int kSt = 4;            // ring stages
+constexpr int kRC = 16;           // records per chunk
+constexpr int kSeg = 2048;        // records per key segment
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) k_c4_dfib(
+    const float* __restrict__ X, int I1, int I2, int I3, int R3,
+    const unsigned long long* __restrict__ ukey, const double* __restrict__ rows,
+    const int* __restrict__ bstart, double* __restrict__ D) {
   extern __shared__ __align__(16) double c4s[];
-  double* At = c4s;                                    // [2][kQC][kQLDT]
-  float* Bf = reinterpret_cast<float*>(At + 2 * kQC * kQLDT);  // [2][kQC][kQLDB]
-  double* W2 = reinterpret_cast<double*>(Bf + 2 * kQC * kQLDB);  // [2][kQC]
-  int* J3 = reinterpret_cast<int*>(W2 + 2 * kQC);      // [2][kQC]
-  double* Ds = reinterpret_cast<double*>(J3 + 2 * kQC);  // [32][17]: D of the bucket
-  double* a2s = Ds + 32 * 17;                          // [32]
+  unsigned long long* Ks = reinterpret_cast<unsigned long long*>(c4s);     // [kSeg]
+  double* At = c4s + kSeg;                                                 // [kSt][kRC][kQLDT]
+  float* Bf = reinterpret_cast<float*>(At + kSt * kRC * kQLDT);            // [kSt][kRC][kQLDB]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int i0 = blockIdx.x * kC4Tile;
   const long long slab = (long long)I2 * I3;
-  const int nch = *nchunks_p;
-  const int mq = tid >> 4, mi = tid & 15;              // this thread's RHS column (q, i)
-  const bool mma_warp = warp < 8;
-  const int mt = warp >> 1, nt = warp & 1;
-  double acc[32];
+  const int NT = (I1 + kDT - 1) / kDT;
+  const long long nitems = (long long)I2 * NT;
+  for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int b = (int)(item / NT), n0 = (int)(item % NT) * kDT;
+    const int r0 = bstart[b], cnt = bstart[b + 1] - r0;
+    double c[4][4][2];
 #pragma unroll
-  for (int p = 0; p < 32; ++p) acc[p] = 0.0;
-  // records of chunk c into record buffer c & 1
-  auto load_records = [&](int c) {
-    if (c >= nch) return;
-    const int4 ch = chunks[c];
-    const int rb = c & 1;
-    for (int k = tid; k < kQC; k += blockDim.x) {
-      const bool v = k < ch.z;
-      cp_async4(J3 + rb * kQC + k, j3s + (v ? ch.y + k : 0), v);
-      cp_async8(W2 + rb * kQC + k, w2s + (v ? ch.y + k : 0), v);
-    }
-  };
-  // data of chunk c (its records landed) into data buffer c & 1
-  auto load_data = [&](int c) {
-    if (c >= nch) return;
-    const int4 ch = chunks[c];
-    const int db = c & 1;
-    const int* j3 = J3 + db * kQC;
-    const int kpad = (ch.z + 3) & ~3;
-    // a3 rows: kpad x 32 doubles, 8 B copies (rows >= len and columns >= R3 zero-filled)
-    for (int e = tid; e < kpad * 32; e += blockDim.x) {
-      const int k = e >> 5, q = e & 31;
-      const bool v = k < ch.z && q < R3;
-      cp_async8(At + ((size_t)db * kQC + k) * kQLDT + q, A3 + (v ? (size_t)j3[k] * R3 + q : 0), v);
-    }
-    const long long rowb = (long long)ch.x * I3;
-    for (int e = tid; e < kpad * kC4Tile; e += blockDim.x) {
-      const int k = e >> 4, i = e & 15;
-      const bool v = k < ch.z && i0 + i < I1;
-      cp_async4(Bf + ((size_t)db * kQC + k) * kQLDB + i,
-                X + (v ? (long long)(i0 + i) * slab + rowb + j3[k] : 0), v);
-    }
-  };
-  load_records(0);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  load_data(0);
-  load_records(1);
-  cp_async_commit();
-  double c0 = 0.0, c1 = 0.0;
-  for (int c = 0; c < nch; ++c) {
-    cp_async_wait<0>();
-    __syncthreads();  // chunk c's data and chunk c+1's records are in; buffers of c-1 free
-    load_data(c + 1);
-    // records of chunk c + 2 go to record buffer c & 1, whose chunk c is still read
-    // below -- so they are issued after this chunk's DMMAs (next iteration's head)
-    cp_async_commit();
-    const int4 ch = chunks[c];
-    const int db = c & 1;
-    if (mma_warp) {
-      const double* at = At + (size_t)db * kQC * kQLDT;
-      const float* bf = Bf + (size_t)db * kQC * kQLDB;
-      const double* w2 = W2 + db * kQC;
-      const int kpad = (ch.z + 3) & ~3;
-      for (int ks = 0; ks < kpad; ks += 4) {
-        const int k = ks + t;
-        const double a = at[k * kQLDT + mt * 8 + g];
-        const double b = (double)bf[k * kQLDB + nt * 8 + g] * w2[k];
-        dmma_8x8x4(c0, c1, a, b);
-      }
-    }
-    const bool last_of_bucket = (c + 1 >= nch) || (chunks[c + 1].x != ch.x);
-    if (last_of_bucket) {
-      if (mma_warp) {
-        Ds[(mt * 8 + g) * 17 + nt * 8 + 2 * t] = c0;
-        Ds[(mt * 8 + g) * 17 + nt * 8 + 2 * t + 1] = c1;
-      }
-      if (tid < 32) a2s[tid] = tid < R2 ? A2[(size_t)ch.x * R2 + tid] : 0.0;
-      c0 = c1 = 0.0;
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+    for (int seg = 0; seg < cnt; seg += kSeg) {
+      const int len = min(kSeg, cnt - seg);
+      __syncthreads();  // Ks / ring free (previous segment or item done)
+      for (int k = tid; k < len; k += 256) cp_async8(Ks + k, ukey + r0 + seg + k, true);
+      cp_async_commit();
+      cp_async_wait<0>();
       __syncthreads();
-      const double dv = Ds[mq * 17 + mi];
+      const int nchk = (len + kRC - 1) / kRC;
+      auto load = [&](int ch) {
+        if (ch >= nchk) return;
+        const int sb = ch % kSt, kb = ch * kRC, n = min(kRC, len - kb);
+        double* at = At + (size_t)sb * kRC * kQLDT;
+        float* bf = Bf + (size_t)sb * kRC * kQLDB;
+        {
+          const int k = tid >> 4, pc = tid & 15;
+          const bool v = k < n;
+          cp_async16(at + k * kQLDT + 2 * pc,
+                     rows + (v ? ((size_t)(r0 + seg + kb + k) * kRowW + 2 * pc) : 0), v);
+        }
+        if (MODE == 1) {
 #pragma unroll
-      for (int p = 0; p < 32; ++p) acc[p] = fma(a2s[p], dv, acc[p]);
+          for (int j = 0; j < 4; ++j) {
+            const int e = tid + 256 * j, k = e >> 6, pc = e & 63;
+            const bool v = k < n && n0 + 4 * pc < I1;
+            const unsigned long long key = Ks[kb + (k < n ? k : 0)];
+            cp_async16(bf + k * kQLDB + 4 * pc, X + (v ? key * (unsigned long long)I1 + n0 + 4 * pc : 0), v);
+          }
+        } else {
+          const int col = n0 + tid;
+#pragma unroll 4
+          for (int k = 0; k < kRC; ++k) {
+            const bool v = k < n && col < I1;
+            const unsigned long long key = Ks[kb + (k < n ? k : 0)];
+            const long long off = !v ? 0
+                                  : MODE == 2 ? (long long)(key * (unsigned long long)I1) + col
+                                              : (long long)col * slab + (long long)key;
+            cp_async4(bf + k * kQLDB + tid, X + off, v);
+          }
+        }
+      };
+#pragma unroll
+      for (int ch = 0; ch < kSt - 1; ++ch) {
+        load(ch);
+        cp_async_commit();
+      }
+      for (int ch = 0; ch < nchk; ++ch) {
+        load(ch + kSt - 1);
+        cp_async_commit();
+        cp_async_wait<kSt - 1>();
+        __syncthreads();  // chunk ch landed
+        const int sb = ch % kSt;
+        const double* at = At + (size_t)sb * kRC * kQLDT;
+        const float* bf = Bf + (size_t)sb * kRC * kQLDB + warp * 32 + g;
+        const int kpad = (min(kRC, len - ch * kRC) + 3) & ~3;
+        for (int ks = 0; ks < kpad; ks += 4) {
+          const int k = ks + t;
+          double a[4], bv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = at[k * kQLDT + i * 8 + g];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bv[j] = (double)bf[k * kQLDB + j * 8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma_8x8x4(c[i][j][0], c[i][j][1], a[i], bv[j]);
+        }
+        __syncthreads();  // stage sb free
+      }
+      cp_async_wait<0>();
     }
-    __syncthreads();  // record buffer c & 1 (chunk c) no longer read
-    load_records(c + 2);
-    cp_async_commit();
-  }
-  cp_async_wait<0>();
-  if (mq < R3 && i0 + mi < I1) {
+    // D tile out (empty buckets write zeros)
 #pragma unroll
-    for (int p = 0; p < 32; ++p)
-      if (p < R2) rhs[(size_t)(p * R3 + mq) * I1 + i0 + mi] = acc[p];
+    for (int i = 0; i < 4; ++i) {
+      const int q = i * 8 + g;
+      if (q >= R3) continue;
+      double* drow = D + ((size_t)b * R3 + q) * I1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = n0 + warp * 32 + j * 8 + 2 * t;
+        if (col + 1 < I1 && (I1 % 2 == 0)) {
+          *reinterpret_cast<double2*>(drow + col) = make_double2(c[i][j][0], c[i][j][1]);
+        } else {
+          if (col < I1) drow[col] = c[i][j][0];
+          if (col + 1 < I1) drow[col + 1] = c[i][j][1];
+        }
+      }
+    }
   }
+}
+
+constexpr size_t kDfibSmem = (size_t)kSeg * 8 + (size_t)kSt * kRC * kQLDT * 8 +
+                             (size_t)kSt * kRC * kQLDB * 4;
+static_assert(kDfibSmem * 2 <= 227 * 1024, "two k_c4_dfib CTAs per SM");
+
+// ---- fiber-major conversion: out[(i2 I3 + i3) I1 + i1] = x[(i1 I2 + i2) I3 + i3] ----
+// a transpose of the I1 x (I2 I3) matrix in 32 x 32 tiles
+__global__ void k_c4_to_fm(const float* __restrict__ x, long long rows, long long cols,
+                           float* __restrict__ out) {
+  __shared__ float tile[32][33];
+  const long long c0 = (long long)blockIdx.x * 32, r0 = (long long)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const long long r = r0 + k, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = x[r * cols + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const long long c = c0 + k, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+  }
+}
+
+struct C4Layout {
+  unsigned long long *keys_s, *ukey, *ndata, *nuniq;
+  unsigned *vals, *vals_s, *head, *uid;
+  int *astart, *bstart;
+  double *uc, *rows, *dfib;
+  void* cub_sort;
+  size_t cub_sort_bytes;
+  void* cub_scan;
+  size_t cub_scan_bytes;
+  char* end;
+};
+
+template <typename F>
+C4Layout c4_carve(unsigned long long s, int I1, int I2, int R3, int W, F&& take) {
+  C4Layout l{};
+  size_t sb = 0, cb = 0;
+  cub::DeviceRadixSort::SortPairs<unsigned long long, unsigned>(
+      nullptr, sb, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+      (const unsigned*)nullptr, (unsigned*)nullptr, (int)s);
+  cub::DeviceScan::ExclusiveSum(nullptr, cb, (const unsigned*)nullptr, (unsigned*)nullptr, (int)s);
+  l.keys_s = (unsigned long long*)take(s * 8);
+  l.ukey = (unsigned long long*)take(s * 8);
+  l.ndata = (unsigned long long*)take(8);
+  l.nuniq = (unsigned long long*)take(8);
+  l.vals = (unsigned*)take(s * 4);
+  l.vals_s = (unsigned*)take(s * 4);
+  l.head = (unsigned*)take(s * 4);
+  l.uid = (unsigned*)take(s * 4);
+  l.astart = (int*)take((size_t)(W + 1) * 4);
+  l.bstart = (int*)take((size_t)(I2 + 1) * 4);
+  l.uc = (double*)take(s * 8);
+  l.rows = (double*)take(s * kRowW * 8);
+  l.dfib = (double*)take((size_t)I2 * R3 * I1 * 8);
+  l.cub_sort_bytes = sb;
+  l.cub_sort = take(sb);
+  l.cub_scan_bytes = cb;
+  l.cub_scan = take(cb);
+  l.end = (char*)take(0);
+  return l;
+}
+
+size_t gram_part_bytes(int I2, int I3, int R2, int R3) {
+  const size_t r2 = (size_t)R2 * R2, r3 = (size_t)R3 * R3;
+  return ((size_t)I3 * I2 + (size_t)I3 * r3 + (size_t)I2 * r2 + (size_t)I2 * r3 + r2 * r3) * 8 +
+         5 * 256;
 }
 
 }  // namespace
 
-size_t c4_fiber_work_bytes(unsigned long long s, int I2) {
-  size_t cub_bytes = 0;
-  cub::DeviceRadixSort::SortPairs<unsigned long long, unsigned>(
-      nullptr, cub_bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
-      (const unsigned*)nullptr, (unsigned*)nullptr, (int)s);
-  return (size_t)s * (8 + 8 + 4 + 4 + 4 + 8) + (size_t)I2 * 16 + cub_bytes +
-         ((size_t)s / 256 + (size_t)I2 + 1) * 16 + 8192;
+size_t c4_work_bytes(unsigned long long s, int I1, int I2, int I3, int R2, int R3, bool gram) {
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    const size_t r = off;
+    off += (b + 255) & ~size_t(255);
+    return (void*)r;
+  };
+  c4_carve(s, I1, I2, R3, R2 * R3, take);
+  return off + (gram ? gram_part_bytes(I2, I3, R2, R3) : 0) + 256;
 }
 
-void c4_fiber_rhs(const float* x, int I1, int I2, int I3, const double* A2, int R2,
-                  const double* A3, int R3, const unsigned long long* idx, const double* w,
-                  unsigned long long s, void* work, size_t work_bytes, double* rhs,
-                  cudaStream_t st) {
-  if (R3 > 32 || R2 > 32) throw Error(1, "c4_fiber_rhs: ranks must be <= 32");
-  if (work_bytes < c4_fiber_work_bytes(s, I2)) throw Error(4, "c4_fiber_rhs: workspace");
+void c4_to_fiber_major(const float* x, int I1, int I2, int I3, float* out, cudaStream_t st) {
+  const long long cols = (long long)I2 * I3;
+  const dim3 grid((unsigned)ceil_div<long long>(cols, 32LL), (unsigned)ceil_div(I1, 32));
+  if (grid.y > 65535) throw Error(1, "c4_to_fiber_major: I1 too large");
+  k_c4_to_fm<<<grid, dim3(32, 8), 0, st>>>(x, I1, cols, out);
+  RTB_LAUNCH_CHECK();
+}
+
+void c4_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const double* A2, int R2,
+               const double* A3, int R3, const unsigned long long* idx, const double* w,
+               unsigned long long s, double lambda, void* work, size_t work_bytes, double* gram,
+               double* rhs, unsigned long long* data_draws_dev, unsigned long long* unique_dev,
+               cudaEvent_t ev_gram_done, cudaStream_t st) {
+  if (R3 > 32 || R2 > 32) throw Error(1, "c4_sketch: ranks must be <= 32");
+  if (s > 0xffffffffULL) throw Error(1, "c4_sketch: at most 2^32 - 1 draws");
+  const int W = R2 * R3;
+  if (work_bytes < c4_work_bytes(s, I1, I2, I3, R2, R3, gram != nullptr))
+    throw Error(4, "c4_sketch: workspace");
   char* p = static_cast<char*>(work);
   auto take = [&](size_t bytes) {
     char* r = p;
     p += (bytes + 255) & ~size_t(255);
-    return r;
+    return (void*)r;
   };
-  auto* keys = reinterpret_cast<unsigned long long*>(take(s * 8));
-  auto* keys_s = reinterpret_cast<unsigned long long*>(take(s * 8));
-  auto* vals = reinterpret_cast<unsigned*>(take(s * 4));
-  auto* vals_s = reinterpret_cast<unsigned*>(take(s * 4));
-  auto* counts = reinterpret_cast<int*>(take((size_t)I2 * 4));
-  auto* start = reinterpret_cast<int*>(take((size_t)I2 * 4));
-  auto* j3s = reinterpret_cast<int*>(take(s * 4));
-  auto* w2s = reinterpret_cast<double*>(take(s * 8));
-  size_t cub_bytes = 0;
-  cub::DeviceRadixSort::SortPairs<unsigned long long, unsigned>(
-      nullptr, cub_bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
-      (const unsigned*)nullptr, (unsigned*)nullptr, (int)s);
-  void* cub_tmp = take(cub_bytes);
+  C4Layout l = c4_carve(s, I1, I2, R3, W, take);
   const unsigned long long total = (unsigned long long)I2 * I3;
   int bits = 1;
-  while ((1ULL << bits) <= total) ++bits;
-  RTB_CUDA(cudaMemsetAsync(counts, 0, (size_t)I2 * 4, st));
-  k_c4_keys<<<(unsigned)ceil_div<unsigned long long>(s, 256ULL), 256, 0, st>>>(idx, s, total, I3,
-                                                                             keys, vals, counts);
+  while ((1ULL << bits) <= total + (unsigned long long)W) ++bits;
+  const unsigned sb = (unsigned)ceil_div<unsigned long long>(s, 256ULL);
+  // sort the raw draw indices (augmented ones, total + j, sort after the data rows)
+  k_c4_iota<<<sb, 256, 0, st>>>(s, l.vals);
   RTB_LAUNCH_CHECK();
-  RTB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys, keys_s, vals, vals_s, (int)s,
-                                           0, bits, st));
-  k_c4_scan<<<1, 1024, 0, st>>>(I2, counts, start);
+  size_t cb = l.cub_sort_bytes;
+  RTB_CUDA(cub::DeviceRadixSort::SortPairs(l.cub_sort, cb, idx, l.keys_s, l.vals, l.vals_s,
+                                           (int)s, 0, bits, st));
+  k_c4_heads<<<sb, 256, 0, st>>>(l.keys_s, s, total, W, l.head, l.astart, l.ndata);
   RTB_LAUNCH_CHECK();
-  // records for the data draws (they sort first: aug draws carry the sentinel key)
-  k_c4_records<<<(unsigned)ceil_div<unsigned long long>(s, 256ULL), 256, 0, st>>>(keys_s, vals_s, w,
-                                                                                s, I3, j3s, w2s);
+  cb = l.cub_scan_bytes;
+  RTB_CUDA(cub::DeviceScan::ExclusiveSum(l.cub_scan, cb, l.head, l.uid, (int)s, st));
+  k_c4_unique<<<sb, 256, 0, st>>>(l.keys_s, l.vals_s, l.head, l.uid, w, s, l.ukey, l.uc, l.nuniq);
   RTB_LAUNCH_CHECK();
-  // chunk descriptors (<= kQC draws, one bucket each)
-  auto* ccnt = reinterpret_cast<int*>(take((size_t)I2 * 4));
-  auto* cstart = reinterpret_cast<int*>(take((size_t)I2 * 4));
-  auto* nch = reinterpret_cast<int*>(take(64));
-  auto* chunks = reinterpret_cast<int4*>(take(((size_t)s / kQC + (size_t)I2 + 1) * 16));
-  k_c4_chunk_counts<<<ceil_div(I2, 256), 256, 0, st>>>(I2, counts, ccnt);
+  k_c4_bounds<<<sb, 256, 0, st>>>(l.ukey, l.nuniq, s, I2, I3, l.bstart);
   RTB_LAUNCH_CHECK();
-  k_c4_scan<<<1, 1024, 0, st>>>(I2, ccnt, cstart);
+  if (data_draws_dev)
+    RTB_CUDA(cudaMemcpyAsync(data_draws_dev, l.ndata, 8, cudaMemcpyDeviceToDevice, st));
+  if (unique_dev) RTB_CUDA(cudaMemcpyAsync(unique_dev, l.nuniq, 8, cudaMemcpyDeviceToDevice, st));
+  if (gram) {
+    double* ct = (double*)take((size_t)I3 * I2 * 8);
+    double* ka3 = (double*)take((size_t)I3 * R3 * R3 * 8);
+    double* ka2 = (double*)take((size_t)I2 * R2 * R2 * 8);
+    double* tm = (double*)take((size_t)I2 * R3 * R3 * 8);
+    double* gp = (double*)take((size_t)R2 * R2 * R3 * R3 * 8);
+    RTB_CUDA(cudaMemsetAsync(ct, 0, (size_t)I3 * I2 * 8, st));
+    k_c4_scatter<<<sb, 256, 0, st>>>(l.ukey, l.uc, l.nuniq, I2, I3, ct);
+    RTB_LAUNCH_CHECK();
+    k_c4_kr<<<(unsigned)ceil_div<long long>((long long)I3 * R3 * R3, 256LL), 256, 0, st>>>(A3, I3, R3, ka3);
+    RTB_LAUNCH_CHECK();
+    k_c4_kr<<<(unsigned)ceil_div<long long>((long long)I2 * R2 * R2, 256LL), 256, 0, st>>>(A2, I2, R2, ka2);
+    RTB_LAUNCH_CHECK();
+    const int r2 = R2 * R2, r3 = R3 * R3;
+    // T (I2 x r3) = C KA3: out[j2][(q,q')] = sum_j3 CT[j3][j2] KA3[j3][(q,q')]
+    gemm_tn(ct, I2, ka3, r3, I2, r3, I3, tm, r3, st);
+    // G' (r2 x r3) = KA2^T T
+    gemm_tn(ka2, r2, tm, r3, r2, r3, I2, gp, r3, st);
+    GramSpec gs{};
+    gs.s = s;
+    gs.d = W;
+    gs.lambda = lambda;
+    k_c4_gram_out<<<(unsigned)ceil_div<long long>((long long)W * W, 256LL), 256, 0, st>>>(
+        gp, R2, R3, l.astart, gram_aug_term(gs), gram);
+    RTB_LAUNCH_CHECK();
+  }
+  if (ev_gram_done) RTB_CUDA(cudaEventRecord(ev_gram_done, st));
+  if (!(x && rhs)) return;
+  k_c4_rows<<<kNumSMs * 8, 256, 0, st>>>(l.ukey, l.uc, l.nuniq, I3, A3, R3, l.rows);
   RTB_LAUNCH_CHECK();
-  k_c4_total<<<1, 1, 0, st>>>(I2, ccnt, cstart, nch);
-  RTB_LAUNCH_CHECK();
-  k_c4_chunks<<<ceil_div(I2, 256), 256, 0, st>>>(I2, start, counts, cstart, chunks);
-  RTB_LAUNCH_CHECK();
-  const size_t smem = (size_t)2 * kQC * kQLDT * 8 + (size_t)2 * kQC * kQLDB * 4 +
-                      (size_t)2 * kQC * 8 + (size_t)2 * kQC * 4 + (2 * 32 * 17 + 32) * 8;
   static bool attr = false;
   if (!attr) {
-    RTB_CUDA(cudaFuncSetAttribute(k_c4_fiber_rhs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024));
+    RTB_CUDA(cudaFuncSetAttribute(k_c4_dfib<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kDfibSmem));
+    RTB_CUDA(cudaFuncSetAttribute(k_c4_dfib<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kDfibSmem));
+    RTB_CUDA(cudaFuncSetAttribute(k_c4_dfib<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kDfibSmem));
     attr = true;
   }
-  k_c4_fiber_rhs<<<ceil_div(I1, kC4Tile), 512, smem, st>>>(x, I1, I2, I3, A2, R2, A3, R3, j3s,
-                                                             w2s, chunks, nch, rhs);
+  auto kern = !fiber_major ? k_c4_dfib<0> : (I1 % 4 == 0 ? k_c4_dfib<1> : k_c4_dfib<2>);
+  const long long nitems = (long long)I2 * ceil_div(I1, kDT);
+  const int grid = (int)std::min<long long>(nitems, 2LL * kNumSMs);
+  kern<<<grid, 256, kDfibSmem, st>>>(x, I1, I2, I3, R3, l.ukey, l.rows, l.bstart, l.dfib);
   RTB_LAUNCH_CHECK();
+  // RHS (R2 x R3 I1) = A2^T D
+  const long long n = (long long)R3 * I1;
+  gemm_tn(A2, R2, l.dfib, n, R2, n, I2, rhs, n, st);
 }
 
 }  // namespace rtb

@@ -105,13 +105,19 @@ void factor_sketch_normal_eq(const FactorSketchSpec& spec, const unsigned long l
                              const double* w, void* work, double* gram, double* M,
                              cudaStream_t st);
 
-// ---- k_c4.cu: fiber RHS of the C4 microbench ----
-size_t c4_fiber_work_bytes(unsigned long long s, int I2);
-// rhs (R2 R3 x I1) = sum over data draws of w^2 (a2 (x) a3) X[:, j2, j3]^T (X FP32, I1 x I2 x I3)
-void c4_fiber_rhs(const float* x, int I1, int I2, int I3, const double* A2, int R2,
-                  const double* A3, int R3, const unsigned long long* idx, const double* w,
-                  unsigned long long s, void* work, size_t work_bytes, double* rhs,
-                  cudaStream_t st);
+// ---- k_c4.cu: BASELINE config-4 microbench (Kronecker sampling + fused fiber gather/SYRK) ----
+size_t c4_work_bytes(unsigned long long s, int I1, int I2, int I3, int R2, int R3, bool gram);
+// canonical row-major I1 x I2 x I3 -> fiber-major (mode 1 fastest: out[(i2 I3 + i3) I1 + i1])
+void c4_to_fiber_major(const float* x, int I1, int I2, int I3, float* out, cudaStream_t st);
+// From draws (idx, w) of [A2 (x) A3; sqrt(lambda) I]: gram (W x W, W = R2 R3, if non-null) and
+// rhs (W x I1, if x and rhs are non-null) = sum over data draws of w^2 (a2 (x) a3) X[:, j2, j3]^T.
+// X is FP32, canonical or fiber-major. *data_draws_dev / *unique_dev (optional): data draws and
+// distinct sampled rows. ev_gram_done (optional) is recorded after the Gram.
+void c4_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const double* A2, int R2,
+               const double* A3, int R3, const unsigned long long* idx, const double* w,
+               unsigned long long s, double lambda, void* work, size_t work_bytes, double* gram,
+               double* rhs, unsigned long long* data_draws_dev, unsigned long long* unique_dev,
+               cudaEvent_t ev_gram_done, cudaStream_t st);
 
 // ---- k_gram.cu ----
 struct GramSpec {

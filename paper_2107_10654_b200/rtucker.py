@@ -147,9 +147,10 @@ def _load() -> C.CDLL:
                                        C.c_uint64, C.c_uint64, _u64p, _f64p]),
         "rtucker_b200_kron_normal_eq": (S, [C.c_uint32, _u64p, _u64p, _f64p, _f64p, C.c_double,
                                             C.c_uint64, _u64p, _f64p, _f64p, _f64p]),
-        "rtucker_b200_kron_fiber_sketch": (S, [_vp, _u64p, _vp, _vp, C.c_uint32, C.c_uint32,
-                                               C.c_double, C.c_uint64, C.c_uint64, _vp, _vp,
-                                               _u64p, _f64p, _u64p, _f64p]),
+        "rtucker_b200_kron_fiber_sketch": (S, [_vp, _u64p, C.c_uint32, _vp, _vp, C.c_uint32,
+                                               C.c_uint32, C.c_double, C.c_uint64, C.c_uint64,
+                                               _vp, _vp, _u64p, _f64p, _u64p, _u64p, _f64p]),
+        "rtucker_b200_tensor_fiber_major": (S, [_vp, _u64p, _vp]),
         "rtucker_b200_spd_solve": (S, [_f64p, _f64p, C.c_uint64, _f64p, _u64p,
                                        C.POINTER(C.c_int)]),
         "rtucker_b200_update_core_sketched": (S, [_vp, _vp, C.c_uint64, C.c_uint64, _f64p, _u64p,
@@ -568,23 +569,32 @@ def kron_normal_eq(shape, ranks, factors, x, lam, idx, w):
 
 
 def kron_fiber_sketch(x_ptr, shape, a2_ptr, a3_ptr, r2, r3, lam, s, seed, gram_ptr=None,
-                      rhs_ptr=None, want_draws=False):
+                      rhs_ptr=None, want_draws=False, fiber_major=False):
     """BASELINE C4 microbench on device pointers (rtucker_b200_kron_fiber_sketch):
-    X (I1 x I2 x I3 FP32), A2 (I2 x r2), A3 (I3 x r3) FP64; gram (W x W) and rhs (W x I1)
-    FP64 outputs, W = r2 r3. Returns {data_draws, phase_ms, [indices, weights]}."""
+    X (I1 x I2 x I3 FP32; canonical row-major, or fiber-major when fiber_major), A2 (I2 x r2),
+    A3 (I3 x r3) FP64; gram (W x W) and rhs (W x I1) FP64 outputs, W = r2 r3.
+    Returns {data_draws, unique_rows, phase_ms, [indices, weights]}."""
     shape = _u64(shape)
     idx = np.zeros(s, np.uint64) if want_draws else None
     w = np.zeros(s) if want_draws else None
-    nd = C.c_uint64()
+    nd, nu = C.c_uint64(), C.c_uint64()
     ms = np.zeros(3)
     _check(lib.rtucker_b200_kron_fiber_sketch(
-        C.c_void_p(x_ptr or 0), _p(shape), C.c_void_p(a2_ptr), C.c_void_p(a3_ptr), r2, r3, lam, s,
-        seed, C.c_void_p(gram_ptr or 0), C.c_void_p(rhs_ptr or 0),
-        _p(idx) if want_draws else None, _p(w) if want_draws else None, C.byref(nd), _p(ms)))
-    out = {"data_draws": nd.value, "phase_ms": ms.tolist()}
+        C.c_void_p(x_ptr or 0), _p(shape), 1 if fiber_major else 0, C.c_void_p(a2_ptr),
+        C.c_void_p(a3_ptr), r2, r3, lam, s, seed, C.c_void_p(gram_ptr or 0),
+        C.c_void_p(rhs_ptr or 0), _p(idx) if want_draws else None, _p(w) if want_draws else None,
+        C.byref(nd), C.byref(nu), _p(ms)))
+    out = {"data_draws": nd.value, "unique_rows": nu.value, "phase_ms": ms.tolist()}
     if want_draws:
         out["indices"], out["weights"] = idx, w
     return out
+
+
+def tensor_fiber_major(x_ptr, shape, out_ptr):
+    """Fiber-major copy (mode 1 fastest) of a device FP32 I1 x I2 x I3 tensor
+    (rtucker_b200_tensor_fiber_major)."""
+    shape = _u64(shape)
+    _check(lib.rtucker_b200_tensor_fiber_major(C.c_void_p(x_ptr), _p(shape), C.c_void_p(out_ptr)))
 
 
 def spd_solve(g, rhs):

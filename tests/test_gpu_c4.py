@@ -8,21 +8,30 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("fm", [False, True])
 @pytest.mark.parametrize("I1,I2,I3,R2,R3,s", [(48, 40, 36, 4, 4, 3000),
                                                (32, 64, 50, 8, 5, 20000),
-                                               (40, 20, 24, 3, 7, 500)])
-def test_c4_gram_rhs_match_definition(rt, oracle, I1, I2, I3, R2, R3, s):
+                                               (40, 20, 24, 3, 7, 500),
+                                               (37, 9, 11, 3, 2, 5000),
+                                               (70, 33, 35, 32, 32, 40000)])
+def test_c4_gram_rhs_match_definition(rt, oracle, fm, I1, I2, I3, R2, R3, s):
     import torch
     g = torch.Generator(device="cuda").manual_seed(3)
     x = torch.randn(I1, I2, I3, dtype=torch.float32, device="cuda", generator=g)
+    xk = x
+    if fm:  # fiber-major copy: mode 1 fastest
+        xk = torch.empty_like(x)
+        rt.tensor_fiber_major(x.data_ptr(), (I1, I2, I3), xk.data_ptr())
+        assert torch.equal(xk.view(I2, I3, I1), x.permute(1, 2, 0))
     a2 = torch.randn(I2, R2, dtype=torch.float64, device="cuda", generator=g)
     a3 = torch.randn(I3, R3, dtype=torch.float64, device="cuda", generator=g)
     W = R2 * R3
     gram = torch.zeros(W, W, dtype=torch.float64, device="cuda")
     rhs = torch.zeros(W, I1, dtype=torch.float64, device="cuda")
     lam = 1e-2
-    out = rt.kron_fiber_sketch(x.data_ptr(), (I1, I2, I3), a2.data_ptr(), a3.data_ptr(), R2, R3,
-                               lam, s, 11, gram.data_ptr(), rhs.data_ptr(), want_draws=True)
+    out = rt.kron_fiber_sketch(xk.data_ptr(), (I1, I2, I3), a2.data_ptr(), a3.data_ptr(), R2, R3,
+                               lam, s, 11, gram.data_ptr(), rhs.data_ptr(), want_draws=True,
+                               fiber_major=fm)
     torch.cuda.synchronize()
     idx, w = out["indices"], out["weights"]
     A2, A3, X = a2.cpu().numpy(), a3.cpu().numpy(), x.cpu().numpy().astype(np.float64)
@@ -38,6 +47,8 @@ def test_c4_gram_rhs_match_definition(rt, oracle, I1, I2, I3, R2, R3, s):
     total = I2 * I3
     data = idx < total
     assert out["data_draws"] == int(data.sum())
+    # distinct sampled rows (equal draws are merged into one record, weights summed)
+    assert out["unique_rows"] == len(np.unique(idx[data]))
     j2, j3 = idx[data] // I3, idx[data] % I3
     Z = np.einsum("tp,tq->tpq", A2[j2], A3[j3]).reshape(-1, W)
     wd = w[data]
@@ -65,3 +76,27 @@ def test_c4_gram_only_and_validation(rt):
     assert out["data_draws"] > 0 and torch.isfinite(gram).all()
     with pytest.raises(rt.RtuckerError):
         rt.kron_fiber_sketch(None, (8, I2, I3), a2.data_ptr(), a3.data_ptr(), 40, R, 1e-2, 10, 1)
+
+
+def test_c4_rhs_only_and_layouts_agree(rt):
+    """RHS without the Gram; canonical and fiber-major X give bitwise-equal RHS (same
+    records, same summation order) and the draws are deterministic per seed."""
+    import torch
+    I1, I2, I3, R = 64, 48, 40, 8
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(I1, I2, I3, dtype=torch.float32, device="cuda", generator=g)
+    xf = torch.empty_like(x)
+    rt.tensor_fiber_major(x.data_ptr(), (I1, I2, I3), xf.data_ptr())
+    a2 = torch.randn(I2, R, dtype=torch.float64, device="cuda", generator=g)
+    a3 = torch.randn(I3, R, dtype=torch.float64, device="cuda", generator=g)
+    r0 = torch.zeros(R * R, I1, dtype=torch.float64, device="cuda")
+    r1 = torch.zeros_like(r0)
+    o0 = rt.kron_fiber_sketch(x.data_ptr(), (I1, I2, I3), a2.data_ptr(), a3.data_ptr(), R, R,
+                              1e-2, 30000, 9, None, r0.data_ptr())
+    o1 = rt.kron_fiber_sketch(xf.data_ptr(), (I1, I2, I3), a2.data_ptr(), a3.data_ptr(), R, R,
+                              1e-2, 30000, 9, None, r1.data_ptr(), fiber_major=True)
+    torch.cuda.synchronize()
+    assert o0["data_draws"] == o1["data_draws"] > 0
+    assert o0["unique_rows"] == o1["unique_rows"] > 0
+    assert torch.equal(r0, r1)
+    assert torch.count_nonzero(r0) > 0

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "lib", "librtucker_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["k_small.cu", "k_ttm.cu", "k_draw.cu", "k_gram.cu", "k_chol.cu", "k_pcg.cu", "k_fsketch.cu", "k_c4.cu", "engine.cu",
+SOURCES = ["k_small.cu", "k_ttm.cu", "k_draw.cu", "k_gram.cu", "k_chol.cu", "k_pcg.cu", "k_fsketch.cu", "k_c4.cu", "k_pinv.cu", "engine.cu",
            "capi.cu"]
 FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
@@ -59,7 +59,7 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
         raise RuntimeError("nvcc failed")
     objs = [os.path.join(OBJ, s.replace(".cu", ".o")) for s in SOURCES]
     if _needs(LIB, objs):
-        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs
+        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)

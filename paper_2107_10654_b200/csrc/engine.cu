@@ -620,6 +620,7 @@ class Engine {
   DevBuf T_, P_, tmp_a_, tmp_b_, partial_, scal_, hist_, init_loss_, xx_, loss_need_, yq_;
   bool xx_valid_ = false;
   DevBuf scores_, cdf_, sums_, score_off_, rows_dev_, cols_dev_, flag_;
+  DevBuf pinv_work_, pinv_rank_;
   DevBuf sk_idx_, sk_w_, draw_work_, gram_work_, G_, rhs_, chol_work_, chol_status_,
       data_draws_, zero_flag_, U_[8], pgram_, pcg_work_, pcg_status_, blocks_, pev_, pvec_, pst_;
   uint64_t sketch_rng_ = 0, sketch_k_ = 0;
@@ -1207,10 +1208,22 @@ class Engine {
     }
     if (status[0]) {
       // not positive definite: recompute the Gram and take the pinv route
-      if (d_ > 64)
-        throw Error(3, "sketched Gram is not positive definite (d > 64 pinv fallback "
-                       "not available)");
       normal_eq(true);  // Cholesky overwrote G and rhs: rebuild them
+      if (d_ > 64) {  // dense eigen pinv with the reference cutoff (k_pinv.cu)
+        Scope sc(prof_, "pinv");
+        pinv_work_.ensure(pinv_large_work_bytes((int)d_), st_);
+        pinv_rank_.ensure(4, st_);
+        pinv_solve_large(G_.as<double>(), (int)d_, rhs_.as<double>(), core_.as<double>(),
+                         pinv_rank_.as<int>(), pinv_work_.p, pinv_work_.bytes, st_);
+        int rank = 0;
+        RTB_CUDA(cudaMemcpyAsync(&rank, pinv_rank_.p, 4, cudaMemcpyDeviceToHost, st_));
+        RTB_CUDA(cudaStreamSynchronize(st_));
+        last_solver_path_ = 1;
+        last_rank_deficient_ = rank < (int)d_;
+        warm_core_ = false;
+        check_core_finite();
+        return;
+      }
       eigen_one(G_.as<double>(), (int)d_);
       double* pv = tmp_a_.as<double>();
       k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one((int)d_),
@@ -1895,9 +1908,15 @@ static void solve_sym_device(double* G, double* rhs, int d, double* x_dev, int* 
     *path = 0;
     return;
   }
-  if (d > 64) {
-    if (need_spd_else_error)
-      throw Error(3, "matrix is not positive definite (pinv fallback limited to d <= 64)");
+  if (d > 64) {  // dense eigen pinv (k_pinv.cu) on a fresh copy of G
+    (void)need_spd_else_error;
+    RTB_CUDA(cudaMemcpyAsync(copy.p, G, (size_t)d * d * 8, cudaMemcpyDeviceToDevice, st));
+    DevBuf pw(pinv_large_work_bytes(d), st), rk(4, st);
+    pinv_solve_large(copy.as<double>(), d, rhs, x_dev, rk.as<int>(), pw.p, pw.bytes, st);
+    RTB_CUDA(cudaMemcpyAsync(rank, rk.p, 4, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaStreamSynchronize(st));
+    *path = 1;
+    return;
   }
   DevBuf ev((size_t)d * d * 8 + 8, st), evec((size_t)d * d * 8, st), es(4, st), ns(4, st),
       pv((size_t)d * d * 8, st), rk(4, st);

@@ -184,6 +184,12 @@ bool pcg_supported(int d, int order, const int* ranks);
 void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, double* x, void* work,
                int* status_dev, cudaStream_t st);
 
+// ---- k_pinv.cu: x = G^+ b (d > 64), reference cutoff d eps max|mu| ----
+size_t pinv_large_work_bytes(int d);
+// G (d x d symmetric, device) is overwritten; *rank_dev = number of kept eigenpairs
+void pinv_solve_large(double* G, int d, const double* b, double* x, int* rank_dev, void* work,
+                      size_t work_bytes, cudaStream_t st);
+
 // ---- k_chol.cu ----
 size_t chol_work_bytes(int d);
 // In-place Cholesky of the lower triangle of a (d x d, row-major) and solve

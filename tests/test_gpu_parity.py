@@ -144,6 +144,28 @@ def test_spd_solve_rank_deficient_small(oracle, rt):
     assert np.linalg.norm(gx - ox) / np.linalg.norm(ox) < 1e-9
 
 
+@pytest.mark.parametrize("d,r", [(100, 60), (150, 150)])
+def test_spd_solve_rank_deficient_large(oracle, rt, d, r):
+    """d > 64 pinv fallback (k_pinv.cu): rank-deficient PSD Gram, checked against the
+    oracle's Jacobi-SVD pinv with the reference cutoff (ref linalg.cpp:8-26, svd.cpp:92-97);
+    (150, 150): a full-rank indefinite symmetric matrix (Cholesky fails; the SVD pinv keeps
+    the negative eigenvalues as singular values |mu|)."""
+    rng = np.random.default_rng(d + r)
+    q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    ev = np.zeros(d)
+    ev[:r] = np.logspace(2, -2, r)
+    if r == d:
+        ev[-5:] = -np.logspace(-1, -3, 5)
+    g = (q * ev) @ q.T
+    g = 0.5 * (g + g.T)
+    b = rng.standard_normal(d)
+    ox, orank = oracle.pinv_solve(g, b)
+    gx, grank, path = rt.spd_solve(g, b)
+    assert path == 1
+    assert grank == orank
+    assert np.linalg.norm(gx - ox) / np.linalg.norm(ox) < 1e-9
+
+
 # ---------------------------------------------------------------- model steps
 CASES = [((12, 10, 8), (3, 2, 4), 0.01), ((30, 30, 30), (4, 4, 4), 1e-3),
          ((9, 8, 7, 6), (2, 3, 2, 2), 0.05), ((40, 35), (5, 4), 1e-2), ((50,), (4,), 1e-2)]

@@ -557,6 +557,64 @@ def run_c4(args):
     return 0
 
 
+def run_c3(args):
+    """BASELINE config 3 (--workload c3): dense 4-way FP64 160^4 (5.2 GB), planted rank
+    (10,10,10,10) with coherent factors (rows scaled by i.i.d. Pareto(1.5) weights), 5% noise,
+    lambda = 0.1, s_core = 500,000; one line with exact factor updates (reference semantics)
+    and one with sketched factor updates (50,000 samples, perf mode). Seeded synthetic data on
+    the device; K sweeps timed with CUDA events after the warm-up sweeps."""
+    import torch
+    from paper_2107_10654_b200 import rtucker as rt
+    torch.cuda.set_device(0)
+    rt.set_stream(torch.cuda.current_stream().cuda_stream)
+    I, R, lam, s = 160, 10, 0.1, 500000
+    shape, ranks = (I,) * 4, (R,) * 4
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(ranks, dtype=torch.float64, device="cuda", generator=g)
+    for n in range(4):
+        f = torch.randn(I, R, dtype=torch.float64, device="cuda", generator=g)
+        u = torch.rand(I, 1, dtype=torch.float64, device="cuda", generator=g)
+        f = f * (1.0 - u) ** (-1.0 / 1.5)  # Pareto(alpha = 1.5) row weights
+        x = torch.movedim(torch.tensordot(f, x, dims=([1], [n])), 0, n)
+    x = x + 0.05 * x.norm() / x.numel() ** 0.5 * torch.randn(x.shape, dtype=torch.float64,
+                                                               device="cuda", generator=g)
+    x = x.contiguous()
+    torch.cuda.synchronize()
+    t = rt.Tensor.from_device(x.data_ptr(), shape)
+    for fs in (0, 50000):
+        opts = rt.options(lam=lam, sketched_core=1, sample_count_override=s, tolerance=0.0,
+                          max_iterations=args.warmup + args.steps + 1)
+        sess = rt.Session(t, ranks, opts, profile=True, factor_samples=fs)
+        sess.sweeps(args.warmup)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        sess.sweeps(args.steps)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        r = sess.result()
+        fam = {}
+        for name, secs, n in r.kernels():
+            fam[name] = fam.get(name, 0.0) + secs
+        tot = sum(fam.values()) or 1.0
+        line = {
+            "metric": "sketched Tucker-ALS sweeps/s (C3)", "value": 1e3 / ms, "unit": "sweeps/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "dtype": "f64", "data": "synthetic (seeded torch)",
+            "config": {"workload": "C3: dense 4-way FP64 160^4 (5.2 GB), planted rank (10,10,10,10), "
+                                   "Pareto(1.5)-scaled factor rows, 5% noise, lambda=0.1, "
+                                   "s_core=500,000",
+                       "factor_updates": "exact" if fs == 0 else f"sketched ({fs} samples)",
+                       "final_loss": r.final_loss},
+            "sketch": r.sketch_info(),
+            "kernel_share": {k: round(v / tot, 4) for k, v in sorted(fam.items(),
+                                                                    key=lambda kv: -kv[1])[:8]},
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -564,9 +622,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
-                    help="c2 (default): the headline ALS sweep; c4: the BASELINE config-4 "
-                         "sampling + fiber gather/SYRK microbench")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
+                    help="c2 (default): the headline ALS sweep; c3: the BASELINE config-3 "
+                         "4-way Pareto-factor sweep; c4: the BASELINE config-4 sampling + "
+                         "fiber gather/SYRK microbench")
     ap.add_argument("--c4-s", default="1e5,1e6,1e7", help="sample counts for --workload c4")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -575,6 +634,8 @@ def main():
         return run_reference_arm(args)
     if args.workload == "c4":
         return run_c4(args)
+    if args.workload == "c3":
+        return run_c3(args)
     return run_our_arm(args)
 
 

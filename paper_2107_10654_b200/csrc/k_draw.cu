@@ -11,8 +11,10 @@
 //   1. k_draw_submaps: for every sub-chunk of SUB stream positions and every
 //      possible entry offset e < L (L = longest rejection-free draw) simulate
 //      the draw boundaries inside the sub-chunk -> exit offset + draw count;
-//   2. k_draw_scan:    one CTA composes these small maps with a block scan and
-//      fixes each sub-chunk's true entry offset and first draw id;
+//   2. k_draw_group / k_draw_scan / k_draw_fix: the small maps are composed per
+//      group of GS sub-chunks (walks in shared memory), one CTA composes the group
+//      maps with a block scan, then each group re-walks its sub-chunks from its true
+//      entry: every sub-chunk's entry offset and first draw id;
 //   3. k_draw_emit:    each sub-chunk re-walks from its true entry and records
 //      the stream position of each of its draws;
 //   4. k_draw_eval:    one thread per draw evaluates it exactly as the
@@ -44,8 +46,15 @@ __device__ __forceinline__ long long step_at(const StreamCfg& c, long long pos) 
   return q + 1 - pos;
 }
 
+constexpr int GS = 16;   // sub-chunks per group (first level of the map composition)
+constexpr int GCTA = 64;   // groups (threads) per CTA in k_draw_group / k_draw_fix
+
 struct Layout {
-  long long nsub;
+  long long nsub, ngrp;
+  unsigned char* gexit;  // [ngrp][L] composed group maps
+  int* gcnt;             // [ngrp][L]
+  int* gentry;           // [ngrp]
+  long long* gbase;      // [ngrp]
   unsigned char* exitm;  // [nsub][L]
   unsigned short* cnt;   // [nsub][L]
   int* entry;            // [nsub]
@@ -59,6 +68,7 @@ Layout layout(const DrawSpec& spec, void* base) {
   const long long positions = (long long)spec.s * (spec.order + 1) + 2 * SUB;
   Layout l;
   l.nsub = ceil_div<long long>(positions, SUB);
+  l.ngrp = ceil_div<long long>(l.nsub, GS);
   char* p = static_cast<char*>(base);
   auto take = [&](size_t bytes) {
     char* r = p;
@@ -71,6 +81,10 @@ Layout layout(const DrawSpec& spec, void* base) {
   l.base = reinterpret_cast<long long*>(take(l.nsub * sizeof(long long)));
   l.start = reinterpret_cast<long long*>(take(spec.s * sizeof(long long)));
   l.overflow = reinterpret_cast<int*>(take(sizeof(int)));
+  l.gexit = reinterpret_cast<unsigned char*>(take(l.ngrp * L));
+  l.gcnt = reinterpret_cast<int*>(take(l.ngrp * L * sizeof(int)));
+  l.gentry = reinterpret_cast<int*>(take(l.ngrp * sizeof(int)));
+  l.gbase = reinterpret_cast<long long*>(take(l.ngrp * sizeof(long long)));
   return l;
 }
 }  // namespace
@@ -87,6 +101,11 @@ size_t draw_work_bytes(const DrawSpec& spec) {
   add(nsub * sizeof(long long));
   add(spec.s * sizeof(long long));
   add(sizeof(int));
+  const long long ngrp = ceil_div<long long>(nsub, GS);
+  add(ngrp * L);
+  add(ngrp * L * sizeof(int));
+  add(ngrp * sizeof(int));
+  add(ngrp * sizeof(long long));
   return b;
 }
 
@@ -113,10 +132,50 @@ __global__ void k_draw_submaps(StreamCfg c, int L, long long nsub, unsigned char
   cnt[e] = (unsigned short)n;
 }
 
-// Single CTA of 1024 threads: compose sub-chunk maps, fix entries and draw ids.
+// Stage the sub-chunk maps of GCTA groups (GCTA * GS sub-chunks) in shared memory, so the
+// per-group walks below are chains of shared-memory loads, not of global loads.
+__device__ __forceinline__ long long stage_maps(int L, long long nsub, const unsigned char* exitm,
+                                                const unsigned short* cnt, unsigned char* sx,
+                                                unsigned short* sc) {
+  const long long j0 = (long long)blockIdx.x * GCTA * GS;
+  const long long n = min((long long)GCTA * GS, nsub - j0) * L;
+  for (long long e = threadIdx.x; e < n; e += blockDim.x) {
+    sx[e] = exitm[j0 * L + e];
+    sc[e] = cnt[j0 * L + e];
+  }
+  __syncthreads();
+  return j0;
+}
+
+// First level: compose the maps of each group of GS sub-chunks (thread = group).
+__global__ void __launch_bounds__(GCTA) k_draw_group(int L, long long nsub, long long ngrp,
+                                                     const unsigned char* exitm,
+                                                     const unsigned short* cnt,
+                                                     unsigned char* gexit, int* gcnt) {
+  __shared__ unsigned char sx[GCTA * GS * LMAX];
+  __shared__ unsigned short sc[GCTA * GS * LMAX];
+  const long long j0 = stage_maps(L, nsub, exitm, cnt, sx, sc);
+  const long long g = (long long)blockIdx.x * GCTA + threadIdx.x;
+  if (g >= ngrp) return;
+  const int k0 = threadIdx.x * GS, k1 = (int)min((long long)k0 + GS, nsub - j0);
+  for (int e = 0; e < L; ++e) {
+    int cur = e, n = 0;
+    for (int k = k0; k < k1; ++k) {
+      n += sc[k * L + cur];
+      cur = sx[k * L + cur];
+    }
+    gexit[g * L + e] = (unsigned char)cur;
+    gcnt[g * L + e] = n;
+  }
+}
+
+// Single CTA of 1024 threads: compose the group maps with a block scan and fix each
+// group's true entry offset and first draw id.
+// (CT = unsigned short: applied to the sub-chunk maps directly, when there are few)
+template <typename CT>
 __global__ void __launch_bounds__(1024) k_draw_scan(StreamCfg c, int L, long long nsub,
-                                                   const unsigned char* exitm,
-                                                   const unsigned short* cnt, int* entry,
+                                                   long long ngrp, const unsigned char* gexit,
+                                                   const CT* gcnt, int* gentry, long long* gbase,
                                                    long long* base, const int* overflow,
                                                    long long* start, long long s) {
   __shared__ unsigned char mx[1024][LMAX];
@@ -134,17 +193,17 @@ __global__ void __launch_bounds__(1024) k_draw_scan(StreamCfg c, int L, long lon
     }
     return;
   }
-  const long long per = ceil_div<long long>(nsub, 1024);
-  const long long j0 = tid * per, j1 = min(nsub, j0 + per);
-  // this thread's composed map over [j0, j1)
+  const long long per = ceil_div<long long>(ngrp, 1024);
+  const long long j0 = tid * per, j1 = min(ngrp, j0 + per);
+  // this thread's composed map over groups [j0, j1)
   unsigned char fx[LMAX];
   long long fc[LMAX];
   for (int e = 0; e < L; ++e) {
     int cur = e;
     long long n = 0;
     for (long long j = j0; j < j1; ++j) {
-      n += cnt[j * L + cur];
-      cur = exitm[j * L + cur];
+      n += gcnt[j * L + cur];
+      cur = gexit[j * L + cur];
     }
     fx[e] = (unsigned char)cur;
     fc[e] = n;
@@ -177,10 +236,33 @@ __global__ void __launch_bounds__(1024) k_draw_scan(StreamCfg c, int L, long lon
   int cur = tid == 0 ? 0 : mx[tid - 1][0];
   long long n = tid == 0 ? 0 : mc[tid - 1][0];
   for (long long j = j0; j < j1; ++j) {
-    entry[j] = cur;
-    base[j] = n;
-    n += cnt[j * L + cur];
-    cur = exitm[j * L + cur];
+    gentry[j] = cur;
+    gbase[j] = n;
+    n += gcnt[j * L + cur];
+    cur = gexit[j * L + cur];
+  }
+}
+
+// Second level: each group walks its GS sub-chunks from its true entry (thread = group).
+__global__ void __launch_bounds__(GCTA) k_draw_fix(int L, long long nsub, long long ngrp,
+                                                   const unsigned char* exitm,
+                                                   const unsigned short* cnt, const int* gentry,
+                                                   const long long* gbase, const int* overflow,
+                                                   int* entry, long long* base) {
+  __shared__ unsigned char sx[GCTA * GS * LMAX];
+  __shared__ unsigned short sc[GCTA * GS * LMAX];
+  if (*overflow) return;
+  const long long j0 = stage_maps(L, nsub, exitm, cnt, sx, sc);
+  const long long g = (long long)blockIdx.x * GCTA + threadIdx.x;
+  if (g >= ngrp) return;
+  const int k0 = threadIdx.x * GS, k1 = (int)min((long long)k0 + GS, nsub - j0);
+  int cur = gentry[g];
+  long long n = gbase[g];
+  for (int k = k0; k < k1; ++k) {
+    entry[j0 + k] = cur;
+    base[j0 + k] = n;
+    n += sc[k * L + cur];
+    cur = sx[k * L + cur];
   }
 }
 
@@ -265,9 +347,22 @@ void draw_sketch(const DrawSpec& spec, const double* scores, const double* cdfs,
   k_draw_submaps<<<(unsigned)ceil_div<long long>(n1, 256), 256, 0, st>>>(c, L, l.nsub, l.exitm,
                                                                        l.cnt, l.overflow);
   RTB_LAUNCH_CHECK();
-  k_draw_scan<<<1, 1024, 0, st>>>(c, L, l.nsub, l.exitm, l.cnt, l.entry, l.base, l.overflow,
-                                  l.start, (long long)spec.s);
-  RTB_LAUNCH_CHECK();
+  if (l.nsub <= 8 * 1024) {  // few sub-chunks: one scan CTA composes them directly
+    k_draw_scan<unsigned short><<<1, 1024, 0, st>>>(c, L, l.nsub, l.nsub, l.exitm, l.cnt, l.entry,
+                                                    l.base, l.base, l.overflow, l.start,
+                                                    (long long)spec.s);
+    RTB_LAUNCH_CHECK();
+  } else {
+    const unsigned gb = (unsigned)ceil_div<long long>(l.ngrp, GCTA);
+    k_draw_group<<<gb, GCTA, 0, st>>>(L, l.nsub, l.ngrp, l.exitm, l.cnt, l.gexit, l.gcnt);
+    RTB_LAUNCH_CHECK();
+    k_draw_scan<int><<<1, 1024, 0, st>>>(c, L, l.nsub, l.ngrp, l.gexit, l.gcnt, l.gentry, l.gbase,
+                                         l.base, l.overflow, l.start, (long long)spec.s);
+    RTB_LAUNCH_CHECK();
+    k_draw_fix<<<gb, GCTA, 0, st>>>(L, l.nsub, l.ngrp, l.exitm, l.cnt, l.gentry, l.gbase,
+                                    l.overflow, l.entry, l.base);
+    RTB_LAUNCH_CHECK();
+  }
   k_draw_emit<<<(unsigned)ceil_div<long long>(l.nsub, 128), 128, 0, st>>>(
       c, l.nsub, l.entry, l.base, l.start, (long long)spec.s);
   RTB_LAUNCH_CHECK();

@@ -69,7 +69,10 @@ def test_factor_scores_zero_factor(rt):
 @pytest.mark.parametrize("shape,ranks,s,seed", [((100, 100, 100), (5, 5, 5), 20000, 7),
                                                  ((30, 20, 10, 8), (3, 2, 4, 2), 5000, 11),
                                                  ((64,), (5,), 3000, 3),
-                                                 ((40, 50), (4, 6), 7777, 99)])
+                                                 ((40, 50), (4, 6), 7777, 99),
+                                                 # > 8192 sub-chunks: two-level map composition
+                                                 ((100, 100, 100), (5, 5, 5), 1000000, 5),
+                                                 ((2048, 2048), (32, 32), 2000000, 1)])
 def test_draws_bit_exact_given_reference_cdfs(oracle, rt, shape, ranks, s, seed):
     rng = np.random.default_rng(seed)
     fs = [rng.random((i, r)) for i, r in zip(shape, ranks)]

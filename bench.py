@@ -525,9 +525,10 @@ def run_c4(args):
     for s in [int(float(v)) for v in args.c4_s.split(",")]:
         (draw_ms, gram_ms, rhs_ms), nd, nu = run(xf.data_ptr(), True, s)
         (_, _, rhs_c_ms), _, _ = run(x.data_ptr(), False, s)
-        # Gram: two DMMA GEMMs over Khatri-Rao row products (T = C KA3, G' = KA2^T T); the
-        # phase also holds the shared sort / merge of the draws
-        gram_flops = 2.0 * I * I * R * R + 2.0 * (R * R) ** 2 * I
+        # Gram: two DMMA GEMMs over vech Khatri-Rao row products (T = C KA3, G' = KA2^T T,
+        # m = R (R + 1) / 2 pair columns); the phase also holds the shared sort / merge
+        m = R * (R + 1) // 2
+        gram_flops = 2.0 * I * I * m + 2.0 * m * m * I
         # RHS: per distinct sampled row 2 R I1 (D_b accumulation), per bucket the a2 (x) D_b fold
         rhs_flops = 2.0 * nu * R * I + 2.0 * I * R * R * I
         fiber_bytes = 4.0 * I * nu                # each distinct FP32 fiber read once

@@ -18,8 +18,9 @@
 //   (B) Gram through a dense record-weight matrix C (I3 x I2, C[j3][j2] = c):
 //         G[(p,q),(p',q')] = sum_{j2} A2[j2,p] A2[j2,p'] T[j2,(q,q')],
 //         T[j2,(q,q')]     = sum_{j3} C[j2,j3] A3[j3,q] A3[j3,q'],
-//       two FP64 DMMA GEMMs (k_gemm_tn) over Khatri-Rao row products, then the permute
-//       into (p,q) order plus the augmented diagonal.
+//       two FP64 DMMA GEMMs (k_gemm_tn) over vech Khatri-Rao row products (unordered
+//       pairs only: 528 of 1024 columns at R = 32), then the expansion into (p,q) order
+//       plus the augmented diagonal.
 //   (C) RHS factored by j2 bucket: D_b = sum_{t in b} c_t a3(j3_t) x_t^T (R3 x I1), 2 R3 I1
 //       flops per record (k_c4_dfib), then RHS = sum_b a2(b) (x) D_b = A2^T D (k_gemm_tn).
 //       The rows c_t a3(j3_t) are pre-scaled into a record-ordered array.
@@ -134,13 +135,14 @@ __global__ void k_c4_scatter(const unsigned long long* __restrict__ ukey, const 
   ct[j3 * (unsigned long long)I2 + j2] = uc[u];
 }
 
-// Khatri-Rao row products: kr[i][(a,b)] = A[i,a] A[i,b]
+// vech Khatri-Rao row products: kr[i][u] = A[i,a] A[i,b], u = vech pair (a <= b)
 __global__ void k_c4_kr(const double* __restrict__ A, int I, int R, double* __restrict__ kr) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long RR = (long long)R * R;
-  if (e >= (long long)I * RR) return;
-  const long long i = e / RR;
-  const int ab = (int)(e % RR), a = ab / R, b = ab % R;
+  const int m = R * (R + 1) / 2;
+  if (e >= (long long)I * m) return;
+  const long long i = e / m;
+  int a, b;
+  pair_of((int)(e % m), R, a, b);
   kr[e] = A[i * R + a] * A[i * R + b];
 }
 
@@ -229,7 +231,8 @@ void gemm_tn(const double* A, long long lda, const double* B, long long ldb, int
   RTB_LAUNCH_CHECK();
 }
 
-// G[(p,q),(p',q')] = G'[(p,p'),(q,q')] + [p = p', q = q'] (augmented draws of (p,q)) aug_term
+// G[(p,q),(p',q')] = G'[v(p,p')][v(q,q')] + [p = p', q = q'] (augmented draws of (p,q)) aug_term
+// (G' over vech pairs: the Gram of Kronecker rows depends on the unordered index pairs)
 __global__ void k_c4_gram_out(const double* __restrict__ gp, int R2, int R3,
                               const int* __restrict__ astart, double aug_term,
                               double* __restrict__ gram) {
@@ -238,7 +241,10 @@ __global__ void k_c4_gram_out(const double* __restrict__ gp, int R2, int R3,
   if (e >= W * W) return;
   const long long r = e / W, col = e % W;
   const int p = (int)(r / R3), q = (int)(r % R3), pp = (int)(col / R3), qq = (int)(col % R3);
-  double v = gp[((long long)p * R2 + pp) * ((long long)R3 * R3) + (long long)q * R3 + qq];
+  const int m3 = R3 * (R3 + 1) / 2;
+  const int u2 = p <= pp ? upper_pair(p, pp, R2) : upper_pair(pp, p, R2);
+  const int u3 = q <= qq ? upper_pair(q, qq, R3) : upper_pair(qq, q, R3);
+  double v = gp[(long long)u2 * m3 + u3];
   if (r == col) v += (double)(astart[r + 1] - astart[r]) * aug_term;
   gram[e] = v;
 }
@@ -440,7 +446,7 @@ C4Layout c4_carve(unsigned long long s, int I1, int I2, int R3, int W, F&& take)
 }
 
 size_t gram_part_bytes(int I2, int I3, int R2, int R3) {
-  const size_t r2 = (size_t)R2 * R2, r3 = (size_t)R3 * R3;
+  const size_t r2 = (size_t)R2 * (R2 + 1) / 2, r3 = (size_t)R3 * (R3 + 1) / 2;
   return ((size_t)I3 * I2 + (size_t)I3 * r3 + (size_t)I2 * r2 + (size_t)I2 * r3 + r2 * r3) * 8 +
          5 * 256;
 }
@@ -506,22 +512,22 @@ void c4_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const d
   if (unique_dev) RTB_CUDA(cudaMemcpyAsync(unique_dev, l.nuniq, 8, cudaMemcpyDeviceToDevice, st));
   if (gram) {
     double* ct = (double*)take((size_t)I3 * I2 * 8);
-    double* ka3 = (double*)take((size_t)I3 * R3 * R3 * 8);
-    double* ka2 = (double*)take((size_t)I2 * R2 * R2 * 8);
-    double* tm = (double*)take((size_t)I2 * R3 * R3 * 8);
-    double* gp = (double*)take((size_t)R2 * R2 * R3 * R3 * 8);
+    const int m2 = R2 * (R2 + 1) / 2, m3 = R3 * (R3 + 1) / 2;
+    double* ka3 = (double*)take((size_t)I3 * m3 * 8);
+    double* ka2 = (double*)take((size_t)I2 * m2 * 8);
+    double* tm = (double*)take((size_t)I2 * m3 * 8);
+    double* gp = (double*)take((size_t)m2 * m3 * 8);
     RTB_CUDA(cudaMemsetAsync(ct, 0, (size_t)I3 * I2 * 8, st));
     k_c4_scatter<<<sb, 256, 0, st>>>(l.ukey, l.uc, l.nuniq, I2, I3, ct);
     RTB_LAUNCH_CHECK();
-    k_c4_kr<<<(unsigned)ceil_div<long long>((long long)I3 * R3 * R3, 256LL), 256, 0, st>>>(A3, I3, R3, ka3);
+    k_c4_kr<<<(unsigned)ceil_div<long long>((long long)I3 * m3, 256LL), 256, 0, st>>>(A3, I3, R3, ka3);
     RTB_LAUNCH_CHECK();
-    k_c4_kr<<<(unsigned)ceil_div<long long>((long long)I2 * R2 * R2, 256LL), 256, 0, st>>>(A2, I2, R2, ka2);
+    k_c4_kr<<<(unsigned)ceil_div<long long>((long long)I2 * m2, 256LL), 256, 0, st>>>(A2, I2, R2, ka2);
     RTB_LAUNCH_CHECK();
-    const int r2 = R2 * R2, r3 = R3 * R3;
-    // T (I2 x r3) = C KA3: out[j2][(q,q')] = sum_j3 CT[j3][j2] KA3[j3][(q,q')]
-    gemm_tn(ct, I2, ka3, r3, I2, r3, I3, tm, r3, st);
-    // G' (r2 x r3) = KA2^T T
-    gemm_tn(ka2, r2, tm, r3, r2, r3, I2, gp, r3, st);
+    // T (I2 x m3) = C KA3: out[j2][v(q,q')] = sum_j3 CT[j3][j2] KA3[j3][v(q,q')]
+    gemm_tn(ct, I2, ka3, m3, I2, m3, I3, tm, m3, st);
+    // G' (m2 x m3) = KA2^T T
+    gemm_tn(ka2, m2, tm, m3, m2, m3, I2, gp, m3, st);
     GramSpec gs{};
     gs.s = s;
     gs.d = W;

@@ -151,12 +151,17 @@ __global__ void k_c4_kr(const double* __restrict__ A, int I, int R, double* __re
 // 8 warps of 32 x 16 (4 x 2 DMMA.8x8x4 tiles), K chunks of 16 through a two-buffer cp.async
 // ring; rows padded to 4 mod 16 doubles make the fragment loads conflict-free.
 constexpr int kGK = 16;
+// blockIdx.z = batch entry (A, B, out advanced by sA, sB, sO).
 template <int WM>
 __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, long long lda,
                                                  const double* __restrict__ B, long long ldb,
                                                  int M, int N, int K, double* __restrict__ out,
-                                                 long long ldo) {
+                                                 long long ldo, long long sA, long long sB,
+                                                 long long sO) {
   constexpr int TM = 32 * WM, TN = 16 * (8 / WM), LDA = TM + 4, LDB = TN + 4;
+  A += blockIdx.z * sA;
+  B += blockIdx.z * sB;
+  out += blockIdx.z * sO;
   __shared__ __align__(16) double As[2][kGK][LDA];
   __shared__ __align__(16) double Bs[2][kGK][LDB];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -212,23 +217,6 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, l
         const long long m = m0 + wm * 32 + i * 8 + g, n = n0 + wn * 16 + j * 8 + 2 * t + h;
         if (m < M && n < N) out[m * ldo + n] = c[i][j][h];
       }
-}
-
-// out = A^T B (k_gemm_tn), tile shape by M
-void gemm_tn(const double* A, long long lda, const double* B, long long ldb, int M, long long N,
-             int K, double* out, long long ldo, cudaStream_t st) {
-  if (M <= 32) {
-    const long long gx = (N + 127) / 128;
-    if (gx > 0x7fffffffLL) throw Error(1, "gemm_tn: N too large");
-    k_gemm_tn<1><<<dim3((unsigned)gx, ceil_div(M, 32)), 256, 0, st>>>(A, lda, B, ldb, M, (int)N, K,
-                                                                       out, ldo);
-  } else {
-    const long long gx = (N + 63) / 64;
-    if (gx > 0x7fffffffLL) throw Error(1, "gemm_tn: N too large");
-    k_gemm_tn<2><<<dim3((unsigned)gx, ceil_div(M, 64)), 256, 0, st>>>(A, lda, B, ldb, M, (int)N, K,
-                                                                       out, ldo);
-  }
-  RTB_LAUNCH_CHECK();
 }
 
 // G[(p,q),(p',q')] = G'[v(p,p')][v(q,q')] + [p = p', q = q'] (augmented draws of (p,q)) aug_term
@@ -452,6 +440,25 @@ size_t gram_part_bytes(int I2, int I3, int R2, int R3) {
 }
 
 }  // namespace
+
+// out = A^T B (k_gemm_tn), tile shape by M; batch entries z = 0 .. batch-1 at strides
+void gemm_tn(const double* A, long long lda, const double* B, long long ldb, int M, long long N,
+             int K, double* out, long long ldo, cudaStream_t st, int batch, long long sA,
+             long long sB, long long sO) {
+  if (batch < 1 || batch > 65535) throw Error(1, "gemm_tn: batch out of range");
+  if (M <= 32) {
+    const long long gx = (N + 127) / 128;
+    if (gx > 0x7fffffffLL) throw Error(1, "gemm_tn: N too large");
+    k_gemm_tn<1><<<dim3((unsigned)gx, ceil_div(M, 32), batch), 256, 0, st>>>(
+        A, lda, B, ldb, M, (int)N, K, out, ldo, sA, sB, sO);
+  } else {
+    const long long gx = (N + 63) / 64;
+    if (gx > 0x7fffffffLL) throw Error(1, "gemm_tn: N too large");
+    k_gemm_tn<2><<<dim3((unsigned)gx, ceil_div(M, 64), batch), 256, 0, st>>>(
+        A, lda, B, ldb, M, (int)N, K, out, ldo, sA, sB, sO);
+  }
+  RTB_LAUNCH_CHECK();
+}
 
 size_t c4_work_bytes(unsigned long long s, int I1, int I2, int I3, int R2, int R3, bool gram) {
   size_t off = 0;

@@ -105,6 +105,12 @@ void factor_sketch_normal_eq(const FactorSketchSpec& spec, const unsigned long l
                              const double* w, void* work, double* gram, double* M,
                              cudaStream_t st);
 
+// ---- FP64 DMMA GEMM (k_c4.cu): out[m][n] = sum_k A[k][m] B[k][n] (A: K x M, B: K x N,
+// row-major with leading dims), optionally batched (blockIdx.z; strides sA, sB, sO) ----
+void gemm_tn(const double* A, long long lda, const double* B, long long ldb, int M, long long N,
+             int K, double* out, long long ldo, cudaStream_t st, int batch = 1, long long sA = 0,
+             long long sB = 0, long long sO = 0);
+
 // ---- k_c4.cu: BASELINE config-4 microbench (Kronecker sampling + fused fiber gather/SYRK) ----
 size_t c4_work_bytes(unsigned long long s, int I1, int I2, int I3, int R2, int R3, bool gram);
 // canonical row-major I1 x I2 x I3 -> fiber-major (mode 1 fastest: out[(i2 I3 + i3) I1 + i1])

@@ -92,6 +92,10 @@ def test_draws_bit_exact_given_reference_cdfs(oracle, rt, shape, ranks, s, seed)
 # ---------------------------------------------------------------- rung 3
 @pytest.mark.parametrize("shape,ranks,lam,s", [((30, 25, 20), (4, 3, 5), 1e-3, 4000),
                                                 ((20, 18, 16, 12), (3, 2, 2, 3), 0.1, 3000),
+                                                # order 4 with draws >> (i1, i2) pairs: the
+                                                # (i1, i2)-bucketed path of k_gram.cu
+                                                ((16, 14, 12, 10), (4, 3, 5, 2), 0.05, 20000),
+                                                ((12, 10, 9, 8), (3, 3, 3, 3), 0.1, 600),
                                                 ((50, 40), (6, 5), 1e-2, 2000),
                                                 ((70,), (9,), 1e-2, 500)])
 def test_normal_equations_from_reference_sketch(oracle, rt, shape, ranks, lam, s):

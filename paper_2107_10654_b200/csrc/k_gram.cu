@@ -1181,6 +1181,7 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
       if (NTn <= 4) launch(k_vech_bucket2<4, H_, R_, C_>);
       else if (NTn <= 8) launch(k_vech_bucket2<8, H_, R_, C_>);
       else if (NTn <= 12) launch(k_vech_bucket2<12, H_, R_, C_>);
+      else if (NTn == 17) launch(k_vech_bucket2<17, H_, R_, C_>);  // R = 16: 136 = 17 x 8
       else launch(k_vech_bucket2<18, H_, R_, C_>);
     };
     using I0 = std::integral_constant<int, 0>;

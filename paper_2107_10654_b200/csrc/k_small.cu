@@ -536,12 +536,17 @@ __global__ void k_score_cdf(const double* scores, const long long* off, const in
   double* c = cdf + off[mode];
   const int n = rows[mode];
   double running = 0.0;
+  // the next block's scores are loaded while this block's dependent sum runs
+  double vnext = lane < n ? s[lane] : 0.0;
   for (int base = 0; base < n; base += 32) {
-    const double v = base + lane < n ? s[base + lane] : 0.0;
+    const double v = vnext;
+    vnext = base + 32 + lane < n ? s[base + 32 + lane] : 0.0;
     double mine = 0.0;
     const int cnt = min(32, n - base);
-    for (int k = 0; k < cnt; ++k) {
-      running = __dadd_rn(running, __shfl_sync(0xffffffffu, v, k));
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double x = __shfl_sync(0xffffffffu, v, k);
+      if (k < cnt) running = __dadd_rn(running, x);
       if (lane == k) mine = running;
     }
     if (base + lane < n) c[base + lane] = mine;

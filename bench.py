@@ -474,12 +474,21 @@ def run_our_arm(args):
 def run_c4(args):
     """BASELINE config 4 microbench (--workload c4): Kronecker-product sampling + fused fiber
     gather/SYRK. 3 factors 2048 x 32 N(0,1) FP64 (A1 unused by the microbench), X 2048^3 FP32
-    N(0,1) (34 GB, resident), lambda = 1e-2; for each s: draws of [A2 (x) A3; sqrt(lambda) I]
-    (W = 1024), the W x W Gram and the W x 2048 mode-1 fiber RHS. One JSON line per s."""
+    N(0,1) (34 GB, resident, replicated per GPU), lambda = 1e-2; for each s: draws of
+    [A2 (x) A3; sqrt(lambda) I] (W = 1024), the W x W Gram and the W x 2048 mode-1 fiber RHS.
+    N > 1 (torchrun): shard r accumulates the draws of its j2 range and an NCCL all-reduce sums
+    the Gram and RHS inside the timed step (device time, max over ranks). One JSON line per s."""
     import numpy as np
     import torch
     from paper_2107_10654_b200 import rtucker as rt
-    torch.cuda.set_device(0)
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rt.set_stream(torch.cuda.current_stream().cuda_stream)
     I, R, lam = 2048, 32, 1e-2
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -509,39 +518,61 @@ def run_c4(args):
     hbm = mp.get("hbm_gbs", 6553.3)
     fp64 = peaks["dmma_m8n8k4_tflops"]
 
+    def step(xp, fm, s, seed):
+        out = rt.kron_fiber_sketch(xp, (I, I, I), a2.data_ptr(), a3.data_ptr(), R, R, lam, s, seed,
+                                   gram.data_ptr(), rhs.data_ptr(), fiber_major=fm,
+                                   shard=(rank, world))
+        if dist is not None:
+            dist.all_reduce(gram)
+            dist.all_reduce(rhs)
+        return out
+
     def run(xp, fm, s):
         for _ in range(args.warmup):
-            rt.kron_fiber_sketch(xp, (I, I, I), a2.data_ptr(), a3.data_ptr(), R, R, lam, s, 1,
-                                 gram.data_ptr(), rhs.data_ptr(), fiber_major=fm)
+            step(xp, fm, s, 1)
         ph, nd, nu = np.zeros(3), 0, 0
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
         for k in range(args.steps):
-            out = rt.kron_fiber_sketch(xp, (I, I, I), a2.data_ptr(), a3.data_ptr(), R, R, lam, s,
-                                       2 + k, gram.data_ptr(), rhs.data_ptr(), fiber_major=fm)
+            out = step(xp, fm, s, 2 + k)
             ph += np.array(out["phase_ms"])
             nd += out["data_draws"]
             nu += out["unique_rows"]
-        return ph / args.steps, nd / args.steps, nu / args.steps
+        t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / args.steps
+        if dist is not None:
+            tt = torch.tensor([ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms, ph / args.steps, nd / args.steps, nu / args.steps
 
     for s in [int(float(v)) for v in args.c4_s.split(",")]:
-        (draw_ms, gram_ms, rhs_ms), nd, nu = run(xf.data_ptr(), True, s)
-        (_, _, rhs_c_ms), _, _ = run(x.data_ptr(), False, s)
+        step_ms, (draw_ms, gram_ms, rhs_ms), nd, nu = run(xf.data_ptr(), True, s)
+        c_ms, (_, _, rhs_c_ms), _, _ = run(x.data_ptr(), False, s) if world == 1 else (0, (0, 0, 0), 0, 0)
         # Gram: two DMMA GEMMs over vech Khatri-Rao row products (T = C KA3, G' = KA2^T T,
         # m = R (R + 1) / 2 pair columns); the phase also holds the shared sort / merge
         m = R * (R + 1) // 2
-        gram_flops = 2.0 * I * I * m + 2.0 * m * m * I
+        gram_flops = (2.0 * I * I * m + 2.0 * m * m * I) / world
         # RHS: per distinct sampled row 2 R I1 (D_b accumulation), per bucket the a2 (x) D_b fold
-        rhs_flops = 2.0 * nu * R * I + 2.0 * I * R * R * I
-        fiber_bytes = 4.0 * I * nu                # each distinct FP32 fiber read once
+        rhs_flops = (2.0 * nu * R * I + 2.0 * I * R * R * I) / world
+        fiber_bytes = 4.0 * I * nu / world        # each distinct FP32 fiber read once
         line = {
             "metric": "C4 sketched Kronecker samples/s (Gram+RHS)",
-            "value": s / ((draw_ms + gram_ms + rhs_ms) / 1e3),
-            "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "dtype": "f64 (FP32 tensor upcast)", "data": "synthetic",
+            "value": s / (step_ms / 1e3),
+            "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+            "dtype": "f64 (FP32 tensor upcast)", "data": "synthetic",
             "config": {"workload": "C4: factors 2048 x 32 N(0,1), X 2048^3 FP32 N(0,1) (34 GB), "
                                    "design A2 (x) A3 (4,194,304 x 1024), lambda 1e-2",
                        "s": s, "data_draws": nd, "distinct_rows": nu,
                        "x_layout": "fiber-major (mode 1 fastest), converted once on device",
-                       "fiber_major_convert_ms": fm_ms},
+                       "fiber_major_convert_ms": fm_ms,
+                       "parallelism": f"j2-bucket shards x {world}, NCCL all-reduce of Gram + RHS"
+                       if world > 1 else "single GPU"},
             "phases_ms": {"scores_and_draws": draw_ms, "sort_merge_and_gram": gram_ms,
                           "fiber_rhs": rhs_ms},
             "gram_only_samples_per_s": s / ((draw_ms + gram_ms) / 1e3),
@@ -551,10 +582,14 @@ def run_c4(args):
                           "frac_fp64": rhs_flops / (rhs_ms / 1e3) / 1e12 / fp64},
             "gram": {"tflops": gram_flops / (gram_ms / 1e3) / 1e12,
                      "frac_fp64": gram_flops / (gram_ms / 1e3) / 1e12 / fp64},
-            "canonical_layout": {"fiber_rhs_ms": rhs_c_ms,
-                                 "samples_per_s": s / ((draw_ms + gram_ms + rhs_c_ms) / 1e3)},
         }
-        print(json.dumps(line), flush=True)
+        if world == 1:
+            line["canonical_layout"] = {"fiber_rhs_ms": rhs_c_ms, "samples_per_s": s / (c_ms / 1e3)}
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 

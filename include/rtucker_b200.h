@@ -165,6 +165,18 @@ rtucker_status rtucker_b200_kron_fiber_sketch(const float* x_dev, const uint64_t
                                               uint64_t* data_draws_out, uint64_t* unique_rows_out,
                                               double* phase_ms_out);
 
+/* Sharded variant (multi-GPU, one process per GPU, X replicated): every shard decodes the
+ * same draws, and shard r of P accumulates only the data draws with j2 in
+ * [I2 r / P, I2 (r + 1) / P) (the augmented diagonal on shard 0), so the caller's sum
+ * all-reduce of gram_dev and rhs_dev over the P shards gives the full Gram and RHS.
+ * data_draws_out / unique_rows_out are the global counts. */
+rtucker_status rtucker_b200_kron_fiber_sketch_shard(
+    const float* x_dev, const uint64_t* shape, uint32_t x_layout, const double* a2_dev,
+    const double* a3_dev, uint32_t r2, uint32_t r3, double lambda, uint64_t s, uint64_t seed,
+    double* gram_dev, double* rhs_dev, uint64_t* indices_out, double* weights_out,
+    uint64_t* data_draws_out, uint64_t* unique_rows_out, double* phase_ms_out,
+    uint32_t shard_rank, uint32_t shard_count);
+
 /* Fiber-major copy of a device FP32 tensor (shape[3] = I1, I2, I3, canonical row-major in):
  * out_dev[(i2 I3 + i3) I1 + i1] = x_dev[(i1 I2 + i2) I3 + i3]. */
 rtucker_status rtucker_b200_tensor_fiber_major(const float* x_dev, const uint64_t* shape,

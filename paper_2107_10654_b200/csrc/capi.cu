@@ -817,6 +817,24 @@ rtucker_status rtucker_b200_kron_draw(uint32_t order, const uint64_t* rows, uint
   });
 }
 
+rtucker_status rtucker_b200_kron_fiber_sketch_shard(
+    const float* x_dev, const uint64_t* shape, uint32_t x_layout, const double* a2_dev,
+    const double* a3_dev, uint32_t r2, uint32_t r3, double lambda, uint64_t s, uint64_t seed,
+    double* gram_dev, double* rhs_dev, uint64_t* indices_out, double* weights_out,
+    uint64_t* data_draws_out, uint64_t* unique_rows_out, double* phase_ms_out,
+    uint32_t shard_rank, uint32_t shard_count) {
+  return guarded([&] {
+    if (!shape || !a2_dev || !a3_dev) throw rtb::Error(1, "kron_fiber_sketch: null argument");
+    if (x_layout > 1) throw rtb::Error(1, "kron_fiber_sketch: x_layout must be 0 or 1");
+    if (shard_count < 1 || shard_rank >= shard_count)
+      throw rtb::Error(1, "kron_fiber_sketch: bad shard");
+    rtb::kron_fiber_sketch(x_dev, x_layout == 1, (int)shape[0], (int)shape[1], (int)shape[2],
+                           a2_dev, a3_dev, (int)r2, (int)r3, lambda, s, seed, gram_dev, rhs_dev,
+                           indices_out, weights_out, data_draws_out, unique_rows_out,
+                           phase_ms_out, (int)shard_rank, (int)shard_count);
+  });
+}
+
 rtucker_status rtucker_b200_kron_fiber_sketch(const float* x_dev, const uint64_t* shape,
                                               uint32_t x_layout, const double* a2_dev,
                                               const double* a3_dev, uint32_t r2, uint32_t r3,
@@ -825,14 +843,10 @@ rtucker_status rtucker_b200_kron_fiber_sketch(const float* x_dev, const uint64_t
                                               uint64_t* indices_out, double* weights_out,
                                               uint64_t* data_draws_out, uint64_t* unique_rows_out,
                                               double* phase_ms_out) {
-  return guarded([&] {
-    if (!shape || !a2_dev || !a3_dev) throw rtb::Error(1, "kron_fiber_sketch: null argument");
-    if (x_layout > 1) throw rtb::Error(1, "kron_fiber_sketch: x_layout must be 0 or 1");
-    rtb::kron_fiber_sketch(x_dev, x_layout == 1, (int)shape[0], (int)shape[1], (int)shape[2],
-                           a2_dev, a3_dev, (int)r2, (int)r3, lambda, s, seed, gram_dev, rhs_dev,
-                           indices_out, weights_out, data_draws_out, unique_rows_out,
-                           phase_ms_out);
-  });
+  return rtucker_b200_kron_fiber_sketch_shard(x_dev, shape, x_layout, a2_dev, a3_dev, r2, r3,
+                                              lambda, s, seed, gram_dev, rhs_dev, indices_out,
+                                              weights_out, data_draws_out, unique_rows_out,
+                                              phase_ms_out, 0, 1);
 }
 
 rtucker_status rtucker_b200_tensor_fiber_major(const float* x_dev, const uint64_t* shape,

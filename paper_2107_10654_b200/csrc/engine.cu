@@ -1759,7 +1759,8 @@ void tensor_fiber_major(const float* x, int I1, int I2, int I3, float* out) {
 void kron_fiber_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const double* a2,
                        const double* a3, int R2, int R3, double lambda, uint64_t s, uint64_t seed,
                        double* gram, double* rhs, uint64_t* idx_host, double* w_host,
-                       uint64_t* data_draws, uint64_t* unique_rows, double* phase_ms) {
+                       uint64_t* data_draws, uint64_t* unique_rows, double* phase_ms,
+                       int shard_rank, int shard_count) {
   if (I1 < 1 || I2 < 1 || I3 < 1 || R2 < 1 || R3 < 1 || R2 > 32 || R3 > 32 || R2 > I2 || R3 > I3)
     throw Error(1, "kron_fiber_sketch: bad shape or ranks (R <= 32, R <= I)");
   if (s == 0) throw Error(1, "solve_sketched_ridge: sample count must be positive");
@@ -1831,7 +1832,7 @@ void kron_fiber_sketch(const float* x, bool fiber_major, int I1, int I2, int I3,
     c4_sketch(want_rhs ? x : nullptr, fiber_major, I1, I2, I3, a2, R2, a3, R3,
               (const unsigned long long*)ix.p, ww.as<double>(), s, lambda, cw.p, cw.bytes, gram,
               want_rhs ? rhs : nullptr, cnt.as<unsigned long long>(),
-              cnt.as<unsigned long long>() + 1, ev[2], st);
+              cnt.as<unsigned long long>() + 1, ev[2], st, shard_rank, shard_count);
   } else {
     RTB_CUDA(cudaMemsetAsync(cnt.p, 0, 16, st));
     RTB_CUDA(cudaEventRecord(ev[2], st));

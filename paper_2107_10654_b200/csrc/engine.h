@@ -117,7 +117,8 @@ void kron_draw(int order, const uint64_t* rows, uint64_t d, const double* scores
 void kron_fiber_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const double* a2,
                        const double* a3, int R2, int R3, double lambda, uint64_t s, uint64_t seed,
                        double* gram, double* rhs, uint64_t* idx_host, double* w_host,
-                       uint64_t* data_draws, uint64_t* unique_rows, double* phase_ms);
+                       uint64_t* data_draws, uint64_t* unique_rows, double* phase_ms,
+                       int shard_rank = 0, int shard_count = 1);
 void tensor_fiber_major(const float* x, int I1, int I2, int I3, float* out);
 void kron_normal_eq(int order, const uint64_t* rows, const uint64_t* ranks, const double* factors,
                     const double* x_host, double lambda, uint64_t s, const uint64_t* idx,

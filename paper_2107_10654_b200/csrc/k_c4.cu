@@ -263,7 +263,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256, 2) k_c4_dfib(
     const float* __restrict__ X, int I1, int I2, int I3, int R3,
     const unsigned long long* __restrict__ ukey, const double* __restrict__ rows,
-    const int* __restrict__ bstart, double* __restrict__ D) {
+    const int* __restrict__ bstart, int blo, int bhi, double* __restrict__ D) {
   extern __shared__ __align__(16) double c4s[];
   unsigned long long* Ks = reinterpret_cast<unsigned long long*>(c4s);     // [kSeg]
   double* At = c4s + kSeg;                                                 // [kSt][kRC][kQLDT]
@@ -272,9 +272,9 @@ __global__ void __launch_bounds__(256, 2) k_c4_dfib(
   const int g = lane >> 2, t = lane & 3;
   const long long slab = (long long)I2 * I3;
   const int NT = (I1 + kDT - 1) / kDT;
-  const long long nitems = (long long)I2 * NT;
+  const long long nitems = (long long)(bhi - blo) * NT;
   for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int b = (int)(item / NT), n0 = (int)(item % NT) * kDT;
+    const int b = blo + (int)(item / NT), n0 = (int)(item % NT) * kDT;
     const int r0 = bstart[b], cnt = bstart[b + 1] - r0;
     double c[4][4][2];
 #pragma unroll
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(256, 2) k_c4_dfib(
     for (int i = 0; i < 4; ++i) {
       const int q = i * 8 + g;
       if (q >= R3) continue;
-      double* drow = D + ((size_t)b * R3 + q) * I1;
+      double* drow = D + ((size_t)(b - blo) * R3 + q) * I1;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int col = n0 + warp * 32 + j * 8 + 2 * t;
@@ -483,8 +483,14 @@ void c4_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const d
                const double* A3, int R3, const unsigned long long* idx, const double* w,
                unsigned long long s, double lambda, void* work, size_t work_bytes, double* gram,
                double* rhs, unsigned long long* data_draws_dev, unsigned long long* unique_dev,
-               cudaEvent_t ev_gram_done, cudaStream_t st) {
+               cudaEvent_t ev_gram_done, cudaStream_t st, int shard_rank, int shard_count) {
   if (R3 > 32 || R2 > 32) throw Error(1, "c4_sketch: ranks must be <= 32");
+  if (shard_count < 1 || shard_rank < 0 || shard_rank >= shard_count)
+    throw Error(1, "c4_sketch: bad shard");
+  // this shard's j2 buckets (its share of the Gram and RHS partial sums)
+  const int blo = (int)((long long)I2 * shard_rank / shard_count);
+  const int bhi = (int)((long long)I2 * (shard_rank + 1) / shard_count);
+  const int nb = bhi - blo;
   if (s > 0xffffffffULL) throw Error(1, "c4_sketch: at most 2^32 - 1 draws");
   const int W = R2 * R3;
   if (work_bytes < c4_work_bytes(s, I1, I2, I3, R2, R3, gram != nullptr))
@@ -531,16 +537,20 @@ void c4_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const d
     RTB_LAUNCH_CHECK();
     k_c4_kr<<<(unsigned)ceil_div<long long>((long long)I2 * m2, 256LL), 256, 0, st>>>(A2, I2, R2, ka2);
     RTB_LAUNCH_CHECK();
-    // T (I2 x m3) = C KA3: out[j2][v(q,q')] = sum_j3 CT[j3][j2] KA3[j3][v(q,q')]
-    gemm_tn(ct, I2, ka3, m3, I2, m3, I3, tm, m3, st);
-    // G' (m2 x m3) = KA2^T T
-    gemm_tn(ka2, m2, tm, m3, m2, m3, I2, gp, m3, st);
+    // T (this shard's j2 rows x m3) = C KA3: out[j2][v(q,q')] = sum_j3 CT[j3][j2] KA3[j3][v(q,q')]
+    if (nb > 0) {
+      gemm_tn(ct + blo, I2, ka3, m3, nb, m3, I3, tm, m3, st);
+      // G' (m2 x m3) = KA2^T T over the shard's j2
+      gemm_tn(ka2 + (size_t)blo * m2, m2, tm, m3, m2, m3, nb, gp, m3, st);
+    } else {
+      RTB_CUDA(cudaMemsetAsync(gp, 0, (size_t)m2 * m3 * 8, st));
+    }
     GramSpec gs{};
     gs.s = s;
     gs.d = W;
     gs.lambda = lambda;
     k_c4_gram_out<<<(unsigned)ceil_div<long long>((long long)W * W, 256LL), 256, 0, st>>>(
-        gp, R2, R3, l.astart, gram_aug_term(gs), gram);
+        gp, R2, R3, l.astart, shard_rank == 0 ? gram_aug_term(gs) : 0.0, gram);
     RTB_LAUNCH_CHECK();
   }
   if (ev_gram_done) RTB_CUDA(cudaEventRecord(ev_gram_done, st));
@@ -558,13 +568,14 @@ void c4_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const d
     attr = true;
   }
   auto kern = !fiber_major ? k_c4_dfib<0> : (I1 % 4 == 0 ? k_c4_dfib<1> : k_c4_dfib<2>);
-  const long long nitems = (long long)I2 * ceil_div(I1, kDT);
-  const int grid = (int)std::min<long long>(nitems, 2LL * kNumSMs);
-  kern<<<grid, 256, kDfibSmem, st>>>(x, I1, I2, I3, R3, l.ukey, l.rows, l.bstart, l.dfib);
+  const long long nitems = (long long)nb * ceil_div(I1, kDT);
+  const int grid = (int)std::max<long long>(1, std::min<long long>(nitems, 2LL * kNumSMs));
+  kern<<<grid, 256, kDfibSmem, st>>>(x, I1, I2, I3, R3, l.ukey, l.rows, l.bstart, blo, bhi, l.dfib);
   RTB_LAUNCH_CHECK();
   // RHS (R2 x R3 I1) = A2^T D
   const long long n = (long long)R3 * I1;
-  gemm_tn(A2, R2, l.dfib, n, R2, n, I2, rhs, n, st);
+  if (nb > 0) gemm_tn(A2 + (size_t)blo * R2, R2, l.dfib, n, R2, n, nb, rhs, n, st);
+  else RTB_CUDA(cudaMemsetAsync(rhs, 0, (size_t)R2 * n * 8, st));
 }
 
 }  // namespace rtb

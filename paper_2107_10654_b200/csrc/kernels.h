@@ -117,13 +117,15 @@ size_t c4_work_bytes(unsigned long long s, int I1, int I2, int I3, int R2, int R
 void c4_to_fiber_major(const float* x, int I1, int I2, int I3, float* out, cudaStream_t st);
 // From draws (idx, w) of [A2 (x) A3; sqrt(lambda) I]: gram (W x W, W = R2 R3, if non-null) and
 // rhs (W x I1, if x and rhs are non-null) = sum over data draws of w^2 (a2 (x) a3) X[:, j2, j3]^T.
+// Sharded (shard_count > 1): only the draws with j2 in this shard's range [I2 r / P, I2 (r+1) / P)
+// contribute (the augmented diagonal on shard 0): the shards' gram / rhs sum to the full ones.
 // X is FP32, canonical or fiber-major. *data_draws_dev / *unique_dev (optional): data draws and
 // distinct sampled rows. ev_gram_done (optional) is recorded after the Gram.
 void c4_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const double* A2, int R2,
                const double* A3, int R3, const unsigned long long* idx, const double* w,
                unsigned long long s, double lambda, void* work, size_t work_bytes, double* gram,
                double* rhs, unsigned long long* data_draws_dev, unsigned long long* unique_dev,
-               cudaEvent_t ev_gram_done, cudaStream_t st);
+               cudaEvent_t ev_gram_done, cudaStream_t st, int shard_rank = 0, int shard_count = 1);
 
 // ---- k_gram.cu ----
 struct GramSpec {

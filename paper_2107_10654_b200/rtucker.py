@@ -151,6 +151,10 @@ def _load() -> C.CDLL:
                                                C.c_uint32, C.c_double, C.c_uint64, C.c_uint64,
                                                _vp, _vp, _u64p, _f64p, _u64p, _u64p, _f64p]),
         "rtucker_b200_tensor_fiber_major": (S, [_vp, _u64p, _vp]),
+        "rtucker_b200_kron_fiber_sketch_shard": (S, [_vp, _u64p, C.c_uint32, _vp, _vp, C.c_uint32,
+                                                     C.c_uint32, C.c_double, C.c_uint64,
+                                                     C.c_uint64, _vp, _vp, _u64p, _f64p, _u64p,
+                                                     _u64p, _f64p, C.c_uint32, C.c_uint32]),
         "rtucker_b200_spd_solve": (S, [_f64p, _f64p, C.c_uint64, _f64p, _u64p,
                                        C.POINTER(C.c_int)]),
         "rtucker_b200_update_core_sketched": (S, [_vp, _vp, C.c_uint64, C.c_uint64, _f64p, _u64p,
@@ -569,21 +573,22 @@ def kron_normal_eq(shape, ranks, factors, x, lam, idx, w):
 
 
 def kron_fiber_sketch(x_ptr, shape, a2_ptr, a3_ptr, r2, r3, lam, s, seed, gram_ptr=None,
-                      rhs_ptr=None, want_draws=False, fiber_major=False):
-    """BASELINE C4 microbench on device pointers (rtucker_b200_kron_fiber_sketch):
+                      rhs_ptr=None, want_draws=False, fiber_major=False, shard=(0, 1)):
+    """BASELINE C4 microbench on device pointers (rtucker_b200_kron_fiber_sketch_shard):
     X (I1 x I2 x I3 FP32; canonical row-major, or fiber-major when fiber_major), A2 (I2 x r2),
-    A3 (I3 x r3) FP64; gram (W x W) and rhs (W x I1) FP64 outputs, W = r2 r3.
+    A3 (I3 x r3) FP64; gram (W x W) and rhs (W x I1) FP64 outputs, W = r2 r3. shard = (rank,
+    count): this shard's partial sums (j2 range), to be summed over the shards.
     Returns {data_draws, unique_rows, phase_ms, [indices, weights]}."""
     shape = _u64(shape)
     idx = np.zeros(s, np.uint64) if want_draws else None
     w = np.zeros(s) if want_draws else None
     nd, nu = C.c_uint64(), C.c_uint64()
     ms = np.zeros(3)
-    _check(lib.rtucker_b200_kron_fiber_sketch(
+    _check(lib.rtucker_b200_kron_fiber_sketch_shard(
         C.c_void_p(x_ptr or 0), _p(shape), 1 if fiber_major else 0, C.c_void_p(a2_ptr),
         C.c_void_p(a3_ptr), r2, r3, lam, s, seed, C.c_void_p(gram_ptr or 0),
         C.c_void_p(rhs_ptr or 0), _p(idx) if want_draws else None, _p(w) if want_draws else None,
-        C.byref(nd), C.byref(nu), _p(ms)))
+        C.byref(nd), C.byref(nu), _p(ms), int(shard[0]), int(shard[1])))
     out = {"data_draws": nd.value, "unique_rows": nu.value, "phase_ms": ms.tolist()}
     if want_draws:
         out["indices"], out["weights"] = idx, w

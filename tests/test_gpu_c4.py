@@ -100,3 +100,38 @@ def test_c4_rhs_only_and_layouts_agree(rt):
     assert o0["unique_rows"] == o1["unique_rows"] > 0
     assert torch.equal(r0, r1)
     assert torch.count_nonzero(r0) > 0
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_c4_shards_sum_to_full(rt, P):
+    """rtucker_b200_kron_fiber_sketch_shard: the P shards' partial Gram / RHS (run one after
+    another on this GPU, summed on the host) equal the unsharded result."""
+    import torch
+    I1, I2, I3, R2, R3, s = 40, 37, 29, 5, 6, 30000
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = torch.randn(I1, I2, I3, dtype=torch.float32, device="cuda", generator=g)
+    xf = torch.empty_like(x)
+    rt.tensor_fiber_major(x.data_ptr(), (I1, I2, I3), xf.data_ptr())
+    a2 = torch.randn(I2, R2, dtype=torch.float64, device="cuda", generator=g)
+    a3 = torch.randn(I3, R3, dtype=torch.float64, device="cuda", generator=g)
+    W = R2 * R3
+    G = torch.zeros(W, W, dtype=torch.float64, device="cuda")
+    R = torch.zeros(W, I1, dtype=torch.float64, device="cuda")
+    full = rt.kron_fiber_sketch(xf.data_ptr(), (I1, I2, I3), a2.data_ptr(), a3.data_ptr(), R2, R3,
+                                1e-2, s, 5, G.data_ptr(), R.data_ptr(), fiber_major=True)
+    Gs, Rs = torch.zeros_like(G), torch.zeros_like(R)
+    for r in range(P):
+        gp, rp = torch.zeros_like(G), torch.zeros_like(R)
+        out = rt.kron_fiber_sketch(xf.data_ptr(), (I1, I2, I3), a2.data_ptr(), a3.data_ptr(), R2,
+                                   R3, 1e-2, s, 5, gp.data_ptr(), rp.data_ptr(), fiber_major=True,
+                                   shard=(r, P))
+        assert out["data_draws"] == full["data_draws"]
+        Gs += gp
+        Rs += rp
+    torch.cuda.synchronize()
+    dg = torch.sqrt(torch.outer(torch.diag(G), torch.diag(G)))
+    assert float(torch.max(torch.abs(Gs - G) / dg)) < 1e-12
+    assert float(torch.linalg.norm(Rs - R) / torch.linalg.norm(R)) < 1e-12
+    with pytest.raises(rt.RtuckerError):
+        rt.kron_fiber_sketch(xf.data_ptr(), (I1, I2, I3), a2.data_ptr(), a3.data_ptr(), R2, R3,
+                             1e-2, 100, 5, G.data_ptr(), R.data_ptr(), shard=(3, 3))

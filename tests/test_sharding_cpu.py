@@ -102,3 +102,72 @@ def test_sharding_decomposition_gloo(oracle, world):
         p.join(timeout=60)
     for rank, msg in res:
         assert msg == "ok", f"rank {rank}:\n{msg}"
+
+
+def _c4_worker(rank, world, port, q):
+    """BASELINE C4 sharding (rtucker_b200_kron_fiber_sketch_shard): every shard takes the
+    same draws, keeps the data draws with j2 in its range (rt.shard_rows over I2) and adds
+    the augmented diagonal on shard 0 only; the sum over shards is the full Gram and RHS."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle.oracle import Oracle
+        from paper_2107_10654_b200 import rtucker as rt
+        ar = rt.host_allreduce(dist)
+        o = Oracle()
+        rng = np.random.default_rng(8)
+        I1, I2, I3, R2, R3, lam, s = 12, 17, 15, 3, 4, 1e-2, 4000
+        X = rng.standard_normal((I1, I2, I3))
+        A2, A3 = rng.standard_normal((I2, R2)), rng.standard_normal((I3, R3))
+        sc, cdf, sums = [], [], []
+        for f in (A2, A3):
+            a, b, c, _ = o.factor_scores(f)
+            sc.append(a)
+            cdf.append(b)
+            sums.append(c)
+        W, total = R2 * R3, I2 * I3
+        idx, w, _ = o.kron_draw([I2, I3], W, sc, cdf, sums, 11, s)
+
+        def normal_eq(sel, with_aug):
+            d = idx < total
+            m = d & sel
+            j2, j3 = idx[m] // I3, idx[m] % I3
+            Z = np.einsum("tp,tq->tpq", A2[j2], A3[j3]).reshape(-1, W) * (w[m] ** 2)[:, None]
+            G = Z.T @ np.einsum("tp,tq->tpq", A2[j2], A3[j3]).reshape(-1, W)
+            Rh = Z.T @ X[:, j2, j3].T
+            if with_aug:
+                for j, wt in zip(idx[~d] - total, w[~d]):
+                    G[j, j] += wt * wt * lam
+            return np.ascontiguousarray(G), np.ascontiguousarray(Rh)
+
+        lo, hi = rt.shard_rows(rank, world, I2)
+        j2all = np.where(idx < total, idx // I3, -1)
+        g, r = normal_eq((j2all >= lo) & (j2all < hi), rank == 0)
+        ar(g.ctypes.data, g.size, 0)
+        ar(r.ctypes.data, r.size, 0)
+        gf, rf = normal_eq(np.ones(s, bool), True)
+        dg = np.sqrt(np.outer(np.diag(gf), np.diag(gf)))
+        assert np.max(np.abs(g - gf) / dg) < 1e-12
+        assert np.linalg.norm(r - rf) / np.linalg.norm(rf) < 1e-12
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except BaseException:  # noqa: BLE001
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2])
+def test_c4_sharding_decomposition_gloo(oracle, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_c4_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=240) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, msg in res:
+        assert msg == "ok", f"rank {rank}:\n{msg}"

@@ -1173,7 +1173,7 @@ class Engine {
       // warm start from the current core (the previous sweep's solution); the first
       // sketch of a run starts cold (the core is the random init then)
       ps.warm = warm_core_ ? 1 : 0;
-      pcg_work_.ensure(pcg_work_bytes((int)d_, rk[0]), st_);
+      pcg_work_.ensure(pcg_work_bytes((int)d_, N_, rk), st_);
       pcg_solve(ps, blocks_.as<double>(), rhs_.as<double>(), core_.as<double>(), pcg_work_.p,
                 pcg_status_.as<int>(), st_);
       int ps_out[2] = {1, 0};

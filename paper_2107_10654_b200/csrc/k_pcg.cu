@@ -74,6 +74,8 @@ struct PcgArgs {
   double tol;
   double check_tol;
   unsigned long long* prof;  // optional: per-phase ns accumulated by CTA 0 (RTB_PCG_PROF)
+  double* vglobal;           // large d: each CTA's redundant vectors in global memory
+                             // (6 dv doubles per CTA, L2-resident); nullptr: shared memory
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -563,15 +565,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   const int dv = (d + 1) & ~1;
   double* Ps = sm;                          // [order][RM][RM]: P_n (P form) or V_n (eigen form)
   double* VTs = Ps + sh.order * RM * RM;    // [order][RM][RM]: V_n^T (eigen form)
-  double* dinv = VTs + sh.order * RM * RM;  // [d]: 1 / (lambda + prod mu) (eigen form)
-  double* r = dinv + ((sh.d + 1) & ~1);
+  // the d-vectors: shared memory, or (large d) this CTA's slice of A.vglobal
+  const bool big = A.vglobal != nullptr;
+  double* vb = big ? A.vglobal + (size_t)blockIdx.x * 6 * dv : VTs + sh.order * RM * RM;
+  double* dinv = vb;                        // [d]: 1 / (lambda + prod mu) (eigen form)
+  double* r = dinv + dv;
   double* p = r + dv;
   double* s0 = p + dv;
   double* s1 = s0 + dv;
   double* xs = s1 + dv;  // full x, kept redundantly like r and p
-  double* red = xs + dv;
+  double* red = big ? VTs + sh.order * RM * RM : xs + dv;
   // fast order-3 matvec: per-warp accumulators, in s0/s1 when they are large enough
-  const bool fast3 = sh.order == 3 && sh.last == 16;
+  const bool fast3 = sh.order == 3 && sh.last == 16 && !big;
   const size_t acc_need = (size_t)kWarps * 2 * sh.dprime;
   double* accw = acc_need <= (size_t)2 * dv ? s0 : red + 32;
 
@@ -842,10 +847,22 @@ size_t pcg_work_bytes(int d, int r1) {
   return ((size_t)d + m1 * 2 * dp + 1024) * 8 + 256;
 }
 
+// large d: the six d-vectors leave shared memory for per-CTA global slices
+static bool pcg_big(int d, int order, const int* ranks) {
+  const int rm = rank_bucket(order, ranks);
+  return rm > 0 && pcg_smem(d, order, ranks, rm) > 220 * 1024;
+}
+static size_t pcg_smem_big(int order, int rm) { return 8 * (2 * (size_t)order * rm * rm + 32); }
+
+size_t pcg_work_bytes(int d, int order, const int* ranks) {
+  size_t b = pcg_work_bytes(d, ranks[0]);
+  if (pcg_big(d, order, ranks)) b += (size_t)num_sms() * 6 * ((d + 1) & ~1) * 8 + 256;
+  return b;
+}
+
 bool pcg_supported(int d, int order, const int* ranks) {
   const int rm = rank_bucket(order, ranks);
-  return d >= 1 && order >= 2 && order <= kMaxOrder && rm > 0 &&
-         pcg_smem(d, order, ranks, rm) <= 220 * 1024;
+  return d >= 1 && d <= (1 << 20) && order >= 2 && order <= kMaxOrder && rm > 0;
 }
 
 void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, double* x, void* work,
@@ -872,7 +889,8 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   for (int n = 1; n < spec.order - 1; ++n) sh.mmid *= sh.m[n];
   sh.m1 = sh.m[0];
   const int rm = rank_bucket(spec.order, spec.ranks);
-  const size_t smem = pcg_smem(d, spec.order, spec.ranks, rm);
+  const bool big = pcg_big(d, spec.order, spec.ranks);
+  const size_t smem = big ? pcg_smem_big(spec.order, rm) : pcg_smem(d, spec.order, spec.ranks, rm);
 
   char* w = static_cast<char*>(work);
   PcgArgs a{};
@@ -883,6 +901,11 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   a.part = a.q + d;
   a.rpart = a.part + (size_t)sh.m1 * 2 * sh.dprime;
   a.counter = reinterpret_cast<unsigned*>(a.rpart + 1024);
+  a.vglobal = nullptr;
+  if (big) {  // after the counter block (pcg_work_bytes(d, order, ranks))
+    const size_t off = ((pcg_work_bytes(d, spec.ranks[0]) + 255) & ~size_t(255));
+    a.vglobal = reinterpret_cast<double*>(w + off);
+  }
   a.status = status_dev;
   a.pinv = spec.pinv;
   a.linv_stride = spec.linv_stride;

@@ -182,6 +182,8 @@ struct PcgSpec {
   int warm = 0;         // 1: x holds a starting guess (kept if ||b - G x0|| < ||b||)
 };
 size_t pcg_work_bytes(int d, int r1);
+// with the per-CTA vector slices of the large-d form (vectors beyond shared memory)
+size_t pcg_work_bytes(int d, int order, const int* ranks);
 // norm estimates and preconditioner form (prep_dev[3]); skip_dev[order] = 1 where the
 // factor-Gram eigenpairs are not needed (feed to sym_eigen as skip flags)
 void pcg_prepare(const PcgSpec& spec, double* prep_dev, int* skip_dev, cudaStream_t st);

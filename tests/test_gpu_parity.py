@@ -324,10 +324,14 @@ def test_pcg_core_solve_matches_cholesky_and_oracle(oracle, rt, shape, ranks, la
 
 
 @pytest.mark.parametrize("shape,ranks,s", [((64, 64, 64), (16, 16, 16), 200000),
-                                          ((80, 70, 60), (12, 10, 14), 100000)])
+                                          ((80, 70, 60), (12, 10, 14), 100000),
+                                          # d beyond shared memory: vectors in global slices
+                                          ((40, 36, 32, 30), (10, 10, 10, 8), 400000),
+                                          ((48, 44, 40), (24, 20, 18), 400000)])
 def test_pcg_matches_cholesky_large_d(rt, shape, ranks, s):
-    """d = 4096 / 1680: CG and Cholesky solve the same sketched system (no oracle:
-    the reference's Jacobi SVD at this d takes hours)."""
+    """d = 4096 / 1680 / 8000 / 8640: CG and Cholesky solve the same sketched system (no
+    oracle: the reference's Jacobi SVD at this d takes hours). s is large enough that every
+    augmented column is drawn (else G may be singular and CG does not apply)."""
     x = planted(shape, ranks, seed=33)
     kw = dict(lam=1e-2, sketched_core=1, max_iterations=4, tolerance=0.0,
               sample_count_override=s, record_history=1, seed=2)

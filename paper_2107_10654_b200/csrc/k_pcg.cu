@@ -30,6 +30,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -48,6 +49,8 @@ struct PcgShared {
   int last;       // R_N
   int mmid;       // prod_{1 <= n < N-1} m_n (middle vech blocks)
   int m1;         // vech pairs of mode 1 (slices)
+  int jc;         // generic slice matvec: each slice split into jc chunks of the middle
+                  // index jm (work units m1 * jc, partial sums per chunk); 1 for fast3
 };
 
 struct PcgArgs {
@@ -299,7 +302,9 @@ template <int RM>
 __device__ void slice_partials(const PcgArgs& A, const PcgShared& sh, const double* p) {
   const int last = sh.last, mid = sh.mid, dp = sh.dprime;
   const int nout = 2 * dp;
-  for (int u1 = blockIdx.x; u1 < sh.m1; u1 += gridDim.x) {
+  for (int unit = blockIdx.x; unit < sh.m1 * sh.jc; unit += gridDim.x) {
+    const int u1 = unit / sh.jc, ch = unit - u1 * sh.jc;
+    const int jm0 = (int)((long long)mid * ch / sh.jc), jm1 = (int)((long long)mid * (ch + 1) / sh.jc);
     int a, b;
     pair_of(u1, sh.R[0], a, b);
     const double* Bs = A.B + (size_t)u1 * sh.mmid * last * last;
@@ -313,7 +318,7 @@ __device__ void slice_partials(const PcgArgs& A, const PcgShared& sh, const doub
       // runs to the compile-time bound with a guard, so indices are static
       int idig[kMaxOrder], jdig[kMaxOrder];
       {
-        int rem = im;
+        int rem = im, remj = jm0;
 #pragma unroll
         for (int n = kMaxOrder - 1; n >= 1; --n) {
           idig[n] = 0;
@@ -321,11 +326,13 @@ __device__ void slice_partials(const PcgArgs& A, const PcgShared& sh, const doub
           if (n <= sh.order - 2) {
             idig[n] = rem % sh.R[n];
             rem /= sh.R[n];
+            jdig[n] = remj % sh.R[n];
+            remj /= sh.R[n];
           }
         }
       }
       double s0 = 0.0, s1 = 0.0;
-      for (int jm = 0; jm < mid; ++jm) {
+      for (int jm = jm0; jm < jm1; ++jm) {
         int umid = 0;
 #pragma unroll
         for (int n = 1; n < kMaxOrder; ++n)
@@ -364,7 +371,7 @@ __device__ void slice_partials(const PcgArgs& A, const PcgShared& sh, const doub
             else jdig[n] = 0;
           }
       }
-      A.part[((size_t)u1 * 2 + side) * dp + (size_t)im * last + r] = s0 + s1;
+      A.part[(((size_t)u1 * sh.jc + ch) * 2 + side) * dp + (size_t)im * last + r] = s0 + s1;
     }
   }
 }
@@ -483,7 +490,8 @@ __device__ void reduce_rows(const PcgArgs& A, const PcgShared& sh, const double*
     for (int j1 = 0; j1 < R1; ++j1) {
       const int u1 = upper_pair(min(i1, j1), max(i1, j1), R1);
       const int side = i1 <= j1 ? 0 : 1;
-      s += __ldcg(A.part + ((size_t)u1 * 2 + side) * dp + rest);
+      for (int ch = 0; ch < sh.jc; ++ch)
+        s += __ldcg(A.part + (((size_t)u1 * sh.jc + ch) * 2 + side) * dp + rest);
     }
     const int c = __ldg(A.aug_count + e);
     if (c > 0) s = fma((double)c * A.aug_term, p[e], s);
@@ -854,9 +862,27 @@ static bool pcg_big(int d, int order, const int* ranks) {
 }
 static size_t pcg_smem_big(int order, int rm) { return 8 * (2 * (size_t)order * rm * rm + 32); }
 
+// chunks per slice of the generic matvec: about three work units per SM (fast3: 1)
+static int pcg_jc(int d, int order, const int* ranks) {
+  const bool fast3 = order == 3 && ranks[2] == 16 && !pcg_big(d, order, ranks);
+  if (fast3) return 1;
+  const int m1 = ranks[0] * (ranks[0] + 1) / 2;
+  int mid = 1;
+  for (int n = 1; n < order - 1; ++n) mid *= ranks[n];
+  const int jc = (3 * num_sms() + m1 - 1) / m1;
+  return std::max(1, std::min(jc, mid));
+}
+
+// q, partials [m1][jc][2][d'], residual partials, counter
+static size_t pcg_base_bytes(int d, int order, const int* ranks) {
+  const size_t m1 = (size_t)ranks[0] * (ranks[0] + 1) / 2;
+  const size_t dp = (size_t)d / ranks[0];
+  return ((size_t)d + m1 * pcg_jc(d, order, ranks) * 2 * dp + 1024) * 8 + 256;
+}
+
 size_t pcg_work_bytes(int d, int order, const int* ranks) {
-  size_t b = pcg_work_bytes(d, ranks[0]);
-  if (pcg_big(d, order, ranks)) b += (size_t)num_sms() * 6 * ((d + 1) & ~1) * 8 + 256;
+  size_t b = pcg_base_bytes(d, order, ranks);
+  if (pcg_big(d, order, ranks)) b = ((b + 255) & ~size_t(255)) + (size_t)num_sms() * 6 * ((d + 1) & ~1) * 8 + 256;
   return b;
 }
 
@@ -888,6 +914,7 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   sh.mmid = 1;
   for (int n = 1; n < spec.order - 1; ++n) sh.mmid *= sh.m[n];
   sh.m1 = sh.m[0];
+  sh.jc = pcg_jc(d, spec.order, spec.ranks);
   const int rm = rank_bucket(spec.order, spec.ranks);
   const bool big = pcg_big(d, spec.order, spec.ranks);
   const size_t smem = big ? pcg_smem_big(spec.order, rm) : pcg_smem(d, spec.order, spec.ranks, rm);
@@ -899,11 +926,11 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   a.x = x;
   a.q = reinterpret_cast<double*>(w);
   a.part = a.q + d;
-  a.rpart = a.part + (size_t)sh.m1 * 2 * sh.dprime;
+  a.rpart = a.part + (size_t)sh.m1 * sh.jc * 2 * sh.dprime;
   a.counter = reinterpret_cast<unsigned*>(a.rpart + 1024);
   a.vglobal = nullptr;
   if (big) {  // after the counter block (pcg_work_bytes(d, order, ranks))
-    const size_t off = ((pcg_work_bytes(d, spec.ranks[0]) + 255) & ~size_t(255));
+    const size_t off = ((pcg_base_bytes(d, spec.order, spec.ranks) + 255) & ~size_t(255));
     a.vglobal = reinterpret_cast<double*>(w + off);
   }
   a.status = status_dev;

@@ -135,3 +135,39 @@ def test_c4_shards_sum_to_full(rt, P):
     with pytest.raises(rt.RtuckerError):
         rt.kron_fiber_sketch(xf.data_ptr(), (I1, I2, I3), a2.data_ptr(), a3.data_ptr(), R2, R3,
                              1e-2, 100, 5, G.data_ptr(), R.data_ptr(), shard=(3, 3))
+
+
+@pytest.mark.parametrize("s,seed", [(1, 1), (1, 2), (2, 3), (7, 4), (7, 5)])
+def test_c4_tiny_sketches(rt, s, seed):
+    """Edge cases of the sort/merge pipeline: a handful of draws, possibly all augmented (no
+    distinct data rows: every bucket empty, D = 0) -- Gram and RHS still match the
+    definition."""
+    import torch
+    I1, I2, I3, R2, R3 = 20, 9, 7, 3, 2
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn(I1, I2, I3, dtype=torch.float32, device="cuda", generator=g)
+    xf = torch.empty_like(x)
+    rt.tensor_fiber_major(x.data_ptr(), (I1, I2, I3), xf.data_ptr())
+    a2 = torch.randn(I2, R2, dtype=torch.float64, device="cuda", generator=g)
+    a3 = torch.randn(I3, R3, dtype=torch.float64, device="cuda", generator=g)
+    W = R2 * R3
+    G = torch.full((W, W), 7.0, dtype=torch.float64, device="cuda")
+    R = torch.full((W, I1), 7.0, dtype=torch.float64, device="cuda")
+    out = rt.kron_fiber_sketch(xf.data_ptr(), (I1, I2, I3), a2.data_ptr(), a3.data_ptr(), R2, R3,
+                               0.5, s, seed, G.data_ptr(), R.data_ptr(), want_draws=True,
+                               fiber_major=True)
+    torch.cuda.synchronize()
+    idx, w = out["indices"], out["weights"]
+    A2, A3, X = a2.cpu().numpy(), a3.cpu().numpy(), x.cpu().numpy().astype(np.float64)
+    total = I2 * I3
+    data = idx < total
+    assert out["data_draws"] == int(data.sum())
+    assert out["unique_rows"] == len(np.unique(idx[data]))
+    j2, j3 = idx[data] // I3, idx[data] % I3
+    Z = np.einsum("tp,tq->tpq", A2[j2], A3[j3]).reshape(-1, W)
+    Gr = (Z * (w[data] ** 2)[:, None]).T @ Z
+    for j, wt in zip(idx[~data] - total, w[~data]):
+        Gr[j, j] += wt * wt * 0.5
+    Rr = (Z * (w[data] ** 2)[:, None]).T @ X[:, j2, j3].T
+    assert np.allclose(G.cpu().numpy(), Gr, rtol=1e-12, atol=1e-12)
+    assert np.allclose(R.cpu().numpy(), Rr, rtol=1e-12, atol=1e-12)

@@ -375,6 +375,159 @@ constexpr size_t kDfibSmem = (size_t)kSeg * 8 + (size_t)kSt * kRC * kQLDT * 8 +
                              (size_t)kSt * kRC * kQLDB * 4;
 static_assert(kDfibSmem * 2 <= 227 * 1024, "two k_c4_dfib CTAs per SM");
 
+// Canonical (row-major) X, I3 % 4 == 0: the sampled values X[i, b, j3] of bucket b lie in the
+// rows X[i, b, :] (contiguous over j3), so instead of gathering strided fibers the kernel
+// reads 16-wide j3 windows of those rows -- only the windows that hold a sampled j3 -- and
+// runs D_b[:, tile] += W_b(window)^T X_b(window) with W_b[j3][q] = c a3(j3)[q] for the
+// sampled j3 (zero rows elsewhere; X values there are masked, so non-finite unsampled
+// entries cannot leak in). Same work items, ring, warp tiling and determinism as k_c4_dfib;
+// the B tile is [i][j3] (64 B row segments, padded to 20 floats: conflict-free fragments).
+constexpr int kSW = 16;            // j3 window per chunk
+constexpr int kSLB = kSW + 4;      // B tile row stride (floats)
+constexpr int kSSt = 3;            // ring stages
+__global__ void __launch_bounds__(256, 2) k_c4_dslab(
+    const float* __restrict__ X, int I1, int I2, int I3, int R3,
+    const unsigned long long* __restrict__ ukey, const double* __restrict__ rows,
+    const int* __restrict__ bstart, int blo, int bhi, double* __restrict__ D) {
+  extern __shared__ __align__(16) double c4s[];
+  unsigned long long* Ks = reinterpret_cast<unsigned long long*>(c4s);     // [kSeg]
+  int* cst = reinterpret_cast<int*>(Ks + kSeg);                            // [kSeg + 1] window starts
+  double* At = reinterpret_cast<double*>(cst + kSeg + 4);                  // [kSSt][kSW][kQLDT] (16 B aligned)
+  float* Bf = reinterpret_cast<float*>(At + kSSt * kSW * kQLDT);           // [kSSt][kDT][kSLB]
+  unsigned* msk = reinterpret_cast<unsigned*>(Bf + kSSt * kDT * kSLB);     // [kSSt] sampled-row masks
+  __shared__ int wsum[8], nwin_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const long long slab = (long long)I2 * I3;
+  const int NT = (I1 + kDT - 1) / kDT;
+  const long long nitems = (long long)(bhi - blo) * NT;
+  for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int b = blo + (int)(item / NT), n0 = (int)(item % NT) * kDT;
+    const int r0 = bstart[b], cnt = bstart[b + 1] - r0;
+    const unsigned long long kb = (unsigned long long)b * I3;
+    double c[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+    for (int seg = 0; seg < cnt; seg += kSeg) {
+      const int len = min(kSeg, cnt - seg);
+      __syncthreads();  // Ks / cst / ring free
+      for (int k = tid; k < len; k += 256) cp_async8(Ks + k, ukey + r0 + seg + k, true);
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      // window list: records k whose window (j3 / kSW) differs from record k-1's start a window
+      {
+        const int per = (len + 255) / 256, k0 = tid * per, k1 = min(len, k0 + per);
+        int n = 0;
+        for (int k = k0; k < k1; ++k)
+          n += (k == 0 || (int)((Ks[k] - kb) / kSW) != (int)((Ks[k - 1] - kb) / kSW));
+        int incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        int off = incl - n;
+        for (int w = 0; w < warp; ++w) off += wsum[w];
+        for (int k = k0; k < k1; ++k)
+          if (k == 0 || (int)((Ks[k] - kb) / kSW) != (int)((Ks[k - 1] - kb) / kSW)) cst[off++] = k;
+        if (tid == 255) {
+          int tot = 0;
+          for (int w = 0; w < 8; ++w) tot += wsum[w];
+          nwin_s = tot;
+          cst[tot] = len;
+        }
+        __syncthreads();
+      }
+      const int nwin = nwin_s;
+      auto load = [&](int ch) {
+        if (ch >= nwin) return;
+        const int sb = ch % kSSt;
+        const int ka = cst[ch], kz = cst[ch + 1];
+        const int j0 = (int)((Ks[ka] - kb) / kSW) * kSW;
+        double* at = At + (size_t)sb * kSW * kQLDT;
+        float* bf = Bf + (size_t)sb * kDT * kSLB;
+        {  // A rows: the window's sampled j3 take their pre-scaled record row, others zero
+          const int r = tid >> 4, pc = tid & 15;
+          int u = -1;
+          for (int k = ka; k < kz; ++k)
+            if ((int)(Ks[k] - kb) - j0 == r) u = k;
+          cp_async16(at + r * kQLDT + 2 * pc,
+                     rows + (u >= 0 ? ((size_t)(r0 + seg + u) * kRowW + 2 * pc) : 0), u >= 0);
+          if (tid < 32) {
+            unsigned m = 0;
+            for (int k = ka; k < kz; ++k) m |= 1u << ((int)(Ks[k] - kb) - j0);
+            if (tid == 0) msk[sb] = m;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // B: the tile's 256 rows X[i, b, j0 .. j0 + 15]
+          const int e = tid + 256 * j, i = e >> 2, pc = e & 3;
+          const bool v = n0 + i < I1 && j0 + 4 * pc < I3;
+          cp_async16(bf + i * kSLB + 4 * pc,
+                     X + (v ? (long long)(n0 + i) * slab + (long long)kb + j0 + 4 * pc : 0), v);
+        }
+      };
+#pragma unroll
+      for (int ch = 0; ch < kSSt - 1; ++ch) {
+        load(ch);
+        cp_async_commit();
+      }
+      for (int ch = 0; ch < nwin; ++ch) {
+        load(ch + kSSt - 1);
+        cp_async_commit();
+        cp_async_wait<kSSt - 1>();
+        __syncthreads();  // window ch landed (and its mask)
+        const int sb = ch % kSSt;
+        const double* at = At + (size_t)sb * kSW * kQLDT;
+        const float* bf = Bf + (size_t)sb * kDT * kSLB + (warp * 32 + g) * kSLB;
+        const unsigned m = msk[sb];
+#pragma unroll
+        for (int ks = 0; ks < kSW; ks += 4) {
+          const int k = ks + t;
+          const bool on = (m >> k) & 1u;
+          double a[4], bv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = at[k * kQLDT + i * 8 + g];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bv[j] = on ? (double)bf[j * 8 * kSLB + k] : 0.0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma_8x8x4(c[i][j][0], c[i][j][1], a[i], bv[j]);
+        }
+        __syncthreads();  // stage sb free
+      }
+      cp_async_wait<0>();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int q = i * 8 + g;
+      if (q >= R3) continue;
+      double* drow = D + ((size_t)(b - blo) * R3 + q) * I1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = n0 + warp * 32 + j * 8 + 2 * t;
+        if (col + 1 < I1 && (I1 % 2 == 0)) {
+          *reinterpret_cast<double2*>(drow + col) = make_double2(c[i][j][0], c[i][j][1]);
+        } else {
+          if (col < I1) drow[col] = c[i][j][0];
+          if (col + 1 < I1) drow[col + 1] = c[i][j][1];
+        }
+      }
+    }
+  }
+}
+
+constexpr size_t kDslabSmem = (size_t)kSeg * 8 + (size_t)(kSeg + 4) * 4 +
+                              (size_t)kSSt * kSW * kQLDT * 8 + (size_t)kSSt * kDT * kSLB * 4 +
+                              kSSt * 4 + 16;
+static_assert(kDslabSmem * 2 <= 227 * 1024, "two k_c4_dslab CTAs per SM");
+
 // ---- fiber-major conversion: out[(i2 I3 + i3) I1 + i1] = x[(i1 I2 + i2) I3 + i3] ----
 // a transpose of the I1 x (I2 I3) matrix in 32 x 32 tiles
 __global__ void k_c4_to_fm(const float* __restrict__ x, long long rows, long long cols,
@@ -567,10 +720,26 @@ void c4_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const d
                                   (int)kDfibSmem));
     attr = true;
   }
-  auto kern = !fiber_major ? k_c4_dfib<0> : (I1 % 4 == 0 ? k_c4_dfib<1> : k_c4_dfib<2>);
   const long long nitems = (long long)nb * ceil_div(I1, kDT);
   const int grid = (int)std::max<long long>(1, std::min<long long>(nitems, 2LL * kNumSMs));
-  kern<<<grid, 256, kDfibSmem, st>>>(x, I1, I2, I3, R3, l.ukey, l.rows, l.bstart, blo, bhi, l.dfib);
+  // canonical X: windows of the rows X[i, b, :] once the sampled rows are dense enough that a
+  // 16-wide window holds more than ~one of them (below, the strided gathers move less)
+  const bool slab_windows = !fiber_major && I3 % 4 == 0 &&
+                            0.5 * (double)s >= 0.03 * (double)I2 * (double)I3;
+  if (slab_windows) {
+    static bool attr_s = false;
+    if (!attr_s) {
+      RTB_CUDA(cudaFuncSetAttribute(k_c4_dslab, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kDslabSmem));
+      attr_s = true;
+    }
+    k_c4_dslab<<<grid, 256, kDslabSmem, st>>>(x, I1, I2, I3, R3, l.ukey, l.rows, l.bstart, blo,
+                                               bhi, l.dfib);
+  } else {
+    auto kern = !fiber_major ? k_c4_dfib<0> : (I1 % 4 == 0 ? k_c4_dfib<1> : k_c4_dfib<2>);
+    kern<<<grid, 256, kDfibSmem, st>>>(x, I1, I2, I3, R3, l.ukey, l.rows, l.bstart, blo, bhi,
+                                       l.dfib);
+  }
   RTB_LAUNCH_CHECK();
   // RHS (R2 x R3 I1) = A2^T D
   const long long n = (long long)R3 * I1;

@@ -481,8 +481,10 @@ __device__ void slice_partials_n3(const PcgArgs& A, const PcgShared& sh, const d
 }
 
 // (B) own rows: q[e] = sum_{j1} partial + augmented diagonal * p[e].
+template <bool JC1>  // JC1: one chunk per slice (the fast order-3 matvec)
 __device__ void reduce_rows(const PcgArgs& A, const PcgShared& sh, const double* p, int row0,
                             int nrows, double* qout) {
+  const int jc = JC1 ? 1 : sh.jc;
   const int dp = sh.dprime, R1 = sh.R[0];
   for (int e = row0 + threadIdx.x; e < row0 + nrows; e += kThreads) {
     const int i1 = e / dp, rest = e - i1 * dp;
@@ -490,8 +492,8 @@ __device__ void reduce_rows(const PcgArgs& A, const PcgShared& sh, const double*
     for (int j1 = 0; j1 < R1; ++j1) {
       const int u1 = upper_pair(min(i1, j1), max(i1, j1), R1);
       const int side = i1 <= j1 ? 0 : 1;
-      for (int ch = 0; ch < sh.jc; ++ch)
-        s += __ldcg(A.part + (((size_t)u1 * sh.jc + ch) * 2 + side) * dp + rest);
+      for (int ch = 0; ch < jc; ++ch)
+        s += __ldcg(A.part + (((size_t)u1 * jc + ch) * 2 + side) * dp + rest);
     }
     const int c = __ldg(A.aug_count + e);
     if (c > 0) s = fma((double)c * A.aug_term, p[e], s);
@@ -565,7 +567,7 @@ __global__ void k_pcg_prep(const double* __restrict__ grams, const double* __res
   }
 }
 
-template <int RM, int RX>
+template <int RM, int RX, bool BIG>
 __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgShared shc) {
   extern __shared__ __align__(16) double sm[];
   const PcgShared& sh = shc;
@@ -574,7 +576,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   double* Ps = sm;                          // [order][RM][RM]: P_n (P form) or V_n (eigen form)
   double* VTs = Ps + sh.order * RM * RM;    // [order][RM][RM]: V_n^T (eigen form)
   // the d-vectors: shared memory, or (large d) this CTA's slice of A.vglobal
-  const bool big = A.vglobal != nullptr;
+  // (BIG is a template parameter so that the shared-memory form keeps LDS/STS accesses)
+  constexpr bool big = BIG;
   double* vb = big ? A.vglobal + (size_t)blockIdx.x * 6 * dv : VTs + sh.order * RM * RM;
   double* dinv = vb;                        // [d]: 1 / (lambda + prod mu) (eigen form)
   double* r = dinv + dv;
@@ -679,7 +682,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
     __syncthreads();
     sync_target += gridDim.x;
     grid_barrier(A.counter, sync_target);
-    reduce_rows(A, sh, p, row0, nrows, A.q);
+    if (fast3) reduce_rows<true>(A, sh, p, row0, nrows, A.q);
+    else reduce_rows<false>(A, sh, p, row0, nrows, A.q);
     __syncthreads();
     sync_target += gridDim.x;
     grid_barrier(A.counter, sync_target);
@@ -724,7 +728,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
     sync_target += gridDim.x;
     grid_barrier(A.counter, sync_target);
     RTB_PCG_MARK(1)
-    reduce_rows(A, sh, p, row0, nrows, A.q);
+    if (fast3) reduce_rows<true>(A, sh, p, row0, nrows, A.q);
+    else reduce_rows<false>(A, sh, p, row0, nrows, A.q);
     __syncthreads();
     RTB_PCG_MARK(2)
     sync_target += gridDim.x;
@@ -782,7 +787,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   else slice_partials<RM>(A, sh, p);
   sync_target += gridDim.x;
   grid_barrier(A.counter, sync_target);
-  reduce_rows(A, sh, p, row0, nrows, A.q);
+  if (fast3) reduce_rows<true>(A, sh, p, row0, nrows, A.q);
+    else reduce_rows<false>(A, sh, p, row0, nrows, A.q);
   __syncthreads();
   double res = 0.0;
   for (int e = row0 + threadIdx.x; e < row0 + nrows; e += kThreads) {
@@ -958,10 +964,13 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   RTB_CUDA(cudaMemsetAsync(a.counter, 0, 64, st));
   bool all16 = true;
   for (int n = 0; n < spec.order; ++n) all16 &= spec.ranks[n] == 16;
-  void* fn = all16 ? (void*)k_pcg<16, 16>
-             : rm == 8 ? (void*)k_pcg<8, 0> : rm == 16 ? (void*)k_pcg<16, 0> : (void*)k_pcg<32, 0>;
-  static bool attr_set[4] = {false, false, false, false};
-  const int slot = all16 ? 3 : rm == 8 ? 0 : rm == 16 ? 1 : 2;
+  void* fn = big ? (rm == 8 ? (void*)k_pcg<8, 0, true>
+                            : rm == 16 ? (void*)k_pcg<16, 0, true> : (void*)k_pcg<32, 0, true>)
+           : all16 ? (void*)k_pcg<16, 16, false>
+           : rm == 8 ? (void*)k_pcg<8, 0, false>
+           : rm == 16 ? (void*)k_pcg<16, 0, false> : (void*)k_pcg<32, 0, false>;
+  static bool attr_set[7] = {false, false, false, false, false, false, false};
+  const int slot = big ? 4 + (rm == 8 ? 0 : rm == 16 ? 1 : 2) : all16 ? 3 : rm == 8 ? 0 : rm == 16 ? 1 : 2;
   if (!attr_set[slot]) {
     RTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr_set[slot] = true;

@@ -30,10 +30,16 @@ rtucker_status rtucker_b200_set_device(int device);
 rtucker_status rtucker_b200_set_stream(void* stream);
 /* Number of this library's kernel launches so far in the process. */
 unsigned long long rtucker_b200_launch_count(void);
+/* Launches so far of one named kernel variant of the headline path ("k_ttm_mid3",
+ * "k_ttm_mid2", "k_ttm_last3", "k_ttm_last3_fused", "k_vech_bucket2<17>",
+ * "k_vech_contract2", "k_pcg<16,16>"): lets tests assert which kernel ran. */
+unsigned long long rtucker_b200_variant_count(const char* name);
 
 /* Wrap a tensor that already lives in device memory of the current device.
- * The data is copied (device to device); rtucker_tensor_data() returns NULL
- * for such a tensor (no host mirror) and sets the last error. */
+ * The data is copied (device to device) before the call returns, so the caller may
+ * free or reuse data_device afterwards. There is no host mirror until one is asked
+ * for: rtucker_tensor_data() then downloads a host copy (device to host) and
+ * returns it (borrowed, valid for the tensor's lifetime). */
 rtucker_status rtucker_b200_tensor_create_device(const uint64_t* shape, uint32_t order,
                                                  const double* data_device,
                                                  rtucker_tensor** out);
@@ -76,7 +82,9 @@ typedef struct rtucker_b200_als_ext {
    * plus the sqrt(lambda) augmentation (BASELINE "samples per factor update"; DESIGN.md
    * section 3). 0 (default) = the reference's exact factor updates. Not with sharding. */
   uint32_t factor_samples;
-  int reserved[3];
+  /* 1 = enqueue every sweep kernel by kernel (no CUDA graph; results are identical) */
+  int disable_graph;
+  int reserved[2];
 } rtucker_b200_als_ext;
 
 rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* ranks,
@@ -94,6 +102,11 @@ rtucker_status rtucker_b200_session_create(const rtucker_tensor* x, const uint64
 rtucker_status rtucker_b200_session_sweeps(rtucker_b200_session* s, uint32_t n);
 rtucker_status rtucker_b200_session_result(rtucker_b200_session* s, rtucker_als_result** out);
 void rtucker_b200_session_free(rtucker_b200_session* s);
+
+/* Sweeps of a result that ran as one CUDA graph launch (from the second sweep on, when
+ * the path allows it: sketched core with the CG solve, no per-kernel profiling, no
+ * sharding; RTB_NO_GRAPH=1 disables). */
+uint64_t rtucker_b200_result_graph_sweeps(const rtucker_als_result* r);
 
 /* Device seconds of the sweep loop of a result (CUDA events). */
 double rtucker_b200_result_sweep_seconds(const rtucker_als_result* r);

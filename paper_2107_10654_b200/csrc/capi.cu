@@ -434,6 +434,21 @@ std::vector<uint64_t> engine_shape(const rtucker_tensor* x, const rtb::AlsOption
   return sh;
 }
 
+static void apply_ext(rtb::AlsOptions& o, const rtucker_b200_als_ext* ext) {
+  if (!ext) return;
+  o.init_core = ext->init_core;
+  o.init_factors = ext->init_factors;
+  o.shard_rank = ext->shard_rank;
+  o.shard_count = ext->shard_count ? ext->shard_count : 1;
+  o.allreduce = ext->allreduce;
+  o.allreduce_user = ext->allreduce_user;
+  o.profile = ext->profile_kernels != 0;
+  o.core_solver = ext->core_solver;
+  o.fast_loss = ext->fast_loss != 0;
+  o.factor_samples = ext->factor_samples;
+  o.no_graph = ext->disable_graph != 0;
+}
+
 rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* ranks,
                                        uint32_t order, const rtucker_als_options* opts,
                                        const rtucker_b200_als_ext* ext,
@@ -443,18 +458,7 @@ rtucker_status rtucker_b200_als_run_ex(const rtucker_tensor* x, const uint64_t* 
     rtb::AlsOptions o = to_options(opts);
     if (order != x->shape.size()) throw rtb::Error(1, "als: ranks order != tensor order");
     if (o.max_iterations == 0) throw rtb::Error(1, "als: max_iterations must be >= 1");
-    if (ext) {
-      o.init_core = ext->init_core;
-      o.init_factors = ext->init_factors;
-      o.shard_rank = ext->shard_rank;
-      o.shard_count = ext->shard_count ? ext->shard_count : 1;
-      o.allreduce = ext->allreduce;
-      o.allreduce_user = ext->allreduce_user;
-      o.profile = ext->profile_kernels != 0;
-      o.core_solver = ext->core_solver;
-      o.fast_loss = ext->fast_loss != 0;
-      o.factor_samples = ext->factor_samples;
-    }
+    apply_ext(o, ext);
     auto r = std::make_unique<rtucker_als_result>();
     rtb::als_run(x->device(), engine_shape(x, o, ext), std::vector<uint64_t>(ranks, ranks + order),
                  o, r->out);
@@ -480,18 +484,7 @@ rtucker_status rtucker_b200_session_create(const rtucker_tensor* x, const uint64
   return guarded([&] {
     rtb::AlsOptions o = to_options(opts);
     if (order != x->shape.size()) throw rtb::Error(1, "als: ranks order != tensor order");
-    if (ext) {
-      o.init_core = ext->init_core;
-      o.init_factors = ext->init_factors;
-      o.shard_rank = ext->shard_rank;
-      o.shard_count = ext->shard_count ? ext->shard_count : 1;
-      o.allreduce = ext->allreduce;
-      o.allreduce_user = ext->allreduce_user;
-      o.profile = ext->profile_kernels != 0;
-      o.core_solver = ext->core_solver;
-      o.fast_loss = ext->fast_loss != 0;
-      o.factor_samples = ext->factor_samples;
-    }
+    apply_ext(o, ext);
     auto s = std::make_unique<rtucker_b200_session>();
     s->s.reset(rtb::session_create(x->device(), engine_shape(x, o, ext),
                                    std::vector<uint64_t>(ranks, ranks + order), o));
@@ -694,6 +687,14 @@ rtucker_status rtucker_b200_set_device(int device) {
 
 unsigned long long rtucker_b200_launch_count(void) { return rtb::launch_counter(); }
 
+uint64_t rtucker_b200_result_graph_sweeps(const rtucker_als_result* r) {
+  return r ? r->out.graph_launches : 0;
+}
+
+unsigned long long rtucker_b200_variant_count(const char* name) {
+  return name ? rtb::variant_count(name) : 0;
+}
+
 rtucker_status rtucker_b200_set_stream(void* stream) {
   rtb::set_stream(static_cast<cudaStream_t>(stream));
   return RTUCKER_OK;
@@ -710,6 +711,8 @@ rtucker_status rtucker_b200_tensor_create_device(const uint64_t* shape, uint32_t
     cudaStream_t st = rtb::current_stream();
     t->dev.ensure(v * 8, st);
     RTB_CUDA(cudaMemcpyAsync(t->dev.p, data_device, v * 8, cudaMemcpyDeviceToDevice, st));
+    // the caller may free or reuse the source as soon as we return
+    RTB_CUDA(cudaStreamSynchronize(st));
     t->dev_valid = true;
     *out = t.release();
   });

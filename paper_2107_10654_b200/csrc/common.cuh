@@ -1,6 +1,7 @@
 // common.cuh -- shared device helpers for the sm_100a kernels.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <stdexcept>
@@ -24,7 +25,20 @@ struct Error : std::runtime_error {
 
 // Every launch site ends with RTB_LAUNCH_CHECK(): it checks the launch and
 // counts it (rtucker_b200_launch_count exposes the total for bench.py).
-unsigned long long& launch_counter();
+std::atomic<unsigned long long>& launch_counter();
+
+// Per-variant launch counters for the headline kernels (tests assert which kernel a
+// configuration actually ran; rtucker_b200_variant_count).
+void count_variant(const char* name);
+unsigned long long variant_count(const char* name);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel): the
+// attribute is per device, so the cache is keyed by the current device ordinal.
+void set_max_smem_impl(const void* fn, int bytes);
+template <typename F>
+inline void set_max_smem(F* fn, int bytes) {
+  set_max_smem_impl(reinterpret_cast<const void*>(fn), bytes);
+}
 #define RTB_LAUNCH_CHECK()          \
   do {                              \
     RTB_CUDA(cudaGetLastError());   \

@@ -53,9 +53,38 @@ cudaStream_t current_stream() {
 
 void set_stream(cudaStream_t s) { t_stream = s; }
 
-unsigned long long& launch_counter() {
-  static unsigned long long n = 0;
+std::atomic<unsigned long long>& launch_counter() {
+  static std::atomic<unsigned long long> n{0};
   return n;
+}
+
+namespace {
+std::mutex g_variant_mu;
+std::map<std::string, unsigned long long>& variants() {
+  static std::map<std::string, unsigned long long> m;
+  return m;
+}
+}  // namespace
+void count_variant(const char* name) {
+  std::lock_guard<std::mutex> lk(g_variant_mu);
+  ++variants()[name];
+}
+unsigned long long variant_count(const char* name) {
+  std::lock_guard<std::mutex> lk(g_variant_mu);
+  auto it = variants().find(name);
+  return it == variants().end() ? 0 : it->second;
+}
+
+void set_max_smem_impl(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  RTB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[{dev, fn}];
+  if (have >= bytes) return;
+  RTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
 }
 
 DevBuf::DevBuf(size_t b, cudaStream_t s) { ensure(b, s); }
@@ -258,6 +287,39 @@ __global__ void k_check_finite(const double* v, long long n, int* bad) {
   if (i < n && !isfinite(v[i])) atomicExch(bad, 1);
 }
 
+// Per-sweep seeds from device counters, so a captured sweep draws new ones every launch:
+// seeds[0] = sketch_rng.next_u64() for sweep k (ref tucker.cpp:254-255), seeds[1 + n] =
+// factor_rng.next_u64() for the n-th sketched factor update (perf mode, orc_als_fs).
+__global__ void k_sweep_seeds(unsigned long long* seeds, unsigned long long* ctr,
+                              unsigned long long sketch_rng, unsigned long long factor_rng,
+                              int nf) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long k = ctr[0], f = ctr[1];
+  seeds[0] = sm_at(sketch_rng, k);
+  for (int n = 0; n < nf; ++n) seeds[1 + n] = sm_at(factor_rng, f + n);
+  ctr[0] = k + 1;
+  ctr[1] = f + nf;
+}
+
+// Verdict of a PCG core solve for the host: post = {PCG status, iterations, zero-factor
+// flag, core not finite}; the warm-start flag of the next solve = accepted and finite.
+__global__ void k_core_post(const double* __restrict__ core, long long d, const int* pcg_status,
+                            const int* zero_flag, int* warm, int* post) {
+  int bad = 0;
+  for (long long i = threadIdx.x; i < d; i += blockDim.x) bad |= !isfinite(core[i]);
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    const int ok = pcg_status[0] == 0 && *zero_flag == 0;
+    post[0] = pcg_status[0];
+    post[1] = pcg_status[1];
+    post[2] = *zero_flag;
+    post[3] = bad;
+    *warm = ok && !bad;
+  }
+}
+
+__global__ void k_set_int(int* p, int v) { *p = v; }
+
 // Grid-stride finiteness scan (exponent field all ones = Inf/NaN), 2 doubles per load.
 __global__ void k_all_finite(const double* v, long long n, int* bad) {
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -440,6 +502,8 @@ class Engine {
     // (orc_als_fs), one next_u64 per (sweep, mode)
     factor_rng_ = sm_at(opt_.seed, 1) ^ 0x5851f42d4c957f2dULL;
     factor_k_ = 0;
+    RTB_CUDA(cudaMemsetAsync(ctr_dev_.p, 0, 16, st_));
+    RTB_CUDA(cudaMemsetAsync(warm_dev_.p, 0, 4, st_));
     scores_valid_ = false;
     t_valid_ = false;
   }
@@ -452,39 +516,131 @@ class Engine {
   }
 
   // ---- one sweep ----
+  // Enqueues sweep `iter` without a host round trip: the per-sweep seeds come from device
+  // counters (k_sweep_seeds), the core solve's verdict goes to pinned host memory behind
+  // the step event core_done (resolve_core() reads it while the GPU runs the loss pass),
+  // and from the second sweep on the whole sweep is one CUDA graph launch when the path
+  // allows it (sketched core with the PCG solve, no profiling, no sharding).
   void sweep(uint32_t iter) {
+    const int rows = opt_.record_history ? N_ + 1 : 1;
+    ensure_hist(hist_rows_.size() + rows);
+    const size_t first = hist_rows_.size();
+    if (opt_.record_history)
+      for (int n = 0; n < N_; ++n) hist_rows_.push_back({iter, "F" + std::to_string(n + 1)});
+    hist_rows_.push_back({iter, "Core"});
+    core_row_ = hist_rows_.size() - 1;
+    if (graph_ok() && sweeps_enqueued_ >= 1 && !gexec_) capture_sweep();
+    if (gexec_) {
+      RTB_CUDA(cudaGraphLaunch(gexec_, st_));
+      launch_counter() += graph_kernels_;
+      ++graph_launches_;
+      RTB_CUDA(cudaMemcpyAsync(hist_loss(first), loss_rows_.p, (size_t)rows * 16,
+                               cudaMemcpyDeviceToDevice, st_));
+    } else {
+      sweep_body(hist_loss(first));
+    }
+    core_pending_ = opt_.sketched && deferred_core_;
+    ++sweeps_enqueued_;
+    iterations_ = iter;
+    if (!core_pending_) {  // exact core / non-CG solve: the stream was synchronised inside
+      RTB_CUDA(cudaEventSynchronize(step_ev_[2 * N_ + 1]));
+      collect_steps();
+    }
+  }
+
+  // the kernels of one sweep; loss rows (loss, rmse) go to rows[0..]
+  void sweep_body(double* rows) {
+    k_sweep_seeds<<<1, 32, 0, st_>>>(seed_dev_.as<unsigned long long>(),
+                                     ctr_dev_.as<unsigned long long>(), sketch_rng_, factor_rng_,
+                                     (opt_.factor_samples > 0 && N_ >= 2) ? N_ : 0);
+    RTB_LAUNCH_CHECK();
+    int r = 0;
     for (int n = 0; n < N_; ++n) {
-      cudaEvent_t a, b;
-      RTB_CUDA(cudaEventCreate(&a));
-      RTB_CUDA(cudaEventCreate(&b));
-      RTB_CUDA(cudaEventRecord(a, st_));
+      rec(step_ev_[2 * n]);
       if (opt_.factor_samples > 0 && N_ >= 2)
-        update_factor_sketched(n, sm_at(factor_rng_, factor_k_++));
+        update_factor_sketched(n, 0, seed_dev_.as<unsigned long long>() + 1 + n);
       else
         update_factor(n);
-      RTB_CUDA(cudaEventRecord(b, st_));
-      step_events_.push_back({n, a, b});
+      rec(step_ev_[2 * n + 1]);
       if (opt_.record_history) {
-        hist_rows_.push_back({iter, "F" + std::to_string(n + 1)});
-        record_loss(hist_rows_.size() - 1);
+        loss_pass(rows + 2 * r, rows + 2 * r + 1);
+        ++r;
       }
     }
-    cudaEvent_t a, b;
-    RTB_CUDA(cudaEventCreate(&a));
-    RTB_CUDA(cudaEventCreate(&b));
-    RTB_CUDA(cudaEventRecord(a, st_));
+    rec(step_ev_[2 * N_]);
+    deferred_core_ = false;
     if (opt_.sketched) {
-      // per-sweep sketch seed = sketch_seed_rng.next_u64() (ref tucker.cpp:254-255)
-      const uint64_t seed = sm_at(sketch_rng_, sketch_k_++);
-      update_core_sketched(seed);
+      // per-sweep sketch seed = sketch_seed_rng.next_u64() (ref tucker.cpp:254-255), read
+      // from seed_dev_[0] on the device
+      update_core_sketched(0, seed_dev_.as<unsigned long long>(), true);
     } else {
       update_core_exact();
     }
-    RTB_CUDA(cudaEventRecord(b, st_));
-    step_events_.push_back({N_, a, b});
-    hist_rows_.push_back({iter, "Core"});
-    record_loss(hist_rows_.size() - 1);
-    iterations_ = iter;
+    rec(step_ev_[2 * N_ + 1]);  // = core_done: the core verdict is in post_host_ after it
+    loss_pass(rows + 2 * r, rows + 2 * r + 1);
+  }
+
+  void rec(cudaEvent_t e) {
+    if (capturing_) RTB_CUDA(cudaEventRecordWithFlags(e, st_, cudaEventRecordExternal));
+    else RTB_CUDA(cudaEventRecord(e, st_));
+  }
+
+  bool graph_ok() const {
+    static const bool off = std::getenv("RTB_NO_GRAPH") != nullptr;
+    return !off && !opt_.no_graph && !graph_failed_ && opt_.sketched && !opt_.profile && !sharded() &&
+           pcg_path_ && !opt_.fast_loss;
+  }
+
+  // Stream-captures one steady-state sweep into gexec_ (loss rows into loss_rows_). Any
+  // failure leaves the engine on the eager path.
+  void capture_sweep() {
+    const unsigned long long before = launch_counter();
+    cudaGraph_t g = nullptr;
+    RTB_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed));
+    capturing_ = true;
+    try {
+      sweep_body(loss_rows_.as<double>());
+    } catch (...) {
+      capturing_ = false;
+      cudaStreamEndCapture(st_, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      graph_failed_ = true;
+      launch_counter() -= launch_counter() - before;
+      return;
+    }
+    capturing_ = false;
+    cudaError_t e = cudaStreamEndCapture(st_, &g);
+    if (e == cudaSuccess && deferred_core_)
+      e = cudaGraphInstantiateWithFlags(&gexec_, g, 0);
+    if (g) cudaGraphDestroy(g);
+    graph_kernels_ = launch_counter() - before;
+    launch_counter() -= graph_kernels_;  // counted per graph launch instead
+    if (e != cudaSuccess || !deferred_core_) {
+      cudaGetLastError();
+      gexec_ = nullptr;
+      graph_failed_ = true;
+    }
+  }
+
+  void drop_graph() {
+    if (gexec_) cudaGraphExecDestroy(gexec_);
+    gexec_ = nullptr;
+  }
+
+  // Lookbehind check of the sweep just enqueued: waits for its core_done event (the GPU
+  // meanwhile runs that sweep's loss pass, and the host then enqueues the next sweep
+  // behind it), reads the core solve's verdict, and runs the fallback solve plus a fresh
+  // loss pass for that sweep if the PCG answer was not accepted.
+  void resolve_core() {
+    if (!core_pending_) return;
+    core_pending_ = false;
+    RTB_CUDA(cudaEventSynchronize(step_ev_[2 * N_ + 1]));
+    collect_steps();
+    if (finish_core_solve()) {
+      drop_graph();  // the fallback may have (re)allocated workspaces
+      record_loss(core_row_);
+    }
   }
 
   double last_loss_host() {
@@ -506,6 +662,7 @@ class Engine {
   }
 
   void output(AlsOutput& out) {
+    resolve_core();
     RTB_CUDA(cudaStreamSynchronize(st_));
     out.shape = shape_;
     out.ranks = ranks_;
@@ -523,11 +680,9 @@ class Engine {
     out.timings.assign(N_ + 1, StepTiming{});
     for (int n = 0; n < N_; ++n) out.timings[n].step = "F" + std::to_string(n + 1);
     out.timings[N_].step = "Core";
-    for (auto& e : step_events_) {
-      float ms = 0.f;
-      RTB_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
-      out.timings[e.step].total += ms * 1e-3;
-      out.timings[e.step].count += 1;
+    for (int k = 0; k <= N_; ++k) {
+      out.timings[k].total = step_total_[k];
+      out.timings[k].count = step_count_[k];
     }
     prof_.collect();
     out.kernels.clear();
@@ -544,12 +699,23 @@ class Engine {
     out.last_solver_path = last_solver_path_;
     out.last_pcg_iterations = last_pcg_iters_;
     out.sweep_seconds = sweep_seconds_;
+    out.graph_launches = graph_launches_;
   }
 
   ~Engine() {
-    for (auto& e : step_events_) {
-      cudaEventDestroy(e.a);
-      cudaEventDestroy(e.b);
+    if (gexec_) cudaGraphExecDestroy(gexec_);
+    for (auto e : step_ev_)
+      if (e) cudaEventDestroy(e);
+    if (post_host_) cudaFreeHost(post_host_);
+  }
+
+  // Adds the elapsed times of the last sweep's step events (the stream has passed them).
+  void collect_steps() {
+    for (int k = 0; k <= N_; ++k) {
+      float ms = 0.f;
+      RTB_CUDA(cudaEventElapsedTime(&ms, step_ev_[2 * k], step_ev_[2 * k + 1]));
+      step_total_[k] += ms * 1e-3;
+      step_count_[k] += 1;
     }
   }
 
@@ -628,14 +794,33 @@ class Engine {
   bool scores_valid_ = false;
   DevBuf fsums_, fsk_idx_, fsk_w_, fsk_work_;
   bool t_valid_ = false;
-  bool warm_core_ = false;  // core_ holds a previous sketched solve's solution
   uint64_t last_s_ = 0;
   int last_rank_deficient_ = 0, last_solver_path_ = 0, last_pcg_iters_ = 0;
-  struct StepEv {
-    int step;
-    cudaEvent_t a, b;
-  };
-  std::vector<StepEv> step_events_;
+  // step events of the sweep in flight: (start, end) per step, F_1..F_N then Core; the
+  // Core end event is also the point after which the core verdict is in post_host_
+  cudaEvent_t step_ev_[2 * (kMaxOrder + 1)] = {};
+  double step_total_[kMaxOrder + 1] = {};
+  uint64_t step_count_[kMaxOrder + 1] = {};
+  // per-sweep device seeds / counters, the core verdict, CUDA graph of a sweep
+  DevBuf seed_dev_, ctr_dev_, post_, warm_dev_, loss_rows_;
+  int* post_host_ = nullptr;  // pinned
+  bool pcg_path_ = false, deferred_core_ = false, core_pending_ = false;
+  bool capturing_ = false, graph_failed_ = false;
+  cudaGraphExec_t gexec_ = nullptr;
+  unsigned long long graph_kernels_ = 0;
+  uint64_t graph_launches_ = 0;
+  uint64_t sweeps_enqueued_ = 0;
+  size_t core_row_ = 0;
+  // history rows (loss, rmse) on the device; grown on demand (copying the rows so far)
+  size_t hist_cap_ = 0;
+  void ensure_hist(size_t rows) {
+    if (rows <= hist_cap_) return;
+    const size_t cap = std::max(rows, 2 * hist_cap_);
+    DevBuf nb(cap * 16 + 16, st_);
+    if (hist_cap_) RTB_CUDA(cudaMemcpyAsync(nb.p, hist_.p, hist_cap_ * 16, cudaMemcpyDeviceToDevice, st_));
+    hist_ = std::move(nb);
+    hist_cap_ = cap;
+  }
   struct HRow {
     uint32_t iter;
     std::string step;
@@ -724,7 +909,7 @@ class Engine {
     xx_.ensure(8, st_);
     loss_need_.ensure(8, st_);
     yq_.ensure(2 * (d_ + 1) * 8, st_);
-    hist_.ensure((size_t)std::max<uint32_t>(opt_.max_iterations, 1) * (N_ + 1) * 16 + 16, st_);
+    ensure_hist((size_t)std::max<uint32_t>(opt_.max_iterations, 1) * (N_ + 1));
     init_loss_.ensure(16, st_);
     uint64_t sum_rows = 0;
     for (auto s : shape_) sum_rows += s;
@@ -754,6 +939,21 @@ class Engine {
     int ns[64];
     for (int i = 0; i < 64; ++i) ns[i] = i < N_ ? (int)ranks_[i] : 1;
     RTB_CUDA(cudaMemcpyAsync(ns_.p, ns, 64 * 4, cudaMemcpyHostToDevice, st_));
+    seed_dev_.ensure(16 * 8, st_);
+    ctr_dev_.ensure(2 * 8, st_);
+    post_.ensure(8 * 4, st_);
+    warm_dev_.ensure(4, st_);
+    loss_rows_.ensure((size_t)(N_ + 1) * 16, st_);
+    RTB_CUDA(cudaMemsetAsync(ctr_dev_.p, 0, 16, st_));
+    RTB_CUDA(cudaMemsetAsync(warm_dev_.p, 0, 4, st_));
+    RTB_CUDA(cudaHostAlloc((void**)&post_host_, 8 * sizeof(int), cudaHostAllocDefault));
+    for (int k = 0; k < 2 * (N_ + 1); ++k) RTB_CUDA(cudaEventCreate(&step_ev_[k]));
+    {
+      int rk[8] = {0};
+      for (int n = 0; n < N_; ++n) rk[n] = (int)ranks_[n];
+      pcg_path_ = opt_.core_solver == 0 && opt_.lambda > 0.0 && rmax_ <= 32 &&
+                  pcg_supported((int)d_, N_, rk);
+    }
     RTB_CUDA(cudaStreamSynchronize(st_));  // host arrays above go out of scope
   }
 
@@ -939,7 +1139,8 @@ class Engine {
   }
 
   // ---- sketched core (ref tucker.cpp:141-166, sketch_ridge.cpp:52-151) ----
-  void update_core_sketched(uint64_t seed) {
+  void update_core_sketched(uint64_t seed, const unsigned long long* seed_dev = nullptr,
+                            bool defer = false) {
     uint64_t s = opt_.sample_override;
     if (s == 0) s = sample_count_formula(0.5, d_, opt_.epsilon, opt_.delta);
     last_s_ = s;
@@ -955,6 +1156,7 @@ class Engine {
     ds.total_rows = total_;
     ds.d = d_;
     ds.seed = seed;
+    ds.seed_dev = seed_dev;
     ds.s = s;
     sk_idx_.ensure(s * 8, st_);
     sk_w_.ensure(s * 8, st_);
@@ -966,11 +1168,12 @@ class Engine {
                   DrawWork{draw_work_.p, draw_work_.bytes}, (unsigned long long*)sk_idx_.p,
                   sk_w_.as<double>(), flag_.as<int>(), st_);
     }
-    solve_sketch(s);
+    solve_sketch(s, defer);
   }
 
   // ---- sketched factor update (perf mode; k_fsketch.cu, orc_update_factor_sketched) ----
-  void update_factor_sketched(int n, uint64_t seed) {
+  void update_factor_sketched(int n, uint64_t seed,
+                              const unsigned long long* seed_dev = nullptr) {
     if (sharded()) throw Error(1, "sketched factor updates are not supported with sharding");
     const int Rn = (int)ranks_[n], In = (int)shape_[n];
     if (Rn > 32) {  // the register-tiled gather kernel covers R_n <= 32
@@ -996,6 +1199,7 @@ class Engine {
     ds.total_rows = total_o;
     ds.d = (uint64_t)Rn;
     ds.seed = seed;
+    ds.seed_dev = seed_dev;
     ds.s = s;
     fsums_.ensure(8 * 8, st_);
     // score sums of the other modes, in order
@@ -1113,37 +1317,25 @@ class Engine {
   }
 
  public:
-  // normal equations from sk_idx_/sk_w_ (s draws) and solve into the core
-  void solve_sketch(uint64_t s) {
+  // normal equations from sk_idx_/sk_w_ (s draws) and solve into the core. With `defer`
+  // (a sweep) and the PCG path, nothing waits here: k_core_post writes the verdict (PCG
+  // status, zero-factor flag, finiteness of the core) to pinned host memory and the
+  // caller's resolve_core() acts on it; otherwise the verdict is resolved right away.
+  void solve_sketch(uint64_t s, bool defer = false) {
     GramSpec gs = gram_spec(s);
     gram_work_.ensure(gram_work_bytes(gs), st_);
     rhs_.ensure(d_ * 8, st_);
     int rk[8];
     for (int n = 0; n < N_; ++n) rk[n] = (int)ranks_[n];
-    const bool try_pcg = opt_.core_solver == 0 && opt_.lambda > 0.0 && rmax_ <= 32 &&
-                         pcg_supported((int)d_, N_, rk);
-    // X slab pointer offset so that global flat indices of this shard's draws land in it
-    const double* xg = x_ - (sharded() ? lo_ * (long long)(total_ / shape_[0]) : 0);
-    auto normal_eq = [&](bool full) {
-      Scope sc(prof_, "gram");
-      if (full) G_.ensure(d_ * d_ * 8, st_);
-      // the full Gram is expanded after the shard sum of the compact one
-      sketch_normal_eq(gs, xg, (const unsigned long long*)sk_idx_.p, sk_w_.as<double>(),
-                       gram_work_.p, gram_work_.bytes, (full && !sharded()) ? G_.as<double>() : nullptr,
-                       rhs_.as<double>(), (unsigned long long*)data_draws_.p, st_);
-      if (sharded()) {
-        size_t ns = 0;
-        double* S = gram_compact(gs, gram_work_.p, &ns);
-        allreduce(S, ns);
-        allreduce(rhs_.as<double>(), d_);
-        if (full) gram_expand_full(gs, gram_work_.p, G_.as<double>(), st_);
-      }
-    };
-    normal_eq(!try_pcg);
-    int status[2] = {0, 0};
-    if (try_pcg) {
+    last_s_ = s;
+    normal_eq(s, !pcg_path_);
+    if (!pcg_path_) {
+      solve_fallback(s, false);
+      return;
+    }
+    {
       // Kronecker-preconditioned CG on the blocked Gram (k_pcg.cu), verified by its
-      // true residual; the Cholesky path below is the fallback
+      // true residual; the Cholesky path (solve_fallback) takes over on failure
       Scope sc(prof_, "pcg");
       blocks_.ensure((size_t)gram_block_elems(gs) * 8, st_);
       gram_expand_blocks(gs, gram_work_.p, blocks_.as<double>(), st_);
@@ -1156,7 +1348,6 @@ class Engine {
       ps.linv_stride = eig_stride_;
       ps.linv_ok = spd_ok_.as<int>();
       ps.grams = grams_.as<double>();
-      ps.lambda = opt_.lambda;
       double* prep = reinterpret_cast<double*>(pst_.as<int>() + 64);
       int* eskip = pst_.as<int>() + 32;
       pcg_prepare(ps, prep, eskip, st_);
@@ -1170,24 +1361,77 @@ class Engine {
       ps.max_iter = 80;
       ps.tol = 1e-15;
       ps.check_tol = 1e-12;
-      // warm start from the current core (the previous sweep's solution); the first
-      // sketch of a run starts cold (the core is the random init then)
-      ps.warm = warm_core_ ? 1 : 0;
+      // warm start from the current core (the previous accepted solve's solution; the
+      // first sketch of a run starts cold from the random init): a device flag
+      ps.warm_dev = warm_dev_.as<int>();
       pcg_work_.ensure(pcg_work_bytes((int)d_, N_, rk), st_);
       pcg_solve(ps, blocks_.as<double>(), rhs_.as<double>(), core_.as<double>(), pcg_work_.p,
                 pcg_status_.as<int>(), st_);
-      int ps_out[2] = {1, 0};
-      RTB_CUDA(cudaMemcpyAsync(ps_out, pcg_status_.p, 8, cudaMemcpyDeviceToHost, st_));
-      RTB_CUDA(cudaMemcpyAsync(&status[1], zero_flag_.p, 4, cudaMemcpyDeviceToHost, st_));
-      RTB_CUDA(cudaStreamSynchronize(st_));
-      last_pcg_iters_ = ps_out[1];
-      if (ps_out[0] == 0 && !status[1]) {
-        warm_core_ = true;
-        last_solver_path_ = 2;
-        last_rank_deficient_ = 0;
-        check_core_finite();
-        return;
-      }
+    }
+    k_core_post<<<1, 1024, 0, st_>>>(core_.as<double>(), (long long)d_, pcg_status_.as<int>(),
+                                     zero_flag_.as<int>(), warm_dev_.as<int>(), post_.as<int>());
+    RTB_LAUNCH_CHECK();
+    RTB_CUDA(cudaMemcpyAsync(post_host_, post_.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st_));
+    if (defer) {
+      deferred_core_ = true;
+      return;
+    }
+    RTB_CUDA(cudaStreamSynchronize(st_));
+    finish_core_solve();
+  }
+
+  // Acts on the verdict of a PCG core solve (post_host_, after the stream passed
+  // k_core_post). Returns true if the core was recomputed by the fallback path.
+  bool finish_core_solve() {
+    const int* ps = post_host_;
+    last_pcg_iters_ = ps[1];
+    if (ps[0] == 0 && !ps[2]) {
+      if (ps[3]) throw Error(1, "DenseTensor: non-finite entry");  // ref tensor.cpp:32-42
+      last_solver_path_ = 2;
+      last_rank_deficient_ = 0;
+      return false;
+    }
+    solve_fallback(last_s_, true);
+    return true;
+  }
+
+  // sketched normal equations of the current draws (compact Gram in the workspace, rhs;
+  // with `full` the d x d Gram in G_ as well)
+  void normal_eq(uint64_t s, bool full) {
+    GramSpec gs = gram_spec(s);
+    // X slab pointer offset so that global flat indices of this shard's draws land in it
+    const double* xg = x_ - (sharded() ? lo_ * (long long)(total_ / shape_[0]) : 0);
+    Scope sc(prof_, "gram");
+    if (full) G_.ensure(d_ * d_ * 8, st_);
+    // the full Gram is expanded after the shard sum of the compact one
+    sketch_normal_eq(gs, xg, (const unsigned long long*)sk_idx_.p, sk_w_.as<double>(),
+                     gram_work_.p, gram_work_.bytes, (full && !sharded()) ? G_.as<double>() : nullptr,
+                     rhs_.as<double>(), (unsigned long long*)data_draws_.p, st_);
+    if (sharded()) {
+      size_t ns = 0;
+      double* S = gram_compact(gs, gram_work_.p, &ns);
+      allreduce(S, ns);
+      allreduce(rhs_.as<double>(), d_);
+      if (full) gram_expand_full(gs, gram_work_.p, G_.as<double>(), st_);
+    }
+  }
+
+  // Cholesky of the full Gram (expanded from the compact one when the PCG path built
+  // only the blocks), the zero-core rule and the pinv fallback; synchronous (a rare path
+  // after a PCG failure, or the solve itself when CG does not apply)
+  void solve_fallback(uint64_t s, bool after_pcg) {
+    GramSpec gs = gram_spec(s);
+    int status[2] = {0, 0};
+    RTB_CUDA(cudaMemcpyAsync(&status[1], zero_flag_.p, 4, cudaMemcpyDeviceToHost, st_));
+    RTB_CUDA(cudaStreamSynchronize(st_));
+    if (status[1]) {  // a zero factor: the minimiser is the zero core (tucker.cpp:148-154)
+      RTB_CUDA(cudaMemsetAsync(core_.p, 0, d_ * 8, st_));
+      last_solver_path_ = 0;
+      last_rank_deficient_ = 0;
+      set_warm(0);
+      return;
+    }
+    if (after_pcg) {
       G_.ensure(d_ * d_ * 8, st_);
       gram_expand_full(gs, gram_work_.p, G_.as<double>(), st_);
     }
@@ -1198,17 +1442,12 @@ class Engine {
                  chol_work_.p, st_);
     }
     RTB_CUDA(cudaMemcpyAsync(&status[0], chol_status_.p, 4, cudaMemcpyDeviceToHost, st_));
-    RTB_CUDA(cudaMemcpyAsync(&status[1], zero_flag_.p, 4, cudaMemcpyDeviceToHost, st_));
     RTB_CUDA(cudaStreamSynchronize(st_));
     last_solver_path_ = 0;
     last_rank_deficient_ = 0;
-    if (status[1]) {  // a zero factor: the minimiser is the zero core (tucker.cpp:148-154)
-      RTB_CUDA(cudaMemsetAsync(core_.p, 0, d_ * 8, st_));
-      return;
-    }
     if (status[0]) {
       // not positive definite: recompute the Gram and take the pinv route
-      normal_eq(true);  // Cholesky overwrote G and rhs: rebuild them
+      normal_eq(s, true);  // Cholesky overwrote G and rhs: rebuild them
       if (d_ > 64) {  // dense eigen pinv with the reference cutoff (k_pinv.cu)
         Scope sc(prof_, "pinv");
         pinv_work_.ensure(pinv_large_work_bytes((int)d_), st_);
@@ -1220,7 +1459,7 @@ class Engine {
         RTB_CUDA(cudaStreamSynchronize(st_));
         last_solver_path_ = 1;
         last_rank_deficient_ = rank < (int)d_;
-        warm_core_ = false;
+        set_warm(0);
         check_core_finite();
         return;
       }
@@ -1238,13 +1477,19 @@ class Engine {
       RTB_CUDA(cudaStreamSynchronize(st_));
       last_solver_path_ = 1;
       last_rank_deficient_ = rank < (int)d_;
+      set_warm(0);
     } else {
       RTB_CUDA(cudaMemcpyAsync(core_.p, rhs_.p, d_ * 8, cudaMemcpyDeviceToDevice, st_));
+      set_warm(1);
     }
     check_core_finite();
   }
 
- private:
+  void set_warm(int v) {
+    k_set_int<<<1, 1, 0, st_>>>(warm_dev_.as<int>(), v);
+    RTB_LAUNCH_CHECK();
+  }
+
   void check_core_finite() {
     RTB_CUDA(cudaMemsetAsync(flag_.p, 0, 4, st_));
     k_check_finite<<<ceil_div<long long>(d_, 256), 256, 0, st_>>>(core_.as<double>(), d_,
@@ -1256,6 +1501,7 @@ class Engine {
     if (bad) throw Error(1, "DenseTensor: non-finite entry");  // ref tensor.cpp:32-42
   }
 
+ private:
   // ---- exact core (ref tucker.cpp:91-129) ----
   void update_core_exact() {
     Scope sc(prof_, "core_exact");
@@ -1532,12 +1778,23 @@ uint32_t session_run(Session* s, uint32_t n, bool check_tol) {
   }
   double prev = e.prev_loss_;
   uint32_t run = 0;
-  cudaEvent_t a, b;
+  struct Ev {
+    cudaEvent_t a = nullptr, b = nullptr;
+    ~Ev() {
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } ev;
+  cudaEvent_t& a = ev.a;
+  cudaEvent_t& b = ev.b;
   RTB_CUDA(cudaEventCreate(&a));
   RTB_CUDA(cudaEventCreate(&b));
   RTB_CUDA(cudaEventRecord(a, e.st_));
   for (uint32_t k = 0; k < n; ++k) {
     e.sweep(e.iterations_ + 1);
+    // the core verdict of this sweep (waits only for its core step; the loss pass keeps
+    // the GPU busy while the host enqueues the next sweep)
+    e.resolve_core();
     ++run;
     if (check_tol) {
       const double loss = e.last_loss_host();
@@ -1555,8 +1812,6 @@ uint32_t session_run(Session* s, uint32_t n, bool check_tol) {
   float ms = 0.f;
   RTB_CUDA(cudaEventElapsedTime(&ms, a, b));
   e.sweep_seconds_ += ms * 1e-3;
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
   return run;
 }
 
@@ -1861,9 +2116,16 @@ void kron_normal_eq(int order, const uint64_t* rows, const uint64_t* ranks, cons
                     const double* x_host, double lambda, uint64_t s, const uint64_t* idx,
                     const double* w, double* gram, double* rhs) {
   if (order < 1 || order > 8) throw Error(1, "kron_normal_eq: order must be in [1, 8]");
+  if (s == 0) throw Error(1, "solve_sketched_ridge: sample count must be positive");
+  for (int n = 0; n < order; ++n)
+    if (ranks[n] == 0 || ranks[n] > rows[n] || rows[n] > (uint64_t)INT32_MAX)
+      throw Error(1, "kron_normal_eq: rank outside [1, I_n]");
   cudaStream_t st = current_stream();
   std::vector<uint64_t> shape(rows, rows + order), rk(ranks, ranks + order);
   const uint64_t total = prod(shape), d = prod(rk);
+  if (d > (uint64_t)INT32_MAX / 2) throw Error(1, "kron_normal_eq: d too large");
+  for (uint64_t t = 0; t < s; ++t)
+    if (idx[t] >= total + d) throw Error(1, "kron_normal_eq: row index out of range");
   uint64_t fe = 0;
   for (int n = 0; n < order; ++n) fe += shape[n] * rk[n];
   DevBuf xd(total * 8, st), fd(fe * 8, st), ix(s * 8, st), ww(s * 8, st), G(d * d * 8, st),

@@ -53,6 +53,7 @@ struct AlsOptions {
   int core_solver = 0;                    // 0 auto (PCG, Cholesky fallback), 1 Cholesky
   bool fast_loss = false;                 // loss by the expansion formula (see engine.cu)
   uint64_t factor_samples = 0;            // > 0: sketched factor updates (perf mode)
+  bool no_graph = false;                  // never run a sweep as a CUDA graph
 };
 
 struct HistoryRow {
@@ -85,6 +86,7 @@ struct AlsOutput {
   uint64_t last_sample_count = 0, last_data_draws = 0;
   int last_rank_deficient = 0, last_solver_path = 0, last_pcg_iterations = 0;
   double sweep_seconds = 0.0;  // device time of the sweep loop
+  uint64_t graph_launches = 0;  // sweeps that ran as one CUDA graph launch
 };
 
 class Engine;  // opaque

@@ -710,16 +710,9 @@ void c4_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const d
   if (!(x && rhs)) return;
   k_c4_rows<<<kNumSMs * 8, 256, 0, st>>>(l.ukey, l.uc, l.nuniq, I3, A3, R3, l.rows);
   RTB_LAUNCH_CHECK();
-  static bool attr = false;
-  if (!attr) {
-    RTB_CUDA(cudaFuncSetAttribute(k_c4_dfib<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kDfibSmem));
-    RTB_CUDA(cudaFuncSetAttribute(k_c4_dfib<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kDfibSmem));
-    RTB_CUDA(cudaFuncSetAttribute(k_c4_dfib<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kDfibSmem));
-    attr = true;
-  }
+  set_max_smem(k_c4_dfib<0>, (int)kDfibSmem);
+  set_max_smem(k_c4_dfib<1>, (int)kDfibSmem);
+  set_max_smem(k_c4_dfib<2>, (int)kDfibSmem);
   const long long nitems = (long long)nb * ceil_div(I1, kDT);
   const int grid = (int)std::max<long long>(1, std::min<long long>(nitems, 2LL * kNumSMs));
   // canonical X: windows of the rows X[i, b, :] once the sampled rows are dense enough that a
@@ -727,12 +720,7 @@ void c4_sketch(const float* x, bool fiber_major, int I1, int I2, int I3, const d
   const bool slab_windows = !fiber_major && I3 % 4 == 0 &&
                             0.5 * (double)s >= 0.03 * (double)I2 * (double)I3;
   if (slab_windows) {
-    static bool attr_s = false;
-    if (!attr_s) {
-      RTB_CUDA(cudaFuncSetAttribute(k_c4_dslab, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kDslabSmem));
-      attr_s = true;
-    }
+    set_max_smem(k_c4_dslab, (int)kDslabSmem);
     k_c4_dslab<<<grid, 256, kDslabSmem, st>>>(x, I1, I2, I3, R3, l.ukey, l.rows, l.bstart, blo,
                                                bhi, l.dfib);
   } else {

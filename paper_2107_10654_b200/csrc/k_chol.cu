@@ -815,7 +815,7 @@ void chol_solve(double* a, int d, double* b, int* status_dev, void* work, cudaSt
   k_chol_init<<<kNumSMs, 256, 0, st>>>(w, b, d);
   RTB_LAUNCH_CHECK();
   const int smem = 5 * NB * LDT * sizeof(double);  // ta, tb, tw, 2 row-task C buffers
-  RTB_CUDA(cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  set_max_smem(k_chol_dag, smem);
   int per_sm = 0;
   RTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_dag, kThreads, smem));
   if (per_sm < 1) throw Error(4, "chol: kernel does not fit on an SM");
@@ -831,7 +831,7 @@ void chol_solve(double* a, int d, double* b, int* status_dev, void* work, cudaSt
   RTB_LAUNCH_CHECK();
   {
     const int bsmem = 3 * NB * LDT * sizeof(double);
-    RTB_CUDA(cudaFuncSetAttribute(k_trsv_back, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
+    set_max_smem(k_trsv_back, bsmem);
     int per2 = 0;
     RTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_trsv_back, kThreads, bsmem));
     const int g2 = std::min(w.T, sms * std::max(per2, 1));

@@ -34,6 +34,7 @@ constexpr int LMAX = 9;  // order <= 8
 
 struct StreamCfg {
   unsigned long long seed;
+  const unsigned long long* seed_ptr;  // non-null: the seed is read from device memory
   unsigned long long thr;  // (2^64 - d) % d: next_below rejection threshold
   int data_step;           // 1 + order
 };
@@ -111,6 +112,7 @@ size_t draw_work_bytes(const DrawSpec& spec) {
 
 __global__ void k_draw_submaps(StreamCfg c, int L, long long nsub, unsigned char* exitm,
                                unsigned short* cnt, int* overflow) {
+  if (c.seed_ptr) c.seed = *c.seed_ptr;
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nsub * L) return;
   const long long j = e / L;
@@ -178,6 +180,7 @@ __global__ void __launch_bounds__(1024) k_draw_scan(StreamCfg c, int L, long lon
                                                    const CT* gcnt, int* gentry, long long* gbase,
                                                    long long* base, const int* overflow,
                                                    long long* start, long long s) {
+  if (c.seed_ptr) c.seed = *c.seed_ptr;
   __shared__ unsigned char mx[1024][LMAX];
   __shared__ int mc[1024][LMAX];  // draws per range (< 2^31)
   const int tid = threadIdx.x;
@@ -268,6 +271,7 @@ __global__ void __launch_bounds__(GCTA) k_draw_fix(int L, long long nsub, long l
 
 __global__ void k_draw_emit(StreamCfg c, long long nsub, const int* entry, const long long* base,
                             long long* start, long long s) {
+  if (c.seed_ptr) c.seed = *c.seed_ptr;
   const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nsub) return;
   long long t = base[j];
@@ -285,6 +289,7 @@ __global__ void k_draw_emit(StreamCfg c, long long nsub, const int* entry, const
 __global__ void k_draw_eval(DrawSpec spec, StreamCfg c, const long long* start,
                             const double* scores, const double* cdfs, const double* sums,
                             unsigned long long* idx_out, double* w_out, int* flag) {
+  if (c.seed_ptr) c.seed = *c.seed_ptr;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)spec.s) return;
   const long long pos = start[t];
@@ -340,6 +345,7 @@ void draw_sketch(const DrawSpec& spec, const double* scores, const double* cdfs,
   Layout l = layout(spec, work.base);
   StreamCfg c;
   c.seed = spec.seed;
+  c.seed_ptr = spec.seed_dev;
   c.thr = (0ULL - spec.d) % spec.d;
   c.data_step = 1 + spec.order;
   RTB_CUDA(cudaMemsetAsync(l.overflow, 0, sizeof(int), st));

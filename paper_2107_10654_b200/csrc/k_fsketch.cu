@@ -381,8 +381,7 @@ void factor_sketch_normal_eq(const FactorSketchSpec& sp, const unsigned long lon
   k_fsk_unfold<RMV><<<ceil_div(f.width, 128), 128, 0, st>>>(f, sp.core, l.gt, l.qdig);          \
   RTB_LAUNCH_CHECK();                                                                            \
   if (rows_smem > 48 * 1024)                                                                     \
-    RTB_CUDA(cudaFuncSetAttribute(k_fsk_rows<RMV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                  (int)rows_smem));                                              \
+    set_max_smem(k_fsk_rows<RMV>, (int)rows_smem);                                               \
   k_fsk_rows<RMV><<<rows_blocks, 256, rows_smem, st>>>(f, l.gt, l.qdig, idx, w, sp.s, srow, l.kw, \
                                                        l.base);                                \
   RTB_LAUNCH_CHECK();                                                                            \

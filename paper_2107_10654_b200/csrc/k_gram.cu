@@ -1170,7 +1170,7 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
     const size_t smb = vech_bucket2_smem(v);
     const int smax = 227 * 1024;
     auto launch = [&](auto kern) {
-      RTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+      set_max_smem(kern, smax);
       kern<<<I1, kBWarps * 32, smb, st>>>(spec, v, l.dw2, l.dwx, l.drow, l.bstart, l.blen,
                                           l.nbuckets, l.H, l.h);
       RTB_LAUNCH_CHECK();
@@ -1181,7 +1181,10 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
       if (NTn <= 4) launch(k_vech_bucket2<4, H_, R_, C_>);
       else if (NTn <= 8) launch(k_vech_bucket2<8, H_, R_, C_>);
       else if (NTn <= 12) launch(k_vech_bucket2<12, H_, R_, C_>);
-      else if (NTn == 17) launch(k_vech_bucket2<17, H_, R_, C_>);  // R = 16: 136 = 17 x 8
+      else if (NTn == 17) {
+        launch(k_vech_bucket2<17, H_, R_, C_>);  // R = 16: 136 = 17 x 8
+        count_variant("k_vech_bucket2<17>");
+      }
       else launch(k_vech_bucket2<18, H_, R_, C_>);
     };
     using I0 = std::integral_constant<int, 0>;
@@ -1304,14 +1307,10 @@ void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
   const int I1 = spec.rows[0];
   if ((v.m[0] + 7) / 8 <= kBWarps) {
     const size_t smc = (size_t)(2 * KCC * LDH2 + 2 * KCC * LDZ) * 8;
-    static bool attr_c = false;
-    if (!attr_c) {
-      RTB_CUDA(cudaFuncSetAttribute(k_vech_contract2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smc));
-      attr_c = true;
-    }
+    set_max_smem(k_vech_contract2, (int)smc);
     k_vech_contract2<<<(unsigned)((v.Hsz + TNC2 - 1) / TNC2), kBWarps * 32, smc, st>>>(
         spec, v, l.H, l.bi1, l.nbuckets, l.S);
+    count_variant("k_vech_contract2");
   } else {
     k_vech_contract<<<dim3((unsigned)((v.Hsz + TNC - 1) / TNC), (unsigned)ceil_div(v.m[0], TB)),
                       kTh, 0, st>>>(spec, v, l.H, l.bi1, l.nbuckets, l.S);

@@ -61,6 +61,7 @@ struct PcgArgs {
   double* part;           // [m1][2][d']
   double* rpart;          // [grid] residual partials
   int warm;               // x holds a starting guess
+  const int* warm_dev;    // non-null: the warm flag is read on the device
   unsigned* counter;
   int* status;            // [0] status, [1] iterations
   const double* pinv;     // per mode (stride): (A_n^T A_n)^-1, row-major
@@ -670,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   }
   // warm start from x0 = A.x (the previous sweep's core: the system changes little
   // between sweeps): r = b - G x0, kept only if it beats the cold residual ||b||
-  if (A.warm) {
+  if (A.warm_dev ? *A.warm_dev : A.warm) {
     for (int e = threadIdx.x; e < d; e += kThreads) {
       const double x0 = A.x[e];
       xs[e] = x0;
@@ -954,6 +955,7 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   a.tol = spec.tol;
   a.check_tol = spec.check_tol;
   a.warm = spec.warm;
+  a.warm_dev = spec.warm_dev;
   static unsigned long long* prof_buf = nullptr;
   static const bool prof_on = std::getenv("RTB_PCG_PROF") != nullptr;
   if (prof_on) {
@@ -969,15 +971,11 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
            : all16 ? (void*)k_pcg<16, 16, false>
            : rm == 8 ? (void*)k_pcg<8, 0, false>
            : rm == 16 ? (void*)k_pcg<16, 0, false> : (void*)k_pcg<32, 0, false>;
-  static bool attr_set[7] = {false, false, false, false, false, false, false};
-  const int slot = big ? 4 + (rm == 8 ? 0 : rm == 16 ? 1 : 2) : all16 ? 3 : rm == 8 ? 0 : rm == 16 ? 1 : 2;
-  if (!attr_set[slot]) {
-    RTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    attr_set[slot] = true;
-  }
+  set_max_smem_impl(fn, 220 * 1024);
   void* args[] = {(void*)&a, (void*)&sh};
   RTB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, st));
   RTB_LAUNCH_CHECK();
+  if (!big && all16) count_variant("k_pcg<16,16>");
   if (prof_on) {
     unsigned long long h[16];
     int stat[2];

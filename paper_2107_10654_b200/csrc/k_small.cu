@@ -607,8 +607,7 @@ void sym_eigen(const double* in, const int* ns_dev, int nmax, int stride, double
     if (nmax > 64) throw Error(4, "eigen: n > 64 not supported");
     const int np = nmax + (nmax & 1);
     const size_t smem = (2 * (size_t)np * (np + 1) + 2 * np) * 8;
-    RTB_CUDA(cudaFuncSetAttribute(k_sym_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (2 * 64 * 65 + 2 * 64) * 8));
+    set_max_smem(k_sym_eigen, (2 * 64 * 65 + 2 * 64) * 8);
     k_sym_eigen<<<nmat, 128, smem, st>>>(in, ns_dev, stride, evals, evecs, status);
   }
   RTB_LAUNCH_CHECK();

@@ -837,11 +837,7 @@ static void launch_last(const double* X, long long O, int I, const double* A, in
                         const double* P, double* partial, cudaStream_t st) {
   constexpr int smem = kStages * 64 * (kBK + kPadX) * sizeof(double);
   auto k = k_ttm_last<RP, VEC, FUSED>;
-  static bool attr = false;
-  if (!attr) {
-    RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  set_max_smem(k, (int)smem);
   const long long blocks = ceil_div<long long>(O, 64);
   k<<<(unsigned)blocks, 128, smem, st>>>(X, O, I, A, R, T, P, partial, g_need);
   RTB_LAUNCH_CHECK();
@@ -1002,11 +998,7 @@ static void launch_last2(const double* X, long long O, int I, const double* A, i
   const size_t ip = (size_t)ceil_div(I, kBK) * kBK;
   const size_t smem = (ip * lda2<RP>() + (size_t)kStages2 * BM2 * (kBK + kPadX)) * 8;
   auto k = k_ttm_last2<RP, FUSED>;
-  static bool attr = false;
-  if (!attr) {
-    RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    attr = true;
-  }
+  set_max_smem(k, 220 * 1024);
   const long long nrb = ceil_div<long long>(O, BM2);
   const int grid = (int)std::min<long long>(nrb, sm_count());
   k<<<grid, 512, smem, st>>>(X, O, I, A, R, T, P, partial, g_need, pg);
@@ -1034,15 +1026,12 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
   if (R <= 16 && (I % 2) == 0 && smem3 <= 227 * 1024 - 1024) {
     const size_t smem = smem3;
     auto k = fused ? k_ttm_last3<true, kL3BK, kL3Stages> : k_ttm_last3<false, kL3BK, kL3Stages>;
-    static bool attr3[2] = {false, false};
-    if (!attr3[fused]) {
-      RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 1024));
-      attr3[fused] = true;
-    }
+    set_max_smem(k, 227 * 1024 - 1024);
     const long long nrb = ceil_div<long long>(O, BM2);
     const int grid = (int)std::min<long long>(nrb, sm_count());
     k<<<grid, 512, smem, st>>>(X, O, I, A, R, T, P, partial, g_need);
     RTB_LAUNCH_CHECK();
+    count_variant(fused ? "k_ttm_last3_fused" : "k_ttm_last3");
     return;
   }
   if (last2_ok(I, R)) {
@@ -1101,11 +1090,7 @@ static void launch_mid(const double* X, long long O, int I, long long J, const d
                        double* out, cudaStream_t st) {
   constexpr int smem = kStages * kBK * (64 + kPadX) * sizeof(double);
   auto k = k_ttm_mid<RP, VEC>;
-  static bool attr = false;
-  if (!attr) {
-    RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  set_max_smem(k, (int)smem);
   const long long tiles = ceil_div<long long>(O * J, 64);
   // split the reduction when the column tiles alone cannot fill the GPU
   int splits = 1;
@@ -1132,20 +1117,21 @@ static void launch_mid2(const double* X, long long O, int I, long long J, const 
   const size_t smem3 = mid3_smem(I, RP);
   if (pc && smem3 <= 227 * 1024 - 2048) {
     auto k3 = probe ? k_ttm_mid3<RP, false> : k_ttm_mid3<RP, true>;
-    RTB_CUDA(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024 - 2048));
+    set_max_smem(k3, 227 * 1024 - 2048);
     const long long ntiles = O * J / BJ2;
     const int grid = (int)std::min<long long>(ntiles, sm_count());
     k3<<<grid, 288, smem3, st>>>(X, O, I, J, A, R, out);
     RTB_LAUNCH_CHECK();
+    count_variant("k_ttm_mid3");
     return;
   }
   auto k = probe ? k_ttm_mid2<RP, false> : k_ttm_mid2<RP, true>;
-  RTB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  set_max_smem(k, 220 * 1024);
   const long long ntiles = O * J / BJ2;
   const int grid = (int)std::min<long long>(ntiles, sm_count());
   k<<<grid, 256, smem, st>>>(X, O, I, J, A, R, out);
   RTB_LAUNCH_CHECK();
+  count_variant("k_ttm_mid2");
 }
 
 void ttm_mid(const double* X, long long O, int I, long long J, const double* A, int R, double* out,

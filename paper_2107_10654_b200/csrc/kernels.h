@@ -75,6 +75,9 @@ struct DrawSpec {
   unsigned long long d;     // prod R_n (augmented block size)
   unsigned long long seed;
   unsigned long long s;     // number of draws
+  // non-null: the seed is read on the device at run time (a CUDA-graph-captured sweep
+  // draws with a new seed every launch); `seed` is then ignored
+  const unsigned long long* seed_dev;
 };
 struct DrawWork {          // device scratch, sized by draw_work_bytes
   void* base;
@@ -180,6 +183,7 @@ struct PcgSpec {
   double tol;           // stop when ||r_k|| <= tol max(||b||, ||G||~ ||x_k||)
   double check_tol;     // accept when ||b - G x|| <= check_tol (||G||~ ||x|| + ||b||)
   int warm = 0;         // 1: x holds a starting guess (kept if ||b - G x0|| < ||b||)
+  const int* warm_dev = nullptr;  // non-null: the warm flag is read on the device
 };
 size_t pcg_work_bytes(int d, int r1);
 // with the per-CTA vector slices of the large-d form (vectors beyond shared memory)

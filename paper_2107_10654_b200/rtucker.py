@@ -65,7 +65,8 @@ class AlsExt(C.Structure):
         ("fast_loss", C.c_int),
         ("shard_rows_total", C.c_int),
         ("factor_samples", C.c_uint32),
-        ("reserved", C.c_int * 3),
+        ("disable_graph", C.c_int),
+        ("reserved", C.c_int * 2),
     ]
 
 
@@ -122,6 +123,7 @@ def _load() -> C.CDLL:
         "rtucker_b200_set_device": (S, [C.c_int]),
         "rtucker_b200_set_stream": (S, [_vp]),
         "rtucker_b200_launch_count": (C.c_ulonglong, []),
+        "rtucker_b200_variant_count": (C.c_ulonglong, [C.c_char_p]),
         "rtucker_b200_tensor_create_device": (S, [_u64p, C.c_uint32, _vp, C.POINTER(_vp)]),
         "rtucker_b200_tensor_device_data": (_vp, [_vp]),
         "rtucker_b200_als_run_ex": (S, [_vp, _u64p, C.c_uint32, C.POINTER(AlsOptions),
@@ -132,6 +134,7 @@ def _load() -> C.CDLL:
         "rtucker_b200_session_result": (S, [_vp, C.POINTER(_vp)]),
         "rtucker_b200_session_free": (None, [_vp]),
         "rtucker_b200_result_sweep_seconds": (C.c_double, [_vp]),
+        "rtucker_b200_result_graph_sweeps": (C.c_uint64, [_vp]),
         "rtucker_b200_model_data": (S, [_vp, _f64p, _f64p]),
         "rtucker_b200_model_create": (S, [_u64p, _u64p, C.c_uint32, _f64p, _f64p, C.c_double,
                                           C.POINTER(_vp)]),
@@ -365,6 +368,10 @@ class Result:
         return lib.rtucker_result_iterations(self.h)
 
     @property
+    def graph_sweeps(self) -> int:
+        return int(lib.rtucker_b200_result_graph_sweeps(self.h))
+
+    @property
     def sweep_seconds(self) -> float:
         return lib.rtucker_b200_result_sweep_seconds(self.h)
 
@@ -414,8 +421,10 @@ class Shard:
 
 
 def _ext(init_model: Model | None = None, profile: bool = False, core_solver: int = 0,
-         fast_loss: bool = False, shard: Shard | None = None, factor_samples: int = 0):
+         fast_loss: bool = False, shard: Shard | None = None, factor_samples: int = 0,
+         graph: bool = True):
     ext = AlsExt()
+    ext.disable_graph = 0 if graph else 1
     ext.core_solver = int(core_solver)
     ext.fast_loss = int(fast_loss)
     ext.factor_samples = int(factor_samples)
@@ -448,7 +457,7 @@ def _ext(init_model: Model | None = None, profile: bool = False, core_solver: in
 
 def als_run(x: Tensor, ranks, opts: AlsOptions | None = None, init_model: Model | None = None,
             profile: bool = False, core_solver: int = 0, fast_loss: bool = False,
-            shard: Shard | None = None, factor_samples: int = 0) -> Result:
+            shard: Shard | None = None, factor_samples: int = 0, graph: bool = True) -> Result:
     """rtucker_als_run (ref capi.cpp:176-201); extensions via rtucker_b200_als_run_ex.
     With `shard`, `x` holds only that shard's rows of mode 1 (see shard_rows).
     factor_samples > 0: sketched factor updates with that many draws (perf mode)."""
@@ -459,10 +468,11 @@ def als_run(x: Tensor, ranks, opts: AlsOptions | None = None, init_model: Model 
     if shard is not None:
         shape = (shard.rows_total,) + shape[1:]
     if (init_model is None and not profile and not core_solver and not fast_loss and shard is None
-            and not factor_samples):
+            and not factor_samples and graph):
         _check(lib.rtucker_als_run(x.h, _p(ranks), len(ranks), C.byref(opts), C.byref(r)))
     else:
-        ext, keep = _ext(init_model, profile, core_solver, fast_loss, shard, factor_samples)
+        ext, keep = _ext(init_model, profile, core_solver, fast_loss, shard, factor_samples,
+                         graph)
         _check(lib.rtucker_b200_als_run_ex(x.h, _p(ranks), len(ranks), C.byref(opts),
                                            C.byref(ext), C.byref(r)))
         del keep
@@ -474,13 +484,14 @@ class Session:
 
     def __init__(self, x: Tensor, ranks, opts: AlsOptions | None = None,
                  init_model: Model | None = None, profile: bool = False, core_solver: int = 0,
-                 shard: Shard | None = None, factor_samples: int = 0):
+                 shard: Shard | None = None, factor_samples: int = 0, graph: bool = True):
         self.shape = tuple(x.shape)
         if shard is not None:
             self.shape = (shard.rows_total,) + self.shape[1:]
         opts = opts or options()
         ranks = _u64(ranks)
-        ext, self._keep = _ext(init_model, profile, core_solver, False, shard, factor_samples)
+        ext, self._keep = _ext(init_model, profile, core_solver, False, shard, factor_samples,
+                               graph)
         self.h = _vp()
         _check(lib.rtucker_b200_session_create(x.h, _p(ranks), len(ranks), C.byref(opts),
                                                C.byref(ext), C.byref(self.h)))
@@ -503,6 +514,11 @@ class Session:
             self.free()
         except Exception:
             pass
+
+
+def variant_count(name: str) -> int:
+    """Launches so far of a named headline kernel variant (e.g. "k_ttm_mid3")."""
+    return int(lib.rtucker_b200_variant_count(name.encode()))
 
 
 def set_stream(stream_ptr: int | None) -> None:

@@ -52,11 +52,15 @@ def env_int(name, default):
 # ---------------------------------------------------------------------------
 # reference CPU arm (oracle/_ref = the reference compiled from its sources)
 
+SVD_GROWTH = 11.3  # the reference's Jacobi SVD, d = 512 -> 1024, measured
+SVD_ANCHOR_R = 7   # the reference's own update_core_fast timed at d = 7^3 = 343
+
+
 def reference_sweep_estimate(ref, np, x_full, core, factors, slab=64, gram_samples=100,
-                             svd_dim=256, seed=12345):
-    """One bounded sample of every phase of a C2 sweep, timed with the
-    reference's own routines (oracle/ref_harness.cpp), extrapolated to C2.
-    Returns (seconds per sweep, detail dict)."""
+                             seed=12345):
+    """One bounded sample of every phase of a C2 sweep, timed with the reference's own
+    routines (oracle/_ref), extrapolated to C2 (labelled "extrapolated": a C2 sweep takes
+    hours on the reference). Returns (seconds per sweep, detail dict)."""
     # update_factor(mode) and the loss are linear in prod(I_n) when the tensor is
     # cut along a mode other than the updated one (the Kronecker of the other
     # factors shrinks with the slab); mode 1 is timed on a mode-3 slab, modes 2
@@ -78,18 +82,31 @@ def reference_sweep_estimate(ref, np, x_full, core, factors, slab=64, gram_sampl
         t_factor += out[0]
         t_loss += out[1]
     scale = SHAPE[0] / slab
+    # the Gram/RHS stream at C2 (d = 4096, the 67 MB upper triangle streamed per data row):
+    # the loop of sketch_ridge.cpp:105-128 over the reference's KroneckerRowSource on 100
+    # real C2 data rows (ref_time_sweep_phases)
     out = ref.time_sweep_phases(SHAPE, RANKS, core, factors, LAM, x_full, S_CORE, seed, 1,
-                                gram_samples=gram_samples, svd_dim=svd_dim, do_factor=False,
+                                gram_samples=gram_samples, svd_dim=0, do_factor=False,
                                 do_loss=False)
-    t_gram_sample, t_setup, t_svd, n_data = out[2], out[3], out[4], out[5]
+    t_gram_sample, t_setup, n_data = out[2], out[3], out[5]
+    # the solve: the reference's own update_core_fast (setup + draws + Gram stream + Jacobi
+    # compact_svd + pinv apply) on the C2 tensor at core rank 7 (d = 343), s = 2,000 (its
+    # Gram stream is ~1% of it), then the SVD grown to d = 4096 by the reference's measured
+    # growth per doubling of d (x11.3)
+    ra = (SVD_ANCHOR_R,) * 3
+    core_a, fac_a = ref.random_model(SHAPE, ra, 0)
+    ta = ref.time_core_fast(SHAPE, ra, core_a, fac_a, LAM, x_full, 2000, seed)
+    d_a = SVD_ANCHOR_R ** 3
     d = int(np.prod(RANKS))
-    t_svd_full = t_svd * (d / svd_dim) ** 3  # d^3 (the measured growth is steeper)
+    t_svd_full = ta[4] * SVD_GROWTH ** np.log2(d / d_a)
     total = scale * (t_factor + t_loss) + t_setup + n_data * t_gram_sample + t_svd_full
     detail = {"factor_updates_s": scale * t_factor, "loss_s": scale * t_loss,
               "kron_setup_s": t_setup, "gram_stream_s": n_data * t_gram_sample,
               "gram_s_per_data_row": t_gram_sample, "data_rows": int(n_data),
-              "svd_solve_s_extrapolated": t_svd_full, "svd_measured_dim": svd_dim,
-              "svd_measured_s": t_svd}
+              "svd_solve_s_extrapolated": t_svd_full,
+              "anchor_update_core_fast": {"d": d_a, "s": 2000, "total_s": ta[0],
+                                          "solve_s": ta[4], "setup_s": ta[1]},
+              "svd_growth_per_doubling": SVD_GROWTH}
     return total, detail
 
 
@@ -102,10 +119,76 @@ def reference_inputs(np):
     return ref, x, core, factors
 
 
-REF_SAMPLE = ("per sweep phase, the reference's own routines on bounded samples: "
-              "update_factor (3 modes) and the loss on 64-wide slabs cut along a mode other "
-              "than the updated one (x8, linear in prod I_n), the Gram/RHS stream on 100 real C2 data rows (x s_data), "
-              "ImplicitKronecker setup at C2, Jacobi compact_svd of a 256^2 SPD Gram (x(4096/256)^3)")
+REF_SAMPLE = ("EXTRAPOLATED C2 sweep from bounded samples of the reference's own routines: "
+              "update_factor (3 modes) and tucker_loss on 64-wide slabs cut along a mode other "
+              "than the updated one (x8, linear in prod I_n); the Gram/RHS stream of "
+              "sketch_ridge.cpp:105-128 on 100 real C2 data rows at d=4096 (x s_data); "
+              "ImplicitKronecker setup at C2; the reference's update_core_fast at d=343 (its "
+              "Jacobi SVD solve) grown to d=4096 by the measured x11.3 per doubling of d")
+
+
+# ---------------------------------------------------------------------------
+# C1 head to head (BASELINE configs[0]): the same C-API job through either library
+
+C1_SHAPE, C1_RANKS, C1_LAM, C1_S, C1_SWEEPS = (100, 100, 100), (5, 5, 5), 1e-3, 20000, 10
+C1_WORKLOAD = ("C1: dense 3-way FP64 100^3, planted rank (5,5,5) N(0,1) core/factors + 1% "
+               "Gaussian noise (seed 0); Tucker rank (5,5,5), lambda=1e-3, 20,000 sampled rows "
+               "for the core update, exact factor updates, 10 sweeps, the reference's uniform init")
+
+
+def c1_input(np):
+    rng = np.random.default_rng(0)
+    core = rng.standard_normal(C1_RANKS)
+    x = core
+    for n, (i, r) in enumerate(zip(C1_SHAPE, C1_RANKS)):
+        x = np.moveaxis(np.tensordot(rng.standard_normal((i, r)), x, axes=(1, n)), 0, n)
+    x = x + NOISE * np.linalg.norm(x) / np.sqrt(x.size) * rng.standard_normal(x.shape)
+    return np.ascontiguousarray(x)
+
+
+def capi_als_job(lib, opts, x, ranks):
+    """One C1 job through the reference's C API (include/rtucker.h, identical in both
+    libraries): rtucker_tensor_create(host X) + rtucker_als_run + rtucker_result_model.
+    Returns (wall seconds, final loss)."""
+    import ctypes as C
+    import numpy as np
+    shape = np.ascontiguousarray(x.shape, dtype=np.uint64)
+    rk = np.ascontiguousarray(ranks, dtype=np.uint64)
+    u64p = C.POINTER(C.c_uint64)
+    f64p = C.POINTER(C.c_double)
+    t, r, m = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    lib.rtucker_result_final_loss.restype = C.c_double
+    t0 = time.perf_counter()
+    rc = lib.rtucker_tensor_create(shape.ctypes.data_as(u64p), len(shape),
+                                   x.ctypes.data_as(f64p), C.byref(t))
+    rc = rc or lib.rtucker_als_run(t, rk.ctypes.data_as(u64p), len(rk), C.byref(opts), C.byref(r))
+    rc = rc or lib.rtucker_result_model(r, C.byref(m))
+    loss = lib.rtucker_result_final_loss(r) if not rc else float("nan")
+    t1 = time.perf_counter()
+    if m:
+        lib.rtucker_model_free(m)
+    if r:
+        lib.rtucker_result_free(r)
+    if t:
+        lib.rtucker_tensor_free(t)
+    if rc:
+        raise RuntimeError(f"C1 job failed: status {rc}")
+    return t1 - t0, loss
+
+
+def c1_head_to_head(lib, opts, jobs):
+    import numpy as np
+    x = c1_input(np)
+    capi_als_job(lib, opts, x, C1_RANKS)  # warm-up job
+    secs, loss = [], None
+    for _ in range(jobs):
+        t, loss = capi_als_job(lib, opts, x, C1_RANKS)
+        secs.append(t)
+    med = statistics.median(secs)
+    return {"workload": C1_WORKLOAD, "sweeps_per_s": C1_SWEEPS / med, "seconds_per_job": med,
+            "jobs": jobs, "final_loss": loss, "measured": True,
+            "step": "one job = rtucker_tensor_create(host X) + rtucker_als_run(10 sweeps) + "
+                    "rtucker_result_model, wall clock, median over jobs"}
 
 
 def run_reference_arm(args):
@@ -114,9 +197,13 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     ref, x, core, factors = reference_inputs(np)
-    # each estimate is a bounded sample of one C2 sweep (~5 s of CPU); the run is capped at
-    # one warm-up and 15 timed estimates so that --steps K --warmup W ends within minutes
-    n_warm, n_timed = min(args.warmup, 1), max(1, min(args.steps, 15))
+    # C1 head to head: the same C-API job our arm runs, on the reference's own library
+    from oracle.oracle import AlsOptions as RefOpts
+    c1 = c1_head_to_head(ref.lib, RefOpts(C1_LAM, 1, 0.1, 0.1, 0, C1_SWEEPS, 0.0, C1_S, 0), 3)
+    c1["library"] = "oracle/_ref/librtucker_ref.so (the reference compiled from its sources)"
+    # each estimate is a bounded sample of one C2 sweep (~8 s of CPU); the run is capped at
+    # one warm-up and 8 timed estimates so that --steps K --warmup W ends within minutes
+    n_warm, n_timed = min(args.warmup, 1), max(1, min(args.steps, 8))
     vals = []
     for i in range(n_warm + n_timed):
         t, detail = reference_sweep_estimate(ref, np, x, core, factors)
@@ -131,8 +218,11 @@ def run_reference_arm(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample": REF_SAMPLE,
                    "timed_estimates": n_timed, "warmup_estimates": n_warm},
+        "extrapolated": True,
         "cpu_baseline": {"value": value, "unit": "sweeps/s", "cores": 1, "kind": "reference",
-                         "sample": REF_SAMPLE, "phases": detail},
+                         "sample": REF_SAMPLE, "phases": detail, "extrapolated": True,
+                         "host_cores": os.cpu_count()},
+        "c1_head_to_head": c1,
         "e2e": {"value": value, "unit": "sweeps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -331,10 +421,11 @@ def run_our_arm(args):
 
     opts = rt.options(lam=LAM, sketched_core=1, sample_count_override=S_CORE, tolerance=0.0,
                       max_iterations=args.warmup + args.steps, seed=0)
-    sess = rt.Session(t, RANKS, opts, profile=True, shard=shard)
+    # headline: K sweeps of one session, kernel by kernel for the first sweep and one CUDA
+    # graph launch per sweep after that (no host round trip inside a sweep)
+    sess = rt.Session(t, RANKS, opts, shard=shard)
     sess.sweeps(args.warmup)
     torch.cuda.synchronize()
-    k0 = {k[0]: k for k in sess.result().kernels()}
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -359,13 +450,31 @@ def run_our_arm(args):
         ms = float(tt.item())
     res = sess.result()
     info = res.sketch_info()
-    k1 = res.kernels()
-    fam = {}
-    for name, secs, n in k1:
-        p = k0.get(name, (name, 0.0, 0))
-        fam[name] = (secs - p[1], n - p[2])
+    graph_sweeps = res.graph_sweeps
     hist = res.history()
     sess.free()
+
+    # per-kernel-family device times for the roofline: the same workload re-run kernel by
+    # kernel with CUDA events around every family on the library's stream (the headline
+    # region runs as graph launches, where no per-kernel events are recorded)
+    prof_steps = min(args.steps, 50)
+    sp = rt.Session(t, RANKS, rt.options(lam=LAM, sketched_core=1, sample_count_override=S_CORE,
+                                         tolerance=0.0, max_iterations=args.warmup + prof_steps,
+                                         seed=0), profile=True, shard=shard)
+    sp.sweeps(args.warmup)
+    torch.cuda.synchronize()
+    k0 = {k[0]: k for k in sp.result().kernels()}
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    sp.sweeps(prof_steps)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    prof_ms = p0.elapsed_time(p1) / prof_steps
+    fam = {}
+    for name, secs, n in sp.result().kernels():
+        p = k0.get(name, (name, 0.0, 0))
+        fam[name] = (secs - p[1], n - p[2])
+    sp.free()
 
     # BASELINE configs[1] as written also samples the factor updates (20,000 draws per mode,
     # design width 256): the library's perf mode (ext.factor_samples; the reference has no
@@ -433,6 +542,7 @@ def run_our_arm(args):
     # e2e through the public C API with host buffers (rank 0 timing, max over ranks)
     e2e_vals = []
     xnp = xh.numpy()
+    h2d_bytes = int(xnp.nbytes)
     rt.set_stream(stream.cuda_stream)
     for i in range(3):
         torch.cuda.synchronize()
@@ -466,6 +576,41 @@ def run_our_arm(args):
             cpu = {"value": None, "unit": "sweeps/s", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    # C1 head to head (BASELINE configs[0]): the same C-API job as the reference arm's, on
+    # this library; plus the device-only C1 sweep rate (resident X, graph launches)
+    c1 = None
+    if rank == 0 and world == 1:
+        c1 = c1_head_to_head(rt.lib, rt.options(lam=C1_LAM, sketched_core=1, tolerance=0.0,
+                                                sample_count_override=C1_S,
+                                                max_iterations=C1_SWEEPS, seed=0), 20)
+        c1["library"] = "paper_2107_10654_b200/lib/librtucker_b200.so"
+        xc = rt.Tensor.from_numpy(c1_input(np))
+        n1 = 200
+        sc = rt.Session(xc, C1_RANKS, rt.options(lam=C1_LAM, sketched_core=1, tolerance=0.0,
+                                                 sample_count_override=C1_S,
+                                                 max_iterations=args.warmup + n1, seed=0))
+        sc.sweeps(args.warmup)
+        torch.cuda.synchronize()
+        c0e, c1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0e.record(stream)
+        sc.sweeps(n1)
+        c1e.record(stream)
+        torch.cuda.synchronize()
+        c1["device_sweeps_per_s"] = n1 / (c0e.elapsed_time(c1e) / 1e3)
+        c1["device_ms_per_sweep"] = c0e.elapsed_time(c1e) / n1
+        c1["device_cuda_graph_sweeps"] = sc.result().graph_sweeps
+        sc.free()
+        xc.free()
+
+    # BASELINE configs 3 and 4, measured in the same run (their own clocks samples)
+    extra = {}
+    if rank == 0 and world == 1 and not args.no_extra:
+        t.free()
+        del xh, xnp
+        torch.cuda.empty_cache()
+        extra["c3"] = c3_lines(args, steps=min(args.steps, 20))
+        extra["c4"] = c4_lines(args, steps=min(args.steps, 5), s_list=[100000, 1000000, 10000000])
+
     if rank == 0:
         sweeps_per_s = args.steps / (ms / 1e3)  # one job across all GPUs
         line = {
@@ -483,17 +628,24 @@ def run_our_arm(args):
                        "final_loss": hist[-1][2] if hist else None},
             "clocks": clk,
             "e2e": {"value": E2E_SWEEPS / e2e_s, "unit": "sweeps/s",
-                    "h2d_bytes_per_step": int(xnp.nbytes) * world, "d2h_bytes_per_step": int(d2h),
+                    "h2d_bytes_per_step": h2d_bytes * world, "d2h_bytes_per_step": int(d2h),
                     "step": "one job: rtucker_tensor_create(host X) + rtucker_als_run(10 sweeps)"
                             " + rtucker_result_model", "seconds_per_job": e2e_s},
             "gpu_launches": int(launches),
             "roofline": roofline,
-            "kernels_ms_per_sweep": {k: v[0] * 1e3 / args.steps for k, v in fam.items()},
-            "families": family_table(fam, args.steps, n_data, n_buckets, info.get("pcg_iterations"),
-                                     peaks, mp.get("hbm_gbs", 6553.3)),
+            "kernels_ms_per_sweep": {k: v[0] * 1e3 / prof_steps for k, v in fam.items()},
+            "families": family_table(fam, prof_steps, n_data, n_buckets,
+                                     info.get("pcg_iterations"), peaks, mp.get("hbm_gbs", 6553.3)),
+            "profiled_region": {"sweeps": prof_steps, "ms_per_step": prof_ms,
+                                "note": "kernel-by-kernel re-run with CUDA events around every "
+                                        "kernel family; source of kernels_ms_per_sweep, "
+                                        "families and roofline"},
+            "cuda_graph_sweeps": graph_sweeps,
             "sketch": info,
             "sketched_factor_updates": fsk,
             "cpu_baseline": cpu,
+            "c1_head_to_head": c1,
+            "other_configs": extra or None,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -502,7 +654,7 @@ def run_our_arm(args):
     return 0
 
 
-def run_c4(args):
+def c4_lines(args, steps=None, s_list=None):
     """BASELINE config 4 microbench (--workload c4): Kronecker-product sampling + fused fiber
     gather/SYRK. 3 factors 2048 x 32 N(0,1) FP64 (A1 unused by the microbench), X 2048^3 FP32
     N(0,1) (34 GB, resident, replicated per GPU), lambda = 1e-2; for each s: draws of
@@ -558,6 +710,9 @@ def run_c4(args):
             dist.all_reduce(rhs)
         return out
 
+    steps = steps or args.steps
+    clk_all = {}
+
     def run(xp, fm, s):
         for _ in range(args.warmup):
             step(xp, fm, s, 1)
@@ -565,23 +720,28 @@ def run_c4(args):
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
+        clocks = Clocks(local)
+        clocks.wait_first()
+        clocks.mark_start()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record()
-        for k in range(args.steps):
+        for k in range(steps):
             out = step(xp, fm, s, 2 + k)
             ph += np.array(out["phase_ms"])
             nd += out["data_draws"]
             nu += out["unique_rows"]
         t1.record()
         torch.cuda.synchronize()
-        ms = t0.elapsed_time(t1) / args.steps
+        clk_all[(s, fm)] = clocks.stop()
+        ms = t0.elapsed_time(t1) / steps
         if dist is not None:
             tt = torch.tensor([ms], device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms = float(tt.item())
-        return ms, ph / args.steps, nd / args.steps, nu / args.steps
+        return ms, ph / steps, nd / steps, nu / steps
 
-    for s in [int(float(v)) for v in args.c4_s.split(",")]:
+    lines = []
+    for s in s_list or [int(float(v)) for v in args.c4_s.split(",")]:
         step_ms, (draw_ms, gram_ms, rhs_ms), nd, nu = run(xf.data_ptr(), True, s)
         c_ms, (_, _, rhs_c_ms), _, _ = run(x.data_ptr(), False, s) if world == 1 else (0, (0, 0, 0), 0, 0)
         # Gram: two DMMA GEMMs over vech Khatri-Rao row products (T = C KA3, G' = KA2^T T,
@@ -594,7 +754,7 @@ def run_c4(args):
         line = {
             "metric": "C4 sketched Kronecker samples/s (Gram+RHS)",
             "value": s / (step_ms / 1e3),
-            "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "unit": "samples/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
             "dtype": "f64 (FP32 tensor upcast)", "data": "synthetic",
             "config": {"workload": "C4: factors 2048 x 32 N(0,1), X 2048^3 FP32 N(0,1) (34 GB), "
@@ -616,15 +776,24 @@ def run_c4(args):
         }
         if world == 1:
             line["canonical_layout"] = {"fiber_rhs_ms": rhs_c_ms, "samples_per_s": s / (c_ms / 1e3)}
+        line["clocks"] = clk_all.get((s, True))
         if rank == 0:
-            print(json.dumps(line), flush=True)
+            lines.append(line)
+    del x, xf
+    torch.cuda.empty_cache()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+    return lines
+
+
+def run_c4(args):
+    for line in c4_lines(args):
+        print(json.dumps(line), flush=True)
     return 0
 
 
-def run_c3(args):
+def c3_lines(args, steps=None):
     """BASELINE config 3 (--workload c3): dense 4-way FP64 160^4 (5.2 GB), planted rank
     (10,10,10,10) with coherent factors (rows scaled by i.i.d. Pareto(1.5) weights), 5% noise,
     lambda = 0.1, s_core = 500,000; one line with exact factor updates (reference semantics)
@@ -648,26 +817,42 @@ def run_c3(args):
     x = x.contiguous()
     torch.cuda.synchronize()
     t = rt.Tensor.from_device(x.data_ptr(), shape)
+    del x
+    steps = steps or args.steps
+    lines = []
     for fs in (0, 50000):
         opts = rt.options(lam=lam, sketched_core=1, sample_count_override=s, tolerance=0.0,
-                          max_iterations=args.warmup + args.steps + 1)
-        sess = rt.Session(t, ranks, opts, profile=True, factor_samples=fs)
+                          max_iterations=args.warmup + steps + 1)
+        sess = rt.Session(t, ranks, opts, factor_samples=fs)
         sess.sweeps(args.warmup)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
+        clocks = Clocks(0)
+        clocks.wait_first()
+        clocks.mark_start()
         e0.record()
-        sess.sweeps(args.steps)
+        sess.sweeps(steps)
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / args.steps
+        clk = clocks.stop()
+        ms = e0.elapsed_time(e1) / steps
         r = sess.result()
+        graph_sweeps = r.graph_sweeps
+        sess.free()
+        # kernel shares from a kernel-by-kernel re-run with per-family CUDA events
+        sp = rt.Session(t, ranks, rt.options(lam=lam, sketched_core=1, sample_count_override=s,
+                                             tolerance=0.0, max_iterations=args.warmup + 5),
+                        profile=True, factor_samples=fs)
+        sp.sweeps(args.warmup + 5)
         fam = {}
-        for name, secs, n in r.kernels():
+        for name, secs, n in sp.result().kernels():
             fam[name] = fam.get(name, 0.0) + secs
+        sp.free()
         tot = sum(fam.values()) or 1.0
         line = {
             "metric": "sketched Tucker-ALS sweeps/s (C3)", "value": 1e3 / ms, "unit": "sweeps/s",
-            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "n_gpus": 1, "steps": steps, "warmup": args.warmup, "ms_per_step": ms,
+            "clocks": clk, "cuda_graph_sweeps": graph_sweeps,
             "higher_is_better": True, "dtype": "f64", "data": "synthetic (seeded torch)",
             "config": {"workload": "C3: dense 4-way FP64 160^4 (5.2 GB), planted rank (10,10,10,10), "
                                    "Pareto(1.5)-scaled factor rows, 5% noise, lambda=0.1, "
@@ -678,6 +863,14 @@ def run_c3(args):
             "kernel_share": {k: round(v / tot, 4) for k, v in sorted(fam.items(),
                                                                     key=lambda kv: -kv[1])[:8]},
         }
+        lines.append(line)
+    t.free()
+    torch.cuda.empty_cache()
+    return lines
+
+
+def run_c3(args):
+    for line in c3_lines(args):
         print(json.dumps(line), flush=True)
     return 0
 
@@ -689,6 +882,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the BASELINE config 3 / 4 measurements of the default run")
     ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
                     help="c2 (default): the headline ALS sweep; c3: the BASELINE config-3 "
                          "4-way Pareto-factor sweep; c4: the BASELINE config-4 sampling + "

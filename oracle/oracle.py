@@ -427,6 +427,16 @@ class Reference:
                                                  C.c_int(int(do_loss)), _p(out)))
         return out
 
+    def time_core_fast(self, shape, ranks, core, factors, lam, x, s, seed):
+        """The reference's own update_core_fast, timed inside the harness (ref_time_core_fast):
+        [total, setup, draw, gather, solve, data_rows]."""
+        o, shape, ranks, core, fc = self._margs(shape, ranks, core, factors)
+        out = np.zeros(6)
+        self._chk(self.lib.ref_time_core_fast(o, _p(shape), _p(ranks), _p(core), _p(fc),
+                                              C.c_double(lam), _p(_f64(x).ravel()),
+                                              C.c_uint64(s), C.c_uint64(seed), _p(out)))
+        return out
+
     def als(self, x, ranks, lam=1e-3, sketched_core=0, epsilon=0.1, delta=0.1, seed=0,
             max_iterations=50, tolerance=1e-6, sample_count_override=0, record_history=0):
         """rtucker_als_run through the reference C API; returns the same dict as Oracle.als."""

@@ -161,6 +161,37 @@ int ref_update_core_fast(uint32_t order, const uint64_t* shape, const uint64_t* 
   });
 }
 
+// Times the reference's own public update_core_fast (ref tucker.cpp:141-166) on a given
+// model (bench.py's reference arm): out[0] = seconds of the call, out[1] = setup (factor
+// SVDs, scores, CDFs), out[2] = draws, out[3] = response gather, out[4] = solve (the
+// streamed Gram/RHS of sketch_ridge.cpp:105-128 + the Jacobi compact_svd of the d x d Gram
+// + the pinv apply), out[5] = data rows among the s draws (the same stream redrawn).
+int ref_time_core_fast(uint32_t order, const uint64_t* shape, const uint64_t* ranks,
+                       const double* core, const double* factors, double lambda,
+                       const double* x, uint64_t s, uint64_t seed, double* out) {
+  return run([&] {
+    const TuckerModel model = make_model(order, shape, ranks, core, factors, lambda);
+    const DenseTensor xt = make_tensor(order, shape, x);
+    SketchConfig cfg;
+    cfg.seed = seed;
+    cfg.sample_count_override = s;
+    const double t0 = now_s();
+    const FastCoreResult r = update_core_fast(model, xt, cfg);
+    out[0] = now_s() - t0;
+    out[1] = r.setup_seconds;
+    out[2] = r.diagnostics.draw_seconds;
+    out[3] = r.diagnostics.gather_seconds;
+    out[4] = r.diagnostics.solve_seconds;
+    const ImplicitKronecker k(model.factors);
+    const ProductLeverageSampler sampler(k, 0.0);
+    SplitMix64 rng(seed);
+    std::size_t n_data = 0;
+    for (std::size_t t = 0; t < s; ++t)
+      if (sampler.draw(rng).first < k.rows()) ++n_data;
+    out[5] = static_cast<double>(n_data);
+  });
+}
+
 int ref_update_factor(uint32_t order, const uint64_t* shape, const uint64_t* ranks,
                       const double* core, const double* factors, double lambda,
                       const double* x, uint32_t mode, double* factor_out) {

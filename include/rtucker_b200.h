@@ -210,6 +210,29 @@ rtucker_status rtucker_b200_kron_normal_eq(uint32_t order, const uint64_t* rows,
 rtucker_status rtucker_b200_spd_solve(const double* gram, const double* rhs, uint64_t d,
                                       double* x_out, uint64_t* rank_out, int* path_out);
 
+/* The dense toolkit's RowSketch (ref sampler.cpp:9-57, sketch_ridge.cpp:80-90): s draws of
+ * AugmentedSampler(candidate_scores[n], d, d_eff_lower) from SplitMix64(seed) on the GPU;
+ * indices in [0, n + d), weights sqrt((1/s)/prob). Bit-exact with the reference. */
+rtucker_status rtucker_b200_aug_draw(const double* candidate_scores, uint64_t n, uint64_t d,
+                                     double d_eff_lower, uint64_t seed, uint64_t s,
+                                     uint64_t* indices_out, double* weights_out);
+/* Sketched normal equations of [A; sqrt(lambda) I] (A n x d row-major, b n) from a given
+ * RowSketch (ref sketch_ridge.cpp:105-128): gram_out d x d (full), rhs_out d. */
+rtucker_status rtucker_b200_dense_normal_eq(const double* a, uint64_t n, uint64_t d,
+                                            const double* b, double lambda, uint64_t s,
+                                            const uint64_t* indices, const double* weights,
+                                            double* gram_out, double* rhs_out);
+/* The sample-count formula ceil(4 d / beta' max{420 ln(4 d / delta), 1 / (delta epsilon)})
+ * (ref sketch_ridge.cpp:40-50); invalid arguments -> RTUCKER_ERR_INVALID_ARGUMENT. */
+rtucker_status rtucker_b200_sample_count(double beta_prime, uint64_t d, double epsilon,
+                                         double delta, uint64_t* out);
+
+/* Symmetric eigendecomposition of a d x d matrix on the GPU: evals_out non-increasing,
+ * evecs_out row-major with eigenvector k in column k. d <= 64: one-CTA cyclic Jacobi;
+ * larger d: the parallel block Jacobi of the pinv fallback (k_eig.cu). */
+rtucker_status rtucker_b200_sym_eig(const double* a, uint64_t d, double* evals_out,
+                                    double* evecs_out);
+
 /* One sketched core update on the GPU for a given model (ref tucker.cpp:141-166).
  * Optional outputs (NULL to skip): indices/weights of the drawn sketch. */
 rtucker_status rtucker_b200_update_core_sketched(const rtucker_tensor* x,

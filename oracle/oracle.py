@@ -157,6 +157,25 @@ class Oracle:
                                               C.byref(s), C.byref(bp)))
         return x, s.value, bp.value
 
+    def aug_draw(self, cand, d, d_eff_lower, seed, s):
+        """AugmentedSampler draws of the dense toolkit (sampler.cpp:9-57)."""
+        cand = _f64(cand)
+        idx, w = np.zeros(s, np.uint64), np.zeros(s)
+        self._chk(self.lib.orc_aug_draw(_p(cand), C.c_uint64(len(cand)), C.c_uint64(d),
+                                        C.c_double(d_eff_lower), C.c_uint64(seed), C.c_uint64(s),
+                                        _p(idx), _p(w)))
+        return idx, w
+
+    def dense_normal_eq(self, a, b, lam, idx, w):
+        a, b = _f64(a), _f64(b)
+        n, d = a.shape
+        idx, w = _u64(idx), _f64(w)
+        g, rhs = np.zeros((d, d)), np.zeros(d)
+        self._chk(self.lib.orc_dense_normal_eq(_p(a), C.c_uint64(n), C.c_uint64(d), _p(b),
+                                               C.c_double(lam), C.c_uint64(len(idx)), _p(idx),
+                                               _p(w), _p(g), _p(rhs)))
+        return g, rhs
+
     def factor_scores(self, f):
         f = _f64(f)
         rows, cols = f.shape
@@ -426,6 +445,16 @@ class Reference:
                                                  C.c_uint64(svd_dim), C.c_int(int(do_factor)),
                                                  C.c_int(int(do_loss)), _p(out)))
         return out
+
+    def aug_sketch(self, a, b, cand, lam, d_eff_lower, s, seed):
+        """The RowSketch of the reference's approximate_ridge_regression (ref_aug_sketch)."""
+        a, b, cand = _f64(a), _f64(b), _f64(cand)
+        n, d = a.shape
+        idx, w = np.zeros(s, np.uint64), np.zeros(s)
+        self._chk(self.lib.ref_aug_sketch(_p(a), C.c_uint64(n), C.c_uint64(d), _p(b), _p(cand),
+                                          C.c_double(lam), C.c_double(d_eff_lower),
+                                          C.c_uint64(s), C.c_uint64(seed), _p(idx), _p(w)))
+        return idx, w
 
     def time_core_fast(self, shape, ranks, core, factors, lam, x, s, seed):
         """The reference's own update_core_fast, timed inside the harness (ref_time_core_fast):

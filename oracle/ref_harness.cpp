@@ -161,6 +161,27 @@ int ref_update_core_fast(uint32_t order, const uint64_t* shape, const uint64_t* 
   });
 }
 
+// The dense toolkit's RowSketch as the reference makes it: approximate_ridge_regression
+// (sketch_ridge.cpp:153-164) with AugmentedSampler(candidate scores, d_eff_lower).
+int ref_aug_sketch(const double* a, uint64_t n, uint64_t d, const double* b, const double* cand,
+                   double lambda, double d_eff_lower, uint64_t s, uint64_t seed,
+                   uint64_t* indices, double* weights) {
+  return run([&] {
+    DenseMatrix am(n, d);
+    std::memcpy(am.data(), a, n * d * sizeof(double));
+    ScoreVector sc;
+    sc.scores.assign(cand, cand + n);
+    SketchConfig cfg;
+    cfg.lambda = lambda;
+    cfg.seed = seed;
+    cfg.sample_count_override = s;
+    const SketchedSolution sol =
+        approximate_ridge_regression(am, std::span<const double>(b, n), sc, d_eff_lower, cfg);
+    std::memcpy(indices, sol.sketch.sampled_indices.data(), s * sizeof(uint64_t));
+    std::memcpy(weights, sol.sketch.weights.data(), s * sizeof(double));
+  });
+}
+
 // Times the reference's own public update_core_fast (ref tucker.cpp:141-166) on a given
 // model (bench.py's reference arm): out[0] = seconds of the call, out[1] = setup (factor
 // SVDs, scores, CDFs), out[2] = draws, out[3] = response gather, out[4] = solve (the

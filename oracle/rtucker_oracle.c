@@ -626,6 +626,41 @@ done:
   return status;
 }
 
+/* The dense toolkit's RowSketch alone: s draws of AugmentedSampler(cand, d, d_eff_lower)
+ * from SplitMix64(seed), weights sqrt((1/s)/prob) (sampler.cpp:9-57,
+ * sketch_ridge.cpp:80-90). */
+int orc_aug_draw(const double* cand, uint64_t n, uint64_t d, double d_eff_lower, uint64_t seed,
+                 uint64_t s, uint64_t* idx_out, double* w_out) {
+  aug_sampler sam;
+  int status = aug_sampler_init(&sam, cand, n, d, d_eff_lower);
+  if (status != ORC_OK) return status;
+  orc_rng rng = {seed};
+  const double inv_s = 1.0 / (double)s;
+  for (uint64_t t = 0; t < s; ++t) {
+    double prob;
+    aug_sampler_draw(&sam, &rng, &idx_out[t], &prob);
+    w_out[t] = sqrt(inv_s / prob);
+  }
+  aug_sampler_free(&sam);
+  return ORC_OK;
+}
+
+/* Sketched normal equations of [A; sqrt(lambda) I] (dense rows) from a given RowSketch
+ * (sketch_ridge.cpp:105-128 with a MatrixRowSource): g (d x d, full), rhs (d). */
+int orc_dense_normal_eq(const double* a, uint64_t n, uint64_t d, const double* b, double lambda,
+                        uint64_t s, const uint64_t* idx, const double* w, double* g,
+                        double* rhs) {
+  double* sb = xcalloc(s ? s : 1, sizeof(double));
+  if (!sb) return fail(ORC_NOMEM, "out of memory");
+  for (uint64_t t = 0; t < s; ++t) sb[t] = idx[t] < n ? b[idx[t]] : 0.0;
+  memset(g, 0, d * d * sizeof(double));
+  memset(rhs, 0, d * sizeof(double));
+  matrix_rows mr = {a, d};
+  normal_equations(matrix_row, &mr, n, d, lambda, s, idx, w, sb, g, rhs);
+  free(sb);
+  return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Kronecker design -- kronecker.cpp                                          */
 

@@ -64,6 +64,11 @@ int orc_sample_count(double beta_prime, size_t d, double epsilon, double delta,
                      uint64_t* out);
 
 /* Dense toolkit path behind rtucker_sketched_ridge (capi.cpp:324-362). */
+int orc_aug_draw(const double* cand, uint64_t n, uint64_t d, double d_eff_lower, uint64_t seed,
+                 uint64_t s, uint64_t* idx_out, double* w_out);
+int orc_dense_normal_eq(const double* a, uint64_t n, uint64_t d, const double* b, double lambda,
+                        uint64_t s, const uint64_t* idx, const double* w, double* g,
+                        double* rhs);
 int orc_sketched_ridge(const double* a, uint64_t n, uint64_t d, const double* b,
                        const double* candidate_scores, double lambda,
                        double d_eff_lower, double epsilon, double delta,

@@ -876,6 +876,37 @@ rtucker_status rtucker_b200_kron_normal_eq(uint32_t order, const uint64_t* rows,
   });
 }
 
+rtucker_status rtucker_b200_aug_draw(const double* candidate_scores, uint64_t n, uint64_t d,
+                                     double d_eff_lower, uint64_t seed, uint64_t s,
+                                     uint64_t* indices_out, double* weights_out) {
+  if (!candidate_scores || !indices_out || !weights_out)
+    return fail(RTUCKER_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded(
+      [&] { rtb::aug_draw(candidate_scores, n, d, d_eff_lower, seed, s, indices_out, weights_out); });
+}
+
+rtucker_status rtucker_b200_dense_normal_eq(const double* a, uint64_t n, uint64_t d,
+                                            const double* b, double lambda, uint64_t s,
+                                            const uint64_t* indices, const double* weights,
+                                            double* gram_out, double* rhs_out) {
+  if (!a || !b || !indices || !weights || !gram_out || !rhs_out)
+    return fail(RTUCKER_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded(
+      [&] { rtb::dense_normal_eq(a, n, d, b, lambda, s, indices, weights, gram_out, rhs_out); });
+}
+
+rtucker_status rtucker_b200_sample_count(double beta_prime, uint64_t d, double epsilon,
+                                         double delta, uint64_t* out) {
+  if (!out) return fail(RTUCKER_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] { *out = rtb::sample_count_formula(beta_prime, d, epsilon, delta); });
+}
+
+rtucker_status rtucker_b200_sym_eig(const double* a, uint64_t d, double* evals_out,
+                                    double* evecs_out) {
+  if (!a || !evals_out || !evecs_out) return fail(RTUCKER_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] { rtb::sym_eig(a, d, evals_out, evecs_out); });
+}
+
 rtucker_status rtucker_b200_spd_solve(const double* gram, const double* rhs, uint64_t d,
                                       double* x_out, uint64_t* rank_out, int* path_out) {
   if (!gram || !rhs || !x_out) return fail(RTUCKER_ERR_INVALID_ARGUMENT, "null argument");

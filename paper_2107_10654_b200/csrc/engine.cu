@@ -12,6 +12,7 @@
 //                registers + next sweep's T                      (tucker.cpp:216-229)
 #include "engine.h"
 
+#include <algorithm>
 #include <cfloat>
 #include <chrono>
 #include <cmath>
@@ -792,7 +793,7 @@ class Engine {
   uint64_t sketch_rng_ = 0, sketch_k_ = 0;
   uint64_t factor_rng_ = 0, factor_k_ = 0;
   bool scores_valid_ = false;
-  DevBuf fsums_, fsk_idx_, fsk_w_, fsk_work_;
+  DevBuf fsums_, fsk_idx_, fsk_w_, fsk_work_, hj_ws_;
   bool t_valid_ = false;
   uint64_t last_s_ = 0;
   int last_rank_deficient_ = 0, last_solver_path_ = 0, last_pcg_iters_ = 0;
@@ -1266,24 +1267,37 @@ class Engine {
     {
       Scope sc(prof_, "scores");
       // classical scores l_i = a_i^T (A^T A)^+ a_i: Cholesky of each factor Gram
-      // (||L^-1 a_i||^2); eigen path (rank cutoff) for modes whose Gram is
-      // numerically singular (ref leverage.cpp:16-37 at lambda = 0)
+      // (||L^-1 a_i||^2); where a Gram's Cholesky meets a pivot below max(I, R) eps (so
+      // sigma_min / sigma_max may be small enough for the reference's cut), the
+      // reference's own route: one-sided Jacobi SVD of the factor and the rank cut on its
+      // singular values (k_hj_cta; ref kronecker.cpp:18-23, svd.cpp:69-111,
+      // leverage.cpp:16-37 at lambda = 0)
       FactorSet fs = factor_set();
       int maxI = 0;
       for (auto v : shape_) maxI = std::max<int>(maxI, (int)v);
       const int* okm = nullptr;
+      dim3 grid(ceil_div(maxI, 128), N_);
       if (rmax_ <= 32) {
         spd_small(grams_.as<double>(), ns_.as<int>(), eig_stride_, (double)maxI * DBL_EPSILON,
                   linv_.as<double>(), pgram_.as<double>(), spd_ok_.as<int>(), N_, st_, rmax_);
         okm = spd_ok_.as<int>();
+        long long stride = 0;
+        for (int n = 0; n < N_; ++n)
+          stride = std::max<long long>(stride, (long long)shape_[n] * (ranks_[n] + (ranks_[n] & 1)));
+        hj_ws_.ensure((size_t)N_ * stride * 8 + 64, st_);
+        k_hj_cta<<<N_, 512, 0, st_>>>(fs, hj_ws_.as<double>(), stride, 0.0, scores_.as<double>(),
+                                      score_off_.as<long long>(), ranks_dev_.as<int>(), okm,
+                                      eig_status_.as<int>());
+        RTB_LAUNCH_CHECK();
+      } else {
+        sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, evals_.as<double>(),
+                  evecs_.as<double>(), eig_status_.as<int>(), N_, st_, okm);
+        k_leverage_rows<<<grid, 128, 0, st_>>>(fs, evals_.as<double>(), evecs_.as<double>(),
+                                              eig_stride_, 0.0, scores_.as<double>(),
+                                              score_off_.as<long long>(), ranks_dev_.as<int>(),
+                                              okm);
+        RTB_LAUNCH_CHECK();
       }
-      sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, evals_.as<double>(),
-                evecs_.as<double>(), eig_status_.as<int>(), N_, st_, okm);
-      dim3 grid(ceil_div(maxI, 128), N_);
-      k_leverage_rows<<<grid, 128, 0, st_>>>(fs, evals_.as<double>(), evecs_.as<double>(),
-                                            eig_stride_, 0.0, scores_.as<double>(),
-                                            score_off_.as<long long>(), ranks_dev_.as<int>(), okm);
-      RTB_LAUNCH_CHECK();
       if (okm) {
         k_leverage_chol<<<grid, 128, 0, st_>>>(fs, linv_.as<double>(), eig_stride_, okm,
                                               scores_.as<double>(), score_off_.as<long long>(),
@@ -1918,43 +1932,42 @@ void model_reconstruct(const std::vector<uint64_t>& shape, const std::vector<uin
 void factor_scores(const double* factor_host, int rows, int cols, double* scores, double* cdf,
                    double* sum, uint64_t* rank) {
   if (rows <= 0 || cols <= 0) throw Error(1, "compact_svd: empty matrix");
-  if (cols > 64) throw Error(4, "factor_scores: rank > 64 not supported");
   cudaStream_t st = current_stream();
-  DevBuf f((size_t)rows * cols * 8, st), g((size_t)cols * cols * 8, st),
-      ev((size_t)cols * cols * 8 + 8, st), evec((size_t)cols * cols * 8, st), stat(4, st),
-      ns(4, st), sc((size_t)rows * 8, st), cd((size_t)rows * 8, st), sm(8, st), off(8, st),
-      rw(4, st), rk(4, st);
+  DevBuf f((size_t)rows * cols * 8, st), sc((size_t)rows * 8, st), cd((size_t)rows * 8, st),
+      sm(8, st), off(8, st), rw(4, st), rk(4, st), stat(4, st);
   RTB_CUDA(cudaMemcpyAsync(f.p, factor_host, (size_t)rows * cols * 8, cudaMemcpyHostToDevice, st));
   long long zero = 0;
   RTB_CUDA(cudaMemcpyAsync(off.p, &zero, 8, cudaMemcpyHostToDevice, st));
   RTB_CUDA(cudaMemcpyAsync(rw.p, &rows, 4, cudaMemcpyHostToDevice, st));
-  RTB_CUDA(cudaMemcpyAsync(ns.p, &cols, 4, cudaMemcpyHostToDevice, st));
+  RTB_CUDA(cudaMemsetAsync(stat.p, 0, 4, st));
   FactorSet fs{};
   fs.order = 1;
   fs.ptr[0] = f.as<double>();
   fs.rows[0] = rows;
   fs.cols[0] = cols;
-  k_factor_gram<<<dim3(cols * cols, 1), 256, 0, st>>>(fs, g.as<double>(), cols);
-  RTB_LAUNCH_CHECK();
-  // same route as the ALS core step: Cholesky of the Gram, eigen fallback
-  DevBuf lv((size_t)cols * cols * 8 + 8, st), okb(4, st);
-  const int* okm = nullptr;
-  if (cols <= 32) {
+  if (cols <= 32 && rows >= cols) {
+    // same route as the ALS core step: Cholesky of the Gram, one-sided Jacobi SVD behind it
+    DevBuf g((size_t)cols * cols * 8, st), ns(4, st), lv((size_t)cols * cols * 8 + 8, st),
+        okb(4, st), ws((size_t)rows * (cols + 1) * 8 + 64, st);
+    RTB_CUDA(cudaMemcpyAsync(ns.p, &cols, 4, cudaMemcpyHostToDevice, st));
+    k_factor_gram<<<dim3(cols * cols, 1), 256, 0, st>>>(fs, g.as<double>(), cols);
+    RTB_LAUNCH_CHECK();
     spd_small(g.as<double>(), ns.as<int>(), cols * cols,
               (double)std::max(rows, cols) * DBL_EPSILON, lv.as<double>(), nullptr, okb.as<int>(), 1,
               st);
-    okm = okb.as<int>();
-  }
-  sym_eigen(g.as<double>(), ns.as<int>(), cols, cols * cols, ev.as<double>(), evec.as<double>(),
-            stat.as<int>(), 1, st, okm);
-  k_leverage_rows<<<dim3(ceil_div(rows, 128), 1), 128, 0, st>>>(
-      fs, ev.as<double>(), evec.as<double>(), cols * cols, 0.0, sc.as<double>(),
-      off.as<long long>(), rk.as<int>(), okm);
-  RTB_LAUNCH_CHECK();
-  if (okm) {
-    k_leverage_chol<<<dim3(ceil_div(rows, 128), 1), 128, 0, st>>>(
-        fs, lv.as<double>(), cols * cols, okm, sc.as<double>(), off.as<long long>(), rk.as<int>());
+    k_hj_cta<<<1, 512, 0, st>>>(fs, ws.as<double>(), (long long)rows * (cols + (cols & 1)), 0.0,
+                                sc.as<double>(), off.as<long long>(), rk.as<int>(), okb.as<int>(),
+                                stat.as<int>());
     RTB_LAUNCH_CHECK();
+    k_leverage_chol<<<dim3(ceil_div(rows, 128), 1), 128, 0, st>>>(
+        fs, lv.as<double>(), cols * cols, okb.as<int>(), sc.as<double>(), off.as<long long>(),
+        rk.as<int>());
+    RTB_LAUNCH_CHECK();
+  } else {
+    DevBuf ws(hj_work_bytes(rows, cols), st);
+    int r = 0;
+    hj_ridge_scores(f.as<double>(), rows, cols, 0.0, sc.as<double>(), &r, ws.p, st);
+    RTB_CUDA(cudaMemcpyAsync(rk.p, &r, 4, cudaMemcpyHostToDevice, st));
   }
   k_score_cdf<<<1, 32, 0, st>>>(sc.as<double>(), off.as<long long>(), rw.as<int>(), 1,
                                 cd.as<double>(), sm.as<double>());
@@ -1966,7 +1979,7 @@ void factor_scores(const double* factor_host, int rows, int cols, double* scores
   RTB_CUDA(cudaMemcpyAsync(&r, rk.p, 4, cudaMemcpyDeviceToHost, st));
   RTB_CUDA(cudaMemcpyAsync(&es, stat.p, 4, cudaMemcpyDeviceToHost, st));
   RTB_CUDA(cudaStreamSynchronize(st));
-  if (es) throw Error(3, "symmetric eigensolver did not converge");
+  if (es) throw Error(3, "compact_svd: Jacobi sweeps did not converge");
   *rank = (uint64_t)r;
 }
 
@@ -2157,8 +2170,8 @@ void kron_normal_eq(int order, const uint64_t* rows, const uint64_t* ranks, cons
 }
 
 // x = gram^+ rhs: Cholesky, else (d <= 64) eigen pinv with the reference cutoff.
-static void solve_sym_device(double* G, double* rhs, int d, double* x_dev, int* rank, int* path,
-                             bool need_spd_else_error, cudaStream_t st) {
+void solve_sym_device(double* G, double* rhs, int d, double* x_dev, int* rank, int* path,
+                      cudaStream_t st) {
   DevBuf work(chol_work_bytes(d), st), stat(4, st), copy((size_t)d * d * 8, st);
   RTB_CUDA(cudaMemcpyAsync(copy.p, G, (size_t)d * d * 8, cudaMemcpyDeviceToDevice, st));
   RTB_CUDA(cudaMemcpyAsync(x_dev, rhs, (size_t)d * 8, cudaMemcpyDeviceToDevice, st));
@@ -2171,8 +2184,7 @@ static void solve_sym_device(double* G, double* rhs, int d, double* x_dev, int* 
     *path = 0;
     return;
   }
-  if (d > 64) {  // dense eigen pinv (k_pinv.cu) on a fresh copy of G
-    (void)need_spd_else_error;
+  if (d > 64) {  // block-Jacobi eigen pinv (k_eig.cu) of G
     RTB_CUDA(cudaMemcpyAsync(copy.p, G, (size_t)d * d * 8, cudaMemcpyDeviceToDevice, st));
     DevBuf pw(pinv_large_work_bytes(d), st), rk(4, st);
     pinv_solve_large(copy.as<double>(), d, rhs, x_dev, rk.as<int>(), pw.p, pw.bytes, st);
@@ -2198,6 +2210,41 @@ static void solve_sym_device(double* G, double* rhs, int d, double* x_dev, int* 
   *path = 1;
 }
 
+void sym_eig(const double* a, uint64_t d, double* evals, double* evecs) {
+  if (d == 0) throw Error(1, "compact_svd: empty matrix");
+  if (d > 46340) throw Error(1, "sym_eig: d too large");
+  cudaStream_t st = current_stream();
+  const int n = (int)d;
+  DevBuf A(d * d * 8, st), ev(d * 8 + 8, st), V(d * d * 8, st);
+  RTB_CUDA(cudaMemcpyAsync(A.p, a, d * d * 8, cudaMemcpyHostToDevice, st));
+  if (n <= 64) {
+    DevBuf es(4, st), ns(4, st);
+    RTB_CUDA(cudaMemcpyAsync(ns.p, &n, 4, cudaMemcpyHostToDevice, st));
+    sym_eigen(A.as<double>(), ns.as<int>(), n, n * n, ev.as<double>(), V.as<double>(),
+              es.as<int>(), 1, st);
+    int e = 0;
+    RTB_CUDA(cudaMemcpyAsync(&e, es.p, 4, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaMemcpyAsync(evals, ev.p, d * 8, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaMemcpyAsync(evecs, V.p, d * d * 8, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaStreamSynchronize(st));
+    if (e) throw Error(3, "symmetric_eigen: Jacobi sweeps did not converge");
+    return;  // already sorted non-increasing
+  }
+  DevBuf work(eig_large_work_bytes(n), st);
+  sym_eig_large(A.as<double>(), n, ev.as<double>(), V.as<double>(), work.p, st);
+  std::vector<double> mu(d), vv(d * d);
+  RTB_CUDA(cudaMemcpyAsync(mu.data(), ev.p, d * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaMemcpyAsync(vv.data(), V.p, d * d * 8, cudaMemcpyDeviceToHost, st));
+  RTB_CUDA(cudaStreamSynchronize(st));
+  std::vector<int> ord(d);
+  for (int i = 0; i < n; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return mu[x] > mu[y]; });
+  for (int k = 0; k < n; ++k) {
+    evals[k] = mu[ord[k]];
+    for (int i = 0; i < n; ++i) evecs[(size_t)i * d + k] = vv[(size_t)i * d + ord[k]];
+  }
+}
+
 void spd_solve(const double* gram, const double* rhs, uint64_t d, double* x, uint64_t* rank,
                int* path) {
   if (d == 0) throw Error(1, "compact_svd: empty matrix");
@@ -2206,249 +2253,11 @@ void spd_solve(const double* gram, const double* rhs, uint64_t d, double* x, uin
   RTB_CUDA(cudaMemcpyAsync(G.p, gram, d * d * 8, cudaMemcpyHostToDevice, st));
   RTB_CUDA(cudaMemcpyAsync(r.p, rhs, d * 8, cudaMemcpyHostToDevice, st));
   int rk = 0, pth = 0;
-  solve_sym_device(G.as<double>(), r.as<double>(), (int)d, xd.as<double>(), &rk, &pth, true, st);
+  solve_sym_device(G.as<double>(), r.as<double>(), (int)d, xd.as<double>(), &rk, &pth, st);
   RTB_CUDA(cudaMemcpyAsync(x, xd.p, d * 8, cudaMemcpyDeviceToHost, st));
   RTB_CUDA(cudaStreamSynchronize(st));
   if (rank) *rank = (uint64_t)rk;
   if (path) *path = pth;
-}
-
-// ---------------------------------------------------------------------------
-// dense ridge toolkit (ref capi.cpp:299-362, linalg.cpp:28-41, leverage.cpp:39-52,
-// sampler.cpp:9-57, sketch_ridge.cpp:52-164)
-
-__global__ void k_atb(const double* a, long long n, int d, const double* b, double* out) {
-  __shared__ double red[32];
-  const int j = blockIdx.x;
-  double s = 0.0;
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) s += a[i * d + j] * b[i];
-  s = block_sum<256>(s, red);
-  if (threadIdx.x == 0) out[j] = s;
-}
-
-__global__ void k_any_nonzero(const double* a, long long n, int* flag) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && a[i] != 0.0) atomicExch(flag, 1);
-}
-
-static void dense_gram(const double* a_dev, uint64_t n, uint64_t d, double* g_dev,
-                       cudaStream_t st) {
-  FactorSet fs{};
-  fs.order = 1;
-  fs.ptr[0] = a_dev;
-  fs.rows[0] = (int)n;
-  fs.cols[0] = (int)d;
-  k_factor_gram<<<dim3((unsigned)(d * d), 1), 256, 0, st>>>(fs, g_dev, (int)d);
-  RTB_LAUNCH_CHECK();
-}
-
-void dense_ridge_scores(const double* a, uint64_t n, uint64_t d, double lambda, double* out) {
-  if (lambda < 0.0) throw Error(1, "ridge_scores: lambda must be non-negative");
-  if (n == 0 || d == 0) throw Error(1, "compact_svd: empty matrix");
-  if (d > 64) throw Error(4, "ridge_scores: d > 64 not supported by this build");
-  cudaStream_t st = current_stream();
-  DevBuf ad(n * d * 8, st), g(d * d * 8, st), ev(d * d * 8 + 8, st), evec(d * d * 8, st),
-      es(4, st), ns(4, st), sc(n * 8, st), off(8, st), rk(4, st), nz(4, st);
-  RTB_CUDA(cudaMemcpyAsync(ad.p, a, n * d * 8, cudaMemcpyHostToDevice, st));
-  RTB_CUDA(cudaMemsetAsync(nz.p, 0, 4, st));
-  k_any_nonzero<<<(unsigned)ceil_div<uint64_t>(n * d, 256), 256, 0, st>>>(ad.as<double>(),
-                                                                        (long long)(n * d),
-                                                                        nz.as<int>());
-  RTB_LAUNCH_CHECK();
-  int any = 0;
-  RTB_CUDA(cudaMemcpyAsync(&any, nz.p, 4, cudaMemcpyDeviceToHost, st));
-  RTB_CUDA(cudaStreamSynchronize(st));
-  if (!any) {  // zero rows score zero (ref leverage.cpp:40-50)
-    std::memset(out, 0, n * 8);
-    return;
-  }
-  dense_gram(ad.as<double>(), n, d, g.as<double>(), st);
-  const int di = (int)d, np = di + (di & 1);
-  long long zero = 0;
-  RTB_CUDA(cudaMemcpyAsync(ns.p, &di, 4, cudaMemcpyHostToDevice, st));
-  RTB_CUDA(cudaMemcpyAsync(off.p, &zero, 8, cudaMemcpyHostToDevice, st));
-  sym_eigen(g.as<double>(), ns.as<int>(), di, di * di, ev.as<double>(), evec.as<double>(),
-            es.as<int>(), 1, st);
-  FactorSet fs{};
-  fs.order = 1;
-  fs.ptr[0] = ad.as<double>();
-  fs.rows[0] = (int)n;
-  fs.cols[0] = di;
-  k_leverage_rows<<<dim3((unsigned)ceil_div<uint64_t>(n, 128), 1), 128, 0, st>>>(
-      fs, ev.as<double>(), evec.as<double>(), di * di, lambda, sc.as<double>(),
-      off.as<long long>(), rk.as<int>(), nullptr);
-  RTB_LAUNCH_CHECK();
-  int e = 0;
-  RTB_CUDA(cudaMemcpyAsync(out, sc.p, n * 8, cudaMemcpyDeviceToHost, st));
-  RTB_CUDA(cudaMemcpyAsync(&e, es.p, 4, cudaMemcpyDeviceToHost, st));
-  RTB_CUDA(cudaStreamSynchronize(st));
-  if (e) throw Error(3, "compact_svd: Jacobi sweeps did not converge");
-}
-
-void dense_solve_ridge(const double* a, uint64_t n, uint64_t d, const double* b, double lambda,
-                       double* x) {
-  if (lambda < 0.0) throw Error(1, "solve_ridge_exact: lambda must be non-negative");
-  if (d == 0) throw Error(1, "compact_svd: empty matrix");
-  cudaStream_t st = current_stream();
-  DevBuf ad(n * d * 8 + 8, st), bd(n * 8 + 8, st), g(d * d * 8, st), atb(d * 8, st),
-      xd(d * 8, st);
-  RTB_CUDA(cudaMemcpyAsync(ad.p, a, n * d * 8, cudaMemcpyHostToDevice, st));
-  RTB_CUDA(cudaMemcpyAsync(bd.p, b, n * 8, cudaMemcpyHostToDevice, st));
-  dense_gram(ad.as<double>(), n, d, g.as<double>(), st);
-  k_add_diag<<<(unsigned)ceil_div<uint64_t>(d, 64), 64, 0, st>>>(g.as<double>(), (int)d, lambda);
-  RTB_LAUNCH_CHECK();
-  k_atb<<<(unsigned)d, 256, 0, st>>>(ad.as<double>(), (long long)n, (int)d, bd.as<double>(),
-                                     atb.as<double>());
-  RTB_LAUNCH_CHECK();
-  int rk = 0, path = 0;
-  solve_sym_device(g.as<double>(), atb.as<double>(), (int)d, xd.as<double>(), &rk, &path, true, st);
-  RTB_CUDA(cudaMemcpyAsync(x, xd.p, d * 8, cudaMemcpyDeviceToHost, st));
-  RTB_CUDA(cudaStreamSynchronize(st));
-}
-
-// AugmentedSampler tables, sequential like the reference (sampler.cpp:9-40):
-// out[0] = data_mass, out[1] = aug_mass_per_row, out[2] = total_mass, flag on bad input.
-__global__ void k_aug_tables(const double* cand, long long n, int d, double d_eff_lower,
-                             double* norm, double* cum, double* out, int* flag) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double l1 = 0.0;
-  for (long long i = 0; i < n; ++i) {
-    const double s = cand[i];
-    if (!(s >= 0.0) || !isfinite(s)) {
-      *flag = 1;
-      return;
-    }
-    l1 = __dadd_rn(l1, s);
-  }
-  if (l1 <= 0.0) {
-    *flag = 2;
-    return;
-  }
-  const double scale = __ddiv_rn((double)d, l1);
-  double running = 0.0;
-  for (long long i = 0; i < n; ++i) {
-    norm[i] = __dmul_rn(cand[i], scale);
-    running = __dadd_rn(running, norm[i]);
-    cum[i] = running;
-  }
-  const double m = __dadd_rn((double)d, -d_eff_lower);
-  const double aug = m < 1.0 ? m : 1.0;
-  out[0] = running;
-  out[1] = aug;
-  out[2] = __dadd_rn(running, __dmul_rn((double)d, aug));
-}
-
-// one u64 per draw: draw t uses stream output t (sampler.cpp:42-57)
-__global__ void k_aug_draw(const double* norm, const double* cum, long long n, int d,
-                           const double* tab, unsigned long long seed, long long s,
-                           unsigned long long* idx, double* w) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= s) return;
-  const double data_mass = tab[0], aug = tab[1], total = tab[2];
-  const double inv_s = __ddiv_rn(1.0, (double)s);
-  const double u = __dmul_rn(u64_to_unit(sm_at(seed, (uint64_t)t)), total);
-  double prob;
-  unsigned long long index;
-  if (u < data_mass || aug == 0.0) {
-    const double key = u < data_mass ? u : data_mass;
-    long long lo = 0, len = n;
-    while (len > 0) {
-      const long long half = len >> 1;
-      if (!(key < cum[lo + half])) {
-        lo += half + 1;
-        len -= half + 1;
-      } else {
-        len = half;
-      }
-    }
-    long long i = lo >= n ? n - 1 : lo;
-    while (i > 0 && norm[i] == 0.0) --i;
-    index = (unsigned long long)i;
-    prob = __ddiv_rn(norm[i], total);
-  } else {
-    long long k = (long long)__ddiv_rn(__dadd_rn(u, -data_mass), aug);
-    if (k >= d) k = d - 1;
-    index = (unsigned long long)(n + k);
-    prob = __ddiv_rn(aug, total);
-  }
-  idx[t] = index;
-  w[t] = __dsqrt_rn(__ddiv_rn(inv_s, prob));
-}
-
-// sketched normal equations over dense rows (+ sqrt(lambda) e_k rows)
-__global__ void k_dense_sketch_gram(const double* a, long long n, int d, const double* b,
-                                    double rl, const unsigned long long* idx, const double* w,
-                                    long long s, double* G, double* rhs) {
-  __shared__ double red[32];
-  const int e = blockIdx.x;
-  const int p = e / (d + 1), q = e % (d + 1);  // q == d -> rhs entry
-  if (q < d && q < p) return;
-  double acc = 0.0;
-  for (long long t = threadIdx.x; t < s; t += blockDim.x) {
-    const unsigned long long j = idx[t];
-    const double w2 = w[t] * w[t];
-    const double rp = j < (unsigned long long)n ? a[j * d + p] : ((long long)j - n == p ? rl : 0.0);
-    double rq;
-    if (q == d) rq = j < (unsigned long long)n ? b[j] : 0.0;
-    else rq = j < (unsigned long long)n ? a[j * d + q] : ((long long)j - n == q ? rl : 0.0);
-    acc += (w2 * rp) * rq;
-  }
-  acc = block_sum<256>(acc, red);
-  if (threadIdx.x == 0) {
-    if (q == d) {
-      rhs[p] = acc;
-    } else {
-      G[(size_t)p * d + q] = acc;
-      G[(size_t)q * d + p] = acc;
-    }
-  }
-}
-
-void dense_sketched_ridge(const double* a, uint64_t n, uint64_t d, const double* b,
-                          const double* cand, double lambda, double d_eff_lower, double eps,
-                          double delta, uint64_t s_override, uint64_t seed, double* x,
-                          uint64_t* s_out, double* beta_out) {
-  if (d == 0) throw Error(1, "AugmentedSampler: d must be positive");
-  if (d_eff_lower < 0.0 || d_eff_lower > (double)d)
-    throw Error(1, "AugmentedSampler: d_eff_lower outside [0, d]");
-  if (lambda < 0.0) throw Error(1, "solve_sketched_ridge: lambda must be non-negative");
-  std::vector<double> scores(n);
-  if (cand) std::memcpy(scores.data(), cand, n * 8);
-  else dense_ridge_scores(a, n, d, 0.0, scores.data());  // classical_scores
-  cudaStream_t st = current_stream();
-  const double m = std::min(1.0, (double)d - d_eff_lower);
-  const double beta_prime = 1.0 / (1.0 + m);
-  const uint64_t s = s_override ? s_override : sample_count_formula(beta_prime, d, eps, delta);
-  DevBuf ad(n * d * 8 + 8, st), bd(n * 8 + 8, st), sc(n * 8 + 8, st), nm(n * 8 + 8, st),
-      cm(n * 8 + 8, st), tab(32, st), fl(4, st), ix(s * 8, st), ww(s * 8, st), G(d * d * 8, st),
-      r(d * 8, st), xd(d * 8, st);
-  RTB_CUDA(cudaMemcpyAsync(ad.p, a, n * d * 8, cudaMemcpyHostToDevice, st));
-  RTB_CUDA(cudaMemcpyAsync(bd.p, b, n * 8, cudaMemcpyHostToDevice, st));
-  RTB_CUDA(cudaMemcpyAsync(sc.p, scores.data(), n * 8, cudaMemcpyHostToDevice, st));
-  RTB_CUDA(cudaMemsetAsync(fl.p, 0, 4, st));
-  k_aug_tables<<<1, 1, 0, st>>>(sc.as<double>(), (long long)n, (int)d, d_eff_lower,
-                                nm.as<double>(), cm.as<double>(), tab.as<double>(), fl.as<int>());
-  RTB_LAUNCH_CHECK();
-  int flag = 0;
-  RTB_CUDA(cudaMemcpyAsync(&flag, fl.p, 4, cudaMemcpyDeviceToHost, st));
-  RTB_CUDA(cudaStreamSynchronize(st));
-  if (flag == 1) throw Error(1, "AugmentedSampler: scores must be finite and non-negative");
-  if (flag == 2) throw Error(1, "AugmentedSampler: scores must not all be zero");
-  k_aug_draw<<<(unsigned)ceil_div<uint64_t>(s, 256), 256, 0, st>>>(
-      nm.as<double>(), cm.as<double>(), (long long)n, (int)d, tab.as<double>(), seed,
-      (long long)s, (unsigned long long*)ix.p, ww.as<double>());
-  RTB_LAUNCH_CHECK();
-  k_dense_sketch_gram<<<(unsigned)(d * (d + 1)), 256, 0, st>>>(
-      ad.as<double>(), (long long)n, (int)d, bd.as<double>(), std::sqrt(lambda),
-      (const unsigned long long*)ix.p, ww.as<double>(), (long long)s, G.as<double>(),
-      r.as<double>());
-  RTB_LAUNCH_CHECK();
-  int rk = 0, path = 0;
-  solve_sym_device(G.as<double>(), r.as<double>(), (int)d, xd.as<double>(), &rk, &path, true, st);
-  RTB_CUDA(cudaMemcpyAsync(x, xd.p, d * 8, cudaMemcpyDeviceToHost, st));
-  RTB_CUDA(cudaStreamSynchronize(st));
-  if (s_out) *s_out = s;
-  if (beta_out) *beta_out = beta_prime;
 }
 
 }  // namespace rtb

@@ -127,6 +127,9 @@ void kron_normal_eq(int order, const uint64_t* rows, const uint64_t* ranks, cons
                     const double* w, double* gram, double* rhs);
 void spd_solve(const double* gram, const double* rhs, uint64_t d, double* x, uint64_t* rank,
                int* path);
+// Symmetric eigendecomposition of a host d x d matrix on the GPU (d <= 64: CTA Jacobi,
+// larger: parallel block Jacobi, k_eig.cu): evals descending, evecs row-major (column k).
+void sym_eig(const double* a, uint64_t d, double* evals, double* evecs);
 // Model-level ops on a device tensor with a host model.
 void model_update_core_sketched(const double* x_dev, const std::vector<uint64_t>& shape,
                                 const std::vector<uint64_t>& ranks, const double* core,
@@ -147,6 +150,12 @@ void model_reconstruct(const std::vector<uint64_t>& shape, const std::vector<uin
 void dense_ridge_scores(const double* a, uint64_t n, uint64_t d, double lambda, double* out);
 void dense_solve_ridge(const double* a, uint64_t n, uint64_t d, const double* b, double lambda,
                        double* x);
+// AugmentedSampler draws (ref sampler.cpp:9-57) of s rows from candidate scores (host)
+void aug_draw(const double* cand, uint64_t n, uint64_t d, double d_eff_lower, uint64_t seed,
+              uint64_t s, uint64_t* idx_out, double* w_out);
+// sketched normal equations of [A; sqrt(lambda) I] from a given RowSketch (host buffers)
+void dense_normal_eq(const double* a, uint64_t n, uint64_t d, const double* b, double lambda,
+                     uint64_t s, const uint64_t* idx, const double* w, double* gram, double* rhs);
 void dense_sketched_ridge(const double* a, uint64_t n, uint64_t d, const double* b,
                           const double* cand, double lambda, double d_eff_lower, double eps,
                           double delta, uint64_t s_override, uint64_t seed, double* x,

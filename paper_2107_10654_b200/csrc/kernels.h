@@ -31,6 +31,14 @@ __global__ void k_leverage_chol(const FactorSet fs, const double* linv, int stri
 // batched small SPD Cholesky (n <= 32): Linv (+ optional P = M^-1), ok flags
 void spd_small(const double* in, const int* ns_dev, int stride, double tolrel, double* linv,
                double* pinv, int* ok, int nmat, cudaStream_t st, int nmax = 32);
+// one-sided Jacobi SVD scores of each matrix b of fs with n <= 32 columns (k_hjsvd.cu),
+// skipped where skip[b]; one CTA of 512 threads per matrix, workspace work_stride doubles each
+__global__ void k_hj_cta(const FactorSet fs, double* work, long long work_stride, double lambda,
+                         double* scores, const long long* score_off, int* ranks, const int* skip,
+                         int* status);
+size_t hj_work_bytes(long long rows, int cols);
+void hj_ridge_scores(const double* A, long long rows, int cols, double lambda, double* scores,
+                     int* rank, void* work, cudaStream_t st);
 __global__ void k_score_cdf(const double* scores, const long long* off, const int* rows,
                             int order, double* cdf, double* sums);
 __global__ void k_sym_pinv(const double* evals, const double* evecs, const int* ns, int stride,
@@ -198,9 +206,14 @@ bool pcg_supported(int d, int order, const int* ranks);
 void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, double* x, void* work,
                int* status_dev, cudaStream_t st);
 
-// ---- k_pinv.cu: x = G^+ b (d > 64), reference cutoff d eps max|mu| ----
+// ---- k_eig.cu: symmetric eigendecomposition (parallel block Jacobi, d > 64) and
+// x = G^+ b with the reference cutoff d eps max|mu| ----
+size_t eig_large_work_bytes(int d);
+// evals[d] (unsorted) and evecs (d x d row-major, column k = eigenvector k; optional)
+void sym_eig_large(const double* A, int d, double* evals, double* evecs, void* work,
+                   cudaStream_t st);
 size_t pinv_large_work_bytes(int d);
-// G (d x d symmetric, device) is overwritten; *rank_dev = number of kept eigenpairs
+// G (d x d symmetric, device) is left unchanged; *rank_dev = number of kept eigenpairs
 void pinv_solve_large(double* G, int d, const double* b, double* x, int* rank_dev, void* work,
                       size_t work_bytes, cudaStream_t st);
 

@@ -158,6 +158,13 @@ def _load() -> C.CDLL:
                                                      C.c_uint32, C.c_double, C.c_uint64,
                                                      C.c_uint64, _vp, _vp, _u64p, _f64p, _u64p,
                                                      _u64p, _f64p, C.c_uint32, C.c_uint32]),
+        "rtucker_b200_sym_eig": (S, [_f64p, C.c_uint64, _f64p, _f64p]),
+        "rtucker_b200_aug_draw": (S, [_f64p, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64,
+                                      C.c_uint64, _u64p, _f64p]),
+        "rtucker_b200_dense_normal_eq": (S, [_f64p, C.c_uint64, C.c_uint64, _f64p, C.c_double,
+                                             C.c_uint64, _u64p, _f64p, _f64p, _f64p]),
+        "rtucker_b200_sample_count": (S, [C.c_double, C.c_uint64, C.c_double, C.c_double,
+                                          _u64p]),
         "rtucker_b200_spd_solve": (S, [_f64p, _f64p, C.c_uint64, _f64p, _u64p,
                                        C.POINTER(C.c_int)]),
         "rtucker_b200_update_core_sketched": (S, [_vp, _vp, C.c_uint64, C.c_uint64, _f64p, _u64p,
@@ -616,6 +623,40 @@ def tensor_fiber_major(x_ptr, shape, out_ptr):
     (rtucker_b200_tensor_fiber_major)."""
     shape = _u64(shape)
     _check(lib.rtucker_b200_tensor_fiber_major(C.c_void_p(x_ptr), _p(shape), C.c_void_p(out_ptr)))
+
+
+def aug_draw(candidate_scores, d, d_eff_lower, seed, s):
+    """Dense-toolkit RowSketch (AugmentedSampler) drawn on the GPU."""
+    cand = _f64(candidate_scores)
+    idx, w = np.zeros(s, np.uint64), np.zeros(s)
+    _check(lib.rtucker_b200_aug_draw(_p(cand), len(cand), d, d_eff_lower, seed, s, _p(idx),
+                                     _p(w)))
+    return idx, w
+
+
+def dense_normal_eq(a, b, lam, idx, w):
+    a, b = _f64(a), _f64(b)
+    n, d = a.shape
+    idx, w = _u64(idx), _f64(w)
+    g, rhs = np.zeros((d, d)), np.zeros(d)
+    _check(lib.rtucker_b200_dense_normal_eq(_p(a), n, d, _p(b), lam, len(idx), _p(idx), _p(w),
+                                            _p(g), _p(rhs)))
+    return g, rhs
+
+
+def sample_count(beta_prime, d, epsilon, delta) -> int:
+    out = np.zeros(1, np.uint64)
+    _check(lib.rtucker_b200_sample_count(beta_prime, d, epsilon, delta, _p(out)))
+    return int(out[0])
+
+
+def sym_eig(a):
+    """(evals non-increasing, evecs with eigenvector k in column k) on the GPU."""
+    a = _f64(a)
+    d = a.shape[0]
+    ev, vec = np.zeros(d), np.zeros((d, d))
+    _check(lib.rtucker_b200_sym_eig(_p(a), d, _p(ev), _p(vec)))
+    return ev, vec
 
 
 def spd_solve(g, rhs):

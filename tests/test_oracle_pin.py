@@ -111,3 +111,19 @@ def test_error_paths_match(oracle, ref):
         with pytest.raises(OracleError) as er:
             ref.als(x, ranks, **kw)
         assert eo.value.code == er.value.code == 1
+
+
+@pytest.mark.parametrize("n,d,del_,s,seed", [(50, 4, 0.0, 3000, 99), (300, 12, 11.5, 5000, 3),
+                                             (120, 6, 6.0, 2000, 8)])
+def test_aug_draw_matches_reference_sketch(oracle, ref, n, d, del_, s, seed):
+    """The oracle's AugmentedSampler draws (the GPU test's checker) are the RowSketch of the
+    reference's own approximate_ridge_regression, bit for bit (sampler.cpp:9-57)."""
+    rng = np.random.default_rng(n + d)
+    a = rng.standard_normal((n, d))
+    b = rng.standard_normal(n)
+    cand = rng.random(n) ** 2
+    cand[::5] = 0.0
+    oi, ow = oracle.aug_draw(cand, d, del_, seed, s)
+    ri, rw = ref.aug_sketch(a, b, cand, 0.1, del_, s, seed)
+    assert np.array_equal(oi, ri)
+    assert np.array_equal(ow, rw)

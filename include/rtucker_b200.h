@@ -31,7 +31,7 @@ rtucker_status rtucker_b200_set_stream(void* stream);
 /* Number of this library's kernel launches so far in the process. */
 unsigned long long rtucker_b200_launch_count(void);
 /* Launches so far of one named kernel variant of the headline path ("k_ttm_mid3",
- * "k_ttm_mid2", "k_ttm_last3", "k_ttm_last3_fused", "k_vech_bucket2<17>",
+ * "k_ttm_mid2", "k_ttm_last3", "k_ttm_last3_fused", "k_vech_bucket2<17>", "k_vech_bucket5",
  * "k_vech_contract2", "k_pcg<16,16>"): lets tests assert which kernel ran. */
 unsigned long long rtucker_b200_variant_count(const char* name);
 

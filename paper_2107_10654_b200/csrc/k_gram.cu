@@ -29,6 +29,9 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <type_traits>
 
 namespace rtb {
@@ -120,6 +123,10 @@ struct GramLayout {
   int* dmode;     // [N][s] mode indices
   double* rhs_part;  // [kRhsSplit][d]
   double* drow;   // [s][rowlen] concatenated factor rows of modes >= 2, bucket order
+  double* vt2;    // [I2][144] vech Khatri-Rao table of A_2 (3-way, R <= 16)
+  double* vt3;    // [I3][144]
+  int* border;    // [I1] compacted buckets, longest first (k_bucket_order)
+  int* bcounter;  // [1] next bucket of the persistent k_vech_bucket3
 };
 
 int key_bits(int I1) {
@@ -163,6 +170,10 @@ size_t carve(const GramSpec& spec, F&& take) {
   t(spec.s * 4 * (size_t)spec.order);          // dmode[n][k]
   t((size_t)kRhsSplit * spec.d * 8);           // rhs partials
   t(spec.s * (size_t)v.rowlen * 8);            // drow: factor rows (modes >= 2) per draw
+  t((size_t)(spec.order >= 2 ? spec.rows[1] : 1) * 144 * 8);  // vt2
+  t((size_t)(spec.order >= 3 ? spec.rows[2] : 1) * 144 * 8);  // vt3
+  t((size_t)I1 * 4);                           // border
+  t(16);                                       // bcounter
   return total;
 }
 
@@ -192,6 +203,10 @@ GramLayout layout(const GramSpec& spec, void* base) {
       case 16: l.dmode = (int*)q; break;
       case 17: l.rhs_part = (double*)q; break;
       case 18: l.drow = (double*)q; break;
+      case 19: l.vt2 = (double*)q; break;
+      case 20: l.vt3 = (double*)q; break;
+      case 21: l.border = (int*)q; break;
+      case 22: l.bcounter = (int*)q; break;
     }
   });
   return l;
@@ -779,6 +794,236 @@ size_t vech_bucket2_smem(const VechSpec& v) {
   return (size_t)(4 * KCB * LDZ + 3 * KCB * rlp + 6 * KCB) * 8 + 16;
 }
 
+// Buckets ranked longest first (ties by index): the persistent bucket kernel takes them in
+// this order (longest-processing-time-first list scheduling over the SMs).
+__global__ void __launch_bounds__(1024) k_bucket_order(const int* __restrict__ blen,
+                                                       const int* __restrict__ nbuckets,
+                                                       int* __restrict__ order, int* counter) {
+  const int nb = *nbuckets;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const int lb = blen[b];
+    int rank = 0;
+    for (int j = 0; j < nb; ++j) {
+      const int lj = blen[j];
+      rank += (lj > lb) || (lj == lb && j < b);
+    }
+    order[rank] = b;
+  }
+  if (threadIdx.x == 0) *counter = 0;
+}
+
+// vech Khatri-Rao tables of the modes 2 and 3 (one per core update, L2-resident):
+// vt[i][u] = A[i, p] A[i, q] for the vech pair u = (p <= q), zero-padded to ld columns.
+__global__ void k_vech_table(const double* __restrict__ A, int I, int R, int ld,
+                             double* __restrict__ vt) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)I * ld) return;
+  const long long i = e / ld;
+  const int u = (int)(e - i * ld);
+  double v = 0.0;
+  if (u < R * (R + 1) / 2) {
+    int pa, pb;
+    pair_of(u, R, pa, pb);
+    v = A[i * R + pa] * A[i * R + pb];
+  }
+  vt[e] = v;
+}
+
+// (B'') 3-way H_b (+ h_b), persistent, two CTAs per SM. A work item is one half of a
+// bucket's H_b (vech rows [72 h, 72 h + 72), all 144 padded columns); items are taken longest
+// bucket first from an atomic counter (no partial last wave). The operands are NOT generated
+// per draw: H_b = sum_t w_t^2 V2[i2_t]^T V3[i3_t] with V2, V3 the vech Khatri-Rao tables of
+// A_2, A_3 (k_vech_table, L2-resident), so a chunk of 16 draws is a cp.async gather of table
+// rows into a 3-stage ring (plus the raw factor rows for h_b) and the DMMA loop reads them
+// directly, w^2 folded into the A fragment. 9 warps own 3 x 6 DMMA tiles each (0.5 fragment
+// loads per DMMA); on the half-0 items warps 0-3 also accumulate one 8 x 8 tile each of
+// h_b[p2][p3] = sum w^2 x a_2[p2] a_3[p3]. The K loop stops at the chunk's last draw
+// (rounded to 4). A half's result does not depend on which CTA computes it.
+#ifndef RTB_B5_WHOLE
+#define RTB_B5_WHOLE 1
+#endif
+#if RTB_B5_WHOLE
+// whole bucket per item: 18 warps, one CTA per SM, 32-draw stages, double buffered
+constexpr int kB5Mma = 18;
+constexpr int kB5K = 32;
+constexpr int kB5St = 2;
+constexpr int kB5Rows = 144;
+constexpr int kB5Halves = 1;
+constexpr int kB5CtaPerSm = 1;
+#else
+// half a bucket per item: 9 warps, two CTAs per SM, 16-draw stages, three deep
+constexpr int kB5Mma = 9;
+constexpr int kB5K = 16;
+constexpr int kB5St = 3;
+constexpr int kB5Rows = 72;
+constexpr int kB5Halves = 2;
+constexpr int kB5CtaPerSm = 2;
+#endif
+constexpr int kB5Threads = kB5Mma * 32;
+constexpr int kB5LdR = kB5Rows + 4;      // conflict-free fragment loads
+constexpr int kB5LdC = 144 + 4;
+constexpr int kB5Tab = 144;              // table row length (136 padded to 18 tiles)
+constexpr int kB5LdF = 16 + 4;           // raw factor rows (R <= 16) for h_b
+__global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
+    GramSpec spec, VechSpec v, const double* __restrict__ V2, const double* __restrict__ V3,
+    const int* __restrict__ dmode, const double* __restrict__ dw2,
+    const double* __restrict__ dwx, const int* __restrict__ bstart,
+    const int* __restrict__ blen, const int* __restrict__ nbuckets,
+    const int* __restrict__ order, int* counter, double* __restrict__ H, double* __restrict__ h) {
+  extern __shared__ __align__(16) double smb[];
+  double* zr = smb;                                  // [St][K][LdR]
+  double* zc = zr + kB5St * kB5K * kB5LdR;           // [St][K][LdC]
+  double* f2 = zc + kB5St * kB5K * kB5LdC;           // [St][K][LdF]  a_2 rows
+  double* f3 = f2 + kB5St * kB5K * kB5LdF;           // [St][K][LdF]  a_3 rows
+  double* w2s = f3 + kB5St * kB5K * kB5LdF;          // [St][K]
+  double* wxs = w2s + kB5St * kB5K;                  // [St][K]
+  __shared__ int s_item;
+  __shared__ __align__(8) unsigned long long full[kB5St];  // table rows landed (TMA bytes)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int rg = warp / 3, cg = warp % 3;
+  const int R2 = v.R[1], R3 = v.R[2];
+  const double* A2 = spec.factors[1];
+  const double* A3 = spec.factors[2];
+  const int nb = *nbuckets;
+  const long long S = (long long)spec.s;
+  // raw factor rows by bulk copy when they are whole 16-byte pieces
+  const bool fbulk = (R2 % 2 == 0) && (R3 % 2 == 0);
+  if (tid == 0) {
+    for (int i = 0; i < kB5St; ++i) mbar_init(&full[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  unsigned uses[kB5St];  // completed phases of each stage's barrier (same in every thread)
+#pragma unroll
+  for (int i = 0; i < kB5St; ++i) uses[i] = 0;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= kB5Halves * nb) break;
+    const int b = order[item / kB5Halves], half = item % kB5Halves;
+    const int start = bstart[b], len = blen[b];
+    const int nch = (len + kB5K - 1) / kB5K;
+    const bool hrows = half == 0;
+    // warp 0 stages chunk ch: lane k handles draw k (w^2, w^2 x, zero rows past the last
+    // draw of the k-step), then lane 0 arms the stage barrier with the byte count and every
+    // lane issues its draw's bulk copies (table rows; raw factor rows for h_b)
+    auto load = [&](int ch) {
+      if (ch >= nch || warp != 0) return;
+      const int sb = ch % kB5St, k0 = ch * kB5K, kn = min(kB5K, len - k0);
+      const int k = lane;
+      const bool ok = k < kn;
+      double* zrk = zr + (sb * kB5K + k) * kB5LdR;
+      double* zck = zc + (sb * kB5K + k) * kB5LdC;
+      double* f2k = f2 + (sb * kB5K + k) * kB5LdF;
+      double* f3k = f3 + (sb * kB5K + k) * kB5LdF;
+      int i2 = 0, i3 = 0;
+      if (ok) {
+        const long long dk = start + k0 + k;
+        i2 = dmode[S + dk];
+        i3 = dmode[2 * S + dk];
+        w2s[sb * kB5K + k] = dw2[dk];
+        wxs[sb * kB5K + k] = dwx[dk];
+        if (hrows && !fbulk) {
+          for (int q = 0; q < R2; ++q) f2k[q] = A2[(long long)i2 * R2 + q];
+          for (int q = 0; q < R3; ++q) f3k[q] = A3[(long long)i3 * R3 + q];
+        }
+      } else if (k < ((kn + 3) & ~3)) {  // padding draws of the last k-step: zero operands
+        w2s[sb * kB5K + k] = 0.0;
+        wxs[sb * kB5K + k] = 0.0;
+        for (int q = 0; q < kB5Rows; ++q) zrk[q] = 0.0;
+        for (int q = 0; q < 144; ++q) zck[q] = 0.0;
+        for (int q = 0; q < 16; ++q) f2k[q] = f3k[q] = 0.0;
+      }
+      const unsigned row_bytes = (kB5Rows + 144) * 8 +
+                                 (hrows && fbulk ? (unsigned)(R2 + R3) * 8 : 0u);
+      fence_proxy_async();  // the generic zero rows above before the async writes of later uses
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&full[sb], row_bytes * (unsigned)kn);
+      __syncwarp();
+      if (ok) {
+        bulk_g2s(zrk, V2 + (long long)i2 * kB5Tab + half * kB5Rows, kB5Rows * 8, &full[sb]);
+        bulk_g2s(zck, V3 + (long long)i3 * kB5Tab, 144 * 8, &full[sb]);
+        if (hrows && fbulk) {
+          bulk_g2s(f2k, A2 + (long long)i2 * R2, R2 * 8, &full[sb]);
+          bulk_g2s(f3k, A3 + (long long)i3 * R3, R3 * 8, &full[sb]);
+        }
+      }
+    };
+    double acc[3][6][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    double hc0 = 0.0, hc1 = 0.0;
+    const bool hw = hrows && warp < 4;  // h_b tile (warp >> 1, warp & 1)
+    const int hi = warp >> 1, hj = warp & 1;
+#pragma unroll
+    for (int ch = 0; ch < kB5St - 1; ++ch) load(ch);
+    for (int ch = 0; ch < nch; ++ch) {
+      load(ch + kB5St - 1);
+      const int sb = ch % kB5St;
+      mbar_wait(&full[sb], uses[sb] & 1);  // chunk ch's rows (and warp 0's scalars) landed
+      ++uses[sb];
+      const int ksn = (min(kB5K, len - ch * kB5K) + 3) >> 2;
+      {
+        const double* zrb = zr + sb * kB5K * kB5LdR + rg * 24 + g;
+        const double* zcb = zc + sb * kB5K * kB5LdC + cg * 48 + g;
+        const double* w2c = w2s + sb * kB5K;
+        for (int ks = 0; ks < ksn; ++ks) {
+          const int k = ks * 4 + t4;
+          const double wk = w2c[k];
+          double av[3], bv[6];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) av[i] = wk * zrb[k * kB5LdR + i * 8];
+#pragma unroll
+          for (int j = 0; j < 6; ++j) bv[j] = zcb[k * kB5LdC + j * 8];
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 6; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+        }
+      }
+      if (hw) {
+        const double* f2c = f2 + sb * kB5K * kB5LdF + hi * 8 + g;
+        const double* f3c = f3 + sb * kB5K * kB5LdF + hj * 8 + g;
+        const double* wxc = wxs + sb * kB5K;
+        for (int ks = 0; ks < ksn; ++ks) {
+          const int k = ks * 4 + t4;
+          const double a = (hi * 8 + g < R2) ? wxc[k] * f2c[k * kB5LdF] : 0.0;
+          const double bb = (hj * 8 + g < R3) ? f3c[k * kB5LdF] : 0.0;
+          dmma_8x8x4(hc0, hc1, a, bb);
+        }
+      }
+      __syncthreads();  // stage sb free for chunk ch + St
+    }
+    {
+      double* Hb = H + (size_t)b * v.Hsz;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const long long row = (long long)half * kB5Rows + rg * 24 + i * 8 + g;
+        if (row >= v.Mrow) continue;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          const long long cc = (long long)cg * 48 + j * 8 + 2 * t4;
+          if (cc < v.Ncol) Hb[row * v.Ncol + cc] = acc[i][j][0];
+          if (cc + 1 < v.Ncol) Hb[row * v.Ncol + cc + 1] = acc[i][j][1];
+        }
+      }
+    }
+    if (hw) {
+      const int p2 = hi * 8 + g, p3 = hj * 8 + 2 * t4;
+      if (p2 < R2 && p3 < R3) h[(size_t)b * spec.dprime + p2 * R3 + p3] = hc0;
+      if (p2 < R2 && p3 + 1 < R3) h[(size_t)b * spec.dprime + p2 * R3 + p3 + 1] = hc1;
+    }
+  }
+}
+
+size_t vech_bucket5_smem() {
+  return (size_t)kB5St * kB5K * (kB5LdR + kB5LdC + 2 * kB5LdF + 2) * 8 + 16;
+}
+
 // h_b[p'] = sum_{t in b} w_t^2 x_t prod_{n>=1} a_n(i_n)[p_n] from the draw records.
 __global__ void __launch_bounds__(256) k_bucket_h2(GramSpec spec, const double* __restrict__ dwx,
                                                    const int* __restrict__ dmode,
@@ -1163,10 +1408,14 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
   // h_b by the bucket kernel's spare warp in the 3-way case (R_2, R_3 <= 16)
   const bool fused_h = whole && nr == 1 && nc == 1 && v.R[1] <= 16 && v.R[2] <= 16 &&
                        (v.Mrow + 7) / 8 < kBWarps;
+  static const bool b5_off_g = std::getenv("RTB_NO_BUCKET5") != nullptr;
+  const bool b5 = fused_h && !b5_off_g && v.N == 3 && v.R[1] <= 16 && v.R[2] <= 16;
   if (whole) {
-    k_gather_rows<<<(unsigned)ceil_div<unsigned long long>(spec.s * v.rowlen, 256ULL), 256, 0,
-                    st>>>(spec, v, l.keys_sorted, l.dmode, l.drow);
-    RTB_LAUNCH_CHECK();
+    if (!b5) {
+      k_gather_rows<<<(unsigned)ceil_div<unsigned long long>(spec.s * v.rowlen, 256ULL), 256, 0,
+                      st>>>(spec, v, l.keys_sorted, l.dmode, l.drow);
+      RTB_LAUNCH_CHECK();
+    }
     const size_t smb = vech_bucket2_smem(v);
     const int smax = 227 * 1024;
     auto launch = [&](auto kern) {
@@ -1196,8 +1445,34 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
       else if (nr == 1 && nc == 2) by_nt(hpt, I1c{}, I2c{});
       else by_nt(hpt, I2c{}, I1c{});
     };
-    if (fused_h) by_nt(I1c{}, I1c{}, I1c{});
-    else by_groups(I0{});
+    static const bool b5_off = std::getenv("RTB_NO_BUCKET5") != nullptr;
+    if (fused_h && !b5_off && v.N == 3 && v.R[1] <= 16 && v.R[2] <= 16) {
+      // vech tables of A_2, A_3, then the persistent table-gather bucket kernel
+      k_vech_table<<<(unsigned)ceil_div<long long>((long long)spec.rows[1] * kB5Tab, 256), 256, 0,
+                     st>>>(spec.factors[1], spec.rows[1], v.R[1], kB5Tab, l.vt2);
+      RTB_LAUNCH_CHECK();
+      k_vech_table<<<(unsigned)ceil_div<long long>((long long)spec.rows[2] * kB5Tab, 256), 256, 0,
+                     st>>>(spec.factors[2], spec.rows[2], v.R[2], kB5Tab, l.vt3);
+      RTB_LAUNCH_CHECK();
+      k_bucket_order<<<1, 1024, 0, st>>>(l.blen, l.nbuckets, l.border, l.bcounter);
+      RTB_LAUNCH_CHECK();
+      const size_t smb5 = vech_bucket5_smem();
+      set_max_smem(k_vech_bucket5, (int)smb5);
+      int dev = 0, sms = 0;
+      RTB_CUDA(cudaGetDevice(&dev));
+      RTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      static const int b5_grid = std::getenv("RTB_B5_GRID") ? std::atoi(std::getenv("RTB_B5_GRID")) : 0;
+      k_vech_bucket5<<<b5_grid > 0 ? b5_grid : std::min(kB5Halves * I1, kB5CtaPerSm * sms),
+                       kB5Threads, smb5, st>>>(
+          spec, v, l.vt2, l.vt3, l.dmode, l.dw2, l.dwx, l.bstart, l.blen, l.nbuckets, l.border,
+          l.bcounter, l.H, l.h);
+      RTB_LAUNCH_CHECK();
+      count_variant("k_vech_bucket5");
+    } else if (fused_h) {
+      by_nt(I1c{}, I1c{}, I1c{});
+    } else {
+      by_groups(I0{});
+    }
   } else {
     const long long tiles_r = (v.Mrow + TB - 1) / TB, tiles_c = (v.Ncol + TB - 1) / TB;
     k_vech_bucket<<<dim3((unsigned)(tiles_r * tiles_c), I1), kTh,
@@ -1304,6 +1579,21 @@ void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
   }
   GramLayout l = layout(spec, work);
   bucket_stage(spec, v, l, x, idx, w, data_draws_dev, st);
+  if (const char* dump = std::getenv("RTB_DUMP_H")) {  // debugging aid: H and bucket table
+    std::vector<double> hh((size_t)spec.rows[0] * v.Hsz);
+    std::vector<int> meta(3 * (size_t)spec.rows[0] + 1);
+    RTB_CUDA(cudaMemcpyAsync(hh.data(), l.H, hh.size() * 8, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaMemcpyAsync(meta.data(), l.bi1, (size_t)spec.rows[0] * 4, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaMemcpyAsync(meta.data() + spec.rows[0], l.blen, (size_t)spec.rows[0] * 4, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaMemcpyAsync(meta.data() + 3 * (size_t)spec.rows[0], l.nbuckets, 4, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaStreamSynchronize(st));
+    FILE* f = std::fopen(dump, "wb");
+    if (f) {
+      std::fwrite(hh.data(), 8, hh.size(), f);
+      std::fwrite(meta.data(), 4, meta.size(), f);
+      std::fclose(f);
+    }
+  }
   const int I1 = spec.rows[0];
   if ((v.m[0] + 7) / 8 <= kBWarps) {
     const size_t smc = (size_t)(2 * KCC * LDH2 + 2 * KCC * LDZ) * 8;

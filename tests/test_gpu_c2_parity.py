@@ -8,7 +8,7 @@ torch cuBLAS) where it does not (the reference's Jacobi SVD at d = 4096 takes ho
   * exact factor updates at R = 16 through k_ttm_mid3 (the F_3 projection) and
     k_ttm_last3 (T = X x_3 A_3^T), all modes, vs orc_update_factor   (ref tucker.cpp:70-89)
   * the fused loss pass (k_ttm_last3<FUSED>) vs orc_tucker_loss       (ref tucker.cpp:216-229)
-  * rung 3 at d = 4096: the sketched Gram/RHS built by k_vech_bucket2<17> +
+  * rung 3 at d = 4096: the sketched Gram/RHS built by k_vech_bucket5 +
     k_vech_contract2 from the oracle's own draws vs orc_kron_sketch_normal_eq
                                                                       (ref sketch_ridge.cpp:105-128)
   * the PCG fast path k_pcg<16,16> (the C2 core solve) vs a LAPACK solve of the same
@@ -121,16 +121,16 @@ def _oracle_draws(oracle, shape, ranks, factors, seed, s):
 
 
 def test_normal_equations_d4096_from_oracle_sketch(oracle, rt, x_c2):
-    """Rung 3 at C2: d = 4096, R = 16 (k_vech_bucket2<17>, k_vech_contract2, k_vech_blocks),
+    """Rung 3 at C2: d = 4096, R = 16 (k_vech_bucket5, k_vech_contract2, k_vech_blocks),
     the draws made by the oracle's sampler, the Gram/RHS by the oracle's restatement of
     the reference's row-by-row stream."""
     shape, ranks, lam, s = x_c2.shape, (16, 16, 16), 1e-2, 4000
     core, factors = model(oracle, shape, ranks, "uniform", 9)
     idx, w = _oracle_draws(oracle, shape, ranks, factors, 2024, s)
-    b17 = rt.variant_count("k_vech_bucket2<17>")
+    b17 = rt.variant_count("k_vech_bucket5")
     c2 = rt.variant_count("k_vech_contract2")
     gg, grhs = rt.kron_normal_eq(shape, ranks, factors, x_c2, lam, idx, w)
-    assert rt.variant_count("k_vech_bucket2<17>") == b17 + 1
+    assert rt.variant_count("k_vech_bucket5") == b17 + 1
     assert rt.variant_count("k_vech_contract2") == c2 + 1
     og, orhs = oracle.kron_normal_eq(shape, ranks, factors, x_c2, lam, idx, w)
     dg = np.sqrt(np.outer(np.diag(og), np.diag(og)))

@@ -839,27 +839,20 @@ __global__ void k_vech_table(const double* __restrict__ A, int I, int R, int ld,
 // loads per DMMA); on the half-0 items warps 0-3 also accumulate one 8 x 8 tile each of
 // h_b[p2][p3] = sum w^2 x a_2[p2] a_3[p3]. The K loop stops at the chunk's last draw
 // (rounded to 4). A half's result does not depend on which CTA computes it.
-#ifndef RTB_B5_WHOLE
-#define RTB_B5_WHOLE 1
-#endif
-#if RTB_B5_WHOLE
-// whole bucket per item: 18 warps, one CTA per SM, 32-draw stages, double buffered
-constexpr int kB5Mma = 18;
-constexpr int kB5K = 32;
-constexpr int kB5St = 2;
-constexpr int kB5Rows = 144;
+// Warp-specialised: one producer warp runs ahead through this CTA's items (fetched from the
+// atomic counter) and chunks, staging each chunk of kB5K draws into a kB5St-deep ring -- the
+// draw scalars and zero padding by plain stores, the table rows (and raw factor rows for
+// h_b) by TMA bulk copies completing on the stage's `full` mbarrier, the chunk's
+// (bucket, position) in a metadata slot -- and 18 consumer warps (3 x 6 DMMA tiles each)
+// wait on `full`, accumulate, write H_b after a bucket's last chunk and release the stage on
+// its `empty` mbarrier. No CTA-wide barrier in the steady state.
+constexpr int kB5Mma = 18;               // consumer warps
+constexpr int kB5K = 24;                 // draws per stage
+constexpr int kB5St = 3;                 // ring stages
+constexpr int kB5Rows = 144;             // whole bucket per item
 constexpr int kB5Halves = 1;
 constexpr int kB5CtaPerSm = 1;
-#else
-// half a bucket per item: 9 warps, two CTAs per SM, 16-draw stages, three deep
-constexpr int kB5Mma = 9;
-constexpr int kB5K = 16;
-constexpr int kB5St = 3;
-constexpr int kB5Rows = 72;
-constexpr int kB5Halves = 2;
-constexpr int kB5CtaPerSm = 2;
-#endif
-constexpr int kB5Threads = kB5Mma * 32;
+constexpr int kB5Threads = (kB5Mma + 1) * 32;
 constexpr int kB5LdR = kB5Rows + 4;      // conflict-free fragment loads
 constexpr int kB5LdC = 144 + 4;
 constexpr int kB5Tab = 144;              // table row length (136 padded to 18 tiles)
@@ -877,128 +870,154 @@ __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
   double* f3 = f2 + kB5St * kB5K * kB5LdF;           // [St][K][LdF]  a_3 rows
   double* w2s = f3 + kB5St * kB5K * kB5LdF;          // [St][K]
   double* wxs = w2s + kB5St * kB5K;                  // [St][K]
-  __shared__ int s_item;
-  __shared__ __align__(8) unsigned long long full[kB5St];  // table rows landed (TMA bytes)
+  __shared__ __align__(8) unsigned long long full[kB5St], empty[kB5St];
+  __shared__ int meta[kB5St][4];  // bucket (-1: no more work), half, draws in chunk, last chunk
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int rg = warp / 3, cg = warp % 3;
   const int R2 = v.R[1], R3 = v.R[2];
-  const double* A2 = spec.factors[1];
-  const double* A3 = spec.factors[2];
-  const int nb = *nbuckets;
-  const long long S = (long long)spec.s;
-  // raw factor rows by bulk copy when they are whole 16-byte pieces
   const bool fbulk = (R2 % 2 == 0) && (R3 % 2 == 0);
   if (tid == 0) {
-    for (int i = 0; i < kB5St; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < kB5St; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kB5Mma);
+    }
     mbar_fence_init();
   }
   __syncthreads();
-  unsigned uses[kB5St];  // completed phases of each stage's barrier (same in every thread)
-#pragma unroll
-  for (int i = 0; i < kB5St; ++i) uses[i] = 0;
-  for (;;) {
-    if (tid == 0) s_item = atomicAdd(counter, 1);
-    __syncthreads();
-    const int item = s_item;
-    if (item >= kB5Halves * nb) break;
-    const int b = order[item / kB5Halves], half = item % kB5Halves;
-    const int start = bstart[b], len = blen[b];
-    const int nch = (len + kB5K - 1) / kB5K;
-    const bool hrows = half == 0;
-    // warp 0 stages chunk ch: lane k handles draw k (w^2, w^2 x, zero rows past the last
-    // draw of the k-step), then lane 0 arms the stage barrier with the byte count and every
-    // lane issues its draw's bulk copies (table rows; raw factor rows for h_b)
-    auto load = [&](int ch) {
-      if (ch >= nch || warp != 0) return;
-      const int sb = ch % kB5St, k0 = ch * kB5K, kn = min(kB5K, len - k0);
-      const int k = lane;
-      const bool ok = k < kn;
-      double* zrk = zr + (sb * kB5K + k) * kB5LdR;
-      double* zck = zc + (sb * kB5K + k) * kB5LdC;
-      double* f2k = f2 + (sb * kB5K + k) * kB5LdF;
-      double* f3k = f3 + (sb * kB5K + k) * kB5LdF;
-      int i2 = 0, i3 = 0;
-      if (ok) {
-        const long long dk = start + k0 + k;
-        i2 = dmode[S + dk];
-        i3 = dmode[2 * S + dk];
-        w2s[sb * kB5K + k] = dw2[dk];
-        wxs[sb * kB5K + k] = dwx[dk];
-        if (hrows && !fbulk) {
-          for (int q = 0; q < R2; ++q) f2k[q] = A2[(long long)i2 * R2 + q];
-          for (int q = 0; q < R3; ++q) f3k[q] = A3[(long long)i3 * R3 + q];
-        }
-      } else if (k < ((kn + 3) & ~3)) {  // padding draws of the last k-step: zero operands
-        w2s[sb * kB5K + k] = 0.0;
-        wxs[sb * kB5K + k] = 0.0;
-        for (int q = 0; q < kB5Rows; ++q) zrk[q] = 0.0;
-        for (int q = 0; q < 144; ++q) zck[q] = 0.0;
-        for (int q = 0; q < 16; ++q) f2k[q] = f3k[q] = 0.0;
-      }
-      const unsigned row_bytes = (kB5Rows + 144) * 8 +
-                                 (hrows && fbulk ? (unsigned)(R2 + R3) * 8 : 0u);
-      fence_proxy_async();  // the generic zero rows above before the async writes of later uses
-      __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(&full[sb], row_bytes * (unsigned)kn);
-      __syncwarp();
-      if (ok) {
-        bulk_g2s(zrk, V2 + (long long)i2 * kB5Tab + half * kB5Rows, kB5Rows * 8, &full[sb]);
-        bulk_g2s(zck, V3 + (long long)i3 * kB5Tab, 144 * 8, &full[sb]);
-        if (hrows && fbulk) {
-          bulk_g2s(f2k, A2 + (long long)i2 * R2, R2 * 8, &full[sb]);
-          bulk_g2s(f3k, A3 + (long long)i3 * R3, R3 * 8, &full[sb]);
-        }
-      }
+  if (warp == kB5Mma) {
+    // ---------------- producer ----------------
+    const double* A2 = spec.factors[1];
+    const double* A3 = spec.factors[2];
+    const int nb = *nbuckets;
+    const long long S = (long long)spec.s;
+    unsigned q = 0;  // chunks staged so far
+    auto next_stage = [&]() {
+      const int sb = (int)(q % kB5St);
+      if (q >= kB5St) mbar_wait(&empty[sb], ((q / kB5St) - 1) & 1);
+      return sb;
     };
-    double acc[3][6][2];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 6; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    double hc0 = 0.0, hc1 = 0.0;
-    const bool hw = hrows && warp < 4;  // h_b tile (warp >> 1, warp & 1)
-    const int hi = warp >> 1, hj = warp & 1;
-#pragma unroll
-    for (int ch = 0; ch < kB5St - 1; ++ch) load(ch);
-    for (int ch = 0; ch < nch; ++ch) {
-      load(ch + kB5St - 1);
-      const int sb = ch % kB5St;
-      mbar_wait(&full[sb], uses[sb] & 1);  // chunk ch's rows (and warp 0's scalars) landed
-      ++uses[sb];
-      const int ksn = (min(kB5K, len - ch * kB5K) + 3) >> 2;
-      {
-        const double* zrb = zr + sb * kB5K * kB5LdR + rg * 24 + g;
-        const double* zcb = zc + sb * kB5K * kB5LdC + cg * 48 + g;
-        const double* w2c = w2s + sb * kB5K;
-        for (int ks = 0; ks < ksn; ++ks) {
-          const int k = ks * 4 + t4;
-          const double wk = w2c[k];
-          double av[3], bv[6];
-#pragma unroll
-          for (int i = 0; i < 3; ++i) av[i] = wk * zrb[k * kB5LdR + i * 8];
-#pragma unroll
-          for (int j = 0; j < 6; ++j) bv[j] = zcb[k * kB5LdC + j * 8];
-#pragma unroll
-          for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int j = 0; j < 6; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+    for (;;) {
+      int item = 0;
+      if (lane == 0) item = atomicAdd(counter, 1);
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= kB5Halves * nb) break;
+      const int b = order[item / kB5Halves], half = item % kB5Halves;
+      const bool hrows = half == 0;
+      const int start = bstart[b], len = blen[b];
+      const int nch = (len + kB5K - 1) / kB5K;
+      for (int ch = 0; ch < nch; ++ch, ++q) {
+        const int sb = next_stage();
+        const int k0 = ch * kB5K, kn = min(kB5K, len - k0);
+        double* zrs = zr + sb * kB5K * kB5LdR;
+        double* zcs = zc + sb * kB5K * kB5LdC;
+        double* f2s = f2 + sb * kB5K * kB5LdF;
+        double* f3s = f3 + sb * kB5K * kB5LdF;
+        int i2 = 0, i3 = 0;
+        const bool ok = lane < kn;
+        if (lane < kB5K) {
+          if (ok) {
+            const long long dk = start + k0 + lane;
+            i2 = dmode[S + dk];
+            i3 = dmode[2 * S + dk];
+            w2s[sb * kB5K + lane] = dw2[dk];
+            wxs[sb * kB5K + lane] = dwx[dk];
+            if (hrows && !fbulk) {
+              for (int c = 0; c < R2; ++c) f2s[lane * kB5LdF + c] = A2[(long long)i2 * R2 + c];
+              for (int c = 0; c < R3; ++c) f3s[lane * kB5LdF + c] = A3[(long long)i3 * R3 + c];
+            }
+          } else if (lane < ((kn + 3) & ~3)) {  // padding draws of the last k-step
+            w2s[sb * kB5K + lane] = 0.0;
+            wxs[sb * kB5K + lane] = 0.0;
+            for (int c = 0; c < kB5Rows; ++c) zrs[lane * kB5LdR + c] = 0.0;
+            for (int c = 0; c < 144; ++c) zcs[lane * kB5LdC + c] = 0.0;
+            for (int c = 0; c < 16; ++c) f2s[lane * kB5LdF + c] = f3s[lane * kB5LdF + c] = 0.0;
+          }
+        }
+        if (lane == 0) {
+          meta[sb][0] = b;
+          meta[sb][1] = half;
+          meta[sb][2] = kn;
+          meta[sb][3] = ch == nch - 1;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        const unsigned row_bytes = (kB5Rows + 144) * 8 +
+                                   (hrows && fbulk ? (unsigned)(R2 + R3) * 8 : 0u);
+        if (lane == 0) mbar_arrive_expect_tx(&full[sb], row_bytes * (unsigned)kn);
+        __syncwarp();
+        if (ok) {
+          bulk_g2s(zrs + lane * kB5LdR, V2 + (long long)i2 * kB5Tab + half * kB5Rows,
+                   kB5Rows * 8, &full[sb]);
+          bulk_g2s(zcs + lane * kB5LdC, V3 + (long long)i3 * kB5Tab, 144 * 8, &full[sb]);
+          if (hrows && fbulk) {
+            bulk_g2s(f2s + lane * kB5LdF, A2 + (long long)i2 * R2, R2 * 8, &full[sb]);
+            bulk_g2s(f3s + lane * kB5LdF, A3 + (long long)i3 * R3, R3 * 8, &full[sb]);
+          }
         }
       }
-      if (hw) {
-        const double* f2c = f2 + sb * kB5K * kB5LdF + hi * 8 + g;
-        const double* f3c = f3 + sb * kB5K * kB5LdF + hj * 8 + g;
-        const double* wxc = wxs + sb * kB5K;
-        for (int ks = 0; ks < ksn; ++ks) {
-          const int k = ks * 4 + t4;
-          const double a = (hi * 8 + g < R2) ? wxc[k] * f2c[k * kB5LdF] : 0.0;
-          const double bb = (hj * 8 + g < R3) ? f3c[k * kB5LdF] : 0.0;
-          dmma_8x8x4(hc0, hc1, a, bb);
-        }
-      }
-      __syncthreads();  // stage sb free for chunk ch + St
     }
+    // end of work: one sentinel stage
+    const int sb = next_stage();
+    if (lane == 0) {
+      meta[sb][0] = -1;
+      mbar_arrive(&full[sb]);
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int g = lane >> 2, t4 = lane & 3;
+  const int rg = warp / 3, cg = warp % 3;
+  const int hi = warp >> 1, hj = warp & 1;
+  double acc[3][6][2];
+  double hc0 = 0.0, hc1 = 0.0;
+  bool fresh = true;
+  for (unsigned q = 0;; ++q) {
+    const int sb = (int)(q % kB5St);
+    mbar_wait(&full[sb], (q / kB5St) & 1);
+    const int b = meta[sb][0];
+    if (b < 0) break;
+    const int half = meta[sb][1], kn = meta[sb][2], last = meta[sb][3];
+    if (fresh) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      hc0 = hc1 = 0.0;
+      fresh = false;
+    }
+    const bool hw = half == 0 && warp < 4;
+    const int ksn = (kn + 3) >> 2;
     {
+      const double* zrb = zr + sb * kB5K * kB5LdR + rg * 24 + g;
+      const double* zcb = zc + sb * kB5K * kB5LdC + cg * 48 + g;
+      const double* w2c = w2s + sb * kB5K;
+      for (int ks = 0; ks < ksn; ++ks) {
+        const int k = ks * 4 + t4;
+        const double wk = w2c[k];
+        double av[3], bv[6];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) av[i] = wk * zrb[k * kB5LdR + i * 8];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) bv[j] = zcb[k * kB5LdC + j * 8];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 6; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+      }
+    }
+    if (hw) {
+      const double* f2c = f2 + sb * kB5K * kB5LdF + hi * 8 + g;
+      const double* f3c = f3 + sb * kB5K * kB5LdF + hj * 8 + g;
+      const double* wxc = wxs + sb * kB5K;
+      for (int ks = 0; ks < ksn; ++ks) {
+        const int k = ks * 4 + t4;
+        const double a = (hi * 8 + g < R2) ? wxc[k] * f2c[k * kB5LdF] : 0.0;
+        const double bb = (hj * 8 + g < R3) ? f3c[k * kB5LdF] : 0.0;
+        dmma_8x8x4(hc0, hc1, a, bb);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sb]);  // this warp is done with the stage
+    if (last) {
       double* Hb = H + (size_t)b * v.Hsz;
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
@@ -1011,11 +1030,12 @@ __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
           if (cc + 1 < v.Ncol) Hb[row * v.Ncol + cc + 1] = acc[i][j][1];
         }
       }
-    }
-    if (hw) {
-      const int p2 = hi * 8 + g, p3 = hj * 8 + 2 * t4;
-      if (p2 < R2 && p3 < R3) h[(size_t)b * spec.dprime + p2 * R3 + p3] = hc0;
-      if (p2 < R2 && p3 + 1 < R3) h[(size_t)b * spec.dprime + p2 * R3 + p3 + 1] = hc1;
+      if (hw) {
+        const int p2 = hi * 8 + g, p3 = hj * 8 + 2 * t4;
+        if (p2 < R2 && p3 < R3) h[(size_t)b * spec.dprime + p2 * R3 + p3] = hc0;
+        if (p2 < R2 && p3 + 1 < R3) h[(size_t)b * spec.dprime + p2 * R3 + p3 + 1] = hc1;
+      }
+      fresh = true;
     }
   }
 }

@@ -123,8 +123,8 @@ struct GramLayout {
   int* dmode;     // [N][s] mode indices
   double* rhs_part;  // [kRhsSplit][d]
   double* drow;   // [s][rowlen] concatenated factor rows of modes >= 2, bucket order
-  double* vt2;    // [I2][144] vech Khatri-Rao table of A_2 (3-way, R <= 16)
-  double* vt3;    // [I3][144]
+  double* vt2;    // [I2][160] vech Khatri-Rao table of A_2 + raw rows (3-way, R <= 16)
+  double* vt3;    // [I3][160]
   int* border;    // [I1] compacted buckets, longest first (k_bucket_order)
   int* bcounter;  // [1] next bucket of the persistent k_vech_bucket3
 };
@@ -170,8 +170,8 @@ size_t carve(const GramSpec& spec, F&& take) {
   t(spec.s * 4 * (size_t)spec.order);          // dmode[n][k]
   t((size_t)kRhsSplit * spec.d * 8);           // rhs partials
   t(spec.s * (size_t)v.rowlen * 8);            // drow: factor rows (modes >= 2) per draw
-  t((size_t)(spec.order >= 2 ? spec.rows[1] : 1) * 144 * 8);  // vt2
-  t((size_t)(spec.order >= 3 ? spec.rows[2] : 1) * 144 * 8);  // vt3
+  t((size_t)(spec.order >= 2 ? spec.rows[1] : 1) * 160 * 8);  // vt2 (k_vech_table, ld 160)
+  t((size_t)(spec.order >= 3 ? spec.rows[2] : 1) * 160 * 8);  // vt3
   t((size_t)I1 * 4);                           // border
   t(16);                                       // bcounter
   return total;
@@ -813,7 +813,8 @@ __global__ void __launch_bounds__(1024) k_bucket_order(const int* __restrict__ b
 }
 
 // vech Khatri-Rao tables of the modes 2 and 3 (one per core update, L2-resident):
-// vt[i][u] = A[i, p] A[i, q] for the vech pair u = (p <= q), zero-padded to ld columns.
+// vt[i][u] = A[i, p] A[i, q] for the vech pair u = (p <= q), zero up to column 144, then the
+// raw row A[i, :] (the h_b operand), zero to ld: one bulk copy stages both per draw.
 __global__ void k_vech_table(const double* __restrict__ A, int I, int R, int ld,
                              double* __restrict__ vt) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -825,6 +826,8 @@ __global__ void k_vech_table(const double* __restrict__ A, int I, int R, int ld,
     int pa, pb;
     pair_of(u, R, pa, pb);
     v = A[i * R + pa] * A[i * R + pb];
+  } else if (u >= 144 && u < 144 + R) {
+    v = A[i * R + (u - 144)];  // the raw factor row (h_b operand) after the padded vech part
   }
   vt[e] = v;
 }
@@ -853,10 +856,8 @@ constexpr int kB5Rows = 144;             // whole bucket per item
 constexpr int kB5Halves = 1;
 constexpr int kB5CtaPerSm = 1;
 constexpr int kB5Threads = (kB5Mma + 1) * 32;
-constexpr int kB5LdR = kB5Rows + 4;      // conflict-free fragment loads
-constexpr int kB5LdC = 144 + 4;
-constexpr int kB5Tab = 144;              // table row length (136 padded to 18 tiles)
-constexpr int kB5LdF = 16 + 4;           // raw factor rows (R <= 16) for h_b
+constexpr int kB5Tab = 160;              // table row: vech (136, padded to 144) + raw row (16)
+constexpr int kB5Ld = kB5Tab + 4;        // staged row stride: conflict-free fragment loads
 __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
     GramSpec spec, VechSpec v, const double* __restrict__ V2, const double* __restrict__ V3,
     const int* __restrict__ dmode, const double* __restrict__ dw2,
@@ -864,17 +865,14 @@ __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
     const int* __restrict__ blen, const int* __restrict__ nbuckets,
     const int* __restrict__ order, int* counter, double* __restrict__ H, double* __restrict__ h) {
   extern __shared__ __align__(16) double smb[];
-  double* zr = smb;                                  // [St][K][LdR]
-  double* zc = zr + kB5St * kB5K * kB5LdR;           // [St][K][LdC]
-  double* f2 = zc + kB5St * kB5K * kB5LdC;           // [St][K][LdF]  a_2 rows
-  double* f3 = f2 + kB5St * kB5K * kB5LdF;           // [St][K][LdF]  a_3 rows
-  double* w2s = f3 + kB5St * kB5K * kB5LdF;          // [St][K]
+  double* zr = smb;                                  // [St][K][Ld] V2 rows (+ raw a_2 rows)
+  double* zc = zr + kB5St * kB5K * kB5Ld;            // [St][K][Ld] V3 rows (+ raw a_3 rows)
+  double* w2s = zc + kB5St * kB5K * kB5Ld;           // [St][K]
   double* wxs = w2s + kB5St * kB5K;                  // [St][K]
   __shared__ __align__(8) unsigned long long full[kB5St], empty[kB5St];
   __shared__ int meta[kB5St][4];  // bucket (-1: no more work), half, draws in chunk, last chunk
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int R2 = v.R[1], R3 = v.R[2];
-  const bool fbulk = (R2 % 2 == 0) && (R3 % 2 == 0);
   if (tid == 0) {
     for (int i = 0; i < kB5St; ++i) {
       mbar_init(&full[i], 1);
@@ -885,8 +883,6 @@ __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
   __syncthreads();
   if (warp == kB5Mma) {
     // ---------------- producer ----------------
-    const double* A2 = spec.factors[1];
-    const double* A3 = spec.factors[2];
     const int nb = *nbuckets;
     const long long S = (long long)spec.s;
     unsigned q = 0;  // chunks staged so far
@@ -895,22 +891,34 @@ __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
       if (q >= kB5St) mbar_wait(&empty[sb], ((q / kB5St) - 1) & 1);
       return sb;
     };
+    // the next item (atomic ticket -> bucket -> its range) is fetched one item ahead, so the
+    // chain of dependent global loads overlaps the staging of the current item's chunks
+    auto fetch = [&](int& it, int& fb, int& fstart, int& flen) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(counter, 1);
+      it = __shfl_sync(0xffffffffu, t, 0);
+      fb = -1;
+      fstart = flen = 0;
+      if (it < kB5Halves * nb) {
+        fb = order[it / kB5Halves];
+        fstart = bstart[fb];
+        flen = blen[fb];
+      }
+    };
+    int nitem, nbk, nstart, nlen;
+    fetch(nitem, nbk, nstart, nlen);
     for (;;) {
-      int item = 0;
-      if (lane == 0) item = atomicAdd(counter, 1);
-      item = __shfl_sync(0xffffffffu, item, 0);
+      const int item = nitem, b = nbk, start = nstart, len = nlen;
       if (item >= kB5Halves * nb) break;
-      const int b = order[item / kB5Halves], half = item % kB5Halves;
+      fetch(nitem, nbk, nstart, nlen);
+      const int half = item % kB5Halves;
       const bool hrows = half == 0;
-      const int start = bstart[b], len = blen[b];
       const int nch = (len + kB5K - 1) / kB5K;
       for (int ch = 0; ch < nch; ++ch, ++q) {
         const int sb = next_stage();
         const int k0 = ch * kB5K, kn = min(kB5K, len - k0);
-        double* zrs = zr + sb * kB5K * kB5LdR;
-        double* zcs = zc + sb * kB5K * kB5LdC;
-        double* f2s = f2 + sb * kB5K * kB5LdF;
-        double* f3s = f3 + sb * kB5K * kB5LdF;
+        double* zrs = zr + sb * kB5K * kB5Ld;
+        double* zcs = zc + sb * kB5K * kB5Ld;
         int i2 = 0, i3 = 0;
         const bool ok = lane < kn;
         if (lane < kB5K) {
@@ -920,16 +928,10 @@ __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
             i3 = dmode[2 * S + dk];
             w2s[sb * kB5K + lane] = dw2[dk];
             wxs[sb * kB5K + lane] = dwx[dk];
-            if (hrows && !fbulk) {
-              for (int c = 0; c < R2; ++c) f2s[lane * kB5LdF + c] = A2[(long long)i2 * R2 + c];
-              for (int c = 0; c < R3; ++c) f3s[lane * kB5LdF + c] = A3[(long long)i3 * R3 + c];
-            }
           } else if (lane < ((kn + 3) & ~3)) {  // padding draws of the last k-step
             w2s[sb * kB5K + lane] = 0.0;
             wxs[sb * kB5K + lane] = 0.0;
-            for (int c = 0; c < kB5Rows; ++c) zrs[lane * kB5LdR + c] = 0.0;
-            for (int c = 0; c < 144; ++c) zcs[lane * kB5LdC + c] = 0.0;
-            for (int c = 0; c < 16; ++c) f2s[lane * kB5LdF + c] = f3s[lane * kB5LdF + c] = 0.0;
+            for (int c = 0; c < kB5Tab; ++c) zrs[lane * kB5Ld + c] = zcs[lane * kB5Ld + c] = 0.0;
           }
         }
         if (lane == 0) {
@@ -940,18 +942,11 @@ __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
         }
         fence_proxy_async();
         __syncwarp();
-        const unsigned row_bytes = (kB5Rows + 144) * 8 +
-                                   (hrows && fbulk ? (unsigned)(R2 + R3) * 8 : 0u);
-        if (lane == 0) mbar_arrive_expect_tx(&full[sb], row_bytes * (unsigned)kn);
+        if (lane == 0) mbar_arrive_expect_tx(&full[sb], 2u * kB5Tab * 8u * (unsigned)kn);
         __syncwarp();
         if (ok) {
-          bulk_g2s(zrs + lane * kB5LdR, V2 + (long long)i2 * kB5Tab + half * kB5Rows,
-                   kB5Rows * 8, &full[sb]);
-          bulk_g2s(zcs + lane * kB5LdC, V3 + (long long)i3 * kB5Tab, 144 * 8, &full[sb]);
-          if (hrows && fbulk) {
-            bulk_g2s(f2s + lane * kB5LdF, A2 + (long long)i2 * R2, R2 * 8, &full[sb]);
-            bulk_g2s(f3s + lane * kB5LdF, A3 + (long long)i3 * R3, R3 * 8, &full[sb]);
-          }
+          bulk_g2s(zrs + lane * kB5Ld, V2 + (long long)i2 * kB5Tab, kB5Tab * 8, &full[sb]);
+          bulk_g2s(zcs + lane * kB5Ld, V3 + (long long)i3 * kB5Tab, kB5Tab * 8, &full[sb]);
         }
       }
     }
@@ -987,17 +982,17 @@ __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
     const bool hw = half == 0 && warp < 4;
     const int ksn = (kn + 3) >> 2;
     {
-      const double* zrb = zr + sb * kB5K * kB5LdR + rg * 24 + g;
-      const double* zcb = zc + sb * kB5K * kB5LdC + cg * 48 + g;
+      const double* zrb = zr + sb * kB5K * kB5Ld + rg * 24 + g;
+      const double* zcb = zc + sb * kB5K * kB5Ld + cg * 48 + g;
       const double* w2c = w2s + sb * kB5K;
       for (int ks = 0; ks < ksn; ++ks) {
         const int k = ks * 4 + t4;
         const double wk = w2c[k];
         double av[3], bv[6];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) av[i] = wk * zrb[k * kB5LdR + i * 8];
+        for (int i = 0; i < 3; ++i) av[i] = wk * zrb[k * kB5Ld + i * 8];
 #pragma unroll
-        for (int j = 0; j < 6; ++j) bv[j] = zcb[k * kB5LdC + j * 8];
+        for (int j = 0; j < 6; ++j) bv[j] = zcb[k * kB5Ld + j * 8];
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -1005,14 +1000,12 @@ __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
       }
     }
     if (hw) {
-      const double* f2c = f2 + sb * kB5K * kB5LdF + hi * 8 + g;
-      const double* f3c = f3 + sb * kB5K * kB5LdF + hj * 8 + g;
+      const double* f2c = zr + sb * kB5K * kB5Ld + 144 + hi * 8 + g;
+      const double* f3c = zc + sb * kB5K * kB5Ld + 144 + hj * 8 + g;
       const double* wxc = wxs + sb * kB5K;
       for (int ks = 0; ks < ksn; ++ks) {
         const int k = ks * 4 + t4;
-        const double a = (hi * 8 + g < R2) ? wxc[k] * f2c[k * kB5LdF] : 0.0;
-        const double bb = (hj * 8 + g < R3) ? f3c[k * kB5LdF] : 0.0;
-        dmma_8x8x4(hc0, hc1, a, bb);
+        dmma_8x8x4(hc0, hc1, wxc[k] * f2c[k * kB5Ld], f3c[k * kB5Ld]);  // rows past R are 0
       }
     }
     __syncwarp();
@@ -1040,9 +1033,7 @@ __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
   }
 }
 
-size_t vech_bucket5_smem() {
-  return (size_t)kB5St * kB5K * (kB5LdR + kB5LdC + 2 * kB5LdF + 2) * 8 + 16;
-}
+size_t vech_bucket5_smem() { return (size_t)kB5St * kB5K * (2 * kB5Ld + 2) * 8 + 16; }
 
 // h_b[p'] = sum_{t in b} w_t^2 x_t prod_{n>=1} a_n(i_n)[p_n] from the draw records.
 __global__ void __launch_bounds__(256) k_bucket_h2(GramSpec spec, const double* __restrict__ dwx,

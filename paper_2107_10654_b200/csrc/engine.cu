@@ -794,6 +794,8 @@ class Engine {
   uint64_t factor_rng_ = 0, factor_k_ = 0;
   bool scores_valid_ = false;
   DevBuf fsums_, fsk_idx_, fsk_w_, fsk_work_, hj_ws_;
+  DevBuf xrot_[kMaxOrder];  // perf mode: X with mode n moved last (n < N - 1)
+  bool xrot_ok_ = std::getenv("RTB_NO_XROT") == nullptr;
   bool t_valid_ = false;
   uint64_t last_s_ = 0;
   int last_rank_deficient_ = 0, last_solver_path_ = 0, last_pcg_iters_ = 0;
@@ -1229,6 +1231,24 @@ class Engine {
     }
     fs.core = core_.as<double>();
     fs.x = x_;
+    // mode-n-last copy of X (made once per engine): every sampled fiber is contiguous
+    if (n != N_ - 1 && xrot_ok_) {
+      if (!xrot_[n].p) {
+        try {
+          xrot_[n].ensure(total_ * 8, st_);
+          move_axis_last(x_, (long long)prod(shape_, 0, n), (int)shape_[n],
+                         (long long)prod(shape_, n + 1), xrot_[n].as<double>(), st_);
+        } catch (const Error&) {
+          cudaGetLastError();
+          xrot_[n] = DevBuf();
+          xrot_ok_ = false;  // no room: keep the strided gathers
+        }
+      }
+      if (xrot_[n].p) {
+        fs.x = xrot_[n].as<double>();
+        fs.x_mode_last = 1;
+      }
+    }
     fs.lambda = opt_.lambda;
     fs.s = s;
     fsk_work_.ensure(factor_sketch_work_bytes(fs), st_);

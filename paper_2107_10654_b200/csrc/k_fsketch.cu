@@ -26,6 +26,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace rtb {
 
 namespace {
@@ -249,6 +251,252 @@ __global__ void __launch_bounds__(kTile) k_fsk_accum(FskDev f, const double* __r
   }
 }
 
+// Contiguous fibers (x is the mode-n-last copy, or n is the last mode) and even I_n: each of
+// 128 threads owns TWO adjacent columns of the 256-column tile (16-byte loads of the gathered
+// fiber values, 16 draws unrolled so ~32 KB per SM are in flight), otherwise as
+// k_fsk_accum (same chunking by the caller, same Gram partials from the tile-0 CTAs).
+constexpr int kT2 = 128;
+template <int RM>
+__global__ void __launch_bounds__(kT2) k_fsk_accum2(FskDev f, const double* __restrict__ x,
+                                                   const double* __restrict__ kw,
+                                                   const long long* __restrict__ base,
+                                                   const double* __restrict__ wts,
+                                                   unsigned long long s, long long chunk,
+                                                   double* __restrict__ part,
+                                                   double* __restrict__ gpart) {
+  __shared__ __align__(16) double skw[kSub][RM];
+  __shared__ long long sb[kSub];
+  __shared__ double sw[kSub];
+  const long long t0 = (long long)blockIdx.x * chunk;
+  const long long t1 = min((long long)s, t0 + chunk);
+  const int i = blockIdx.y * kTile + 2 * threadIdx.x;
+  const bool col = i < f.in;
+  const double2* xcol = reinterpret_cast<const double2*>(x + (col ? i : 0));
+  const bool do_gram = blockIdx.y == 0;
+  const int rn = f.rn;
+  double acc0[RM], acc1[RM];
+#pragma unroll
+  for (int r = 0; r < RM; ++r) acc0[r] = acc1[r] = 0.0;
+  constexpr int NG = (RM * RM + kT2 - 1) / kT2;
+  double gacc[NG];
+#pragma unroll
+  for (int k = 0; k < NG; ++k) gacc[k] = 0.0;
+  for (long long ts = t0; ts < t1; ts += kSub) {
+    const int n = (int)min((long long)kSub, t1 - ts);
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * RM; e += kT2) skw[e / RM][e % RM] = kw[(ts + e / RM) * RM + e % RM];
+    for (int e = threadIdx.x; e < n; e += kT2) {
+      sb[e] = base[ts + e];
+      sw[e] = wts[ts + e];
+    }
+    __syncthreads();
+    if (col) {
+#pragma unroll 16
+      for (int tt = 0; tt < n; ++tt) {
+        const long long bb = sb[tt];
+        double2 v = make_double2(0.0, 0.0);
+        if (bb >= 0) {
+          const double2 xv = __ldg(xcol + (bb >> 1));  // bb is a multiple of I_n (even)
+          v.x = sw[tt] * xv.x;
+          v.y = sw[tt] * xv.y;
+        }
+#pragma unroll
+        for (int r = 0; r < RM; r += 2) {
+          const double2 k2 = *reinterpret_cast<const double2*>(&skw[tt][r]);
+          acc0[r] = fma(k2.x, v.x, acc0[r]);
+          acc0[r + 1] = fma(k2.y, v.x, acc0[r + 1]);
+          acc1[r] = fma(k2.x, v.y, acc1[r]);
+          acc1[r + 1] = fma(k2.y, v.y, acc1[r + 1]);
+        }
+      }
+    }
+    if (do_gram) {
+#pragma unroll
+      for (int k = 0; k < NG; ++k) {
+        const int e = threadIdx.x + k * kT2;
+        if (e < rn * rn) {
+          const int p = e / rn, q = e - p * rn;
+          double g = gacc[k];
+          for (int tt = 0; tt < n; ++tt) {
+            const long long bb = sb[tt];
+            if (bb >= 0) {
+              g = fma(skw[tt][p], skw[tt][q], g);
+            } else if (p == q && (int)(-1 - bb) == p) {
+              const double w2 = sw[tt] * sw[tt];
+              g = fma(w2 * f.root_lambda, f.root_lambda, g);
+            }
+          }
+          gacc[k] = g;
+        }
+      }
+    }
+  }
+  if (col) {
+    double* o = part + ((size_t)blockIdx.x * f.in + i) * RM;
+#pragma unroll
+    for (int r = 0; r < RM; ++r) {
+      o[r] = acc0[r];
+      o[RM + r] = acc1[r];
+    }
+  }
+  if (do_gram) {
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+      const int e = threadIdx.x + k * kT2;
+      if (e < rn * rn) gpart[(size_t)blockIdx.x * rn * rn + e] = gacc[k];
+    }
+  }
+}
+
+// Contiguous fibers, TMA-staged: one CTA per chunk of draws. Warp 0 scans the chunk's draws
+// (32 at a time, ballot on "data draw") and bulk-copies each data draw's fiber (I_n values,
+// contiguous in the mode-n-last copy) and its w k row into a kFq-deep ring of kFg-fiber
+// stages (full mbarrier with the byte count, empty mbarrier per consumer warp); 8 consumer
+// warps, thread = 2 adjacent columns of up to 512 (I_n <= 2 * 256 * kFcols), accumulate
+// M[i] += x_t[i] (w_t k_t) from shared memory. The bytes in flight per SM are the ring, not
+// registers, so the gather runs at HBM speed. The chunk's Gram partial comes from the same
+// staged w k rows (one entry per consumer thread, R_n^2 <= 256) plus the augmented diagonal
+// (count per column x the common weight^2 x lambda).
+constexpr int kFg = 8;       // fibers per stage
+constexpr int kFq = 4;       // stages
+constexpr int kFthreads = 9 * 32;
+template <int RM>
+__global__ void __launch_bounds__(kFthreads, 1) k_fsk_accum3(FskDev f, const double* __restrict__ x,
+                                                           const double* __restrict__ kw,
+                                                           const long long* __restrict__ base,
+                                                           const double* __restrict__ wts,
+                                                           unsigned long long s, long long chunk,
+                                                           double* __restrict__ part,
+                                                           double* __restrict__ gpart) {
+  extern __shared__ __align__(16) double fsm[];
+  const int in = f.in;
+  const int ldf = in + 2;                              // fiber row stride (16-byte aligned)
+  double* fib = fsm;                                   // [kFq][kFg][ldf]
+  double* kws = fib + (size_t)kFq * kFg * ldf;         // [kFq][kFg][RM]  (w k)
+  __shared__ __align__(8) unsigned long long full[kFq], empty[kFq];
+  __shared__ int cnt[kFq];                             // fibers in the stage (0: end)
+  __shared__ double wfib[kFq][kFg];                    // w_t of each staged fiber
+  __shared__ int aug_cnt[RM];                          // augmented draws per column
+  __shared__ double aug_w2;                            // their (common) weight^2
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid < RM) aug_cnt[tid] = 0;
+  if (tid == 0) aug_w2 = 0.0;
+  const long long t0 = (long long)blockIdx.x * chunk;
+  const long long t1 = min((long long)s, t0 + chunk);
+  if (tid == 0) {
+    for (int q = 0; q < kFq; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], kFthreads / 32 - 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == 0) {  // producer
+    unsigned q = 0;
+    int fill = 0;
+    long long my_t = 0, my_b = 0;  // lane k holds the k-th fiber of the stage being filled
+    auto flush = [&](bool last) {
+      const int sb = (int)(q % kFq);
+      if (q >= kFq) mbar_wait(&empty[sb], ((q / kFq) - 1) & 1);
+      if (lane == 0) cnt[sb] = last && fill == 0 ? 0 : fill;
+      if (lane < fill) wfib[sb][lane] = wts[my_t];
+      __syncwarp();
+      const unsigned bytes = (unsigned)fill * ((unsigned)in * 8u + RM * 8u);
+      if (lane == 0) mbar_arrive_expect_tx(&full[sb], bytes);
+      __syncwarp();
+      if (lane < fill) {
+        bulk_g2s(fib + ((size_t)sb * kFg + lane) * ldf, x + my_b, in * 8, &full[sb]);
+        bulk_g2s(kws + ((size_t)sb * kFg + lane) * RM, kw + my_t * RM, RM * 8, &full[sb]);
+      }
+      ++q;
+      fill = 0;
+    };
+    for (long long tb = t0; tb < t1; tb += 32) {
+      const long long t = tb + lane;
+      const long long bb = t < t1 ? base[t] : 0;
+      if (t < t1 && bb < 0) {  // augmented draw of column -1 - bb (all share one weight)
+        atomicAdd(&aug_cnt[(int)(-1 - bb)], 1);
+        aug_w2 = wts[t] * wts[t];
+      }
+      unsigned m = __ballot_sync(0xffffffffu, t < t1 && bb >= 0);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const long long b_src = __shfl_sync(0xffffffffu, bb, src);
+        if (lane == fill) {
+          my_b = b_src;
+          my_t = tb + src;
+        }
+        ++fill;
+        if (fill == kFg) flush(false);
+      }
+    }
+    if (fill) flush(false);
+    flush(true);  // end marker
+    return;
+  }
+  // consumers: thread (warp - 1, lane) owns columns 2 c, 2 c + 1 for c = tid - 32 + 256 j
+  const int c0 = tid - 32;
+  constexpr int kCols = 2;  // column pairs per thread: I_n <= 2 * 256 * kCols
+  double acc[kCols][2][RM];
+#pragma unroll
+  for (int a = 0; a < kCols; ++a)
+#pragma unroll
+    for (int r = 0; r < RM; ++r) acc[a][0][r] = acc[a][1][r] = 0.0;
+  // Gram entry (gp, gq) of this thread over the data draws (w k staged with the fibers)
+  const int rn = f.rn;
+  const bool gth = c0 < rn * rn;
+  const int gp = gth ? c0 / rn : 0, gq = gth ? c0 - gp * rn : 0;
+  double gacc = 0.0;
+  for (unsigned q = 0;; ++q) {
+    const int sb = (int)(q % kFq);
+    mbar_wait(&full[sb], (q / kFq) & 1);
+    const int n = cnt[sb];
+    if (n == 0) break;
+    for (int j = 0; j < n; ++j) {
+      const double* fr = fib + ((size_t)sb * kFg + j) * ldf;
+      const double* kr = kws + ((size_t)sb * kFg + j) * RM;
+      const double wj = wfib[sb][j];
+      if (gth) gacc = fma(kr[gp], kr[gq], gacc);
+#pragma unroll
+      for (int a = 0; a < kCols; ++a) {
+        const int i = 2 * (c0 + 256 * a);
+        if (i < in) {
+          double2 xv = *reinterpret_cast<const double2*>(fr + i);
+          xv.x *= wj;  // M += (w x)(w k)^T, as k_fsk_accum
+          xv.y *= wj;
+#pragma unroll
+          for (int r = 0; r < RM; r += 2) {
+            const double2 k2 = *reinterpret_cast<const double2*>(kr + r);
+            acc[a][0][r] = fma(k2.x, xv.x, acc[a][0][r]);
+            acc[a][0][r + 1] = fma(k2.y, xv.x, acc[a][0][r + 1]);
+            acc[a][1][r] = fma(k2.x, xv.y, acc[a][1][r]);
+            acc[a][1][r + 1] = fma(k2.y, xv.y, acc[a][1][r + 1]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sb]);
+  }
+  if (gth) {
+    if (gp == gq && aug_cnt[gp]) gacc += (double)aug_cnt[gp] * ((aug_w2 * f.root_lambda) * f.root_lambda);
+    gpart[(size_t)blockIdx.x * rn * rn + c0] = gacc;
+  }
+#pragma unroll
+  for (int a = 0; a < kCols; ++a) {
+    const int i = 2 * (c0 + 256 * a);
+    if (i < in) {
+      double* o = part + ((size_t)blockIdx.x * in + i) * RM;
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        o[r] = acc[a][0][r];
+        o[RM + r] = acc[a][1][r];
+      }
+    }
+  }
+}
+
 // One warp per output entry: lanes stride over the chunk partials, a fixed butterfly sums
 // the lanes (deterministic; the chunk partials of one entry are read in parallel).
 template <int RM>
@@ -277,6 +525,8 @@ __global__ void k_fsk_reduce(const double* __restrict__ part, const double* __re
 
 int rm_of(int rn) { return rn <= 8 ? 8 : rn <= 16 ? 16 : 32; }
 
+size_t tma_smem(int in, int rm) { return ((size_t)kFq * kFg * (in + 2) + (size_t)kFq * kFg * rm) * 8; }
+
 struct FskLayout {
   int nchunks;
   long long chunk;
@@ -289,12 +539,23 @@ struct FskLayout {
   size_t bytes;
 };
 
+// the TMA-staged gather applies: contiguous fibers of even length <= 1024, R_n^2 <= 256
+bool fsk_tma(const FactorSketchSpec& sp) {
+  const int n = sp.mode, in = sp.rows[n], rn = sp.ranks[n];
+  const bool contiguous = (sp.x_mode_last || n == sp.order - 1) && in % 2 == 0 &&
+                          std::getenv("RTB_NO_FSK2") == nullptr;
+  return contiguous && in <= 1024 && rn * rn <= 256 && tma_smem(in, rm_of(rn)) <= 220 * 1024 &&
+         std::getenv("RTB_NO_FSK3") == nullptr;
+}
+
 FskLayout fsk_layout(const FactorSketchSpec& sp, void* work) {
   const int RM = rm_of(sp.ranks[sp.mode]);
   const int in = sp.rows[sp.mode], rn = sp.ranks[sp.mode];
   const int tiles = ceil_div(in, kTile);
   const long long s = (long long)sp.s;
-  int nchunks = std::max(1, std::min<int>((int)ceil_div<long long>(s, kSub), 2 * kNumSMs / tiles));
+  // one wave of work units: the TMA gather runs one CTA per SM (fewer chunk partials too)
+  const int units = fsk_tma(sp) ? kNumSMs : 4 * kNumSMs / tiles;
+  int nchunks = std::max(1, std::min<int>((int)ceil_div<long long>(s, kSub), units));
   long long chunk = ceil_div<long long>(ceil_div<long long>(s, nchunks), kSub) * kSub;
   nchunks = (int)ceil_div<long long>(s, chunk);
   FskLayout l{};
@@ -324,6 +585,38 @@ FskLayout fsk_layout(const FactorSketchSpec& sp, void* work) {
 
 size_t factor_sketch_work_bytes(const FactorSketchSpec& sp) { return fsk_layout(sp, nullptr).bytes; }
 
+namespace {
+// [A][In][B] -> [A][B][In]: 32 x 32 tiles through shared memory, batch a = blockIdx.z
+__global__ void k_move_axis_last(const double* __restrict__ x, int In, long long B,
+                                 double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const long long a = blockIdx.z;
+  const int i0 = blockIdx.y * 32;
+  const long long b0 = (long long)blockIdx.x * 32;
+  const double* xa = x + a * In * B;
+  double* oa = out + a * In * B;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = i0 + r;
+    const long long b = b0 + threadIdx.x;
+    if (i < In && b < B) tile[r][threadIdx.x] = xa[(long long)i * B + b];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const long long b = b0 + r;
+    const int i = i0 + threadIdx.x;
+    if (i < In && b < B) oa[b * In + i] = tile[threadIdx.x][r];
+  }
+}
+}  // namespace
+
+void move_axis_last(const double* x, long long A, int In, long long B, double* out,
+                    cudaStream_t st) {
+  if (A > 65535) throw Error(4, "move_axis_last: batch too large");
+  const dim3 grid((unsigned)ceil_div<long long>(B, 32), (unsigned)ceil_div(In, 32), (unsigned)A);
+  k_move_axis_last<<<grid, dim3(32, 8), 0, st>>>(x, In, B, out);
+  RTB_LAUNCH_CHECK();
+}
+
 void factor_sketch_normal_eq(const FactorSketchSpec& sp, const unsigned long long* idx,
                              const double* w, void* work, double* gram, double* M,
                              cudaStream_t st) {
@@ -347,6 +640,15 @@ void factor_sketch_normal_eq(const FactorSketchSpec& sp, const unsigned long lon
       a *= sp.rows[m];
       c *= sp.ranks[m];
     }
+    if (sp.x_mode_last) {  // axes: other modes ascending, then mode n (stride 1)
+      a = sp.rows[n];
+      xs[n] = 1;
+      for (int m = sp.order - 1; m >= 0; --m) {
+        if (m == n) continue;
+        xs[m] = a;
+        a *= sp.rows[m];
+      }
+    }
   }
   f.cstride_n = cs[n];
   f.xstride_n = xs[n];
@@ -369,6 +671,10 @@ void factor_sketch_normal_eq(const FactorSketchSpec& sp, const unsigned long lon
   if (sp.s == 0) throw Error(1, "solve_sketched_ridge: sample count must be positive");
   FskLayout l = fsk_layout(sp, work);
   const int RM = rm_of(rn);
+  const bool contiguous = f.xstride_n == 1 && f.in % 2 == 0 &&
+                          std::getenv("RTB_NO_FSK2") == nullptr;
+  // TMA-staged gather: one CTA per chunk, one chunk per SM (fsk_layout)
+  const bool tma = fsk_tma(sp);
   // 8 draws per warp, 8 warps per block
   const unsigned rows_blocks = (unsigned)ceil_div<unsigned long long>(sp.s, 64ULL);
   int srow = 0;
@@ -385,8 +691,16 @@ void factor_sketch_normal_eq(const FactorSketchSpec& sp, const unsigned long lon
   k_fsk_rows<RMV><<<rows_blocks, 256, rows_smem, st>>>(f, l.gt, l.qdig, idx, w, sp.s, srow, l.kw, \
                                                        l.base);                                \
   RTB_LAUNCH_CHECK();                                                                            \
-  k_fsk_accum<RMV><<<agrid, kTile, 0, st>>>(f, sp.x, l.kw, l.base, w, sp.s, l.chunk, l.part,    \
-                                            l.gpart);                                            \
+  if (tma) {                                                                                     \
+    set_max_smem(k_fsk_accum3<RMV>, (int)tma_smem(f.in, RMV));                                   \
+    k_fsk_accum3<RMV><<<l.nchunks, kFthreads, tma_smem(f.in, RMV), st>>>(                        \
+        f, sp.x, l.kw, l.base, w, sp.s, l.chunk, l.part, l.gpart);                               \
+  } else if (contiguous)                                                                         \
+    k_fsk_accum2<RMV><<<agrid, kT2, 0, st>>>(f, sp.x, l.kw, l.base, w, sp.s, l.chunk, l.part,   \
+                                             l.gpart);                                           \
+  else                                                                                           \
+    k_fsk_accum<RMV><<<agrid, kTile, 0, st>>>(f, sp.x, l.kw, l.base, w, sp.s, l.chunk, l.part,  \
+                                              l.gpart);                                          \
   RTB_LAUNCH_CHECK();                                                                            \
   k_fsk_reduce<RMV><<<rblocks, 256, 0, st>>>(l.part, l.gpart, l.nchunks, f.in, rn, M, gram);    \
   RTB_LAUNCH_CHECK();

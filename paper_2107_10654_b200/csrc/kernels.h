@@ -108,7 +108,13 @@ struct FactorSketchSpec {
   const double* x;
   double lambda;
   unsigned long long s;     // draws (indices over the other modes + R_n augmented rows)
+  // 1: x is the mode-n-last copy of X (axes: the other modes ascending, then mode n;
+  // move_axis_last), so every sampled fiber is one contiguous run of I_n values
+  int x_mode_last = 0;
 };
+// out = X with axis of length In moved last: X viewed as [A][In][B] -> out [A][B][In]
+void move_axis_last(const double* x, long long A, int In, long long B, double* out,
+                    cudaStream_t st);
 size_t factor_sketch_work_bytes(const FactorSketchSpec& spec);
 // gram (R_n x R_n) and M (I_n x R_n) from the draws idx/w (k_draw.cu format with
 // total_rows = prod_{m != n} I_m, d = R_n)

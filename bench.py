@@ -801,7 +801,15 @@ def c3_lines(args, steps=None):
     the device; K sweeps timed with CUDA events after the warm-up sweeps."""
     import torch
     from paper_2107_10654_b200 import rtucker as rt
-    torch.cuda.set_device(0)
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:  # N > 1: X split along mode 1, NCCL all-reduce of every partial sum
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rt.set_stream(torch.cuda.current_stream().cuda_stream)
     I, R, lam, s = 160, 10, 0.1, 500000
     shape, ranks = (I,) * 4, (R,) * 4
@@ -814,20 +822,29 @@ def c3_lines(args, steps=None):
         x = torch.movedim(torch.tensordot(f, x, dims=([1], [n])), 0, n)
     x = x + 0.05 * x.norm() / x.numel() ** 0.5 * torch.randn(x.shape, dtype=torch.float64,
                                                                device="cuda", generator=g)
+    shard, lshape = None, shape
+    if world > 1:
+        lo, hi = rt.shard_rows(rank, world, I)
+        x = x[lo:hi]
+        lshape = (hi - lo,) + shape[1:]
+        shard = rt.Shard(rank, world, I, rt.torch_allreduce(dist))
     x = x.contiguous()
     torch.cuda.synchronize()
-    t = rt.Tensor.from_device(x.data_ptr(), shape)
+    t = rt.Tensor.from_device(x.data_ptr(), lshape)
     del x
     steps = steps or args.steps
     lines = []
-    for fs in (0, 50000):
+    # sketched factor updates are a single-GPU perf mode
+    for fs in ((0, 50000) if world == 1 else (0,)):
         opts = rt.options(lam=lam, sketched_core=1, sample_count_override=s, tolerance=0.0,
                           max_iterations=args.warmup + steps + 1)
-        sess = rt.Session(t, ranks, opts, factor_samples=fs)
+        sess = rt.Session(t, ranks, opts, factor_samples=fs, shard=shard)
         sess.sweeps(args.warmup)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        clocks = Clocks(0)
+        if dist:
+            dist.barrier()
+        clocks = Clocks(local)
         clocks.wait_first()
         clocks.mark_start()
         e0.record()
@@ -836,13 +853,17 @@ def c3_lines(args, steps=None):
         torch.cuda.synchronize()
         clk = clocks.stop()
         ms = e0.elapsed_time(e1) / steps
+        if dist:
+            tt = torch.tensor([ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
         r = sess.result()
         graph_sweeps = r.graph_sweeps
         sess.free()
         # kernel shares from a kernel-by-kernel re-run with per-family CUDA events
         sp = rt.Session(t, ranks, rt.options(lam=lam, sketched_core=1, sample_count_override=s,
                                              tolerance=0.0, max_iterations=args.warmup + 5),
-                        profile=True, factor_samples=fs)
+                        profile=True, factor_samples=fs, shard=shard)
         sp.sweeps(args.warmup + 5)
         fam = {}
         for name, secs, n in sp.result().kernels():
@@ -851,7 +872,8 @@ def c3_lines(args, steps=None):
         tot = sum(fam.values()) or 1.0
         line = {
             "metric": "sketched Tucker-ALS sweeps/s (C3)", "value": 1e3 / ms, "unit": "sweeps/s",
-            "n_gpus": 1, "steps": steps, "warmup": args.warmup, "ms_per_step": ms,
+            "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": ms,
+            "scaling": "strong" if world > 1 else "weak",
             "clocks": clk, "cuda_graph_sweeps": graph_sweeps,
             "higher_is_better": True, "dtype": "f64", "data": "synthetic (seeded torch)",
             "config": {"workload": "C3: dense 4-way FP64 160^4 (5.2 GB), planted rank (10,10,10,10), "
@@ -863,7 +885,10 @@ def c3_lines(args, steps=None):
             "kernel_share": {k: round(v / tot, 4) for k, v in sorted(fam.items(),
                                                                     key=lambda kv: -kv[1])[:8]},
         }
-        lines.append(line)
+        line["config"]["parallelism"] = (f"X sharded along mode 1 over {world} GPUs, NCCL "
+                                         "all-reduce of partial sums" if world > 1 else "single GPU")
+        if rank == 0:
+            lines.append(line)
     t.free()
     torch.cuda.empty_cache()
     return lines
@@ -872,6 +897,10 @@ def c3_lines(args, steps=None):
 def run_c3(args):
     for line in c3_lines(args):
         print(json.dumps(line), flush=True)
+    if env_int("WORLD_SIZE", 1) > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 

@@ -229,11 +229,14 @@ GramSpec merged_spec(const GramSpec& s4) {
   g.dprime = s4.ranks[2] * s4.ranks[3];
   g.lambda = s4.lambda;
   g.s = s4.s;
+  // sharded along mode 1: the merged mode's rows (i1, i2) of this shard are contiguous
+  g.i1_lo = s4.i1_hi > 0 ? s4.i1_lo * s4.rows[1] : 0;
+  g.i1_hi = s4.i1_hi > 0 ? s4.i1_hi * s4.rows[1] : 0;
   return g;
 }
 
 bool merged4_ok(const GramSpec& spec) {
-  if (spec.order != 4 || spec.i1_hi > 0) return false;
+  if (spec.order != 4) return false;
   if ((long long)spec.rows[0] * spec.rows[1] > (1LL << 30)) return false;
   if (spec.ranks[2] > 16 || spec.ranks[3] > 16) return false;
   // worth it when the draws outnumber the (i1, i2) pairs
@@ -1420,7 +1423,10 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
   const bool fused_h = whole && nr == 1 && nc == 1 && v.R[1] <= 16 && v.R[2] <= 16 &&
                        (v.Mrow + 7) / 8 < kBWarps;
   static const bool b5_off_g = std::getenv("RTB_NO_BUCKET5") != nullptr;
-  const bool b5 = fused_h && !b5_off_g && v.N == 3 && v.R[1] <= 16 && v.R[2] <= 16;
+  // the 144 x 144-tile bucket kernel pays off for R_2 = R_3 = 16 (136 vech pairs) and
+  // buckets long enough to fill its 24-draw stages (C2: ~195 draws per bucket)
+  const bool b5 = fused_h && !b5_off_g && v.N == 3 && v.R[1] <= 16 && v.R[2] <= 16 &&
+                  v.Mrow > 120 && v.Ncol > 120 && (double)spec.s >= 48.0 * I1;
   if (whole) {
     if (!b5) {
       k_gather_rows<<<(unsigned)ceil_div<unsigned long long>(spec.s * v.rowlen, 256ULL), 256, 0,
@@ -1456,8 +1462,7 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
       else if (nr == 1 && nc == 2) by_nt(hpt, I1c{}, I2c{});
       else by_nt(hpt, I2c{}, I1c{});
     };
-    static const bool b5_off = std::getenv("RTB_NO_BUCKET5") != nullptr;
-    if (fused_h && !b5_off && v.N == 3 && v.R[1] <= 16 && v.R[2] <= 16) {
+    if (b5) {
       // vech tables of A_2, A_3, then the persistent table-gather bucket kernel
       k_vech_table<<<(unsigned)ceil_div<long long>((long long)spec.rows[1] * kB5Tab, 256), 256, 0,
                      st>>>(spec.factors[1], spec.rows[1], v.R[1], kB5Tab, l.vt2);
@@ -1557,16 +1562,23 @@ void sketch_normal_eq_m4(const GramSpec& spec, const double* x, const unsigned l
   k_vech_kr<<<ceil_div(I2 * m2, 256), 256, 0, st>>>(spec.factors[1], I2, R2, e.ka2);
   RTB_LAUNCH_CHECK();
   const long long U = v3.Hsz;  // m3 m4
+  // sharded along mode 1: only this shard's i1 rows hold draws, so the contractions run over
+  // them alone and S / rhs are this shard's partial sums (the engine all-reduces them)
+  const int i1lo = spec.i1_hi > 0 ? spec.i1_lo : 0, i1hi = spec.i1_hi > 0 ? spec.i1_hi : I1;
+  const int nl = i1hi - i1lo;
+  const double* Hd = e.Hd + (size_t)i1lo * I2 * U;
+  const double* hd = e.hd + (size_t)i1lo * I2 * g.dprime;
   // T_{i1} (m2 x U) = KA2^T Hd_{i1}
-  gemm_tn(e.ka2, m2, e.Hd, U, m2, U, I2, e.T, U, st, I1, 0, (long long)I2 * U, (long long)m2 * U);
+  gemm_tn(e.ka2, m2, Hd, U, m2, U, I2, e.T, U, st, nl, 0, (long long)I2 * U, (long long)m2 * U);
   // S (m1 x m2 U) = KA1^T T, straight into the order-4 layout's compact Gram
-  gemm_tn(e.ka1, m1, e.T, (long long)m2 * U, m1, (long long)m2 * U, I1, l4.S, (long long)m2 * U, st);
+  gemm_tn(e.ka1 + (size_t)i1lo * m1, m1, e.T, (long long)m2 * U, m1, (long long)m2 * U, nl, l4.S,
+          (long long)m2 * U, st);
   // rhs: Tr_{i1} (R2 x R3 R4) = A2^T hd_{i1}; rhs (R1 x R2 R3 R4) = A1^T Tr
   const long long hp = g.dprime;
-  gemm_tn(spec.factors[1], R2, e.hd, hp, R2, hp, I2, e.Tr, hp, st, I1, 0, (long long)I2 * hp,
+  gemm_tn(spec.factors[1], R2, hd, hp, R2, hp, I2, e.Tr, hp, st, nl, 0, (long long)I2 * hp,
           (long long)R2 * hp);
-  gemm_tn(spec.factors[0], R1, e.Tr, (long long)R2 * hp, R1, (long long)R2 * hp, I1, rhs,
-          (long long)R2 * hp, st);
+  gemm_tn(spec.factors[0] + (size_t)i1lo * R1, R1, e.Tr, (long long)R2 * hp, R1,
+          (long long)R2 * hp, nl, rhs, (long long)R2 * hp, st);
   RTB_CUDA(cudaMemcpyAsync(l4.aug_count, l3.aug_count, (size_t)spec.d * 4,
                            cudaMemcpyDeviceToDevice, st));
   if (gram) {

@@ -105,6 +105,25 @@ def test_sharded_als_matches_single_process(rt, P, sketched):
         assert sum(o[2]["data_draws"] for o in outs) == ref.sketch_info()["data_draws"]
 
 
+@pytest.mark.parametrize("P", [2, 3])
+def test_sharded_order4_bucketed_path(rt, P):
+    """Order 4 with draws >> (i1, i2) pairs: the (i1, i2)-bucketed Gram (k_gram.cu,
+    sketch_normal_eq_m4) restricted to this shard's i1 rows (BASELINE config 3 across GPUs)."""
+    shape, ranks = (20, 18, 16, 14), (3, 3, 2, 2)
+    x = planted(shape, ranks, seed=43)
+    kw = dict(lam=0.1, sketched_core=1, sample_count_override=20000, max_iterations=3,
+              tolerance=0.0, record_history=1, seed=7)
+    ref = rt.als_run(rt.Tensor.from_numpy(x), ranks, rt.options(**kw))
+    outs = run_sharded(rt, x, ranks, kw, P)
+    rh, rm = ref.history(), ref.model()
+    for hist, model, info in outs:
+        assert [(h[0], h[1]) for h in hist] == [(h[0], h[1]) for h in rh]
+        for (gi, gs, gl, grm), (_, _, fl, frm) in zip(hist, rh):
+            assert abs(gl - fl) / fl < 1e-7, (gi, gs, gl, fl)
+        assert np.linalg.norm(model.core - rm.core) / np.linalg.norm(rm.core) < 1e-5
+    assert sum(o[2]["data_draws"] for o in outs) == ref.sketch_info()["data_draws"]
+
+
 def test_sharded_rejects_bad_split(rt):
     x = planted((20, 10, 8), (2, 2, 2), seed=1)
     with pytest.raises(rt.RtuckerError):

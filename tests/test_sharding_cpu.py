@@ -36,7 +36,10 @@ def _planted(shape, ranks, seed):
     return x + 0.01 * rng.standard_normal(x.shape), core, fs
 
 
-def _worker(rank, world, port, q):
+CASES = [((13, 9, 7), (3, 2, 2)), ((12, 9, 7, 6), (2, 3, 2, 2))]
+
+
+def _worker(rank, world, port, q, case=0):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -44,7 +47,7 @@ def _worker(rank, world, port, q):
         from oracle.oracle import Oracle
         from paper_2107_10654_b200 import rtucker as rt
         ar = rt.host_allreduce(dist)
-        shape, ranks = (13, 9, 7), (3, 2, 2)
+        shape, ranks = CASES[case]
         x, core, fs = _planted(shape, ranks, 5)
         I1 = shape[0]
         lo, hi = rt.shard_rows(rank, world, I1)
@@ -60,7 +63,9 @@ def _worker(rank, world, port, q):
         assert np.allclose(part, full, rtol=1e-13, atol=1e-12)
         # (3) sketched normal equations: data draws split by i1, augmented draws once
         o = Oracle()
-        lam, s, seed = 0.05, 900, 17
+        # order 4: s above 2 I1 I2 (the library's (i1, i2)-bucketed path, whose shard split
+        # is the same i1 ownership of the data draws)
+        lam, s, seed = 0.05, 900 if len(shape) == 3 else 2500, 17
         _, idx, w, _ = o.update_core_fast(shape, ranks, core, fs, lam, x, s, seed)
         total = int(np.prod(shape))
         inner = total // I1
@@ -90,11 +95,12 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.parametrize("world", [2])
-def test_sharding_decomposition_gloo(oracle, world):
+@pytest.mark.parametrize("case", [0, 1])
+def test_sharding_decomposition_gloo(oracle, world, case):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q, case)) for r in range(world)]
     for p in ps:
         p.start()
     res = [q.get(timeout=240) for _ in ps]

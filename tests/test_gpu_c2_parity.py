@@ -120,19 +120,22 @@ def _oracle_draws(oracle, shape, ranks, factors, seed, s):
     return idx, w
 
 
-def test_normal_equations_d4096_from_oracle_sketch(oracle, rt, x_c2):
-    """Rung 3 at C2: d = 4096, R = 16 (k_vech_bucket5, k_vech_contract2, k_vech_blocks),
-    the draws made by the oracle's sampler, the Gram/RHS by the oracle's restatement of
-    the reference's row-by-row stream."""
-    shape, ranks, lam, s = x_c2.shape, (16, 16, 16), 1e-2, 4000
+@pytest.mark.parametrize("i1,kernel", [(32, "k_vech_bucket5"), (512, "k_vech_bucket2<17>")])
+def test_normal_equations_d4096_from_oracle_sketch(oracle, rt, x_c2, i1, kernel):
+    """Rung 3 at d = 4096, R = 16 (the C2 Gram kernels: k_vech_bucket5 for C2's ~390 draws per
+    i_1 bucket, here 32 buckets of ~60 data draws; k_vech_bucket2<17> for short buckets;
+    k_vech_contract2, k_vech_blocks), the draws made by the oracle's sampler, the Gram/RHS by
+    the oracle's restatement of the reference's row-by-row stream."""
+    x = np.ascontiguousarray(x_c2[:i1])
+    shape, ranks, lam, s = x.shape, (16, 16, 16), 1e-2, 4000
     core, factors = model(oracle, shape, ranks, "uniform", 9)
     idx, w = _oracle_draws(oracle, shape, ranks, factors, 2024, s)
-    b17 = rt.variant_count("k_vech_bucket5")
+    b17 = rt.variant_count(kernel)
     c2 = rt.variant_count("k_vech_contract2")
-    gg, grhs = rt.kron_normal_eq(shape, ranks, factors, x_c2, lam, idx, w)
-    assert rt.variant_count("k_vech_bucket5") == b17 + 1
+    gg, grhs = rt.kron_normal_eq(shape, ranks, factors, x, lam, idx, w)
+    assert rt.variant_count(kernel) == b17 + 1
     assert rt.variant_count("k_vech_contract2") == c2 + 1
-    og, orhs = oracle.kron_normal_eq(shape, ranks, factors, x_c2, lam, idx, w)
+    og, orhs = oracle.kron_normal_eq(shape, ranks, factors, x, lam, idx, w)
     dg = np.sqrt(np.outer(np.diag(og), np.diag(og)))
     eg = float(np.max(np.abs(gg - og) / dg))
     er = float(np.linalg.norm(grhs - orhs) / np.linalg.norm(orhs))
@@ -188,7 +191,9 @@ def test_pcg_c2_core_solve_vs_lapack(oracle, rt, x_c2, kind):
     assert np.array_equal(gidx, oidx)
     assert np.max(np.abs(gw - ow) / ow) < 1e-12
     G, b = _torch_normal_eq(shape, ranks, factors, x_c2, lam, gidx, gw)
+    b5 = rt.variant_count("k_vech_bucket5")
     gg, grhs = rt.kron_normal_eq(shape, ranks, factors, x_c2, lam, gidx, gw)
+    assert rt.variant_count("k_vech_bucket5") == b5 + 1  # the C2 bucket kernel at C2's density
     Gh, bh = G.cpu().numpy(), b.cpu().numpy()
     dg = np.sqrt(np.outer(np.diag(Gh), np.diag(Gh)))
     eg = float(np.max(np.abs(gg - Gh) / dg))

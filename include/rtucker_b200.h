@@ -43,6 +43,23 @@ unsigned long long rtucker_b200_variant_count(const char* name);
 rtucker_status rtucker_b200_tensor_create_device(const uint64_t* shape, uint32_t order,
                                                  const double* data_device,
                                                  rtucker_tensor** out);
+/* Planted synthetic tensor generated on the GPU (BASELINE configs; a large tensor never
+ * exists on the host): core and factors i.i.d. N(0,1), factor rows scaled by i.i.d.
+ * Pareto(pareto_alpha) weights when pareto_alpha > 0 (BASELINE config 3), X = the
+ * reconstruction plus i.i.d. N(0, sigma^2) noise on every entry with sigma = noise_level *
+ * ||X_planted||_F / sqrt(prod I_n). Counter-based SplitMix64 streams (one per role) and
+ * Box-Muller, so shard r of P (rows [r I1 / P, (r + 1) I1 / P) of mode 1; shard_count 0 or
+ * 1 = the whole tensor) is generated on its own and equals that slab of the unsharded
+ * tensor. Not the reference generator's stream (rtucker_tensor_generate is). The result is
+ * device-resident (no host mirror until rtucker_tensor_data asks for one). core_out
+ * (prod ranks) / factors_out (sum I_n R_n, full A_1) optional, host. */
+rtucker_status rtucker_b200_tensor_generate_device(const uint64_t* shape,
+                                                   const uint64_t* planted_ranks, uint32_t order,
+                                                   double noise_level, double pareto_alpha,
+                                                   uint64_t seed, uint32_t shard_rank,
+                                                   uint32_t shard_count, rtucker_tensor** out,
+                                                   double* core_out, double* factors_out);
+
 /* Device pointer of a tensor's resident copy (borrowed). */
 const double* rtucker_b200_tensor_device_data(const rtucker_tensor* t);
 

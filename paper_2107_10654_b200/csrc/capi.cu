@@ -718,6 +718,31 @@ rtucker_status rtucker_b200_tensor_create_device(const uint64_t* shape, uint32_t
   });
 }
 
+rtucker_status rtucker_b200_tensor_generate_device(const uint64_t* shape,
+                                                   const uint64_t* planted_ranks, uint32_t order,
+                                                   double noise_level, double pareto_alpha,
+                                                   uint64_t seed, uint32_t shard_rank,
+                                                   uint32_t shard_count, rtucker_tensor** out,
+                                                   double* core_out, double* factors_out) {
+  if (!shape || !planted_ranks || !out) return fail(RTUCKER_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    checked_volume(shape, order);
+    const uint32_t P = shard_count ? shard_count : 1;
+    if (shard_rank >= P || P > shape[0]) throw rtb::Error(1, "generate: bad shard");
+    std::vector<uint64_t> sh(shape, shape + order), rk(planted_ranks, planted_ranks + order);
+    auto t = std::make_unique<rtucker_tensor>();
+    t->shape = sh;
+    t->shape[0] = (uint64_t)(shard_rank + 1) * shape[0] / P - (uint64_t)shard_rank * shape[0] / P;
+    t->host_valid = false;
+    cudaStream_t st = rtb::current_stream();
+    t->dev.ensure(t->size() * 8, st);
+    rtb::generate_planted_device(sh, rk, noise_level, pareto_alpha, seed, shard_rank, P,
+                                 t->dev.as<double>(), core_out, factors_out);
+    t->dev_valid = true;
+    *out = t.release();
+  });
+}
+
 const double* rtucker_b200_tensor_device_data(const rtucker_tensor* t) {
   if (!t) return nullptr;
   try {

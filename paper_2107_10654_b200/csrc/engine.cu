@@ -1935,6 +1935,145 @@ void model_loss(const double* x_dev, const std::vector<uint64_t>& shape,
   e.loss_public(loss, rmse);
 }
 
+namespace {
+// stream constants of the device generator (documented in engine.h)
+constexpr uint64_t kGenCore = 0x243f6a8885a308d3ULL, kGenFactor = 0x13198a2e03707344ULL,
+                   kGenNoise = 0xa4093822299f31d0ULL, kGenPareto = 0x082efa98ec4e6c89ULL;
+
+// N(0,1) from stream outputs 2k, 2k + 1 (Box-Muller, cosine branch). Streams: core
+// seed ^ kGenCore; factor n sm_at(seed ^ kGenFactor, n) (hashed, so the modes' streams do not
+// overlap); Pareto weights of mode n sm_at(seed ^ kGenPareto, n); noise seed ^ kGenNoise at
+// the entry's global flat index.
+__device__ __forceinline__ double gen_normal(uint64_t stream, uint64_t k) {
+  double u1 = u64_to_unit(sm_at(stream, 2 * k));
+  const double u2 = u64_to_unit(sm_at(stream, 2 * k + 1));
+  if (u1 <= 0.0) u1 = 0x1.0p-53;
+  return sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925286766559 * u2);
+}
+
+__global__ void k_gen_normal(double* out, long long n, uint64_t stream, long long offset) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = gen_normal(stream, (uint64_t)(offset + e));
+}
+
+// factor rows scaled by Pareto(alpha) weights (1 - u)^(-1/alpha), one draw per row
+__global__ void k_gen_pareto_rows(double* a, int I, int R, uint64_t stream, double alpha) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= I) return;
+  const double u = u64_to_unit(sm_at(stream, (uint64_t)i));
+  const double wgt = pow(1.0 - u, -1.0 / alpha);
+  for (int r = 0; r < R; ++r) a[(size_t)i * R + r] *= wgt;
+}
+
+__global__ void k_gen_noise(double* x, long long n, uint64_t stream, long long offset,
+                            const double* sigma) {
+  const double sg = *sigma;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    x[e] += sg * gen_normal(stream, (uint64_t)(offset + e));
+}
+
+// sigma = level * sqrt(<G, Q> / total), Q = G x_n (A_n^T A_n) (so ||X||_F^2 = <G, Q>)
+__global__ void k_gen_sigma(const double* G, const double* Q, long long d, double level,
+                            double total, double* sigma) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < d; i += blockDim.x) s = fma(G[i], Q[i], s);
+  s = block_sum<1024>(s, red);
+  if (threadIdx.x == 0) *sigma = level * sqrt(fmax(s, 0.0) / total);
+}
+}  // namespace
+
+void generate_planted_device(const std::vector<uint64_t>& shape,
+                             const std::vector<uint64_t>& ranks, double noise_level,
+                             double pareto_alpha, uint64_t seed, uint32_t shard_rank,
+                             uint32_t shard_count, double* x_dev, double* core_host,
+                             double* factors_host) {
+  AlsOptions o = op_opts(0.0);
+  validate(shape, ranks, o);
+  if (shard_count == 0) shard_count = 1;
+  if (shard_rank >= shard_count || shard_count > shape[0])
+    throw Error(1, "generate: bad shard (rank >= count or more shards than rows)");
+  if (noise_level < 0.0) throw Error(1, "generate: noise level must be non-negative");
+  cudaStream_t st = current_stream();
+  const int N = (int)shape.size();
+  uint64_t d = 1, fe = 0;
+  std::vector<uint64_t> foff(N);
+  for (int n = 0; n < N; ++n) {
+    d *= ranks[n];
+    foff[n] = fe;
+    fe += shape[n] * ranks[n];
+  }
+  DevBuf core(d * 8, st), fac(fe * 8, st), sig(8, st);
+  const unsigned gb = (unsigned)std::min<uint64_t>(ceil_div<uint64_t>(std::max(d, fe), 256), 1024);
+  k_gen_normal<<<gb, 256, 0, st>>>(core.as<double>(), (long long)d, seed ^ kGenCore, 0);
+  RTB_LAUNCH_CHECK();
+  for (int n = 0; n < N; ++n) {
+    const uint64_t cnt = shape[n] * ranks[n];
+    k_gen_normal<<<(unsigned)std::min<uint64_t>(ceil_div<uint64_t>(cnt, 256), 1024), 256, 0, st>>>(
+        fac.as<double>() + foff[n], (long long)cnt, sm_at(seed ^ kGenFactor, (uint64_t)n), 0);
+    RTB_LAUNCH_CHECK();
+    if (pareto_alpha > 0.0) {
+      k_gen_pareto_rows<<<ceil_div((int)shape[n], 256), 256, 0, st>>>(
+          fac.as<double>() + foff[n], (int)shape[n], (int)ranks[n],
+          sm_at(seed ^ kGenPareto, (uint64_t)n), pareto_alpha);
+      RTB_LAUNCH_CHECK();
+    }
+  }
+  // ||X_planted||^2 = <G, G x_n (A_n^T A_n)> from the full factors (same on every shard)
+  {
+    DevBuf grams((size_t)N * 64 * 64 * 8, st), q0(d * 8, st), q1(d * 8, st);
+    const double* cur = core.as<double>();
+    double* qb[2] = {q0.as<double>(), q1.as<double>()};
+    std::vector<uint64_t> gd = ranks;
+    for (int n = 0; n < N; ++n) {
+      const int R = (int)ranks[n];
+      FactorSet fs{};
+      fs.order = 1;
+      fs.ptr[0] = fac.as<double>() + foff[n];
+      fs.rows[0] = (int)shape[n];
+      fs.cols[0] = R;
+      double* gn = grams.as<double>() + (size_t)n * 64 * 64;
+      k_factor_gram<<<dim3(R * R, 1), 256, 0, st>>>(fs, gn, R);
+      RTB_LAUNCH_CHECK();
+      ttm_generic(cur, (long long)prod(gd, 0, n), R, (long long)prod(gd, n + 1), gn, R, 1, R,
+                  qb[n & 1], st);
+      cur = qb[n & 1];
+    }
+    k_gen_sigma<<<1, 1024, 0, st>>>(core.as<double>(), cur, (long long)d, noise_level,
+                                    (double)prod(shape), sig.as<double>());
+    RTB_LAUNCH_CHECK();
+  }
+  // this shard's rows of mode 1: reconstruct with the slab of A_1, then the noise at the
+  // entries' global flat indices
+  const uint64_t I1 = shape[0], P = shard_count, r = shard_rank;
+  const uint64_t lo = r * I1 / P, hi = (r + 1) * I1 / P;
+  std::vector<uint64_t> lshape = shape;
+  lshape[0] = hi - lo;
+  {
+    std::vector<double> ch(d), fh(fe);
+    RTB_CUDA(cudaMemcpyAsync(ch.data(), core.p, d * 8, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaMemcpyAsync(fh.data(), fac.p, fe * 8, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaStreamSynchronize(st));
+    if (core_host) std::memcpy(core_host, ch.data(), d * 8);
+    if (factors_host) std::memcpy(factors_host, fh.data(), fe * 8);
+    // slab model: A_1 rows lo..hi
+    std::vector<double> fs(fh.begin() + (long long)(lo * ranks[0]),
+                           fh.begin() + (long long)(hi * ranks[0]));
+    fs.insert(fs.end(), fh.begin() + (long long)(I1 * ranks[0]), fh.end());
+    Engine e(x_dev, lshape, ranks, op_opts(0.0));
+    e.set_model(ch.data(), fs.data());
+    e.reconstruct(x_dev);
+  }
+  const long long ltot = (long long)prod(lshape);
+  const long long inner = (long long)(prod(shape) / I1);
+  k_gen_noise<<<(unsigned)std::min<long long>(ceil_div<long long>(ltot, 256), 8 * kNumSMs), 256, 0,
+                st>>>(x_dev, ltot, seed ^ kGenNoise, (long long)lo * inner, sig.as<double>());
+  RTB_LAUNCH_CHECK();
+  RTB_CUDA(cudaStreamSynchronize(st));
+}
+
 void model_reconstruct(const std::vector<uint64_t>& shape, const std::vector<uint64_t>& ranks,
                        const double* core, const double* factors, double* out_host) {
   validate(shape, ranks, op_opts(0.0));

@@ -161,6 +161,20 @@ void dense_sketched_ridge(const double* a, uint64_t n, uint64_t d, const double*
                           double delta, uint64_t s_override, uint64_t seed, double* x,
                           uint64_t* s_out, double* beta_out);
 
+// Planted synthetic tensor generated on the device (BASELINE configs; counter-based
+// SplitMix64 streams, so any shard of rows can be generated independently and a sharded
+// generation equals the unsharded one): core and factors i.i.d. N(0,1) (Box-Muller on the
+// stream pairs), factor rows optionally scaled by Pareto(alpha) weights (alpha > 0), X = the
+// reconstruction plus i.i.d. N(0, sigma^2) noise on every entry, sigma = noise_level
+// ||X_planted||_F / sqrt(prod I_n) (the norm from the model: <G, G x_n A_n^T A_n>).
+// Writes this shard's rows [r I1 / P, (r + 1) I1 / P) of mode 1 into x_dev; core_host /
+// factors_host (optional) receive the planted model.
+void generate_planted_device(const std::vector<uint64_t>& shape,
+                             const std::vector<uint64_t>& ranks, double noise_level,
+                             double pareto_alpha, uint64_t seed, uint32_t shard_rank,
+                             uint32_t shard_count, double* x_dev, double* core_host,
+                             double* factors_host);
+
 // True when at least one CUDA device is visible (cached).
 bool cuda_device_present();
 // H2D copy of n doubles on st, then a device-side finiteness scan; synchronises st and

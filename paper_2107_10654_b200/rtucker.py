@@ -126,6 +126,9 @@ def _load() -> C.CDLL:
         "rtucker_b200_variant_count": (C.c_ulonglong, [C.c_char_p]),
         "rtucker_b200_tensor_create_device": (S, [_u64p, C.c_uint32, _vp, C.POINTER(_vp)]),
         "rtucker_b200_tensor_device_data": (_vp, [_vp]),
+        "rtucker_b200_tensor_generate_device": (S, [_u64p, _u64p, C.c_uint32, C.c_double, C.c_double,
+                                                    C.c_uint64, C.c_uint32, C.c_uint32,
+                                                    C.POINTER(_vp), _f64p, _f64p]),
         "rtucker_b200_als_run_ex": (S, [_vp, _u64p, C.c_uint32, C.POINTER(AlsOptions),
                                         C.POINTER(AlsExt), C.POINTER(_vp)]),
         "rtucker_b200_session_create": (S, [_vp, _u64p, C.c_uint32, C.POINTER(AlsOptions),
@@ -264,6 +267,27 @@ class Tensor:
         _check(lib.rtucker_tensor_generate(_p(shape), _p(pr), len(shape), noise_fraction,
                                            noise_sigma, seed, C.byref(h), C.byref(ck)))
         return cls(h), ck.value
+
+    @classmethod
+    def generate_device(cls, shape, planted_ranks, noise_level, seed, pareto_alpha=0.0,
+                        shard=(0, 1), want_model=False):
+        """Planted tensor generated on the GPU (rtucker_b200_tensor_generate_device); with
+        want_model, also (core, factors) of the planted model."""
+        shape, pr = _u64(shape), _u64(planted_ranks)
+        h = _vp()
+        core = np.zeros(int(np.prod(pr))) if want_model else None
+        fac = np.zeros(int(np.sum(shape * pr))) if want_model else None
+        _check(lib.rtucker_b200_tensor_generate_device(_p(shape), _p(pr), len(shape),
+                                                       noise_level, pareto_alpha, seed, shard[0],
+                                                       shard[1], C.byref(h), _p(core), _p(fac)))
+        t = cls(h)
+        if not want_model:
+            return t
+        fs, off = [], 0
+        for i, r in zip(shape, pr):
+            fs.append(fac[off:off + int(i * r)].reshape(int(i), int(r)))
+            off += int(i * r)
+        return t, core.reshape(tuple(int(r) for r in pr)), fs
 
     @property
     def shape(self):

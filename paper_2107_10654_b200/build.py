@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "lib", "librtucker_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["k_small.cu", "k_ttm.cu", "k_draw.cu", "k_gram.cu", "k_chol.cu", "k_pcg.cu", "k_fsketch.cu", "k_c4.cu", "k_eig.cu", "k_hjsvd.cu", "toolkit.cu", "engine.cu",
+SOURCES = ["k_small.cu", "k_ttm.cu", "k_draw.cu", "k_gram.cu", "k_chol.cu", "k_pcg.cu", "k_fsketch.cu", "k_c4.cu", "k_eig.cu", "k_hjsvd.cu", "toolkit.cu", "verify.cu", "engine.cu",
            "capi.cu"]
 FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

@@ -670,11 +670,18 @@ rtucker_status rtucker_sketched_ridge(const double* a, uint64_t n, uint64_t d, c
 
 rtucker_status rtucker_verify_suite(const char* name, uint64_t seed, int* passed_out,
                                     char** json_report_out) {
-  (void)seed;
-  (void)json_report_out;
   if (!name || !passed_out) return fail(RTUCKER_ERR_INVALID_ARGUMENT, "null argument");
-  return fail(RTUCKER_ERR_UNKNOWN,
-              "rtucker_verify_suite: property suites are not part of the B200 build");
+  return guarded([&] {
+    // ref capi.cpp:364-403; the suites run against the GPU routines (verify.cu)
+    std::string json;
+    const bool ok = rtb::verify_suites(name, seed, json);
+    *passed_out = ok ? 1 : 0;
+    if (json_report_out) {
+      char* buf = new char[json.size() + 1];
+      std::memcpy(buf, json.c_str(), json.size() + 1);
+      *json_report_out = buf;
+    }
+  });
 }
 
 void rtucker_string_free(char* s) { delete[] s; }

@@ -175,6 +175,10 @@ void generate_planted_device(const std::vector<uint64_t>& shape,
                              uint32_t shard_count, double* x_dev, double* core_host,
                              double* factors_host);
 
+// Property suites of rtucker_verify_suite (verify.cu): name = leverage | kronecker |
+// missing | structural | all; JSON report; true when every check passed.
+bool verify_suites(const std::string& name, uint64_t seed, std::string& json);
+
 // True when at least one CUDA device is visible (cached).
 bool cuda_device_present();
 // H2D copy of n doubles on st, then a device-side finiteness scan; synchronises st and

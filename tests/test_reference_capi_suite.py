@@ -6,7 +6,7 @@ paper_2107_10654_b200/lib/librtucker_b200.so (binary: oracle/_ref/test_capi_b200
 built here, shipped prebuilt to the GPU box). Passing it is the drop-in claim:
 a consumer of the reference header links against us unchanged.
 
-Excluded: "verify suites" (rtucker_verify_suite is out of scope).
+All eight cases run, including "verify suites" (rtucker_verify_suite, verify.cu).
 """
 import os
 import subprocess
@@ -34,6 +34,6 @@ def test_reference_capi_host_cases():
 
 @pytest.mark.gpu
 def test_reference_capi_suite_on_gpu():
-    rc, out = _run("-tce=verify suites")
+    rc, out = _run()
     assert rc == 0, out
-    assert "7 run, 0 failed, 1 skipped" in out, out
+    assert "8 run, 0 failed" in out, out

@@ -497,9 +497,10 @@ def run_our_arm(args):
         fsk = {"sweeps_per_s": fs_steps / (f0.elapsed_time(f1) / 1e3), "steps": fs_steps,
                "factor_samples": S_FACTOR, "final_loss": fh[-1][2] if fh else None,
                "note": "perf mode (sketched factor updates, BASELINE configs[1] literally); "
-                       "not the reference's semantics. At C2 it is slower than the exact updates: "
-                       "those reuse T = X x3 A3 from the loss pass, while each sampled mode-1/2 "
-                       "fiber is a strided 512-value gather"}
+                       "not the reference's semantics. At C2 it stays slower than the exact "
+                       "updates: those reuse T = X x3 A3 from the loss pass, while every sketched "
+                       "mode pays a latency-bound scores + draw-decode chain (~0.1 ms); the fiber "
+                       "gathers read mode-n-last copies of X (contiguous, 1.05x useful bytes)"}
 
     # roofline of the dominant kernel: the largest single kernel of the step, which in
     # the ncu launch list of this command (profiles/r01_launches_bench_v6.txt) is

@@ -34,6 +34,21 @@ std::mutex g_stream_mu;
 std::map<int, cudaStream_t> g_default_streams;
 }  // namespace
 
+// per-device stream for parallel graph branches (Engine::fork); never destroyed
+cudaStream_t side_stream() {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  int dev = 0;
+  RTB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t s;
+  RTB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  streams[dev] = s;
+  return s;
+}
+
 cudaStream_t current_stream() {
   if (t_stream) return t_stream;
   int dev = 0;
@@ -708,6 +723,8 @@ class Engine {
     for (auto e : step_ev_)
       if (e) cudaEventDestroy(e);
     if (post_host_) cudaFreeHost(post_host_);
+    if (fork_ev_) cudaEventDestroy(fork_ev_);
+    if (join_ev_) cudaEventDestroy(join_ev_);
   }
 
   // Adds the elapsed times of the last sweep's step events (the stream has passed them).
@@ -951,6 +968,8 @@ class Engine {
     RTB_CUDA(cudaMemsetAsync(warm_dev_.p, 0, 4, st_));
     RTB_CUDA(cudaHostAlloc((void**)&post_host_, 8 * sizeof(int), cudaHostAllocDefault));
     for (int k = 0; k < 2 * (N_ + 1); ++k) RTB_CUDA(cudaEventCreate(&step_ev_[k]));
+    RTB_CUDA(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
+    RTB_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
     {
       int rk[8] = {0};
       for (int n = 0; n < N_; ++n) rk[n] = (int)ranks_[n];
@@ -1053,54 +1072,62 @@ class Engine {
   void update_factor(int n) {
     // mode 1 under sharding: this shard computes its own rows of A_1
     const int In = (n == 0) ? (int)nloc_ : (int)shape_[n], Rn = (int)ranks_[n];
-    std::vector<uint64_t> dims;
-    const double* Y = factor_projection(n, dims);
-    // M = Y_(n) G_(n)^T  (I_n x R_n)
-    double* M = (Y == tmp_a_.as<double>()) ? tmp_b_.as<double>() : tmp_a_.as<double>();
-    const long long O = (long long)prod(ranks_, 0, n);
-    const long long J = (long long)prod(ranks_, n + 1);
+    double* pv = pinv2_.as<double>();
+    // (KK^T + lambda I)^+ with KK^T = G_(n) (kron_{m!=n} A_m^T A_m) G_(n)^T does not depend on
+    // the projection of X (or T) below, so it runs on the side stream -- a parallel branch of
+    // the sweep's graph -- while the projection and M = Y_(n) G_(n)^T run on the main stream
     {
-      Scope sc(prof_, "contract");
-      contract_except(Y, core_.as<double>(), O, In, Rn, J, M, st_);
-    }
-    // KK^T = G_(n) (kron_{m!=n} A_m^T A_m) G_(n)^T: Q = G x_{m!=n} Gram_m
-    {
+      double* qb[2] = {scratch_q(0), scratch_q(1)};  // allocated in main-stream order
+      const cudaStream_t ss = fork();
       Scope sc(prof_, "small_linalg");
       std::vector<uint64_t> gd = ranks_;
       const double* cur = core_.as<double>();
-      double* qb[2] = {scratch_q(0), scratch_q(1)};
       int which = 0;
       for (int m = 0; m < N_; ++m) {
         if (m == n) continue;
         const int R = (int)ranks_[m];
         ttm_generic(cur, (long long)prod(gd, 0, m), R, (long long)prod(gd, m + 1), gram(m), R, 1, R,
-                    qb[which], st_);
+                    qb[which], ss);
         cur = qb[which];
         which ^= 1;
       }
+      const long long O = (long long)prod(ranks_, 0, n);
+      const long long J = (long long)prod(ranks_, n + 1);
       double* kk = pinv_.as<double>();
-      contract_except(core_.as<double>(), cur, O, Rn, Rn, J, kk, st_);
-      k_add_diag<<<ceil_div(Rn, 64), 64, 0, st_>>>(kk, Rn, opt_.lambda);
+      contract_except(core_.as<double>(), cur, O, Rn, Rn, J, kk, ss);
+      k_add_diag<<<ceil_div(Rn, 64), 64, 0, ss>>>(kk, Rn, opt_.lambda);
       RTB_LAUNCH_CHECK();
       // (KK^T + lambda I)^+ (ref linalg.cpp:8-26): warp Cholesky inverse; if a
       // pivot is below R*eps*max diag the eigen/pinv path (singular values =
       // |eigenvalues|, cutoff R*eps*sigma_max) takes over on the device.
-      double* pv = pinv2_.as<double>();
       int* okf = spd_ok_.as<int>();
       const int stride = std::max(eig_stride_, Rn * Rn);
       if (Rn <= 32) {
         spd_small(kk, ns_one(Rn), stride, (double)Rn * DBL_EPSILON, linv_.as<double>(), pv, okf,
-                  1, st_, Rn);
+                  1, ss, Rn);
         sym_eigen(kk, ns_one(Rn), Rn, stride, evals_.as<double>(), evecs_.as<double>(),
-                  eig_status_.as<int>(), 1, st_, okf);
-        k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one(Rn),
+                  eig_status_.as<int>(), 1, ss, okf);
+        k_sym_pinv<<<1, 256, 0, ss>>>(evals_.as<double>(), evecs_.as<double>(), ns_one(Rn),
                                        stride, pv, nullptr, okf);
       } else {
-        eigen_one(kk, Rn);
-        k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one(Rn),
+        eigen_one(kk, Rn, ss);
+        k_sym_pinv<<<1, 256, 0, ss>>>(evals_.as<double>(), evecs_.as<double>(), ns_one(Rn),
                                        stride, pv, nullptr, nullptr);
       }
       RTB_LAUNCH_CHECK();
+    }
+    std::vector<uint64_t> dims;
+    const double* Y = factor_projection(n, dims);
+    // M = Y_(n) G_(n)^T  (I_n x R_n)
+    double* M = (Y == tmp_a_.as<double>()) ? tmp_b_.as<double>() : tmp_a_.as<double>();
+    {
+      Scope sc(prof_, "contract");
+      contract_except(Y, core_.as<double>(), (long long)prod(ranks_, 0, n), In, Rn,
+                      (long long)prod(ranks_, n + 1), M, st_);
+    }
+    join();
+    {
+      Scope sc(prof_, "small_linalg");
       // A_n = M pinv
       const long long tot = (long long)In * Rn;
       if (n == 0 && sharded()) {
@@ -1121,6 +1148,28 @@ class Engine {
     if (n == N_ - 1) t_valid_ = false;
   }
 
+  // ---- side stream: independent work as a parallel branch (fork / join on events) ----
+  // Work on the side stream only launches kernels into buffers allocated beforehand on the
+  // main stream (every DevBuf is allocated and freed in main-stream order); the side stream
+  // itself is per device and lives as long as the process.
+  cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
+  bool forked_ = false;
+  // returns the stream for the branch: the side stream, or the main one when profiling
+  cudaStream_t fork() {
+    if (opt_.profile || !fork_ev_) return st_;
+    const cudaStream_t side = side_stream();
+    RTB_CUDA(cudaEventRecord(fork_ev_, st_));
+    RTB_CUDA(cudaStreamWaitEvent(side, fork_ev_, 0));
+    forked_ = true;
+    return side;
+  }
+  void join() {
+    if (!forked_) return;
+    RTB_CUDA(cudaEventRecord(join_ev_, side_stream()));
+    RTB_CUDA(cudaStreamWaitEvent(st_, join_ev_, 0));
+    forked_ = false;
+  }
+
   DevBuf qbuf_[2];
   double* scratch_q(int i) {
     qbuf_[i].ensure((std::max<uint64_t>(d_, (uint64_t)rmax_ * rmax_) + 1) * 8, st_);
@@ -1130,9 +1179,9 @@ class Engine {
   int* ns_one(int n) { return ns_vals_.as<int>() + n; }
 
   // eigen of one symmetric n x n matrix (device) into slot 0 of evals/evecs
-  void eigen_one(const double* m, int n) {
+  void eigen_one(const double* m, int n, cudaStream_t st = nullptr) {
     sym_eigen(m, ns_one(n), n, eig_stride_ > n * n ? eig_stride_ : n * n, evals_.as<double>(),
-              evecs_.as<double>(), eig_status_.as<int>(), 1, st_);
+              evecs_.as<double>(), eig_status_.as<int>(), 1, st ? st : st_);
   }
 
   // eigen of all factor Grams (batched)
@@ -1362,6 +1411,26 @@ class Engine {
     int rk[8];
     for (int n = 0; n < N_; ++n) rk[n] = (int)ranks_[n];
     last_s_ = s;
+    PcgSpec ps{};
+    double* prep = reinterpret_cast<double*>(pst_.as<int>() + 64);
+    if (pcg_path_) {
+      ps.order = N_;
+      for (int n = 0; n < N_; ++n) ps.ranks[n] = rk[n];
+      ps.d = (int)d_;
+      ps.lambda = opt_.lambda;
+      ps.pinv = pgram_.as<double>();  // (A_n^T A_n)^-1 from the score step's Cholesky
+      ps.linv_stride = eig_stride_;
+      ps.linv_ok = spd_ok_.as<int>();
+      ps.grams = grams_.as<double>();
+      // the Kronecker preconditioner depends on the factor Grams only: a parallel branch
+      // next to the sketched Gram build
+      const cudaStream_t ss = fork();
+      Scope sc(prof_, "pcg");
+      int* eskip = pst_.as<int>() + 32;
+      pcg_prepare(ps, prep, eskip, ss);
+      sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, pev_.as<double>(),
+                pvec_.as<double>(), pst_.as<int>(), N_, ss, eskip);
+    }
     normal_eq(s, !pcg_path_);
     if (!pcg_path_) {
       solve_fallback(s, false);
@@ -1373,20 +1442,7 @@ class Engine {
       Scope sc(prof_, "pcg");
       blocks_.ensure((size_t)gram_block_elems(gs) * 8, st_);
       gram_expand_blocks(gs, gram_work_.p, blocks_.as<double>(), st_);
-      PcgSpec ps{};
-      ps.order = N_;
-      for (int n = 0; n < N_; ++n) ps.ranks[n] = rk[n];
-      ps.d = (int)d_;
-      ps.lambda = opt_.lambda;
-      ps.pinv = pgram_.as<double>();  // (A_n^T A_n)^-1 from the score step's Cholesky
-      ps.linv_stride = eig_stride_;
-      ps.linv_ok = spd_ok_.as<int>();
-      ps.grams = grams_.as<double>();
-      double* prep = reinterpret_cast<double*>(pst_.as<int>() + 64);
-      int* eskip = pst_.as<int>() + 32;
-      pcg_prepare(ps, prep, eskip, st_);
-      sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, pev_.as<double>(),
-                pvec_.as<double>(), pst_.as<int>(), N_, st_, eskip);
+      join();
       ps.evals = pev_.as<double>();
       ps.evecs = pvec_.as<double>();
       ps.prep = prep;

@@ -1,0 +1,21 @@
+#!/bin/bash
+# Measurement artifacts of one code state (run under gpurun; TAG names the outputs):
+#   1. the default bench line (no profiler),
+#   2. the ncu launch list of a short bench run (per-launch device times, serialized),
+#   3. one ncu --set full capture of each top C2 kernel.
+# Each ncu pass runs only after the same command exited 0 without ncu.
+TAG=${1:-cur}
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+timeout 900 python bench.py --steps 20 --warmup 3 --no-extra > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+rc=$?; echo "bench rc=$rc" >> gpurun_out/bench_$TAG.err
+[ $rc -eq 0 ] || exit $rc
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extra \
+  > gpurun_out/ncu_launch_$TAG.log 2>&1
+echo "ncu launch rc=$?" >> gpurun_out/ncu_launch_$TAG.log
+timeout 1200 ncu --set full --clock-control none --import-source on \
+  -k "regex:^k_pcg$|k_ttm_last3|k_vech_bucket5|k_ttm_mid3|k_vech_contract2|k_fsk_accum3" -c 6 \
+  -o gpurun_out/full_$TAG python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extra \
+  > gpurun_out/ncu_full_$TAG.log 2>&1
+echo "ncu full rc=$?" >> gpurun_out/ncu_full_$TAG.log

@@ -480,7 +480,7 @@ def run_our_arm(args):
     # design width 256): the library's perf mode (ext.factor_samples; the reference has no
     # such update, so the headline keeps its exact factor updates). Timed the same way.
     fsk = None
-    if world == 1:
+    if world == 1 and not args.c2_only:
         fs_steps = min(args.steps, 50)
         opts_f = rt.options(lam=LAM, sketched_core=1, sample_count_override=S_CORE,
                             tolerance=0.0, max_iterations=args.warmup + fs_steps, seed=0)
@@ -580,7 +580,7 @@ def run_our_arm(args):
     # C1 head to head (BASELINE configs[0]): the same C-API job as the reference arm's, on
     # this library; plus the device-only C1 sweep rate (resident X, graph launches)
     c1 = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.c2_only:
         c1 = c1_head_to_head(rt.lib, rt.options(lam=C1_LAM, sketched_core=1, tolerance=0.0,
                                                 sample_count_override=C1_S,
                                                 max_iterations=C1_SWEEPS, seed=0), 20)
@@ -914,6 +914,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the BASELINE config 3 / 4 measurements of the default run")
+    ap.add_argument("--c2-only", action="store_true",
+                    help="only the C2 headline and its profiled re-run (for ncu launch lists): "
+                         "implies --no-extra, skips the C1 head-to-head and the perf-mode line")
     ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
                     help="c2 (default): the headline ALS sweep; c3: the BASELINE config-3 "
                          "4-way Pareto-factor sweep; c4: the BASELINE config-4 sampling + "
@@ -922,6 +925,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.c2_only:
+        args.no_extra = True
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.workload == "c4":

@@ -1154,6 +1154,7 @@ class Engine {
   // itself is per device and lives as long as the process.
   cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
   bool forked_ = false;
+  bool blocks_ready_ = false;  // the last normal_eq wrote blocks_ (fused contraction epilogue)
   // returns the stream for the branch: the side stream, or the main one when profiling
   cudaStream_t fork() {
     if (opt_.profile || !fork_ev_) return st_;
@@ -1440,8 +1441,10 @@ class Engine {
       // Kronecker-preconditioned CG on the blocked Gram (k_pcg.cu), verified by its
       // true residual; the Cholesky path (solve_fallback) takes over on failure
       Scope sc(prof_, "pcg");
-      blocks_.ensure((size_t)gram_block_elems(gs) * 8, st_);
-      gram_expand_blocks(gs, gram_work_.p, blocks_.as<double>(), st_);
+      if (!blocks_ready_) {
+        blocks_.ensure((size_t)gram_block_elems(gs) * 8, st_);
+        gram_expand_blocks(gs, gram_work_.p, blocks_.as<double>(), st_);
+      }
       join();
       ps.evals = pev_.as<double>();
       ps.evecs = pvec_.as<double>();
@@ -1493,10 +1496,18 @@ class Engine {
     const double* xg = x_ - (sharded() ? lo_ * (long long)(total_ / shape_[0]) : 0);
     Scope sc(prof_, "gram");
     if (full) G_.ensure(d_ * d_ * 8, st_);
+    // the PCG's last-mode blocks come out of the contraction itself when it can write them
+    // (one shard only: under sharding they follow the all-reduce of the compact Gram)
+    double* bl = nullptr;
+    if (!full && !sharded()) {
+      blocks_.ensure((size_t)gram_block_elems(gs) * 8, st_);
+      bl = blocks_.as<double>();
+    }
     // the full Gram is expanded after the shard sum of the compact one
-    sketch_normal_eq(gs, xg, (const unsigned long long*)sk_idx_.p, sk_w_.as<double>(),
-                     gram_work_.p, gram_work_.bytes, (full && !sharded()) ? G_.as<double>() : nullptr,
-                     rhs_.as<double>(), (unsigned long long*)data_draws_.p, st_);
+    blocks_ready_ = sketch_normal_eq(gs, xg, (const unsigned long long*)sk_idx_.p,
+                                     sk_w_.as<double>(), gram_work_.p, gram_work_.bytes,
+                                     (full && !sharded()) ? G_.as<double>() : nullptr,
+                                     rhs_.as<double>(), (unsigned long long*)data_draws_.p, st_, bl);
     if (sharded()) {
       size_t ns = 0;
       double* S = gram_compact(gs, gram_work_.p, &ns);

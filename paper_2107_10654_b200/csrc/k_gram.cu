@@ -127,6 +127,7 @@ struct GramLayout {
   double* vt3;    // [I3][160]
   int* border;    // [I1] compacted buckets, longest first (k_bucket_order)
   int* bcounter;  // [1] next bucket of the persistent k_vech_bucket3
+  double* vt1;    // [I1][160] mode-1 table per compacted bucket (k_vech_table1)
 };
 
 int key_bits(int I1) {
@@ -174,6 +175,7 @@ size_t carve(const GramSpec& spec, F&& take) {
   t((size_t)(spec.order >= 3 ? spec.rows[2] : 1) * 160 * 8);  // vt3
   t((size_t)I1 * 4);                           // border
   t(16);                                       // bcounter
+  t((size_t)I1 * 160 * 8);                     // vt1 (k_vech_table1)
   return total;
 }
 
@@ -207,6 +209,7 @@ GramLayout layout(const GramSpec& spec, void* base) {
       case 20: l.vt3 = (double*)q; break;
       case 21: l.border = (int*)q; break;
       case 22: l.bcounter = (int*)q; break;
+      case 23: l.vt1 = (double*)q; break;
     }
   });
   return l;
@@ -1307,6 +1310,169 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_contract2(GramSpec spe
   }
 }
 
+// Mode-1 table of every compacted bucket's i_1 (rows b < nbuckets, ld kC3Ldt): vech(a_1 a_1^T)
+// in columns [0, m_1) (zero to 144), the raw row a_1 in [144, 144 + R_1) (zero after) -- the A
+// operands of k_vech_contract3's Gram and rhs tiles, built once per core update.
+constexpr int kC3Ldt = 160, kC3Raw = 144;
+__global__ void k_vech_table1(const double* __restrict__ A, int R, const int* __restrict__ bi1,
+                              const int* __restrict__ nbuckets, double* __restrict__ out) {
+  const int b = blockIdx.x;
+  if (b >= *nbuckets) return;
+  const double* a = A + (size_t)__ldg(bi1 + b) * R;
+  const int m = R * (R + 1) / 2;
+  for (int u = threadIdx.x; u < kC3Ldt; u += blockDim.x) {
+    double val = 0.0;
+    if (u < m) {
+      int p, q;
+      pair_of(u, R, p, q);
+      val = __ldg(a + p) * __ldg(a + q);
+    } else if (u >= kC3Raw && u < kC3Raw + R) {
+      val = __ldg(a + u - kC3Raw);
+    }
+    out[(size_t)b * kC3Ldt + u] = val;
+  }
+}
+
+// (C'') + (E), warp-specialised: S = V1^T H and rhs = A1_b^T h in one launch. A Gram CTA
+// owns all m_1 (<= 136) rows x 128 columns of S (one wave at C2: 145 CTAs); an rhs CTA owns
+// the R_1 (<= 16) rows x 128 columns of rhs (R_1 x d'), the same loop with the raw-row columns
+// of the table as A and h as B. K = buckets in chunks of 32: a producer warp stages each
+// chunk -- 32 row segments of H (or h) and 32 table rows -- by TMA bulk copies into a
+// 3-deep ring (full / empty mbarriers); consumer warps own one 8-row tile x 16 column tiles
+// each (17 fragment loads per 16 DMMAs). No generation, no CTA-wide barrier in the K loop.
+// With `blocks` (order 3) the epilogue also writes S in the PCG's last-mode block layout
+// (k_vech_blocks' output: B[u_1][u_2][p][q] = S[u_1][u_2 m_3 + vech(p, q)]).
+constexpr int kC3N = 128, kC3K = 32, kC3St = 3;
+constexpr int kC3Ldh = kC3N + 4, kC3Ldv = kC3Ldt + 4;  // conflict-free fragment loads
+constexpr int kC3Mma = 17;
+constexpr int kC3Threads = (kC3Mma + 1) * 32;
+size_t vech_contract3_smem() { return (size_t)kC3St * kC3K * (kC3Ldh + kC3Ldv) * 8; }
+__global__ void __launch_bounds__(kC3Threads, 1) k_vech_contract3(
+    VechSpec v, const double* __restrict__ H, const double* __restrict__ V1,
+    const int* __restrict__ nbuckets, double* __restrict__ S, const double* __restrict__ h,
+    int dprime, double* __restrict__ rhs, double* __restrict__ blocks) {
+  extern __shared__ __align__(16) double smc3[];
+  double* hs = smc3;                          // [St][K][Ldh]
+  double* vs = hs + kC3St * kC3K * kC3Ldh;    // [St][K][Ldv]
+  __shared__ __align__(8) unsigned long long full[kC3St], empty[kC3St];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gram_ctas = (int)((v.Hsz + kC3N - 1) / kC3N);
+  const bool is_rhs = (int)blockIdx.x >= gram_ctas;
+  const int rows = is_rhs ? v.R[0] : v.m[0], MT = (rows + 7) / 8;
+  const int acol = is_rhs ? kC3Raw : 0;
+  const long long ld = is_rhs ? dprime : v.Hsz;
+  const double* B = is_rhs ? h : H;
+  const long long n0 = (long long)(is_rhs ? (int)blockIdx.x - gram_ctas : (int)blockIdx.x) * kC3N;
+  const int ncols = (int)(ld - n0 < kC3N ? ld - n0 : kC3N);
+  const int nb = *nbuckets;
+  const int nch = (nb + kC3K - 1) / kC3K;
+  if (tid == 0) {
+    for (int i = 0; i < kC3St; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], MT);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kC3Mma) {
+    // ---------------- producer ----------------
+    const unsigned hbytes = (unsigned)ncols * 8u;
+    for (int ch = 0; ch < nch; ++ch) {
+      const int sb = ch % kC3St;
+      if (ch >= kC3St) mbar_wait(&empty[sb], ((ch / kC3St) - 1) & 1);
+      const int k = ch * kC3K + lane;
+      double* hrow = hs + (sb * kC3K + lane) * kC3Ldh;
+      double* vrow = vs + (sb * kC3K + lane) * kC3Ldv;
+      const bool ok = k < nb;
+      if (!ok) {  // past the last bucket: zero rows (finite products with the zero V rows)
+        for (int c = 0; c < kC3N; ++c) hrow[c] = 0.0;
+        for (int c = 0; c < kC3Ldt; ++c) vrow[c] = 0.0;
+      }
+      const int kn = min(kC3K, nb - ch * kC3K);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&full[sb], (hbytes + kC3Ldt * 8u) * (unsigned)kn);
+      __syncwarp();
+      if (ok) {
+        bulk_g2s(hrow, B + (size_t)k * ld + n0, hbytes, &full[sb]);
+        bulk_g2s(vrow, V1 + (size_t)k * kC3Ldt, kC3Ldt * 8u, &full[sb]);
+      }
+    }
+    return;
+  }
+  if (warp >= MT) return;
+  // ---------------- consumers ----------------
+  const int g = lane >> 2, t4 = lane & 3;
+  double acc[16][2];
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int sb = ch % kC3St;
+    mbar_wait(&full[sb], (ch / kC3St) & 1);
+    const double* hb = hs + sb * kC3K * kC3Ldh + g;
+    const double* vb = vs + sb * kC3K * kC3Ldv + acol + warp * 8 + g;
+    const int ksn = (min(kC3K, nb - ch * kC3K) + 3) >> 2;
+    for (int ks = 0; ks < ksn; ++ks) {
+      const int k = ks * 4 + t4;
+      const double af = vb[k * kC3Ldv];
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) dmma_8x8x4(acc[nt][0], acc[nt][1], af, hb[k * kC3Ldh + nt * 8]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sb]);
+  }
+  const int uu = warp * 8 + g;
+  if (is_rhs) {
+    if (uu >= rows) return;
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      const int c = nt * 8 + 2 * t4;
+      if (c < ncols) rhs[(size_t)uu * dprime + n0 + c] = acc[nt][0];
+      if (c + 1 < ncols) rhs[(size_t)uu * dprime + n0 + c + 1] = acc[nt][1];
+    }
+    return;
+  }
+  // epilogue through shared memory (the ring is free: every chunk was consumed): the tile
+  // (rows x 128) is staged, then S rows and the PCG blocks are written coalesced
+  asm volatile("bar.sync 1, %0;" ::"r"(MT * 32) : "memory");
+  double* T = smc3;  // [rows][kC3Ldh]
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    T[uu * kC3Ldh + nt * 8 + 2 * t4] = acc[nt][0];
+    T[uu * kC3Ldh + nt * 8 + 2 * t4 + 1] = acc[nt][1];
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(MT * 32) : "memory");
+  const int nth = MT * 32;
+  for (int i = tid; i < rows * ncols; i += nth) {
+    const int r = i / ncols, c = i - r * ncols;
+    S[(size_t)r * v.Hsz + n0 + c] = T[r * kC3Ldh + c];
+  }
+  if (!blocks) return;
+  // column c of the tile is U = n0 + c = (u_2, vech(p, q)): entries (p, q) and (q, p) of block
+  // (u_1, u_2); the map is built once per CTA, then every thread writes tile entries
+  const int m3 = (int)v.Ncol, R3 = v.R[2], RR = R3 * R3;
+  __shared__ int cmap[3][kC3N];
+  asm volatile("bar.sync 1, %0;" ::"r"(MT * 32) : "memory");
+  for (int c = tid; c < ncols; c += nth) {
+    const long long U = n0 + c;
+    const int u2 = (int)(U / m3);
+    int p, q;
+    pair_of((int)(U - (long long)u2 * m3), R3, p, q);
+    cmap[0][c] = u2 * RR;
+    cmap[1][c] = p * R3 + q;
+    cmap[2][c] = q * R3 + p;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(MT * 32) : "memory");
+  for (int i = tid; i < rows * kC3N; i += nth) {
+    const int r = i / kC3N, c = i % kC3N;
+    if (c >= ncols) continue;
+    const double val = T[r * kC3Ldh + c];
+    double* bb = blocks + (size_t)r * v.m[1] * RR + cmap[0][c];
+    bb[cmap[1][c]] = val;
+    bb[cmap[2][c]] = val;
+  }
+}
+
 // (D) full Gram from S plus the augmented diagonal.
 __global__ void k_vech_expand(GramSpec spec, VechSpec v, const double* __restrict__ S,
                               const int* __restrict__ aug_count, double aug_term,
@@ -1590,15 +1756,15 @@ void sketch_normal_eq_m4(const GramSpec& spec, const double* x, const unsigned l
 
 }  // namespace
 
-void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long long* idx,
+bool sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long long* idx,
                       const double* w, void* work, size_t work_bytes, double* gram, double* rhs,
-                      unsigned long long* data_draws_dev, cudaStream_t st) {
+                      unsigned long long* data_draws_dev, cudaStream_t st, double* blocks) {
   if (work_bytes < gram_work_bytes(spec)) throw Error(4, "sketch_normal_eq: workspace too small");
   const VechSpec v = make_vech(spec);
   if (v.rowlen > kMaxRow) throw Error(4, "sketch_normal_eq: sum of ranks beyond mode 1 > 256");
   if (merged4_ok(spec)) {
     sketch_normal_eq_m4(spec, x, idx, w, work, gram, rhs, data_draws_dev, st);
-    return;
+    return false;
   }
   GramLayout l = layout(spec, work);
   bucket_stage(spec, v, l, x, idx, w, data_draws_dev, st);
@@ -1618,7 +1784,26 @@ void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
     }
   }
   const int I1 = spec.rows[0];
-  if ((v.m[0] + 7) / 8 <= kBWarps) {
+  static const bool no_c3 = std::getenv("RTB_NO_CONTRACT3") != nullptr;
+  bool rhs_done = false, blocks_done = false;
+  if (!no_c3 && v.m[0] <= 8 * kC3Mma && (v.Hsz & 1) == 0 && v.Hsz >= 16 * kC3N) {
+    k_vech_table1<<<I1, 160, 0, st>>>(spec.factors[0], v.R[0], l.bi1, l.nbuckets, l.vt1);
+    RTB_LAUNCH_CHECK();
+    const size_t smc = vech_contract3_smem();
+    set_max_smem(k_vech_contract3, (int)smc);
+    // rhs tiles in the same launch when a_1 fits the table's raw-row columns
+    static const bool no_rhs = std::getenv("RTB_C3_NORHS") != nullptr;  // experiments
+    static const bool no_blk = std::getenv("RTB_C3_NOBLK") != nullptr;
+    const bool fuse_rhs = !no_rhs && v.R[0] <= kC3Ldt - kC3Raw && (spec.dprime & 1) == 0;
+    const unsigned gram_ctas = (unsigned)((v.Hsz + kC3N - 1) / kC3N);
+    const unsigned rhs_ctas = fuse_rhs ? (unsigned)ceil_div(spec.dprime, kC3N) : 0u;
+    double* bl = (blocks && v.N == 3 && !no_blk) ? blocks : nullptr;
+    k_vech_contract3<<<gram_ctas + rhs_ctas, kC3Threads, smc, st>>>(
+        v, l.H, l.vt1, l.nbuckets, l.S, l.h, spec.dprime, fuse_rhs ? rhs : nullptr, bl);
+    count_variant("k_vech_contract3");
+    rhs_done = fuse_rhs;
+    blocks_done = bl != nullptr;
+  } else if ((v.m[0] + 7) / 8 <= kBWarps) {
     const size_t smc = (size_t)(2 * KCC * LDH2 + 2 * KCC * LDZ) * 8;
     set_max_smem(k_vech_contract2, (int)smc);
     k_vech_contract2<<<(unsigned)((v.Hsz + TNC2 - 1) / TNC2), kBWarps * 32, smc, st>>>(
@@ -1634,11 +1819,14 @@ void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
     k_vech_expand<<<kNumSMs * 8, 256, 0, st>>>(spec, v, l.S, l.aug_count, aug_term, gram);
     RTB_LAUNCH_CHECK();
   }
-  k_rhs_part<<<dim3(ceil_div(spec.d, 256), kRhsSplit), 256, 0, st>>>(spec, l.h, l.bi1,
-                                                                      l.nbuckets, l.rhs_part);
-  RTB_LAUNCH_CHECK();
-  k_rhs_sum<<<ceil_div(spec.d, 256), 256, 0, st>>>(spec.d, l.rhs_part, rhs);
-  RTB_LAUNCH_CHECK();
+  if (!rhs_done) {
+    k_rhs_part<<<dim3(ceil_div(spec.d, 256), kRhsSplit), 256, 0, st>>>(spec, l.h, l.bi1,
+                                                                        l.nbuckets, l.rhs_part);
+    RTB_LAUNCH_CHECK();
+    k_rhs_sum<<<ceil_div(spec.d, 256), 256, 0, st>>>(spec.d, l.rhs_part, rhs);
+    RTB_LAUNCH_CHECK();
+  }
+  return blocks_done;
 }
 
 void gram_expand_full(const GramSpec& spec, void* work, double* gram, cudaStream_t st) {

@@ -164,10 +164,12 @@ size_t gram_work_bytes(const GramSpec& spec);
 // the compact (vech) Gram S [m_1][Hsz] inside the workspace (sum it across shards)
 double* gram_compact(const GramSpec& spec, void* work, size_t* count);
 // Sketched normal equations from (idx, w): rhs, the compact (vech) Gram in the
-// workspace and, if gram != nullptr, the full d x d Gram.
-void sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long long* idx,
+// workspace and, if gram != nullptr, the full d x d Gram. With blocks != nullptr the last-mode
+// blocks (gram_expand_blocks' output) may be written by the same pass: returns true if so.
+bool sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long long* idx,
                       const double* w, void* work, size_t work_bytes, double* gram,
-                      double* rhs, unsigned long long* data_draws_dev, cudaStream_t st);
+                      double* rhs, unsigned long long* data_draws_dev, cudaStream_t st,
+                      double* blocks = nullptr);
 
 // augmented-row draw counts [d] inside a gram workspace (valid after sketch_normal_eq)
 const int* gram_aug_counts(const GramSpec& spec, void* work);

@@ -9,7 +9,7 @@ torch cuBLAS) where it does not (the reference's Jacobi SVD at d = 4096 takes ho
     k_ttm_last3 (T = X x_3 A_3^T), all modes, vs orc_update_factor   (ref tucker.cpp:70-89)
   * the fused loss pass (k_ttm_last3<FUSED>) vs orc_tucker_loss       (ref tucker.cpp:216-229)
   * rung 3 at d = 4096: the sketched Gram/RHS built by k_vech_bucket5 +
-    k_vech_contract2 from the oracle's own draws vs orc_kron_sketch_normal_eq
+    k_vech_contract3 from the oracle's own draws vs orc_kron_sketch_normal_eq
                                                                       (ref sketch_ridge.cpp:105-128)
   * the PCG fast path k_pcg<16,16> (the C2 core solve) vs a LAPACK solve of the same
     sketched system                                                   (ref sketch_ridge.cpp:130-139)
@@ -124,17 +124,17 @@ def _oracle_draws(oracle, shape, ranks, factors, seed, s):
 def test_normal_equations_d4096_from_oracle_sketch(oracle, rt, x_c2, i1, kernel):
     """Rung 3 at d = 4096, R = 16 (the C2 Gram kernels: k_vech_bucket5 for C2's ~390 draws per
     i_1 bucket, here 32 buckets of ~60 data draws; k_vech_bucket2<17> for short buckets;
-    k_vech_contract2, k_vech_blocks), the draws made by the oracle's sampler, the Gram/RHS by
+    k_vech_table1 + k_vech_contract3, k_vech_blocks), the draws made by the oracle's sampler, the Gram/RHS by
     the oracle's restatement of the reference's row-by-row stream."""
     x = np.ascontiguousarray(x_c2[:i1])
     shape, ranks, lam, s = x.shape, (16, 16, 16), 1e-2, 4000
     core, factors = model(oracle, shape, ranks, "uniform", 9)
     idx, w = _oracle_draws(oracle, shape, ranks, factors, 2024, s)
     b17 = rt.variant_count(kernel)
-    c2 = rt.variant_count("k_vech_contract2")
+    c3 = rt.variant_count("k_vech_contract3")
     gg, grhs = rt.kron_normal_eq(shape, ranks, factors, x, lam, idx, w)
     assert rt.variant_count(kernel) == b17 + 1
-    assert rt.variant_count("k_vech_contract2") == c2 + 1
+    assert rt.variant_count("k_vech_contract3") == c3 + 1
     og, orhs = oracle.kron_normal_eq(shape, ranks, factors, x, lam, idx, w)
     dg = np.sqrt(np.outer(np.diag(og), np.diag(og)))
     eg = float(np.max(np.abs(gg - og) / dg))

@@ -174,6 +174,12 @@ constexpr int kStages2 = 3;
 #endif
 constexpr int kL3BK = RTB_L3BK;     // k_ttm_last3 chunk width (columns per barrier)
 constexpr int kL3Stages = RTB_L3ST; // k_ttm_last3 ring depth
+#ifndef RTB_L4BK
+#define RTB_L4BK 32
+#define RTB_L4ST 4
+#endif
+constexpr int kL4BK = RTB_L4BK;     // k_ttm_last4 chunk width
+constexpr int kL4Stages = RTB_L4ST; // k_ttm_last4 ring depth
 constexpr int BM2 = 128;
 template <int RP>
 constexpr int lda2() { return RP + 4; }
@@ -974,6 +980,163 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last3(const double* __restrict__
   }
 }
 
+// k_ttm_last3 without CTA-wide barriers: the X ring is filled by TMA bulk row copies and
+// handed over by mbarriers. T warp w (rows 16 w .. 16 w + 15 of the row block) also stages
+// those 16 rows of every chunk: before computing item q it refills the slot of item q - 1
+// (freed when all 16 warps arrived on that slot's `empty` barrier) with item q + ST - 1,
+// each of its lanes 0-15 copying one row segment onto the slot's `full` barrier (8 arrivals
+// + transaction bytes). Residual warp w + 8 reads the same rows. The warps of a CTA drift by
+// up to ST - 1 chunks, so the DMMA pipe is not drained at every chunk boundary.
+template <bool FUSED, int BK, int ST>
+__global__ void __launch_bounds__(512, 1) k_ttm_last4(const double* __restrict__ X, long long O,
+                                                      int I, const double* __restrict__ A, int R,
+                                                      double* __restrict__ T,
+                                                      const double* __restrict__ P,
+                                                      double* __restrict__ partial,
+                                                      const int* __restrict__ need) {
+  RTB_GUARD()
+  constexpr int RP = 16;
+  constexpr int LD = BK + kPadX;
+  constexpr int LDA = RP + 4;
+  constexpr int ROWS = 16;  // rows per warp (m16)
+  extern __shared__ __align__(16) double sm4[];
+  const int Ip = ceil_div(I, BK) * BK;
+  double* as = sm4;                        // [Ip][LDA]
+  double* xs = as + (size_t)Ip * LDA;      // [ST][BM2][LD]
+  __shared__ double red[32];
+  __shared__ __align__(8) unsigned long long full[ST], empty[ST];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const bool rwarp = FUSED && warp >= 8;
+  const int wrow = warp & 7;
+  const bool idle = !FUSED && warp >= 8;
+  const long long nrb = ceil_div<long long>(O, BM2);
+  const int nchunks = ceil_div(I, BK);
+  for (int e = tid; e < Ip * LDA; e += 512) {
+    const int i = e / LDA, r = e - i * LDA;
+    as[e] = (i < I && r < R) ? A[(size_t)i * R + r] : 0.0;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 8);
+      mbar_init(&empty[i], FUSED ? 16 : 8);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const long long my_blocks = blockIdx.x < nrb ? (nrb - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long nitems = my_blocks * nchunks;
+  // T warp: stage its 16 rows of item q into slot q % ST
+  auto stage_rows = [&](long long q) {
+    const int slot = (int)(q % ST);
+    const long long rb = blockIdx.x + (q / nchunks) * gridDim.x;
+    const int c = (int)(q % nchunks);
+    const long long o = rb * BM2 + wrow * ROWS + lane;
+    const int i0 = c * BK;
+    const int cols = min(BK, I - i0);
+    const long long rem = O - (rb * BM2 + wrow * ROWS);
+    const int rows_ok = rem < ROWS ? (rem > 0 ? (int)rem : 0) : ROWS;
+    double* dst = xs + ((size_t)slot * BM2 + wrow * ROWS + lane) * LD;
+    if (lane < ROWS) {  // zero what the copies do not cover (row / column tails)
+      if (lane >= rows_ok) {
+        for (int k = 0; k < BK; ++k) dst[k] = 0.0;
+      } else {
+        for (int k = cols; k < BK; ++k) dst[k] = 0.0;
+      }
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0)
+      mbar_arrive_expect_tx(&full[slot], (unsigned)rows_ok * cols * 8u);
+    __syncwarp();
+    if (lane < rows_ok) bulk_g2s(dst, X + o * I + i0, (unsigned)cols * 8u, &full[slot]);
+  };
+  if (!rwarp && !idle) {
+    for (long long q = 0; q < ST - 1 && q < nitems; ++q) stage_rows(q);
+  }
+  double acc[2][4];
+  double pa[8];
+  double resid0 = 0.0, resid1 = 0.0;
+  for (long long q = 0; q < nitems; ++q) {
+    const int c = (int)(q % nchunks);
+    const long long rb = blockIdx.x + (q / nchunks) * gridDim.x;
+    const long long o0 = rb * BM2 + wrow * ROWS;
+    if (idle) continue;
+    if (!rwarp && q + ST - 1 < nitems) {
+      const long long qn = q + ST - 1;
+      if (qn >= ST) mbar_wait(&empty[qn % ST], (unsigned)(((qn / ST) - 1) & 1));
+      stage_rows(qn);
+    }
+    if (c == 0) {
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[n][v] = 0.0;
+      if (rwarp) {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const long long o = o0 + g + 8 * (v & 1);
+          const int k = t + 4 * (v >> 1);
+          pa[v] = (o < O && k < R) ? P[o * R + k] : 0.0;
+        }
+      }
+    }
+    const int slot = (int)(q % ST);
+    mbar_wait(&full[slot], (unsigned)((q / ST) & 1));
+    const double* xt = xs + (size_t)slot * BM2 * LD + wrow * ROWS * LD;
+    const int i0 = c * BK;
+    if (!rwarp) {
+#pragma unroll
+      for (int kb = 0; kb < BK; kb += 16) {
+        double a[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) a[v] = xt[(g + 8 * (v & 1)) * LD + kb + t + 4 * (v >> 1)];
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          double b[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) b[v] = as[(size_t)(i0 + kb + t + 4 * v) * LDA + n * 8 + g];
+          dmma_16x8x16(acc[n], a, b);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (c == nchunks - 1) {
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const long long o = o0 + g + 8 * (v >> 1);
+            const int r = n * 8 + 2 * t + (v & 1);
+            if (o < O && r < R) T[o * R + r] = acc[n][v];
+          }
+      }
+    } else {
+#pragma unroll
+      for (int nb = 0; nb < BK; nb += 8) {
+        double b[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) b[v] = as[(size_t)(i0 + nb + g) * LDA + t + 4 * v];
+        double cx[4] = {0.0, 0.0, 0.0, 0.0};
+        dmma_16x8x16(cx, pa, b);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double2 xv = *reinterpret_cast<const double2*>(xt + (g + 8 * h) * LD + nb + 2 * t);
+          const double d0 = xv.x - cx[2 * h], d1 = xv.y - cx[2 * h + 1];
+          resid0 = fma(d0, d0, resid0);  // zero-filled tails contribute exactly 0
+          resid1 = fma(d1, d1, resid1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+  }
+  if (FUSED) {
+    const double s = block_sum<512>(resid0 + resid1, red);
+    if (tid == 0) partial[blockIdx.x] = s;
+  }
+}
+
 static int sm_count() {
   static int n = [] {
     int dev = 0, v = 0;
@@ -1023,6 +1186,19 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
   if (R > 32) throw Error(4, "ttm_last: rank > 32 not supported by the DMMA path");
   const size_t ip3 = (size_t)ceil_div(I, kL3BK) * kL3BK;
   const size_t smem3 = (ip3 * lda2<16>() + (size_t)kL3Stages * BM2 * (kL3BK + kPadX)) * 8;
+  static const bool no_l4 = std::getenv("RTB_NO_LAST4") != nullptr;
+  const size_t smem4 = (ip3 * lda2<16>() + (size_t)kL4Stages * BM2 * (kL4BK + kPadX)) * 8;
+  if (!no_l4 && R <= 16 && (I % 2) == 0 && I % kL4BK == 0 && smem4 <= 227 * 1024 - 1024) {
+    auto k = fused ? k_ttm_last4<true, kL4BK, kL4Stages> : k_ttm_last4<false, kL4BK, kL4Stages>;
+    set_max_smem(k, (int)smem4);
+    const long long nrb = ceil_div<long long>(O, BM2);
+    const int grid = (int)std::min<long long>(nrb, sm_count());
+    k<<<grid, 512, smem4, st>>>(X, O, I, A, R, T, P, partial, g_need);
+    RTB_LAUNCH_CHECK();
+    count_variant(fused ? "k_ttm_last3_fused" : "k_ttm_last3");
+    count_variant(fused ? "k_ttm_last4_fused" : "k_ttm_last4");
+    return;
+  }
   if (R <= 16 && (I % 2) == 0 && smem3 <= 227 * 1024 - 1024) {
     const size_t smem = smem3;
     auto k = fused ? k_ttm_last3<true, kL3BK, kL3Stages> : k_ttm_last3<false, kL3BK, kL3Stages>;

@@ -154,6 +154,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// 2-D tensor-map TMA load (cp.async.bulk.tensor): box at (c0 innermost, c1) -> smem, completing
+// on `bar`; `map` is the address of a __grid_constant__ CUtensorMap kernel parameter
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* map, int c0, int c1,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
 // this thread's prior cp.async copies arrive on `bar` when they complete (counts
 // as one of the barrier's expected arrivals)
 __device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* bar) {

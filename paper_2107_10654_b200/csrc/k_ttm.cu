@@ -20,6 +20,9 @@
 #include <cstdlib>
 #include "kernels.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 namespace rtb {
 
 namespace {
@@ -1137,6 +1140,200 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last4(const double* __restrict__
   }
 }
 
+// The last-mode pass with the X tiles moved by tensor-map TMA. A stage is one 128-row x 32-
+// column chunk of X as two 128 x 16 boxes (128 B rows, SWIZZLE_128B: the 16-byte chunk j of
+// row r sits at chunk j ^ (r & 7)); out-of-range rows / columns arrive zero-filled. One thread
+// issues both boxes of a stage (full barrier: 1 arrival + 32 KB); the 16 warps release a
+// stage on its `empty` barrier. Conflict-free fragment reads of the swizzled tile come from
+// two free relabellings, applied consistently to every operand:
+//  * the k16 reduction order of the T GEMM: fragment slot kappa = t + 4 vh reads X column
+//    pi(kappa) = (t & 1) + 2 vh + 8 (t >> 1) of the 16-column half, and the A_3 rows are
+//    staged in the same order (smem row kappa holds A_3 row pi(kappa)), so the B fragments and
+//    the residual GEMM's columns (A_3 rows) keep their plain addressing;
+//  * the rows of a warp's 16-row tile: MMA row m reads X row rho(m) = (m & 8) | s(m & 7),
+//    s = swap of bits 0 and 1, for the T output rows, the P rows and the residual alike.
+__device__ __forceinline__ int l5_rho(int m) {
+  return (m & 12) | ((m & 1) << 1) | ((m >> 1) & 1);
+}
+template <bool FUSED, int ST>
+__global__ void __launch_bounds__(512, 1) k_ttm_last5(const __grid_constant__ CUtensorMap xmap,
+                                                      long long O, int I,
+                                                      const double* __restrict__ A, int R,
+                                                      double* __restrict__ T,
+                                                      const double* __restrict__ P,
+                                                      double* __restrict__ partial,
+                                                      const int* __restrict__ need) {
+  RTB_GUARD()
+  constexpr int BK = 32;
+  constexpr int LDA = 20;
+  constexpr int ROWS = 16;
+  constexpr int kHalf = BM2 * 16;  // doubles per 128 x 16 box
+  extern __shared__ __align__(1024) double sm5[];
+  // the dynamic smem base is 16-byte aligned only: round up to the 1 KB swizzle atom
+  double* xs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sm5) + 1023) & ~uintptr_t(1023));
+  double* as = xs + (size_t)ST * 2 * kHalf;  // [Ip][LDA], rows in pi order per 16-block
+  __shared__ double red[32];
+  __shared__ __align__(8) unsigned long long full[ST], empty[ST];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const bool rwarp = FUSED && warp >= 8;
+  const int wrow = warp & 7;
+  const bool idle = !FUSED && warp >= 8;
+  const long long nrb = ceil_div<long long>(O, BM2);
+  const int nchunks = ceil_div(I, BK);
+  const int Ip = nchunks * BK;
+  for (int e = tid; e < Ip * LDA; e += 512) {
+    const int i = e / LDA, r = e - i * LDA;
+    const int kap = i & 15;
+    const int src = (i & ~15) | ((kap & 1) + 2 * (kap >> 2) + 8 * ((kap >> 1) & 1));
+    as[e] = (src < I && r < R) ? A[(size_t)src * R + r] : 0.0;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], FUSED ? 16 : 8);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const long long my_blocks = blockIdx.x < nrb ? (nrb - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long nitems = my_blocks * nchunks;
+  const bool producer = tid == 0;
+  auto issue = [&](long long q) {
+    const int slot = (int)(q % ST);
+    const long long rb = blockIdx.x + (q / nchunks) * gridDim.x;
+    const int c = (int)(q % nchunks);
+    double* dst = xs + (size_t)slot * 2 * kHalf;
+    mbar_arrive_expect_tx(&full[slot], 2u * kHalf * 8u);
+    tma_load_2d(dst, &xmap, c * BK, (int)(rb * BM2), &full[slot]);
+    tma_load_2d(dst + kHalf, &xmap, c * BK + 16, (int)(rb * BM2), &full[slot]);
+  };
+  if (producer)
+    for (long long q = 0; q < ST - 1 && q < nitems; ++q) issue(q);
+  // this lane's tile rows (rho of MMA rows g and g + 8)
+  const int ra = l5_rho(g), rb8 = l5_rho(g + 8);
+  const int sw = ra & 7;  // = rb8 & 7
+  double acc[2][4];
+  double pa[8];
+  double resid0 = 0.0, resid1 = 0.0;
+  for (long long q = 0; q < nitems; ++q) {
+    const int c = (int)(q % nchunks);
+    const long long rbk = blockIdx.x + (q / nchunks) * gridDim.x;
+    const long long o0 = rbk * BM2 + wrow * ROWS;
+    if (idle) continue;
+    if (producer && q + ST - 1 < nitems) {
+      const long long qn = q + ST - 1;
+      if (qn >= ST) mbar_wait(&empty[qn % ST], (unsigned)(((qn / ST) - 1) & 1));
+      issue(qn);
+    }
+    __syncwarp();
+    if (c == 0) {
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[n][v] = 0.0;
+      if (rwarp) {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const long long o = o0 + ((v & 1) ? rb8 : ra);
+          const int k = t + 4 * (v >> 1);
+          pa[v] = (o < O && k < R) ? P[o * R + k] : 0.0;
+        }
+      }
+    }
+    const int slot = (int)(q % ST);
+    mbar_wait(&full[slot], (unsigned)((q / ST) & 1));
+    const double* xt = xs + (size_t)slot * 2 * kHalf + (size_t)wrow * ROWS * 16;
+    const int i0 = c * BK;
+    if (!rwarp) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double* xh = xt + h * kHalf;
+        double a[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int row = (v & 1) ? rb8 : ra;
+          const int chunk = ((v >> 1) + 4 * (t >> 1)) ^ sw;
+          a[v] = xh[row * 16 + chunk * 2 + (t & 1)];
+        }
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          double b[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) b[v] = as[(size_t)(i0 + 16 * h + t + 4 * v) * LDA + n * 8 + g];
+          dmma_16x8x16(acc[n], a, b);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (c == nchunks - 1) {
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const long long o = o0 + ((v >> 1) ? rb8 : ra);
+            const int r = n * 8 + 2 * t + (v & 1);
+            if (o < O && r < R) T[o * R + r] = acc[n][v];
+          }
+      }
+    } else {
+#pragma unroll
+      for (int nb = 0; nb < BK; nb += 8) {
+        double b[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) b[v] = as[(size_t)(i0 + nb + g) * LDA + t + 4 * v];
+        double cx[4] = {0.0, 0.0, 0.0, 0.0};
+        dmma_16x8x16(cx, pa, b);
+        // output columns 2t, 2t + 1 of this 8-column group = smem A rows nb + 2t (+1) = X
+        // columns pi(kappa), pi(kappa + 1) (adjacent): chunk (kappa >> 2) + 4 (t & 1)
+        const double* xh = xt + (nb >> 4) * kHalf;
+        const int chunk = ((((nb & 15) + 2 * t) >> 2) + 4 * (t & 1)) ^ sw;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int row = hh ? rb8 : ra;
+          const double2 xv = *reinterpret_cast<const double2*>(xh + row * 16 + chunk * 2);
+          const double d0 = xv.x - cx[2 * hh], d1 = xv.y - cx[2 * hh + 1];
+          resid0 = fma(d0, d0, resid0);  // zero-filled tails contribute exactly 0
+          resid1 = fma(d1, d1, resid1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+  }
+  if (FUSED) {
+    const double s = block_sum<512>(resid0 + resid1, red);
+    if (tid == 0) partial[blockIdx.x] = s;
+  }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// row-major O x I FP64 matrix as 128-row x 16-column boxes, SWIZZLE_128B, zero OOB fill
+static bool x_tensor_map(CUtensorMap* m, const double* X, long long O, int I) {
+  auto enc = tmap_encode();
+  if (!enc || (I % 2) || (reinterpret_cast<uintptr_t>(X) & 15) || O >= (1LL << 31)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)I, (cuuint64_t)O};
+  cuuint64_t strides[1] = {(cuuint64_t)I * 8};
+  cuuint32_t box[2] = {16, (cuuint32_t)BM2};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int sm_count() {
   static int n = [] {
     int dev = 0, v = 0;
@@ -1186,6 +1383,22 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
   if (R > 32) throw Error(4, "ttm_last: rank > 32 not supported by the DMMA path");
   const size_t ip3 = (size_t)ceil_div(I, kL3BK) * kL3BK;
   const size_t smem3 = (ip3 * lda2<16>() + (size_t)kL3Stages * BM2 * (kL3BK + kPadX)) * 8;
+  static const bool no_l5 = std::getenv("RTB_NO_LAST5") != nullptr;
+  constexpr int kL5St = 4;
+  const size_t smem5 = (size_t)kL5St * 2 * BM2 * 16 * 8 + 1024 +
+                       (size_t)ceil_div(I, 32) * 32 * 20 * 8;
+  CUtensorMap xmap;
+  if (!no_l5 && R <= 16 && smem5 <= 227 * 1024 && x_tensor_map(&xmap, X, O, I)) {
+    auto k = fused ? k_ttm_last5<true, kL5St> : k_ttm_last5<false, kL5St>;
+    set_max_smem(k, (int)smem5);
+    const long long nrb = ceil_div<long long>(O, BM2);
+    const int grid = (int)std::min<long long>(nrb, sm_count());
+    k<<<grid, 512, smem5, st>>>(xmap, O, I, A, R, T, P, partial, g_need);
+    RTB_LAUNCH_CHECK();
+    count_variant(fused ? "k_ttm_last3_fused" : "k_ttm_last3");
+    count_variant(fused ? "k_ttm_last5_fused" : "k_ttm_last5");
+    return;
+  }
   static const bool no_l4 = std::getenv("RTB_NO_LAST4") != nullptr;
   const size_t smem4 = (ip3 * lda2<16>() + (size_t)kL4Stages * BM2 * (kL4BK + kPadX)) * 8;
   if (!no_l4 && R <= 16 && (I % 2) == 0 && I % kL4BK == 0 && smem4 <= 227 * 1024 - 1024) {

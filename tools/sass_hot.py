@@ -1,10 +1,12 @@
-"""Top SASS instructions by stall samples: python tools/sass_hot.py rep.ncu-rep [n]"""
+"""Top SASS instructions by stall samples: python tools/sass_hot.py rep.ncu-rep [n] [kernel-regex]"""
 import csv
 import subprocess
 import sys
 
-out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source=sass"],
-                     capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source=sass"]
+if len(sys.argv) > 3:
+    cmd += ["--kernel-name", "regex:" + sys.argv[3], "--launch-count", "1"]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 h = rows[1]
 cols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]

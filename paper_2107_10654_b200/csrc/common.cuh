@@ -164,6 +164,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* map, int c0, 
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* map, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(smem_u32(bar))
+      : "memory");
+}
 // this thread's prior cp.async copies arrive on `bar` when they complete (counts
 // as one of the barrier's expected arrivals)
 __device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* bar) {

@@ -666,6 +666,161 @@ __global__ void __launch_bounds__(288, 1) k_ttm_mid3(const double* __restrict__ 
   }
 }
 
+constexpr int kMid5KB = 32, kMid5St = 4;  // k_ttm_mid5: rows per box, ring depth
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// row-major O x I FP64 matrix as 128-row x 16-column boxes, SWIZZLE_128B, zero OOB fill
+static bool x_tensor_map(CUtensorMap* m, const double* X, long long O, int I) {
+  auto enc = tmap_encode();
+  if (!enc || (I % 2) || (reinterpret_cast<uintptr_t>(X) & 15) || O >= (1LL << 31)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)I, (cuuint64_t)O};
+  cuuint64_t strides[1] = {(cuuint64_t)I * 8};
+  cuuint32_t box[2] = {16, (cuuint32_t)BM2};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// X (O, I, J) row-major FP64 as 16 (j) x kMid5KB (i) x 1 (o) boxes, SWIZZLE_128B, zero OOB fill
+static bool mid_tensor_map(CUtensorMap* m, const double* X, long long O, int I, long long J) {
+  auto enc = tmap_encode();
+  if (!enc || (J % 2) || (reinterpret_cast<uintptr_t>(X) & 15) || J >= (1LL << 31) ||
+      O >= (1LL << 31))
+    return false;
+  cuuint64_t dims[3] = {(cuuint64_t)J, (cuuint64_t)I, (cuuint64_t)O};
+  cuuint64_t strides[2] = {(cuuint64_t)J * 8, (cuuint64_t)I * J * 8};
+  cuuint32_t box[3] = {16, (cuuint32_t)kMid5KB, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(X), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// k_ttm_mid3 with the X tiles moved by tensor-map TMA: one 3-D box (16 columns x kMid5KB
+// rows x 1, SWIZZLE_128B) per consumer warp and stage, 8 boxes per stage issued by one lane
+// of the producer warp (k_ttm_mid3 issues one bulk copy per row: ~64 per stage, serialised
+// in the producer, which bounded that kernel). Rows past I arrive zero-filled. Conflict-free
+// B fragments of the swizzled box come from relabelling the reduction index: slot
+// kappa = 4 ks + t of each 16-row block reads X row sigma(kappa) = 2 t + (ks & 1) + 8 (ks >> 1)
+// (rows 2t + b sit in distinct 16-byte chunk pairs after the XOR), and A^T is staged with its
+// columns in the same order.
+template <int RP>
+__global__ void __launch_bounds__(288, 1) k_ttm_mid5(const __grid_constant__ CUtensorMap xmap,
+                                                     long long O, int I, long long J,
+                                                     const double* __restrict__ A, int R,
+                                                     double* __restrict__ out) {
+  constexpr int S = kMid5St;
+  constexpr int kBox = kMid5KB * 16;  // doubles per box
+  extern __shared__ __align__(1024) double sm5m[];
+  double* xs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sm5m) + 1023) & ~uintptr_t(1023));
+  double* at = xs + (size_t)S * 8 * kBox;  // [RP][LDT], columns in sigma order
+  __shared__ __align__(8) unsigned long long full[S], empty[S];
+  const int Ip = ceil_div(I, kMid5KB) * kMid5KB;
+  const int LDT = Ip + 4;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const long long ntiles = O * J / BJ2;
+  const int nchunks = ceil_div(I, kMid5KB);
+  for (int e = tid; e < RP * LDT; e += blockDim.x) {
+    const int r = e / LDT, i = e - r * LDT;
+    const int kap = i & 15;
+    const int src = (i & ~15) | (2 * (kap & 3) + ((kap >> 2) & 1) + 8 * ((kap >> 3) & 1));
+    at[e] = (i < Ip && src < I && r < R) ? A[(size_t)src * R + r] : 0.0;
+  }
+  if (tid == 0) {
+    for (int s2 = 0; s2 < S; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], 8);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const long long my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long nitems = my_tiles * nchunks;
+  if (warp == 8) {
+    if (lane == 0) {
+      for (long long q = 0; q < nitems; ++q) {
+        const int st = (int)(q % S);
+        if (q >= S) mbar_wait(&empty[st], (unsigned)(((q / S) - 1) & 1));
+        const long long tile = blockIdx.x + (q / nchunks) * gridDim.x;
+        const int c = (int)(q % nchunks);
+        const long long c0 = tile * BJ2;
+        const long long o = c0 / J, j0 = c0 - o * J;
+        double* dst = xs + (size_t)st * 8 * kBox;
+        mbar_arrive_expect_tx(&full[st], 8u * kBox * 8u);
+        for (int w = 0; w < 8; ++w)
+          tma_load_3d(dst + w * kBox, &xmap, (int)(j0 + 16 * w), c * kMid5KB, (int)o, &full[st]);
+      }
+    }
+    return;
+  }
+  double acc[RP / 8][2][2];
+  for (long long q = 0; q < nitems; ++q) {
+    const int st = (int)(q % S);
+    const int c = (int)(q % nchunks);
+    if (c == 0) {
+#pragma unroll
+      for (int mt = 0; mt < RP / 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    }
+    mbar_wait(&full[st], (unsigned)((q / S) & 1));
+    const double* xb = xs + (size_t)st * 8 * kBox + warp * kBox;
+    const int i0 = c * kMid5KB;
+#pragma unroll
+    for (int ks = 0; ks < kMid5KB / 4; ++ks) {
+      double af[RP / 8];
+#pragma unroll
+      for (int mt = 0; mt < RP / 8; ++mt) af[mt] = at[(size_t)(mt * 8 + g) * LDT + i0 + ks * 4 + t];
+      const int ksl = ks & 3;
+      const int row = 16 * (ks >> 2) + 2 * t + (ksl & 1) + 8 * (ksl >> 1);
+      const int sw = row & 7;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const double bf = xb[row * 16 + (((4 * nt + (g >> 1)) ^ sw) << 1) + (g & 1)];
+#pragma unroll
+        for (int mt = 0; mt < RP / 8; ++mt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (c == nchunks - 1) {
+      const long long tile = blockIdx.x + (q / nchunks) * gridDim.x;
+      const long long c0 = tile * BJ2;
+      const long long o = c0 / J, j0 = c0 - o * J + warp * 16;
+#pragma unroll
+      for (int mt = 0; mt < RP / 8; ++mt) {
+        const int r = mt * 8 + g;
+        if (r >= R) continue;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          double2 v2;
+          v2.x = acc[mt][nt][0];
+          v2.y = acc[mt][nt][1];
+          *reinterpret_cast<double2*>(out + (o * R + r) * J + j0 + nt * 8 + 2 * t) = v2;
+        }
+      }
+    }
+  }
+}
+static size_t mid5_smem(int I, int rp) {
+  const size_t ip = (size_t)ceil_div(I, kMid5KB) * kMid5KB;
+  return (size_t)kMid5St * 8 * kMid5KB * 16 * 8 + 1024 + (size_t)rp * (ip + 4) * 8;
+}
+
 static size_t mid3_smem(int I, int rp) {
   const size_t ip = (size_t)ceil_div(I, kMidKB) * kMidKB;
   return ((size_t)rp * (ip + 4) + (size_t)kMidStages * kMidKB * (BJ2 + 8)) * 8;
@@ -1307,33 +1462,6 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last5(const __grid_constant__ CU
   }
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      p = nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }();
-  return fn;
-}
-
-// row-major O x I FP64 matrix as 128-row x 16-column boxes, SWIZZLE_128B, zero OOB fill
-static bool x_tensor_map(CUtensorMap* m, const double* X, long long O, int I) {
-  auto enc = tmap_encode();
-  if (!enc || (I % 2) || (reinterpret_cast<uintptr_t>(X) & 15) || O >= (1LL << 31)) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)I, (cuuint64_t)O};
-  cuuint64_t strides[1] = {(cuuint64_t)I * 8};
-  cuuint32_t box[2] = {16, (cuuint32_t)BM2};
-  cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box,
-             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 static int sm_count() {
   static int n = [] {
     int dev = 0, v = 0;
@@ -1504,6 +1632,19 @@ static void launch_mid2(const double* X, long long O, int I, long long J, const 
   static const bool probe = std::getenv("RTB_TTM_STREAM_ONLY") != nullptr;
   static const bool pc = std::getenv("RTB_TTM_NO_PRODUCER") == nullptr;
   const size_t smem3 = mid3_smem(I, RP);
+  static const bool no_m5 = std::getenv("RTB_NO_MID5") != nullptr;
+  const size_t smem5 = mid5_smem(I, RP);
+  CUtensorMap xmap;
+  if (!no_m5 && !probe && smem5 <= 227 * 1024 - 2048 && mid_tensor_map(&xmap, X, O, I, J)) {
+    set_max_smem(k_ttm_mid5<RP>, (int)smem5);
+    const long long ntiles = O * J / BJ2;
+    const int grid = (int)std::min<long long>(ntiles, sm_count());
+    k_ttm_mid5<RP><<<grid, 288, smem5, st>>>(xmap, O, I, J, A, R, out);
+    RTB_LAUNCH_CHECK();
+    count_variant("k_ttm_mid3");
+    count_variant("k_ttm_mid5");
+    return;
+  }
   if (pc && smem3 <= 227 * 1024 - 2048) {
     auto k3 = probe ? k_ttm_mid3<RP, false> : k_ttm_mid3<RP, true>;
     set_max_smem(k3, 227 * 1024 - 2048);

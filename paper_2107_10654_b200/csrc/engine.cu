@@ -1432,7 +1432,9 @@ class Engine {
       sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, pev_.as<double>(),
                 pvec_.as<double>(), pst_.as<int>(), N_, ss, eskip);
     }
-    normal_eq(s, !pcg_path_);
+    // the split-role PCG keeps the compact Gram in shared memory: no block expansion
+    const bool split = pcg_path_ && !sharded() && pcg_split_ok((int)d_, N_, rk);
+    normal_eq(s, !pcg_path_, !split);
     if (!pcg_path_) {
       solve_fallback(s, false);
       return;
@@ -1441,7 +1443,7 @@ class Engine {
       // Kronecker-preconditioned CG on the blocked Gram (k_pcg.cu), verified by its
       // true residual; the Cholesky path (solve_fallback) takes over on failure
       Scope sc(prof_, "pcg");
-      if (!blocks_ready_) {
+      if (!split && !blocks_ready_) {
         blocks_.ensure((size_t)gram_block_elems(gs) * 8, st_);
         gram_expand_blocks(gs, gram_work_.p, blocks_.as<double>(), st_);
       }
@@ -1458,8 +1460,12 @@ class Engine {
       // first sketch of a run starts cold from the random init): a device flag
       ps.warm_dev = warm_dev_.as<int>();
       pcg_work_.ensure(pcg_work_bytes((int)d_, N_, rk), st_);
-      pcg_solve(ps, blocks_.as<double>(), rhs_.as<double>(), core_.as<double>(), pcg_work_.p,
-                pcg_status_.as<int>(), st_);
+      if (split)
+        pcg_solve_compact(ps, gram_compact(gs, gram_work_.p, nullptr), rhs_.as<double>(),
+                          core_.as<double>(), pcg_work_.p, pcg_status_.as<int>(), st_);
+      else
+        pcg_solve(ps, blocks_.as<double>(), rhs_.as<double>(), core_.as<double>(), pcg_work_.p,
+                  pcg_status_.as<int>(), st_);
     }
     k_core_post<<<1, 1024, 0, st_>>>(core_.as<double>(), (long long)d_, pcg_status_.as<int>(),
                                      zero_flag_.as<int>(), warm_dev_.as<int>(), post_.as<int>());
@@ -1490,7 +1496,7 @@ class Engine {
 
   // sketched normal equations of the current draws (compact Gram in the workspace, rhs;
   // with `full` the d x d Gram in G_ as well)
-  void normal_eq(uint64_t s, bool full) {
+  void normal_eq(uint64_t s, bool full, bool want_blocks = true) {
     GramSpec gs = gram_spec(s);
     // X slab pointer offset so that global flat indices of this shard's draws land in it
     const double* xg = x_ - (sharded() ? lo_ * (long long)(total_ / shape_[0]) : 0);
@@ -1499,7 +1505,7 @@ class Engine {
     // the PCG's last-mode blocks come out of the contraction itself when it can write them
     // (one shard only: under sharding they follow the all-reduce of the compact Gram)
     double* bl = nullptr;
-    if (!full && !sharded()) {
+    if (!full && !sharded() && want_blocks) {
       blocks_.ensure((size_t)gram_block_elems(gs) * 8, st_);
       bl = blocks_.as<double>();
     }

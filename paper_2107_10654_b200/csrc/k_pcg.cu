@@ -259,6 +259,85 @@ __device__ __forceinline__ void mode_product_dmma16(const double* X, double* out
   }
 }
 
+// Modes 2 and 3 of a 16 x 16 x 16 vector, slab-local: warp w owns slab i_1 = w (256 values)
+// and computes out_w = W2^T (X_w W3) with two 16x16x16 DMMA GEMMs (the product of each mode
+// as in mode_product: out_j = sum_i W[i][j] x_i), the intermediate in Y_w; no CTA barrier.
+// out may alias X (the warp reads its X slab completely before writing).
+__device__ __forceinline__ void slab23_dmma16(const double* X, double* Y, double* out,
+                                              const double* W2, const double* W3) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const double* xs = X + w * 256;
+  double* ys = Y + w * 256;
+  double* os = out + w * 256;
+  double c[2][2][2];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    double a[2], b[2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) a[mt] = xs[(8 * mt + g) * 16 + 4 * ks + t];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) b[nt] = W3[(4 * ks + t) * 16 + 8 * nt + g];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) dmma_8x8x4(c[mt][nt][0], c[mt][nt][1], a[mt], b[nt]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      ys[(8 * mt + g) * 16 + 8 * nt + 2 * t] = c[mt][nt][0];
+      ys[(8 * mt + g) * 16 + 8 * nt + 2 * t + 1] = c[mt][nt][1];
+      c[mt][nt][0] = c[mt][nt][1] = 0.0;
+    }
+  __syncwarp();
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    double a[2], b[2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) a[mt] = W2[(4 * ks + t) * 16 + 8 * mt + g];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) b[nt] = ys[(4 * ks + t) * 16 + 8 * nt + g];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) dmma_8x8x4(c[mt][nt][0], c[mt][nt][1], a[mt], b[nt]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      os[(8 * mt + g) * 16 + 8 * nt + 2 * t] = c[mt][nt][0];
+      os[(8 * mt + g) * 16 + 8 * nt + 2 * t + 1] = c[mt][nt][1];
+    }
+}
+
+// z = M^-1 r for 16 x 16 x 16 (order 3, all ranks 16, kWarps = 16 slabs): modes 2-3 slab by
+// slab (slab23_dmma16), one CTA barrier, mode 1 (mode_product_dmma16 with J = 256). Returns
+// the buffer holding z (r is preserved).
+__device__ double* precondition16(const double* r, double* a, double* b, const double* W1,
+                                  const double* W2, const double* dinv, bool eig) {
+  slab23_dmma16(r, a, b, W1 + 256, W1 + 512);
+  __syncthreads();
+  mode_product_dmma16(b, a, W1, 4096, 256);
+  __syncthreads();
+  if (!eig) return a;
+  for (int e = threadIdx.x; e < 4096; e += kThreads) a[e] *= dinv[e];
+  __syncthreads();
+  slab23_dmma16(a, b, a, W2 + 256, W2 + 512);
+  __syncthreads();
+  mode_product_dmma16(a, b, W2, 4096, 256);
+  __syncthreads();
+  return b;
+}
+
 // z = M^-1 r with scratch a, b; returns the buffer holding z. Two forms:
 //  * P form (eig == false): M = (x)_n A_n^T A_n, M^-1 = (x)_n P_n: N mode products.
 //  * eigen form: M = (x)_n A_n^T A_n + lambda I = V diag(lambda + prod mu) V^T:
@@ -811,6 +890,483 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   }
 }
 
+// ---------------------------------------------------------------------------
+// Split-role PCG (order 3, R_3 = 16, m_1 slices < #SMs): the Gram stays in SHARED MEMORY for
+// the whole solve. CTA u < m_1 holds slice u_1 = u of the compact (vech) Gram S -- row u_1
+// of S, m_2 x 136 values, 148 KB at C2 -- and computes that slice's matvec partials; the
+// remaining CTAs ("vector CTAs", 12 at C2) hold r, p, x and the scratch vectors and run the
+// CG recurrences, redundantly and bit-identically, each publishing its share of the next
+// matvec source (p, or x0 / x) to global memory. Per matvec, three grid barriers: source
+// published -> slice partials -> own-row sums (all CTAs) -> q read by the vector CTAs.
+// The slices are read from shared memory instead of streaming 38 MB of blocks from L2 per
+// iteration (k_pcg's slice phase). Matvec source selector `ctl` (first vector CTA):
+// 1 = CG step / warm start, 2 = final residual check, 0 = done.
+struct PcgSplitArgs {
+  const double* S;   // compact Gram [m1][m2 * 136]
+  double* pg;        // [d] published matvec source
+  int* ctl;
+};
+
+// slice partials from the shared-memory slice Bp (m2 x 136): warp w takes a contiguous range
+// of the slice's row-major (i2 <= j2) blocks; along a row i2 the sources p_b(i2), p_a(i2)
+// stay in registers and the targets q_a(i2), q_b(i2) accumulate in registers; the
+// transposed targets q_a(j2), q_b(j2) go to the warp's shared accumulators.
+// lane l: block row r = l & 15, columns c = 8 (l >> 4) + k, k < 8.
+__device__ void split_slice(const PcgShared& sh, const double* Bp, const double* pa,
+                            const double* pb, bool two_sides, double* accw, int m2,
+                            const int (&off)[8]) {
+  const int R2 = sh.R[1], dp = sh.dprime;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane & 15, h = lane >> 4;
+  double* acc = accw + (size_t)w * 2 * dp;
+  const int blo = (m2 * w) / kWarps, bhi = (m2 * (w + 1)) / kWarps;
+  if (blo >= bhi) return;
+  int i2, j2;
+  pair_of(blo, R2, i2, j2);
+  double xb_i[8], xa_i[8];  // p_b(i2), p_a(i2) at this lane's columns
+  double y0 = 0.0, y2 = 0.0;  // q_a(i2)[r], q_b(i2)[r] (this lane's column half)
+  auto load_row = [&]() {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      xb_i[k] = pb[i2 * 16 + 8 * h + k];
+      xa_i[k] = two_sides ? pa[i2 * 16 + 8 * h + k] : 0.0;
+    }
+  };
+  auto flush_row = [&]() {
+    y0 += __shfl_xor_sync(0xffffffffu, y0, 16);
+    y2 += __shfl_xor_sync(0xffffffffu, y2, 16);
+    if (h == 0) {
+      acc[i2 * 16 + r] += y0;
+      if (two_sides) acc[dp + i2 * 16 + r] += y2;
+    }
+    __syncwarp();
+    y0 = y2 = 0.0;
+  };
+  load_row();
+  for (int u = blo; u < bhi; ++u) {
+    const double* Bu = Bp + (size_t)u * 136;
+    double m[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = Bu[off[k]];
+    const double* xbj = pb + j2 * 16 + 8 * h;
+    const double* xaj = pa + j2 * 16 + 8 * h;
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      const double2 vb = *reinterpret_cast<const double2*>(xbj + k);
+      t0 = fma(m[k], vb.x, t0);
+      t0 = fma(m[k + 1], vb.y, t0);
+      t1 = fma(m[k], xb_i[k], t1);
+      t1 = fma(m[k + 1], xb_i[k + 1], t1);
+      if (two_sides) {
+        const double2 va = *reinterpret_cast<const double2*>(xaj + k);
+        t2 = fma(m[k], va.x, t2);
+        t2 = fma(m[k + 1], va.y, t2);
+        t3 = fma(m[k], xa_i[k], t3);
+        t3 = fma(m[k + 1], xa_i[k + 1], t3);
+      }
+    }
+    y0 += t0;  // q_a(i2) += M p_b(j2)
+    y2 += t2;  // q_b(i2) += M p_a(j2)
+    if (j2 != i2) {  // q_a(j2) += M p_b(i2), q_b(j2) += M p_a(i2)
+      t1 += __shfl_xor_sync(0xffffffffu, t1, 16);
+      t3 += __shfl_xor_sync(0xffffffffu, t3, 16);
+      if (h == 0) {
+        acc[j2 * 16 + r] += t1;
+        if (two_sides) acc[dp + j2 * 16 + r] += t3;
+      }
+      __syncwarp();
+    }
+    // next block (row-major upper triangle)
+    if (u + 1 < bhi) {
+      if (++j2 == R2) {
+        flush_row();
+        ++i2;
+        j2 = i2;
+        load_row();
+      }
+    }
+  }
+  flush_row();
+}
+
+// The same slice matvec on the FP64 tensor cores: per block, C (16 x 8) += M (16 x 16) B with
+// B's columns the four sources p_b(j2), p_b(i2), p_a(j2), p_a(i2) (columns 4-7 zero), one
+// m16n8k16 DMMA. Columns 0 / 2 (targets q_a(i2), q_b(i2)) accumulate in the C registers
+// along a row of blocks; columns 1 / 3 (q_a(j2), q_b(j2)) are added to the warp's shared
+// accumulators after each off-diagonal block and reset. offA: this lane's packed offsets of
+// its A-fragment entries M[g + 8 (v & 1)][t + 4 (v >> 1)].
+__device__ void split_slice_dmma(const PcgShared& sh, const double* __restrict__ Bp,
+                                 const double* __restrict__ pa, const double* __restrict__ pb,
+                                 bool two_sides, double* __restrict__ accw, int m2,
+                                 const int (&offA)[8]) {
+  const int R2 = sh.R[1], dp = sh.dprime;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  double* acc = accw + (size_t)w * 2 * dp;
+  const int blo = (m2 * w) / kWarps, bhi = (m2 * (w + 1)) / kWarps;
+  if (blo >= bhi) return;
+  int i2, j2;
+  pair_of(blo, R2, i2, j2);
+  // B column g (< 4) of this lane: which source, and whether it is the row's (i2) block
+  const bool srcb = g < 2, src_i = (g & 1) != 0;
+  const bool bcol = g < 4 && (srcb || two_sides);
+  const double* sbase = srcb ? pb : pa;
+  const bool tgt = t < 2 && (t == 0 || two_sides);  // lanes t = 0 / 1: side-0 / side-1 targets
+  double c[4] = {0.0, 0.0, 0.0, 0.0};
+  double a[8], b[4];
+  auto load = [&](int u, int ii, int jj) {  // operands of block u = (ii, jj)
+    const double* Bu = Bp + (size_t)u * 136;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) a[v] = Bu[offA[v]];
+    const double* src = sbase + (src_i ? ii : jj) * 16;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) b[v] = bcol ? src[t + 4 * v] : 0.0;
+  };
+  load(blo, i2, j2);
+  for (int u = blo; u < bhi; ++u) {
+    dmma_16x8x16(c, a, b);
+    // next block's operands while this one's DMMAs run (the shared loads do not alias acc)
+    int ni = i2, nj = j2 + 1;
+    if (nj == R2) {
+      ++ni;
+      nj = ni;
+    }
+    if (u + 1 < bhi) load(u + 1, ni, nj);
+    const double t1 = c[1], t3 = c[3];
+    c[1] = c[3] = 0.0;
+    if (j2 != i2 && tgt) {  // columns 1 / 3: q_side(j2)
+      double* q = acc + t * dp + j2 * 16;
+      q[g] += t1;
+      q[g + 8] += t3;
+    }
+    if (ni != i2 || u + 1 == bhi) {  // row done: columns 0 / 2: q_side(i2)
+      if (tgt) {
+        double* q = acc + t * dp + i2 * 16;
+        q[g] += c[0];
+        q[g + 8] += c[2];
+      }
+      c[0] = c[2] = 0.0;
+    }
+    i2 = ni;
+    j2 = nj;
+  }
+}
+
+template <int RX>
+__global__ void __launch_bounds__(kThreads, 1) k_pcg_split(const PcgArgs A, const PcgShared shc,
+                                                          const PcgSplitArgs X) {
+  extern __shared__ __align__(16) double sm[];
+  const PcgShared& sh = shc;
+  const int d = sh.d, dp = sh.dprime;
+  const int dv = (d + 1) & ~1;
+  const int m1 = sh.m1, m2 = sh.m[1];
+  const bool slice_cta = (int)blockIdx.x < m1;
+  const int nvec = (int)gridDim.x - m1, vid = (int)blockIdx.x - m1;
+  const int tid = threadIdx.x;
+  constexpr int RM = 16;
+
+  // applicability (every CTA decides the same)
+  int missing = 0;
+  for (int e = tid; e < d; e += kThreads) missing |= __ldg(A.aug_count + e) == 0;
+  if (tid < sh.order) missing |= __ldg(A.linv_ok + tid) == 0;
+  const double pnorm = A.prep[1];
+  if (__syncthreads_or(missing) || !(A.lambda > 0.0) || !(A.lambda * pnorm <= kMaxLambdaOverMu)) {
+    if (blockIdx.x == 0 && tid == 0) {
+      A.status[0] = 3;
+      A.status[1] = 0;
+    }
+    return;
+  }
+  const int row0 = min(d, (int)blockIdx.x * sh.rows_per_cta);
+  const int nrows = min(d, row0 + sh.rows_per_cta) - row0;
+  unsigned sync_target = 0;
+  auto gsync = [&]() {
+    sync_target += gridDim.x;
+    grid_barrier(A.counter, sync_target);
+  };
+  // own rows: q[e] = sum over the slices' partials + augmented diagonal * source[e]
+  // 16 lanes per row, one slice partial each (R_1 <= 16), summed by a fixed shuffle tree
+  auto reduce_own = [&]() {
+    const int R1 = sh.R[0];
+    const int j1 = tid & 15;
+    for (int base = row0; base < row0 + nrows; base += kThreads / 16) {
+      const int e = base + (tid >> 4);
+      const bool ok = e < row0 + nrows;
+      double s = 0.0;
+      if (ok && j1 < R1) {
+        const int i1 = e / dp, rest = e - i1 * dp;
+        const int u1 = upper_pair(min(i1, j1), max(i1, j1), R1);
+        const int side = i1 <= j1 ? 0 : 1;
+        s = __ldcg(A.part + ((size_t)u1 * 2 + side) * dp + rest);
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (ok && j1 == 0) {
+        const int c = __ldg(A.aug_count + e);
+        if (c > 0) s = fma((double)c * A.aug_term, __ldcg(X.pg + e), s);
+        A.q[e] = s;
+      }
+    }
+  };
+
+  if (slice_cta) {
+    // ---------------- slice CTA ----------------
+    double* Bp = sm;                                   // [m2][136]
+    double* pa = Bp + (size_t)m2 * 136;                // [dp]
+    double* pb = pa + dp;                              // [dp]
+    double* accw = pb + dp;                            // [kWarps][2][dp]
+    const int u1 = blockIdx.x;
+    int a, b;
+    pair_of(u1, sh.R[0], a, b);
+    const bool two = a != b;
+    {
+      const double2* src = reinterpret_cast<const double2*>(X.S + (size_t)u1 * m2 * 136);
+      double2* dst = reinterpret_cast<double2*>(Bp);
+      for (int e = tid; e < m2 * 68; e += kThreads) dst[e] = __ldg(src + e);
+    }
+    const int lane = tid & 31;
+    int off[8];
+    static constexpr bool kDmmaSlice = true;
+    if (kDmmaSlice) {
+      const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int rr = g + 8 * (v & 1), cc = t + 4 * (v >> 1);
+        off[v] = upper_pair(min(rr, cc), max(rr, cc), 16);
+      }
+    } else {
+      const int r = lane & 15, h = lane >> 4;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int c = 8 * h + k;
+        off[k] = upper_pair(min(r, c), max(r, c), 16);
+      }
+    }
+    for (;;) {
+      gsync();  // source published
+      if (__ldcg(X.ctl) == 0) break;
+      for (int e = tid; e < dp; e += kThreads) {
+        pa[e] = __ldcg(X.pg + (size_t)a * dp + e);
+        pb[e] = __ldcg(X.pg + (size_t)b * dp + e);
+      }
+      for (int e = tid; e < kWarps * 2 * dp; e += kThreads) accw[e] = 0.0;
+      __syncthreads();
+      const bool pf = A.prof && blockIdx.x == 0 && tid == 0;
+      const unsigned long long ts0 = pf ? gtimer() : 0;
+      if (kDmmaSlice) split_slice_dmma(sh, Bp, pa, pb, two, accw, m2, off);
+      else split_slice(sh, Bp, pa, pb, two, accw, m2, off);
+      __syncthreads();
+      if (pf) A.prof[4] += gtimer() - ts0;
+      for (int e = tid; e < 2 * dp; e += kThreads) {
+        const int side = e >= dp;
+        if (side && !two) continue;
+        double s = 0.0;
+        for (int w = 0; w < kWarps; ++w) s += accw[(size_t)w * 2 * dp + e];
+        A.part[((size_t)u1 * 2 + side) * dp + (e - side * dp)] = s;
+      }
+      gsync();  // partials
+      reduce_own();
+      gsync();  // q
+    }
+    return;
+  }
+
+  // ---------------- vector CTA ----------------
+  double* Ps = sm;                          // [order][RM][RM]
+  double* VTs = Ps + sh.order * RM * RM;
+  double* dinv = VTs + sh.order * RM * RM;
+  double* r = dinv + dv;
+  double* p = r + dv;
+  double* s0 = p + dv;
+  double* s1 = s0 + dv;
+  double* xs = s1 + dv;
+  double* red = xs + dv;
+  const int sh0 = (int)((long long)d * vid / nvec), sh1 = (int)((long long)d * (vid + 1) / nvec);
+  auto publish = [&](const double* v, int c) {  // my share of the next matvec source
+    for (int e = sh0 + tid; e < sh1; e += kThreads) X.pg[e] = v[e];
+    if (vid == 0 && tid == 0) *X.ctl = c;
+  };
+  for (int n = 0; n < sh.order; ++n) {
+    const int R = sh.R[n];
+    const double* Pg = A.pinv + (size_t)n * A.linv_stride;
+    for (int e = tid; e < RM * RM; e += kThreads) {
+      const int i = e / RM, j = e - i * RM;
+      Ps[n * RM * RM + e] = (i < R && j < R) ? Pg[i * R + j] : 0.0;
+    }
+  }
+  __syncthreads();
+  const double gnorm = A.prep[0];
+  const bool eig = A.prep[2] != 0.0;
+  if (eig) {
+    for (int n = 0; n < sh.order; ++n) {
+      const int R = sh.R[n];
+      const double* Vg = A.evecs + (size_t)n * A.linv_stride;
+      for (int e = tid; e < RM * RM; e += kThreads) {
+        const int i = e / RM, j = e - i * RM;
+        const bool in = i < R && j < R;
+        Ps[n * RM * RM + e] = in ? Vg[i * R + j] : 0.0;
+        VTs[n * RM * RM + e] = in ? Vg[j * R + i] : 0.0;
+      }
+    }
+    for (int e = tid; e < d; e += kThreads) {
+      double m = 1.0;
+      int rem = e;
+      for (int n = sh.order - 1; n >= 0; --n) {
+        const int j = rem % sh.R[n];
+        rem /= sh.R[n];
+        m *= fmax(A.evals[(size_t)n * A.linv_stride + j], 0.0);
+      }
+      dinv[e] = 1.0 / (m + A.lambda);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < d; e += kThreads) {
+    r[e] = A.b[e];
+    xs[e] = 0.0;
+  }
+  __syncthreads();
+  double bb = 0.0;
+  for (int e = tid; e < d; e += kThreads) bb = fma(r[e], r[e], bb);
+  bb = block_sum_det(bb, red);
+  const double tol2 = A.tol * A.tol;
+  enum { kWarm, kCg, kCheck };
+  int mode = kCg, it = 0, fail = 0;
+  double rho = 0.0, xx = 0.0;
+  auto precond = [&]() -> double* {
+    if constexpr (RX == 16) {
+      if (sh.order == 3 && sh.R[0] == 16) return precondition16(r, s0, s1, Ps, VTs, dinv, eig);
+    }
+    return precondition<RM, RX>(sh, r, s0, s1, Ps, VTs, dinv, eig);
+  };
+  auto start_cg = [&]() {  // z = M^-1 r, p = z, rho; publish p
+    double* z = precond();
+    double rh = 0.0;
+    for (int e = tid; e < d; e += kThreads) {
+      p[e] = z[e];
+      rh = fma(r[e], z[e], rh);
+    }
+    rho = block_sum_det(rh, red);
+    publish(p, 1);
+    mode = kCg;
+  };
+  auto start_check = [&]() {  // final residual check: matvec with x
+    double t = 0.0;
+    for (int e = tid; e < d; e += kThreads) t = fma(xs[e], xs[e], t);
+    xx = block_sum_det(t, red);
+    publish(xs, 2);
+    mode = kCheck;
+  };
+  if (bb == 0.0) {
+    for (int e = sh0 + tid; e < sh1; e += kThreads) A.x[e] = 0.0;
+    if (vid == 0 && tid == 0) {
+      A.status[0] = 0;
+      A.status[1] = 0;
+    }
+    publish(xs, 0);
+  } else if (A.warm_dev ? *A.warm_dev : A.warm) {
+    for (int e = tid; e < d; e += kThreads) xs[e] = A.x[e];
+    __syncthreads();
+    publish(xs, 1);
+    mode = kWarm;
+  } else {
+    start_cg();
+  }
+  const bool pf = A.prof && vid == 0 && tid == 0;
+  unsigned long long tv = pf ? gtimer() : 0;
+  auto mark = [&](int k) {
+    if (pf) {
+      const unsigned long long t1 = gtimer();
+      A.prof[k] += t1 - tv;
+      tv = t1;
+    }
+  };
+  for (;;) {
+    mark(3);
+    gsync();  // source published
+    mark(0);
+    if (__ldcg(X.ctl) == 0) break;
+    gsync();  // partials
+    mark(1);
+    reduce_own();
+    gsync();  // q
+    mark(2);
+    if (mode == kWarm) {
+      double r0 = 0.0;
+      for (int e = tid; e < d; e += kThreads) {
+        const double re = A.b[e] - __ldcg(A.q + e);
+        s0[e] = re;
+        r0 = fma(re, re, r0);
+      }
+      r0 = block_sum_det(r0, red);
+      if (r0 < bb && isfinite(r0)) {
+        for (int e = tid; e < d; e += kThreads) r[e] = s0[e];
+      } else {
+        for (int e = tid; e < d; e += kThreads) xs[e] = 0.0;
+      }
+      __syncthreads();
+      start_cg();
+    } else if (mode == kCg) {
+      double pq = 0.0;
+      for (int e = tid; e < d; e += kThreads) {
+        const double qe = __ldcg(A.q + e);
+        s0[e] = qe;
+        pq = fma(p[e], qe, pq);
+      }
+      pq = block_sum_det(pq, red);
+      if (!(pq > 0.0) || !isfinite(pq)) {
+        fail = 2;
+        start_check();
+        continue;
+      }
+      const double alpha = rho / pq;
+      double rr = 0.0, xq = 0.0;
+      for (int e = tid; e < d; e += kThreads) {
+        const double re = fma(-alpha, s0[e], r[e]);
+        r[e] = re;
+        rr = fma(re, re, rr);
+        const double xe = fma(alpha, p[e], xs[e]);
+        xs[e] = xe;
+        xq = fma(xe, xe, xq);
+      }
+      block_sum2_det(rr, xq, red);
+      ++it;
+      if (rr <= tol2 * fmax(bb, gnorm * gnorm * xq) || it >= A.max_iter) {
+        start_check();
+        continue;
+      }
+      double* z = precond();
+      double rho2 = 0.0;
+      for (int e = tid; e < d; e += kThreads) rho2 = fma(r[e], z[e], rho2);
+      rho2 = block_sum_det(rho2, red);
+      const double beta = rho2 / rho;
+      rho = rho2;
+      for (int e = tid; e < d; e += kThreads) p[e] = fma(beta, p[e], z[e]);
+      __syncthreads();
+      publish(p, 1);
+      mark(5);
+    } else {  // kCheck: q = G x
+      for (int e = sh0 + tid; e < sh1; e += kThreads) A.x[e] = xs[e];
+      if (vid == 0) {
+        double res = 0.0;
+        for (int e = tid; e < d; e += kThreads) {
+          const double t = A.b[e] - __ldcg(A.q + e);
+          res = fma(t, t, res);
+        }
+        res = block_sum_det(res, red);
+        if (tid == 0) {
+          int st = fail;
+          const double scale = gnorm * sqrt(xx) + sqrt(bb);
+          if (!st && !(res <= A.check_tol * A.check_tol * scale * scale)) st = 1;
+          A.status[0] = st;
+          A.status[1] = it;
+        }
+      }
+      publish(xs, 0);
+    }
+  }
+}
+
 int num_sms() {
   static int sms = [] {
     int dev = 0, n = 0;
@@ -884,7 +1440,8 @@ static int pcg_jc(int d, int order, const int* ranks) {
 static size_t pcg_base_bytes(int d, int order, const int* ranks) {
   const size_t m1 = (size_t)ranks[0] * (ranks[0] + 1) / 2;
   const size_t dp = (size_t)d / ranks[0];
-  return ((size_t)d + m1 * pcg_jc(d, order, ranks) * 2 * dp + 1024) * 8 + 256;
+  return ((size_t)d + m1 * pcg_jc(d, order, ranks) * 2 * dp + 1024) * 8 + 256 +
+         ((size_t)d + 32) * 8;  // + the split form's published source and selector
 }
 
 size_t pcg_work_bytes(int d, int order, const int* ranks) {
@@ -987,6 +1544,106 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
                  "vec %llu precond %llu tail %llu | stages %llu %llu %llu | gnorm %.3e pnorm %.3e\n",
                  d, stat[1], stat[0], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[8], h[9], h[10],
                  __builtin_bit_cast(double, h[14]), __builtin_bit_cast(double, h[15]));
+  }
+}
+
+
+static size_t split_slice_smem(int d, const int* ranks) {
+  const size_t m2 = (size_t)ranks[1] * (ranks[1] + 1) / 2, dp = (size_t)d / ranks[0];
+  return (m2 * 136 + 2 * dp + (size_t)kWarps * 2 * dp) * 8;
+}
+static size_t split_vector_smem(int d, int order) {
+  return ((size_t)2 * order * 16 * 16 + 6 * (size_t)((d + 1) & ~1) + 64) * 8;
+}
+
+bool pcg_split_ok(int d, int order, const int* ranks) {
+  static const bool off = std::getenv("RTB_NO_PCG_SPLIT") != nullptr;
+  if (off || order != 3 || ranks[2] != 16 || ranks[0] > 16 || ranks[1] > 16) return false;
+  if (!pcg_supported(d, order, ranks) || pcg_big(d, order, ranks)) return false;
+  const int m1 = ranks[0] * (ranks[0] + 1) / 2;
+  if (m1 + 4 > num_sms()) return false;
+  return std::max(split_slice_smem(d, ranks), split_vector_smem(d, order)) <= 227 * 1024 - 1024;
+}
+
+void pcg_solve_compact(const PcgSpec& spec, const double* S, const double* b, double* x,
+                       void* work, int* status_dev, cudaStream_t st) {
+  const int d = spec.d;
+  const int grid = num_sms();
+  if (!pcg_split_ok(d, spec.order, spec.ranks)) throw Error(4, "pcg_solve_compact: unsupported shape");
+  PcgShared sh{};
+  sh.d = d;
+  sh.order = spec.order;
+  sh.rows_per_cta = (d + grid - 1) / grid;
+  int inner = 1;
+  for (int n = spec.order - 1; n >= 0; --n) {
+    sh.R[n] = spec.ranks[n];
+    sh.m[n] = spec.ranks[n] * (spec.ranks[n] + 1) / 2;
+    sh.J[n] = inner;
+    inner *= spec.ranks[n];
+  }
+  if (inner != d) throw Error(1, "pcg_solve_compact: prod(ranks) != d");
+  sh.dprime = d / sh.R[0];
+  sh.last = sh.R[spec.order - 1];
+  sh.mid = sh.dprime / sh.last;
+  sh.mmid = sh.m[1];
+  sh.m1 = sh.m[0];
+  sh.jc = 1;
+  const size_t smem = std::max(split_slice_smem(d, spec.ranks), split_vector_smem(d, spec.order));
+  char* w = static_cast<char*>(work);
+  PcgArgs a{};
+  a.b = b;
+  a.x = x;
+  a.q = reinterpret_cast<double*>(w);
+  a.part = a.q + d;
+  a.rpart = a.part + (size_t)sh.m1 * 2 * sh.dprime;
+  a.counter = reinterpret_cast<unsigned*>(a.rpart + 1024);
+  a.status = status_dev;
+  a.pinv = spec.pinv;
+  a.linv_stride = spec.linv_stride;
+  a.linv_ok = spec.linv_ok;
+  a.grams = spec.grams;
+  a.evals = spec.evals;
+  a.evecs = spec.evecs;
+  a.prep = spec.prep;
+  a.aug_count = spec.aug_count;
+  a.aug_term = spec.aug_term;
+  a.lambda = spec.lambda;
+  a.max_iter = spec.max_iter;
+  a.tol = spec.tol;
+  a.check_tol = spec.check_tol;
+  a.warm = spec.warm;
+  a.warm_dev = spec.warm_dev;
+  PcgSplitArgs xa{};
+  xa.S = S;
+  xa.pg = reinterpret_cast<double*>(reinterpret_cast<char*>(a.counter) + 256);
+  xa.ctl = reinterpret_cast<int*>(xa.pg + d);
+  RTB_CUDA(cudaMemsetAsync(a.counter, 0, 64, st));
+  bool all16 = true;
+  for (int n = 0; n < spec.order; ++n) all16 &= spec.ranks[n] == 16;
+  void* fn = all16 ? (void*)k_pcg_split<16> : (void*)k_pcg_split<0>;
+  set_max_smem_impl(fn, (int)smem);
+  static unsigned long long* prof_buf = nullptr;
+  static const bool prof_on = std::getenv("RTB_PCG_PROF") != nullptr;
+  if (prof_on) {
+    if (!prof_buf) RTB_CUDA(cudaMalloc(&prof_buf, 16 * 8));
+    RTB_CUDA(cudaMemsetAsync(prof_buf, 0, 16 * 8, st));
+    a.prof = prof_buf;
+  }
+  void* args[] = {(void*)&a, (void*)&sh, (void*)&xa};
+  RTB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, st));
+  RTB_LAUNCH_CHECK();
+  count_variant("k_pcg_split");
+  if (prof_on) {
+    unsigned long long h[16];
+    int stat[2];
+    RTB_CUDA(cudaMemcpyAsync(h, prof_buf, 128, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaMemcpyAsync(stat, status_dev, 8, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaStreamSynchronize(st));
+    std::fprintf(stderr,
+                 "[pcg_split] d=%d iters=%d status=%d ns (vector CTA 0): publish-barrier %llu "
+                 "slice+barrier %llu reduce+barrier %llu cg-vector %llu other-vector %llu | "
+                 "slice CTA 0 compute %llu\n",
+                 d, stat[1], stat[0], h[0], h[1], h[2], h[5], h[3], h[4]);
   }
 }
 

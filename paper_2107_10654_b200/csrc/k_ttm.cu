@@ -1310,8 +1310,8 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last4(const double* __restrict__
 __device__ __forceinline__ int l5_rho(int m) {
   return (m & 12) | ((m & 1) << 1) | ((m >> 1) & 1);
 }
-template <bool FUSED, int ST>
-__global__ void __launch_bounds__(512, 1) k_ttm_last5(const __grid_constant__ CUtensorMap xmap,
+template <bool FUSED, int ST, bool PW>
+__global__ void __launch_bounds__(PW ? 544 : 512, 1) k_ttm_last5(const __grid_constant__ CUtensorMap xmap,
                                                       long long O, int I,
                                                       const double* __restrict__ A, int R,
                                                       double* __restrict__ T,
@@ -1353,7 +1353,8 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last5(const __grid_constant__ CU
   __syncthreads();
   const long long my_blocks = blockIdx.x < nrb ? (nrb - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const long long nitems = my_blocks * nchunks;
-  const bool producer = tid == 0;
+  // PW: a dedicated producer warp (warp 16) runs ahead of the ring; else thread 0 of warp 0
+  const bool producer = PW ? tid == 512 : tid == 0;
   auto issue = [&](long long q) {
     const int slot = (int)(q % ST);
     const long long rb = blockIdx.x + (q / nchunks) * gridDim.x;
@@ -1363,7 +1364,16 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last5(const __grid_constant__ CU
     tma_load_2d(dst, &xmap, c * BK, (int)(rb * BM2), &full[slot]);
     tma_load_2d(dst + kHalf, &xmap, c * BK + 16, (int)(rb * BM2), &full[slot]);
   };
-  if (producer)
+  if (PW && warp == 16) {
+    if (producer) {
+      for (long long q = 0; q < nitems; ++q) {
+        if (q >= ST) mbar_wait(&empty[q % ST], (unsigned)(((q / ST) - 1) & 1));
+        issue(q);
+      }
+    }
+    return;
+  }
+  if (!PW && producer)
     for (long long q = 0; q < ST - 1 && q < nitems; ++q) issue(q);
   // this lane's tile rows (rho of MMA rows g and g + 8)
   const int ra = l5_rho(g), rb8 = l5_rho(g + 8);
@@ -1376,7 +1386,7 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last5(const __grid_constant__ CU
     const long long rbk = blockIdx.x + (q / nchunks) * gridDim.x;
     const long long o0 = rbk * BM2 + wrow * ROWS;
     if (idle) continue;
-    if (producer && q + ST - 1 < nitems) {
+    if (!PW && producer && q + ST - 1 < nitems) {
       const long long qn = q + ST - 1;
       if (qn >= ST) mbar_wait(&empty[qn % ST], (unsigned)(((qn / ST) - 1) & 1));
       issue(qn);
@@ -1457,8 +1467,17 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last5(const __grid_constant__ CU
     }
   }
   if (FUSED) {
-    const double s = block_sum<512>(resid0 + resid1, red);
-    if (tid == 0) partial[blockIdx.x] = s;
+    // (a producer warp has exited: a named barrier over the 16 compute warps)
+    double v = resid0 + resid1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+    asm volatile("bar.sync 1, 512;" ::: "memory");
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < 16; ++w) tot += red[w];
+      partial[blockIdx.x] = tot;
+    }
   }
 }
 
@@ -1517,11 +1536,13 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
                        (size_t)ceil_div(I, 32) * 32 * 20 * 8;
   CUtensorMap xmap;
   if (!no_l5 && R <= 16 && smem5 <= 227 * 1024 && x_tensor_map(&xmap, X, O, I)) {
-    auto k = fused ? k_ttm_last5<true, kL5St> : k_ttm_last5<false, kL5St>;
+    static const bool pw = std::getenv("RTB_L5_NO_PW") == nullptr;
+    auto k = fused ? (pw ? k_ttm_last5<true, kL5St, true> : k_ttm_last5<true, kL5St, false>)
+                   : (pw ? k_ttm_last5<false, kL5St, true> : k_ttm_last5<false, kL5St, false>);
     set_max_smem(k, (int)smem5);
     const long long nrb = ceil_div<long long>(O, BM2);
     const int grid = (int)std::min<long long>(nrb, sm_count());
-    k<<<grid, 512, smem5, st>>>(xmap, O, I, A, R, T, P, partial, g_need);
+    k<<<grid, pw ? 544 : 512, smem5, st>>>(xmap, O, I, A, R, T, P, partial, g_need);
     RTB_LAUNCH_CHECK();
     count_variant(fused ? "k_ttm_last3_fused" : "k_ttm_last3");
     count_variant(fused ? "k_ttm_last5_fused" : "k_ttm_last5");

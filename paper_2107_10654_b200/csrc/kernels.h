@@ -211,6 +211,11 @@ bool pcg_supported(int d, int order, const int* ranks);
 // x = G^-1 b by Kronecker-preconditioned CG; status_dev[0] = 0 ok, 1 residual check
 // failed, 2 breakdown (non-SPD), 3 not applicable; status_dev[1] = iterations.
 // G is given as its last-mode blocks (gram_expand_blocks) + augmented diagonal.
+// the split-role form (order 3, R_3 = 16): the compact vech Gram S [m_1][m_2 * 136] is held
+// in shared memory across the solve (k_pcg_split); same contract as pcg_solve
+bool pcg_split_ok(int d, int order, const int* ranks);
+void pcg_solve_compact(const PcgSpec& spec, const double* S, const double* b, double* x,
+                       void* work, int* status_dev, cudaStream_t st);
 void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, double* x, void* work,
                int* status_dev, cudaStream_t st);
 

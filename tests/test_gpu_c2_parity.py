@@ -11,7 +11,7 @@ torch cuBLAS) where it does not (the reference's Jacobi SVD at d = 4096 takes ho
   * rung 3 at d = 4096: the sketched Gram/RHS built by k_vech_bucket5 +
     k_vech_contract3 from the oracle's own draws vs orc_kron_sketch_normal_eq
                                                                       (ref sketch_ridge.cpp:105-128)
-  * the PCG fast path k_pcg<16,16> (the C2 core solve) vs a LAPACK solve of the same
+  * the PCG fast path k_pcg_split (the C2 core solve) vs a LAPACK solve of the same
     sketched system                                                   (ref sketch_ridge.cpp:130-139)
 
 Every floating-point bar is c * kappa * eps with kappa the condition number of the system
@@ -174,7 +174,7 @@ def _torch_normal_eq(shape, ranks, factors, x, lam, idx, w):
 
 @pytest.mark.parametrize("kind", ["normal", "uniform"])
 def test_pcg_c2_core_solve_vs_lapack(oracle, rt, x_c2, kind):
-    """The C2 core update (s = 200,000, d = 4096) through k_pcg<16,16>: the GPU core vs
+    """The C2 core update (s = 200,000, d = 4096) through k_pcg_split: the GPU core vs
     x = G^-1 b by LAPACK on an independently built FP64 Gram of the same draws; the Gram
     itself vs the library's normal equations at C2's draw density (~195 data draws per
     i_1 bucket)."""
@@ -182,9 +182,9 @@ def test_pcg_c2_core_solve_vs_lapack(oracle, rt, x_c2, kind):
     shape, ranks, lam, s = x_c2.shape, (16, 16, 16), 1e-2, 200000
     core, factors = model(oracle, shape, ranks, kind, 11)
     xt = rt.Tensor.from_numpy(x_c2)
-    pcg = rt.variant_count("k_pcg<16,16>")
+    pcg = rt.variant_count("k_pcg_split")
     gcore, gidx, gw = rt.update_core_sketched(xt, rt.Model(core, factors, lam), s, 99)
-    assert rt.variant_count("k_pcg<16,16>") == pcg + 1, "C2 core solve did not take k_pcg<16,16>"
+    assert rt.variant_count("k_pcg_split") == pcg + 1, "C2 core solve did not take k_pcg_split"
     # the draws are the oracle's: indices bitwise; weights to the scores' agreement (the
     # scores come from the Cholesky route here, the oracle's from the Jacobi SVD: rung 2)
     oidx, ow = _oracle_draws(oracle, shape, ranks, factors, 99, s)

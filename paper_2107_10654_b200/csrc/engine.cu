@@ -921,7 +921,7 @@ class Engine {
     tmp_a_.ensure(mx * 8, st_);
     tmp_b_.ensure(mx * 8, st_);
     const long long nblk = std::max<long long>(
-        ttm_last_blocks((long long)(total_ / shape_[N_ - 1]), (int)shape_[N_ - 1],
+        ttm_last_parts_bound((long long)(total_ / shape_[N_ - 1]), (int)shape_[N_ - 1],
                         (int)ranks_[N_ - 1]),
         kNumSMs * 8);
     partial_.ensure(std::max<size_t>(nblk, kNumSMs * 4) * 8, st_);
@@ -1317,6 +1317,15 @@ class Engine {
       const int stride = std::max(eig_stride_, Rn * Rn);
       spd_small(kk, ns_one(Rn), stride, (double)Rn * DBL_EPSILON, linv_.as<double>(), pv, okf, 1,
                 st_, Rn);
+      if (std::getenv("RTB_DEBUG_FSK_SPD")) {
+        int okh = -1;
+        std::vector<double> kh((size_t)Rn * Rn);
+        RTB_CUDA(cudaMemcpyAsync(&okh, okf, 4, cudaMemcpyDeviceToHost, st_));
+        RTB_CUDA(cudaMemcpyAsync(kh.data(), kk, kh.size() * 8, cudaMemcpyDeviceToHost, st_));
+        RTB_CUDA(cudaStreamSynchronize(st_));
+        std::fprintf(stderr, "[fsk] mode %d ok %d diag %.3e %.3e offd %.3e sym %.3e\n", n, okh,
+                     kh[0], kh[(size_t)Rn * Rn - 1], kh[1], kh[1] - kh[Rn]);
+      }
       sym_eigen(kk, ns_one(Rn), Rn, stride, evals_.as<double>(), evecs_.as<double>(),
                 eig_status_.as<int>(), 1, st_, okf);
       k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one(Rn), stride,
@@ -1807,9 +1816,16 @@ class Engine {
       std::vector<uint64_t> dims;
       const double* P = build_P(dims);
       Scope sc(prof_, "ttm_last_loss");
-      ttm_last(x_, O, I, factor(N_ - 1), R, T_.as<double>(), P, partial, st_);
+      // sketched factor updates (R_n <= 32) never read T: the pass computes the residual alone
+      bool t_needed = opt_.factor_samples == 0 || N_ < 2;
+      for (int n = 0; n < N_; ++n) t_needed |= ranks_[n] > 32;
+      if (!t_needed && ttm_last_resid(x_, O, I, factor(N_ - 1), R, P, partial, st_)) {
+        t_valid_ = false;
+      } else {
+        ttm_last(x_, O, I, factor(N_ - 1), R, T_.as<double>(), P, partial, st_);
+        t_valid_ = true;
+      }
       nparts = ttm_last_blocks(O, I, R);
-      t_valid_ = true;
     } else {
       std::vector<uint64_t> dims;
       const double* P = build_P(dims);

@@ -996,6 +996,9 @@ __global__ void k_sum_partials(const double* __restrict__ partial, long long n,
 // ---------------------------------------------------------------------------
 // Host launchers.
 
+// grid of the last partial-producing last-mode launch of this host thread (ttm_last_blocks)
+static thread_local long long t_last_parts = -1;
+
 template <int RP, int VEC, bool FUSED>
 static void launch_last(const double* X, long long O, int I, const double* A, int R, double* T,
                         const double* P, double* partial, cudaStream_t st) {
@@ -1004,6 +1007,7 @@ static void launch_last(const double* X, long long O, int I, const double* A, in
   set_max_smem(k, (int)smem);
   const long long blocks = ceil_div<long long>(O, 64);
   k<<<(unsigned)blocks, 128, smem, st>>>(X, O, I, A, R, T, P, partial, g_need);
+  t_last_parts = blocks;
   RTB_LAUNCH_CHECK();
 }
 
@@ -1310,7 +1314,8 @@ __global__ void __launch_bounds__(512, 1) k_ttm_last4(const double* __restrict__
 __device__ __forceinline__ int l5_rho(int m) {
   return (m & 12) | ((m & 1) << 1) | ((m >> 1) & 1);
 }
-template <bool FUSED, int ST, bool PW>
+// RONLY (with FUSED): residual only, no T -- all 16 warps take residual column groups
+template <bool FUSED, int ST, bool PW, bool RONLY = false>
 __global__ void __launch_bounds__(PW ? 544 : 512, 1) k_ttm_last5(const __grid_constant__ CUtensorMap xmap,
                                                       long long O, int I,
                                                       const double* __restrict__ A, int R,
@@ -1331,7 +1336,9 @@ __global__ void __launch_bounds__(PW ? 544 : 512, 1) k_ttm_last5(const __grid_co
   __shared__ __align__(8) unsigned long long full[ST], empty[ST];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const bool rwarp = FUSED && warp >= 8;
+  const bool rwarp = FUSED && (RONLY || warp >= 8);
+  // residual column groups of this warp (8-column steps within the 32-column chunk)
+  const int nb_lo = RONLY ? 16 * (warp >> 3) : 0, nb_hi = RONLY ? nb_lo + 16 : 32;
   const int wrow = warp & 7;
   const bool idle = !FUSED && warp >= 8;
   const long long nrb = ceil_div<long long>(O, BM2);
@@ -1444,6 +1451,7 @@ __global__ void __launch_bounds__(PW ? 544 : 512, 1) k_ttm_last5(const __grid_co
     } else {
 #pragma unroll
       for (int nb = 0; nb < BK; nb += 8) {
+        if (RONLY && (nb < nb_lo || nb >= nb_hi)) continue;
         double b[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) b[v] = as[(size_t)(i0 + nb + g) * LDA + t + 4 * v];
@@ -1509,12 +1517,40 @@ static void launch_last2(const double* X, long long O, int I, const double* A, i
   const long long nrb = ceil_div<long long>(O, BM2);
   const int grid = (int)std::min<long long>(nrb, sm_count());
   k<<<grid, 512, smem, st>>>(X, O, I, A, R, T, P, partial, g_need, pg);
+  t_last_parts = grid;
   RTB_LAUNCH_CHECK();
+}
+
+bool ttm_last_resid(const double* X, long long O, int I, const double* A, int R, const double* P,
+                    double* partial, cudaStream_t st) {
+  static const bool no_l5 = std::getenv("RTB_NO_LAST5") != nullptr;
+  constexpr int kL5St = 4;
+  const size_t smem5 = (size_t)kL5St * 2 * BM2 * 16 * 8 + 1024 +
+                       (size_t)ceil_div(I, 32) * 32 * 20 * 8;
+  CUtensorMap xmap;
+  if (no_l5 || R > 16 || smem5 > 227 * 1024 || !x_tensor_map(&xmap, X, O, I)) return false;
+  auto k = k_ttm_last5<true, kL5St, true, true>;
+  set_max_smem(k, (int)smem5);
+  const long long nrb = ceil_div<long long>(O, BM2);
+  const int grid = (int)std::min<long long>(nrb, sm_count());
+  k<<<grid, 544, smem5, st>>>(xmap, O, I, A, R, nullptr, P, partial, g_need);
+  t_last_parts = grid;
+  RTB_LAUNCH_CHECK();
+  count_variant("k_ttm_last5_resid");
+  return true;
 }
 
 bool ttm_last_pgen_ok(int I, int R) { return R <= 32 && last2_ok(I, R); }
 
+long long ttm_last_parts_bound(long long O, int I, int R) {
+  (void)I;
+  (void)R;
+  return std::max(ceil_div<long long>(O, 64), std::min<long long>(ceil_div<long long>(O, BM2),
+                                                                   sm_count()));
+}
+
 long long ttm_last_blocks(long long O, int I, int R) {
+  if (t_last_parts >= 0) return t_last_parts;  // the launch just made by this thread
   if (last2_ok(I, R)) return std::min<long long>(ceil_div<long long>(O, BM2), sm_count());
   return ceil_div<long long>(O, 64);
 }
@@ -1543,6 +1579,7 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
     const long long nrb = ceil_div<long long>(O, BM2);
     const int grid = (int)std::min<long long>(nrb, sm_count());
     k<<<grid, pw ? 544 : 512, smem5, st>>>(xmap, O, I, A, R, T, P, partial, g_need);
+    t_last_parts = grid;
     RTB_LAUNCH_CHECK();
     count_variant(fused ? "k_ttm_last3_fused" : "k_ttm_last3");
     count_variant(fused ? "k_ttm_last5_fused" : "k_ttm_last5");
@@ -1556,6 +1593,7 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
     const long long nrb = ceil_div<long long>(O, BM2);
     const int grid = (int)std::min<long long>(nrb, sm_count());
     k<<<grid, 512, smem4, st>>>(X, O, I, A, R, T, P, partial, g_need);
+    t_last_parts = grid;
     RTB_LAUNCH_CHECK();
     count_variant(fused ? "k_ttm_last3_fused" : "k_ttm_last3");
     count_variant(fused ? "k_ttm_last4_fused" : "k_ttm_last4");
@@ -1568,6 +1606,7 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
     const long long nrb = ceil_div<long long>(O, BM2);
     const int grid = (int)std::min<long long>(nrb, sm_count());
     k<<<grid, 512, smem, st>>>(X, O, I, A, R, T, P, partial, g_need);
+    t_last_parts = grid;
     RTB_LAUNCH_CHECK();
     count_variant(fused ? "k_ttm_last3_fused" : "k_ttm_last3");
     return;

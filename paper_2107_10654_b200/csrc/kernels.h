@@ -49,7 +49,10 @@ __global__ void k_rows_times_small(const double* M, const double* P, int I, int 
 // While a guard is set (non-null), ttm_last / ttm_generic / ttm_expand / sum_partials
 // kernels do nothing unless *need != 0 at run time (nullptr clears the guard).
 void set_ttm_guard(const int* need);
+// partial count of the last ttm_last / ttm_last_resid launch of this host thread
 long long ttm_last_blocks(long long O, int I, int R);
+// upper bound on that count for any path (workspace sizing)
+long long ttm_last_parts_bound(long long O, int I, int R);
 // T (O x R) = X (O x I) A (I x R); if P != null also partial[block] = sum (X - P A^T)^2
 // With W != nullptr (3-way), P is not read but generated per row: P[(i1,i2),:] =
 // A2[i2,:] W[i1] with W = G x_1 A_1 (I1 x R2 x R3) -- saves writing / reading P.
@@ -57,6 +60,10 @@ void ttm_last(const double* X, long long O, int I, const double* A, int R, doubl
               const double* P, double* partial, cudaStream_t st, const double* W = nullptr,
               const double* A2 = nullptr, int I2 = 0, int R2 = 0);
 bool ttm_last_pgen_ok(int I, int R);
+// partial[block] = sum (X - P A^T)^2 alone (no T), when the tensor-map kernel applies
+// (R <= 16); false: not launched, use ttm_last. Same partial count as ttm_last_blocks.
+bool ttm_last_resid(const double* X, long long O, int I, const double* A, int R, const double* P,
+                    double* partial, cudaStream_t st);
 // out[o,r,j] = sum_i A[i,r] X[o,i,j]
 void ttm_mid(const double* X, long long O, int I, long long J, const double* A, int R, double* out,
              cudaStream_t st);

@@ -45,10 +45,13 @@ def test_als_factor_sketch_matches_oracle(oracle, rt, shape, ranks, lam, sc, sf,
     x = planted(shape, ranks, seed=3)
     o = oracle.als(x, ranks, lam=lam, sketched_core=1, max_iterations=sweeps, tolerance=0.0,
                    sample_count_override=sc, record_history=1, seed=5, factor_samples=sf)
+    resid = rt.variant_count("k_ttm_last5_resid")
     r = rt.als_run(rt.Tensor.from_numpy(x), ranks,
                    rt.options(lam=lam, sketched_core=1, max_iterations=sweeps, tolerance=0.0,
                               sample_count_override=sc, record_history=1, seed=5),
                    factor_samples=sf)
+    if shape[-1] % 2 == 0:  # sketched factor updates never read T: residual-only loss passes
+        assert rt.variant_count("k_ttm_last5_resid") > resid
     gh = r.history()
     assert [(h[0], h[1]) for h in gh] == [(h[0], h[1]) for h in o["history"]]
     floor = noise_floor(oracle, x, ranks, o, lam=lam, sketched_core=1, max_iterations=sweeps,

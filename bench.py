@@ -504,7 +504,7 @@ def run_our_arm(args):
 
     # roofline of the dominant kernel: the largest single kernel of the step, which in
     # the ncu launch list of this command (profiles/r01_launches_bench_v6.txt) is
-    # k_ttm_last3, the whole of the ttm_last_loss family. The library's other families
+    # k_ttm_last5, the whole of the ttm_last_loss family. The library's other families
     # group several kernels (gram: 8 launches, largest k_vech_bucket2; pcg: 5, largest
     # k_pcg); their own rooflines are in "families".
     dom = "ttm_last_loss" if "ttm_last_loss" in fam else max(fam, key=lambda k: fam[k][0])
@@ -534,7 +534,7 @@ def run_our_arm(args):
         tf = os.path.join(ROOT, "profiles", "r01_traffic.json")
         if os.path.exists(tf):
             traffic = json.load(open(tf)).get(dom)
-        roofline = {"kernel": dom + (" (k_ttm_last3)" if dom == "ttm_last_loss" else " (family)"),
+        roofline = {"kernel": dom + (" (k_ttm_last5)" if dom == "ttm_last_loss" else " (family)"),
                     "bound": bound, "achieved": achieved, "peak": peak,
                     "unit": unit, "frac": achieved / peak, "traffic": traffic,
                     "peak_source": peak_src, "work_per_launch": work,

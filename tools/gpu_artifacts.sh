@@ -15,7 +15,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   > gpurun_out/ncu_launch_$TAG.log 2>&1
 echo "ncu launch rc=$?" >> gpurun_out/ncu_launch_$TAG.log
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k "regex:^k_pcg$|k_ttm_last3|k_vech_bucket5|k_ttm_mid3|k_vech_contract2|k_fsk_accum3" -c 6 \
+  -k "regex:k_pcg_split|k_ttm_last5|k_vech_bucket5|k_ttm_mid5|k_vech_contract3" -c 5 \
   -o gpurun_out/full_$TAG python bench.py --steps 3 --warmup 3 --no-cpu-baseline --c2-only \
   > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/ncu_full_$TAG.log

@@ -611,6 +611,7 @@ def run_our_arm(args):
         torch.cuda.empty_cache()
         extra["c3"] = c3_lines(args, steps=min(args.steps, 20))
         extra["c4"] = c4_lines(args, steps=min(args.steps, 5), s_list=[100000, 1000000, 10000000])
+        extra["c5"] = c5_lines(args, steps=min(args.steps, 5))
 
     if rank == 0:
         sweeps_per_s = args.steps / (ms / 1e3)  # one job across all GPUs
@@ -895,6 +896,102 @@ def c3_lines(args, steps=None):
     return lines
 
 
+def c5_lines(args, steps=None):
+    """BASELINE config 5 (--workload c5): 3-way FP64 planted rank (32,32,32), 1% noise,
+    lambda = 1e-2, s_core = 1e6, X sharded along mode 1 with 34.4 GB (512 x 4096 x 2048) per
+    GPU: at N GPUs the tensor is (512 N) x 4096 x 2048, so N = 8 is BASELINE's 4096 x 4096 x 2048
+    (275 GB) and N = 1 is the one-GPU share of it run as a whole ALS problem (weak scaling).
+    Generated on the device shard by shard (rtucker_b200_tensor_generate_device); exact factor
+    updates (reference semantics) and, at N = 1, a sketched-factor line (1e5 samples)."""
+    import torch
+    from paper_2107_10654_b200 import rtucker as rt
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rt.set_stream(torch.cuda.current_stream().cuda_stream)
+    I1, lam, s = 512 * world, 1e-2, 1000000
+    shape, ranks = (I1, 4096, 2048), (32, 32, 32)
+    t = rt.Tensor.generate_device(shape, ranks, 0.01, 0, shard=(rank, world))
+    shard = rt.Shard(rank, world, I1, rt.torch_allreduce(dist)) if world > 1 else None
+    torch.cuda.synchronize()
+    steps = steps or args.steps
+    lines = []
+    for fs in ((0, 100000) if world == 1 else (0,)):
+        opts = rt.options(lam=lam, sketched_core=1, sample_count_override=s, tolerance=0.0,
+                          max_iterations=args.warmup + steps + 1)
+        sess = rt.Session(t, ranks, opts, factor_samples=fs, shard=shard)
+        sess.sweeps(args.warmup)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        clocks = Clocks(local)
+        clocks.wait_first()
+        clocks.mark_start()
+        e0.record()
+        sess.sweeps(steps)
+        e1.record()
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+        ms = e0.elapsed_time(e1) / steps
+        if dist:
+            tt = torch.tensor([ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        r = sess.result()
+        graph_sweeps = r.graph_sweeps
+        sess.free()
+        sp = rt.Session(t, ranks, rt.options(lam=lam, sketched_core=1, sample_count_override=s,
+                                             tolerance=0.0, max_iterations=args.warmup + 3),
+                        profile=True, factor_samples=fs, shard=shard)
+        sp.sweeps(args.warmup + 2)
+        fam = {}
+        for name, secs, n in sp.result().kernels():
+            fam[name] = fam.get(name, 0.0) + secs
+        sp.free()
+        tot = sum(fam.values()) or 1.0
+        line = {
+            "metric": "sketched Tucker-ALS sweeps/s (C5)", "value": 1e3 / ms, "unit": "sweeps/s",
+            "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": ms,
+            "scaling": "weak", "clocks": clk, "cuda_graph_sweeps": graph_sweeps,
+            "higher_is_better": True, "dtype": "f64",
+            "data": "synthetic (generated on the device from seed 0)",
+            "config": {"workload": f"C5 weak-scaling unit: 3-way FP64 {I1}x4096x2048 "
+                                   f"({8 * I1 * 4096 * 2048 / 1e9:.1f} GB, 34.4 GB per GPU; "
+                                   "N = 8 is BASELINE's 275 GB), planted rank (32,32,32) N(0,1) "
+                                   "+ 1% noise, lambda=1e-2, s_core=1,000,000 (d = 32768)",
+                       "factor_updates": "exact" if fs == 0 else f"sketched ({fs} samples)",
+                       "final_loss": r.final_loss,
+                       "parallelism": (f"X sharded along mode 1 over {world} GPUs, NCCL "
+                                       "all-reduce of partial sums" if world > 1
+                                       else "single GPU")},
+            "sketch": r.sketch_info(),
+            "kernel_share": {k: round(v / tot, 4) for k, v in sorted(fam.items(),
+                                                                    key=lambda kv: -kv[1])[:8]},
+        }
+        if rank == 0:
+            lines.append(line)
+    t.free()
+    torch.cuda.empty_cache()
+    return lines
+
+
+def run_c5(args):
+    for line in c5_lines(args):
+        print(json.dumps(line), flush=True)
+    if env_int("WORLD_SIZE", 1) > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def run_c3(args):
     for line in c3_lines(args):
         print(json.dumps(line), flush=True)
@@ -917,10 +1014,11 @@ def main():
     ap.add_argument("--c2-only", action="store_true",
                     help="only the C2 headline and its profiled re-run (for ncu launch lists): "
                          "implies --no-extra, skips the C1 head-to-head and the perf-mode line")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
                     help="c2 (default): the headline ALS sweep; c3: the BASELINE config-3 "
                          "4-way Pareto-factor sweep; c4: the BASELINE config-4 sampling + "
-                         "fiber gather/SYRK microbench")
+                         "fiber gather/SYRK microbench; c5: the BASELINE config-5 rank-32 "
+                         "sweep, 34.4 GB of X per GPU (N = 8: the 275 GB tensor)")
     ap.add_argument("--c4-s", default="1e5,1e6,1e7", help="sample counts for --workload c4")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -933,6 +1031,8 @@ def main():
         return run_c4(args)
     if args.workload == "c3":
         return run_c3(args)
+    if args.workload == "c5":
+        return run_c5(args)
     return run_our_arm(args)
 
 

@@ -125,6 +125,12 @@ void DevBuf::ensure(size_t b, cudaStream_t s) {
   st = s;
   bytes = b;
   if (b == 0) return;
+  static const bool trace = std::getenv("RTB_ALLOC_TRACE") != nullptr;  // debugging aid
+  if (trace && b >= (64u << 20)) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    std::fprintf(stderr, "[rtb alloc] %.3f GB (free %.3f GB)\n", b / 1e9, fr / 1e9);
+  }
   RTB_CUDA(cudaMallocAsync(&p, b, s));
 }
 
@@ -893,25 +899,28 @@ class Engine {
     pcg_status_.ensure(16, st_);
     ns_.ensure(64 * 4, st_);
     ranks_dev_.ensure(64 * 4, st_);
-    // T and P: (total / I_N) x R_N
-    const uint64_t tsz = total_ / shape_[N_ - 1] * ranks_[N_ - 1];
+    // T and P: (this shard's total / I_N) x R_N
+    const uint64_t tsz = ltotal_ / shape_[N_ - 1] * ranks_[N_ - 1];
     T_.ensure(tsz * 8, st_);
     P_.ensure(tsz * 8, st_);
-    // chain temporaries: largest intermediate of any TTM chain we run
+    // chain temporaries: largest intermediate of any TTM chain we run, on this shard's slab
+    // (a 275 GB C5 tensor is 34 GB per GPU at P = 8: nothing here may scale with the whole)
     uint64_t mx = d_;
     {
-      // X x_1 A_1^T: R_1 * total / I_1 ; P chain: prod I_{<N-1} * R_{>=N-1}...
+      // factor projections and the exact core: X (or T) x_m A_m^T over the other modes
       for (int n = 0; n < N_; ++n) {
-        std::vector<uint64_t> dims = shape_;
+        std::vector<uint64_t> dims = lshape_;
         for (int m = 0; m < N_; ++m) {
           if (m == n) continue;
           dims[m] = ranks_[m];
           mx = std::max(mx, prod(dims));
         }
       }
+      // P = G x_1 A_1 ... x_{N-1} A_{N-1} (build_P; the last mode stays R_N); the unsharded
+      // fast-loss Y chain runs on T, whose intermediates the projections above bound
       std::vector<uint64_t> dims = ranks_;
-      for (int m = 0; m < N_; ++m) {
-        dims[m] = shape_[m];
+      for (int m = 0; m + 1 < N_; ++m) {
+        dims[m] = lshape_[m];
         mx = std::max(mx, prod(dims));
       }
     }

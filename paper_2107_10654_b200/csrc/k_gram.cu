@@ -123,12 +123,16 @@ struct GramLayout {
   int* dmode;     // [N][s] mode indices
   double* rhs_part;  // [kRhsSplit][d]
   double* drow;   // [s][rowlen] concatenated factor rows of modes >= 2, bucket order
-  double* vt2;    // [I2][160] vech Khatri-Rao table of A_2 + raw rows (3-way, R <= 16)
-  double* vt3;    // [I3][160]
+  double* vt2;    // [I2][tab_width(m2)] vech Khatri-Rao table of A_2 (+ raw rows when R <= 16)
+  double* vt3;    // [I3][tab_width(m3)]
   int* border;    // [I1] compacted buckets, longest first (k_bucket_order)
   int* bcounter;  // [1] next bucket of the persistent k_vech_bucket3
   double* vt1;    // [I1][160] mode-1 table per compacted bucket (k_vech_table1)
 };
+
+// vech table row length of mode n: 160 (136 vech padded to 144 + the raw row, k_vech_bucket5)
+// for m_n <= 144; above that (R_n > 16, k_vech_bucket6) m_n rounded up to whole 144-wide tiles
+int tab_width(int m) { return m <= 144 ? 160 : (m + 143) / 144 * 144; }
 
 int key_bits(int I1) {
   int b = 1;
@@ -171,8 +175,8 @@ size_t carve(const GramSpec& spec, F&& take) {
   t(spec.s * 4 * (size_t)spec.order);          // dmode[n][k]
   t((size_t)kRhsSplit * spec.d * 8);           // rhs partials
   t(spec.s * (size_t)v.rowlen * 8);            // drow: factor rows (modes >= 2) per draw
-  t((size_t)(spec.order >= 2 ? spec.rows[1] : 1) * 160 * 8);  // vt2 (k_vech_table, ld 160)
-  t((size_t)(spec.order >= 3 ? spec.rows[2] : 1) * 160 * 8);  // vt3
+  t((size_t)(spec.order >= 2 ? spec.rows[1] : 1) * tab_width(spec.order >= 2 ? v.m[1] : 1) * 8);  // vt2
+  t((size_t)(spec.order >= 3 ? spec.rows[2] : 1) * tab_width(spec.order >= 3 ? v.m[2] : 1) * 8);  // vt3
   t((size_t)I1 * 4);                           // border
   t(16);                                       // bcounter
   t((size_t)I1 * 160 * 8);                     // vt1 (k_vech_table1)
@@ -1041,6 +1045,173 @@ __global__ void __launch_bounds__(kB5Threads, kB5CtaPerSm) k_vech_bucket5(
 
 size_t vech_bucket5_smem() { return (size_t)kB5St * kB5K * (2 * kB5Ld + 2) * 8 + 16; }
 
+// (B''') 3-way H_b for large ranks (m_2 or m_3 above 144 vech pairs; C5: R = 32, m = 528):
+// the H_b tile of k_vech_bucket5 (144 x 144, 18 consumer warps x 3 x 6 DMMA tiles, one producer
+// warp, TMA bulk copies into a full/empty mbarrier ring) becomes a work item (bucket, row tile,
+// column tile): per draw the producer copies the 144-wide slices [144 rt, 144 rt + 144) of the
+// V2 table row and [144 ct, ...) of the V3 table row (tables of width tab_width(m), zero past
+// m, L2-resident: C5 19 + 9 MB). Items run longest bucket first from an atomic counter. Warps
+// whose 24 rows or 48 columns lie wholly in the zero padding of an edge tile skip their DMMAs,
+// so the padded 576^2 tile grid costs (almost) only the 528^2 useful work on the shared FP64
+// pipe. h_b comes from k_bucket_h2.
+constexpr int kB6Ld = 144 + 4;            // staged slice stride (conflict-free fragment loads)
+__global__ void __launch_bounds__(kB5Threads, 1) k_vech_bucket6(
+    GramSpec spec, VechSpec v, int tw2, int tw3, const double* __restrict__ V2,
+    const double* __restrict__ V3, const int* __restrict__ dmode, const double* __restrict__ dw2,
+    const int* __restrict__ bstart, const int* __restrict__ blen,
+    const int* __restrict__ nbuckets, const int* __restrict__ order, int* counter,
+    double* __restrict__ H) {
+  extern __shared__ __align__(16) double smb[];
+  double* zr = smb;                                  // [St][K][Ld] V2 row slices
+  double* zc = zr + kB5St * kB5K * kB6Ld;            // [St][K][Ld] V3 row slices
+  double* w2s = zc + kB5St * kB5K * kB6Ld;           // [St][K]
+  __shared__ __align__(8) unsigned long long full[kB5St], empty[kB5St];
+  __shared__ int meta[kB5St][5];  // bucket (-1: no more work), row tile, col tile, draws, last
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T2 = tw2 / 144, T3 = tw3 / 144, TT = T2 * T3;
+  if (tid == 0) {
+    for (int i = 0; i < kB5St; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kB5Mma);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kB5Mma) {
+    // ---------------- producer ----------------
+    const int nb = *nbuckets;
+    const long long S = (long long)spec.s;
+    unsigned q = 0;
+    auto next_stage = [&]() {
+      const int sb = (int)(q % kB5St);
+      if (q >= kB5St) mbar_wait(&empty[sb], ((q / kB5St) - 1) & 1);
+      return sb;
+    };
+    auto fetch = [&](int& it, int& fb, int& fstart, int& flen) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(counter, 1);
+      it = __shfl_sync(0xffffffffu, t, 0);
+      fb = -1;
+      fstart = flen = 0;
+      if (it < TT * nb) {
+        fb = order[it / TT];
+        fstart = bstart[fb];
+        flen = blen[fb];
+      }
+    };
+    int nitem, nbk, nstart, nlen;
+    fetch(nitem, nbk, nstart, nlen);
+    for (;;) {
+      const int item = nitem, b = nbk, start = nstart, len = nlen;
+      if (item >= TT * nb) break;
+      fetch(nitem, nbk, nstart, nlen);
+      const int tile = item % TT, rt = tile / T3, ct = tile - rt * T3;
+      const int nch = (len + kB5K - 1) / kB5K;
+      for (int ch = 0; ch < nch; ++ch, ++q) {
+        const int sb = next_stage();
+        const int k0 = ch * kB5K, kn = min(kB5K, len - k0);
+        double* zrs = zr + sb * kB5K * kB6Ld;
+        double* zcs = zc + sb * kB5K * kB6Ld;
+        int i2 = 0, i3 = 0;
+        const bool ok = lane < kn;
+        if (lane < kB5K) {
+          if (ok) {
+            const long long dk = start + k0 + lane;
+            i2 = dmode[S + dk];
+            i3 = dmode[2 * S + dk];
+            w2s[sb * kB5K + lane] = dw2[dk];
+          } else if (lane < ((kn + 3) & ~3)) {  // padding draws of the last k-step
+            w2s[sb * kB5K + lane] = 0.0;
+            for (int c = 0; c < 144; ++c) zrs[lane * kB6Ld + c] = zcs[lane * kB6Ld + c] = 0.0;
+          }
+        }
+        if (lane == 0) {
+          meta[sb][0] = b;
+          meta[sb][1] = rt;
+          meta[sb][2] = ct;
+          meta[sb][3] = kn;
+          meta[sb][4] = ch == nch - 1;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&full[sb], 2u * 144u * 8u * (unsigned)kn);
+        __syncwarp();
+        if (ok) {
+          bulk_g2s(zrs + lane * kB6Ld, V2 + (long long)i2 * tw2 + rt * 144, 144 * 8, &full[sb]);
+          bulk_g2s(zcs + lane * kB6Ld, V3 + (long long)i3 * tw3 + ct * 144, 144 * 8, &full[sb]);
+        }
+      }
+    }
+    const int sb = next_stage();
+    if (lane == 0) {
+      meta[sb][0] = -1;
+      mbar_arrive(&full[sb]);
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int g = lane >> 2, t4 = lane & 3;
+  const int rg = warp / 3, cg = warp % 3;
+  double acc[3][6][2];
+  bool fresh = true;
+  for (unsigned q = 0;; ++q) {
+    const int sb = (int)(q % kB5St);
+    mbar_wait(&full[sb], (q / kB5St) & 1);
+    const int b = meta[sb][0];
+    if (b < 0) break;
+    const int rt = meta[sb][1], ct = meta[sb][2], kn = meta[sb][3], last = meta[sb][4];
+    if (fresh) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      fresh = false;
+    }
+    const long long row0 = (long long)rt * 144 + rg * 24, col0 = (long long)ct * 144 + cg * 48;
+    const bool live = row0 < v.Mrow && col0 < v.Ncol;  // warp-uniform
+    if (live) {
+      const int ksn = (kn + 3) >> 2;
+      const double* zrb = zr + sb * kB5K * kB6Ld + rg * 24 + g;
+      const double* zcb = zc + sb * kB5K * kB6Ld + cg * 48 + g;
+      const double* w2c = w2s + sb * kB5K;
+      for (int ks = 0; ks < ksn; ++ks) {
+        const int k = ks * 4 + t4;
+        const double wk = w2c[k];
+        double av[3], bv[6];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) av[i] = wk * zrb[k * kB6Ld + i * 8];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) bv[j] = zcb[k * kB6Ld + j * 8];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 6; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sb]);
+    if (last) {
+      if (live) {
+        double* Hb = H + (size_t)b * v.Hsz;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const long long row = row0 + i * 8 + g;
+          if (row >= v.Mrow) continue;
+#pragma unroll
+          for (int j = 0; j < 6; ++j) {
+            const long long cc = col0 + j * 8 + 2 * t4;
+            if (cc < v.Ncol) Hb[row * v.Ncol + cc] = acc[i][j][0];
+            if (cc + 1 < v.Ncol) Hb[row * v.Ncol + cc + 1] = acc[i][j][1];
+          }
+        }
+      }
+      fresh = true;
+    }
+  }
+}
+
+size_t vech_bucket6_smem() { return (size_t)kB5St * kB5K * (2 * kB6Ld + 1) * 8 + 16; }
+
 // h_b[p'] = sum_{t in b} w_t^2 x_t prod_{n>=1} a_n(i_n)[p_n] from the draw records.
 __global__ void __launch_bounds__(256) k_bucket_h2(GramSpec spec, const double* __restrict__ dwx,
                                                    const int* __restrict__ dmode,
@@ -1589,6 +1760,7 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
   const bool fused_h = whole && nr == 1 && nc == 1 && v.R[1] <= 16 && v.R[2] <= 16 &&
                        (v.Mrow + 7) / 8 < kBWarps;
   static const bool b5_off_g = std::getenv("RTB_NO_BUCKET5") != nullptr;
+  static const bool b6_off_g = std::getenv("RTB_NO_BUCKET6") != nullptr;
   // the 144 x 144-tile bucket kernel pays off for R_2 = R_3 = 16 (136 vech pairs) and
   // buckets long enough to fill its 24-draw stages (C2: ~195 draws per bucket)
   const bool b5 = fused_h && !b5_off_g && v.N == 3 && v.R[1] <= 16 && v.R[2] <= 16 &&
@@ -1655,6 +1827,29 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
     } else {
       by_groups(I0{});
     }
+  } else if (v.N == 3 && nr == 1 && nc == 1 && v.R[1] <= 32 && v.R[2] <= 32 && !b6_off_g) {
+    // large ranks (C5): table-gather tiles of 144 x 144
+    const int tw2 = tab_width(v.m[1]) == 160 ? 144 : tab_width(v.m[1]);
+    const int tw3 = tab_width(v.m[2]) == 160 ? 144 : tab_width(v.m[2]);
+    k_vech_table<<<(unsigned)ceil_div<long long>((long long)spec.rows[1] * tw2, 256), 256, 0, st>>>(
+        spec.factors[1], spec.rows[1], v.R[1], tw2, l.vt2);
+    RTB_LAUNCH_CHECK();
+    k_vech_table<<<(unsigned)ceil_div<long long>((long long)spec.rows[2] * tw3, 256), 256, 0, st>>>(
+        spec.factors[2], spec.rows[2], v.R[2], tw3, l.vt3);
+    RTB_LAUNCH_CHECK();
+    k_bucket_order<<<1, 1024, 0, st>>>(l.blen, l.nbuckets, l.border, l.bcounter);
+    RTB_LAUNCH_CHECK();
+    const size_t smb6 = vech_bucket6_smem();
+    set_max_smem(k_vech_bucket6, (int)smb6);
+    int dev = 0, sms = 0;
+    RTB_CUDA(cudaGetDevice(&dev));
+    RTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const long long items = (long long)(tw2 / 144) * (tw3 / 144) * I1;
+    k_vech_bucket6<<<(unsigned)std::min<long long>(items, sms), kB5Threads, smb6, st>>>(
+        spec, v, tw2, tw3, l.vt2, l.vt3, l.dmode, l.dw2, l.bstart, l.blen, l.nbuckets, l.border,
+        l.bcounter, l.H);
+    RTB_LAUNCH_CHECK();
+    count_variant("k_vech_bucket6");
   } else {
     const long long tiles_r = (v.Mrow + TB - 1) / TB, tiles_c = (v.Ncol + TB - 1) / TB;
     k_vech_bucket<<<dim3((unsigned)(tiles_r * tiles_c), I1), kTh,

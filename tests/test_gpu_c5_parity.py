@@ -1,0 +1,80 @@
+"""Parity of the rank-32 kernels the C5 line runs (BASELINE configs[4]: R = (32,32,32), d = 32768).
+
+  * rung 3: the sketched Gram/RHS of k_vech_bucket6 (144 x 144 tiles of the 528-pair vech
+    tables) + the contraction, from the oracle's own draws, vs orc_kron_sketch_normal_eq at
+    ranks (4, 32, 32) (d = 4096, where the oracle's row-by-row stream finishes in seconds)
+                                                                  (ref sketch_ridge.cpp:105-128)
+  * the large-d core solve (PCG on the blocked Gram) at R_2 = R_3 = 32 vs a cuSOLVER solve of
+    an independently built FP64 Gram of the same draws (the reference's Jacobi SVD at
+    d = 8192 .. 32768 takes days)                                 (ref sketch_ridge.cpp:130-139)
+
+Bars are c * kappa * eps with kappa printed, as in test_gpu_c2_parity.py.
+"""
+import numpy as np
+import pytest
+
+from tests.bars import frel
+from tests.test_gpu_c2_parity import _oracle_draws, _torch_normal_eq, model, planted
+
+pytestmark = pytest.mark.gpu
+
+EPS = np.finfo(np.float64).eps
+
+
+@pytest.mark.parametrize("shape,ranks", [((16, 64, 48), (4, 32, 32)),
+                                         ((12, 40, 64), (3, 20, 32))])
+def test_normal_equations_r32_from_oracle_sketch(oracle, rt, shape, ranks):
+    x = planted(shape, ranks, seed=51)
+    lam, s = 1e-2, 4000
+    core, factors = model(oracle, shape, ranks, "uniform", 13)
+    idx, w = _oracle_draws(oracle, shape, ranks, factors, 77, s)
+    b6 = rt.variant_count("k_vech_bucket6")
+    gg, grhs = rt.kron_normal_eq(shape, ranks, factors, x, lam, idx, w)
+    assert rt.variant_count("k_vech_bucket6") == b6 + 1, "large-rank Gram did not take bucket6"
+    og, orhs = oracle.kron_normal_eq(shape, ranks, factors, x, lam, idx, w)
+    dg = np.sqrt(np.outer(np.diag(og), np.diag(og)))
+    eg = float(np.max(np.abs(gg - og) / dg))
+    er = float(np.linalg.norm(grhs - orhs) / np.linalg.norm(orhs))
+    print(f"{ranks} rung 3: Gram {eg:.3e} (normalised), rhs {er:.3e}")
+    assert eg < 1e-12 and er < 1e-12
+
+
+def _kappa_spd(torch, G, L, iters=60):
+    """kappa_2 of an SPD matrix by power iteration on G (largest eigenvalue) and on G^-1
+    through its Cholesky factor (smallest): a d^2 per step instead of an O(d^3) eigensolve
+    (d = 32768); accurate to a few percent, which is all a c * kappa * eps bar needs."""
+    g = torch.Generator(device=G.device).manual_seed(0)
+    v = torch.randn(G.shape[0], 1, dtype=G.dtype, device=G.device, generator=g)
+    u = v.clone()
+    hi = lo = 1.0
+    for _ in range(iters):
+        v = G @ v
+        hi = float(v.norm())
+        v /= hi
+        u = torch.cholesky_solve(u, L)
+        lo = float(u.norm())
+        u /= lo
+    return hi * lo
+
+
+@pytest.mark.parametrize("shape,ranks,s", [((40, 64, 48), (8, 32, 32), 60000),
+                                           ((64, 64, 48), (32, 32, 32), 120000)])
+def test_pcg_r32_core_solve_vs_cusolver(oracle, rt, shape, ranks, s):
+    torch = pytest.importorskip("torch")
+    x = planted(shape, ranks, seed=52)
+    lam = 1e-2
+    core, factors = model(oracle, shape, ranks, "normal", 17)
+    xt = rt.Tensor.from_numpy(x)
+    gcore, gidx, gw = rt.update_core_sketched(xt, rt.Model(core, factors, lam), s, 5)
+    oidx, ow = _oracle_draws(oracle, shape, ranks, factors, 5, s)
+    assert np.array_equal(gidx, oidx)
+    G, b = _torch_normal_eq(shape, ranks, factors, x, lam, gidx, gw)
+    L = torch.linalg.cholesky(G)
+    xs = torch.cholesky_solve(b[:, None], L)[:, 0].cpu().numpy()
+    kappa = _kappa_spd(torch, G, L)
+    del G, L
+    torch.cuda.empty_cache()
+    err = frel(gcore, xs)
+    print(f"{ranks} d={int(np.prod(ranks))} core: kappa {kappa:.3e} err {err:.3e} "
+          f"err/(kappa eps) {err / (kappa * EPS):.3g}")
+    assert err < 64 * kappa * EPS, (kappa, err)

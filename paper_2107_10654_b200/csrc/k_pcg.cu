@@ -51,6 +51,9 @@ struct PcgShared {
   int m1;         // vech pairs of mode 1 (slices)
   int jc;         // generic slice matvec: each slice split into jc chunks of the middle
                   // index jm (work units m1 * jc, partial sums per chunk); 1 for fast3
+  int t32;        // tiled rank-32 matvec (slice_partials_t32): order 3, R_3 = 32, R_2 % 8 == 0
+  int ng;         // t32: groups of 8 middle indices (R_2 / 8)
+  int ntile;      // t32: tiles per slice, ng (ng + 1) / 2 (off-diagonal first)
 };
 
 struct PcgArgs {
@@ -456,6 +459,188 @@ __device__ void slice_partials(const PcgArgs& A, const PcgShared& sh, const doub
   }
 }
 
+// (A) tiled path, order 3 with R_3 == 32 (C5: d = 32768, 2.3 GB of blocks streamed from HBM
+// per matvec): every block B[u1][v(i2, j2)] (32 x 32, symmetric, 8 KB) is read ONCE and applied
+// to the four targets q_a(i2) <- p_b(j2), q_b(i2) <- p_a(j2), q_a(j2) <- p_b(i2),
+// q_b(j2) <- p_a(i2) (u1 = v(a, b)). Work unit = one warp on one tile of a slice: the blocks
+// (i2, j2) with i2 in group I and j2 in group J (groups of 8, I <= J; off-diagonal tiles, 64
+// blocks, are handed out first, then the 36-block diagonal ones) from an atomic ticket
+// counter, so the 16 warps of every CTA stay busy to the end of the matvec. Lane (rq, c) =
+// (l / 4, l % 4) holds rows rq + 8 rr (rr < 4), columns 8 h + 2 c + {0, 1} (h < 4) of a block:
+// each load instruction covers 8 rows x 64 contiguous bytes. Row targets q(i2) accumulate
+// in registers along a tile row, column targets q(j2) in the warp's shared accumulator; the
+// tile's result (both sides, both roles: 1024 doubles) goes to part[u1][tile]. Which warp
+// computes a tile does not change its value: the matvec is deterministic.
+__device__ __forceinline__ int t32_tile_of(int I, int J, int ng) {
+  return I == J ? ng * (ng - 1) / 2 + I : I * ng - I * (I + 1) / 2 + (J - I - 1);
+}
+
+__device__ void slice_partials_t32(const PcgArgs& A, const PcgShared& sh, const double* p,
+                                   double* accw, unsigned ticket_base) {
+  const int R2 = sh.R[1], dp = sh.dprime, ng = sh.ng;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rq = lane >> 2, c = lane & 3;
+  const int nod = ng * (ng - 1) / 2;
+  const unsigned nunits = (unsigned)sh.m1 * sh.ntile;
+  double* acc = accw + (size_t)w * 1024;
+  unsigned* tickets = A.counter + 8;
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(tickets, 1u) - ticket_base;
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= nunits) break;
+    int u1, tile, I, J;
+    if (t < (unsigned)sh.m1 * nod) {
+      u1 = (int)(t / nod);
+      tile = (int)(t % nod);
+      I = 0;
+      int rem = tile;
+      while (rem >= ng - 1 - I) {
+        rem -= ng - 1 - I;
+        ++I;
+      }
+      J = I + 1 + rem;
+    } else {
+      const unsigned v = t - (unsigned)sh.m1 * nod;
+      u1 = (int)(v / ng);
+      I = J = (int)(v % ng);
+      tile = nod + I;
+    }
+    int a, b;
+    pair_of(u1, sh.R[0], a, b);
+    const bool two_sides = a != b;
+    const double* Bs = A.B + (size_t)u1 * sh.mmid * 1024;
+    const double* pa = p + (size_t)a * dp;
+    const double* pb = p + (size_t)b * dp;
+    for (int e = lane; e < 1024; e += 32) acc[e] = 0.0;
+    __syncwarp();
+    for (int kk = 0; kk < 8; ++kk) {
+      const int i2 = 8 * I + kk;
+      double xbi[8], xai[8];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 vb = *reinterpret_cast<const double2*>(pb + i2 * 32 + 8 * h + 2 * c);
+        xbi[2 * h] = vb.x;
+        xbi[2 * h + 1] = vb.y;
+        const double2 va = two_sides ? *reinterpret_cast<const double2*>(pa + i2 * 32 + 8 * h + 2 * c)
+                                     : make_double2(0.0, 0.0);
+        xai[2 * h] = va.x;
+        xai[2 * h + 1] = va.y;
+      }
+      double y0[4] = {0.0, 0.0, 0.0, 0.0}, y2[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int jj = (I == J ? kk : 0); jj < 8; ++jj) {
+        const int j2 = 8 * J + jj;
+        const double* blk = Bs + (size_t)upper_pair(i2, j2, R2) * 1024;
+        double2 g[4][4];
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            g[rr][h] = __ldcs(reinterpret_cast<const double2*>(blk + (rq + 8 * rr) * 32 + 8 * h + 2 * c));
+        double xbj[8], xaj[8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const double2 vb = *reinterpret_cast<const double2*>(pb + j2 * 32 + 8 * h + 2 * c);
+          xbj[2 * h] = vb.x;
+          xbj[2 * h + 1] = vb.y;
+          const double2 va = *reinterpret_cast<const double2*>(pa + j2 * 32 + 8 * h + 2 * c);
+          xaj[2 * h] = va.x;
+          xaj[2 * h + 1] = va.y;
+        }
+        const bool off = j2 != i2;
+        double t1[4], t3[4];
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          double s0 = 0.0, s2 = 0.0, s1 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const double2 gg = g[rr][h];
+            s0 = fma(gg.x, xbj[2 * h], s0);
+            s0 = fma(gg.y, xbj[2 * h + 1], s0);
+            s2 = fma(gg.x, xaj[2 * h], s2);
+            s2 = fma(gg.y, xaj[2 * h + 1], s2);
+            s1 = fma(gg.x, xbi[2 * h], s1);
+            s1 = fma(gg.y, xbi[2 * h + 1], s1);
+            s3 = fma(gg.x, xai[2 * h], s3);
+            s3 = fma(gg.y, xai[2 * h + 1], s3);
+          }
+          y0[rr] += s0;
+          y2[rr] += s2;
+          t1[rr] = s1;
+          t3[rr] = s3;
+        }
+        if (off) {  // column targets q_a(j2), q_b(j2): sum over the 4 column lanes
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) {
+            t1[rr] += __shfl_xor_sync(0xffffffffu, t1[rr], 1);
+            t1[rr] += __shfl_xor_sync(0xffffffffu, t1[rr], 2);
+            t3[rr] += __shfl_xor_sync(0xffffffffu, t3[rr], 1);
+            t3[rr] += __shfl_xor_sync(0xffffffffu, t3[rr], 2);
+          }
+          if (c == 0) {
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+              acc[(1 * 8 + jj) * 32 + rq + 8 * rr] += t1[rr];        // side 0, role 1
+              acc[(3 * 8 + jj) * 32 + rq + 8 * rr] += t3[rr];        // side 1, role 1
+            }
+          }
+          __syncwarp();
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        y0[rr] += __shfl_xor_sync(0xffffffffu, y0[rr], 1);
+        y0[rr] += __shfl_xor_sync(0xffffffffu, y0[rr], 2);
+        y2[rr] += __shfl_xor_sync(0xffffffffu, y2[rr], 1);
+        y2[rr] += __shfl_xor_sync(0xffffffffu, y2[rr], 2);
+      }
+      if (c == 0) {
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          acc[(0 * 8 + kk) * 32 + rq + 8 * rr] += y0[rr];             // side 0, role 0
+          acc[(2 * 8 + kk) * 32 + rq + 8 * rr] += y2[rr];             // side 1, role 0
+        }
+      }
+      __syncwarp();
+    }
+    double* out = A.part + ((size_t)u1 * sh.ntile + tile) * 1024;
+    const int ne = two_sides ? 1024 : 512;
+    for (int e = lane; e < ne; e += 32) out[e] = acc[e];
+    __syncwarp();
+  }
+}
+
+// (B) own rows for the tiled path: q[i1, i2, r] = sum over j1 (slice v(i1, j1), side i1 > j1)
+// of the tiles holding i2 as a row (role 0) or column (role 1) target, in a fixed order.
+__device__ void reduce_rows_t32(const PcgArgs& A, const PcgShared& sh, const double* p, int row0,
+                                int nrows, double* qout) {
+  const int dp = sh.dprime, R1 = sh.R[0], ng = sh.ng;
+  for (int e = row0 + threadIdx.x; e < row0 + nrows; e += kThreads) {
+    const int i1 = e / dp, rest = e - i1 * dp;
+    const int i2 = rest >> 5, r = rest & 31;
+    const int G = i2 >> 3, k = i2 & 7;
+    double s = 0.0;
+#pragma unroll 4
+    for (int j1 = 0; j1 < R1; ++j1) {
+      const int u1 = upper_pair(min(i1, j1), max(i1, j1), R1);
+      const int side = i1 <= j1 ? 0 : 1;
+      const double* base = A.part + (size_t)u1 * sh.ntile * 1024 + (size_t)(side * 2) * 256 + k * 32 + r;
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        // role 0: tiles (G, J), J >= G; role 1: tiles (I, G), I <= G
+        v[q] = (G + q < ng) ? __ldcg(base + (size_t)t32_tile_of(G, G + q, ng) * 1024) : 0.0;
+        v[4 + q] = (q <= G) ? __ldcg(base + 256 + (size_t)t32_tile_of(q, G, ng) * 1024) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += v[q];
+    }
+    const int cnt = __ldg(A.aug_count + e);
+    if (cnt > 0) s = fma((double)cnt * A.aug_term, p[e], s);
+    qout[e] = s;
+  }
+}
+
 // (A) fast path, order 3 with R_3 == 16: every unordered middle pair (i2 <= j2)
 // of the slice is read ONCE (one 2 KB block) and applied to the four (side,
 // orientation) targets -- q_a(i2) += B p_b(j2), q_a(j2) += B p_b(i2), q_b(i2) +=
@@ -668,8 +853,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   double* red = big ? VTs + sh.order * RM * RM : xs + dv;
   // fast order-3 matvec: per-warp accumulators, in s0/s1 when they are large enough
   const bool fast3 = sh.order == 3 && sh.last == 16 && !big;
+  const int row0 = min(d, (int)blockIdx.x * sh.rows_per_cta);
+  const int nrows = min(d, row0 + sh.rows_per_cta) - row0;
   const size_t acc_need = (size_t)kWarps * 2 * sh.dprime;
   double* accw = acc_need <= (size_t)2 * dv ? s0 : red + 32;
+  // tiled rank-32 matvec (large d): per-warp tile accumulators after red
+  const bool t32 = big && sh.t32;
+  double* acc32 = red + 32;
+  unsigned mv = 0;  // matvecs so far: ticket base of the next one
+  const unsigned tick_per = (unsigned)sh.m1 * sh.ntile + gridDim.x * kWarps;
+  auto mv_partials = [&]() {
+    if (t32) slice_partials_t32(A, sh, p, acc32, (mv++) * tick_per);
+    else if (fast3) slice_partials_n3(A, sh, p, accw);
+    else slice_partials<RM>(A, sh, p);
+  };
+  auto mv_reduce = [&]() {
+    if (t32) reduce_rows_t32(A, sh, p, row0, nrows, A.q);
+    else if (fast3) reduce_rows<true>(A, sh, p, row0, nrows, A.q);
+    else reduce_rows<false>(A, sh, p, row0, nrows, A.q);
+  };
 
   // applicability: every augmented column drawn (then G >= lambda * min c_j > 0)
   // and every factor Gram Cholesky-factorable (the preconditioner)
@@ -733,8 +935,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   }
   __syncthreads();
 
-  const int row0 = min(d, (int)blockIdx.x * sh.rows_per_cta);
-  const int nrows = min(d, row0 + sh.rows_per_cta) - row0;
   unsigned sync_target = 0;
 
   double bb = 0.0;
@@ -757,13 +957,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
       p[e] = x0;
     }
     __syncthreads();
-    if (fast3) slice_partials_n3(A, sh, p, accw);
-    else slice_partials<RM>(A, sh, p);
+    mv_partials();
     __syncthreads();
     sync_target += gridDim.x;
     grid_barrier(A.counter, sync_target);
-    if (fast3) reduce_rows<true>(A, sh, p, row0, nrows, A.q);
-    else reduce_rows<false>(A, sh, p, row0, nrows, A.q);
+    mv_reduce();
     __syncthreads();
     sync_target += gridDim.x;
     grid_barrier(A.counter, sync_target);
@@ -801,15 +999,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
     t0 = t1;                            \
   }
   for (; it < A.max_iter; ++it) {
-    if (fast3) slice_partials_n3(A, sh, p, accw);
-    else slice_partials<RM>(A, sh, p);
+    mv_partials();
     __syncthreads();
     RTB_PCG_MARK(0)
     sync_target += gridDim.x;
     grid_barrier(A.counter, sync_target);
     RTB_PCG_MARK(1)
-    if (fast3) reduce_rows<true>(A, sh, p, row0, nrows, A.q);
-    else reduce_rows<false>(A, sh, p, row0, nrows, A.q);
+    mv_reduce();
     __syncthreads();
     RTB_PCG_MARK(2)
     sync_target += gridDim.x;
@@ -863,12 +1059,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   }
   xx = block_sum_det(xx, red);
   for (int e = row0 + threadIdx.x; e < row0 + nrows; e += kThreads) A.x[e] = xs[e];
-  if (fast3) slice_partials_n3(A, sh, p, accw);
-  else slice_partials<RM>(A, sh, p);
+  mv_partials();
   sync_target += gridDim.x;
   grid_barrier(A.counter, sync_target);
-  if (fast3) reduce_rows<true>(A, sh, p, row0, nrows, A.q);
-    else reduce_rows<false>(A, sh, p, row0, nrows, A.q);
+  mv_reduce();
   __syncthreads();
   double res = 0.0;
   for (int e = row0 + threadIdx.x; e < row0 + nrows; e += kThreads) {
@@ -1425,6 +1619,16 @@ static bool pcg_big(int d, int order, const int* ranks) {
 }
 static size_t pcg_smem_big(int order, int rm) { return 8 * (2 * (size_t)order * rm * rm + 32); }
 
+// tiled rank-32 matvec (slice_partials_t32): large d, order 3, R_3 = 32, R_2 a multiple of 8
+static bool pcg_t32(int d, int order, const int* ranks) {
+  static const bool off = std::getenv("RTB_NO_PCG_T32") != nullptr;  // experiments
+  return !off && order == 3 && ranks[2] == 32 && ranks[1] % 8 == 0 && pcg_big(d, order, ranks);
+}
+static int t32_ntile(const int* ranks) {
+  const int ng = ranks[1] / 8;
+  return ng * (ng + 1) / 2;
+}
+
 // chunks per slice of the generic matvec: about three work units per SM (fast3: 1)
 static int pcg_jc(int d, int order, const int* ranks) {
   const bool fast3 = order == 3 && ranks[2] == 16 && !pcg_big(d, order, ranks);
@@ -1440,7 +1644,9 @@ static int pcg_jc(int d, int order, const int* ranks) {
 static size_t pcg_base_bytes(int d, int order, const int* ranks) {
   const size_t m1 = (size_t)ranks[0] * (ranks[0] + 1) / 2;
   const size_t dp = (size_t)d / ranks[0];
-  return ((size_t)d + m1 * pcg_jc(d, order, ranks) * 2 * dp + 1024) * 8 + 256 +
+  const size_t part = pcg_t32(d, order, ranks) ? m1 * t32_ntile(ranks) * 1024
+                                               : m1 * pcg_jc(d, order, ranks) * 2 * dp;
+  return ((size_t)d + part + 1024) * 8 + 256 +
          ((size_t)d + 32) * 8;  // + the split form's published source and selector
 }
 
@@ -1481,7 +1687,11 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   sh.jc = pcg_jc(d, spec.order, spec.ranks);
   const int rm = rank_bucket(spec.order, spec.ranks);
   const bool big = pcg_big(d, spec.order, spec.ranks);
-  const size_t smem = big ? pcg_smem_big(spec.order, rm) : pcg_smem(d, spec.order, spec.ranks, rm);
+  sh.t32 = pcg_t32(d, spec.order, spec.ranks) ? 1 : 0;
+  sh.ng = spec.ranks[1] / 8;
+  sh.ntile = t32_ntile(spec.ranks);
+  const size_t smem = big ? pcg_smem_big(spec.order, rm) + (sh.t32 ? (size_t)kWarps * 1024 * 8 : 0)
+                          : pcg_smem(d, spec.order, spec.ranks, rm);
 
   char* w = static_cast<char*>(work);
   PcgArgs a{};
@@ -1490,7 +1700,7 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   a.x = x;
   a.q = reinterpret_cast<double*>(w);
   a.part = a.q + d;
-  a.rpart = a.part + (size_t)sh.m1 * sh.jc * 2 * sh.dprime;
+  a.rpart = a.part + (sh.t32 ? (size_t)sh.m1 * sh.ntile * 1024 : (size_t)sh.m1 * sh.jc * 2 * sh.dprime);
   a.counter = reinterpret_cast<unsigned*>(a.rpart + 1024);
   a.vglobal = nullptr;
   if (big) {  // after the counter block (pcg_work_bytes(d, order, ranks))
@@ -1533,6 +1743,7 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   RTB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, st));
   RTB_LAUNCH_CHECK();
   if (!big && all16) count_variant("k_pcg<16,16>");
+  if (sh.t32) count_variant("k_pcg_t32");
   if (prof_on) {
     unsigned long long h[16];
     int stat[2];

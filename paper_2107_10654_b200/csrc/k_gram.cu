@@ -1244,6 +1244,56 @@ __global__ void __launch_bounds__(256) k_bucket_h2(GramSpec spec, const double* 
   }
 }
 
+// h_b for order 3 with the draws' raw factor rows staged in shared memory, 64 draws per
+// chunk (C5: ~980 draws x 1024 outputs per bucket; k_bucket_h2's per-output chains of
+// dependent gathers took 2.7 ms there): h_b[p2, p3] = sum_k (w^2 x)_k a_2(i2_k)[p2] a_3(i3_k)[p3].
+constexpr int kH4K = 64;
+__global__ void __launch_bounds__(256) k_bucket_h4(GramSpec spec, const double* __restrict__ dwx,
+                                                   const int* __restrict__ dmode,
+                                                   const int* __restrict__ bstart,
+                                                   const int* __restrict__ blen,
+                                                   const int* __restrict__ nbuckets,
+                                                   double* __restrict__ h) {
+  __shared__ double f2[kH4K][33], f3[kH4K][33], wx[kH4K];
+  const int b = blockIdx.x;
+  if (b >= *nbuckets) return;
+  const int R2 = spec.ranks[1], R3 = spec.ranks[2], dp = spec.dprime;
+  const int start = bstart[b], len = blen[b];
+  const double* A2 = spec.factors[1];
+  const double* A3 = spec.factors[2];
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int p2[4], p3[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int pp = threadIdx.x + 256 * j;
+    p2[j] = pp < dp ? pp / R3 : 0;
+    p3[j] = pp < dp ? pp - (pp / R3) * R3 : 0;
+  }
+  for (int k0 = 0; k0 < len; k0 += kH4K) {
+    const int kn = min(kH4K, len - k0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kn * 32; e += 256) {
+      const int k = e >> 5, c = e & 31;
+      const long long dk = (long long)start + k0 + k;
+      const int i2 = __ldg(dmode + spec.s + dk), i3 = __ldg(dmode + 2 * spec.s + dk);
+      f2[k][c] = c < R2 ? __ldg(A2 + (size_t)i2 * R2 + c) : 0.0;
+      f3[k][c] = c < R3 ? __ldg(A3 + (size_t)i3 * R3 + c) : 0.0;
+      if (c == 0) wx[k] = __ldg(dwx + dk);
+    }
+    __syncthreads();
+    for (int k = 0; k < kn; ++k) {
+      const double w = wx[k];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] = fma(w * f2[k][p2[j]], f3[k][p3[j]], acc[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int pp = threadIdx.x + 256 * j;
+    if (pp < dp) h[(size_t)b * dp + pp] = acc[j];
+  }
+}
+
 // h_b from the contiguous draw records (drow rows are shared by the whole CTA -> L1).
 __global__ void __launch_bounds__(256) k_bucket_h3(GramSpec spec, VechSpec v,
                                                    const double* __restrict__ dwx,
@@ -1859,6 +1909,9 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
   }
   if (whole && !fused_h) {
     k_bucket_h3<<<I1, 256, 0, st>>>(spec, v, l.dwx, l.drow, l.bstart, l.blen, l.nbuckets, l.h);
+    RTB_LAUNCH_CHECK();
+  } else if (!fused_h && v.N == 3 && v.R[1] <= 32 && v.R[2] <= 32 && spec.dprime <= 1024) {
+    k_bucket_h4<<<I1, 256, 0, st>>>(spec, l.dwx, l.dmode, l.bstart, l.blen, l.nbuckets, l.h);
     RTB_LAUNCH_CHECK();
   } else if (!fused_h) {
     k_bucket_h2<<<I1, 256, 0, st>>>(spec, l.dwx, l.dmode, l.bstart, l.blen, l.nbuckets, l.h);

@@ -695,14 +695,15 @@ static bool x_tensor_map(CUtensorMap* m, const double* X, long long O, int I) {
 }
 
 // X (O, I, J) row-major FP64 as 16 (j) x kMid5KB (i) x 1 (o) boxes, SWIZZLE_128B, zero OOB fill
-static bool mid_tensor_map(CUtensorMap* m, const double* X, long long O, int I, long long J) {
+static bool mid_tensor_map(CUtensorMap* m, const double* X, long long O, int I, long long J,
+                           int kb = kMid5KB) {
   auto enc = tmap_encode();
   if (!enc || (J % 2) || (reinterpret_cast<uintptr_t>(X) & 15) || J >= (1LL << 31) ||
       O >= (1LL << 31))
     return false;
   cuuint64_t dims[3] = {(cuuint64_t)J, (cuuint64_t)I, (cuuint64_t)O};
   cuuint64_t strides[2] = {(cuuint64_t)J * 8, (cuuint64_t)I * J * 8};
-  cuuint32_t box[3] = {16, (cuuint32_t)kMid5KB, 1};
+  cuuint32_t box[3] = {16, (cuuint32_t)kb, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(X), dims, strides, box,
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -717,23 +718,24 @@ static bool mid_tensor_map(CUtensorMap* m, const double* X, long long O, int I, 
 // kappa = 4 ks + t of each 16-row block reads X row sigma(kappa) = 2 t + (ks & 1) + 8 (ks >> 1)
 // (rows 2t + b sit in distinct 16-byte chunk pairs after the XOR), and A^T is staged with its
 // columns in the same order.
-template <int RP>
+// Rank 32 (C5): A^T (32 x I) takes 132 KB of shared memory at I = 512, so the ring holds five
+// stages of 16-row boxes (KB = 16) instead of four of 32.
+template <int RP, int KB = kMid5KB, int S = kMid5St>
 __global__ void __launch_bounds__(288, 1) k_ttm_mid5(const __grid_constant__ CUtensorMap xmap,
                                                      long long O, int I, long long J,
                                                      const double* __restrict__ A, int R,
                                                      double* __restrict__ out) {
-  constexpr int S = kMid5St;
-  constexpr int kBox = kMid5KB * 16;  // doubles per box
+  constexpr int kBox = KB * 16;  // doubles per box
   extern __shared__ __align__(1024) double sm5m[];
   double* xs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sm5m) + 1023) & ~uintptr_t(1023));
   double* at = xs + (size_t)S * 8 * kBox;  // [RP][LDT], columns in sigma order
   __shared__ __align__(8) unsigned long long full[S], empty[S];
-  const int Ip = ceil_div(I, kMid5KB) * kMid5KB;
+  const int Ip = ceil_div(I, KB) * KB;
   const int LDT = Ip + 4;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const long long ntiles = O * J / BJ2;
-  const int nchunks = ceil_div(I, kMid5KB);
+  const int nchunks = ceil_div(I, KB);
   for (int e = tid; e < RP * LDT; e += blockDim.x) {
     const int r = e / LDT, i = e - r * LDT;
     const int kap = i & 15;
@@ -762,7 +764,7 @@ __global__ void __launch_bounds__(288, 1) k_ttm_mid5(const __grid_constant__ CUt
         double* dst = xs + (size_t)st * 8 * kBox;
         mbar_arrive_expect_tx(&full[st], 8u * kBox * 8u);
         for (int w = 0; w < 8; ++w)
-          tma_load_3d(dst + w * kBox, &xmap, (int)(j0 + 16 * w), c * kMid5KB, (int)o, &full[st]);
+          tma_load_3d(dst + w * kBox, &xmap, (int)(j0 + 16 * w), c * KB, (int)o, &full[st]);
       }
     }
     return;
@@ -779,9 +781,9 @@ __global__ void __launch_bounds__(288, 1) k_ttm_mid5(const __grid_constant__ CUt
     }
     mbar_wait(&full[st], (unsigned)((q / S) & 1));
     const double* xb = xs + (size_t)st * 8 * kBox + warp * kBox;
-    const int i0 = c * kMid5KB;
+    const int i0 = c * KB;
 #pragma unroll
-    for (int ks = 0; ks < kMid5KB / 4; ++ks) {
+    for (int ks = 0; ks < KB / 4; ++ks) {
       double af[RP / 8];
 #pragma unroll
       for (int mt = 0; mt < RP / 8; ++mt) af[mt] = at[(size_t)(mt * 8 + g) * LDT + i0 + ks * 4 + t];
@@ -816,9 +818,9 @@ __global__ void __launch_bounds__(288, 1) k_ttm_mid5(const __grid_constant__ CUt
     }
   }
 }
-static size_t mid5_smem(int I, int rp) {
-  const size_t ip = (size_t)ceil_div(I, kMid5KB) * kMid5KB;
-  return (size_t)kMid5St * 8 * kMid5KB * 16 * 8 + 1024 + (size_t)rp * (ip + 4) * 8;
+static size_t mid5_smem(int I, int rp, int kb = kMid5KB, int st = kMid5St) {
+  const size_t ip = (size_t)ceil_div(I, kb) * kb;
+  return (size_t)st * 8 * kb * 16 * 8 + 1024 + (size_t)rp * (ip + 4) * 8;
 }
 
 static size_t mid3_smem(int I, int rp) {
@@ -1705,6 +1707,19 @@ static void launch_mid2(const double* X, long long O, int I, long long J, const 
     count_variant("k_ttm_mid5");
     return;
   }
+  if constexpr (RP > 16) {
+    // rank 32: 16-row boxes, five stages
+    const size_t smem6 = mid5_smem(I, RP, 16, 5);
+    if (!no_m5 && !probe && smem6 <= 227 * 1024 - 2048 && mid_tensor_map(&xmap, X, O, I, J, 16)) {
+      set_max_smem(k_ttm_mid5<RP, 16, 5>, (int)smem6);
+      const long long ntiles = O * J / BJ2;
+      const int grid = (int)std::min<long long>(ntiles, sm_count());
+      k_ttm_mid5<RP, 16, 5><<<grid, 288, smem6, st>>>(xmap, O, I, J, A, R, out);
+      RTB_LAUNCH_CHECK();
+      count_variant("k_ttm_mid5<32>");
+      return;
+    }
+  }
   if (pc && smem3 <= 227 * 1024 - 2048) {
     auto k3 = probe ? k_ttm_mid3<RP, false> : k_ttm_mid3<RP, true>;
     set_max_smem(k3, 227 * 1024 - 2048);
@@ -1733,7 +1748,16 @@ void ttm_mid(const double* X, long long O, int I, long long J, const double* A, 
     // persistent path: whole 128-column tiles, enough of them to keep every SM busy,
     // and A resident next to the pipeline
     const size_t smem = mid2_smem(I, rp);
-    if (J % BJ2 == 0 && O * J / BJ2 >= 4LL * sm_count() && smem <= 220 * 1024) {
+    const bool tiles_ok = J % BJ2 == 0 && O * J / BJ2 >= 4LL * sm_count();
+    // rank 32 with I beyond k_ttm_mid2's shared memory (C5: I = 512): the 16-row-box mid5 only
+    static const bool no_m5 = std::getenv("RTB_NO_MID5") != nullptr;
+    CUtensorMap probe_map;
+    if (tiles_ok && smem > 220 * 1024 && rp == 32 && !no_m5 &&
+        mid5_smem(I, 32, 16, 5) <= 227 * 1024 - 2048 && mid_tensor_map(&probe_map, X, O, I, J, 16)) {
+      launch_mid2<32>(X, O, I, J, A, R, out, st);
+      return;
+    }
+    if (tiles_ok && smem <= 220 * 1024) {
       switch (rp) {
         case 8: launch_mid2<8>(X, O, I, J, A, R, out, st); return;
         case 16: launch_mid2<16>(X, O, I, J, A, R, out, st); return;

@@ -78,3 +78,48 @@ def test_pcg_r32_core_solve_vs_cusolver(oracle, rt, shape, ranks, s):
     print(f"{ranks} d={int(np.prod(ranks))} core: kappa {kappa:.3e} err {err:.3e} "
           f"err/(kappa eps) {err / (kappa * EPS):.3g}")
     assert err < 64 * kappa * EPS, (kappa, err)
+
+
+def _torch_update_factor(torch, x, core, factors, lam, mode):
+    """Independent FP64 update_factor on the GPU (ref tucker.cpp:70-89): A_n = X_(n) K^T
+    (K K^T + lam I)^-1 with K = G_(n) (kron_{m != n} A_m)^T, formed by mode products."""
+    dev = "cuda"
+    y = torch.from_numpy(x).to(dev)
+    A = [torch.from_numpy(np.ascontiguousarray(f)).to(dev) for f in factors]
+    G = torch.from_numpy(np.ascontiguousarray(core)).to(dev)
+    q = G
+    for m in range(len(factors)):
+        if m == mode:
+            continue
+        y = torch.movedim(torch.tensordot(A[m].T, y, dims=([1], [m])), 0, m)
+        q = torch.movedim(torch.tensordot(A[m].T @ A[m], q, dims=([1], [m])), 0, m)
+    yn = torch.movedim(y, mode, 0).reshape(x.shape[mode], -1)
+    gn = torch.movedim(G, mode, 0).reshape(core.shape[mode], -1)
+    qn = torch.movedim(q, mode, 0).reshape(core.shape[mode], -1)
+    M = yn @ gn.T
+    kk = gn @ qn.T + lam * torch.eye(core.shape[mode], dtype=torch.float64, device=dev)
+    return torch.linalg.solve(kk, M.T).T.cpu().numpy()
+
+
+def test_update_factor_f3_r32_mid5(oracle, rt):
+    """Rank 32 with I_1 = 384 (beyond k_ttm_mid2's shared memory, as C5's I_1 = 512): the F_3
+    projection X x_1 A_1^T takes k_ttm_mid5<32> (16-row TMA boxes, five stages); all three
+    modes vs an independent FP64 update_factor."""
+    from tests.bars import factor_bar, kkt_kappa
+    torch = pytest.importorskip("torch")
+    shape, ranks, lam = (384, 40, 2048), (32, 32, 32), 1e-2
+    x = planted(shape, ranks, seed=53)
+    core, factors = model(oracle, shape, ranks, "normal", 19)
+    xt = rt.Tensor.from_numpy(x)
+    m = rt.Model(core, factors, lam)
+    for mode in (1, 2, 3):
+        m5 = rt.variant_count("k_ttm_mid5<32>")
+        g = rt.update_factor(xt, m, mode)
+        if mode == 3:
+            assert rt.variant_count("k_ttm_mid5<32>") == m5 + 1, "F3 did not take k_ttm_mid5<32>"
+        o = _torch_update_factor(torch, x, core, factors, lam, mode - 1)
+        kappa = kkt_kappa(core, factors, mode - 1, lam)
+        err = frel(g, o)
+        bar = factor_bar(kappa, shape, mode - 1)
+        print(f"R=32 F{mode}: kappa {kappa:.3e} err {err:.3e} bar {bar:.3e}")
+        assert err < bar, (mode, kappa, err)

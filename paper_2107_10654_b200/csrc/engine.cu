@@ -35,17 +35,17 @@ std::map<int, cudaStream_t> g_default_streams;
 }  // namespace
 
 // per-device stream for parallel graph branches (Engine::fork); never destroyed
-cudaStream_t side_stream() {
+cudaStream_t side_stream(int k = 0) {
   static std::mutex mu;
-  static std::map<int, cudaStream_t> streams;
+  static std::map<std::pair<int, int>, cudaStream_t> streams;
   int dev = 0;
   RTB_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
-  auto it = streams.find(dev);
+  auto it = streams.find({dev, k});
   if (it != streams.end()) return it->second;
   cudaStream_t s;
   RTB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  streams[dev] = s;
+  streams[{dev, k}] = s;
   return s;
 }
 
@@ -576,6 +576,8 @@ class Engine {
                                      ctr_dev_.as<unsigned long long>(), sketch_rng_, factor_rng_,
                                      (opt_.factor_samples > 0 && N_ >= 2) ? N_ : 0);
     RTB_LAUNCH_CHECK();
+    decoded_ahead_ = false;
+    if (opt_.sketched) decode_ahead(seed_dev_.as<unsigned long long>());
     int r = 0;
     for (int n = 0; n < N_; ++n) {
       rec(step_ev_[2 * n]);
@@ -731,6 +733,8 @@ class Engine {
     if (post_host_) cudaFreeHost(post_host_);
     if (fork_ev_) cudaEventDestroy(fork_ev_);
     if (join_ev_) cudaEventDestroy(join_ev_);
+    if (dfork_ev_) cudaEventDestroy(dfork_ev_);
+    if (djoin_ev_) cudaEventDestroy(djoin_ev_);
   }
 
   // Adds the elapsed times of the last sweep's step events (the stream has passed them).
@@ -979,6 +983,8 @@ class Engine {
     for (int k = 0; k < 2 * (N_ + 1); ++k) RTB_CUDA(cudaEventCreate(&step_ev_[k]));
     RTB_CUDA(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
     RTB_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
+    RTB_CUDA(cudaEventCreateWithFlags(&dfork_ev_, cudaEventDisableTiming));
+    RTB_CUDA(cudaEventCreateWithFlags(&djoin_ev_, cudaEventDisableTiming));
     {
       int rk[8] = {0};
       for (int n = 0; n < N_; ++n) rk[n] = (int)ranks_[n];
@@ -1162,6 +1168,10 @@ class Engine {
   // main stream (every DevBuf is allocated and freed in main-stream order); the side stream
   // itself is per device and lives as long as the process.
   cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
+  // the core sketch's stream decode, run ahead as a second side branch (decode_ahead)
+  cudaEvent_t dfork_ev_ = nullptr, djoin_ev_ = nullptr;
+  bool decoded_ahead_ = false;
+  DevBuf cdraw_work_;
   bool forked_ = false;
   bool blocks_ready_ = false;  // the last normal_eq wrote blocks_ (fused contraction epilogue)
   // returns the stream for the branch: the side stream, or the main one when profiling
@@ -1201,12 +1211,12 @@ class Engine {
   }
 
   // ---- sketched core (ref tucker.cpp:141-166, sketch_ridge.cpp:52-151) ----
-  void update_core_sketched(uint64_t seed, const unsigned long long* seed_dev = nullptr,
-                            bool defer = false) {
+  uint64_t core_sample_count() const {
     uint64_t s = opt_.sample_override;
     if (s == 0) s = sample_count_formula(0.5, d_, opt_.epsilon, opt_.delta);
-    last_s_ = s;
-    compute_scores();
+    return s;
+  }
+  DrawSpec core_draw_spec(uint64_t s, uint64_t seed, const unsigned long long* seed_dev) {
     DrawSpec ds{};
     ds.order = N_;
     long long off = 0;
@@ -1222,13 +1232,45 @@ class Engine {
     ds.s = s;
     sk_idx_.ensure(s * 8, st_);
     sk_w_.ensure(s * 8, st_);
-    draw_work_.ensure(draw_work_bytes(ds), st_);
+    // its own workspace: the perf mode's factor sketches reuse draw_work_ while the core
+    // sketch's decode runs ahead on a side stream
+    cdraw_work_.ensure(draw_work_bytes(ds), st_);
+    return ds;
+  }
+
+  // The core sketch's stream decode (draw positions: seed, s, d and N only) as a side branch
+  // from the start of the sweep, overlapping the factor updates; update_core_sketched joins it.
+  void decode_ahead(const unsigned long long* seed_dev) {
+    static const bool off = std::getenv("RTB_NO_DECODE_AHEAD") != nullptr;  // experiments
+    if (off || opt_.profile || !dfork_ev_ || !opt_.sketched) return;
+    const DrawSpec ds = core_draw_spec(core_sample_count(), 0, seed_dev);
+    const cudaStream_t side = side_stream(1);
+    RTB_CUDA(cudaEventRecord(dfork_ev_, st_));
+    RTB_CUDA(cudaStreamWaitEvent(side, dfork_ev_, 0));
+    draw_decode(ds, DrawWork{cdraw_work_.p, cdraw_work_.bytes}, side);
+    RTB_CUDA(cudaEventRecord(djoin_ev_, side));
+    decoded_ahead_ = true;
+  }
+
+  void update_core_sketched(uint64_t seed, const unsigned long long* seed_dev = nullptr,
+                            bool defer = false) {
+    const uint64_t s = core_sample_count();
+    last_s_ = s;
+    compute_scores();
+    const DrawSpec ds = core_draw_spec(s, seed, seed_dev);
     RTB_CUDA(cudaMemsetAsync(flag_.p, 0, 4, st_));
     {
       Scope sc(prof_, "draw");
-      draw_sketch(ds, scores_.as<double>(), cdf_.as<double>(), sums_.as<double>(),
-                  DrawWork{draw_work_.p, draw_work_.bytes}, (unsigned long long*)sk_idx_.p,
-                  sk_w_.as<double>(), flag_.as<int>(), st_);
+      const DrawWork dw{cdraw_work_.p, cdraw_work_.bytes};
+      if (decoded_ahead_ && seed_dev) {
+        RTB_CUDA(cudaStreamWaitEvent(st_, djoin_ev_, 0));
+        draw_evaluate(ds, scores_.as<double>(), cdf_.as<double>(), sums_.as<double>(), dw,
+                      (unsigned long long*)sk_idx_.p, sk_w_.as<double>(), flag_.as<int>(), st_);
+      } else {
+        draw_sketch(ds, scores_.as<double>(), cdf_.as<double>(), sums_.as<double>(), dw,
+                    (unsigned long long*)sk_idx_.p, sk_w_.as<double>(), flag_.as<int>(), st_);
+      }
+      decoded_ahead_ = false;
     }
     solve_sketch(s, defer);
   }

@@ -337,17 +337,24 @@ __global__ void k_draw_eval(DrawSpec spec, StreamCfg c, const long long* start,
   w_out[t] = __dsqrt_rn(__ddiv_rn(inv_s, prob));
 }
 
-void draw_sketch(const DrawSpec& spec, const double* scores, const double* cdfs,
-                 const double* sums, DrawWork work, unsigned long long* idx_out, double* w_out,
-                 int* flag_dev, cudaStream_t st) {
-  if (spec.s == 0) return;
-  const int L = spec.order + 1 > 2 ? spec.order + 1 : 2;
-  Layout l = layout(spec, work.base);
+namespace {
+StreamCfg stream_cfg(const DrawSpec& spec) {
   StreamCfg c;
   c.seed = spec.seed;
   c.seed_ptr = spec.seed_dev;
   c.thr = (0ULL - spec.d) % spec.d;
   c.data_step = 1 + spec.order;
+  return c;
+}
+}  // namespace
+
+// Steps 1-3: the stream position of every draw. Depends on the seed, s, d and the order only
+// (not on the CDFs), so a sweep runs it as a side branch next to the factor updates.
+void draw_decode(const DrawSpec& spec, DrawWork work, cudaStream_t st) {
+  if (spec.s == 0) return;
+  const int L = spec.order + 1 > 2 ? spec.order + 1 : 2;
+  Layout l = layout(spec, work.base);
+  const StreamCfg c = stream_cfg(spec);
   RTB_CUDA(cudaMemsetAsync(l.overflow, 0, sizeof(int), st));
   const long long n1 = l.nsub * L;
   k_draw_submaps<<<(unsigned)ceil_div<long long>(n1, 256), 256, 0, st>>>(c, L, l.nsub, l.exitm,
@@ -372,9 +379,25 @@ void draw_sketch(const DrawSpec& spec, const double* scores, const double* cdfs,
   k_draw_emit<<<(unsigned)ceil_div<long long>(l.nsub, 128), 128, 0, st>>>(
       c, l.nsub, l.entry, l.base, l.start, (long long)spec.s);
   RTB_LAUNCH_CHECK();
+}
+
+// Step 4 on the positions draw_decode left in the workspace.
+void draw_evaluate(const DrawSpec& spec, const double* scores, const double* cdfs,
+                   const double* sums, DrawWork work, unsigned long long* idx_out, double* w_out,
+                   int* flag_dev, cudaStream_t st) {
+  if (spec.s == 0) return;
+  Layout l = layout(spec, work.base);
+  const StreamCfg c = stream_cfg(spec);
   k_draw_eval<<<(unsigned)ceil_div<unsigned long long>(spec.s, 256ULL), 256, 0, st>>>(
       spec, c, l.start, scores, cdfs, sums, idx_out, w_out, flag_dev);
   RTB_LAUNCH_CHECK();
+}
+
+void draw_sketch(const DrawSpec& spec, const double* scores, const double* cdfs,
+                 const double* sums, DrawWork work, unsigned long long* idx_out, double* w_out,
+                 int* flag_dev, cudaStream_t st) {
+  draw_decode(spec, work, st);
+  draw_evaluate(spec, scores, cdfs, sums, work, idx_out, w_out, flag_dev, st);
 }
 
 }  // namespace rtb

@@ -104,6 +104,11 @@ size_t draw_work_bytes(const DrawSpec& spec);
 void draw_sketch(const DrawSpec& spec, const double* scores, const double* cdfs,
                  const double* sums, DrawWork work, unsigned long long* idx_out,
                  double* w_out, int* flag_dev, cudaStream_t st);
+// the two halves of draw_sketch: stream positions (no CDFs needed), then evaluation
+void draw_decode(const DrawSpec& spec, DrawWork work, cudaStream_t st);
+void draw_evaluate(const DrawSpec& spec, const double* scores, const double* cdfs,
+                   const double* sums, DrawWork work, unsigned long long* idx_out,
+                   double* w_out, int* flag_dev, cudaStream_t st);
 
 // ---- k_fsketch.cu: sketched factor update (perf mode) ----
 struct FactorSketchSpec {

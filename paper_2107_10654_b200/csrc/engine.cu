@@ -577,6 +577,7 @@ class Engine {
                                      (opt_.factor_samples > 0 && N_ >= 2) ? N_ : 0);
     RTB_LAUNCH_CHECK();
     decoded_ahead_ = false;
+    keys_ahead_ = keys_ready_ = false;
     if (opt_.sketched) decode_ahead(seed_dev_.as<unsigned long long>());
     int r = 0;
     for (int n = 0; n < N_; ++n) {
@@ -585,6 +586,7 @@ class Engine {
         update_factor_sketched(n, 0, seed_dev_.as<unsigned long long>() + 1 + n);
       else
         update_factor(n);
+      if (n == 0) keys_ahead();
       rec(step_ev_[2 * n + 1]);
       if (opt_.record_history) {
         loss_pass(rows + 2 * r, rows + 2 * r + 1);
@@ -734,6 +736,7 @@ class Engine {
     if (fork_ev_) cudaEventDestroy(fork_ev_);
     if (join_ev_) cudaEventDestroy(join_ev_);
     if (dfork_ev_) cudaEventDestroy(dfork_ev_);
+    if (kfork_ev_) cudaEventDestroy(kfork_ev_);
     if (djoin_ev_) cudaEventDestroy(djoin_ev_);
   }
 
@@ -810,6 +813,9 @@ class Engine {
   Profiler prof_;
 
   DevBuf ns_vals_, pinv2_, linv_, spd_ok_;
+  // the factor updates' (K K^T + lambda I)^+ scratch: their own slots, so a score step for
+  // finished modes can run on a side branch meanwhile (keys_ahead)
+  DevBuf fu_linv_, fu_ok_, fu_evals_, fu_evecs_, fu_status_;
   DevBuf core_, fac_, grams_, evals_, evecs_, eig_status_, ns_, pinv_, ranks_dev_;
   DevBuf T_, P_, tmp_a_, tmp_b_, partial_, scal_, hist_, init_loss_, xx_, loss_need_, yq_;
   bool xx_valid_ = false;
@@ -896,6 +902,22 @@ class Engine {
       RTB_CUDA(cudaMemcpy(ns_vals_.p, vals, 65 * 4, cudaMemcpyHostToDevice));
     }
     eig_status_.ensure(64 * 4, st_);
+    {
+      // one-sided Jacobi workspace of the score step (allocated here: the step may run on a
+      // side stream)
+      long long stride = 0;
+      for (int n = 0; n < N_; ++n)
+        stride = std::max<long long>(stride, (long long)shape_[n] * (ranks_[n] + (ranks_[n] & 1)));
+      hj_ws_.ensure((size_t)N_ * stride * 8 + 64, st_);
+    }
+    {
+      const size_t fb = (size_t)std::max(eig_stride_, 64 * 64) * 8 + 8;
+      fu_linv_.ensure(fb, st_);
+      fu_evals_.ensure(fb, st_);
+      fu_evecs_.ensure(fb, st_);
+      fu_ok_.ensure(64 * 4, st_);
+      fu_status_.ensure(64 * 4, st_);
+    }
     pgram_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
     pev_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
     pvec_.ensure((size_t)N_ * eig_stride_ * 8 + 8, st_);
@@ -984,6 +1006,7 @@ class Engine {
     RTB_CUDA(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
     RTB_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
     RTB_CUDA(cudaEventCreateWithFlags(&dfork_ev_, cudaEventDisableTiming));
+    RTB_CUDA(cudaEventCreateWithFlags(&kfork_ev_, cudaEventDisableTiming));
     RTB_CUDA(cudaEventCreateWithFlags(&djoin_ev_, cudaEventDisableTiming));
     {
       int rk[8] = {0};
@@ -1115,14 +1138,14 @@ class Engine {
       // (KK^T + lambda I)^+ (ref linalg.cpp:8-26): warp Cholesky inverse; if a
       // pivot is below R*eps*max diag the eigen/pinv path (singular values =
       // |eigenvalues|, cutoff R*eps*sigma_max) takes over on the device.
-      int* okf = spd_ok_.as<int>();
+      int* okf = fu_ok_.as<int>();
       const int stride = std::max(eig_stride_, Rn * Rn);
       if (Rn <= 32) {
-        spd_small(kk, ns_one(Rn), stride, (double)Rn * DBL_EPSILON, linv_.as<double>(), pv, okf,
+        spd_small(kk, ns_one(Rn), stride, (double)Rn * DBL_EPSILON, fu_linv_.as<double>(), pv, okf,
                   1, ss, Rn);
-        sym_eigen(kk, ns_one(Rn), Rn, stride, evals_.as<double>(), evecs_.as<double>(),
-                  eig_status_.as<int>(), 1, ss, okf);
-        k_sym_pinv<<<1, 256, 0, ss>>>(evals_.as<double>(), evecs_.as<double>(), ns_one(Rn),
+        sym_eigen(kk, ns_one(Rn), Rn, stride, fu_evals_.as<double>(), fu_evecs_.as<double>(),
+                  fu_status_.as<int>(), 1, ss, okf);
+        k_sym_pinv<<<1, 256, 0, ss>>>(fu_evals_.as<double>(), fu_evecs_.as<double>(), ns_one(Rn),
                                        stride, pv, nullptr, okf);
       } else {
         eigen_one(kk, Rn, ss);
@@ -1172,6 +1195,10 @@ class Engine {
   cudaEvent_t dfork_ev_ = nullptr, djoin_ev_ = nullptr;
   bool decoded_ahead_ = false;
   DevBuf cdraw_work_;
+  // keys ahead: mode-1 scores, the Gram's bucket keys and their sort on the same side branch
+  // after F1 (order 3, exact factor updates); the first normal_eq of the core step skips them
+  cudaEvent_t kfork_ev_ = nullptr;
+  bool keys_ahead_ = false, keys_ready_ = false;
   bool forked_ = false;
   bool blocks_ready_ = false;  // the last normal_eq wrote blocks_ (fused contraction epilogue)
   // returns the stream for the branch: the side stream, or the main one when profiling
@@ -1252,11 +1279,45 @@ class Engine {
     decoded_ahead_ = true;
   }
 
+  // After F1 (A_1 final): on the decode branch, A_1's scores and CDF, every draw's bucket key
+  // from A_1's CDF alone (k_draw_keys), the stable key sort, the bucket table and the bucket
+  // order -- the Gram's whole sort stage leaves the critical path (it overlaps F2 and F3).
+  void keys_ahead() {
+    static const bool off = std::getenv("RTB_NO_KEYS_AHEAD") != nullptr;  // experiments
+    if (off || !decoded_ahead_ || N_ != 3 || opt_.factor_samples > 0 || rmax_ > 32 ||
+        opt_.profile)
+      return;
+    const uint64_t s = core_sample_count();
+    const GramSpec gs = gram_spec(s);
+    gram_work_.ensure(gram_work_bytes(gs), st_);
+    const DrawSpec ds = core_draw_spec(s, 0, seed_dev_.as<unsigned long long>());
+    const cudaStream_t side = side_stream(1);
+    RTB_CUDA(cudaEventRecord(kfork_ev_, st_));
+    RTB_CUDA(cudaStreamWaitEvent(side, kfork_ev_, 0));
+    compute_scores_range(0, 1, side);
+    const GramKeyBufs kb = gram_key_buffers(gs, gram_work_.p);
+    gram_keys_reset(gs, gram_work_.p, (unsigned long long*)data_draws_.p, side);
+    draw_keys(ds, scores_.as<double>(), cdf_.as<double>(), sums_.as<double>(),
+              DrawWork{cdraw_work_.p, cdraw_work_.bytes}, gs.i1_lo, gs.i1_hi, kb.keys, kb.vals,
+              kb.counts, kb.aug_count, (unsigned long long*)data_draws_.p, side);
+    gram_sort_keys(gs, gram_work_.p, side);
+    RTB_CUDA(cudaEventRecord(djoin_ev_, side));
+    keys_ahead_ = true;
+  }
+
   void update_core_sketched(uint64_t seed, const unsigned long long* seed_dev = nullptr,
                             bool defer = false) {
     const uint64_t s = core_sample_count();
     last_s_ = s;
-    compute_scores();
+    if (keys_ahead_ && seed_dev) {
+      // mode 1's scores came with the keys: join that branch, then the other modes
+      RTB_CUDA(cudaStreamWaitEvent(st_, djoin_ev_, 0));
+      compute_scores_range(1, N_, st_);
+      keys_ready_ = true;
+    } else {
+      compute_scores();
+    }
+    keys_ahead_ = false;
     const DrawSpec ds = core_draw_spec(s, seed, seed_dev);
     RTB_CUDA(cudaMemsetAsync(flag_.p, 0, 4, st_));
     {
@@ -1364,9 +1425,9 @@ class Engine {
       // A_n = M pinv(Gram) (ref sketch_ridge.cpp:130-139 per fiber row), as in update_factor
       Scope sc(prof_, "small_linalg");
       double* pv = pinv2_.as<double>();
-      int* okf = spd_ok_.as<int>();
+      int* okf = fu_ok_.as<int>();
       const int stride = std::max(eig_stride_, Rn * Rn);
-      spd_small(kk, ns_one(Rn), stride, (double)Rn * DBL_EPSILON, linv_.as<double>(), pv, okf, 1,
+      spd_small(kk, ns_one(Rn), stride, (double)Rn * DBL_EPSILON, fu_linv_.as<double>(), pv, okf, 1,
                 st_, Rn);
       if (std::getenv("RTB_DEBUG_FSK_SPD")) {
         int okh = -1;
@@ -1377,10 +1438,10 @@ class Engine {
         std::fprintf(stderr, "[fsk] mode %d ok %d diag %.3e %.3e offd %.3e sym %.3e\n", n, okh,
                      kh[0], kh[(size_t)Rn * Rn - 1], kh[1], kh[1] - kh[Rn]);
       }
-      sym_eigen(kk, ns_one(Rn), Rn, stride, evals_.as<double>(), evecs_.as<double>(),
-                eig_status_.as<int>(), 1, st_, okf);
-      k_sym_pinv<<<1, 256, 0, st_>>>(evals_.as<double>(), evecs_.as<double>(), ns_one(Rn), stride,
-                                     pv, nullptr, okf);
+      sym_eigen(kk, ns_one(Rn), Rn, stride, fu_evals_.as<double>(), fu_evecs_.as<double>(),
+                fu_status_.as<int>(), 1, st_, okf);
+      k_sym_pinv<<<1, 256, 0, st_>>>(fu_evals_.as<double>(), fu_evecs_.as<double>(), ns_one(Rn),
+                                     stride, pv, nullptr, okf);
       RTB_LAUNCH_CHECK();
       const long long tot = (long long)In * Rn;
       k_rows_times_small<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(M, pv, In, Rn,
@@ -1393,7 +1454,10 @@ class Engine {
   }
 
   // per-mode classical leverage scores, CDFs and sums of the current factors
-  void compute_scores() {
+  void compute_scores() { compute_scores_range(0, N_, st_); }
+
+  // scores, CDFs and sums of modes [n0, n1) on stream `st`; the zero-rank flag when n1 == N
+  void compute_scores_range(int n0, int n1, cudaStream_t st) {
     {
       Scope sc(prof_, "scores");
       // classical scores l_i = a_i^T (A^T A)^+ a_i: Cholesky of each factor Gram
@@ -1402,43 +1466,56 @@ class Engine {
       // reference's own route: one-sided Jacobi SVD of the factor and the rank cut on its
       // singular values (k_hj_cta; ref kronecker.cpp:18-23, svd.cpp:69-111,
       // leverage.cpp:16-37 at lambda = 0)
-      FactorSet fs = factor_set();
+      const FactorSet all = factor_set();
+      FactorSet fs{};
+      const int cnt = n1 - n0;
+      fs.order = cnt;
+      for (int k = 0; k < cnt; ++k) {
+        fs.ptr[k] = all.ptr[n0 + k];
+        fs.rows[k] = all.rows[n0 + k];
+        fs.cols[k] = all.cols[n0 + k];
+      }
       int maxI = 0;
-      for (auto v : shape_) maxI = std::max<int>(maxI, (int)v);
+      for (int n = n0; n < n1; ++n) maxI = std::max<int>(maxI, (int)shape_[n]);
       const int* okm = nullptr;
-      dim3 grid(ceil_div(maxI, 128), N_);
+      dim3 grid(ceil_div(maxI, 128), cnt);
+      const size_t so = (size_t)n0 * eig_stride_;
+      long long* soff = score_off_.as<long long>() + n0;
+      int* rkd = ranks_dev_.as<int>() + n0;
       if (rmax_ <= 32) {
-        spd_small(grams_.as<double>(), ns_.as<int>(), eig_stride_, (double)maxI * DBL_EPSILON,
-                  linv_.as<double>(), pgram_.as<double>(), spd_ok_.as<int>(), N_, st_, rmax_);
-        okm = spd_ok_.as<int>();
+        spd_small(grams_.as<double>() + so, ns_.as<int>() + n0, eig_stride_,
+                  (double)maxI * DBL_EPSILON, linv_.as<double>() + so, pgram_.as<double>() + so,
+                  spd_ok_.as<int>() + n0, cnt, st, rmax_);
+        okm = spd_ok_.as<int>() + n0;
         long long stride = 0;
         for (int n = 0; n < N_; ++n)
           stride = std::max<long long>(stride, (long long)shape_[n] * (ranks_[n] + (ranks_[n] & 1)));
         hj_ws_.ensure((size_t)N_ * stride * 8 + 64, st_);
-        k_hj_cta<<<N_, 512, 0, st_>>>(fs, hj_ws_.as<double>(), stride, 0.0, scores_.as<double>(),
-                                      score_off_.as<long long>(), ranks_dev_.as<int>(), okm,
-                                      eig_status_.as<int>());
+        k_hj_cta<<<cnt, 512, 0, st>>>(fs, hj_ws_.as<double>() + (size_t)n0 * stride, stride, 0.0,
+                                      scores_.as<double>(), soff, rkd, okm,
+                                      eig_status_.as<int>() + n0);
         RTB_LAUNCH_CHECK();
       } else {
-        sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, evals_.as<double>(),
-                  evecs_.as<double>(), eig_status_.as<int>(), N_, st_, okm);
-        k_leverage_rows<<<grid, 128, 0, st_>>>(fs, evals_.as<double>(), evecs_.as<double>(),
-                                              eig_stride_, 0.0, scores_.as<double>(),
-                                              score_off_.as<long long>(), ranks_dev_.as<int>(),
-                                              okm);
+        sym_eigen(grams_.as<double>() + so, ns_.as<int>() + n0, rmax_, eig_stride_,
+                  evals_.as<double>() + so, evecs_.as<double>() + so, eig_status_.as<int>() + n0,
+                  cnt, st, okm);
+        k_leverage_rows<<<grid, 128, 0, st>>>(fs, evals_.as<double>() + so,
+                                             evecs_.as<double>() + so, eig_stride_, 0.0,
+                                             scores_.as<double>(), soff, rkd, okm);
         RTB_LAUNCH_CHECK();
       }
       if (okm) {
-        k_leverage_chol<<<grid, 128, 0, st_>>>(fs, linv_.as<double>(), eig_stride_, okm,
-                                              scores_.as<double>(), score_off_.as<long long>(),
-                                              ranks_dev_.as<int>());
+        k_leverage_chol<<<grid, 128, 0, st>>>(fs, linv_.as<double>() + so, eig_stride_, okm,
+                                             scores_.as<double>(), soff, rkd);
         RTB_LAUNCH_CHECK();
       }
-      k_score_cdf<<<1, 32 * N_, 0, st_>>>(scores_.as<double>(), score_off_.as<long long>(),
-                                     rows_dev_.as<int>(), N_, cdf_.as<double>(), sums_.as<double>());
+      k_score_cdf<<<1, 32 * cnt, 0, st>>>(scores_.as<double>(), soff, rows_dev_.as<int>() + n0, cnt,
+                                          cdf_.as<double>(), sums_.as<double>() + n0);
       RTB_LAUNCH_CHECK();
-      k_any_zero_rank<<<1, 32, 0, st_>>>(ranks_dev_.as<int>(), N_, zero_flag_.as<int>());
-      RTB_LAUNCH_CHECK();
+      if (n1 == N_) {
+        k_any_zero_rank<<<1, 32, 0, st>>>(ranks_dev_.as<int>(), N_, zero_flag_.as<int>());
+        RTB_LAUNCH_CHECK();
+      }
     }
   }
 
@@ -1573,7 +1650,9 @@ class Engine {
     blocks_ready_ = sketch_normal_eq(gs, xg, (const unsigned long long*)sk_idx_.p,
                                      sk_w_.as<double>(), gram_work_.p, gram_work_.bytes,
                                      (full && !sharded()) ? G_.as<double>() : nullptr,
-                                     rhs_.as<double>(), (unsigned long long*)data_draws_.p, st_, bl);
+                                     rhs_.as<double>(), (unsigned long long*)data_draws_.p, st_, bl,
+                                     keys_ready_);
+    keys_ready_ = false;  // a fallback's second normal_eq sorts again
     if (sharded()) {
       size_t ns = 0;
       double* S = gram_compact(gs, gram_work_.p, &ns);

@@ -393,6 +393,68 @@ void draw_evaluate(const DrawSpec& spec, const double* scores, const double* cdf
   RTB_LAUNCH_CHECK();
 }
 
+// The first-mode half of k_draw_eval fused with k_sketch_keys (k_gram.cu): a data draw's i_1
+// is fixed by its first uniform and A_1's CDF alone (modes are drawn in order, ref
+// kronecker.cpp:125-144), so the bucket keys, the bucket histogram and the augmented-row
+// histogram -- exactly what k_sketch_keys derives from the evaluated indices -- can be made
+// as soon as A_1 is final, while A_2 and A_3 are still being updated.
+__global__ void k_draw_keys(DrawSpec spec, StreamCfg c, const long long* start,
+                            const double* scores, const double* cdfs, const double* sums,
+                            int i1_lo, int i1_hi, unsigned* keys, unsigned* vals, int* counts,
+                            int* aug_count, unsigned long long* data_draws) {
+  if (c.seed_ptr) c.seed = *c.seed_ptr;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)spec.s) return;
+  const long long pos = start[t];
+  const uint64_t coin = sm_at(c.seed, (uint64_t)pos);
+  const unsigned I1 = (unsigned)spec.rows[0];
+  vals[t] = (unsigned)t;
+  if ((coin >> 63) == 0) {
+    const long long I = spec.rows[0];
+    const double S = sums[0];
+    const double* cdf = cdfs + spec.cdf_off[0];
+    const double* sc = scores + spec.cdf_off[0];
+    const double u = __dmul_rn(u64_to_unit(sm_at(c.seed, (uint64_t)(pos + 1))), S);
+    long long lo = 0, len = I;
+    while (len > 0) {
+      const long long half = len >> 1;
+      if (!(u < cdf[lo + half])) {
+        lo += half + 1;
+        len -= half + 1;
+      } else {
+        len = half;
+      }
+    }
+    long long i = lo >= I ? I - 1 : lo;
+    while (i > 0 && sc[i] == 0.0) --i;
+    if (i1_hi > 0 && ((int)i < i1_lo || (int)i >= i1_hi)) {
+      keys[t] = I1;  // another shard's draw
+      return;
+    }
+    keys[t] = (unsigned)i;
+    atomicAdd(&counts[i], 1);
+    atomicAdd(data_draws, 1ULL);
+  } else {
+    long long q = pos + 1;
+    uint64_t r = sm_at(c.seed, (uint64_t)q);
+    while (r < c.thr) r = sm_at(c.seed, (uint64_t)(++q));
+    keys[t] = I1;
+    atomicAdd(&aug_count[r % spec.d], 1);
+  }
+}
+
+void draw_keys(const DrawSpec& spec, const double* scores, const double* cdfs, const double* sums,
+               DrawWork work, int i1_lo, int i1_hi, unsigned* keys, unsigned* vals, int* counts,
+               int* aug_count, unsigned long long* data_draws, cudaStream_t st) {
+  if (spec.s == 0) return;
+  Layout l = layout(spec, work.base);
+  const StreamCfg c = stream_cfg(spec);
+  k_draw_keys<<<(unsigned)ceil_div<unsigned long long>(spec.s, 256ULL), 256, 0, st>>>(
+      spec, c, l.start, scores, cdfs, sums, i1_lo, i1_hi, keys, vals, counts, aug_count,
+      data_draws);
+  RTB_LAUNCH_CHECK();
+}
+
 void draw_sketch(const DrawSpec& spec, const double* scores, const double* cdfs,
                  const double* sums, DrawWork work, unsigned long long* idx_out, double* w_out,
                  int* flag_dev, cudaStream_t st) {

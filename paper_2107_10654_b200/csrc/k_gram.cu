@@ -1780,22 +1780,40 @@ namespace {
 
 // (A)-(B) and the rhs ingredient: sort the draws by i1, gather their records, H_b and h_b
 // per nonempty bucket (compacted: bucket b holds i1 = bi1[b]).
-void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, const double* x,
-                  const unsigned long long* idx, const double* w,
-                  unsigned long long* data_draws_dev, cudaStream_t st) {
-  const int I1 = spec.rows[0];
-  RTB_CUDA(cudaMemsetAsync(l.counts, 0, (size_t)I1 * 4, st));
+void keys_reset(const GramSpec& spec, const GramLayout& l, unsigned long long* data_draws_dev,
+                cudaStream_t st) {
+  RTB_CUDA(cudaMemsetAsync(l.counts, 0, (size_t)spec.rows[0] * 4, st));
   RTB_CUDA(cudaMemsetAsync(l.aug_count, 0, (size_t)spec.d * 4, st));
   RTB_CUDA(cudaMemsetAsync(data_draws_dev, 0, 8, st));
-  const unsigned sb = (unsigned)ceil_div<unsigned long long>(spec.s, 256ULL);
-  k_sketch_keys<<<sb, 256, 0, st>>>(spec, idx, l.keys, l.vals, l.counts, l.aug_count,
-                                    data_draws_dev);
-  RTB_LAUNCH_CHECK();
+}
+
+// stable sort of the draws by key (i1), the compacted bucket table, and (with `order`) the
+// buckets longest first for the persistent bucket kernels
+void sort_keys(const GramSpec& spec, const GramLayout& l, bool order, cudaStream_t st) {
+  const int I1 = spec.rows[0];
   size_t cb = l.cub_bytes;
   RTB_CUDA(cub::DeviceRadixSort::SortPairs(l.cub_tmp, cb, l.keys, l.keys_sorted, l.vals,
                                            l.vals_sorted, (int)spec.s, 0, key_bits(I1), st));
   k_bucket_scan<<<1, 1024, 0, st>>>(I1, l.counts, l.bstart, l.blen, l.bi1, l.nbuckets);
   RTB_LAUNCH_CHECK();
+  if (order) {
+    k_bucket_order<<<1, 1024, 0, st>>>(l.blen, l.nbuckets, l.border, l.bcounter);
+    RTB_LAUNCH_CHECK();
+  }
+}
+
+void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, const double* x,
+                  const unsigned long long* idx, const double* w,
+                  unsigned long long* data_draws_dev, cudaStream_t st, bool keys_ready = false) {
+  const int I1 = spec.rows[0];
+  const unsigned sb = (unsigned)ceil_div<unsigned long long>(spec.s, 256ULL);
+  if (!keys_ready) {
+    keys_reset(spec, l, data_draws_dev, st);
+    k_sketch_keys<<<sb, 256, 0, st>>>(spec, idx, l.keys, l.vals, l.counts, l.aug_count,
+                                      data_draws_dev);
+    RTB_LAUNCH_CHECK();
+    sort_keys(spec, l, false, st);
+  }
   // draw records in bucket order (one gather of x per draw)
   k_gather_draws<<<sb, 256, 0, st>>>(spec, x, idx, w, l.vals_sorted, l.keys_sorted, l.dw2, l.dwx,
                                      l.dmode);
@@ -1858,8 +1876,10 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
       k_vech_table<<<(unsigned)ceil_div<long long>((long long)spec.rows[2] * kB5Tab, 256), 256, 0,
                      st>>>(spec.factors[2], spec.rows[2], v.R[2], kB5Tab, l.vt3);
       RTB_LAUNCH_CHECK();
-      k_bucket_order<<<1, 1024, 0, st>>>(l.blen, l.nbuckets, l.border, l.bcounter);
-      RTB_LAUNCH_CHECK();
+      if (!keys_ready) {
+        k_bucket_order<<<1, 1024, 0, st>>>(l.blen, l.nbuckets, l.border, l.bcounter);
+        RTB_LAUNCH_CHECK();
+      }
       const size_t smb5 = vech_bucket5_smem();
       set_max_smem(k_vech_bucket5, (int)smb5);
       int dev = 0, sms = 0;
@@ -1887,8 +1907,10 @@ void bucket_stage(const GramSpec& spec, const VechSpec& v, const GramLayout& l, 
     k_vech_table<<<(unsigned)ceil_div<long long>((long long)spec.rows[2] * tw3, 256), 256, 0, st>>>(
         spec.factors[2], spec.rows[2], v.R[2], tw3, l.vt3);
     RTB_LAUNCH_CHECK();
-    k_bucket_order<<<1, 1024, 0, st>>>(l.blen, l.nbuckets, l.border, l.bcounter);
-    RTB_LAUNCH_CHECK();
+    if (!keys_ready) {
+      k_bucket_order<<<1, 1024, 0, st>>>(l.blen, l.nbuckets, l.border, l.bcounter);
+      RTB_LAUNCH_CHECK();
+    }
     const size_t smb6 = vech_bucket6_smem();
     set_max_smem(k_vech_bucket6, (int)smb6);
     int dev = 0, sms = 0;
@@ -2004,18 +2026,35 @@ void sketch_normal_eq_m4(const GramSpec& spec, const double* x, const unsigned l
 
 }  // namespace
 
+GramKeyBufs gram_key_buffers(const GramSpec& spec, void* work) {
+  const GramLayout l = layout(spec, work);
+  return GramKeyBufs{l.keys, l.vals, l.counts, l.aug_count};
+}
+
+void gram_keys_reset(const GramSpec& spec, void* work, unsigned long long* data_draws_dev,
+                     cudaStream_t st) {
+  keys_reset(spec, layout(spec, work), data_draws_dev, st);
+}
+
+void gram_sort_keys(const GramSpec& spec, void* work, cudaStream_t st) {
+  if (spec.order != 3) throw Error(4, "gram_sort_keys: order 3 only");
+  sort_keys(spec, layout(spec, work), true, st);
+}
+
 bool sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long long* idx,
                       const double* w, void* work, size_t work_bytes, double* gram, double* rhs,
-                      unsigned long long* data_draws_dev, cudaStream_t st, double* blocks) {
+                      unsigned long long* data_draws_dev, cudaStream_t st, double* blocks,
+                      bool keys_ready) {
   if (work_bytes < gram_work_bytes(spec)) throw Error(4, "sketch_normal_eq: workspace too small");
   const VechSpec v = make_vech(spec);
   if (v.rowlen > kMaxRow) throw Error(4, "sketch_normal_eq: sum of ranks beyond mode 1 > 256");
+  if (keys_ready && spec.order != 3) throw Error(4, "sketch_normal_eq: keys ahead for order 3 only");
   if (merged4_ok(spec)) {
     sketch_normal_eq_m4(spec, x, idx, w, work, gram, rhs, data_draws_dev, st);
     return false;
   }
   GramLayout l = layout(spec, work);
-  bucket_stage(spec, v, l, x, idx, w, data_draws_dev, st);
+  bucket_stage(spec, v, l, x, idx, w, data_draws_dev, st, keys_ready);
   if (const char* dump = std::getenv("RTB_DUMP_H")) {  // debugging aid: H and bucket table
     std::vector<double> hh((size_t)spec.rows[0] * v.Hsz);
     std::vector<int> meta(3 * (size_t)spec.rows[0] + 1);

@@ -106,6 +106,10 @@ void draw_sketch(const DrawSpec& spec, const double* scores, const double* cdfs,
                  double* w_out, int* flag_dev, cudaStream_t st);
 // the two halves of draw_sketch: stream positions (no CDFs needed), then evaluation
 void draw_decode(const DrawSpec& spec, DrawWork work, cudaStream_t st);
+// after draw_decode: the Gram's bucket keys from the first mode's CDF alone (k_draw_keys)
+void draw_keys(const DrawSpec& spec, const double* scores, const double* cdfs, const double* sums,
+               DrawWork work, int i1_lo, int i1_hi, unsigned* keys, unsigned* vals, int* counts,
+               int* aug_count, unsigned long long* data_draws, cudaStream_t st);
 void draw_evaluate(const DrawSpec& spec, const double* scores, const double* cdfs,
                    const double* sums, DrawWork work, unsigned long long* idx_out,
                    double* w_out, int* flag_dev, cudaStream_t st);
@@ -173,6 +177,18 @@ struct GramSpec {
   int i1_lo, i1_hi;
 };
 size_t gram_work_bytes(const GramSpec& spec);
+// keys ahead (order 3): the workspace's key buffers, their reset, and the sort + bucket table
+// + bucket order that sketch_normal_eq(..., keys_ready = true) then skips
+struct GramKeyBufs {
+  unsigned* keys;
+  unsigned* vals;
+  int* counts;
+  int* aug_count;
+};
+GramKeyBufs gram_key_buffers(const GramSpec& spec, void* work);
+void gram_keys_reset(const GramSpec& spec, void* work, unsigned long long* data_draws_dev,
+                     cudaStream_t st);
+void gram_sort_keys(const GramSpec& spec, void* work, cudaStream_t st);
 // the compact (vech) Gram S [m_1][Hsz] inside the workspace (sum it across shards)
 double* gram_compact(const GramSpec& spec, void* work, size_t* count);
 // Sketched normal equations from (idx, w): rhs, the compact (vech) Gram in the
@@ -181,7 +197,7 @@ double* gram_compact(const GramSpec& spec, void* work, size_t* count);
 bool sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long long* idx,
                       const double* w, void* work, size_t work_bytes, double* gram,
                       double* rhs, unsigned long long* data_draws_dev, cudaStream_t st,
-                      double* blocks = nullptr);
+                      double* blocks = nullptr, bool keys_ready = false);
 
 // augmented-row draw counts [d] inside a gram workspace (valid after sketch_normal_eq)
 const int* gram_aug_counts(const GramSpec& spec, void* work);

@@ -143,6 +143,65 @@ __global__ void k_uniform_init(double* out, long long n, unsigned long long seed
   if (i < n) out[i] = u64_to_unit(sm_at(seed, (uint64_t)(offset + i)));
 }
 
+// K K^T + lambda I of an order-3 factor update (ref tucker.cpp:70-89), one CTA per column r:
+// Q_r = Gram_a S_r Gram_b with S_r the slice of G at index r of mode n (a < b the other modes),
+// then kk[i][r] = <S_i, Q_r> + lambda [i == r]. One launch with R_n CTAs instead of the chain of
+// two mode products, the contraction and the diagonal (4 launches) on the factor-update branch.
+__global__ void __launch_bounds__(256) k_fu_kkt3(const double* __restrict__ core,
+                                                 const double* __restrict__ grams, int stride,
+                                                 int n, int R0, int R1, int R2, double lambda,
+                                                 double* __restrict__ kk) {
+  __shared__ double Ga[32 * 33], Gb[32 * 33], S[32 * 33], T[32 * 33];
+  const int Rs[3] = {R0, R1, R2};
+  const int a = n == 0 ? 1 : 0, b = n == 2 ? 1 : 2;
+  const int Ra = Rs[a], Rb = Rs[b], Rn = Rs[n];
+  const int r = blockIdx.x;
+  // G index (i0, i1, i2) -> flat; the slice at mode-n index q: S[p][t] over (mode a, mode b)
+  auto gidx = [&](int q, int p, int t) {
+    int id[3];
+    id[n] = q;
+    id[a] = p;
+    id[b] = t;
+    return (id[0] * R1 + id[1]) * R2 + id[2];
+  };
+  for (int e = threadIdx.x; e < Ra * Ra; e += blockDim.x)
+    Ga[(e / Ra) * 33 + e % Ra] = grams[(size_t)a * stride + e];
+  for (int e = threadIdx.x; e < Rb * Rb; e += blockDim.x)
+    Gb[(e / Rb) * 33 + e % Rb] = grams[(size_t)b * stride + e];
+  for (int e = threadIdx.x; e < Ra * Rb; e += blockDim.x) {
+    const int p = e / Rb, t = e - p * Rb;
+    S[p * 33 + t] = core[gidx(r, p, t)];
+  }
+  __syncthreads();
+  // T = S Gram_b
+  for (int e = threadIdx.x; e < Ra * Rb; e += blockDim.x) {
+    const int p = e / Rb, t = e - p * Rb;
+    double acc = 0.0;
+    for (int k = 0; k < Rb; ++k) acc = fma(S[p * 33 + k], Gb[k * 33 + t], acc);
+    T[p * 33 + t] = acc;
+  }
+  __syncthreads();
+  // Q = Gram_a T (into S)
+  for (int e = threadIdx.x; e < Ra * Rb; e += blockDim.x) {
+    const int p = e / Rb, t = e - p * Rb;
+    double acc = 0.0;
+    for (int k = 0; k < Ra; ++k) acc = fma(Ga[p * 33 + k], T[k * 33 + t], acc);
+    S[p * 33 + t] = acc;
+  }
+  __syncthreads();
+  // kk[i][r] = <G slice i, Q_r>: warp per i
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = warp; i < Rn; i += nw) {
+    double acc = 0.0;
+    for (int e = lane; e < Ra * Rb; e += 32) {
+      const int p = e / Rb, t = e - p * Rb;
+      acc = fma(__ldg(core + gidx(i, p, t)), S[p * 33 + t], acc);
+    }
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) kk[i * Rn + r] = acc + (i == r ? lambda : 0.0);
+  }
+}
+
 __global__ void k_add_diag(double* a, int n, double v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[(size_t)i * n + i] += v;
@@ -1118,23 +1177,31 @@ class Engine {
       double* qb[2] = {scratch_q(0), scratch_q(1)};  // allocated in main-stream order
       const cudaStream_t ss = fork();
       Scope sc(prof_, "small_linalg");
-      std::vector<uint64_t> gd = ranks_;
-      const double* cur = core_.as<double>();
-      int which = 0;
-      for (int m = 0; m < N_; ++m) {
-        if (m == n) continue;
-        const int R = (int)ranks_[m];
-        ttm_generic(cur, (long long)prod(gd, 0, m), R, (long long)prod(gd, m + 1), gram(m), R, 1, R,
-                    qb[which], ss);
-        cur = qb[which];
-        which ^= 1;
-      }
-      const long long O = (long long)prod(ranks_, 0, n);
-      const long long J = (long long)prod(ranks_, n + 1);
       double* kk = pinv_.as<double>();
-      contract_except(core_.as<double>(), cur, O, Rn, Rn, J, kk, ss);
-      k_add_diag<<<ceil_div(Rn, 64), 64, 0, ss>>>(kk, Rn, opt_.lambda);
-      RTB_LAUNCH_CHECK();
+      static const bool no_fused = std::getenv("RTB_NO_FU_KKT") != nullptr;  // experiments
+      if (!no_fused && N_ == 3 && rmax_ <= 32) {
+        k_fu_kkt3<<<Rn, 256, 0, ss>>>(core_.as<double>(), grams_.as<double>(), eig_stride_, n,
+                                      (int)ranks_[0], (int)ranks_[1], (int)ranks_[2], opt_.lambda,
+                                      kk);
+        RTB_LAUNCH_CHECK();
+      } else {
+        std::vector<uint64_t> gd = ranks_;
+        const double* cur = core_.as<double>();
+        int which = 0;
+        for (int m = 0; m < N_; ++m) {
+          if (m == n) continue;
+          const int R = (int)ranks_[m];
+          ttm_generic(cur, (long long)prod(gd, 0, m), R, (long long)prod(gd, m + 1), gram(m), R, 1,
+                      R, qb[which], ss);
+          cur = qb[which];
+          which ^= 1;
+        }
+        const long long O = (long long)prod(ranks_, 0, n);
+        const long long J = (long long)prod(ranks_, n + 1);
+        contract_except(core_.as<double>(), cur, O, Rn, Rn, J, kk, ss);
+        k_add_diag<<<ceil_div(Rn, 64), 64, 0, ss>>>(kk, Rn, opt_.lambda);
+        RTB_LAUNCH_CHECK();
+      }
       // (KK^T + lambda I)^+ (ref linalg.cpp:8-26): warp Cholesky inverse; if a
       // pivot is below R*eps*max diag the eigen/pinv path (singular values =
       // |eigenvalues|, cutoff R*eps*sigma_max) takes over on the device.

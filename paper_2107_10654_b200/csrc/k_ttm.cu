@@ -984,6 +984,52 @@ __global__ void __launch_bounds__(256) k_ttm_expand(const double* __restrict__ Y
   }
 }
 
+// Same up-projection for R, J <= 16 (P = W x_2 A_2 at C2: 512 o x 512 i x 16 j): a thread owns
+// one output row i (A[i, :] in registers) and all J outputs of it, for och consecutive o; Y[o]
+// (R x J) is staged in shared memory and read as broadcasts. The general kernel above reads two
+// shared operands per FMA and was bound by shared-memory wavefronts there (40 us).
+template <int RM, int JM>
+__global__ void __launch_bounds__(256) k_ttm_expand_rows(const double* __restrict__ Y, int R, int J,
+                                                        const double* __restrict__ A, int I,
+                                                        long long O, int och,
+                                                        double* __restrict__ out,
+                                                        const int* __restrict__ need) {
+  RTB_GUARD()
+  __shared__ double ys[RM * JM];
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  double a[RM];
+#pragma unroll
+  for (int r = 0; r < RM; ++r) a[r] = (i < I && r < R) ? A[(long long)i * R + r] : 0.0;
+  const long long o0 = (long long)blockIdx.y * och;
+  const long long o1 = o0 + och < O ? o0 + och : O;
+  for (long long o = o0; o < o1; ++o) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < RM * JM; e += 256) {
+      const int r = e / JM, j = e - r * JM;
+      ys[e] = (r < R && j < J) ? Y[(o * R + r) * J + j] : 0.0;
+    }
+    __syncthreads();
+    double acc[JM];
+#pragma unroll
+    for (int j = 0; j < JM; ++j) acc[j] = 0.0;
+#pragma unroll
+    for (int r = 0; r < RM; ++r)
+#pragma unroll
+      for (int j = 0; j < JM; ++j) acc[j] = fma(a[r], ys[r * JM + j], acc[j]);
+    if (i < I) {
+      double* op = out + (o * I + i) * J;
+      if (J == JM && (JM % 2) == 0) {
+#pragma unroll
+        for (int j = 0; j < JM; j += 2) *reinterpret_cast<double2*>(op + j) = make_double2(acc[j], acc[j + 1]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < JM; ++j)
+          if (j < J) op[j] = acc[j];
+      }
+    }
+  }
+}
+
 // Deterministic sum of per-block partials (fixed order), one block.
 __global__ void k_sum_partials(const double* __restrict__ partial, long long n,
                                double* __restrict__ out, const int* __restrict__ need) {
@@ -1801,8 +1847,25 @@ bool ttm_expand(const double* Y, long long O, int R, long long J, const double* 
                 double* out, cudaStream_t st) {
   // big i chunks (A rows staged once per CTA, several outputs per thread), shrunk
   // until there are enough blocks to fill the GPU
+  // (each CTA stages all of Y[o] (R x J): when that is large, about one wave of CTAs
+  // amortises it better than many small ones -- W = G x_1 A_1 at C2: 512 CTAs each staging
+  // 32 KB took 23 us)
   int ich = 128;
-  while (ich > 1 && O * ceil_div(I, ich) < 4 * kNumSMs) ich >>= 1;
+  const long long minb = (long long)R * J >= 2048 ? kNumSMs / 2 : 4LL * kNumSMs;
+  while (ich > 1 && O * ceil_div(I, ich) < minb) ich >>= 1;
+  if (R <= 16 && J <= 16 && (((uintptr_t)out & 15) == 0) && I >= 256) {
+    // row-owner kernel: about two CTAs per SM over (i blocks) x (o ranges)
+    const long long ib = ceil_div(I, 256);
+    int och = (int)std::max<long long>(1, (O * ib) / (2LL * kNumSMs));
+    if (ceil_div<long long>(O, och) > 65535) och = (int)ceil_div<long long>(O, 65535);
+    const dim3 grid((unsigned)ib, (unsigned)ceil_div<long long>(O, och));
+    if (J <= 8)
+      k_ttm_expand_rows<16, 8><<<grid, 256, 0, st>>>(Y, R, (int)J, A, I, O, och, out, g_need);
+    else
+      k_ttm_expand_rows<16, 16><<<grid, 256, 0, st>>>(Y, R, (int)J, A, I, O, och, out, g_need);
+    RTB_LAUNCH_CHECK();
+    return true;
+  }
   const size_t smem = ((size_t)R * J + (size_t)ich * R) * sizeof(double);
   if (smem > 48 * 1024 || O > 65535) return false;
   k_ttm_expand<<<dim3((unsigned)ceil_div(I, ich), (unsigned)O), 256, smem, st>>>(Y, R, J, A, I,

@@ -1993,6 +1993,9 @@ class Engine {
     const int I = (int)shape_[N_ - 1];
     double* partial = partial_.as<double>();
     long long nparts;
+    // the ridge term's norms (core and factors are final here) on a side branch next to the
+    // X pass
+    norms_into(scal_.as<double>() + 1, fork());
     if (kGenerateP && N_ == 3 && ttm_last_pgen_ok(I, R)) {
       // P rows generated inside the pass from W = G x_1 A_1 and A_2 (no P in HBM)
       double* W = tmp_a_.as<double>();
@@ -2038,13 +2041,13 @@ class Engine {
     double* sc = scal_.as<double>();
     sum_partials(partial, nparts, sc, st_);
     allreduce(sc, 1);  // shard residuals
-    norms_into(sc + 1);
+    join();
     k_finish_loss<<<1, 1, 0, st_>>>(sc, sc + 1, opt_.lambda, (double)total_, loss_dev, rmse_dev);
     RTB_LAUNCH_CHECK();
   }
 
   // sum of squares of the core and all factors (the ridge term) into *out
-  void norms_into(double* out) {
+  void norms_into(double* out, cudaStream_t st = nullptr) {
     NormSet ns{};
     ns.count = N_ + 1;
     ns.p[0] = core_.as<double>();
@@ -2053,7 +2056,7 @@ class Engine {
       ns.p[n + 1] = factor(n);
       ns.n[n + 1] = (long long)(shape_[n] * ranks_[n]);
     }
-    k_norms<<<1, 1024, 0, st_>>>(ns, out);
+    k_norms<<<1, 1024, 0, st ? st : st_>>>(ns, out);
     RTB_LAUNCH_CHECK();
   }
 

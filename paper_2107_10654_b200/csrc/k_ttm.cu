@@ -995,8 +995,10 @@ __global__ void __launch_bounds__(256) k_ttm_expand_rows(const double* __restric
                                                         double* __restrict__ out,
                                                         const int* __restrict__ need) {
   RTB_GUARD()
-  __shared__ double ys[RM * JM];
+  __shared__ __align__(16) double ys[RM * JM];
+  __shared__ __align__(16) double ot[8][32 * (JM + 1)];  // per warp: 32 rows of outputs
   const int i = blockIdx.x * 256 + threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double a[RM];
 #pragma unroll
   for (int r = 0; r < RM; ++r) a[r] = (i < I && r < R) ? A[(long long)i * R + r] : 0.0;
@@ -1015,18 +1017,24 @@ __global__ void __launch_bounds__(256) k_ttm_expand_rows(const double* __restric
 #pragma unroll
     for (int r = 0; r < RM; ++r)
 #pragma unroll
-      for (int j = 0; j < JM; ++j) acc[j] = fma(a[r], ys[r * JM + j], acc[j]);
-    if (i < I) {
-      double* op = out + (o * I + i) * J;
-      if (J == JM && (JM % 2) == 0) {
-#pragma unroll
-        for (int j = 0; j < JM; j += 2) *reinterpret_cast<double2*>(op + j) = make_double2(acc[j], acc[j + 1]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < JM; ++j)
-          if (j < J) op[j] = acc[j];
+      for (int j = 0; j < JM; j += 2) {
+        const double2 y2 = *reinterpret_cast<const double2*>(ys + r * JM + j);  // broadcast
+        acc[j] = fma(a[r], y2.x, acc[j]);
+        acc[j + 1] = fma(a[r], y2.y, acc[j + 1]);
       }
+    // the warp's 32 rows x J outputs are one contiguous run: stage them and store coalesced
+    double* ow = ot[warp];
+#pragma unroll
+    for (int j = 0; j < JM; ++j) ow[lane * (JM + 1) + j] = acc[j];
+    __syncwarp();
+    const int wi0 = blockIdx.x * 256 + warp * 32;
+    const int nr = min(32, I - wi0);
+    double* op = out + (o * I + wi0) * J;
+    for (int e = lane; e < nr * J; e += 32) {
+      const int rr = e / J, j = e - rr * J;
+      op[e] = ow[rr * (JM + 1) + j];
     }
+    __syncwarp();
   }
 }
 
@@ -1853,7 +1861,7 @@ bool ttm_expand(const double* Y, long long O, int R, long long J, const double* 
   int ich = 128;
   const long long minb = (long long)R * J >= 2048 ? kNumSMs / 2 : 4LL * kNumSMs;
   while (ich > 1 && O * ceil_div(I, ich) < minb) ich >>= 1;
-  if (R <= 16 && J <= 16 && (((uintptr_t)out & 15) == 0) && I >= 256) {
+  if (R <= 16 && J <= 16 && (J % 2) == 0 && I >= 256) {
     // row-owner kernel: about two CTAs per SM over (i blocks) x (o ranges)
     const long long ib = ceil_div(I, 256);
     int och = (int)std::max<long long>(1, (O * ib) / (2LL * kNumSMs));

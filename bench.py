@@ -337,7 +337,12 @@ def family_table(fam, steps, n_data, n_buckets, pcg_iters, peaks, hbm_peak):
     per = {k: v_[0] / steps for k, v_ in fam.items()}
     if "gram" in per:
         add("gram", per["gram"], flops=2.0 * (n_data * v[1] * v[2] + n_buckets * v[0] * v[1] * v[2]),
-            note="vech Gram: H_b GEMMs + contraction over buckets")
+            note="vech Gram: draw records + tables, H_b GEMMs (k_vech_bucket5), contraction over "
+                 "buckets (k_vech_contract3)")
+    if "gram_sort" in per:
+        add("gram_sort", per["gram_sort"],
+            note="bucket keys from A_1's CDF, stable key sort, bucket table and order; a side "
+                 "branch after F1 in the timed (graph) sweeps, off the critical path")
     if "ttm_last_loss" in per:
         add("ttm_last_loss", per["ttm_last_loss"], flops=4.0 * total * R3, hbm_bytes=8.0 * total,
             note="one X pass: T = X A_3 and the direct residual (X - P A_3^T)^2")
@@ -346,8 +351,9 @@ def family_table(fam, steps, n_data, n_buckets, pcg_iters, peaks, hbm_peak):
             note="X x_1 A_1^T (F3 projection) + three 32 MB T-based products")
     if "pcg" in per:
         d = RANKS[0] * RANKS[1] * RANKS[2]
-        add("pcg", per["pcg"], note=f"{pcg_iters} CG iterations on the blocked Gram "
-            f"({v[0] * v[1] * R3 * R3 * 8 / 1e6:.0f} MB, L2-resident), d={d}")
+        add("pcg", per["pcg"], note=f"{pcg_iters} CG iterations on the compact Gram "
+            f"({v[0] * v[1] * v[2] * 8 / 1e6:.0f} MB, slices resident in shared memory, "
+            f"k_pcg_split), d={d}")
     if "chol" in per:
         d = RANKS[0] * RANKS[1] * RANKS[2]
         add("chol", per["chol"], flops=d ** 3 / 3 + 2 * d * d)
@@ -366,10 +372,10 @@ def kernel_work(family, n_data, n_buckets):
     if family == "chol":
         return "tensor", "TFLOP/s", d ** 3 / 3 + 2 * d * d
     if family == "pcg":
-        # per solve: every CG iteration (+1 residual check) reads the blocked Gram once
-        # (L2-resident, but counted against the HBM roofline it would otherwise hit)
+        # per solve: every CG iteration (+1 residual check) reads the compact Gram once
+        # (shared-memory resident in k_pcg_split, counted against the HBM roofline)
         v = [r * (r + 1) // 2 for r in RANKS]
-        blk = v[0] * v[1] * RANKS[2] * RANKS[2] * 8
+        blk = v[0] * v[1] * v[2] * 8
         return "hbm", "GB/s", (PCG_ITERS[0] + 1) * blk
     if family == "gram":
         # vech-factored Gram: per data draw one rank-1 update of

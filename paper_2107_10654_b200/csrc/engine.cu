@@ -1336,12 +1336,18 @@ class Engine {
   // from the start of the sweep, overlapping the factor updates; update_core_sketched joins it.
   void decode_ahead(const unsigned long long* seed_dev) {
     static const bool off = std::getenv("RTB_NO_DECODE_AHEAD") != nullptr;  // experiments
-    if (off || opt_.profile || !dfork_ev_ || !opt_.sketched) return;
+    if (off || !dfork_ev_ || !opt_.sketched) return;
     const DrawSpec ds = core_draw_spec(core_sample_count(), 0, seed_dev);
-    const cudaStream_t side = side_stream(1);
-    RTB_CUDA(cudaEventRecord(dfork_ev_, st_));
-    RTB_CUDA(cudaStreamWaitEvent(side, dfork_ev_, 0));
-    draw_decode(ds, DrawWork{cdraw_work_.p, cdraw_work_.bytes}, side);
+    // profiled runs keep the same kernels, in line on the main stream (per-family events)
+    const cudaStream_t side = opt_.profile ? st_ : side_stream(1);
+    if (!opt_.profile) {
+      RTB_CUDA(cudaEventRecord(dfork_ev_, st_));
+      RTB_CUDA(cudaStreamWaitEvent(side, dfork_ev_, 0));
+    }
+    {
+      Scope sc(prof_, "draw");
+      draw_decode(ds, DrawWork{cdraw_work_.p, cdraw_work_.bytes}, side);
+    }
     RTB_CUDA(cudaEventRecord(djoin_ev_, side));
     decoded_ahead_ = true;
   }
@@ -1351,23 +1357,26 @@ class Engine {
   // order -- the Gram's whole sort stage leaves the critical path (it overlaps F2 and F3).
   void keys_ahead() {
     static const bool off = std::getenv("RTB_NO_KEYS_AHEAD") != nullptr;  // experiments
-    if (off || !decoded_ahead_ || N_ != 3 || opt_.factor_samples > 0 || rmax_ > 32 ||
-        opt_.profile)
-      return;
+    if (off || !decoded_ahead_ || N_ != 3 || opt_.factor_samples > 0 || rmax_ > 32) return;
     const uint64_t s = core_sample_count();
     const GramSpec gs = gram_spec(s);
     gram_work_.ensure(gram_work_bytes(gs), st_);
     const DrawSpec ds = core_draw_spec(s, 0, seed_dev_.as<unsigned long long>());
-    const cudaStream_t side = side_stream(1);
-    RTB_CUDA(cudaEventRecord(kfork_ev_, st_));
-    RTB_CUDA(cudaStreamWaitEvent(side, kfork_ev_, 0));
+    const cudaStream_t side = opt_.profile ? st_ : side_stream(1);
+    if (!opt_.profile) {
+      RTB_CUDA(cudaEventRecord(kfork_ev_, st_));
+      RTB_CUDA(cudaStreamWaitEvent(side, kfork_ev_, 0));
+    }
     compute_scores_range(0, 1, side);
-    const GramKeyBufs kb = gram_key_buffers(gs, gram_work_.p);
-    gram_keys_reset(gs, gram_work_.p, (unsigned long long*)data_draws_.p, side);
-    draw_keys(ds, scores_.as<double>(), cdf_.as<double>(), sums_.as<double>(),
-              DrawWork{cdraw_work_.p, cdraw_work_.bytes}, gs.i1_lo, gs.i1_hi, kb.keys, kb.vals,
-              kb.counts, kb.aug_count, (unsigned long long*)data_draws_.p, side);
-    gram_sort_keys(gs, gram_work_.p, side);
+    {
+      Scope sc(prof_, "gram_sort");
+      const GramKeyBufs kb = gram_key_buffers(gs, gram_work_.p);
+      gram_keys_reset(gs, gram_work_.p, (unsigned long long*)data_draws_.p, side);
+      draw_keys(ds, scores_.as<double>(), cdf_.as<double>(), sums_.as<double>(),
+                DrawWork{cdraw_work_.p, cdraw_work_.bytes}, gs.i1_lo, gs.i1_hi, kb.keys, kb.vals,
+                kb.counts, kb.aug_count, (unsigned long long*)data_draws_.p, side);
+      gram_sort_keys(gs, gram_work_.p, side);
+    }
     RTB_CUDA(cudaEventRecord(djoin_ev_, side));
     keys_ahead_ = true;
   }

@@ -842,8 +842,8 @@ def c3_lines(args, steps=None):
     del x
     steps = steps or args.steps
     lines = []
-    # sketched factor updates are a single-GPU perf mode
-    for fs in ((0, 50000) if world == 1 else (0,)):
+    # exact (reference semantics) and sketched (perf mode) factor updates, sharded alike
+    for fs in (0, 50000):
         opts = rt.options(lam=lam, sketched_core=1, sample_count_override=s, tolerance=0.0,
                           max_iterations=args.warmup + steps + 1)
         sess = rt.Session(t, ranks, opts, factor_samples=fs, shard=shard)
@@ -908,7 +908,7 @@ def c5_lines(args, steps=None):
     GPU: at N GPUs the tensor is (512 N) x 4096 x 2048, so N = 8 is BASELINE's 4096 x 4096 x 2048
     (275 GB) and N = 1 is the one-GPU share of it run as a whole ALS problem (weak scaling).
     Generated on the device shard by shard (rtucker_b200_tensor_generate_device); exact factor
-    updates (reference semantics) and, at N = 1, a sketched-factor line (1e5 samples)."""
+    updates (reference semantics) and a sketched-factor line (1e5 samples, perf mode)."""
     import torch
     from paper_2107_10654_b200 import rtucker as rt
     world = env_int("WORLD_SIZE", 1)
@@ -928,7 +928,7 @@ def c5_lines(args, steps=None):
     torch.cuda.synchronize()
     steps = steps or args.steps
     lines = []
-    for fs in ((0, 100000) if world == 1 else (0,)):
+    for fs in (0, 100000):
         opts = rt.options(lam=lam, sketched_core=1, sample_count_override=s, tolerance=0.0,
                           max_iterations=args.warmup + steps + 1)
         sess = rt.Session(t, ranks, opts, factor_samples=fs, shard=shard)

@@ -1415,8 +1415,10 @@ class Engine {
   // ---- sketched factor update (perf mode; k_fsketch.cu, orc_update_factor_sketched) ----
   void update_factor_sketched(int n, uint64_t seed,
                               const unsigned long long* seed_dev = nullptr) {
-    if (sharded()) throw Error(1, "sketched factor updates are not supported with sharding");
-    const int Rn = (int)ranks_[n], In = (int)shape_[n];
+    // under sharding (X split along mode 1): mode 1's fibers are this shard's segments (own
+    // rows of A_1, stitched by a zero-padded all-reduce as in update_factor); the other
+    // modes' Gram and M are partial sums over this shard's draws, all-reduced
+    const int Rn = (int)ranks_[n], In = (n == 0) ? (int)nloc_ : (int)shape_[n];
     if (Rn > 32) {  // the register-tiled gather kernel covers R_n <= 32
       update_factor(n);
       return;
@@ -1469,13 +1471,19 @@ class Engine {
     }
     fs.core = core_.as<double>();
     fs.x = x_;
-    // mode-n-last copy of X (made once per engine): every sampled fiber is contiguous
+    if (sharded()) {
+      fs.shard_lo = (int)lo_;
+      fs.shard_rows = (int)nloc_;
+      fs.count_aug = opt_.shard_rank == 0 ? 1 : 0;
+    }
+    // mode-n-last copy of this shard's X (made once per engine): every sampled fiber is
+    // contiguous
     if (n != N_ - 1 && xrot_ok_) {
       if (!xrot_[n].p) {
         try {
-          xrot_[n].ensure(total_ * 8, st_);
-          move_axis_last(x_, (long long)prod(shape_, 0, n), (int)shape_[n],
-                         (long long)prod(shape_, n + 1), xrot_[n].as<double>(), st_);
+          xrot_[n].ensure(ltotal_ * 8, st_);
+          move_axis_last(x_, (long long)prod(lshape_, 0, n), (int)lshape_[n],
+                         (long long)prod(lshape_, n + 1), xrot_[n].as<double>(), st_);
         } catch (const Error&) {
           cudaGetLastError();
           xrot_[n] = DevBuf();
@@ -1496,6 +1504,10 @@ class Engine {
       Scope sc(prof_, "factor_sketch");
       factor_sketch_normal_eq(fs, (const unsigned long long*)fsk_idx_.p, fsk_w_.as<double>(),
                               fsk_work_.p, kk, M, st_);
+      if (sharded() && n > 0) {  // partial sums over this shard's draws
+        allreduce(kk, (size_t)Rn * Rn);
+        allreduce(M, (size_t)In * Rn);
+      }
     }
     {
       // A_n = M pinv(Gram) (ref sketch_ridge.cpp:130-139 per fiber row), as in update_factor
@@ -1520,9 +1532,19 @@ class Engine {
                                      stride, pv, nullptr, okf);
       RTB_LAUNCH_CHECK();
       const long long tot = (long long)In * Rn;
-      k_rows_times_small<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(M, pv, In, Rn,
-                                                                        factor(n));
-      RTB_LAUNCH_CHECK();
+      if (n == 0 && sharded()) {
+        // own rows into a zeroed full-size A_1, then the sum over shards is the whole A_1
+        double* a1 = factor(0);
+        RTB_CUDA(cudaMemsetAsync(a1, 0, shape_[0] * Rn * 8, st_));
+        k_rows_times_small<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(M, pv, In, Rn,
+                                                                          a1 + (size_t)lo_ * Rn);
+        RTB_LAUNCH_CHECK();
+        allreduce(a1, shape_[0] * Rn);
+      } else {
+        k_rows_times_small<<<ceil_div<long long>(tot, 256), 256, 0, st_>>>(M, pv, In, Rn,
+                                                                          factor(n));
+        RTB_LAUNCH_CHECK();
+      }
     }
     factor_gram(n);
     scores_valid_ = false;

@@ -47,6 +47,8 @@ struct FskDev {
   int in;                           // I_n
   unsigned long long total_other;
   double root_lambda;
+  int o0_lo, o0_hi;                 // sharded, n > 0: mode-1 rows owned (o0_hi = 0: all)
+  int skip_aug;                     // sharded, n > 0: augmented rows counted elsewhere
 };
 
 // Gt[q][r] = G_(n)[r][q] (W x RM, zero-padded) and the digit offsets of q over the
@@ -107,11 +109,15 @@ __global__ void __launch_bounds__(256) k_fsk_rows(FskDev f, const double* __rest
           if (m < f.nother) {
             const int jm = (int)(rem % (unsigned long long)f.orow[m]);
             rem /= (unsigned long long)f.orow[m];
-            b += (long long)jm * f.oxstride[m];
+            // other mode 0 is mode 1 when n > 0: under sharding only its own rows are in x
+            const int jx = (m == 0 && f.o0_hi > 0) ? jm - f.o0_lo : jm;
+            if (m == 0 && f.o0_hi > 0 && (jm < f.o0_lo || jm >= f.o0_hi)) data = 0;
+            b += (long long)jx * f.oxstride[m];
             sj[lane * 8 + m] = jm;
           }
+        if (!data) b = 0;  // another shard's draw: k = 0 at a valid fiber, contributes nothing
       } else {
-        b = -1 - (long long)(id - f.total_other);
+        b = f.skip_aug ? 0 : -1 - (long long)(id - f.total_other);
       }
       base[t] = b;
     }
@@ -540,8 +546,13 @@ struct FskLayout {
 };
 
 // the TMA-staged gather applies: contiguous fibers of even length <= 1024, R_n^2 <= 256
+// fiber length in x: mode 1 under sharding holds this shard's rows only
+int fsk_in(const FactorSketchSpec& sp) {
+  return (sp.mode == 0 && sp.shard_rows > 0) ? sp.shard_rows : sp.rows[sp.mode];
+}
+
 bool fsk_tma(const FactorSketchSpec& sp) {
-  const int n = sp.mode, in = sp.rows[n], rn = sp.ranks[n];
+  const int n = sp.mode, in = fsk_in(sp), rn = sp.ranks[n];
   const bool contiguous = (sp.x_mode_last || n == sp.order - 1) && in % 2 == 0 &&
                           std::getenv("RTB_NO_FSK2") == nullptr;
   return contiguous && in <= 1024 && rn * rn <= 256 && tma_smem(in, rm_of(rn)) <= 220 * 1024 &&
@@ -550,7 +561,7 @@ bool fsk_tma(const FactorSketchSpec& sp) {
 
 FskLayout fsk_layout(const FactorSketchSpec& sp, void* work) {
   const int RM = rm_of(sp.ranks[sp.mode]);
-  const int in = sp.rows[sp.mode], rn = sp.ranks[sp.mode];
+  const int in = fsk_in(sp), rn = sp.ranks[sp.mode];
   const int tiles = ceil_div(in, kTile);
   const long long s = (long long)sp.s;
   // one wave of work units: the TMA gather runs one CTA per SM (fewer chunk partials too)
@@ -628,28 +639,37 @@ void factor_sketch_normal_eq(const FactorSketchSpec& sp, const unsigned long lon
   f.order = sp.order;
   f.mode = n;
   f.rn = rn;
-  f.in = sp.rows[n];
+  f.in = fsk_in(sp);
+  const bool sharded = sp.shard_rows > 0;
+  if (sharded && (sp.shard_lo < 0 || sp.shard_lo + sp.shard_rows > sp.rows[0]))
+    throw Error(1, "factor_sketch: bad shard rows");
   long long xs[8];
   int cs[8];
   {
+    // X strides over the rows x actually holds (mode 1: this shard's)
+    int xr[8];
+    for (int m = 0; m < sp.order; ++m) xr[m] = (m == 0 && sharded) ? sp.shard_rows : sp.rows[m];
     long long a = 1;
     int c = 1;
     for (int m = sp.order - 1; m >= 0; --m) {
       xs[m] = a;
       cs[m] = c;
-      a *= sp.rows[m];
+      a *= xr[m];
       c *= sp.ranks[m];
     }
     if (sp.x_mode_last) {  // axes: other modes ascending, then mode n (stride 1)
-      a = sp.rows[n];
+      a = xr[n];
       xs[n] = 1;
       for (int m = sp.order - 1; m >= 0; --m) {
         if (m == n) continue;
         xs[m] = a;
-        a *= sp.rows[m];
+        a *= xr[m];
       }
     }
   }
+  f.o0_lo = (sharded && n > 0) ? sp.shard_lo : 0;
+  f.o0_hi = (sharded && n > 0) ? sp.shard_lo + sp.shard_rows : 0;
+  f.skip_aug = (sharded && n > 0 && !sp.count_aug) ? 1 : 0;
   f.cstride_n = cs[n];
   f.xstride_n = xs[n];
   f.width = 1;

@@ -127,6 +127,12 @@ struct FactorSketchSpec {
   // 1: x is the mode-n-last copy of X (axes: the other modes ascending, then mode n;
   // move_axis_last), so every sampled fiber is one contiguous run of I_n values
   int x_mode_last = 0;
+  // multi-GPU (X split along mode 1): x holds mode-1 rows [shard_lo, shard_lo + shard_rows)
+  // (shard_rows = 0: the whole tensor). Draws are decoded with the global rows. For mode n > 0
+  // only this shard's data draws contribute (partial Gram / M, to be summed over shards) and
+  // the augmented rows only where count_aug; for n == 0 the fibers are this shard's segments
+  // (M has shard_rows rows) and the Gram is the whole one on every shard.
+  int shard_lo = 0, shard_rows = 0, count_aug = 1;
 };
 // out = X with axis of length In moved last: X viewed as [A][In][B] -> out [A][B][In]
 void move_axis_last(const double* x, long long A, int In, long long B, double* out,

@@ -89,10 +89,3 @@ def test_factor_sketch_keeps_a_converged_model(rt):
     sk = rt.als_run(xt, ranks, rt.options(max_iterations=2, **opts), init_model=m,
                     factor_samples=20000)
     assert sk.final_loss <= 1.05 * base.final_loss
-
-
-def test_factor_sketch_rejects_sharding(rt):
-    x = rt.Tensor.from_numpy(planted((8, 6, 5), (2, 2, 2)))
-    sh = rt.Shard(0, 2, 16, lambda ptr, n, st: None)
-    with pytest.raises(rt.RtuckerError):
-        rt.als_run(x, (2, 2, 2), rt.options(max_iterations=1), shard=sh, factor_samples=100)

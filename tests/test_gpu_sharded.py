@@ -124,6 +124,33 @@ def test_sharded_order4_bucketed_path(rt, P):
     assert sum(o[2]["data_draws"] for o in outs) == ref.sketch_info()["data_draws"]
 
 
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("order", [3, 4])
+def test_sharded_factor_sketch_matches_single_process(rt, P, order):
+    """Sketched factor updates (perf mode) across shards: mode 1's sampled fibers are split
+    into the shards' segments (own rows of A_1, stitched), the other modes' fibers are
+    gathered by the shard owning their i_1 and the partial Gram / M all-reduced; augmented rows
+    count on shard 0 only. Same draws on every shard, so the result is the single-process one
+    up to the regrouped sums."""
+    if order == 3:
+        shape, ranks, fs = (36, 30, 28), (4, 3, 5), 3000
+    else:
+        shape, ranks, fs = (20, 18, 16, 14), (3, 3, 2, 2), 4000
+    x = planted(shape, ranks, seed=44)
+    kw = dict(lam=1e-2, sketched_core=1, sample_count_override=8000, max_iterations=3,
+              tolerance=0.0, record_history=1, seed=9)
+    ref = rt.als_run(rt.Tensor.from_numpy(x), ranks, rt.options(**kw), factor_samples=fs)
+    outs = run_sharded(rt, x, ranks, kw, P, factor_samples=fs)
+    rh, rm = ref.history(), ref.model()
+    for hist, model, info in outs:
+        assert [(h[0], h[1]) for h in hist] == [(h[0], h[1]) for h in rh]
+        for (gi, gs, gl, grm), (_, _, fl, frm) in zip(hist, rh):
+            assert abs(gl - fl) / fl < 1e-7, (gi, gs, gl, fl)
+        for a, b in zip(model.factors, rm.factors):
+            assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-5
+        assert np.linalg.norm(model.core - rm.core) / np.linalg.norm(rm.core) < 1e-5
+
+
 def test_sharded_rejects_bad_split(rt):
     x = planted((20, 10, 8), (2, 2, 2), seed=1)
     with pytest.raises(rt.RtuckerError):

@@ -8,7 +8,9 @@ the collective: (1) the row split partitions [0, I_1); (2) the mode-1
 contraction of the X slabs sums to the full X x_1 A_1^T; (3) the normal
 equations of the shard-local data draws plus the (replicated) augmented draws
 sum to the full sketched normal equations; (4) the stitched A_1 rows (zero
-elsewhere) sum to the full factor."""
+elsewhere) sum to the full factor; (5) the perf-mode sketched factor update across shards:
+mode 1's fibers split into the shards' row segments, the other modes' draws owned by the
+shard of their i_1 (augmented rows on shard 0), partial Gram / M summed."""
 import os
 import socket
 
@@ -86,12 +88,82 @@ def _worker(rank, world, port, q, case=0):
         a1[lo:hi] = fs[0][lo:hi]
         ar(a1.ctypes.data, a1.size, 0)
         assert np.array_equal(a1, fs[0])
+        # (5) sketched factor updates (perf mode) across shards, with the oracle's draws
+        for mode in range(len(shape)):
+            _fsk_decomposition(o, ar, rank, shape, ranks, core, fs, x, lo, hi, mode)
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
     except BaseException as e:  # noqa: BLE001
         import traceback
         q.put((rank, traceback.format_exc()))
+
+
+def _fsk_normal_eq(shape, ranks, core, fs, x, lam, mode, idx, w, keep, rows=None):
+    """Gram (R_n x R_n) and M (I_n x R_n) of the perf-mode factor sketch (k_fsketch.cu) over
+    the draws selected by `keep`; `rows` restricts the fibers to mode-1 rows [lo, hi) (mode 1
+    sharded)."""
+    other = [m for m in range(len(shape)) if m != mode]
+    total_o = int(np.prod([shape[m] for m in other]))
+    gn = np.moveaxis(core, mode, 0).reshape(ranks[mode], -1)  # G_(n), other modes ascending
+    rn = ranks[mode]
+    G = np.zeros((rn, rn))
+    M = np.zeros((shape[mode] if rows is None else rows[1] - rows[0], rn))
+    for t in np.nonzero(keep)[0]:
+        i = int(idx[t])
+        if i >= total_o:
+            j = i - total_o
+            G[j, j] += lam * w[t] ** 2
+            continue
+        js, rem = [], i
+        for m in reversed(other):
+            js.append(rem % shape[m])
+            rem //= shape[m]
+        js = js[::-1]
+        z = np.ones(1)
+        for m, jm in zip(other, js):
+            z = np.kron(z, fs[m][jm])
+        k = gn @ z
+        G += w[t] ** 2 * np.outer(k, k)
+        sl = [slice(None)] * len(shape)
+        for m, jm in zip(other, js):
+            sl[m] = jm
+        fib = x[tuple(sl)]
+        if rows is not None:
+            fib = fib[rows[0]:rows[1]]
+        M += w[t] ** 2 * np.outer(fib, k)
+    return G, M
+
+
+def _fsk_decomposition(o, ar, rank, shape, ranks, core, fs, x, lo, hi, mode):
+    lam, s, seed = 0.05, 600, 23
+    new, idx, w = o.update_factor_sketched(shape, ranks, core, fs, lam, x, mode + 1, s, seed)
+    allk = np.ones(s, bool)
+    Gf, Mf = _fsk_normal_eq(shape, ranks, core, fs, x, lam, mode, idx, w, allk)
+    # the restatement reproduces the oracle's update: A_n = M Gram^-1
+    assert np.linalg.norm(Mf @ np.linalg.inv(Gf) - new) / np.linalg.norm(new) < 1e-10
+    other = [m for m in range(len(shape)) if m != mode]
+    total_o = int(np.prod([shape[m] for m in other]))
+    if mode == 0:
+        # fibers along the sharded mode: this shard's segments, the whole Gram everywhere
+        G, M = _fsk_normal_eq(shape, ranks, core, fs, x, lam, 0, idx, w, allk, rows=(lo, hi))
+        assert np.allclose(G, Gf, rtol=1e-13, atol=0)
+        full = np.zeros_like(Mf)
+        full[lo:hi] = M
+        ar(full.ctypes.data, full.size, 0)
+        assert np.allclose(full, Mf, rtol=1e-12, atol=1e-12 * np.abs(Mf).max())
+    else:
+        # the data draws of this shard's i_1 rows, the augmented rows on shard 0
+        inner = total_o // shape[0]
+        data = idx < total_o
+        i1 = np.where(data, idx // inner, -1)
+        keep = (data & (i1 >= lo) & (i1 < hi)) | (~data & (rank == 0))
+        G, M = _fsk_normal_eq(shape, ranks, core, fs, x, lam, mode, idx, w, keep)
+        G, M = np.ascontiguousarray(G), np.ascontiguousarray(M)
+        ar(G.ctypes.data, G.size, 0)
+        ar(M.ctypes.data, M.size, 0)
+        assert np.allclose(G, Gf, rtol=1e-12, atol=1e-12 * np.abs(Gf).max())
+        assert np.allclose(M, Mf, rtol=1e-12, atol=1e-12 * np.abs(Mf).max())
 
 
 @pytest.mark.parametrize("world", [2])

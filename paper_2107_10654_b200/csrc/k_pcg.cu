@@ -1085,6 +1085,294 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
 }
 
 // ---------------------------------------------------------------------------
+// Large-d PCG with DISTRIBUTED vectors (k_pcg_dv). k_pcg's large-d form keeps six d-vectors per
+// CTA in global memory and updates / preconditions all of them redundantly in every CTA: at
+// C5 (d = 32768) that is 148 x 1.5 MB of vector traffic per iteration (3.7 ms of
+// preconditioning per solve), at C3 (d = 10^4) 0.6 ms. Here every d-vector exists once (x, r,
+// p, z, scratch, in the workspace); each CTA updates its own rows, dot products are per-CTA
+// partials summed by every CTA in a fixed order after a grid barrier (deterministic), and
+// M^-1 r = (x)_n P_n r is N grid-strided mode products with a grid barrier between modes.
+// Per iteration: matvec (slice partials, own-row sums), alpha, the r / x update, N mode
+// products, rho, the p update: 5 + N grid barriers and no redundant vector work.
+__device__ __forceinline__ void mode_product_dv(const double* __restrict__ in, double* __restrict__ out,
+                                                const double* P, int RM, int R, int J, int d) {
+  const int RJ = R * J;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d; e += gridDim.x * blockDim.x) {
+    const int o = e / RJ, rem = e - o * RJ;
+    const int j = rem / J, k = rem - j * J;
+    const double* x = in + o * RJ + k;
+    double acc = 0.0;
+    for (int i = 0; i < R; ++i) acc = fma(P[i * RM + j], __ldcg(x + i * J), acc);
+    out[e] = acc;
+  }
+}
+
+template <int RM>
+__global__ void __launch_bounds__(kThreads, 1) k_pcg_dv(const PcgArgs A, const PcgShared shc) {
+  extern __shared__ __align__(16) double sm[];
+  const PcgShared& sh = shc;
+  const int d = sh.d;
+  const int dv = (d + 1) & ~1;
+  double* Ps = sm;                          // [order][RM][RM]: P_n (P form) or V_n (eigen form)
+  double* VTs = Ps + sh.order * RM * RM;    // [order][RM][RM]: V_n^T (eigen form)
+  double* red = VTs + sh.order * RM * RM;   // [32] block reductions
+  double* acc32 = red + 32;                 // tiled rank-32 matvec accumulators
+  double* gx = A.vglobal;                   // the d-vectors, one copy each
+  double* gr = gx + dv;
+  double* gp = gr + dv;
+  double* ga = gp + dv;
+  double* gb = ga + dv;
+  double* gdinv = gb + dv;
+  __shared__ double bcast[2];
+  double* gpart0 = gdinv + dv;              // [2][gridDim.x][2] per-CTA partial sums,
+  int nsum = 0;                             // double-buffered by sum parity
+  const bool t32 = sh.t32 != 0;
+  const int row0 = min(d, (int)blockIdx.x * sh.rows_per_cta);
+  const int row1 = min(d, row0 + sh.rows_per_cta);
+  unsigned sync_target = 0;
+  auto gsync = [&]() {
+    sync_target += gridDim.x;
+    grid_barrier(A.counter, sync_target);
+  };
+  // sums of up to 2 per-CTA partials over the grid, identical in every CTA
+  // (a CTA writes sum k + 2's partial only after sum k + 1's barrier, which every CTA reaches
+  // only after reading sum k's partials: two buffers suffice)
+  auto gsum2 = [&](double& v0, double& v1) {
+    block_sum2_det(v0, v1, red);
+    double* gpart = gpart0 + (size_t)(nsum & 1) * gridDim.x * 2;
+    ++nsum;
+    if (threadIdx.x == 0) {
+      gpart[blockIdx.x * 2] = v0;
+      gpart[blockIdx.x * 2 + 1] = v1;
+    }
+    gsync();
+    // warp 0 sums the partials (lane-strided, then a fixed shuffle tree: the same order in
+    // every CTA) and broadcasts
+    if (threadIdx.x < 32) {
+      double t0 = 0.0, t1 = 0.0;
+      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) {
+        t0 += __ldcg(gpart + c * 2);
+        t1 += __ldcg(gpart + c * 2 + 1);
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+        t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+      }
+      if (threadIdx.x == 0) {
+        bcast[0] = t0;
+        bcast[1] = t1;
+      }
+    }
+    __syncthreads();
+    v0 = bcast[0];
+    v1 = bcast[1];
+    __syncthreads();
+  };
+  auto gsum = [&](double v) {
+    double z = 0.0;
+    gsum2(v, z);
+    return v;
+  };
+  unsigned mv = 0;
+  const unsigned tick_per = (unsigned)sh.m1 * sh.ntile + gridDim.x * kWarps;
+  // q (own rows, A.q) = G src, src published in global memory
+  auto matvec = [&](const double* src) {
+    if (t32) slice_partials_t32(A, sh, src, acc32, (mv++) * tick_per);
+    else slice_partials<RM>(A, sh, src);
+    __syncthreads();
+    gsync();
+    if (t32) reduce_rows_t32(A, sh, src, row0, row1 - row0, A.q);
+    else reduce_rows<false>(A, sh, src, row0, row1 - row0, A.q);
+    __syncthreads();
+  };
+
+  int missing = 0;
+  for (int e = threadIdx.x; e < d; e += kThreads) missing |= __ldg(A.aug_count + e) == 0;
+  if (threadIdx.x < sh.order) missing |= __ldg(A.linv_ok + threadIdx.x) == 0;
+  const double pnorm = A.prep[1];
+  if (__syncthreads_or(missing) || !(A.lambda > 0.0) || !(A.lambda * pnorm <= kMaxLambdaOverMu)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      A.status[0] = 3;
+      A.status[1] = 0;
+    }
+    return;
+  }
+  for (int n = 0; n < sh.order; ++n) {
+    const int R = sh.R[n];
+    const double* Pg = A.pinv + (size_t)n * A.linv_stride;
+    for (int e = threadIdx.x; e < RM * RM; e += kThreads) {
+      const int i = e / RM, j = e - i * RM;
+      Ps[n * RM * RM + e] = (i < R && j < R) ? Pg[i * R + j] : 0.0;
+    }
+  }
+  const double gnorm = A.prep[0];
+  const bool eig = A.prep[2] != 0.0;
+  if (eig) {
+    for (int n = 0; n < sh.order; ++n) {
+      const int R = sh.R[n];
+      const double* Vg = A.evecs + (size_t)n * A.linv_stride;
+      for (int e = threadIdx.x; e < RM * RM; e += kThreads) {
+        const int i = e / RM, j = e - i * RM;
+        const bool in = i < R && j < R;
+        Ps[n * RM * RM + e] = in ? Vg[i * R + j] : 0.0;
+        VTs[n * RM * RM + e] = in ? Vg[j * R + i] : 0.0;
+      }
+    }
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+      double m = 1.0;
+      int rem = e;
+      for (int n = sh.order - 1; n >= 0; --n) {
+        const int j = rem % sh.R[n];
+        rem /= sh.R[n];
+        m *= fmax(A.evals[(size_t)n * A.linv_stride + j], 0.0);
+      }
+      gdinv[e] = 1.0 / (m + A.lambda);
+    }
+  }
+  __syncthreads();
+  // z = M^-1 src (src complete in global memory): N (or 2N + 1) grid-strided passes
+  auto precond = [&](const double* src) -> double* {
+    const double* cur = src;
+    double* dst = ga;
+    for (int n = 0; n < sh.order; ++n) {
+      mode_product_dv(cur, dst, Ps + n * RM * RM, RM, sh.R[n], sh.J[n], d);
+      gsync();
+      cur = dst;
+      dst = (dst == ga) ? gb : ga;
+    }
+    if (eig) {
+      double* t = const_cast<double*>(cur);
+      for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d; e += gridDim.x * blockDim.x)
+        t[e] *= gdinv[e];
+      gsync();
+      for (int n = 0; n < sh.order; ++n) {
+        mode_product_dv(cur, dst, VTs + n * RM * RM, RM, sh.R[n], sh.J[n], d);
+        gsync();
+        cur = dst;
+        dst = (dst == ga) ? gb : ga;
+      }
+    }
+    return const_cast<double*>(cur);
+  };
+
+  double bb = 0.0;
+  for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+    const double be = A.b[e];
+    gr[e] = be;
+    gx[e] = 0.0;
+    bb = fma(be, be, bb);
+  }
+  bb = gsum(bb);
+  if (bb == 0.0) {
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) A.x[e] = 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      A.status[0] = 0;
+      A.status[1] = 0;
+    }
+    return;
+  }
+  if (A.warm_dev ? *A.warm_dev : A.warm) {
+    // r0 = b - G x0, kept only if it beats the cold residual ||b||
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) gx[e] = A.x[e];
+    __syncthreads();
+    gsync();
+    matvec(gx);
+    double r0 = 0.0;
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+      const double re = A.b[e] - A.q[e];
+      r0 = fma(re, re, r0);
+    }
+    r0 = gsum(r0);
+    const bool keep = r0 < bb && isfinite(r0);
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+      if (keep) gr[e] = A.b[e] - A.q[e];
+      else gx[e] = 0.0;
+    }
+    __syncthreads();
+    gsync();
+  } else {
+    gsync();  // r complete before the first preconditioning
+  }
+  double* z = precond(gr);
+  double rho = 0.0;
+  for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+    gp[e] = z[e];
+    rho = fma(gr[e], z[e], rho);
+  }
+  rho = gsum(rho);  // its barrier also publishes p
+  const double tol2 = A.tol * A.tol;
+  int it = 0, fail = 0;
+  const bool prof = A.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long t0 = prof ? gtimer() : 0, t1;
+#define RTB_DV_MARK(k)                  \
+  if (prof) {                           \
+    t1 = gtimer();                      \
+    A.prof[k] += t1 - t0;               \
+    t0 = t1;                            \
+  }
+  for (; it < A.max_iter; ++it) {
+    matvec(gp);
+    RTB_DV_MARK(0)
+    double pq = 0.0;
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) pq = fma(gp[e], A.q[e], pq);
+    pq = gsum(pq);
+    if (!(pq > 0.0) || !isfinite(pq)) {
+      fail = 2;
+      break;
+    }
+    const double alpha = rho / pq;
+    double rr = 0.0, xx = 0.0;
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+      const double re = fma(-alpha, A.q[e], gr[e]);
+      gr[e] = re;
+      rr = fma(re, re, rr);
+      const double xe = fma(alpha, gp[e], gx[e]);
+      gx[e] = xe;
+      xx = fma(xe, xe, xx);
+    }
+    gsum2(rr, xx);  // its barrier also completes r for the preconditioner
+    RTB_DV_MARK(4)
+    if (rr <= tol2 * fmax(bb, gnorm * gnorm * xx)) {
+      ++it;
+      break;
+    }
+    z = precond(gr);
+    RTB_DV_MARK(5)
+    double rho2 = 0.0;
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) rho2 = fma(gr[e], z[e], rho2);
+    rho2 = gsum(rho2);
+    const double beta = rho2 / rho;
+    rho = rho2;
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) gp[e] = fma(beta, gp[e], z[e]);
+    __syncthreads();
+    gsync();  // p published
+    RTB_DV_MARK(6)
+  }
+#undef RTB_DV_MARK
+  // x out; true residual ||b - G x|| with one more matvec
+  double xx = 0.0;
+  for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+    A.x[e] = gx[e];
+    xx = fma(gx[e], gx[e], xx);
+  }
+  xx = gsum(xx);  // also publishes x for the matvec
+  matvec(gx);
+  double res = 0.0;
+  for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+    const double t = A.b[e] - A.q[e];
+    res = fma(t, t, res);
+  }
+  res = gsum(res);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int st = fail;
+    const double scale = gnorm * sqrt(xx) + sqrt(bb);
+    if (!st && !(res <= A.check_tol * A.check_tol * scale * scale)) st = 1;
+    A.status[0] = st;
+    A.status[1] = it;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Split-role PCG (order 3, R_3 = 16, m_1 slices < #SMs): the Gram stays in SHARED MEMORY for
 // the whole solve. CTA u < m_1 holds slice u_1 = u of the compact (vech) Gram S -- row u_1
 // of S, m_2 x 136 values, 148 KB at C2 -- and computes that slice's matvec partials; the
@@ -1733,8 +2021,11 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   RTB_CUDA(cudaMemsetAsync(a.counter, 0, 64, st));
   bool all16 = true;
   for (int n = 0; n < spec.order; ++n) all16 &= spec.ranks[n] == 16;
-  void* fn = big ? (rm == 8 ? (void*)k_pcg<8, 0, true>
-                            : rm == 16 ? (void*)k_pcg<16, 0, true> : (void*)k_pcg<32, 0, true>)
+  static const bool no_dv = std::getenv("RTB_NO_PCG_DV") != nullptr;  // experiments
+  void* fn = big ? (no_dv ? (rm == 8 ? (void*)k_pcg<8, 0, true>
+                                     : rm == 16 ? (void*)k_pcg<16, 0, true> : (void*)k_pcg<32, 0, true>)
+                          : (rm == 8 ? (void*)k_pcg_dv<8>
+                                     : rm == 16 ? (void*)k_pcg_dv<16> : (void*)k_pcg_dv<32>))
            : all16 ? (void*)k_pcg<16, 16, false>
            : rm == 8 ? (void*)k_pcg<8, 0, false>
            : rm == 16 ? (void*)k_pcg<16, 0, false> : (void*)k_pcg<32, 0, false>;
@@ -1744,6 +2035,7 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   RTB_LAUNCH_CHECK();
   if (!big && all16) count_variant("k_pcg<16,16>");
   if (sh.t32) count_variant("k_pcg_t32");
+  if (big && !no_dv) count_variant("k_pcg_dv");
   if (prof_on) {
     unsigned long long h[16];
     int stat[2];

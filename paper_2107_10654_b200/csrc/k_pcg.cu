@@ -54,6 +54,7 @@ struct PcgShared {
   int t32;        // tiled rank-32 matvec (slice_partials_t32): order 3, R_3 = 32, R_2 % 8 == 0
   int ng;         // t32: groups of 8 middle indices (R_2 / 8)
   int ntile;      // t32: tiles per slice, ng (ng + 1) / 2 (off-diagonal first)
+  int t4;         // tiled order-4 matvec (slice_partials_t4)
 };
 
 struct PcgArgs {
@@ -641,6 +642,154 @@ __device__ void reduce_rows_t32(const PcgArgs& A, const PcgShared& sh, const dou
   }
 }
 
+// (A) tiled path, order 4 (C3: R = 10, d = 10^4, 133 MB of blocks per matvec): every block
+// B[u1][u2][u3] (L x L, L = R_4, symmetric) is read ONCE and applied to all of its targets:
+// sides (q_a <- p_b, q_b <- p_a) x orientations of u2 = v(i2, j2) x orientations of
+// u3 = v(i3, j3) (up to 8). Work unit = one warp on (u1, u2) and all m3 blocks of u3, from a
+// ticket counter; the sources p_{a,b}[{i2, j2}][:][:] and the targets q_{a,b}[{i2, j2}][:][:]
+// (4 R3 L values each) live in the warp's shared memory. Lanes form G = 32 / L groups, group g
+// takes block u3 = u3_0 + g, lane r of a group row r of it; the groups add their
+// contributions to the shared targets one after another (fixed order: deterministic). The
+// unit's targets go to part[u1 m2 + u2][side][role][x3][r] (role 0: i2's row, 1: j2's).
+template <int LM>  // L <= LM
+__device__ void slice_partials_t4(const PcgArgs& A, const PcgShared& sh, const double* p,
+                                  double* accw, unsigned ticket_base) {
+  const int R1 = sh.R[0], R2 = sh.R[1], R3 = sh.R[2], L = sh.R[3];
+  const int m2 = sh.m[1], m3 = sh.m[2];
+  const int dp = sh.dprime, RL = R3 * L;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = 32 / L, g = lane / L, r = lane - g * L;
+  const bool lane_on = g < G;
+  double* src = accw + (size_t)w * 8 * RL;  // [side source: 0 = p_b, 1 = p_a][role][x3][c]
+  double* acc = src + 4 * RL;               // [side][role][x3][r]
+  const unsigned nunits = (unsigned)sh.m1 * m2;
+  unsigned* tickets = A.counter + 8;
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(tickets, 1u) - ticket_base;
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= nunits) break;
+    const int u1 = (int)(t / m2), u2 = (int)(t - (unsigned)u1 * m2);
+    int a, b, i2, j2;
+    pair_of(u1, R1, a, b);
+    pair_of(u2, R2, i2, j2);
+    const bool two_sides = a != b, two2 = i2 != j2;
+    // sources: side 0 reads p_b, side 1 reads p_a; role 0 = row i2, role 1 = row j2
+    // (all of a lane's loads issued before any store: one L2 latency, not one per element)
+    {
+      constexpr int kPer = 16;  // 4 R3 L <= 512
+      double tv[kPer];
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int e = lane + 32 * k;
+        tv[k] = 0.0;
+        if (e < 4 * RL) {
+          const int sd = e / (2 * RL), rem = e - sd * 2 * RL, role = rem / RL, xr = rem - role * RL;
+          const int vec = sd == 0 ? b : a, row = role == 0 ? i2 : j2;
+          if (sd == 0 || two_sides) tv[k] = __ldcg(p + (size_t)vec * dp + row * RL + xr);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int e = lane + 32 * k;
+        if (e < 4 * RL) {
+          src[e] = tv[k];
+          acc[e] = 0.0;
+        }
+      }
+    }
+    __syncwarp();
+    const double* Bu = A.B + ((size_t)u1 * sh.mmid + (size_t)u2 * m3) * L * L;
+    for (int u30 = 0; u30 < m3; u30 += G) {
+      const int u3 = u30 + g;
+      const bool on = lane_on && u3 < m3;
+      double brow[LM];
+      int i3 = 0, j3 = 0;
+      if (on) {
+        pair_of(u3, R3, i3, j3);
+        const double* br = Bu + ((size_t)u3 * L + r) * L;
+#pragma unroll
+        for (int c = 0; c < LM; ++c)
+          if (c < L) brow[c] = __ldcs(br + c);
+      }
+      // up to 8 contributions of this lane: [side][orientation 2][orientation 3]
+      double v[2][2][2];
+#pragma unroll
+      for (int sd = 0; sd < 2; ++sd)
+#pragma unroll
+        for (int o2 = 0; o2 < 2; ++o2)
+#pragma unroll
+          for (int o3 = 0; o3 < 2; ++o3) {
+            double sacc = 0.0;
+            if (on && (sd == 0 || two_sides) && (o2 == 0 || two2) && (o3 == 0 || i3 != j3)) {
+              const int yrole = o2 == 0 ? 1 : 0;  // x2 = i2 reads row j2 and vice versa
+              const int y3 = o3 == 0 ? j3 : i3;
+              const double* sv = src + (sd * 2 + yrole) * RL + y3 * L;
+#pragma unroll
+              for (int c = 0; c < LM; ++c)
+                if (c < L) sacc = fma(brow[c], sv[c], sacc);
+            }
+            v[sd][o2][o3] = sacc;
+          }
+      for (int gg = 0; gg < G; ++gg) {
+        if (on && g == gg) {
+#pragma unroll
+          for (int sd = 0; sd < 2; ++sd)
+#pragma unroll
+            for (int o2 = 0; o2 < 2; ++o2)
+#pragma unroll
+              for (int o3 = 0; o3 < 2; ++o3)
+                if ((sd == 0 || two_sides) && (o2 == 0 || two2) && (o3 == 0 || i3 != j3)) {
+                  const int x3 = o3 == 0 ? i3 : j3;
+                  acc[(sd * 2 + o2) * RL + x3 * L + r] += v[sd][o2][o3];
+                }
+        }
+        __syncwarp();
+      }
+    }
+    double* out = A.part + (size_t)t * 4 * RL;
+    const int ne = two_sides ? 4 * RL : 2 * RL;
+    for (int e = lane; e < ne; e += 32) out[e] = acc[e];
+    __syncwarp();
+  }
+}
+
+// (B) own rows for the order-4 tiled path: q[i1, x2, x3, r] = sum over j1 (slice v(i1, j1),
+// side i1 > j1) and y (unit u2 = v(x2, y), role x2 > y) of part[u1 m2 + u2][side][role][x3 r].
+// 16 lanes per row (lane k takes j1 = k, k + 16, ...), a fixed shuffle tree over them.
+__device__ void reduce_rows_t4(const PcgArgs& A, const PcgShared& sh, const double* p, int row0,
+                               int nrows, double* qout) {
+  const int R1 = sh.R[0], R2 = sh.R[1], RL = sh.R[2] * sh.R[3], m2 = sh.m[1];
+  const int dp = sh.dprime;
+  const int k = threadIdx.x & 15;
+  for (int base = row0; base < row0 + nrows; base += kThreads / 16) {
+    const int e = base + (threadIdx.x >> 4);
+    const bool ok = e < row0 + nrows;
+    double s = 0.0;
+    if (ok) {
+      const int i1 = e / dp, rest = e - i1 * dp;
+      const int x2 = rest / RL, xr = rest - x2 * RL;
+      for (int j1 = k; j1 < R1; j1 += 16) {
+        const int u1 = upper_pair(min(i1, j1), max(i1, j1), R1);
+        const int side = i1 <= j1 ? 0 : 1;
+        const double* pb = A.part + (size_t)u1 * m2 * 4 * RL + (size_t)(side * 2) * RL + xr;
+        for (int y = 0; y < R2; ++y) {
+          const int u2 = upper_pair(min(x2, y), max(x2, y), R2);
+          const int role = x2 <= y ? 0 : 1;
+          s += __ldcg(pb + (size_t)u2 * 4 * RL + (size_t)role * RL);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (ok && k == 0) {
+      const int c = __ldg(A.aug_count + e);
+      if (c > 0) s = fma((double)c * A.aug_term, p[e], s);
+      qout[e] = s;
+    }
+  }
+}
+
 // (A) fast path, order 3 with R_3 == 16: every unordered middle pair (i2 <= j2)
 // of the slice is read ONCE (one 2 KB block) and applied to the four (side,
 // orientation) targets -- q_a(i2) += B p_b(j2), q_a(j2) += B p_b(i2), q_b(i2) +=
@@ -1176,14 +1325,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_dv(const PcgArgs A, const P
   unsigned mv = 0;
   const unsigned tick_per = (unsigned)sh.m1 * sh.ntile + gridDim.x * kWarps;
   // q (own rows, A.q) = G src, src published in global memory
+  const bool t4 = sh.t4 != 0;
+  const unsigned tick4 = (unsigned)sh.m1 * sh.m[1] + gridDim.x * kWarps;
+  const bool mprof = A.prof && blockIdx.x == 0 && threadIdx.x == 0;
   auto matvec = [&](const double* src) {
+    const unsigned long long m0 = mprof ? gtimer() : 0;
     if (t32) slice_partials_t32(A, sh, src, acc32, (mv++) * tick_per);
+    else if (t4) slice_partials_t4<RM>(A, sh, src, acc32, (mv++) * tick4);
     else slice_partials<RM>(A, sh, src);
     __syncthreads();
+    const unsigned long long m1 = mprof ? gtimer() : 0;
     gsync();
+    const unsigned long long m2 = mprof ? gtimer() : 0;
     if (t32) reduce_rows_t32(A, sh, src, row0, row1 - row0, A.q);
+    else if (t4) reduce_rows_t4(A, sh, src, row0, row1 - row0, A.q);
     else reduce_rows<false>(A, sh, src, row0, row1 - row0, A.q);
     __syncthreads();
+    if (mprof) {  // CTA 0: its own partials, the wait for the slowest CTA, its row sums
+      A.prof[1] += m1 - m0;
+      A.prof[2] += m2 - m1;
+      A.prof[3] += gtimer() - m2;
+    }
   };
 
   int missing = 0;
@@ -1907,6 +2069,14 @@ static bool pcg_big(int d, int order, const int* ranks) {
 }
 static size_t pcg_smem_big(int order, int rm) { return 8 * (2 * (size_t)order * rm * rm + 32); }
 
+// tiled order-4 matvec (slice_partials_t4, k_pcg_dv only): the warp's sources and targets
+// (8 R3 R4 doubles) in shared memory, R4 <= 32
+static bool pcg_t4(int d, int order, const int* ranks) {
+  static const bool off = std::getenv("RTB_NO_PCG_T4") != nullptr;  // experiments
+  return !off && order == 4 && ranks[3] <= 16 && ranks[2] * ranks[3] <= 128 &&
+         (size_t)kWarps * 8 * ranks[2] * ranks[3] * 8 <= 160 * 1024 && pcg_big(d, order, ranks);
+}
+
 // tiled rank-32 matvec (slice_partials_t32): large d, order 3, R_3 = 32, R_2 a multiple of 8
 static bool pcg_t32(int d, int order, const int* ranks) {
   static const bool off = std::getenv("RTB_NO_PCG_T32") != nullptr;  // experiments
@@ -1933,7 +2103,9 @@ static size_t pcg_base_bytes(int d, int order, const int* ranks) {
   const size_t m1 = (size_t)ranks[0] * (ranks[0] + 1) / 2;
   const size_t dp = (size_t)d / ranks[0];
   const size_t part = pcg_t32(d, order, ranks) ? m1 * t32_ntile(ranks) * 1024
-                                               : m1 * pcg_jc(d, order, ranks) * 2 * dp;
+                    : pcg_t4(d, order, ranks)
+                        ? m1 * ((size_t)ranks[1] * (ranks[1] + 1) / 2) * 4 * ranks[2] * ranks[3]
+                        : m1 * pcg_jc(d, order, ranks) * 2 * dp;
   return ((size_t)d + part + 1024) * 8 + 256 +
          ((size_t)d + 32) * 8;  // + the split form's published source and selector
 }
@@ -1976,9 +2148,12 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   const int rm = rank_bucket(spec.order, spec.ranks);
   const bool big = pcg_big(d, spec.order, spec.ranks);
   sh.t32 = pcg_t32(d, spec.order, spec.ranks) ? 1 : 0;
+  static const bool no_dv_t4 = std::getenv("RTB_NO_PCG_DV") != nullptr;
+  sh.t4 = (!no_dv_t4 && pcg_t4(d, spec.order, spec.ranks)) ? 1 : 0;
   sh.ng = spec.ranks[1] / 8;
   sh.ntile = t32_ntile(spec.ranks);
-  const size_t smem = big ? pcg_smem_big(spec.order, rm) + (sh.t32 ? (size_t)kWarps * 1024 * 8 : 0)
+  const size_t smem = big ? pcg_smem_big(spec.order, rm) + (sh.t32 ? (size_t)kWarps * 1024 * 8 : 0) +
+                                (sh.t4 ? (size_t)kWarps * 8 * spec.ranks[2] * spec.ranks[3] * 8 : 0)
                           : pcg_smem(d, spec.order, spec.ranks, rm);
 
   char* w = static_cast<char*>(work);
@@ -1988,7 +2163,9 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   a.x = x;
   a.q = reinterpret_cast<double*>(w);
   a.part = a.q + d;
-  a.rpart = a.part + (sh.t32 ? (size_t)sh.m1 * sh.ntile * 1024 : (size_t)sh.m1 * sh.jc * 2 * sh.dprime);
+  a.rpart = a.part + (sh.t32 ? (size_t)sh.m1 * sh.ntile * 1024
+                      : sh.t4 ? (size_t)sh.m1 * sh.m[1] * 4 * spec.ranks[2] * spec.ranks[3]
+                              : (size_t)sh.m1 * sh.jc * 2 * sh.dprime);
   a.counter = reinterpret_cast<unsigned*>(a.rpart + 1024);
   a.vglobal = nullptr;
   if (big) {  // after the counter block (pcg_work_bytes(d, order, ranks))
@@ -2036,6 +2213,7 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   if (!big && all16) count_variant("k_pcg<16,16>");
   if (sh.t32) count_variant("k_pcg_t32");
   if (big && !no_dv) count_variant("k_pcg_dv");
+  if (sh.t4) count_variant("k_pcg_t4");
   if (prof_on) {
     unsigned long long h[16];
     int stat[2];

@@ -123,3 +123,58 @@ def test_update_factor_f3_r32_mid5(oracle, rt):
         bar = factor_bar(kappa, shape, mode - 1)
         print(f"R=32 F{mode}: kappa {kappa:.3e} err {err:.3e} bar {bar:.3e}")
         assert err < bar, (mode, kappa, err)
+
+
+def _torch_normal_eq_nway(shape, ranks, factors, x, lam, idx, w):
+    """N-way version of test_gpu_c2_parity._torch_normal_eq (independent FP64 Gram/RHS)."""
+    import torch
+    dev = "cuda"
+    d = int(np.prod(ranks))
+    total = int(np.prod(shape))
+    A = [torch.from_numpy(np.ascontiguousarray(f)).to(dev) for f in factors]
+    xi = torch.from_numpy(x.ravel()).to(dev)
+    ti = torch.from_numpy(idx.astype(np.int64)).to(dev)
+    tw = torch.from_numpy(w).to(dev)
+    data = ti < total
+    i, wd = ti[data], tw[data]
+    G = torch.zeros((d, d), dtype=torch.float64, device=dev)
+    rhs = torch.zeros(d, dtype=torch.float64, device=dev)
+    for c in range(0, i.numel(), 4096):
+        ic, wc = i[c:c + 4096], wd[c:c + 4096]
+        rem, js = ic.clone(), []
+        for I in reversed(shape):
+            js.append(rem % I)
+            rem = rem // I
+        js = js[::-1]
+        r = A[0][js[0]]
+        for n in range(1, len(shape)):
+            r = (r[:, :, None] * A[n][js[n]][:, None, :]).reshape(r.shape[0], -1)
+        r = r * wc[:, None]
+        G += r.T @ r
+        rhs += r.T @ (wc * xi[ic])
+    j = ti[~data] - total
+    G.view(-1).index_put_((j * d + j,), lam * tw[~data] ** 2, accumulate=True)
+    return G, rhs
+
+
+def test_pcg_order4_large_d_vs_cusolver(oracle, rt):
+    """The order-4 large-d core solve (C3's: k_pcg_dv with the tiled order-4 matvec,
+    d = 10^4) vs a cuSOLVER Cholesky solve of an independently built Gram of the same draws."""
+    torch = pytest.importorskip("torch")
+    shape, ranks, s, lam = (24, 22, 20, 18), (10, 10, 10, 10), 200000, 0.1
+    x = planted(shape, ranks, seed=54)
+    core, factors = model(oracle, shape, ranks, "normal", 23)
+    dv, t4 = rt.variant_count("k_pcg_dv"), rt.variant_count("k_pcg_t4")
+    gcore, gidx, gw = rt.update_core_sketched(rt.Tensor.from_numpy(x),
+                                              rt.Model(core, factors, lam), s, 8)
+    assert rt.variant_count("k_pcg_dv") == dv + 1 and rt.variant_count("k_pcg_t4") == t4 + 1
+    G, b = _torch_normal_eq_nway(shape, ranks, factors, x, lam, gidx, gw)
+    L = torch.linalg.cholesky(G)
+    xs = torch.cholesky_solve(b[:, None], L)[:, 0].cpu().numpy()
+    kappa = _kappa_spd(torch, G, L)
+    del G, L
+    torch.cuda.empty_cache()
+    err = frel(gcore, xs)
+    print(f"order 4 d=10^4 core: kappa {kappa:.3e} err {err:.3e} err/(kappa eps) "
+          f"{err / (kappa * EPS):.3g}")
+    assert err < 64 * kappa * EPS, (kappa, err)

@@ -27,3 +27,21 @@ for i in range(3):
     r = rt.als_run(xt, bench.C1_RANKS, opts)
     t1 = time.perf_counter()
     print("als_run only ms %.3f  device sweep_seconds %.4f" % (1e3 * (t1 - t0), r.sweep_seconds))
+
+# host-side phases of a 10-sweep job through the session API
+for i in range(3):
+    t0 = time.perf_counter()
+    s = rt.Session(xt, bench.C1_RANKS, opts)
+    t1 = time.perf_counter()
+    s.sweeps(1)
+    t2 = time.perf_counter()
+    s.sweeps(1)
+    t3 = time.perf_counter()
+    s.sweeps(8)
+    t4 = time.perf_counter()
+    r = s.result()
+    t5 = time.perf_counter()
+    s.free()
+    t6 = time.perf_counter()
+    print("session ms: create %.3f sweep1 %.3f sweep2(capture) %.3f sweeps3-10 %.3f result %.3f "
+          "free %.3f" % tuple(1e3 * v for v in (t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4, t6 - t5)))

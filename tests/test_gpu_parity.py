@@ -417,19 +417,20 @@ def test_graph_sweeps_match_eager(rt, shape, ranks, lam, s, fs):
     device counters, the core verdict read behind the loss pass); the histories and the
     model must be bitwise those of the kernel-by-kernel path."""
     x = planted(shape, ranks, seed=51)
-    kw = dict(lam=lam, sketched_core=1, max_iterations=5, tolerance=0.0,
+    # (runs shorter than 16 sweeps stay eager: capturing costs about one sweep)
+    kw = dict(lam=lam, sketched_core=1, max_iterations=16, tolerance=0.0,
               sample_count_override=s, record_history=1, seed=8)
     xt = rt.Tensor.from_numpy(x)
     rg = rt.als_run(xt, ranks, rt.options(**kw), factor_samples=fs)
     re = rt.als_run(xt, ranks, rt.options(**kw), factor_samples=fs, graph=False)
-    assert rg.graph_sweeps == 4 and re.graph_sweeps == 0
+    assert rg.graph_sweeps == 15 and re.graph_sweeps == 0
     assert rg.history() == re.history()
     mg, me = rg.model(), re.model()
     assert np.array_equal(mg.core, me.core)
     assert all(np.array_equal(a, b) for a, b in zip(mg.factors, me.factors))
     assert rg.sketch_info() == re.sketch_info()
     tg, te = rg.timings(), re.timings()
-    assert [t[0] for t in tg] == [t[0] for t in te] and all(t[2] == 5 for t in tg)
+    assert [t[0] for t in tg] == [t[0] for t in te] and all(t[2] == 16 for t in tg)
 
 
 def test_session_sweeps_beyond_max_iterations(rt):

@@ -1703,7 +1703,17 @@ class Engine {
       // Kronecker-preconditioned CG on the blocked Gram (k_pcg.cu), verified by its
       // true residual; the Cholesky path (solve_fallback) takes over on failure
       Scope sc(prof_, "pcg");
-      if (!split && !blocks_ready_) {
+      // multi-GPU with a large d: the solve is distributed by mode-1 slices (pcg_solve_dist),
+      // each shard expands and multiplies its own slices' blocks only
+      const bool dist = sharded() && pcg_dist_ok((int)d_, N_, rk);
+      int u_lo = 0, u_hi = 0;
+      if (dist) {
+        const int m1 = rk[0] * (rk[0] + 1) / 2;
+        pcg_dist_slices(m1, (int)opt_.shard_rank, (int)opt_.shard_count, &u_lo, &u_hi);
+        const long long per = gram_block_elems(gs) / m1;
+        blocks_.ensure((size_t)std::max<long long>(1, per * (u_hi - u_lo)) * 8, st_);
+        gram_expand_blocks_range(gs, gram_work_.p, blocks_.as<double>(), u_lo, u_hi, st_);
+      } else if (!split && !blocks_ready_) {
         blocks_.ensure((size_t)gram_block_elems(gs) * 8, st_);
         gram_expand_blocks(gs, gram_work_.p, blocks_.as<double>(), st_);
       }
@@ -1720,7 +1730,11 @@ class Engine {
       // first sketch of a run starts cold from the random init): a device flag
       ps.warm_dev = warm_dev_.as<int>();
       pcg_work_.ensure(pcg_work_bytes((int)d_, N_, rk), st_);
-      if (split)
+      if (dist)
+        pcg_solve_dist(ps, blocks_.as<double>(), (int)opt_.shard_rank, (int)opt_.shard_count,
+                       rhs_.as<double>(), core_.as<double>(), pcg_work_.p, pcg_status_.as<int>(),
+                       st_, [this](double* p, size_t n) { allreduce(p, n); });
+      else if (split)
         pcg_solve_compact(ps, gram_compact(gs, gram_work_.p, nullptr), rhs_.as<double>(),
                           core_.as<double>(), pcg_work_.p, pcg_status_.as<int>(), st_);
       else

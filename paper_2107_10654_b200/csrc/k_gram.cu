@@ -1726,12 +1726,13 @@ __global__ void k_vech_expand(GramSpec spec, VechSpec v, const double* __restric
 // prod_{n<N} m_n blocks of R_N x R_N (C2: 136^2 x 16^2 doubles = 38 MB, vs
 // 134 MB for the full Gram); consumed by the CG matvec (k_pcg.cu).
 __global__ void k_vech_blocks(GramSpec spec, VechSpec v, const double* __restrict__ S,
-                              double* __restrict__ B) {
-  // one CTA per block (u_1..u_{N-1}); threads over the R_N x R_N entries
+                              double* __restrict__ B, unsigned boff = 0) {
+  // one CTA per block (u_1..u_{N-1}); threads over the R_N x R_N entries; boff: the first
+  // block of a slice range (the output starts there)
   const int N = v.N, RL = v.R[N - 1];
   int un[kMaxOrder];
   {
-    unsigned t = blockIdx.x;
+    unsigned t = blockIdx.x + boff;
     for (int n = N - 2; n >= 0; --n) {
       un[n] = (int)(t % (unsigned)v.m[n]);
       t /= (unsigned)v.m[n];
@@ -2120,6 +2121,18 @@ void gram_expand_full(const GramSpec& spec, void* work, double* gram, cudaStream
   const VechSpec v = make_vech(spec);
   GramLayout l = layout(spec, work);
   k_vech_expand<<<kNumSMs * 8, 256, 0, st>>>(spec, v, l.S, l.aug_count, gram_aug_term(spec), gram);
+  RTB_LAUNCH_CHECK();
+}
+
+void gram_expand_blocks_range(const GramSpec& spec, void* work, double* blocks, int u_lo, int u_hi,
+                              cudaStream_t st) {
+  const VechSpec v = make_vech(spec);
+  GramLayout l = layout(spec, work);
+  const long long mmid = gram_block_elems(spec) / ((long long)v.R[v.N - 1] * v.R[v.N - 1]) / v.m[0];
+  const long long nblk = (long long)(u_hi - u_lo) * mmid;
+  if (nblk <= 0) return;
+  if (nblk > 0x7fffffffLL) throw Error(4, "gram_expand_blocks: too many blocks");
+  k_vech_blocks<<<(unsigned)nblk, 256, 0, st>>>(spec, v, l.S, blocks, (unsigned)(u_lo * mmid));
   RTB_LAUNCH_CHECK();
 }
 

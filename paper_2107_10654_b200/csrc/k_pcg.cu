@@ -31,6 +31,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 
@@ -55,6 +56,10 @@ struct PcgShared {
   int ng;         // t32: groups of 8 middle indices (R_2 / 8)
   int ntile;      // t32: tiles per slice, ng (ng + 1) / 2 (off-diagonal first)
   int t4;         // tiled order-4 matvec (slice_partials_t4)
+  // distributed solve (k_pcg_dist_*): this rank holds and multiplies the slices u1 in
+  // [u_lo, u_hi) only (blocks stored from u_lo on); aug_on: it also adds the augmented diagonal
+  // (one rank). Single GPU: [0, m1), aug_on = 1.
+  int u_lo, u_hi, aug_on;
 };
 
 struct PcgArgs {
@@ -386,12 +391,12 @@ template <int RM>
 __device__ void slice_partials(const PcgArgs& A, const PcgShared& sh, const double* p) {
   const int last = sh.last, mid = sh.mid, dp = sh.dprime;
   const int nout = 2 * dp;
-  for (int unit = blockIdx.x; unit < sh.m1 * sh.jc; unit += gridDim.x) {
+  for (int unit = sh.u_lo * sh.jc + blockIdx.x; unit < sh.u_hi * sh.jc; unit += gridDim.x) {
     const int u1 = unit / sh.jc, ch = unit - u1 * sh.jc;
     const int jm0 = (int)((long long)mid * ch / sh.jc), jm1 = (int)((long long)mid * (ch + 1) / sh.jc);
     int a, b;
     pair_of(u1, sh.R[0], a, b);
-    const double* Bs = A.B + (size_t)u1 * sh.mmid * last * last;
+    const double* Bs = A.B + (size_t)(u1 - sh.u_lo) * sh.mmid * last * last;
     for (int o = threadIdx.x; o < nout; o += kThreads) {
       const int r = o % last;
       const int t = o / last;
@@ -482,7 +487,8 @@ __device__ void slice_partials_t32(const PcgArgs& A, const PcgShared& sh, const 
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rq = lane >> 2, c = lane & 3;
   const int nod = ng * (ng - 1) / 2;
-  const unsigned nunits = (unsigned)sh.m1 * sh.ntile;
+  const int nsl = sh.u_hi - sh.u_lo;  // this rank's slices
+  const unsigned nunits = (unsigned)nsl * sh.ntile;
   double* acc = accw + (size_t)w * 1024;
   unsigned* tickets = A.counter + 8;
   for (;;) {
@@ -491,7 +497,7 @@ __device__ void slice_partials_t32(const PcgArgs& A, const PcgShared& sh, const 
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= nunits) break;
     int u1, tile, I, J;
-    if (t < (unsigned)sh.m1 * nod) {
+    if (t < (unsigned)nsl * nod) {
       u1 = (int)(t / nod);
       tile = (int)(t % nod);
       I = 0;
@@ -502,15 +508,17 @@ __device__ void slice_partials_t32(const PcgArgs& A, const PcgShared& sh, const 
       }
       J = I + 1 + rem;
     } else {
-      const unsigned v = t - (unsigned)sh.m1 * nod;
+      const unsigned v = t - (unsigned)nsl * nod;
       u1 = (int)(v / ng);
       I = J = (int)(v % ng);
       tile = nod + I;
     }
+    const int ul = u1;  // slice within this rank's blocks
+    u1 += sh.u_lo;
     int a, b;
     pair_of(u1, sh.R[0], a, b);
     const bool two_sides = a != b;
-    const double* Bs = A.B + (size_t)u1 * sh.mmid * 1024;
+    const double* Bs = A.B + (size_t)ul * sh.mmid * 1024;
     const double* pa = p + (size_t)a * dp;
     const double* pb = p + (size_t)b * dp;
     for (int e = lane; e < 1024; e += 32) acc[e] = 0.0;
@@ -624,6 +632,7 @@ __device__ void reduce_rows_t32(const PcgArgs& A, const PcgShared& sh, const dou
 #pragma unroll 4
     for (int j1 = 0; j1 < R1; ++j1) {
       const int u1 = upper_pair(min(i1, j1), max(i1, j1), R1);
+      if (u1 < sh.u_lo || u1 >= sh.u_hi) continue;  // another rank's slice
       const int side = i1 <= j1 ? 0 : 1;
       const double* base = A.part + (size_t)u1 * sh.ntile * 1024 + (size_t)(side * 2) * 256 + k * 32 + r;
       double v[8];
@@ -637,7 +646,7 @@ __device__ void reduce_rows_t32(const PcgArgs& A, const PcgShared& sh, const dou
       for (int q = 0; q < 8; ++q) s += v[q];
     }
     const int cnt = __ldg(A.aug_count + e);
-    if (cnt > 0) s = fma((double)cnt * A.aug_term, p[e], s);
+    if (cnt > 0 && sh.aug_on) s = fma((double)cnt * A.aug_term, p[e], s);
     qout[e] = s;
   }
 }
@@ -662,14 +671,15 @@ __device__ void slice_partials_t4(const PcgArgs& A, const PcgShared& sh, const d
   const bool lane_on = g < G;
   double* src = accw + (size_t)w * 8 * RL;  // [side source: 0 = p_b, 1 = p_a][role][x3][c]
   double* acc = src + 4 * RL;               // [side][role][x3][r]
-  const unsigned nunits = (unsigned)sh.m1 * m2;
+  const unsigned nunits = (unsigned)(sh.u_hi - sh.u_lo) * m2;
   unsigned* tickets = A.counter + 8;
   for (;;) {
     unsigned t = 0;
     if (lane == 0) t = atomicAdd(tickets, 1u) - ticket_base;
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= nunits) break;
-    const int u1 = (int)(t / m2), u2 = (int)(t - (unsigned)u1 * m2);
+    const int ul = (int)(t / m2), u2 = (int)(t - (unsigned)ul * m2);
+    const int u1 = ul + sh.u_lo;
     int a, b, i2, j2;
     pair_of(u1, R1, a, b);
     pair_of(u2, R2, i2, j2);
@@ -699,7 +709,7 @@ __device__ void slice_partials_t4(const PcgArgs& A, const PcgShared& sh, const d
       }
     }
     __syncwarp();
-    const double* Bu = A.B + ((size_t)u1 * sh.mmid + (size_t)u2 * m3) * L * L;
+    const double* Bu = A.B + ((size_t)ul * sh.mmid + (size_t)u2 * m3) * L * L;
     for (int u30 = 0; u30 < m3; u30 += G) {
       const int u3 = u30 + g;
       const bool on = lane_on && u3 < m3;
@@ -747,7 +757,7 @@ __device__ void slice_partials_t4(const PcgArgs& A, const PcgShared& sh, const d
         __syncwarp();
       }
     }
-    double* out = A.part + (size_t)t * 4 * RL;
+    double* out = A.part + ((size_t)u1 * m2 + u2) * 4 * RL;
     const int ne = two_sides ? 4 * RL : 2 * RL;
     for (int e = lane; e < ne; e += 32) out[e] = acc[e];
     __syncwarp();
@@ -771,6 +781,7 @@ __device__ void reduce_rows_t4(const PcgArgs& A, const PcgShared& sh, const doub
       const int x2 = rest / RL, xr = rest - x2 * RL;
       for (int j1 = k; j1 < R1; j1 += 16) {
         const int u1 = upper_pair(min(i1, j1), max(i1, j1), R1);
+        if (u1 < sh.u_lo || u1 >= sh.u_hi) continue;  // another rank's slice
         const int side = i1 <= j1 ? 0 : 1;
         const double* pb = A.part + (size_t)u1 * m2 * 4 * RL + (size_t)(side * 2) * RL + xr;
         for (int y = 0; y < R2; ++y) {
@@ -784,7 +795,7 @@ __device__ void reduce_rows_t4(const PcgArgs& A, const PcgShared& sh, const doub
     for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (ok && k == 0) {
       const int c = __ldg(A.aug_count + e);
-      if (c > 0) s = fma((double)c * A.aug_term, p[e], s);
+      if (c > 0 && sh.aug_on) s = fma((double)c * A.aug_term, p[e], s);
       qout[e] = s;
     }
   }
@@ -905,12 +916,13 @@ __device__ void reduce_rows(const PcgArgs& A, const PcgShared& sh, const double*
     double s = 0.0;
     for (int j1 = 0; j1 < R1; ++j1) {
       const int u1 = upper_pair(min(i1, j1), max(i1, j1), R1);
+      if (u1 < sh.u_lo || u1 >= sh.u_hi) continue;  // another rank's slice
       const int side = i1 <= j1 ? 0 : 1;
       for (int ch = 0; ch < jc; ++ch)
         s += __ldcg(A.part + (((size_t)u1 * jc + ch) * 2 + side) * dp + rest);
     }
     const int c = __ldg(A.aug_count + e);
-    if (c > 0) s = fma((double)c * A.aug_term, p[e], s);
+    if (c > 0 && sh.aug_on) s = fma((double)c * A.aug_term, p[e], s);
     qout[e] = s;
   }
 }
@@ -1010,7 +1022,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(const PcgArgs A, const PcgS
   const bool t32 = big && sh.t32;
   double* acc32 = red + 32;
   unsigned mv = 0;  // matvecs so far: ticket base of the next one
-  const unsigned tick_per = (unsigned)sh.m1 * sh.ntile + gridDim.x * kWarps;
+  const unsigned tick_per = (unsigned)(sh.u_hi - sh.u_lo) * sh.ntile + gridDim.x * kWarps;
   auto mv_partials = [&]() {
     if (t32) slice_partials_t32(A, sh, p, acc32, (mv++) * tick_per);
     else if (fast3) slice_partials_n3(A, sh, p, accw);
@@ -1323,7 +1335,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_dv(const PcgArgs A, const P
     return v;
   };
   unsigned mv = 0;
-  const unsigned tick_per = (unsigned)sh.m1 * sh.ntile + gridDim.x * kWarps;
+  const unsigned tick_per = (unsigned)(sh.u_hi - sh.u_lo) * sh.ntile + gridDim.x * kWarps;
   // q (own rows, A.q) = G src, src published in global memory
   const bool t4 = sh.t4 != 0;
   const unsigned tick4 = (unsigned)sh.m1 * sh.m[1] + gridDim.x * kWarps;
@@ -1531,6 +1543,347 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_dv(const PcgArgs A, const P
     if (!st && !(res <= A.check_tol * A.check_tol * scale * scale)) st = 1;
     A.status[0] = st;
     A.status[1] = it;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Distributed solve across GPUs (k_pcg_dist_*): the large-d PCG of k_pcg_dv with the matvec
+// split over ranks by mode-1 slices. Rank r holds the blocks of slices u1 in [u_lo, u_hi) only
+// and computes q_r = sum over its slices (+ the augmented diagonal on one rank); the caller's
+// all-reduce sums q over ranks between launches; every rank then runs the identical CG vector
+// step on its own GPU (distributed over its CTAs as in k_pcg_dv), so x, r and p stay identical
+// everywhere without exchanging them. Three cooperative launches per iteration
+// (matvec | all-reduce | step), the CG state in device memory; the host checks the done flag
+// every few iterations. The single-GPU case is k_pcg_dv (one launch).
+struct DistState {
+  double rho, bb, xx, gn;
+  int mode, it, fail, pad;  // mode: 0 warm-start matvec, 1 CG, 2 final check, 3 done
+};
+enum { kDWarm = 0, kDCg = 1, kDCheck = 2, kDDone = 3 };
+
+struct DvCtx {  // the k_pcg_dv helpers for the split kernels
+  double *gx, *gr, *gp, *ga, *gb, *gdinv, *gpart0;
+};
+
+template <int RM>
+__device__ void dist_setup(const PcgArgs& A, const PcgShared& sh, double* Ps, double* VTs,
+                           bool eig) {
+  for (int n = 0; n < sh.order; ++n) {
+    const int R = sh.R[n];
+    const double* Pg = eig ? A.evecs + (size_t)n * A.linv_stride : A.pinv + (size_t)n * A.linv_stride;
+    for (int e = threadIdx.x; e < RM * RM; e += kThreads) {
+      const int i = e / RM, j = e - i * RM;
+      const bool in = i < R && j < R;
+      Ps[n * RM * RM + e] = in ? Pg[i * R + j] : 0.0;
+      if (eig) VTs[n * RM * RM + e] = in ? Pg[j * R + i] : 0.0;
+    }
+  }
+  __syncthreads();
+}
+
+// block sums of per-CTA partials across the grid (the k_pcg_dv scheme; parity per launch)
+struct GridSum {
+  double* gpart0;
+  double* red;
+  double* bcast;
+  unsigned* counter;
+  unsigned target = 0;
+  int nsum = 0;
+  __device__ void sync() {
+    target += gridDim.x;
+    grid_barrier(counter, target);
+  }
+  __device__ void sum2(double& v0, double& v1) {
+    block_sum2_det(v0, v1, red);
+    double* gpart = gpart0 + (size_t)(nsum & 1) * gridDim.x * 2;
+    ++nsum;
+    if (threadIdx.x == 0) {
+      gpart[blockIdx.x * 2] = v0;
+      gpart[blockIdx.x * 2 + 1] = v1;
+    }
+    sync();
+    if (threadIdx.x < 32) {
+      double t0 = 0.0, t1 = 0.0;
+      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) {
+        t0 += __ldcg(gpart + c * 2);
+        t1 += __ldcg(gpart + c * 2 + 1);
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+        t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+      }
+      if (threadIdx.x == 0) {
+        bcast[0] = t0;
+        bcast[1] = t1;
+      }
+    }
+    __syncthreads();
+    v0 = bcast[0];
+    v1 = bcast[1];
+    __syncthreads();
+  }
+  __device__ double sum(double v) {
+    double z = 0.0;
+    sum2(v, z);
+    return v;
+  }
+};
+
+template <int RM>
+__device__ double* dist_precond(const PcgShared& sh, GridSum& gs, const double* src, const DvCtx& c,
+                                const double* Ps, const double* VTs, bool eig) {
+  const double* cur = src;
+  double* dst = c.ga;
+  for (int n = 0; n < sh.order; ++n) {
+    mode_product_dv(cur, dst, Ps + n * RM * RM, RM, sh.R[n], sh.J[n], sh.d);
+    gs.sync();
+    cur = dst;
+    dst = (dst == c.ga) ? c.gb : c.ga;
+  }
+  if (eig) {
+    double* t = const_cast<double*>(cur);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < sh.d; e += gridDim.x * blockDim.x)
+      t[e] *= c.gdinv[e];
+    gs.sync();
+    for (int n = 0; n < sh.order; ++n) {
+      mode_product_dv(cur, dst, VTs + n * RM * RM, RM, sh.R[n], sh.J[n], sh.d);
+      gs.sync();
+      cur = dst;
+      dst = (dst == c.ga) ? c.gb : c.ga;
+    }
+  }
+  return const_cast<double*>(cur);
+}
+
+__device__ DvCtx dv_ctx(const PcgArgs& A, int d) {
+  const int dv = (d + 1) & ~1;
+  DvCtx c;
+  c.gx = A.vglobal;
+  c.gr = c.gx + dv;
+  c.gp = c.gr + dv;
+  c.ga = c.gp + dv;
+  c.gb = c.ga + dv;
+  c.gdinv = c.gb + dv;
+  c.gpart0 = c.gdinv + dv;
+  return c;
+}
+
+// z = M^-1 r, rho = r.z, p = z; the caller's barrier after the sum publishes p
+template <int RM>
+__device__ void dist_start_cg(const PcgArgs& A, const PcgShared& sh, GridSum& gs, const DvCtx& c,
+                              const double* Ps, const double* VTs, bool eig, int row0, int row1,
+                              DistState* S) {
+  double* z = dist_precond<RM>(sh, gs, c.gr, c, Ps, VTs, eig);
+  double rho = 0.0;
+  for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+    c.gp[e] = z[e];
+    rho = fma(c.gr[e], z[e], rho);
+  }
+  rho = gs.sum(rho);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    S->rho = rho;
+    S->mode = kDCg;
+  }
+}
+
+template <int RM>
+__global__ void __launch_bounds__(kThreads, 1) k_pcg_dist_init(const PcgArgs A, const PcgShared shc) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double bcast[2];
+  const PcgShared& sh = shc;
+  const int d = sh.d;
+  double* Ps = sm;
+  double* VTs = Ps + sh.order * RM * RM;
+  double* red = VTs + sh.order * RM * RM;
+  const DvCtx c = dv_ctx(A, d);
+  GridSum gs{c.gpart0, red, bcast, A.counter};
+  DistState* S = reinterpret_cast<DistState*>(A.rpart);
+  const int row0 = min(d, (int)blockIdx.x * sh.rows_per_cta), row1 = min(d, row0 + sh.rows_per_cta);
+  int missing = 0;
+  for (int e = threadIdx.x; e < d; e += kThreads) missing |= __ldg(A.aug_count + e) == 0;
+  if (threadIdx.x < sh.order) missing |= __ldg(A.linv_ok + threadIdx.x) == 0;
+  if (__syncthreads_or(missing) || !(A.lambda > 0.0) || !(A.lambda * A.prep[1] <= kMaxLambdaOverMu)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      A.status[0] = 3;
+      A.status[1] = 0;
+      S->mode = kDDone;
+    }
+    return;
+  }
+  const bool eig = A.prep[2] != 0.0;
+  dist_setup<RM>(A, sh, Ps, VTs, eig);
+  if (eig) {
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+      double m = 1.0;
+      int rem = e;
+      for (int n = sh.order - 1; n >= 0; --n) {
+        const int j = rem % sh.R[n];
+        rem /= sh.R[n];
+        m *= fmax(A.evals[(size_t)n * A.linv_stride + j], 0.0);
+      }
+      c.gdinv[e] = 1.0 / (m + A.lambda);
+    }
+  }
+  double bb = 0.0;
+  for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+    const double be = A.b[e];
+    c.gr[e] = be;
+    c.gx[e] = 0.0;
+    bb = fma(be, be, bb);
+  }
+  bb = gs.sum(bb);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    S->bb = bb;
+    S->gn = A.prep[0];
+    S->it = 0;
+    S->fail = 0;
+  }
+  if (bb == 0.0) {
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) A.x[e] = 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      A.status[0] = 0;
+      A.status[1] = 0;
+      S->mode = kDDone;
+    }
+    return;
+  }
+  if (A.warm_dev ? *A.warm_dev : A.warm) {
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) c.gx[e] = A.x[e];
+    if (blockIdx.x == 0 && threadIdx.x == 0) S->mode = kDWarm;
+    return;
+  }
+  dist_start_cg<RM>(A, sh, gs, c, Ps, VTs, eig, row0, row1, S);
+}
+
+// this rank's share of q = G src (src: x for the warm start and the final check, else p)
+template <int RM>
+__global__ void __launch_bounds__(kThreads, 1) k_pcg_dist_mv(const PcgArgs A, const PcgShared shc) {
+  extern __shared__ __align__(16) double sm[];
+  const PcgShared& sh = shc;
+  const DistState* S = reinterpret_cast<const DistState*>(A.rpart);
+  const int mode = S->mode;
+  if (mode == kDDone) return;
+  const int d = sh.d;
+  double* red = sm + 2 * sh.order * RM * RM;
+  double* acc32 = red + 32;
+  const DvCtx c = dv_ctx(A, d);
+  const double* src = mode == kDCg ? c.gp : c.gx;
+  const int row0 = min(d, (int)blockIdx.x * sh.rows_per_cta), row1 = min(d, row0 + sh.rows_per_cta);
+  const unsigned nsl = (unsigned)(sh.u_hi - sh.u_lo);
+  if (sh.t32) slice_partials_t32(A, sh, src, acc32, 0u);
+  else if (sh.t4) slice_partials_t4<RM>(A, sh, src, acc32, 0u);
+  else slice_partials<RM>(A, sh, src);
+  (void)nsl;
+  __syncthreads();
+  grid_barrier(A.counter, gridDim.x);
+  if (sh.t32) reduce_rows_t32(A, sh, src, row0, row1 - row0, A.q);
+  else if (sh.t4) reduce_rows_t4(A, sh, src, row0, row1 - row0, A.q);
+  else reduce_rows<false>(A, sh, src, row0, row1 - row0, A.q);
+}
+
+// one CG state transition on the summed q (identical on every rank)
+template <int RM>
+__global__ void __launch_bounds__(kThreads, 1) k_pcg_dist_step(const PcgArgs A, const PcgShared shc) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double bcast[2];
+  const PcgShared& sh = shc;
+  DistState* S = reinterpret_cast<DistState*>(A.rpart);
+  const int mode = S->mode;
+  if (mode == kDDone) return;
+  const int d = sh.d;
+  double* Ps = sm;
+  double* VTs = Ps + sh.order * RM * RM;
+  double* red = VTs + sh.order * RM * RM;
+  const DvCtx c = dv_ctx(A, d);
+  GridSum gs{c.gpart0, red, bcast, A.counter};
+  const int row0 = min(d, (int)blockIdx.x * sh.rows_per_cta), row1 = min(d, row0 + sh.rows_per_cta);
+  const bool eig = A.prep[2] != 0.0;
+  const double bb = S->bb, gnorm = S->gn;
+  __syncthreads();  // every thread has read the state before CTA 0 may rewrite it
+  gs.sync();
+  if (mode == kDWarm) {
+    double r0 = 0.0;
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+      const double re = A.b[e] - A.q[e];
+      r0 = fma(re, re, r0);
+    }
+    r0 = gs.sum(r0);
+    const bool keep = r0 < bb && isfinite(r0);
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+      if (keep) c.gr[e] = A.b[e] - A.q[e];
+      else c.gx[e] = 0.0;
+    }
+    __syncthreads();
+    gs.sync();
+    dist_setup<RM>(A, sh, Ps, VTs, eig);
+    dist_start_cg<RM>(A, sh, gs, c, Ps, VTs, eig, row0, row1, S);
+    return;
+  }
+  if (mode == kDCheck) {
+    double res = 0.0;
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+      const double t = A.b[e] - A.q[e];
+      res = fma(t, t, res);
+      A.x[e] = c.gx[e];
+    }
+    res = gs.sum(res);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      int st = S->fail;
+      const double scale = gnorm * sqrt(S->xx) + sqrt(bb);
+      if (!st && !(res <= A.check_tol * A.check_tol * scale * scale)) st = 1;
+      A.status[0] = st;
+      A.status[1] = S->it;
+      S->mode = kDDone;
+    }
+    return;
+  }
+  // kDCg
+  const double rho = S->rho;
+  int it = S->it;
+  double pq = 0.0;
+  for (int e = row0 + threadIdx.x; e < row1; e += kThreads) pq = fma(c.gp[e], A.q[e], pq);
+  pq = gs.sum(pq);
+  auto to_check = [&](int fail) {
+    double xx = 0.0;
+    for (int e = row0 + threadIdx.x; e < row1; e += kThreads) xx = fma(c.gx[e], c.gx[e], xx);
+    xx = gs.sum(xx);  // its barrier also completes x as the next matvec source
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      S->xx = xx;
+      S->fail = fail;
+      S->it = it;
+      S->mode = kDCheck;
+    }
+  };
+  if (!(pq > 0.0) || !isfinite(pq)) {
+    to_check(2);
+    return;
+  }
+  const double alpha = rho / pq;
+  double rr = 0.0, xq = 0.0;
+  for (int e = row0 + threadIdx.x; e < row1; e += kThreads) {
+    const double re = fma(-alpha, A.q[e], c.gr[e]);
+    c.gr[e] = re;
+    rr = fma(re, re, rr);
+    const double xe = fma(alpha, c.gp[e], c.gx[e]);
+    c.gx[e] = xe;
+    xq = fma(xe, xe, xq);
+  }
+  gs.sum2(rr, xq);
+  ++it;
+  if (rr <= A.tol * A.tol * fmax(bb, gnorm * gnorm * xq) || it >= A.max_iter) {
+    to_check(0);
+    return;
+  }
+  dist_setup<RM>(A, sh, Ps, VTs, eig);
+  double* z = dist_precond<RM>(sh, gs, c.gr, c, Ps, VTs, eig);
+  double rho2 = 0.0;
+  for (int e = row0 + threadIdx.x; e < row1; e += kThreads) rho2 = fma(c.gr[e], z[e], rho2);
+  rho2 = gs.sum(rho2);
+  const double beta = rho2 / rho;
+  for (int e = row0 + threadIdx.x; e < row1; e += kThreads) c.gp[e] = fma(beta, c.gp[e], z[e]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    S->rho = rho2;
+    S->it = it;
   }
 }
 
@@ -2121,12 +2474,14 @@ bool pcg_supported(int d, int order, const int* ranks) {
   return d >= 1 && d <= (1 << 20) && order >= 2 && order <= kMaxOrder && rm > 0;
 }
 
-void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, double* x, void* work,
-               int* status_dev, cudaStream_t st) {
+// shape, workspace carving and launch arguments shared by pcg_solve and pcg_solve_dist
+static void pcg_setup(const PcgSpec& spec, const double* blocks, const double* b, double* x,
+                      void* work, int* status_dev, PcgShared& sh, PcgArgs& a, size_t& smem,
+                      bool& big, int& rm) {
   const int d = spec.d;
   const int grid = num_sms();
   if (!pcg_supported(d, spec.order, spec.ranks)) throw Error(4, "pcg_solve: unsupported shape");
-  PcgShared sh{};
+  sh = PcgShared{};
   sh.d = d;
   sh.order = spec.order;
   sh.rows_per_cta = (d + grid - 1) / grid;
@@ -2144,20 +2499,23 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   sh.mmid = 1;
   for (int n = 1; n < spec.order - 1; ++n) sh.mmid *= sh.m[n];
   sh.m1 = sh.m[0];
+  sh.u_lo = 0;
+  sh.u_hi = sh.m1;
+  sh.aug_on = 1;
   sh.jc = pcg_jc(d, spec.order, spec.ranks);
-  const int rm = rank_bucket(spec.order, spec.ranks);
-  const bool big = pcg_big(d, spec.order, spec.ranks);
+  rm = rank_bucket(spec.order, spec.ranks);
+  big = pcg_big(d, spec.order, spec.ranks);
   sh.t32 = pcg_t32(d, spec.order, spec.ranks) ? 1 : 0;
   static const bool no_dv_t4 = std::getenv("RTB_NO_PCG_DV") != nullptr;
   sh.t4 = (!no_dv_t4 && pcg_t4(d, spec.order, spec.ranks)) ? 1 : 0;
   sh.ng = spec.ranks[1] / 8;
   sh.ntile = t32_ntile(spec.ranks);
-  const size_t smem = big ? pcg_smem_big(spec.order, rm) + (sh.t32 ? (size_t)kWarps * 1024 * 8 : 0) +
+  smem = big ? pcg_smem_big(spec.order, rm) + (sh.t32 ? (size_t)kWarps * 1024 * 8 : 0) +
                                 (sh.t4 ? (size_t)kWarps * 8 * spec.ranks[2] * spec.ranks[3] * 8 : 0)
                           : pcg_smem(d, spec.order, spec.ranks, rm);
 
   char* w = static_cast<char*>(work);
-  PcgArgs a{};
+  a = PcgArgs{};
   a.B = blocks;
   a.b = b;
   a.x = x;
@@ -2188,6 +2546,18 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
   a.check_tol = spec.check_tol;
   a.warm = spec.warm;
   a.warm_dev = spec.warm_dev;
+}
+
+void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, double* x, void* work,
+               int* status_dev, cudaStream_t st) {
+  const int d = spec.d;
+  const int grid = num_sms();
+  PcgShared sh;
+  PcgArgs a;
+  size_t smem = 0;
+  bool big = false;
+  int rm = 0;
+  pcg_setup(spec, blocks, b, x, work, status_dev, sh, a, smem, big, rm);
   static unsigned long long* prof_buf = nullptr;
   static const bool prof_on = std::getenv("RTB_PCG_PROF") != nullptr;
   if (prof_on) {
@@ -2229,6 +2599,75 @@ void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, doubl
 }
 
 
+bool pcg_dist_ok(int d, int order, const int* ranks) {
+  static const bool off = std::getenv("RTB_NO_PCG_DIST") != nullptr;  // experiments
+  return !off && pcg_supported(d, order, ranks) && pcg_big(d, order, ranks);
+}
+
+void pcg_dist_slices(int m1, int rank, int count, int* u_lo, int* u_hi) {
+  *u_lo = (int)((long long)m1 * rank / count);
+  *u_hi = (int)((long long)m1 * (rank + 1) / count);
+}
+
+void pcg_solve_dist(const PcgSpec& spec, const double* blocks_local, int rank, int count,
+                    const double* b, double* x, void* work, int* status_dev, cudaStream_t st,
+                    const std::function<void(double*, size_t)>& allreduce) {
+  if (!pcg_dist_ok(spec.d, spec.order, spec.ranks)) throw Error(4, "pcg_solve_dist: unsupported shape");
+  const int d = spec.d;
+  const int grid = num_sms();
+  PcgShared sh;
+  PcgArgs a;
+  size_t smem = 0;
+  bool big = false;
+  int rm = 0;
+  pcg_setup(spec, blocks_local, b, x, work, status_dev, sh, a, smem, big, rm);
+  pcg_dist_slices(sh.m1, rank, count, &sh.u_lo, &sh.u_hi);
+  sh.aug_on = rank == 0 ? 1 : 0;
+  void *fi, *fm, *fs;
+  if (rm == 8) {
+    fi = (void*)k_pcg_dist_init<8>; fm = (void*)k_pcg_dist_mv<8>; fs = (void*)k_pcg_dist_step<8>;
+  } else if (rm == 16) {
+    fi = (void*)k_pcg_dist_init<16>; fm = (void*)k_pcg_dist_mv<16>; fs = (void*)k_pcg_dist_step<16>;
+  } else {
+    fi = (void*)k_pcg_dist_init<32>; fm = (void*)k_pcg_dist_mv<32>; fs = (void*)k_pcg_dist_step<32>;
+  }
+  for (void* f : {fi, fm, fs}) set_max_smem_impl(f, 220 * 1024);
+  void* args[] = {(void*)&a, (void*)&sh};
+  auto launch = [&](void* f) {
+    RTB_CUDA(cudaMemsetAsync(a.counter, 0, 64, st));  // barrier counter and matvec tickets
+    RTB_CUDA(cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kThreads), args, smem, st));
+    RTB_LAUNCH_CHECK();
+  };
+  launch(fi);
+  // the CG state is on the device: the host polls its mode every few iterations
+  static int* done_host = nullptr;
+  if (!done_host) RTB_CUDA(cudaMallocHost(&done_host, 4));
+  const int* mode_dev = &reinterpret_cast<const DistState*>(a.rpart)->mode;
+  const int max_steps = spec.max_iter + 3;  // warm start + iterations + final check
+  for (int k = 0; k < max_steps; ++k) {
+    launch(fm);
+    allreduce(a.q, (size_t)d);
+    launch(fs);
+    if (k >= 6 && (k % 3 == 0 || k == max_steps - 1)) {
+      RTB_CUDA(cudaMemcpyAsync(done_host, mode_dev, 4, cudaMemcpyDeviceToHost, st));
+      RTB_CUDA(cudaStreamSynchronize(st));
+      if (*done_host == kDDone) break;
+    }
+  }
+  count_variant("k_pcg_dist");
+  static const bool prof_on = std::getenv("RTB_PCG_PROF") != nullptr;
+  if (prof_on) {
+    int stat[2];
+    DistState S;
+    RTB_CUDA(cudaMemcpyAsync(stat, status_dev, 8, cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaMemcpyAsync(&S, a.rpart, sizeof(S), cudaMemcpyDeviceToHost, st));
+    RTB_CUDA(cudaStreamSynchronize(st));
+    std::fprintf(stderr, "[pcg_dist] rank %d/%d slices [%d,%d) d=%d status=%d iters=%d mode=%d "
+                 "bb=%.3e xx=%.3e rho=%.3e\n", rank, count, sh.u_lo, sh.u_hi, d, stat[0], stat[1],
+                 S.mode, S.bb, S.xx, S.rho);
+  }
+}
+
 static size_t split_slice_smem(int d, const int* ranks) {
   const size_t m2 = (size_t)ranks[1] * (ranks[1] + 1) / 2, dp = (size_t)d / ranks[0];
   return (m2 * 136 + 2 * dp + (size_t)kWarps * 2 * dp) * 8;
@@ -2268,6 +2707,9 @@ void pcg_solve_compact(const PcgSpec& spec, const double* S, const double* b, do
   sh.mid = sh.dprime / sh.last;
   sh.mmid = sh.m[1];
   sh.m1 = sh.m[0];
+  sh.u_lo = 0;
+  sh.u_hi = sh.m1;
+  sh.aug_on = 1;
   sh.jc = 1;
   const size_t smem = std::max(split_slice_smem(d, spec.ranks), split_vector_smem(d, spec.order));
   char* w = static_cast<char*>(work);

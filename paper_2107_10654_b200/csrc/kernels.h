@@ -1,5 +1,6 @@
 // kernels.h -- host-side launchers of the sm_100a kernels (namespace rtb).
 #pragma once
+#include <functional>
 
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -213,6 +214,9 @@ double gram_aug_term(const GramSpec& spec);
 void gram_expand_full(const GramSpec& spec, void* work, double* gram, cudaStream_t st);
 long long gram_block_elems(const GramSpec& spec);
 void gram_expand_blocks(const GramSpec& spec, void* work, double* blocks, cudaStream_t st);
+// the blocks of the mode-1 slices u1 in [u_lo, u_hi) only (a distributed solve's share)
+void gram_expand_blocks_range(const GramSpec& spec, void* work, double* blocks, int u_lo, int u_hi,
+                              cudaStream_t st);
 
 // ---- k_pcg.cu ----
 struct PcgSpec {
@@ -250,6 +254,14 @@ bool pcg_supported(int d, int order, const int* ranks);
 bool pcg_split_ok(int d, int order, const int* ranks);
 void pcg_solve_compact(const PcgSpec& spec, const double* S, const double* b, double* x,
                        void* work, int* status_dev, cudaStream_t st);
+// Distributed large-d solve (multi-GPU): rank `rank` of `count` holds the blocks of its mode-1
+// slices only (pcg_dist_slices; gram_expand_blocks_range) and the ranks' matvec shares are
+// summed by `allreduce(q, d)` between launches; every rank ends with the same x and status.
+bool pcg_dist_ok(int d, int order, const int* ranks);
+void pcg_dist_slices(int m1, int rank, int count, int* u_lo, int* u_hi);
+void pcg_solve_dist(const PcgSpec& spec, const double* blocks_local, int rank, int count,
+                    const double* b, double* x, void* work, int* status_dev, cudaStream_t st,
+                    const std::function<void(double*, size_t)>& allreduce);
 void pcg_solve(const PcgSpec& spec, const double* blocks, const double* b, double* x, void* work,
                int* status_dev, cudaStream_t st);
 

@@ -151,6 +151,33 @@ def test_sharded_factor_sketch_matches_single_process(rt, P, order):
         assert np.linalg.norm(model.core - rm.core) / np.linalg.norm(rm.core) < 1e-5
 
 
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("shape,ranks,s", [((40, 36, 34), (8, 32, 32), 400000),
+                                           ((24, 22, 20, 18), (10, 10, 10, 10), 500000)])
+def test_sharded_distributed_core_solve(rt, P, shape, ranks, s):
+    """Large d under sharding: the core solve is distributed by mode-1 slices
+    (pcg_solve_dist: each shard expands and multiplies its own slices' blocks -- the tiled
+    rank-32 matvec at d = 8192, the order-4 one at d = 10^4 -- and the matvec shares are
+    all-reduced every iteration); every shard ends with the single-process core up to the
+    regrouped sums."""
+    x = planted(shape, ranks, seed=45)
+    kw = dict(lam=1e-2, sketched_core=1, sample_count_override=s, max_iterations=2,
+              tolerance=0.0, record_history=1, seed=10)
+    before = rt.variant_count("k_pcg_dist")
+    ref = rt.als_run(rt.Tensor.from_numpy(x), ranks, rt.options(**kw))
+    outs = run_sharded(rt, x, ranks, kw, P)
+    assert rt.variant_count("k_pcg_dist") >= before + P, "sharded solve was not distributed"
+    rh, rm = ref.history(), ref.model()
+    for hist, model, info in outs:
+        assert info["solver_path"] == 2  # the CG answer was accepted
+        for (gi, gs, gl, grm), (_, _, fl, frm) in zip(hist, rh):
+            assert abs(gl - fl) / fl < 1e-8, (gi, gs, gl, fl)
+        assert np.linalg.norm(model.core - rm.core) / np.linalg.norm(rm.core) < 1e-7
+    # every shard holds the same model
+    for o in outs[1:]:
+        assert np.array_equal(o[1].core, outs[0][1].core)
+
+
 def test_sharded_rejects_bad_split(rt):
     x = planted((20, 10, 8), (2, 2, 2), seed=1)
     with pytest.raises(rt.RtuckerError):

@@ -56,6 +56,7 @@ struct PcgShared {
   int ng;         // t32: groups of 8 middle indices (R_2 / 8)
   int ntile;      // t32: tiles per slice, ng (ng + 1) / 2 (off-diagonal first)
   int t4;         // tiled order-4 matvec (slice_partials_t4)
+  int t4h;        // t4: u3 ranges per (u1, u2) unit (finer work units for the tail)
   // distributed solve (k_pcg_dist_*): this rank holds and multiplies the slices u1 in
   // [u_lo, u_hi) only (blocks stored from u_lo on); aug_on: it also adds the augmented diagonal
   // (one rank). Single GPU: [0, m1), aug_on = 1.
@@ -660,32 +661,40 @@ __device__ void reduce_rows_t32(const PcgArgs& A, const PcgShared& sh, const dou
 // takes block u3 = u3_0 + g, lane r of a group row r of it; the groups add their
 // contributions to the shared targets one after another (fixed order: deterministic). The
 // unit's targets go to part[u1 m2 + u2][side][role][x3][r] (role 0: i2's row, 1: j2's).
-template <int LM>  // L <= LM
+template <int LM>  // L <= LM <= 16
 __device__ void slice_partials_t4(const PcgArgs& A, const PcgShared& sh, const double* p,
                                   double* accw, unsigned ticket_base) {
+  // per block one m16n8k16 DMMA: C (16 x 8) = B_blk (L x L, zero-padded to 16 x 16) x S, the
+  // 8 columns of S the sources of the block's 8 (side, u2 orientation, u3 orientation)
+  // combinations; C[r][n] is combination n's contribution to its target row r. The 8 targets
+  // of one block are distinct addresses, so the warp adds them to its shared targets at once.
   const int R1 = sh.R[0], R2 = sh.R[1], R3 = sh.R[2], L = sh.R[3];
   const int m2 = sh.m[1], m3 = sh.m[2];
   const int dp = sh.dprime, RL = R3 * L;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = 32 / L, g = lane / L, r = lane - g * L;
-  const bool lane_on = g < G;
+  const int g = lane >> 2, t = lane & 3;
   double* src = accw + (size_t)w * 8 * RL;  // [side source: 0 = p_b, 1 = p_a][role][x3][c]
   double* acc = src + 4 * RL;               // [side][role][x3][r]
-  const unsigned nunits = (unsigned)(sh.u_hi - sh.u_lo) * m2;
+  const int H = sh.t4h;
+  const unsigned nunits = (unsigned)(sh.u_hi - sh.u_lo) * m2 * H;
   unsigned* tickets = A.counter + 8;
+  // B-fragment column g = combination n = g: side sd = g >> 2, o2 = (g >> 1) & 1, o3 = g & 1
+  const int n_sd = g >> 2, n_o2 = (g >> 1) & 1, n_o3 = g & 1;
+  // C columns of this lane: 2t, 2t + 1
   for (;;) {
-    unsigned t = 0;
-    if (lane == 0) t = atomicAdd(tickets, 1u) - ticket_base;
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= nunits) break;
-    const int ul = (int)(t / m2), u2 = (int)(t - (unsigned)ul * m2);
+    unsigned tk = 0;
+    if (lane == 0) tk = atomicAdd(tickets, 1u) - ticket_base;
+    tk = __shfl_sync(0xffffffffu, tk, 0);
+    if (tk >= nunits) break;
+    const int hh = (int)(tk % (unsigned)H);
+    const unsigned tu = tk / (unsigned)H;
+    const int ul = (int)(tu / m2), u2 = (int)(tu - (unsigned)ul * m2);
     const int u1 = ul + sh.u_lo;
+    const int u3lo = (int)((long long)m3 * hh / H), u3hi = (int)((long long)m3 * (hh + 1) / H);
     int a, b, i2, j2;
     pair_of(u1, R1, a, b);
     pair_of(u2, R2, i2, j2);
     const bool two_sides = a != b, two2 = i2 != j2;
-    // sources: side 0 reads p_b, side 1 reads p_a; role 0 = row i2, role 1 = row j2
-    // (all of a lane's loads issued before any store: one L2 latency, not one per element)
     {
       constexpr int kPer = 16;  // 4 R3 L <= 512
       double tv[kPer];
@@ -710,54 +719,57 @@ __device__ void slice_partials_t4(const PcgArgs& A, const PcgShared& sh, const d
     }
     __syncwarp();
     const double* Bu = A.B + ((size_t)ul * sh.mmid + (size_t)u2 * m3) * L * L;
-    for (int u30 = 0; u30 < m3; u30 += G) {
-      const int u3 = u30 + g;
-      const bool on = lane_on && u3 < m3;
-      double brow[LM];
-      int i3 = 0, j3 = 0;
-      if (on) {
-        pair_of(u3, R3, i3, j3);
-        const double* br = Bu + ((size_t)u3 * L + r) * L;
+    const bool n_side_on = n_sd == 0 || two_sides;
+    const bool n_o2_on = n_o2 == 0 || two2;
+    const int n_yrole = n_o2 == 0 ? 1 : 0;  // x2 = i2 reads row j2 and vice versa
+    constexpr int kAhead = 4;
+    for (int u30 = u3lo; u30 < u3hi; u30 += kAhead) {
+      double af[kAhead][8];
 #pragma unroll
-        for (int c = 0; c < LM; ++c)
-          if (c < L) brow[c] = __ldcs(br + c);
+      for (int k = 0; k < kAhead; ++k) {
+        const int u3 = u30 + k;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int rr = g + 8 * (v & 1), cc = t + 4 * (v >> 1);
+          af[k][v] = (u3 < u3hi && rr < L && cc < L) ? __ldcs(Bu + ((size_t)u3 * L + rr) * L + cc) : 0.0;
+        }
       }
-      // up to 8 contributions of this lane: [side][orientation 2][orientation 3]
-      double v[2][2][2];
 #pragma unroll
-      for (int sd = 0; sd < 2; ++sd)
+      for (int k = 0; k < kAhead; ++k) {
+        const int u3 = u30 + k;
+        if (u3 >= u3hi) break;
+        int i3, j3;
+        pair_of(u3, R3, i3, j3);
+        const bool two3 = i3 != j3;
+        // B fragment: column g's source at rows t + 4 v
+        double bf[4];
+        {
+          const bool on = n_side_on && n_o2_on && (n_o3 == 0 || two3);
+          const int y3 = n_o3 == 0 ? j3 : i3;
+          const double* sv = src + (n_sd * 2 + n_yrole) * RL + y3 * L;
 #pragma unroll
-        for (int o2 = 0; o2 < 2; ++o2)
-#pragma unroll
-          for (int o3 = 0; o3 < 2; ++o3) {
-            double sacc = 0.0;
-            if (on && (sd == 0 || two_sides) && (o2 == 0 || two2) && (o3 == 0 || i3 != j3)) {
-              const int yrole = o2 == 0 ? 1 : 0;  // x2 = i2 reads row j2 and vice versa
-              const int y3 = o3 == 0 ? j3 : i3;
-              const double* sv = src + (sd * 2 + yrole) * RL + y3 * L;
-#pragma unroll
-              for (int c = 0; c < LM; ++c)
-                if (c < L) sacc = fma(brow[c], sv[c], sacc);
-            }
-            v[sd][o2][o3] = sacc;
+          for (int v = 0; v < 4; ++v) {
+            const int kk = t + 4 * v;
+            bf[v] = (on && kk < L) ? sv[kk] : 0.0;
           }
-      for (int gg = 0; gg < G; ++gg) {
-        if (on && g == gg) {
+        }
+        double c[4] = {0.0, 0.0, 0.0, 0.0};
+        dmma_16x8x16(c, af[k], bf);
+        // C[r][n]: rows g, g + 8; columns 2t, 2t + 1 -> targets
 #pragma unroll
-          for (int sd = 0; sd < 2; ++sd)
-#pragma unroll
-            for (int o2 = 0; o2 < 2; ++o2)
-#pragma unroll
-              for (int o3 = 0; o3 < 2; ++o3)
-                if ((sd == 0 || two_sides) && (o2 == 0 || two2) && (o3 == 0 || i3 != j3)) {
-                  const int x3 = o3 == 0 ? i3 : j3;
-                  acc[(sd * 2 + o2) * RL + x3 * L + r] += v[sd][o2][o3];
-                }
+        for (int v = 0; v < 4; ++v) {
+          const int r = g + 8 * (v >> 1), n = 2 * t + (v & 1);
+          const int sd = n >> 2, o2 = (n >> 1) & 1, o3 = n & 1;
+          const bool on = r < L && (sd == 0 || two_sides) && (o2 == 0 || two2) && (o3 == 0 || two3);
+          if (on) {
+            const int x3 = o3 == 0 ? i3 : j3;
+            acc[(sd * 2 + o2) * RL + x3 * L + r] += c[v];
+          }
         }
         __syncwarp();
       }
     }
-    double* out = A.part + ((size_t)u1 * m2 + u2) * 4 * RL;
+    double* out = A.part + (((size_t)u1 * m2 + u2) * H + hh) * 4 * RL;
     const int ne = two_sides ? 4 * RL : 2 * RL;
     for (int e = lane; e < ne; e += 32) out[e] = acc[e];
     __syncwarp();
@@ -783,11 +795,13 @@ __device__ void reduce_rows_t4(const PcgArgs& A, const PcgShared& sh, const doub
         const int u1 = upper_pair(min(i1, j1), max(i1, j1), R1);
         if (u1 < sh.u_lo || u1 >= sh.u_hi) continue;  // another rank's slice
         const int side = i1 <= j1 ? 0 : 1;
-        const double* pb = A.part + (size_t)u1 * m2 * 4 * RL + (size_t)(side * 2) * RL + xr;
+        const int H = sh.t4h;
+        const double* pb = A.part + (size_t)u1 * m2 * H * 4 * RL + (size_t)(side * 2) * RL + xr;
         for (int y = 0; y < R2; ++y) {
           const int u2 = upper_pair(min(x2, y), max(x2, y), R2);
           const int role = x2 <= y ? 0 : 1;
-          s += __ldcg(pb + (size_t)u2 * 4 * RL + (size_t)role * RL);
+          for (int h = 0; h < H; ++h)
+            s += __ldcg(pb + ((size_t)u2 * H + h) * 4 * RL + (size_t)role * RL);
         }
       }
     }
@@ -1338,7 +1352,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_dv(const PcgArgs A, const P
   const unsigned tick_per = (unsigned)(sh.u_hi - sh.u_lo) * sh.ntile + gridDim.x * kWarps;
   // q (own rows, A.q) = G src, src published in global memory
   const bool t4 = sh.t4 != 0;
-  const unsigned tick4 = (unsigned)sh.m1 * sh.m[1] + gridDim.x * kWarps;
+  const unsigned tick4 = (unsigned)(sh.u_hi - sh.u_lo) * sh.m[1] * sh.t4h + gridDim.x * kWarps;
   const bool mprof = A.prof && blockIdx.x == 0 && threadIdx.x == 0;
   auto matvec = [&](const double* src) {
     const unsigned long long m0 = mprof ? gtimer() : 0;
@@ -2422,6 +2436,8 @@ static bool pcg_big(int d, int order, const int* ranks) {
 }
 static size_t pcg_smem_big(int order, int rm) { return 8 * (2 * (size_t)order * rm * rm + 32); }
 
+constexpr int kT4H = 1;  // u3 ranges per t4 work unit (3 at C3 balanced the tail but tripled the per-unit
+                         // source loads and partials: slower)
 // tiled order-4 matvec (slice_partials_t4, k_pcg_dv only): the warp's sources and targets
 // (8 R3 R4 doubles) in shared memory, R4 <= 32
 static bool pcg_t4(int d, int order, const int* ranks) {
@@ -2457,7 +2473,7 @@ static size_t pcg_base_bytes(int d, int order, const int* ranks) {
   const size_t dp = (size_t)d / ranks[0];
   const size_t part = pcg_t32(d, order, ranks) ? m1 * t32_ntile(ranks) * 1024
                     : pcg_t4(d, order, ranks)
-                        ? m1 * ((size_t)ranks[1] * (ranks[1] + 1) / 2) * 4 * ranks[2] * ranks[3]
+                        ? m1 * ((size_t)ranks[1] * (ranks[1] + 1) / 2) * kT4H * 4 * ranks[2] * ranks[3]
                         : m1 * pcg_jc(d, order, ranks) * 2 * dp;
   return ((size_t)d + part + 1024) * 8 + 256 +
          ((size_t)d + 32) * 8;  // + the split form's published source and selector
@@ -2508,6 +2524,7 @@ static void pcg_setup(const PcgSpec& spec, const double* blocks, const double* b
   sh.t32 = pcg_t32(d, spec.order, spec.ranks) ? 1 : 0;
   static const bool no_dv_t4 = std::getenv("RTB_NO_PCG_DV") != nullptr;
   sh.t4 = (!no_dv_t4 && pcg_t4(d, spec.order, spec.ranks)) ? 1 : 0;
+  sh.t4h = kT4H;
   sh.ng = spec.ranks[1] / 8;
   sh.ntile = t32_ntile(spec.ranks);
   smem = big ? pcg_smem_big(spec.order, rm) + (sh.t32 ? (size_t)kWarps * 1024 * 8 : 0) +
@@ -2522,7 +2539,7 @@ static void pcg_setup(const PcgSpec& spec, const double* blocks, const double* b
   a.q = reinterpret_cast<double*>(w);
   a.part = a.q + d;
   a.rpart = a.part + (sh.t32 ? (size_t)sh.m1 * sh.ntile * 1024
-                      : sh.t4 ? (size_t)sh.m1 * sh.m[1] * 4 * spec.ranks[2] * spec.ranks[3]
+                      : sh.t4 ? (size_t)sh.m1 * sh.m[1] * kT4H * 4 * spec.ranks[2] * spec.ranks[3]
                               : (size_t)sh.m1 * sh.jc * 2 * sh.dprime);
   a.counter = reinterpret_cast<unsigned*>(a.rpart + 1024);
   a.vglobal = nullptr;

@@ -661,6 +661,8 @@ __device__ void reduce_rows_t32(const PcgArgs& A, const PcgShared& sh, const dou
 // takes block u3 = u3_0 + g, lane r of a group row r of it; the groups add their
 // contributions to the shared targets one after another (fixed order: deterministic). The
 // unit's targets go to part[u1 m2 + u2][side][role][x3][r] (role 0: i2's row, 1: j2's).
+constexpr int kT4H = 1;  // u3 ranges per t4 work unit (3 at C3 balanced the tail but tripled the per-unit
+                         // source loads and partials: slower)
 template <int LM>  // L <= LM <= 16
 __device__ void slice_partials_t4(const PcgArgs& A, const PcgShared& sh, const double* p,
                                   double* accw, unsigned ticket_base) {
@@ -675,7 +677,7 @@ __device__ void slice_partials_t4(const PcgArgs& A, const PcgShared& sh, const d
   const int g = lane >> 2, t = lane & 3;
   double* src = accw + (size_t)w * 8 * RL;  // [side source: 0 = p_b, 1 = p_a][role][x3][c]
   double* acc = src + 4 * RL;               // [side][role][x3][r]
-  const int H = sh.t4h;
+  constexpr int H = kT4H;
   const unsigned nunits = (unsigned)(sh.u_hi - sh.u_lo) * m2 * H;
   unsigned* tickets = A.counter + 8;
   // B-fragment column g = combination n = g: side sd = g >> 2, o2 = (g >> 1) & 1, o3 = g & 1
@@ -795,7 +797,7 @@ __device__ void reduce_rows_t4(const PcgArgs& A, const PcgShared& sh, const doub
         const int u1 = upper_pair(min(i1, j1), max(i1, j1), R1);
         if (u1 < sh.u_lo || u1 >= sh.u_hi) continue;  // another rank's slice
         const int side = i1 <= j1 ? 0 : 1;
-        const int H = sh.t4h;
+        constexpr int H = kT4H;
         const double* pb = A.part + (size_t)u1 * m2 * H * 4 * RL + (size_t)(side * 2) * RL + xr;
         for (int y = 0; y < R2; ++y) {
           const int u2 = upper_pair(min(x2, y), max(x2, y), R2);
@@ -2436,8 +2438,6 @@ static bool pcg_big(int d, int order, const int* ranks) {
 }
 static size_t pcg_smem_big(int order, int rm) { return 8 * (2 * (size_t)order * rm * rm + 32); }
 
-constexpr int kT4H = 1;  // u3 ranges per t4 work unit (3 at C3 balanced the tail but tripled the per-unit
-                         // source loads and partials: slower)
 // tiled order-4 matvec (slice_partials_t4, k_pcg_dv only): the warp's sources and targets
 // (8 R3 R4 doubles) in shared memory, R4 <= 32
 static bool pcg_t4(int d, int order, const int* ranks) {

@@ -134,6 +134,27 @@ struct GramLayout {
 // for m_n <= 144; above that (R_n > 16, k_vech_bucket6) m_n rounded up to whole 144-wide tiles
 int tab_width(int m) { return m <= 144 ? 160 : (m + 143) / 144 * 144; }
 
+constexpr int kC3Ldt = 160, kC3Raw = 144;
+constexpr int kC3Rows = 136;  // S rows per CTA (17 consumer warps x 8)
+// Table geometry: m_1 <= 136 (C2): width 160, raw row at 144 (one staged window holds both).
+// Larger m_1 (C5: 528): the Gram CTAs take row blocks of 136, each staging the 160-wide window
+// at 136 rb; the raw row sits after all of them, at raw = 136 nrb + 24, in its own window.
+struct C3Geom {
+  int nrb, tw, raw;
+};
+C3Geom c3_geom(int m1) {
+  C3Geom gm;
+  gm.nrb = (m1 + kC3Rows - 1) / kC3Rows;
+  if (gm.nrb <= 1) {
+    gm.nrb = 1;
+    gm.tw = kC3Ldt;
+    gm.raw = kC3Raw;
+  } else {
+    gm.raw = gm.nrb * kC3Rows + 24;
+    gm.tw = gm.raw + kC3Ldt;
+  }
+  return gm;
+}
 int key_bits(int I1) {
   int b = 1;
   while ((1 << b) <= I1) ++b;
@@ -179,7 +200,7 @@ size_t carve(const GramSpec& spec, F&& take) {
   t((size_t)(spec.order >= 3 ? spec.rows[2] : 1) * tab_width(spec.order >= 3 ? v.m[2] : 1) * 8);  // vt3
   t((size_t)I1 * 4);                           // border
   t(16);                                       // bcounter
-  t((size_t)I1 * 160 * 8);                     // vt1 (k_vech_table1)
+  t((size_t)I1 * c3_geom(v.m[0]).tw * 8);      // vt1 (k_vech_table1)
   return total;
 }
 
@@ -1534,23 +1555,23 @@ __global__ void __launch_bounds__(kBWarps * 32, 1) k_vech_contract2(GramSpec spe
 // Mode-1 table of every compacted bucket's i_1 (rows b < nbuckets, ld kC3Ldt): vech(a_1 a_1^T)
 // in columns [0, m_1) (zero to 144), the raw row a_1 in [144, 144 + R_1) (zero after) -- the A
 // operands of k_vech_contract3's Gram and rhs tiles, built once per core update.
-constexpr int kC3Ldt = 160, kC3Raw = 144;
 __global__ void k_vech_table1(const double* __restrict__ A, int R, const int* __restrict__ bi1,
-                              const int* __restrict__ nbuckets, double* __restrict__ out) {
+                              const int* __restrict__ nbuckets, double* __restrict__ out, int tw,
+                              int raw) {
   const int b = blockIdx.x;
   if (b >= *nbuckets) return;
   const double* a = A + (size_t)__ldg(bi1 + b) * R;
   const int m = R * (R + 1) / 2;
-  for (int u = threadIdx.x; u < kC3Ldt; u += blockDim.x) {
+  for (int u = threadIdx.x; u < tw; u += blockDim.x) {
     double val = 0.0;
     if (u < m) {
       int p, q;
       pair_of(u, R, p, q);
       val = __ldg(a + p) * __ldg(a + q);
-    } else if (u >= kC3Raw && u < kC3Raw + R) {
-      val = __ldg(a + u - kC3Raw);
+    } else if (u >= raw && u < raw + R) {
+      val = __ldg(a + u - raw);
     }
-    out[(size_t)b * kC3Ldt + u] = val;
+    out[(size_t)b * tw + u] = val;
   }
 }
 
@@ -1571,19 +1592,25 @@ size_t vech_contract3_smem() { return (size_t)kC3St * kC3K * (kC3Ldh + kC3Ldv) *
 __global__ void __launch_bounds__(kC3Threads, 1) k_vech_contract3(
     VechSpec v, const double* __restrict__ H, const double* __restrict__ V1,
     const int* __restrict__ nbuckets, double* __restrict__ S, const double* __restrict__ h,
-    int dprime, double* __restrict__ rhs, double* __restrict__ blocks) {
+    int dprime, double* __restrict__ rhs, double* __restrict__ blocks, C3Geom gm) {
   extern __shared__ __align__(16) double smc3[];
   double* hs = smc3;                          // [St][K][Ldh]
   double* vs = hs + kC3St * kC3K * kC3Ldh;    // [St][K][Ldv]
   __shared__ __align__(8) unsigned long long full[kC3St], empty[kC3St];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gram_ctas = (int)((v.Hsz + kC3N - 1) / kC3N);
+  const int gram_ctas = (int)((v.Hsz + kC3N - 1) / kC3N) * gm.nrb;
   const bool is_rhs = (int)blockIdx.x >= gram_ctas;
-  const int rows = is_rhs ? v.R[0] : v.m[0], MT = (rows + 7) / 8;
-  const int acol = is_rhs ? kC3Raw : 0;
+  // Gram CTA: column tile ct, row block rb (consecutive CTAs share the column tile of H)
+  const int ct = is_rhs ? (int)blockIdx.x - gram_ctas : (int)blockIdx.x / gm.nrb;
+  const int rb = is_rhs ? 0 : (int)blockIdx.x - ct * gm.nrb;
+  const int row0 = rb * kC3Rows;
+  const int rows = is_rhs ? v.R[0] : min(kC3Rows, v.m[0] - row0), MT = (rows + 7) / 8;
+  // staged window of the table row, and the A columns within it
+  const int woff = is_rhs ? (gm.nrb == 1 ? 0 : gm.raw) : row0;
+  const int acol = is_rhs ? (gm.nrb == 1 ? kC3Raw : 0) : 0;
   const long long ld = is_rhs ? dprime : v.Hsz;
   const double* B = is_rhs ? h : H;
-  const long long n0 = (long long)(is_rhs ? (int)blockIdx.x - gram_ctas : (int)blockIdx.x) * kC3N;
+  const long long n0 = (long long)ct * kC3N;
   const int ncols = (int)(ld - n0 < kC3N ? ld - n0 : kC3N);
   const int nb = *nbuckets;
   const int nch = (nb + kC3K - 1) / kC3K;
@@ -1616,7 +1643,7 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_vech_contract3(
       __syncwarp();
       if (ok) {
         bulk_g2s(hrow, B + (size_t)k * ld + n0, hbytes, &full[sb]);
-        bulk_g2s(vrow, V1 + (size_t)k * kC3Ldt, kC3Ldt * 8u, &full[sb]);
+        bulk_g2s(vrow, V1 + (size_t)k * gm.tw + woff, kC3Ldt * 8u, &full[sb]);
       }
     }
     return;
@@ -1666,7 +1693,7 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_vech_contract3(
   const int nth = MT * 32;
   for (int i = tid; i < rows * ncols; i += nth) {
     const int r = i / ncols, c = i - r * ncols;
-    S[(size_t)r * v.Hsz + n0 + c] = T[r * kC3Ldh + c];
+    S[(size_t)(row0 + r) * v.Hsz + n0 + c] = T[r * kC3Ldh + c];
   }
   if (!blocks) return;
   // column c of the tile is U = n0 + c = (u_2, vech(p, q)): entries (p, q) and (q, p) of block
@@ -1688,7 +1715,7 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_vech_contract3(
     const int r = i / kC3N, c = i % kC3N;
     if (c >= ncols) continue;
     const double val = T[r * kC3Ldh + c];
-    double* bb = blocks + (size_t)r * v.m[1] * RR + cmap[0][c];
+    double* bb = blocks + (size_t)(row0 + r) * v.m[1] * RR + cmap[0][c];
     bb[cmap[1][c]] = val;
     bb[cmap[2][c]] = val;
   }
@@ -2074,20 +2101,26 @@ bool sketch_normal_eq(const GramSpec& spec, const double* x, const unsigned long
   const int I1 = spec.rows[0];
   static const bool no_c3 = std::getenv("RTB_NO_CONTRACT3") != nullptr;
   bool rhs_done = false, blocks_done = false;
-  if (!no_c3 && v.m[0] <= 8 * kC3Mma && (v.Hsz & 1) == 0 && v.Hsz >= 16 * kC3N) {
-    k_vech_table1<<<I1, 160, 0, st>>>(spec.factors[0], v.R[0], l.bi1, l.nbuckets, l.vt1);
+  static const bool no_c3big = std::getenv("RTB_NO_CONTRACT3_BIG") != nullptr;  // experiments
+  if (!no_c3 && (v.m[0] <= 8 * kC3Mma || (!no_c3big && v.R[0] <= 32)) && (v.Hsz & 1) == 0 &&
+      v.Hsz >= 16 * kC3N) {
+    const C3Geom gm = c3_geom(v.m[0]);
+    k_vech_table1<<<I1, 256, 0, st>>>(spec.factors[0], v.R[0], l.bi1, l.nbuckets, l.vt1, gm.tw,
+                                      gm.raw);
     RTB_LAUNCH_CHECK();
     const size_t smc = vech_contract3_smem();
     set_max_smem(k_vech_contract3, (int)smc);
-    // rhs tiles in the same launch when a_1 fits the table's raw-row columns
+    // rhs tiles in the same launch when a_1 fits the table's raw-row window
     static const bool no_rhs = std::getenv("RTB_C3_NORHS") != nullptr;  // experiments
     static const bool no_blk = std::getenv("RTB_C3_NOBLK") != nullptr;
-    const bool fuse_rhs = !no_rhs && v.R[0] <= kC3Ldt - kC3Raw && (spec.dprime & 1) == 0;
-    const unsigned gram_ctas = (unsigned)((v.Hsz + kC3N - 1) / kC3N);
+    const int rawcap = gm.nrb == 1 ? kC3Ldt - kC3Raw : kC3Rows;
+    const bool fuse_rhs = !no_rhs && v.R[0] <= rawcap && (spec.dprime & 1) == 0;
+    const unsigned gram_ctas = (unsigned)((v.Hsz + kC3N - 1) / kC3N) * gm.nrb;
     const unsigned rhs_ctas = fuse_rhs ? (unsigned)ceil_div(spec.dprime, kC3N) : 0u;
     double* bl = (blocks && v.N == 3 && !no_blk) ? blocks : nullptr;
     k_vech_contract3<<<gram_ctas + rhs_ctas, kC3Threads, smc, st>>>(
-        v, l.H, l.vt1, l.nbuckets, l.S, l.h, spec.dprime, fuse_rhs ? rhs : nullptr, bl);
+        v, l.H, l.vt1, l.nbuckets, l.S, l.h, spec.dprime, fuse_rhs ? rhs : nullptr, bl, gm);
+    if (gm.nrb > 1) count_variant("k_vech_contract3_rows");
     count_variant("k_vech_contract3");
     rhs_done = fuse_rhs;
     blocks_done = bl != nullptr;

@@ -178,3 +178,22 @@ def test_pcg_order4_large_d_vs_cusolver(oracle, rt):
     print(f"order 4 d=10^4 core: kappa {kappa:.3e} err {err:.3e} err/(kappa eps) "
           f"{err / (kappa * EPS):.3g}")
     assert err < 64 * kappa * EPS, (kappa, err)
+
+
+@pytest.mark.parametrize("shape,ranks", [((40, 24, 24), (20, 12, 12)), ((36, 40, 36), (24, 20, 16))])
+def test_normal_equations_large_r1_contraction(oracle, rt, shape, ranks):
+    """Rung 3 with m_1 above one CTA's 136 rows (k_vech_contract3 in row blocks, as C5's
+    m_1 = 528 runs it) vs the oracle's row-by-row stream."""
+    x = planted(shape, ranks, seed=55)
+    lam, s = 1e-2, 3000
+    core, factors = model(oracle, shape, ranks, "uniform", 29)
+    idx, w = _oracle_draws(oracle, shape, ranks, factors, 91, s)
+    before = rt.variant_count("k_vech_contract3_rows")
+    gg, grhs = rt.kron_normal_eq(shape, ranks, factors, x, lam, idx, w)
+    assert rt.variant_count("k_vech_contract3_rows") == before + 1
+    og, orhs = oracle.kron_normal_eq(shape, ranks, factors, x, lam, idx, w)
+    dg = np.sqrt(np.outer(np.diag(og), np.diag(og)))
+    eg = float(np.max(np.abs(gg - og) / dg))
+    er = float(np.linalg.norm(grhs - orhs) / np.linalg.norm(orhs))
+    print(f"{ranks} rung 3 (row-blocked contraction): Gram {eg:.3e}, rhs {er:.3e}")
+    assert eg < 1e-12 and er < 1e-12

@@ -26,6 +26,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace rtb {
 
 namespace {
@@ -356,6 +358,10 @@ void draw_decode(const DrawSpec& spec, DrawWork work, cudaStream_t st) {
   Layout l = layout(spec, work.base);
   const StreamCfg c = stream_cfg(spec);
   RTB_CUDA(cudaMemsetAsync(l.overflow, 0, sizeof(int), st));
+  // test hook: take the exact serial walk (the path a next_below rejection triggers, which
+  // real seeds reach with probability ~ (2^64 mod d) / 2^64 per augmented draw)
+  static const bool force_serial = std::getenv("RTB_DRAW_FORCE_SERIAL") != nullptr;
+  if (force_serial) RTB_CUDA(cudaMemsetAsync(l.overflow, 1, 1, st));
   const long long n1 = l.nsub * L;
   k_draw_submaps<<<(unsigned)ceil_div<long long>(n1, 256), 256, 0, st>>>(c, L, l.nsub, l.exitm,
                                                                        l.cnt, l.overflow);

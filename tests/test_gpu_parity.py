@@ -91,6 +91,43 @@ def test_draws_bit_exact_given_reference_cdfs(oracle, rt, shape, ranks, s, seed)
     assert np.array_equal(ow, gw)  # same IEEE ops -> bitwise weights
 
 
+_SERIAL_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, {root!r})
+from oracle.oracle import Oracle
+from paper_2107_10654_b200 import rtucker as rt
+o = Oracle()
+shape, ranks, s, seed = (60, 50, 40), (4, 3, 5), 30000, 13
+rng = np.random.default_rng(seed)
+fs = [rng.random((i, r)) for i, r in zip(shape, ranks)]
+scs, cdfs, sums = [], [], []
+for f in fs:
+    sc, cdf, tot, _ = o.factor_scores(f)
+    scs.append(sc); cdfs.append(cdf); sums.append(tot)
+d = int(np.prod(ranks))
+oidx, ow, _ = o.kron_draw(shape, d, scs, cdfs, sums, seed, s)
+gidx, gw = rt.kron_draw(shape, d, scs, cdfs, sums, seed, s)
+assert np.array_equal(oidx, gidx) and np.array_equal(ow, gw)
+print("serial walk bit-exact", len(gidx))
+"""
+
+
+def test_draws_serial_walk_bit_exact():
+    """The draw decoder's exact serial fallback (k_draw_scan with the overflow flag: the path a
+    next_below rejection takes) forced by RTB_DRAW_FORCE_SERIAL, in a child process (the
+    library reads the switch once): bit-exact vs the oracle like the parallel decode."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RTB_DRAW_FORCE_SERIAL="1")
+    r = subprocess.run([sys.executable, "-c", _SERIAL_SCRIPT.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "bit-exact" in r.stdout
+
+
 # ---------------------------------------------------------------- rung 3
 @pytest.mark.parametrize("shape,ranks,lam,s", [((30, 25, 20), (4, 3, 5), 1e-3, 4000),
                                                 ((20, 18, 16, 12), (3, 2, 2, 3), 0.1, 3000),

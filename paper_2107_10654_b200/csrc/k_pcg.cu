@@ -2327,6 +2327,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_split(const PcgArgs A, cons
         pq = fma(p[e], qe, pq);
       }
       pq = block_sum_det(pq, red);
+      mark(8);
       if (!(pq > 0.0) || !isfinite(pq)) {
         fail = 2;
         start_check();
@@ -2343,15 +2344,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_split(const PcgArgs A, cons
         xq = fma(xe, xe, xq);
       }
       block_sum2_det(rr, xq, red);
+      mark(9);
       ++it;
       if (rr <= tol2 * fmax(bb, gnorm * gnorm * xq) || it >= A.max_iter) {
         start_check();
         continue;
       }
       double* z = precond();
+      mark(10);
       double rho2 = 0.0;
       for (int e = tid; e < d; e += kThreads) rho2 = fma(r[e], z[e], rho2);
       rho2 = block_sum_det(rho2, red);
+      mark(11);
       const double beta = rho2 / rho;
       rho = rho2;
       for (int e = tid; e < d; e += kThreads) p[e] = fma(beta, p[e], z[e]);
@@ -2782,8 +2786,8 @@ void pcg_solve_compact(const PcgSpec& spec, const double* S, const double* b, do
     std::fprintf(stderr,
                  "[pcg_split] d=%d iters=%d status=%d ns (vector CTA 0): publish-barrier %llu "
                  "slice+barrier %llu reduce+barrier %llu cg-vector %llu other-vector %llu | "
-                 "slice CTA 0 compute %llu\n",
-                 d, stat[1], stat[0], h[0], h[1], h[2], h[5], h[3], h[4]);
+                 "slice CTA 0 compute %llu | cg: q+pq %llu update+rr %llu precond %llu rho %llu\n",
+                 d, stat[1], stat[0], h[0], h[1], h[2], h[5], h[3], h[4], h[8], h[9], h[10], h[11]);
   }
 }
 

@@ -572,18 +572,9 @@ def run_our_arm(args):
         e2e_s = float(tt.item())
     d2h = (m.core.size + sum(f.size for f in m.factors)) * 8 + 8
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            ref, xr, core, factors = reference_inputs(np)
-            sec, detail = reference_sweep_estimate(ref, np, xr, core, factors)
-            cpu = {"value": 1.0 / sec, "unit": "sweeps/s", "cores": 1, "kind": "reference",
-                   "sample": REF_SAMPLE, "host_cores": os.cpu_count(), "phases": detail}
-        except Exception as e:  # oracle/_ref missing on this box
-            cpu = {"value": None, "unit": "sweeps/s", "cores": 1, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
-
     # C1 head to head (BASELINE configs[0]): the same C-API job as the reference arm's, on
+    # (before the CPU baseline: its host-side numpy work leaves BLAS threads spinning, which
+    # slowed these wall-clocked millisecond jobs)
     # this library; plus the device-only C1 sweep rate (resident X, graph launches)
     c1 = None
     if rank == 0 and world == 1 and not args.c2_only:
@@ -608,6 +599,17 @@ def run_our_arm(args):
         c1["device_cuda_graph_sweeps"] = sc.result().graph_sweeps
         sc.free()
         xc.free()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            ref, xr, core, factors = reference_inputs(np)
+            sec, detail = reference_sweep_estimate(ref, np, xr, core, factors)
+            cpu = {"value": 1.0 / sec, "unit": "sweeps/s", "cores": 1, "kind": "reference",
+                   "sample": REF_SAMPLE, "host_cores": os.cpu_count(), "phases": detail}
+        except Exception as e:  # oracle/_ref missing on this box
+            cpu = {"value": None, "unit": "sweeps/s", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
 
     # BASELINE configs 3 and 4, measured in the same run (their own clocks samples)
     extra = {}

@@ -1628,12 +1628,11 @@ class Engine {
         RTB_LAUNCH_CHECK();
       }
       if (okm) {
-        k_leverage_chol<<<grid, 128, 0, st>>>(fs, linv_.as<double>() + so, eig_stride_, okm,
-                                             scores_.as<double>(), soff, rkd);
-        RTB_LAUNCH_CHECK();
+        leverage_chol(fs, linv_.as<double>() + so, eig_stride_, okm, scores_.as<double>(), soff,
+                      rkd, maxI, cnt, rmax_, st);
       }
-      k_score_cdf<<<1, 32 * cnt, 0, st>>>(scores_.as<double>(), soff, rows_dev_.as<int>() + n0, cnt,
-                                          cdf_.as<double>(), sums_.as<double>() + n0);
+      k_score_cdf<<<cnt, 256, 0, st>>>(scores_.as<double>(), soff, rows_dev_.as<int>() + n0, cnt,
+                                       cdf_.as<double>(), sums_.as<double>() + n0);
       RTB_LAUNCH_CHECK();
       if (n1 == N_) {
         k_any_zero_rank<<<1, 32, 0, st>>>(ranks_dev_.as<int>(), N_, zero_flag_.as<int>());
@@ -2477,18 +2476,16 @@ void factor_scores(const double* factor_host, int rows, int cols, double* scores
                                 sc.as<double>(), off.as<long long>(), rk.as<int>(), okb.as<int>(),
                                 stat.as<int>());
     RTB_LAUNCH_CHECK();
-    k_leverage_chol<<<dim3(ceil_div(rows, 128), 1), 128, 0, st>>>(
-        fs, lv.as<double>(), cols * cols, okb.as<int>(), sc.as<double>(), off.as<long long>(),
-        rk.as<int>());
-    RTB_LAUNCH_CHECK();
+    leverage_chol(fs, lv.as<double>(), cols * cols, okb.as<int>(), sc.as<double>(),
+                  off.as<long long>(), rk.as<int>(), rows, 1, cols, st);
   } else {
     DevBuf ws(hj_work_bytes(rows, cols), st);
     int r = 0;
     hj_ridge_scores(f.as<double>(), rows, cols, 0.0, sc.as<double>(), &r, ws.p, st);
     RTB_CUDA(cudaMemcpyAsync(rk.p, &r, 4, cudaMemcpyHostToDevice, st));
   }
-  k_score_cdf<<<1, 32, 0, st>>>(sc.as<double>(), off.as<long long>(), rw.as<int>(), 1,
-                                cd.as<double>(), sm.as<double>());
+  k_score_cdf<<<1, 256, 0, st>>>(sc.as<double>(), off.as<long long>(), rw.as<int>(), 1,
+                                 cd.as<double>(), sm.as<double>());
   RTB_LAUNCH_CHECK();
   int r = 0, es = 0;
   RTB_CUDA(cudaMemcpyAsync(scores, sc.p, (size_t)rows * 8, cudaMemcpyDeviceToHost, st));
@@ -2588,11 +2585,10 @@ void kron_fiber_sketch(const float* x, bool fiber_major, int I1, int I2, int I3,
   k_leverage_rows<<<lg, 128, 0, st>>>(fs, evals.as<double>(), evecs.as<double>(), stride, 0.0,
                                       scores.as<double>(), off_dev, ranks_dev, ok.as<int>());
   RTB_LAUNCH_CHECK();
-  k_leverage_chol<<<lg, 128, 0, st>>>(fs, linv.as<double>(), stride, ok.as<int>(),
-                                      scores.as<double>(), off_dev, ranks_dev);
-  RTB_LAUNCH_CHECK();
-  k_score_cdf<<<1, 64, 0, st>>>(scores.as<double>(), off_dev, rows_dev, 2, cdf.as<double>(),
-                                sums.as<double>());
+  leverage_chol(fs, linv.as<double>(), stride, ok.as<int>(), scores.as<double>(), off_dev,
+                ranks_dev, maxI, 2, rmax, st);
+  k_score_cdf<<<2, 256, 0, st>>>(scores.as<double>(), off_dev, rows_dev, 2, cdf.as<double>(),
+                                 sums.as<double>());
   RTB_LAUNCH_CHECK();
   DrawSpec ds{};
   ds.order = 2;

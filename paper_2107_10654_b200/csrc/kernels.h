@@ -27,8 +27,9 @@ void sym_eigen(const double* in, const int* ns_dev, int nmax, int stride, double
 __global__ void k_leverage_rows(const FactorSet fs, const double* evals, const double* evecs,
                                 int stride, double lambda, double* scores,
                                 const long long* score_off, int* ranks, const int* skip);
-__global__ void k_leverage_chol(const FactorSet fs, const double* linv, int stride, const int* ok,
-                                double* scores, const long long* score_off, int* ranks);
+void leverage_chol(const FactorSet& fs, const double* linv, int stride, const int* ok,
+                   double* scores, const long long* score_off, int* ranks, int max_rows,
+                   int nmodes, int rmax, cudaStream_t st);
 // batched small SPD Cholesky (n <= 32): Linv (+ optional P = M^-1), ok flags
 void spd_small(const double* in, const int* ns_dev, int stride, double tolrel, double* linv,
                double* pinv, int* ok, int nmat, cudaStream_t st, int nmax = 32);

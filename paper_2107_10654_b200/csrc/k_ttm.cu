@@ -984,6 +984,52 @@ __global__ void __launch_bounds__(256) k_ttm_expand(const double* __restrict__ Y
   }
 }
 
+// Same up-projection for R, J <= 16 on the FP64 tensor cores: per o, a warp's 16 output rows x 16
+// columns are out = A[rows, :] (16 x R) x Y[o] (R x J) as two m16n8k16 DMMAs, the A fragment
+// loaded once per warp, Y[o] staged in shared memory per CTA. The row-owner kernel below was
+// bound by shared-memory instruction throughput (two LDS per FMA pair; L1/TEX 80% at 28 us).
+__global__ void __launch_bounds__(256) k_ttm_expand_dmma(const double* __restrict__ Y, int R, int J,
+                                                        const double* __restrict__ A, int I,
+                                                        long long O, int och,
+                                                        double* __restrict__ out,
+                                                        const int* __restrict__ need) {
+  RTB_GUARD()
+  __shared__ double ys[16 * 16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int i0 = blockIdx.x * 128 + warp * 16;
+  double a[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    const int row = i0 + g + 8 * (v & 1), k = t + 4 * (v >> 1);
+    a[v] = (row < I && k < R) ? A[(long long)row * R + k] : 0.0;
+  }
+  const long long o0 = (long long)blockIdx.y * och;
+  const long long o1 = o0 + och < O ? o0 + och : O;
+  for (long long o = o0; o < o1; ++o) {
+    __syncthreads();
+    {
+      const int e = threadIdx.x;  // 256 = 16 x 16
+      const int k = e >> 4, j = e & 15;
+      ys[e] = (k < R && j < J) ? Y[(o * R + k) * J + j] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      double b[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) b[v] = ys[(t + 4 * v) * 16 + nt * 8 + g];
+      double c[4] = {0.0, 0.0, 0.0, 0.0};
+      dmma_16x8x16(c, a, b);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int row = i0 + g + 8 * (v >> 1), col = nt * 8 + 2 * t + (v & 1);
+        if (row < I && col < J) out[(o * I + row) * J + col] = c[v];
+      }
+    }
+  }
+}
+
 // Same up-projection for R, J <= 16 (P = W x_2 A_2 at C2: 512 o x 512 i x 16 j): a thread owns
 // one output row i (A[i, :] in registers) and all J outputs of it, for och consecutive o; Y[o]
 // (R x J) is staged in shared memory and read as broadcasts. The general kernel above reads two
@@ -1861,6 +1907,16 @@ bool ttm_expand(const double* Y, long long O, int R, long long J, const double* 
   int ich = 128;
   const long long minb = (long long)R * J >= 2048 ? kNumSMs / 2 : 4LL * kNumSMs;
   while (ich > 1 && O * ceil_div(I, ich) < minb) ich >>= 1;
+  static const bool no_dx = std::getenv("RTB_NO_EXPAND_DMMA") != nullptr;  // experiments
+  if (!no_dx && R <= 16 && J <= 16 && I >= 128) {
+    const long long ib = ceil_div(I, 128);
+    int och = (int)std::max<long long>(1, (O * ib) / (2LL * kNumSMs));
+    if (ceil_div<long long>(O, och) > 65535) och = (int)ceil_div<long long>(O, 65535);
+    const dim3 grid((unsigned)ib, (unsigned)ceil_div<long long>(O, och));
+    k_ttm_expand_dmma<<<grid, 256, 0, st>>>(Y, R, (int)J, A, I, O, och, out, g_need);
+    RTB_LAUNCH_CHECK();
+    return true;
+  }
   if (R <= 16 && J <= 16 && (J % 2) == 0 && I >= 256) {
     // row-owner kernel: about two CTAs per SM over (i blocks) x (o ranges)
     const long long ib = ceil_div(I, 256);

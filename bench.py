@@ -537,7 +537,7 @@ def run_our_arm(args):
             peak = mp.get("hbm_gbs", 6553.3)
             peak_src = "MEASURED_PEAKS.json hbm_gbs"
         traffic = None
-        tf = os.path.join(ROOT, "profiles", "r01_traffic.json")
+        tf = os.path.join(ROOT, "profiles", "r02_traffic.json")
         if os.path.exists(tf):
             traffic = json.load(open(tf)).get(dom)
         roofline = {"kernel": dom + (" (k_ttm_last5)" if dom == "ttm_last_loss" else " (family)"),

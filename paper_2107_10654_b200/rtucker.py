@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# RTB_LIB_PATH: developer experiments with variant builds (tools/varlib.sh); never set in use
+# RTB_LIB_PATH: developer experiments with variant builds (tools/varlib.sh builds one); never
+# set in use
 LIB_PATH = os.environ.get("RTB_LIB_PATH") or os.path.join(_HERE, "lib", "librtucker_b200.so")
 
 OK, ERR_INVALID_ARGUMENT, ERR_IO, ERR_NUMERICAL, ERR_UNKNOWN = 0, 1, 2, 3, 4

@@ -724,7 +724,7 @@ __device__ void slice_partials_t4(const PcgArgs& A, const PcgShared& sh, const d
     const bool n_side_on = n_sd == 0 || two_sides;
     const bool n_o2_on = n_o2 == 0 || two2;
     const int n_yrole = n_o2 == 0 ? 1 : 0;  // x2 = i2 reads row j2 and vice versa
-    constexpr int kAhead = 4;
+    constexpr int kAhead = 4;  // blocks in flight per warp (8: 2x slower, register spills)
     for (int u30 = u3lo; u30 < u3hi; u30 += kAhead) {
       double af[kAhead][8];
 #pragma unroll

@@ -1270,11 +1270,22 @@ class Engine {
       }
       RTB_LAUNCH_CHECK();
     }
-    std::vector<uint64_t> dims;
-    const double* Y = factor_projection(n, dims);
-    // M = Y_(n) G_(n)^T  (I_n x R_n)
-    double* M = (Y == tmp_a_.as<double>()) ? tmp_b_.as<double>() : tmp_a_.as<double>();
-    {
+    // M = Y_(n) G_(n)^T  (I_n x R_n); order 3, modes 1-2, one shard: projection and
+    // contraction from T in one launch (k_fu_proj3)
+    double* M = tmp_b_.as<double>();
+    bool fused = false;
+    if (N_ == 3 && n < 2 && !sharded()) {
+      if (!t_valid_) compute_T();
+      Scope sc(prof_, "ttm_mid");
+      const int m = 1 - n;
+      fused = fu_proj3(T_.as<double>(), (int)shape_[0], (int)shape_[1], (int)ranks_[2], factor(m),
+                       (int)ranks_[m], core_.as<double>(), (int)ranks_[0], (int)ranks_[1], n, M,
+                       st_);
+    }
+    if (!fused) {
+      std::vector<uint64_t> dims;
+      const double* Y = factor_projection(n, dims);
+      M = (Y == tmp_a_.as<double>()) ? tmp_b_.as<double>() : tmp_a_.as<double>();
       Scope sc(prof_, "contract");
       contract_except(Y, core_.as<double>(), (long long)prod(ranks_, 0, n), In, Rn,
                       (long long)prod(ranks_, n + 1), M, st_);

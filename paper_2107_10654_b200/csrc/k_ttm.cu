@@ -1897,6 +1897,106 @@ bool ttm_smallj(const double* X, long long O, int I, int J, const double* A, int
   return true;
 }
 
+// F_1 / F_2 of an order-3 exact factor update from T = X x_3 A_3^T (I_1 x I_2 x R_3, L2-resident)
+// in ONE launch: per unit u of mode n (a warp), Y_u = A_m^T S_u (R_m x R_3, S_u the I_m x R_3
+// slice of T at u; m the other non-last mode) on the DMMA pipe (m16n8k16, K = I_m), then
+// M[u, :] = G_(n) vec(Y_u) from shared memory. Replaces the mode product, its split-K sum and
+// the core contraction (3 launches, ~30 us at C2). R_m, R_3, R_n <= 16.
+__global__ void __launch_bounds__(256) k_fu_proj3(const double* __restrict__ T, int I1, int I2,
+                                                  int R3, const double* __restrict__ Am, int Rm,
+                                                  const double* __restrict__ G, int R1, int R2,
+                                                  int n, double* __restrict__ M) {
+  // a CTA per unit u (persistent over units); its 8 warps split the K = I_m contraction
+  // (all of a warp's loads issued before its DMMAs), partial Y summed in shared memory
+  extern __shared__ double fps[];
+  double* Gs = fps;               // [16 rn][16 rm][16 r3]
+  double* Yp = Gs + 4096;         // [8 warps][256]
+  double* Y = Yp + 8 * 256;       // [256]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int Rn = n == 0 ? R1 : R2;
+  for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
+    const int rn = e >> 8, rm = (e >> 4) & 15, r3 = e & 15;
+    double v = 0.0;
+    if (rn < Rn && rm < Rm && r3 < R3) {
+      const int r1 = n == 0 ? rn : rm, r2 = n == 0 ? rm : rn;
+      v = G[((size_t)r1 * R2 + r2) * R3 + r3];
+    }
+    Gs[e] = v;
+  }
+  const int In = n == 0 ? I1 : I2, Im = n == 0 ? I2 : I1;
+  const long long su = n == 0 ? (long long)I2 * R3 : (long long)R3;  // stride of u
+  const long long sk = n == 0 ? (long long)R3 : (long long)I2 * R3;  // stride of k
+  const int kper = ((Im + 7) / 8 + 15) / 16 * 16;                      // k range per warp
+  for (int u = blockIdx.x; u < In; u += gridDim.x) {
+    const double* S = T + (long long)u * su;
+    double c[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+    const int kw0 = warp * kper, kw1 = min(Im, kw0 + kper);
+    for (int kb = kw0; kb < kw1; kb += 64) {
+      double a[4][8], b[4][2][4];
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4) {
+        const int k0 = kb + 16 * s4;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int k = k0 + t + 4 * (v >> 1), r = g + 8 * (v & 1);
+          a[s4][v] = (k < kw1 && r < Rm) ? __ldg(Am + (size_t)k * Rm + r) : 0.0;
+        }
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int k = k0 + t + 4 * v, r3 = nt * 8 + g;
+            b[s4][nt][v] = (k < kw1 && r3 < R3) ? __ldcg(S + (long long)k * sk + r3) : 0.0;
+          }
+      }
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma_16x8x16(c[nt], a[s4], b[s4][nt]);
+    }
+    double* yw = Yp + warp * 256;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) yw[(g + 8 * (v >> 1)) * 16 + nt * 8 + 2 * t + (v & 1)] = c[nt][v];
+    __syncthreads();
+    {
+      const int e = threadIdx.x;  // 256 = 16 rm x 16 r3
+      double y = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) y += Yp[w * 256 + e];
+      Y[e] = y;
+    }
+    __syncthreads();
+    // M[u, rn] = sum_{rm, r3} G_(n)[rn][rm][r3] Y[rm][r3]: warp w takes rn = w, w + 8
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int rn = warp + 8 * q;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc = fma(Gs[rn * 256 + lane + 32 * j], Y[lane + 32 * j], acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0 && rn < Rn) M[(size_t)u * Rn + rn] = acc;
+    }
+    __syncthreads();  // Yp / Y reused by the next unit
+  }
+}
+
+bool fu_proj3(const double* T, int I1, int I2, int R3, const double* Am, int Rm, const double* G,
+              int R1, int R2, int n, double* M, cudaStream_t st) {
+  static const bool off = std::getenv("RTB_NO_FU_PROJ3") != nullptr;  // experiments
+  if (off || n > 1 || R1 > 16 || R2 > 16 || R3 > 16) return false;
+  const int In = n == 0 ? I1 : I2;
+  const int grid = std::max(1, std::min(In, 2 * sm_count()));
+  const size_t smem = (size_t)(4096 + 8 * 256 + 256) * 8;
+  set_max_smem(k_fu_proj3, (int)smem);
+  k_fu_proj3<<<grid, 256, smem, st>>>(T, I1, I2, R3, Am, Rm, G, R1, R2, n, M);
+  RTB_LAUNCH_CHECK();
+  return true;
+}
+
 bool ttm_expand(const double* Y, long long O, int R, long long J, const double* A, int I,
                 double* out, cudaStream_t st) {
   // big i chunks (A rows staged once per CTA, several outputs per thread), shrunk

@@ -79,6 +79,10 @@ bool ttm_smallj(const double* X, long long O, int I, int J, const double* A, int
 bool ttm_expand(const double* Y, long long O, int R, long long J, const double* A, int I,
                 double* out, cudaStream_t st);
 // M[i,r] = sum_{o,j} Y[o,i,j] G[o,r,j]
+// F_1 / F_2 (n = 0 / 1) of an order-3 exact factor update straight from T (I1 x I2 x R3):
+// M[u, :] = G_(n) vec(A_m^T T-slice_u) for every u of mode n; false if not applicable (R > 16)
+bool fu_proj3(const double* T, int I1, int I2, int R3, const double* Am, int Rm, const double* G,
+              int R1, int R2, int n, double* M, cudaStream_t st);
 void contract_except(const double* Y, const double* G, long long O, int I, int R, long long J,
                      double* M, cudaStream_t st);
 void sum_partials(const double* partial, long long n, double* out, cudaStream_t st);

@@ -144,7 +144,7 @@ static void keep_pool_memory() {
 // (cudaFreeHost also synchronises the device), which a C1 job of 10 sweeps noticed.
 static std::mutex g_pin_mu;
 static std::vector<int*> g_pin_free;
-static int* pinned_slot() {
+int* pinned_slot() {
   std::lock_guard<std::mutex> lk(g_pin_mu);
   if (g_pin_free.empty()) {
     constexpr int kSlots = 64, kInts = 16;
@@ -157,7 +157,7 @@ static int* pinned_slot() {
   g_pin_free.pop_back();
   return p;
 }
-static void pinned_slot_free(int* p) {
+void pinned_slot_free(int* p) {
   if (!p) return;
   std::lock_guard<std::mutex> lk(g_pin_mu);
   g_pin_free.push_back(p);

@@ -2660,9 +2660,13 @@ void pcg_solve_dist(const PcgSpec& spec, const double* blocks_local, int rank, i
     RTB_LAUNCH_CHECK();
   };
   launch(fi);
-  // the CG state is on the device: the host polls its mode every few iterations
-  static int* done_host = nullptr;
-  if (!done_host) RTB_CUDA(cudaMallocHost(&done_host, 4));
+  // the CG state is on the device: the host polls its mode every few iterations (a pinned
+  // slot of this call's own: shards may run in threads of one process)
+  struct Slot {
+    int* p = pinned_slot();
+    ~Slot() { pinned_slot_free(p); }
+  } slot;
+  int* done_host = slot.p;
   const int* mode_dev = &reinterpret_cast<const DistState*>(a.rpart)->mode;
   const int max_steps = spec.max_iter + 3;  // warm start + iterations + final check
   for (int k = 0; k < max_steps; ++k) {

@@ -262,6 +262,9 @@ void pcg_solve_compact(const PcgSpec& spec, const double* S, const double* b, do
 // Distributed large-d solve (multi-GPU): rank `rank` of `count` holds the blocks of its mode-1
 // slices only (pcg_dist_slices; gram_expand_blocks_range) and the ranks' matvec shares are
 // summed by `allreduce(q, d)` between launches; every rank ends with the same x and status.
+// 16 ints of pinned host memory from a per-process pool (engine.cu), and their return
+int* pinned_slot();
+void pinned_slot_free(int* p);
 bool pcg_dist_ok(int d, int order, const int* ranks);
 void pcg_dist_slices(int m1, int rank, int count, int* u_lo, int* u_hi);
 void pcg_solve_dist(const PcgSpec& spec, const double* blocks_local, int rank, int count,

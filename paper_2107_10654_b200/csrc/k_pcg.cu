@@ -333,18 +333,31 @@ __device__ __forceinline__ void slab23_dmma16(const double* X, double* Y, double
 // slab (slab23_dmma16), one CTA barrier, mode 1 (mode_product_dmma16 with J = 256). Returns
 // the buffer holding z (r is preserved).
 __device__ double* precondition16(const double* r, double* a, double* b, const double* W1,
-                                  const double* W2, const double* dinv, bool eig) {
+                                  const double* W2, const double* dinv, bool eig,
+                                  unsigned long long* pf = nullptr) {
+  unsigned long long t0 = pf ? gtimer() : 0;
+  auto mk = [&](int k) {
+    if (pf) {
+      const unsigned long long t1 = gtimer();
+      pf[k] += t1 - t0;
+      t0 = t1;
+    }
+  };
   slab23_dmma16(r, a, b, W1 + 256, W1 + 512);
   __syncthreads();
+  mk(12);
   mode_product_dmma16(b, a, W1, 4096, 256);
   __syncthreads();
+  mk(13);
   if (!eig) return a;
   for (int e = threadIdx.x; e < 4096; e += kThreads) a[e] *= dinv[e];
   __syncthreads();
   slab23_dmma16(a, b, a, W2 + 256, W2 + 512);
   __syncthreads();
+  mk(6);
   mode_product_dmma16(a, b, W2, 4096, 256);
   __syncthreads();
+  mk(7);
   return b;
 }
 
@@ -2248,7 +2261,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_split(const PcgArgs A, cons
   double rho = 0.0, xx = 0.0;
   auto precond = [&]() -> double* {
     if constexpr (RX == 16) {
-      if (sh.order == 3 && sh.R[0] == 16) return precondition16(r, s0, s1, Ps, VTs, dinv, eig);
+      if (sh.order == 3 && sh.R[0] == 16)
+        return precondition16(r, s0, s1, Ps, VTs, dinv, eig,
+                              (A.prof && vid == 0 && tid == 0) ? A.prof : nullptr);
     }
     return precondition<RM, RX>(sh, r, s0, s1, Ps, VTs, dinv, eig);
   };
@@ -2790,8 +2805,10 @@ void pcg_solve_compact(const PcgSpec& spec, const double* S, const double* b, do
     std::fprintf(stderr,
                  "[pcg_split] d=%d iters=%d status=%d ns (vector CTA 0): publish-barrier %llu "
                  "slice+barrier %llu reduce+barrier %llu cg-vector %llu other-vector %llu | "
-                 "slice CTA 0 compute %llu | cg: q+pq %llu update+rr %llu precond %llu rho %llu\n",
-                 d, stat[1], stat[0], h[0], h[1], h[2], h[5], h[3], h[4], h[8], h[9], h[10], h[11]);
+                 "slice CTA 0 compute %llu | cg: q+pq %llu update+rr %llu precond %llu rho %llu | "
+                 "precond: slab23 %llu mode1 %llu eig-slab23 %llu eig-mode1 %llu\n",
+                 d, stat[1], stat[0], h[0], h[1], h[2], h[5], h[3], h[4], h[8], h[9], h[10], h[11],
+                 h[12], h[13], h[6], h[7]);
   }
 }
 

@@ -269,72 +269,110 @@ __device__ __forceinline__ void mode_product_dmma16(const double* X, double* out
   }
 }
 
-// Modes 2 and 3 of a 16 x 16 x 16 vector, slab-local: warp w owns slab i_1 = w (256 values)
-// and computes out_w = W2^T (X_w W3) with two 16x16x16 DMMA GEMMs (the product of each mode
-// as in mode_product: out_j = sum_i W[i][j] x_i), the intermediate in Y_w; no CTA barrier.
-// out may alias X (the warp reads its X slab completely before writing).
-__device__ __forceinline__ void slab23_dmma16(const double* X, double* Y, double* out,
-                                              const double* W2, const double* W3) {
+// The 16 x 16 x 16 preconditioner below works on the FP64 pipe from fragment tables and
+// XOR-swizzled shared layouts, so none of its shared-memory accesses is bank-conflicted
+// beyond the 4-way read of the canonical r (the previous form, with its row stride of 16
+// doubles on every fragment access, ran at 8-way conflicts: ~4.6k wavefronts per call).
+// Fragment tables, Wf[set][mode][v][lane] (set 0 = W1, 1 = W2; v < 8; g = lane/4, t = lane%4):
+//   modes 0, 1 (A operand W^T):      W[4 ks + t][8 mt + g],          v = 4 mt + ks
+//   mode 2 (B operand, k permuted):  W[pi(ks, t)][8 nt + g],         v = 4 nt + ks
+// pi(ks, t) = 8 (ks >> 1) + 2 t + (ks & 1) is the column a lane's C fragment of the previous
+// GEMM holds, so the mode-3 GEMM takes that C fragment as its A operand without a round trip.
+constexpr int kWfDoubles = 2 * 3 * 8 * 32;
+__device__ __forceinline__ int pre16_pi(int ks, int t) { return 8 * (ks >> 1) + 2 * t + (ks & 1); }
+__device__ void build_frags16(const double* W1, const double* W2, double* Wf) {
+  for (int e = threadIdx.x; e < kWfDoubles; e += blockDim.x) {
+    const int set = e / 768, n = (e / 256) % 3, v = (e / 32) & 7, lane = e & 31;
+    const int g = lane >> 2, t = lane & 3, hi = v >> 2, ks = v & 3;
+    const double* W = (set ? W2 : W1) + n * 256;
+    Wf[e] = n < 2 ? W[(4 * ks + t) * 16 + 8 * hi + g] : W[pre16_pi(ks, t) * 16 + 8 * hi + g];
+  }
+}
+// Layout of the preconditioner's output (and of its swizzled input in the eigen form):
+// canonical element e lives at e ^ (8 * bit 8 of e), i.e. i3 ^ 8 (i1 & 1).
+__device__ __forceinline__ int pre16_swz(int e) { return e ^ ((e >> 5) & 8); }
+
+// One pass out = (W_1^T x W_2^T x W_3^T) src: warp w takes slab i1 = w through modes 2 and 3
+// (two chained GEMMs, the intermediate in registers), writes it to scr in the exchange layout
+// [i1][i2][i3 ^ (4 (i1 & 3) ^ 8 (i2 & 1))], one CTA barrier, then mode 1 (32 column tiles
+// of 8, two per warp) into dst (pre16_swz layout). src_swz: src is in the pre16_swz layout.
+// dst may alias src, not scr.
+__device__ __forceinline__ void pre16_pass(const double* src, bool src_swz, double* scr,
+                                           double* dst, const double* Wf) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const double* xs = X + w * 256;
-  double* ys = Y + w * 256;
-  double* os = out + w * 256;
-  double c[2][2][2];
+  const double* xs = src + w * 256;
+  const int sx = src_swz ? 8 * (w & 1) : 0;
+  double c[2][2][2], z[2][2][2];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
+    for (int nt = 0; nt < 2; ++nt) c[mt][nt][0] = c[mt][nt][1] = z[mt][nt][0] = z[mt][nt][1] = 0.0;
+  // mode 2: Y[j2][i3] = sum_i2 W2[i2][j2] X[i2][i3]
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
     double a[2], b[2];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) a[mt] = xs[(8 * mt + g) * 16 + 4 * ks + t];
+    for (int mt = 0; mt < 2; ++mt) a[mt] = Wf[(256 + (4 * mt + ks) * 32) + lane];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) b[nt] = W3[(4 * ks + t) * 16 + 8 * nt + g];
+    for (int nt = 0; nt < 2; ++nt) b[nt] = xs[(4 * ks + t) * 16 + ((8 * nt + g) ^ sx)];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) dmma_8x8x4(c[mt][nt][0], c[mt][nt][1], a[mt], b[nt]);
   }
-  __syncwarp();
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      ys[(8 * mt + g) * 16 + 8 * nt + 2 * t] = c[mt][nt][0];
-      ys[(8 * mt + g) * 16 + 8 * nt + 2 * t + 1] = c[mt][nt][1];
-      c[mt][nt][0] = c[mt][nt][1] = 0.0;
-    }
-  __syncwarp();
+  // mode 3: Z[j2][j3] = sum_i3 Y[j2][i3] W3[i3][j3], A = Y's C fragment (k = pi(ks, t))
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
-    double a[2], b[2];
+    double b[2];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) a[mt] = W2[(4 * ks + t) * 16 + 8 * mt + g];
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) b[nt] = ys[(4 * ks + t) * 16 + 8 * nt + g];
+    for (int nt = 0; nt < 2; ++nt) b[nt] = Wf[(512 + (4 * nt + ks) * 32) + lane];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) dmma_8x8x4(c[mt][nt][0], c[mt][nt][1], a[mt], b[nt]);
+      for (int nt = 0; nt < 2; ++nt)
+        dmma_8x8x4(z[mt][nt][0], z[mt][nt][1], c[mt][ks >> 1][ks & 1], b[nt]);
   }
-  __syncwarp();
+  {
+    double* zs = scr + w * 256;
+    const int fz = 4 * (w & 3) ^ 8 * (g & 1);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+        *reinterpret_cast<double2*>(zs + (8 * mt + g) * 16 + ((8 * nt + 2 * t) ^ fz)) =
+            make_double2(z[mt][nt][0], z[mt][nt][1]);
+  }
+  __syncthreads();
+  // mode 1: out[j1][n] = sum_i1 W1[i1][j1] Z[i1][n], n = 16 i2 + i3
+  double a1[2][4];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      os[(8 * mt + g) * 16 + 8 * nt + 2 * t] = c[mt][nt][0];
-      os[(8 * mt + g) * 16 + 8 * nt + 2 * t + 1] = c[mt][nt][1];
+    for (int ks = 0; ks < 4; ++ks) a1[mt][ks] = Wf[(4 * mt + ks) * 32 + lane];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int nt = w + 16 * h, i2 = nt >> 1, b8 = 8 * (nt & 1);
+    double o[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int i1 = 4 * ks + t;
+      const double b = scr[i1 * 256 + i2 * 16 + ((b8 + g) ^ (4 * t ^ 8 * (i2 & 1)))];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) dmma_8x8x4(o[mt][0], o[mt][1], a1[mt][ks], b);
     }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+      *reinterpret_cast<double2*>(dst + (8 * mt + g) * 256 + i2 * 16 + ((b8 + 2 * t) ^ (8 * (g & 1)))) =
+          make_double2(o[mt][0], o[mt][1]);
+  }
 }
 
-// z = M^-1 r for 16 x 16 x 16 (order 3, all ranks 16, kWarps = 16 slabs): modes 2-3 slab by
-// slab (slab23_dmma16), one CTA barrier, mode 1 (mode_product_dmma16 with J = 256). Returns
-// the buffer holding z (r is preserved).
-__device__ double* precondition16(const double* r, double* a, double* b, const double* W1,
-                                  const double* W2, const double* dinv, bool eig,
-                                  unsigned long long* pf = nullptr) {
+// z = M^-1 r for 16 x 16 x 16 (order 3, all ranks 16, kWarps = 16 slabs) from the fragment
+// tables Wf (build_frags16 of W1, W2). r is canonical and preserved; returns the buffer
+// holding z in the pre16_swz layout.
+__device__ double* precondition16(const double* r, double* a, double* b, const double* Wf,
+                                  const double* dinv, bool eig, unsigned long long* pf = nullptr) {
   unsigned long long t0 = pf ? gtimer() : 0;
   auto mk = [&](int k) {
     if (pf) {
@@ -343,21 +381,15 @@ __device__ double* precondition16(const double* r, double* a, double* b, const d
       t0 = t1;
     }
   };
-  slab23_dmma16(r, a, b, W1 + 256, W1 + 512);
+  pre16_pass(r, false, a, b, Wf);
   __syncthreads();
   mk(12);
-  mode_product_dmma16(b, a, W1, 4096, 256);
+  if (!eig) return b;
+  for (int e = threadIdx.x; e < 4096; e += kThreads) b[pre16_swz(e)] *= dinv[e];
   __syncthreads();
-  mk(13);
-  if (!eig) return a;
-  for (int e = threadIdx.x; e < 4096; e += kThreads) a[e] *= dinv[e];
-  __syncthreads();
-  slab23_dmma16(a, b, a, W2 + 256, W2 + 512);
+  pre16_pass(b, true, a, b, Wf + 768);
   __syncthreads();
   mk(6);
-  mode_product_dmma16(a, b, W2, 4096, 256);
-  __syncthreads();
-  mk(7);
   return b;
 }
 
@@ -2208,6 +2240,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_split(const PcgArgs A, cons
   double* s1 = s0 + dv;
   double* xs = s1 + dv;
   double* red = xs + dv;
+  double* Wf = red + 64;                    // [kWfDoubles] (precondition16's fragment tables)
   const int sh0 = (int)((long long)d * vid / nvec), sh1 = (int)((long long)d * (vid + 1) / nvec);
   auto publish = [&](const double* v, int c) {  // my share of the next matvec source
     for (int e = sh0 + tid; e < sh1; e += kThreads) X.pg[e] = v[e];
@@ -2247,6 +2280,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_split(const PcgArgs A, cons
     }
     __syncthreads();
   }
+  bool pre16 = false;
+  if constexpr (RX == 16) pre16 = sh.order == 3 && sh.R[0] == 16;
+  if (pre16) build_frags16(Ps, VTs, Wf);
   for (int e = tid; e < d; e += kThreads) {
     r[e] = A.b[e];
     xs[e] = 0.0;
@@ -2256,23 +2292,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_split(const PcgArgs A, cons
   for (int e = tid; e < d; e += kThreads) bb = fma(r[e], r[e], bb);
   bb = block_sum_det(bb, red);
   const double tol2 = A.tol * A.tol;
+  // z from precond() is canonical, or in the pre16_swz layout on the 16 x 16 x 16 path
+  auto zi = [&](int e) { return pre16 ? pre16_swz(e) : e; };
   enum { kWarm, kCg, kCheck };
   int mode = kCg, it = 0, fail = 0;
   double rho = 0.0, xx = 0.0;
   auto precond = [&]() -> double* {
-    if constexpr (RX == 16) {
-      if (sh.order == 3 && sh.R[0] == 16)
-        return precondition16(r, s0, s1, Ps, VTs, dinv, eig,
-                              (A.prof && vid == 0 && tid == 0) ? A.prof : nullptr);
-    }
+    if (pre16)
+      return precondition16(r, s0, s1, Wf, dinv, eig,
+                            (A.prof && vid == 0 && tid == 0) ? A.prof : nullptr);
     return precondition<RM, RX>(sh, r, s0, s1, Ps, VTs, dinv, eig);
   };
   auto start_cg = [&]() {  // z = M^-1 r, p = z, rho; publish p
     double* z = precond();
     double rh = 0.0;
     for (int e = tid; e < d; e += kThreads) {
-      p[e] = z[e];
-      rh = fma(r[e], z[e], rh);
+      const double ze = z[zi(e)];
+      p[e] = ze;
+      rh = fma(r[e], ze, rh);
     }
     rho = block_sum_det(rh, red);
     publish(p, 1);
@@ -2368,12 +2405,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_split(const PcgArgs A, cons
       double* z = precond();
       mark(10);
       double rho2 = 0.0;
-      for (int e = tid; e < d; e += kThreads) rho2 = fma(r[e], z[e], rho2);
+      for (int e = tid; e < d; e += kThreads) rho2 = fma(r[e], z[zi(e)], rho2);
       rho2 = block_sum_det(rho2, red);
       mark(11);
       const double beta = rho2 / rho;
       rho = rho2;
-      for (int e = tid; e < d; e += kThreads) p[e] = fma(beta, p[e], z[e]);
+      for (int e = tid; e < d; e += kThreads) p[e] = fma(beta, p[e], z[zi(e)]);
       __syncthreads();
       publish(p, 1);
       mark(5);
@@ -2713,7 +2750,7 @@ static size_t split_slice_smem(int d, const int* ranks) {
   return (m2 * 136 + 2 * dp + (size_t)kWarps * 2 * dp) * 8;
 }
 static size_t split_vector_smem(int d, int order) {
-  return ((size_t)2 * order * 16 * 16 + 6 * (size_t)((d + 1) & ~1) + 64) * 8;
+  return ((size_t)2 * order * 16 * 16 + 6 * (size_t)((d + 1) & ~1) + 64 + kWfDoubles) * 8;
 }
 
 bool pcg_split_ok(int d, int order, const int* ranks) {
@@ -2806,7 +2843,7 @@ void pcg_solve_compact(const PcgSpec& spec, const double* S, const double* b, do
                  "[pcg_split] d=%d iters=%d status=%d ns (vector CTA 0): publish-barrier %llu "
                  "slice+barrier %llu reduce+barrier %llu cg-vector %llu other-vector %llu | "
                  "slice CTA 0 compute %llu | cg: q+pq %llu update+rr %llu precond %llu rho %llu | "
-                 "precond: slab23 %llu mode1 %llu eig-slab23 %llu eig-mode1 %llu\n",
+                 "precond: pass %llu (unused %llu) eig-pass %llu (unused %llu)\n",
                  d, stat[1], stat[0], h[0], h[1], h[2], h[5], h[3], h[4], h[8], h[9], h[10], h[11],
                  h[12], h[13], h[6], h[7]);
   }

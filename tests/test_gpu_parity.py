@@ -444,6 +444,26 @@ def test_pcg_lambda_dominated_system(rt):
         assert abs(ha[2] - hc[2]) / hc[2] < 1e-9, (ha[:2], ha[2], hc[2])
 
 
+def test_pcg_split_eigen_form_rank16(rt):
+    """The same lambda-dominated regime at ranks (16, 16, 16): the split-role solve
+    (k_pcg_split) with the eigen-form preconditioner of its 16 x 16 x 16 path (two
+    swizzled fragment passes around the diagonal scaling) matches the Cholesky path."""
+    shape, ranks = (64, 64, 64), (16, 16, 16)
+    x = np.random.default_rng(13).standard_normal(shape)  # a noise fit: lambda dominates
+    # (s = 200,000 puts augmented draws on every diagonal entry, which the split solve
+    # needs; this regime was checked to take the eigen form with RTB_PCG_PROF)
+    kw = dict(lam=0.5, sketched_core=1, max_iterations=3, tolerance=0.0,
+              sample_count_override=200000, record_history=1, seed=5)
+    xt = rt.Tensor.from_numpy(x)
+    before = rt.variant_count("k_pcg_split")
+    ra = rt.als_run(xt, ranks, rt.options(**kw))
+    assert rt.variant_count("k_pcg_split") > before
+    rc = rt.als_run(xt, ranks, rt.options(**kw), core_solver=1)
+    assert ra.sketch_info()["solver_path"] == 2
+    for ha, hc in zip(ra.history(), rc.history()):
+        assert abs(ha[2] - hc[2]) / hc[2] < 1e-9, (ha[:2], ha[2], hc[2])
+
+
 # ---------------------------------------------------------------- sweep execution
 @pytest.mark.parametrize("shape,ranks,lam,s,fs", [((40, 36, 32), (6, 5, 4), 1e-2, 8000, 0),
                                                  ((64, 64, 64), (16, 16, 16), 1e-2, 200000, 0),

@@ -401,6 +401,17 @@ def run_our_arm(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif args.nccl_p1:
+        # diagnostic: the sharded code path (kernel-by-kernel sweeps, partial sums through the
+        # NCCL all-reduce callback) with ONE shard on one GPU -- the collective plumbing run for
+        # real, and its cost before any scaling
+        import socket
+        import torch.distributed as dist
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                world_size=1, device_id=torch.device("cuda", local))
     from paper_2107_10654_b200 import rtucker as rt
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
@@ -417,6 +428,8 @@ def run_our_arm(args):
         x = x[lo:hi].contiguous()
         lshape = (hi - lo,) + tuple(SHAPE[1:])
         shard = rt.Shard(rank, world, SHAPE[0], rt.torch_allreduce(dist))
+    elif args.nccl_p1:
+        shard = rt.Shard(0, 1, SHAPE[0], rt.torch_allreduce(dist))
     torch.cuda.synchronize()
     t = rt.Tensor.from_device(x.data_ptr(), lshape)
     torch.cuda.synchronize()
@@ -634,7 +647,10 @@ def run_our_arm(args):
                        "l2": "inputs larger than L2 (X = 1.07 GB > 126 MB)",
                        "step": "one ALS sweep (3 factor updates + sketched core + loss)",
                        "parallelism": (f"X sharded along mode 1 over {world} GPUs, NCCL all-reduce"
-                                       " of partial sums" if world > 1 else "single GPU"),
+                                       " of partial sums" if world > 1 else
+                                       "single GPU, sharded code path with one shard (one-rank NCCL "
+                                       "all-reduce behind every partial sum)" if args.nccl_p1
+                                       else "single GPU"),
                        "final_loss": hist[-1][2] if hist else None},
             "clocks": clk,
             "e2e": {"value": E2E_SWEEPS / e2e_s, "unit": "sweeps/s",
@@ -1022,6 +1038,9 @@ def main():
     ap.add_argument("--c2-only", action="store_true",
                     help="only the C2 headline and its profiled re-run (for ncu launch lists): "
                          "implies --no-extra, skips the C1 head-to-head and the perf-mode line")
+    ap.add_argument("--nccl-p1", action="store_true",
+                    help="diagnostic (N = 1): run the sharded code path with one shard and a "
+                         "one-rank NCCL group behind the all-reduce callback")
     ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
                     help="c2 (default): the headline ALS sweep; c3: the BASELINE config-3 "
                          "4-way Pareto-factor sweep; c4: the BASELINE config-4 sampling + "
@@ -1031,6 +1050,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.nccl_p1:
+        args.c2_only = args.no_cpu_baseline = True
     if args.c2_only:
         args.no_extra = True
     if args.impl == "reference":

@@ -907,7 +907,9 @@ class Engine {
   long long lo_ = 0, nloc_ = 0;
   std::vector<uint64_t> lshape_;
   uint64_t ltotal_ = 0;
-  bool sharded() const { return opt_.shard_count > 1 && opt_.allreduce; }
+  // a caller that installs the all-reduce callback gets the sharded path, one shard included
+  // (P = 1 runs the collective plumbing for real on a single GPU: bench.py --nccl-p1)
+  bool sharded() const { return opt_.allreduce != nullptr; }
   void allreduce(double* buf, uint64_t n) {
     if (sharded()) opt_.allreduce(buf, n, st_, opt_.allreduce_user);
   }

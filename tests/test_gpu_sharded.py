@@ -183,3 +183,60 @@ def test_sharded_rejects_bad_split(rt):
     with pytest.raises(rt.RtuckerError):
         rt.als_run(rt.Tensor.from_numpy(x[:7]), (2, 2, 2), rt.options(max_iterations=1),
                    shard=rt.Shard(0, 2, 20, lambda p, n, s: None))
+
+
+_NCCL_CB = r"""
+import os, sys
+import torch
+import torch.distributed as dist
+sys.path.insert(0, os.environ["RTB_ROOT"])
+from paper_2107_10654_b200 import rtucker as rt
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%d" % int(os.environ["RTB_PORT"]),
+                        rank=0, world_size=1, device_id=torch.device("cuda", 0))
+fn = rt.torch_allreduce(dist)
+stream = torch.cuda.current_stream()
+rt.set_stream(stream.cuda_stream)
+buf = torch.arange(1000, dtype=torch.float64, device="cuda") * 0.5
+want = buf.clone()
+# the library hands the callback a raw device address, a count and its stream
+fn(buf.data_ptr() + 8 * 10, 900, stream.cuda_stream)
+torch.cuda.synchronize()
+assert torch.equal(buf, want), "a one-rank NCCL sum must leave the buffer unchanged"
+# and through the C ABI: with the callback installed the library takes its sharded path (one
+# shard: every partial sum goes through the NCCL all-reduce) and must reproduce the plain run
+import numpy as np
+rng = np.random.default_rng(3)
+x = rng.standard_normal((20, 18, 16))
+kw = dict(lam=1e-2, sketched_core=1, sample_count_override=3000, max_iterations=2,
+          tolerance=0.0, record_history=1, seed=5)
+a = rt.als_run(rt.Tensor.from_numpy(x), (3, 3, 3), rt.options(**kw))
+b = rt.als_run(rt.Tensor.from_numpy(x), (3, 3, 3), rt.options(**kw),
+               shard=rt.Shard(0, 1, 20, fn))
+ha, hb = a.history(), b.history()
+assert len(ha) == len(hb) and len(ha) > 0
+for p, q in zip(ha, hb):
+    assert p[:2] == q[:2]
+    assert abs(p[2] - q[2]) <= 1e-9 * abs(p[2]), (p, q)
+assert b.graph_sweeps == 0  # the sharded path runs kernel by kernel
+dist.destroy_process_group()
+print("nccl-callback-ok")
+"""
+
+
+def test_nccl_allreduce_callback_one_rank(rt):
+    """bench.py's N > 1 plumbing (rt.torch_allreduce: raw device pointer -> torch view ->
+    NCCL all-reduce in place on the library's stream) run for real on a one-rank NCCL group,
+    in a child process so the process group does not outlive the test."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RTB_ROOT=root, RTB_PORT=str(port))
+    p = subprocess.run([sys.executable, "-c", _NCCL_CB], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert p.returncode == 0 and "nccl-callback-ok" in p.stdout, p.stdout + p.stderr

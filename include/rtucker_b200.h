@@ -74,7 +74,9 @@ typedef struct rtucker_b200_als_ext {
    * shard_rows_total) as `x`. X passes, mode-1 factor rows and the sketch's data
    * draws stay local; every partial sum (projections, A_1 rows, compact Gram + rhs,
    * residual) goes through `allreduce` (in place, doubles, enqueued on the
-   * library's stream, e.g. ncclAllReduce sum). shard_count 0/1 = no sharding. */
+   * library's stream, e.g. ncclAllReduce sum). shard_count 0/1 with a NULL
+   * `allreduce` = no sharding; with a callback installed the sharded path runs
+   * with one shard (every partial sum still goes through the callback). */
   uint32_t shard_rank;
   uint32_t shard_count;
   void (*allreduce)(double* device_buf, uint64_t count, void* stream, void* user);

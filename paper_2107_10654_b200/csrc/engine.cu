@@ -1728,8 +1728,9 @@ class Engine {
       sym_eigen(grams_.as<double>(), ns_.as<int>(), rmax_, eig_stride_, pev_.as<double>(),
                 pvec_.as<double>(), pst_.as<int>(), N_, ss, eskip);
     }
-    // the split-role PCG keeps the compact Gram in shared memory: no block expansion
-    const bool split = pcg_path_ && !sharded() && pcg_split_ok((int)d_, N_, rk);
+    // the split-role PCG keeps the compact Gram in shared memory: no block expansion (under
+    // sharding it reads the all-reduced compact Gram, the same buffer)
+    const bool split = pcg_path_ && pcg_split_ok((int)d_, N_, rk);
     normal_eq(s, !pcg_path_, !split);
     if (!pcg_path_) {
       solve_fallback(s, false);

@@ -178,6 +178,30 @@ def test_sharded_distributed_core_solve(rt, P, shape, ranks, s):
         assert np.array_equal(o[1].core, outs[0][1].core)
 
 
+@pytest.mark.parametrize("P", [2, 3])
+def test_sharded_c2_rank16_split_pcg(rt, P):
+    """Rank (16,16,16) under sharding (the C2 shape class): the replicated core solve is the
+    split-role PCG on the all-reduced compact Gram (k_pcg_split, no block expansion), as in
+    the single-process run."""
+    shape, ranks = (48, 40, 36), (16, 16, 16)
+    x = planted(shape, ranks, seed=47)
+    kw = dict(lam=1e-2, sketched_core=1, sample_count_override=120000, max_iterations=2,
+              tolerance=0.0, record_history=1, seed=12)
+    ref = rt.als_run(rt.Tensor.from_numpy(x), ranks, rt.options(**kw))
+    before = rt.variant_count("k_pcg_split")
+    outs = run_sharded(rt, x, ranks, kw, P)
+    assert rt.variant_count("k_pcg_split") >= before + P, "sharded C2 solve did not take k_pcg_split"
+    rh, rm = ref.history(), ref.model()
+    assert ref.sketch_info()["solver_path"] == 2
+    for hist, model, info in outs:
+        assert info["solver_path"] == 2  # the CG answer was accepted
+        for (gi, gs, gl, grm), (_, _, fl, frm) in zip(hist, rh):
+            assert abs(gl - fl) / fl < 1e-8, (gi, gs, gl, fl)
+        assert np.linalg.norm(model.core - rm.core) / np.linalg.norm(rm.core) < 1e-7
+    for o in outs[1:]:
+        assert np.array_equal(o[1].core, outs[0][1].core)
+
+
 def test_sharded_rejects_bad_split(rt):
     x = planted((20, 10, 8), (2, 2, 2), seed=1)
     with pytest.raises(rt.RtuckerError):

@@ -144,6 +144,9 @@ __global__ void __launch_bounds__(256) k_fsk_rows(FskDev f, const double* __rest
   double c[RM / 8][2];
 #pragma unroll
   for (int nt = 0; nt < RM / 8; ++nt) c[nt][0] = c[nt][1] = 0.0;
+  // unrolled so that the digit and Gt loads of four k-steps are in flight together (the loop
+  // was bound by one L1/L2 round trip per step); the DMMA order is unchanged
+#pragma unroll 4
   for (int q0 = 0; q0 < f.width; q0 += 4) {
     const int q = q0 + tq;
     const bool qv = q < f.width;

@@ -8,10 +8,15 @@ an identity all-reduce: every kernel rank r launches at P = 8, without the excha
 
 usage: python tools/c5_probe.py [P=8] [sweeps=3] [factor_samples=0] [I1_total=4096]
 """
+import os
 import sys
 import time
 
 import torch
+
+# an identity all-reduce cannot feed the distributed core solve (each shard multiplies only its
+# own mode-1 slices and the shares meet in the all-reduce): the probe keeps the replicated solve
+os.environ.setdefault("RTB_NO_PCG_DIST", "1")
 
 sys.path.insert(0, ".")
 from paper_2107_10654_b200 import rtucker as rt  # noqa: E402

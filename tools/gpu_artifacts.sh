@@ -16,6 +16,11 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 echo "ncu launch rc=$?" >> gpurun_out/ncu_launch_$TAG.log
 timeout 1200 ncu --set full --clock-control none --import-source on \
   -k "regex:k_pcg_split|k_ttm_last5|k_vech_bucket5|k_ttm_mid5|k_vech_contract3" -c 5 \
-  -o gpurun_out/full_$TAG python bench.py --steps 3 --warmup 3 --no-cpu-baseline --c2-only \
+  -f -o /tmp/full_$TAG python bench.py --steps 3 --warmup 3 --no-cpu-baseline --c2-only \
   > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/ncu_full_$TAG.log
+# the report (with source) is too big to travel with the rest: summarise it on the box
+(echo "# ncu --set full --clock-control none, C2 bench, code state $TAG, one launch of each top kernel"
+ python tools/ncu_summary.py /tmp/full_$TAG.ncu-rep; echo
+ python tools/ncu_pipe_summary.py /tmp/full_$TAG.ncu-rep) > gpurun_out/ncu_top_$TAG.txt 2>&1
+timeout 300 python tools/perf_c2.py 512,512,512 16 200000 3 0 20000 > gpurun_out/perf_c2_fsk_$TAG.txt 2>&1
